@@ -1,0 +1,171 @@
+/*
+ * cvxreg_b200.h -- C ABI of the B200 pair-sweep solver (libcvxreg_b200.so).
+ *
+ * Drop-in for the singleton-block dual path of the reference solver
+ * (arXiv 1407.7220 `cvxreg`, /root/reference/proj/core). Plain pointers and
+ * sizes only; every function returns a cr_status and never throws. The C++
+ * shim in include/cvxreg_b200/papg.hpp maps statuses back to the reference's
+ * exceptions (std::invalid_argument / std::runtime_error).
+ *
+ * Reference interfaces replaced (file:line under proj/core/):
+ *   cr_papg_*            papg_solve / dual_gradient_ascent      include/cvxreg/papg.hpp:75-82
+ *                        (loop: src/papg.cpp:136-283)
+ *   cr_sigma_C           estimate_sigma_max(op_C(ops))           src/operators.cpp:302-339, :353-369
+ *                        (called from DualDecomposition ctor     src/papg.cpp:68)
+ *   cr_get_primal        PapgResult::point                       include/cvxreg/papg.hpp:61
+ *   cr_get_theta         PapgResult::dual (DualPoint)            include/cvxreg/types.hpp:50-53
+ *   cr_get_rows          DualGradientResult::C_eta               include/cvxreg/papg.hpp:25
+ *   cr_gen_instance      gen_instance                            src/testgen.cpp:36-87
+ *   cr_prepare_problem   prepare_problem                         src/preprocess.cpp:50-65
+ *   cr_certificate       certificate_for_iterate                 src/papg.cpp:298-303
+ *
+ * Threading: a handle is confined to one host thread. Distinct handles may
+ * be driven concurrently. Sharded runs use one handle (and one process) per
+ * GPU; rank r owns pair rows [row_begin, row_end) of the N x N pair matrix.
+ */
+#ifndef CVXREG_B200_H
+#define CVXREG_B200_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  CR_OK = 0,
+  CR_EINVAL = 1,      /* shape / precondition (reference: std::invalid_argument) */
+  CR_ENOMEM = 2,      /* device or pinned allocation failed */
+  CR_ECUDA = 3,       /* CUDA runtime error */
+  CR_ENCCL = 4,       /* NCCL error */
+  CR_ENONFINITE = 5,  /* "papg: non-finite dual gradient" (papg.cpp:184-185) */
+  CR_ESTATE = 6       /* call out of order (e.g. iterate before begin) */
+} cr_status;
+
+/* termination reasons, metrics.hpp:41 TermReason */
+enum { CR_THRESHOLDS = 0, CR_ITER_BUDGET = 1, CR_TIME_BUDGET = 2, CR_ERROR = 3 };
+
+typedef struct cr_handle cr_handle;
+
+/* PapgConfig (papg.hpp:7-21) minus the inner ALCC settings, which the
+   singleton closed form does not use, plus two device knobs. */
+typedef struct {
+  double gamma;             /* 1e-3 */
+  double B_theta;           /* <= 0: adaptive, start at 10 sqrt(N) */
+  int32_t adaptive_B_theta; /* 1 */
+  int32_t max_restarts;     /* 6 */
+  double gap_norm_tol;      /* 1e-6 */
+  double infeas_norm_tol;   /* 1e-1 */
+  int64_t max_iters;        /* 100000 */
+  double max_seconds;       /* 7200 */
+  double inner_tol_floor;   /* 1e-6: enters the g* cushion 2 tol K (papg.cpp:198) */
+  double final_resolve_tol; /* 1e-10 */
+  int32_t record_history;   /* 1 */
+  int32_t use_momentum;     /* 1: papg_solve, 0: dual_gradient_ascent */
+  double sigma_C;           /* > 0: use this sigma_max(C) instead of estimating it */
+  int32_t graph_iters;      /* iterations per CUDA graph launch; <= 0: auto */
+  int32_t pad_;
+} cr_papg_config;
+
+/* one MetricsSnapshot (metrics.hpp:13-22) */
+typedef struct {
+  double iter, objective, reg_objective, infeas_raw, infeas_norm, gap_raw, gap_norm, wall_time_s;
+} cr_snapshot;
+
+/* PapgResult scalars (papg.hpp:60-69) + SolveReport (metrics.hpp:45-54) */
+typedef struct {
+  int64_t iters;
+  int32_t reason;
+  int32_t restarts;
+  int32_t saturated;
+  int32_t sigma_iters;
+  int32_t sigma_converged;
+  int32_t pad_;
+  double g_final;
+  double delta_estimate;
+  double sigma_C;
+  double L_g;
+  double B_theta;
+  double wall_seconds;     /* device clock, begin -> stop */
+  double sigma_seconds;    /* power iteration time (0 if injected) */
+  double loop_seconds;     /* dual loop time */
+  double last_gap_norm;
+  double last_infeas_norm;
+} cr_papg_result;
+
+/* ---- handle lifetime ---------------------------------------------------- */
+/* Copies X (N x n, row-major) and the SHIFTED observations ybar (N) to the
+   device. Rows [row_begin, row_end) of the pair matrix are owned by this
+   handle (pass 0, N for a single GPU). gamma > 0. */
+cr_status cr_create(const double *X, const double *ybar_shifted, int64_t N, int64_t n,
+                    double gamma, int device, int64_t row_begin, int64_t row_end,
+                    cr_handle **out);
+void cr_destroy(cr_handle *h);
+const char *cr_last_error(const cr_handle *h);
+const char *cr_status_string(cr_status s);
+
+/* ---- multi-GPU: one handle per rank, NCCL allreduce over NVLink ----------- */
+cr_status cr_nccl_unique_id(uint8_t id_out[128]);
+cr_status cr_attach_nccl(cr_handle *h, const uint8_t id[128], int rank, int world);
+/* Host-exchange seam (tests / emulation): bytes of the per-iteration
+   aggregate payload, see cr_papg_iterate_phased. */
+int64_t cr_exchange_len(const cr_handle *h);
+
+/* ---- sigma_max(C) by power iteration (operators.cpp:302-339) ------------- */
+cr_status cr_sigma_C(cr_handle *h, double tol, int32_t max_iters, double *sigma,
+                     int32_t *iters, int32_t *converged);
+
+/* ---- the dual loop ------------------------------------------------------ */
+/* theta0: canonical [theta_cross (N(N-1)); theta_pos (N)] or NULL (= 0).
+   Estimates sigma_C unless cfg->sigma_C > 0. */
+cr_status cr_papg_begin(cr_handle *h, const cr_papg_config *cfg, const double *theta0);
+/* Runs up to max_steps more iterations (stops early at termination).
+   *done = iterations completed so far; *stopped = 1 once terminated. */
+cr_status cr_papg_iterate(cr_handle *h, int64_t max_steps, int64_t *done, int32_t *stopped);
+/* Same loop, one iteration at a time with the cross-shard exchange done by
+   the caller: local phase, then the caller sums the exchange payloads of all
+   shards (cr_exchange_get/put), then the finish phase. */
+cr_status cr_iter_local(cr_handle *h);
+cr_status cr_exchange_get(cr_handle *h, double *buf);
+cr_status cr_exchange_put(cr_handle *h, const double *buf);
+cr_status cr_iter_finish(cr_handle *h, int32_t *stopped);
+/* Final re-solve at theta1 (papg.cpp:265-282): fills res, y (N), xi (N*n) and,
+   when history != NULL, res->iters snapshots. */
+cr_status cr_papg_finish(cr_handle *h, cr_papg_result *res, double *y, double *xi,
+                         cr_snapshot *history);
+/* begin + iterate to termination + finish */
+cr_status cr_papg_solve(cr_handle *h, const cr_papg_config *cfg, const double *theta0,
+                        cr_papg_result *res, double *y, double *xi, cr_snapshot *history);
+
+/* theta1 of this shard's rows in canonical order: out receives
+   theta_cross[row_begin*(N-1) .. row_end*(N-1)) followed by theta_pos (N). */
+cr_status cr_get_theta(cr_handle *h, double *out);
+/* C eta of the last loop iteration (the residual rows at eta(theta2)), same
+   layout as cr_get_theta. */
+cr_status cr_get_rows(cr_handle *h, double *out);
+/* device timing of the last cr_papg_iterate call and the number of kernel
+   launches it issued (for bench.py) */
+cr_status cr_last_timing(const cr_handle *h, double *seconds, int64_t *launches,
+                         double *sweep_seconds);
+/* Time k sweep-kernel launches alone on the handle's stream with CUDA events
+   (the dominant kernel in isolation, for the roofline). */
+cr_status cr_time_sweep(cr_handle *h, int32_t k, double *avg_seconds);
+
+/* ---- host utilities (no device) ----------------------------------------- */
+/* kinds: 0 quadratic, 1 exponential, 2 affine-noiseless, 3 custom-1d
+   (testgen.hpp:18-25); 10 sqnorm-uniform, 11 maxaffine-uniform,
+   12 lse-uniform (BASELINE.json configs). */
+cr_status cr_gen_instance(int32_t kind, int64_t N, int64_t n, double noise, uint64_t seed,
+                          int64_t pieces, double *X, double *y);
+/* prepare_problem: ys_shifted (N), shift, feasible affine point (shifted
+   frame), bounds4 = {B_theta, Bbar_y, Bbar_xi, gamma} */
+cr_status cr_prepare_problem(const double *X, const double *y, int64_t N, int64_t n,
+                             double gamma, double *ys_shifted, double *shift, double *feas_y,
+                             double *feas_xi, double *bounds4);
+void cr_certificate(double gamma, double delta, double B_xi_estimate, double sigma_max_C,
+                    double out2[2]);
+double cr_momentum_next(double t);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,769 @@
+/*
+ * cvxreg_oracle.c -- TEST INFRASTRUCTURE ONLY (see cvxreg_oracle.h).
+ *
+ * Literal CPU restatement of the reference's singleton-block P-APG path.
+ * Every function cites the reference lines it follows; loops keep the
+ * reference's canonical row order and accumulation order. Compiled with
+ * -ffp-contract=off so a*b+c stays two roundings, as the reference's default
+ * x86-64 build (no -march, so no FMA) computes it.
+ */
+#include "cvxreg_oracle.h"
+
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+#include <time.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+/* ------------------------------------------------------------------ PRNG */
+/* rng.hpp:7-59 */
+static uint64_t splitmix64(uint64_t *state) {
+  uint64_t z = (*state += 0x9e3779b97f4a7c15ULL);
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+static uint64_t mix64(uint64_t x) { return splitmix64(&x); }
+
+typedef struct { uint64_t s[4]; } xo256;
+
+static uint64_t rotl(uint64_t x, int k) { return (x << k) | (x >> (64 - k)); }
+
+static void xo_seed(xo256 *g, uint64_t seed) {
+  for (int i = 0; i < 4; ++i) g->s[i] = splitmix64(&seed);
+}
+static uint64_t xo_next(xo256 *g) {
+  uint64_t *s = g->s;
+  const uint64_t result = rotl(s[0] + s[3], 23) + s[0];
+  const uint64_t t = s[1] << 17;
+  s[2] ^= s[0];
+  s[3] ^= s[1];
+  s[1] ^= s[2];
+  s[0] ^= s[3];
+  s[2] ^= t;
+  s[3] = rotl(s[3], 45);
+  return result;
+}
+static double xo_uniform(xo256 *g) { return (double)(xo_next(g) >> 11) * 0x1.0p-53; }
+static double xo_normal(xo256 *g) {
+  double u1 = xo_uniform(g);
+  if (u1 <= 0.0) u1 = 0x1.0p-53;
+  const double u2 = xo_uniform(g);
+  return sqrt(-2.0 * log(u1)) * cos(6.28318530717958647692528676655900577 * u2);
+}
+/* rng.hpp:57-59 */
+static xo256 rng_stream(uint64_t seed, uint64_t tag) {
+  xo256 g;
+  xo_seed(&g, mix64(seed) ^ mix64(0x517cc1b727220a95ULL + tag));
+  return g;
+}
+
+uint64_t cro_rng_draws(uint64_t seed, uint64_t tag, int64_t count, int kind, double *out) {
+  xo256 g = rng_stream(seed, tag);
+  uint64_t last = 0;
+  for (int64_t i = 0; i < count; ++i) {
+    if (kind == 0) out[i] = xo_uniform(&g);
+    else if (kind == 1) out[i] = xo_normal(&g);
+    else { last = xo_next(&g); out[i] = (double)(last >> 11); }
+  }
+  return last;
+}
+
+/* ------------------------------------------------------------ generators */
+/* tags: testgen.cpp:12-16; 6/7 are the new BASELINE kinds */
+enum { TAG_LAMBDA = 1, TAG_X = 2, TAG_EPS = 3, TAG_P = 4, TAG_AFFINE = 5, TAG_A = 6, TAG_B = 7 };
+
+static void normal_fill(uint64_t seed, uint64_t tag, int64_t count, double *out) {
+  xo256 g = rng_stream(seed, tag);
+  for (int64_t i = 0; i < count; ++i) out[i] = xo_normal(&g); /* row-major, testgen.cpp:22-23 */
+}
+static void uniform_fill(uint64_t seed, uint64_t tag, int64_t count, double lo, double hi,
+                         double *out) {
+  xo256 g = rng_stream(seed, tag);
+  for (int64_t i = 0; i < count; ++i) out[i] = lo + (hi - lo) * xo_uniform(&g);
+}
+
+static int row_cmp_n;
+static const double *row_cmp_X;
+static int row_cmp(const void *a, const void *b) {
+  const int64_t ia = *(const int64_t *)a, ib = *(const int64_t *)b;
+  for (int j = 0; j < row_cmp_n; ++j) {
+    const double xa = row_cmp_X[ia * row_cmp_n + j], xb = row_cmp_X[ib * row_cmp_n + j];
+    if (xa != xb) return xa < xb ? -1 : 1;
+  }
+  return 0;
+}
+
+/* dataset.cpp:14-42 */
+static int validate_dataset(const double *X, const double *y, int64_t N, int64_t n) {
+  if (n < 1 || N < n + 1) return -1;
+  for (int64_t i = 0; i < N * n; ++i) if (!isfinite(X[i])) return -1;
+  for (int64_t i = 0; i < N; ++i) if (!isfinite(y[i])) return -1;
+  int64_t *order = (int64_t *)malloc(sizeof(int64_t) * (size_t)N);
+  for (int64_t i = 0; i < N; ++i) order[i] = i;
+  row_cmp_n = (int)n;
+  row_cmp_X = X;
+  qsort(order, (size_t)N, sizeof(int64_t), row_cmp);
+  int rc = 0;
+  for (int64_t k = 1; k < N; ++k)
+    if (row_cmp(&order[k - 1], &order[k]) == 0) { rc = -2; break; }
+  free(order);
+  return rc;
+}
+
+/* testgen.cpp:36-87 plus the BASELINE.json kinds */
+int cro_gen_instance(int kind, int64_t N, int64_t n, double noise, uint64_t seed,
+                     int64_t pieces, double *X, double *y) {
+  if (N < n + 1 || n < 1) return -1;
+  switch (kind) {
+    case CRO_GEN_QUADRATIC: {
+      double *Lam = (double *)malloc(sizeof(double) * (size_t)(n * n));
+      double *Q = (double *)calloc((size_t)(n * n), sizeof(double));
+      double *eps = (double *)malloc(sizeof(double) * (size_t)N);
+      normal_fill(seed, TAG_LAMBDA, n * n, Lam);
+      for (int64_t i = 0; i < n; ++i)
+        for (int64_t j = 0; j < n; ++j) {
+          double acc = 0;
+          for (int64_t k = 0; k < n; ++k) acc += Lam[k * n + i] * Lam[k * n + j];
+          Q[i * n + j] = acc;
+        }
+      normal_fill(seed, TAG_X, N * n, X);
+      normal_fill(seed, TAG_EPS, N, eps);
+      for (int64_t l = 0; l < N; ++l) {
+        const double *x = X + l * n;
+        double quad = 0;
+        for (int64_t i = 0; i < n; ++i) {
+          double qx = 0;
+          for (int64_t j = 0; j < n; ++j) qx += Q[i * n + j] * x[j];
+          quad += x[i] * qx;
+        }
+        y[l] = 0.5 * quad + noise * eps[l];
+      }
+      free(Lam); free(Q); free(eps);
+      break;
+    }
+    case CRO_GEN_EXPONENTIAL: {
+      double *eps = (double *)malloc(sizeof(double) * (size_t)N);
+      double *p = (double *)malloc(sizeof(double) * (size_t)n);
+      normal_fill(seed, TAG_X, N * n, X);
+      normal_fill(seed, TAG_EPS, N, eps);
+      xo256 pg = rng_stream(seed, TAG_P);
+      for (int64_t j = 0; j < n; ++j) p[j] = xo_uniform(&pg);
+      for (int64_t l = 0; l < N; ++l) {
+        double d = 0;
+        for (int64_t j = 0; j < n; ++j) d += p[j] * X[l * n + j];
+        y[l] = exp(d) + noise * eps[l];
+      }
+      free(eps); free(p);
+      break;
+    }
+    case CRO_GEN_AFFINE_NOISELESS: {
+      double *coef = (double *)malloc(sizeof(double) * (size_t)(n + 1));
+      normal_fill(seed, TAG_X, N * n, X);
+      normal_fill(seed, TAG_AFFINE, n + 1, coef);
+      for (int64_t l = 0; l < N; ++l) {
+        double d = 0;
+        for (int64_t j = 0; j < n; ++j) d += X[l * n + j] * coef[1 + j];
+        y[l] = coef[0] + d;
+      }
+      free(coef);
+      break;
+    }
+    case CRO_GEN_CUSTOM_1D: {
+      if (n != 1) return -1;
+      double *eps = (double *)malloc(sizeof(double) * (size_t)N);
+      for (int64_t l = 0; l < N; ++l) X[l] = (double)l;
+      normal_fill(seed, TAG_EPS, N, eps);
+      const double mid = 0.5 * (double)(N - 1);
+      for (int64_t l = 0; l < N; ++l) y[l] = fabs(X[l] - mid) + noise * eps[l];
+      free(eps);
+      break;
+    }
+    case CRO_GEN_SQNORM_UNIFORM: {
+      double *eps = (double *)malloc(sizeof(double) * (size_t)N);
+      uniform_fill(seed, TAG_X, N * n, -1.0, 1.0, X);
+      uniform_fill(seed, TAG_EPS, N, -noise, noise, eps);
+      for (int64_t l = 0; l < N; ++l) {
+        double s = 0;
+        for (int64_t j = 0; j < n; ++j) s += X[l * n + j] * X[l * n + j];
+        y[l] = s + eps[l];
+      }
+      free(eps);
+      break;
+    }
+    case CRO_GEN_MAXAFFINE_UNIFORM: {
+      if (pieces < 1) return -1;
+      double *eps = (double *)malloc(sizeof(double) * (size_t)N);
+      double *A = (double *)malloc(sizeof(double) * (size_t)(pieces * n));
+      double *B = (double *)malloc(sizeof(double) * (size_t)pieces);
+      uniform_fill(seed, TAG_X, N * n, -1.0, 1.0, X);
+      uniform_fill(seed, TAG_EPS, N, -noise, noise, eps);
+      normal_fill(seed, TAG_A, pieces * n, A);
+      normal_fill(seed, TAG_B, pieces, B);
+      for (int64_t l = 0; l < N; ++l) {
+        double best = -INFINITY;
+        for (int64_t i = 0; i < pieces; ++i) {
+          double d = B[i];
+          for (int64_t j = 0; j < n; ++j) d += A[i * n + j] * X[l * n + j];
+          if (d > best) best = d;
+        }
+        y[l] = best + eps[l];
+      }
+      free(eps); free(A); free(B);
+      break;
+    }
+    case CRO_GEN_LSE_UNIFORM: {
+      if (pieces < 1) return -1;
+      double *eps = (double *)malloc(sizeof(double) * (size_t)N);
+      double *A = (double *)malloc(sizeof(double) * (size_t)(pieces * n));
+      uniform_fill(seed, TAG_X, N * n, -1.0, 1.0, X);
+      uniform_fill(seed, TAG_EPS, N, -noise, noise, eps);
+      normal_fill(seed, TAG_A, pieces * n, A);
+      const double scale = sqrt(1.0 / 20.0); /* a_k ~ N(0, I/20) (BASELINE cfg 3) */
+      for (int64_t i = 0; i < pieces * n; ++i) A[i] *= scale;
+      for (int64_t l = 0; l < N; ++l) {
+        double s = 0;
+        for (int64_t k = 0; k < pieces; ++k) {
+          double d = 0;
+          for (int64_t j = 0; j < n; ++j) d += A[k * n + j] * X[l * n + j];
+          s += exp(d);
+        }
+        y[l] = log(s) + eps[l];
+      }
+      free(eps); free(A);
+      break;
+    }
+    default:
+      return -1;
+  }
+  return validate_dataset(X, y, N, n);
+}
+
+/* ------------------------------------------------------------ preprocess */
+/* Least squares min |D c - y| with D = [1, X] by column-pivoted Householder
+   QR; rank test as Eigen's ColPivHouseholderQR default threshold
+   (preprocess.cpp:26-36). */
+static int lsq_affine(const double *X, const double *y, int64_t N, int64_t n, double *coef) {
+  const int64_t m = n + 1;
+  double *D = (double *)malloc(sizeof(double) * (size_t)(N * m)); /* column-major */
+  double *b = (double *)malloc(sizeof(double) * (size_t)N);
+  int64_t *perm = (int64_t *)malloc(sizeof(int64_t) * (size_t)m);
+  double *cn = (double *)malloc(sizeof(double) * (size_t)m);
+  for (int64_t i = 0; i < N; ++i) {
+    D[i] = 1.0;
+    for (int64_t j = 0; j < n; ++j) D[(j + 1) * N + i] = X[i * n + j];
+    b[i] = y[i];
+  }
+  for (int64_t j = 0; j < m; ++j) {
+    perm[j] = j;
+    double s = 0;
+    for (int64_t i = 0; i < N; ++i) s += D[j * N + i] * D[j * N + i];
+    cn[j] = s;
+  }
+  double maxpivot = 0;
+  int64_t rank = 0;
+  double *rdiag = (double *)malloc(sizeof(double) * (size_t)m);
+  for (int64_t k = 0; k < m; ++k) {
+    int64_t best = k;
+    for (int64_t j = k + 1; j < m; ++j) if (cn[j] > cn[best]) best = j;
+    if (best != k) {
+      for (int64_t i = 0; i < N; ++i) {
+        double t = D[k * N + i]; D[k * N + i] = D[best * N + i]; D[best * N + i] = t;
+      }
+      double t = cn[k]; cn[k] = cn[best]; cn[best] = t;
+      int64_t tp = perm[k]; perm[k] = perm[best]; perm[best] = tp;
+    }
+    double *col = D + k * N;
+    double norm = 0;
+    for (int64_t i = k; i < N; ++i) norm += col[i] * col[i];
+    norm = sqrt(norm);
+    double alpha = col[k] > 0 ? -norm : norm;
+    rdiag[k] = alpha;
+    if (fabs(alpha) > maxpivot) maxpivot = fabs(alpha);
+    if (norm > 0) {
+      col[k] -= alpha;
+      double vnorm2 = 0;
+      for (int64_t i = k; i < N; ++i) vnorm2 += col[i] * col[i];
+      if (vnorm2 > 0) {
+        for (int64_t j = k + 1; j < m; ++j) {
+          double *cj = D + j * N;
+          double d = 0;
+          for (int64_t i = k; i < N; ++i) d += col[i] * cj[i];
+          const double f = 2.0 * d / vnorm2;
+          for (int64_t i = k; i < N; ++i) cj[i] -= f * col[i];
+        }
+        double d = 0;
+        for (int64_t i = k; i < N; ++i) d += col[i] * b[i];
+        const double f = 2.0 * d / vnorm2;
+        for (int64_t i = k; i < N; ++i) b[i] -= f * col[i];
+      }
+    }
+    for (int64_t j = k + 1; j < m; ++j) {
+      double s = 0;
+      for (int64_t i = k + 1; i < N; ++i) s += D[j * N + i] * D[j * N + i];
+      cn[j] = s;
+    }
+  }
+  const double threshold = 2.220446049250313e-16 * (double)m;
+  for (int64_t k = 0; k < m; ++k) if (fabs(rdiag[k]) > threshold * maxpivot) ++rank;
+  int ok = rank == m;
+  if (ok) {
+    double *z = (double *)malloc(sizeof(double) * (size_t)m);
+    for (int64_t k = m - 1; k >= 0; --k) {
+      double s = b[k];
+      for (int64_t j = k + 1; j < m; ++j) s -= D[j * N + k] * z[j];
+      z[k] = s / rdiag[k];
+    }
+    for (int64_t k = 0; k < m; ++k) coef[perm[k]] = z[k];
+    free(z);
+  }
+  free(D); free(b); free(perm); free(cn); free(rdiag);
+  return ok;
+}
+
+int cro_prepare(const double *X, const double *y, int64_t N, int64_t n, double gamma,
+                double *ys_shifted, double *shift, double *feas_y, double *feas_xi,
+                double *bounds4, double *intercept, double *slope) {
+  if (gamma <= 0 || N < n + 1) return -1;
+  double *coef = (double *)malloc(sizeof(double) * (size_t)(n + 1));
+  if (lsq_affine(X, y, N, n, coef)) {
+    *intercept = coef[0];
+    for (int64_t j = 0; j < n; ++j) slope[j] = coef[1 + j];
+  } else { /* preprocess.cpp:36-40 constant fallback */
+    double s = 0;
+    for (int64_t i = 0; i < N; ++i) s += y[i];
+    *intercept = s / (double)N;
+    for (int64_t j = 0; j < n; ++j) slope[j] = 0;
+  }
+  free(coef);
+  /* preprocess.cpp:42-50 */
+  double bsq_y = 0, bsq_xi = 0;
+  for (int64_t l = 0; l < N; ++l) {
+    double d = 0;
+    for (int64_t j = 0; j < n; ++j) d += X[l * n + j] * slope[j];
+    feas_y[l] = *intercept + d;
+    const double r = feas_y[l] - y[l];
+    bsq_y += r * r;
+    for (int64_t j = 0; j < n; ++j) feas_xi[l * n + j] = slope[j];
+  }
+  for (int64_t i = 0; i < N * n; ++i) bsq_xi += feas_xi[i] * feas_xi[i];
+  double Bbar = sqrt(bsq_y + gamma * bsq_xi);
+  if (Bbar < 1e-8) Bbar = 1e-8;
+  /* preprocess.cpp:43-48 shift */
+  double ymin = y[0];
+  for (int64_t i = 1; i < N; ++i) if (y[i] < ymin) ymin = y[i];
+  double s = Bbar - ymin;
+  if (s < 0) s = 0;
+  *shift = s;
+  for (int64_t i = 0; i < N; ++i) { ys_shifted[i] = y[i] + s; feas_y[i] += s; }
+  bounds4[0] = 10.0 * sqrt((double)N);
+  bounds4[1] = Bbar;
+  bounds4[2] = Bbar / sqrt(gamma);
+  bounds4[3] = gamma;
+  return 0;
+}
+
+/* ------------------------------------------------------------- operators */
+/* operators.cpp:128-153, singleton partition: cross order == full (l1,l2)
+   lexicographic order with the diagonal skipped (indexing.hpp:30-37). */
+void cro_apply_C(const double *X, int64_t N, int64_t n, const double *y, const double *xi,
+                 double *out) {
+  int64_t r = 0;
+  for (int64_t l1 = 0; l1 < N; ++l1) {
+    const double y1 = y[l1];
+    const double *x1 = X + l1 * n;
+    for (int64_t l2 = 0; l2 < N; ++l2) {
+      if (l1 == l2) continue;
+      double acc = y1 - y[l2];
+      const double *xi2 = xi + l2 * n;
+      const double *x2 = X + l2 * n;
+      for (int64_t j = 0; j < n; ++j) acc -= xi2[j] * (x1[j] - x2[j]);
+      out[r++] = acc;
+    }
+  }
+  for (int64_t l = 0; l < N; ++l) out[r + l] = y[l]; /* :152 */
+}
+
+/* operators.cpp:155-180 */
+void cro_apply_C_T(const double *X, int64_t N, int64_t n, const double *theta,
+                   double *out_y, double *out_xi) {
+  const int64_t rows_cross = N * (N - 1);
+  for (int64_t l = 0; l < N; ++l) out_y[l] = theta[rows_cross + l]; /* :161 */
+  memset(out_xi, 0, sizeof(double) * (size_t)(N * n));
+  int64_t r = 0;
+  for (int64_t l1 = 0; l1 < N; ++l1) {
+    const double *x1 = X + l1 * n;
+    for (int64_t l2 = 0; l2 < N; ++l2) {
+      if (l1 == l2) continue;
+      const double tr = theta[r++];
+      out_y[l1] += tr;
+      out_y[l2] -= tr;
+      double *o2 = out_xi + l2 * n;
+      const double *x2 = X + l2 * n;
+      for (int64_t j = 0; j < n; ++j) o2[j] -= tr * (x1[j] - x2[j]);
+    }
+  }
+}
+
+/* Row-parallel variants for the timed multi-core CPU baseline. apply_C is
+   embarrassingly parallel by l1; apply_C_T accumulates per-thread partials
+   over contiguous l1 ranges and combines them in thread order. */
+static void apply_C_omp(const double *X, int64_t N, int64_t n, const double *y,
+                        const double *xi, double *out, int threads) {
+#pragma omp parallel for schedule(static) num_threads(threads)
+  for (int64_t l1 = 0; l1 < N; ++l1) {
+    int64_t r = l1 * (N - 1);
+    const double y1 = y[l1];
+    const double *x1 = X + l1 * n;
+    for (int64_t l2 = 0; l2 < N; ++l2) {
+      if (l1 == l2) continue;
+      double acc = y1 - y[l2];
+      const double *xi2 = xi + l2 * n;
+      const double *x2 = X + l2 * n;
+      for (int64_t j = 0; j < n; ++j) acc -= xi2[j] * (x1[j] - x2[j]);
+      out[r++] = acc;
+    }
+  }
+  for (int64_t l = 0; l < N; ++l) out[N * (N - 1) + l] = y[l];
+}
+
+static void apply_C_T_omp(const double *X, int64_t N, int64_t n, const double *theta,
+                          double *out_y, double *out_xi, int threads) {
+  const int64_t rows_cross = N * (N - 1);
+  const int64_t w = N * (n + 1);
+  double *part = (double *)calloc((size_t)(w * threads), sizeof(double));
+#pragma omp parallel num_threads(threads)
+  {
+    int tid = 0, nt = 1;
+#ifdef _OPENMP
+    tid = omp_get_thread_num();
+    nt = omp_get_num_threads();
+#endif
+    double *py = part + (int64_t)tid * w;
+    double *pxi = py + N;
+    const int64_t lo = N * tid / nt, hi = N * (tid + 1) / nt;
+    for (int64_t l1 = lo; l1 < hi; ++l1) {
+      int64_t r = l1 * (N - 1);
+      const double *x1 = X + l1 * n;
+      for (int64_t l2 = 0; l2 < N; ++l2) {
+        if (l1 == l2) continue;
+        const double tr = theta[r++];
+        py[l1] += tr;
+        py[l2] -= tr;
+        double *o2 = pxi + l2 * n;
+        const double *x2 = X + l2 * n;
+        for (int64_t j = 0; j < n; ++j) o2[j] -= tr * (x1[j] - x2[j]);
+      }
+    }
+  }
+#pragma omp parallel for schedule(static) num_threads(threads)
+  for (int64_t k = 0; k < w; ++k) {
+    double s = k < N ? theta[rows_cross + k] : 0.0;
+    for (int t = 0; t < threads; ++t) s += part[(int64_t)t * w + k];
+    if (k < N) out_y[k] = s; else out_xi[k - N] = s;
+  }
+  free(part);
+}
+
+static double dot(const double *a, const double *b, int64_t len) {
+  double s = 0;
+  for (int64_t i = 0; i < len; ++i) s += a[i] * b[i];
+  return s;
+}
+static double dot_omp(const double *a, const double *b, int64_t len, int threads) {
+  double s = 0;
+#pragma omp parallel for reduction(+ : s) schedule(static) num_threads(threads)
+  for (int64_t i = 0; i < len; ++i) s += a[i] * b[i];
+  return s;
+}
+
+/* --------------------------------------------------------- power method */
+/* operators.cpp:302-339 applied to op_C (:353-369) */
+int cro_sigma_C(const double *X, int64_t N, int64_t n, double tol, int max_iters,
+                double *sigma, int *iters, int *converged) {
+  const int64_t cols = N * (n + 1);
+  const int64_t rows = N * (N - 1) + N;
+  double *v = (double *)malloc(sizeof(double) * (size_t)cols);
+  double *u = (double *)malloc(sizeof(double) * (size_t)cols);
+  double *w = (double *)malloc(sizeof(double) * (size_t)rows);
+  if (!v || !u || !w) { free(v); free(u); free(w); return -1; }
+  xo256 g = rng_stream(0x5eedULL, 97);
+  for (int64_t k = 0; k < cols; ++k) v[k] = xo_normal(&g);
+  double nv = sqrt(dot(v, v, cols));
+  for (int64_t k = 0; k < cols; ++k) v[k] /= nv;
+  double lambda_prev = 0;
+  *converged = 1;
+  *iters = 0;
+  for (int it = 1; it <= max_iters; ++it) {
+    cro_apply_C(X, N, n, v, v + N, w);
+    const double lambda = dot(w, w, rows);
+    cro_apply_C_T(X, N, n, w, u, u + N);
+    const double norm_u = sqrt(dot(u, u, cols));
+    if (norm_u == 0 || lambda == 0) {
+      *sigma = 0;
+      *iters = it;
+      free(v); free(u); free(w);
+      return 0;
+    }
+    for (int64_t k = 0; k < cols; ++k) v[k] = u[k] / norm_u;
+    *iters = it;
+    if (it > 1 && fabs(lambda - lambda_prev) <= tol * lambda) {
+      *sigma = sqrt(lambda) * 1.01;
+      *converged = 1;
+      free(v); free(u); free(w);
+      return 0;
+    }
+    lambda_prev = lambda;
+  }
+  *sigma = sqrt(lambda_prev) * 1.10;
+  *converged = 0;
+  free(v); free(u); free(w);
+  return 0;
+}
+
+/* ----------------------------------------------------------- small ops */
+void cro_project_nonneg_ball(double *v, int64_t len, double radius) { /* projections.hpp:9-13 */
+  for (int64_t i = 0; i < len; ++i) v[i] = v[i] > 0.0 ? v[i] : 0.0;
+  const double norm = sqrt(dot(v, v, len));
+  if (norm > radius) {
+    const double s = radius / norm;
+    for (int64_t i = 0; i < len; ++i) v[i] *= s;
+  }
+}
+double cro_momentum_next(double t) { return 0.5 * (1.0 + sqrt(1.0 + 4.0 * t * t)); }
+void cro_certificate(double gamma, double delta, double B_xi, double sigma, double out2[2]) {
+  const double spread = sqrt(2.0 * (delta > 0 ? delta : 0.0) / gamma) * sigma; /* papg.cpp:301 */
+  out2[0] = B_xi * sqrt(gamma) + spread;
+  out2[1] = spread;
+}
+int64_t cro_cross_position(int64_t N, int64_t K, int64_t l1, int64_t l2) { /* indexing.hpp:30-37 */
+  const int64_t nbar = N / K;
+  const int64_t i = l1 / nbar, j = l2 / nbar;
+  if (i == j) return -1;
+  const int64_t pair_rank = i * (K - 1) + j - (j > i ? 1 : 0);
+  const int64_t local = (l1 - i * nbar) * nbar + (l2 - j * nbar);
+  return pair_rank * nbar * nbar + local;
+}
+
+static double now_seconds(void) {
+  struct timespec ts;
+  clock_gettime(CLOCK_MONOTONIC, &ts);
+  return (double)ts.tv_sec + 1e-9 * (double)ts.tv_nsec;
+}
+
+/* ------------------------------------------------------ dual ascent loop */
+typedef struct {
+  const double *X, *ys;
+  int64_t N, n;
+  double gamma;
+  int threads;
+  double *q_y, *q_xi; /* C^T theta */
+  double *ey, *exi;   /* eta */
+} dg_ctx;
+
+/* papg.cpp:89-132 with the singleton closed-form block minimiser
+   (alcc.cpp:233-235 centres; block objective alcc.cpp:254-256). */
+static double dual_gradient(dg_ctx *c, const double *theta, double *C_eta) {
+  const int64_t N = c->N, n = c->n;
+  if (c->threads > 1) apply_C_T_omp(c->X, N, n, theta, c->q_y, c->q_xi, c->threads);
+  else cro_apply_C_T(c->X, N, n, theta, c->q_y, c->q_xi);
+  double g = 0;
+  for (int64_t i = 0; i < N; ++i) { /* block i = {i}; gathered in block order (:124-128) */
+    const double y = c->ys[i] + c->q_y[i];
+    c->ey[i] = y;
+    double xx = 0, qx = 0;
+    for (int64_t j = 0; j < n; ++j) {
+      const double xi = c->q_xi[i * n + j] / c->gamma;
+      c->exi[i * n + j] = xi;
+      xx += xi * xi;
+      qx += c->q_xi[i * n + j] * xi;
+    }
+    const double dy = y - c->ys[i];
+    const double obj = 0.5 * (dy * dy) + 0.5 * c->gamma * xx - c->q_y[i] * y - qx;
+    g += obj;
+  }
+  if (c->threads > 1) apply_C_omp(c->X, N, n, c->ey, c->exi, C_eta, c->threads);
+  else cro_apply_C(c->X, N, n, c->ey, c->exi, C_eta);
+  return g;
+}
+
+int cro_papg(const double *X, const double *ys, int64_t N, int64_t n, const cro_config *cfg,
+             const double *theta0, cro_result *res) {
+  const double start = now_seconds();
+  if (N < 2 || n < 1 || cfg->gamma <= 0) return -1;
+  const int threads = cfg->threads > 1 ? cfg->threads : 1;
+  const int64_t rows_total = N * (N - 1); /* papg.cpp:142-145 */
+  const int64_t rows_cross = rows_total;  /* singleton: rows_cross = N(N - nbar) = N(N-1) */
+  const int64_t dim = rows_cross + N;
+  const double infeas_div = sqrt((double)rows_total);
+  const double gap_div = (double)rows_total;
+
+  double sigma_C = cfg->sigma_C;
+  res->sigma_iters = 0;
+  res->sigma_converged = 1;
+  if (!(sigma_C > 0)) {
+    int it = 0, conv = 0;
+    if (cro_sigma_C(X, N, n, 1e-6, 5000, &sigma_C, &it, &conv)) return -2;
+    res->sigma_iters = it;
+    res->sigma_converged = conv;
+  }
+  const double L_g = sigma_C * sigma_C / cfg->gamma; /* papg.hpp:43 */
+  double B_theta = cfg->B_theta > 0 ? cfg->B_theta : 10.0 * sqrt((double)N);
+  res->sigma_C = sigma_C;
+  res->L_g = L_g;
+  res->reason = CRO_ITER_BUDGET;
+
+  double *theta1 = (double *)calloc((size_t)dim, sizeof(double));
+  double *theta1_prev = (double *)malloc(sizeof(double) * (size_t)dim);
+  double *theta2 = (double *)malloc(sizeof(double) * (size_t)dim);
+  double *C_eta = (double *)malloc(sizeof(double) * (size_t)dim);
+  dg_ctx c = {X, ys, N, n, cfg->gamma, threads,
+              (double *)malloc(sizeof(double) * (size_t)N),
+              (double *)malloc(sizeof(double) * (size_t)(N * n)),
+              (double *)malloc(sizeof(double) * (size_t)N),
+              (double *)malloc(sizeof(double) * (size_t)(N * n))};
+  if (!theta1 || !theta1_prev || !theta2 || !C_eta) return -3;
+  if (theta0) { /* papg.cpp:159-164 */
+    memcpy(theta1, theta0, sizeof(double) * (size_t)dim);
+    cro_project_nonneg_ball(theta1, dim, B_theta);
+  }
+  memcpy(theta1_prev, theta1, sizeof(double) * (size_t)dim);
+  memcpy(theta2, theta1, sizeof(double) * (size_t)dim);
+  double t = 1.0;
+  double g_star_upper = INFINITY;
+  const int64_t K = N; /* singleton partition */
+  int64_t ell = 0;
+  int restarts = 0;
+  int rc = 0;
+
+  while (1) {
+    ++ell;
+    const double inv3 = 1.0 / ((double)ell * (double)ell * (double)ell);
+    const double inner_tol = cfg->inner_tol_floor < inv3 ? cfg->inner_tol_floor : inv3;
+
+    const double g_value = dual_gradient(&c, theta2, C_eta); /* :183 */
+    int finite = 1;
+    for (int64_t i = 0; i < dim; ++i) if (!isfinite(C_eta[i])) { finite = 0; break; }
+    if (!finite) { res->reason = CRO_ERROR; rc = -4; break; } /* :184-185 */
+
+    { double *tmp = theta1_prev; theta1_prev = theta1; theta1 = tmp; } /* :187 */
+    if (threads > 1) {
+#pragma omp parallel for schedule(static) num_threads(threads)
+      for (int64_t i = 0; i < dim; ++i) theta1[i] = theta2[i] - C_eta[i] / L_g; /* :188 */
+      double ss = 0;
+#pragma omp parallel for reduction(+ : ss) schedule(static) num_threads(threads)
+      for (int64_t i = 0; i < dim; ++i) {
+        theta1[i] = theta1[i] > 0.0 ? theta1[i] : 0.0;
+        ss += theta1[i] * theta1[i];
+      }
+      const double norm = sqrt(ss);
+      if (norm > B_theta) {
+        const double s = B_theta / norm;
+#pragma omp parallel for schedule(static) num_threads(threads)
+        for (int64_t i = 0; i < dim; ++i) theta1[i] *= s;
+      }
+    } else {
+      for (int64_t i = 0; i < dim; ++i) theta1[i] = theta2[i] - C_eta[i] / L_g; /* :188 */
+      cro_project_nonneg_ball(theta1, dim, B_theta);                          /* :189 */
+    }
+
+    /* :191-199 linearisation bound */
+    double cross_sq = 0, all_sq = 0;
+    for (int64_t i = 0; i < dim; ++i) {
+      const double m = -C_eta[i] > 0.0 ? -C_eta[i] : 0.0;
+      if (i < rows_cross) cross_sq += m * m;
+      all_sq += m * m;
+    }
+    const double cross_infeas = rows_cross > 0 ? sqrt(cross_sq) : 0.0;
+    const double t2c = threads > 1 ? dot_omp(theta2, C_eta, dim, threads) : dot(theta2, C_eta, dim);
+    const double fw = B_theta * sqrt(all_sq) + t2c;
+    const double cushion = 2.0 * inner_tol * (double)K;
+    const double cand = g_value + fw + cushion;
+    if (cand < g_star_upper) g_star_upper = cand;
+
+    /* :201-208 */
+    const double gap_raw =
+        cfg->use_momentum ? (threads > 1 ? dot_omp(theta1, C_eta, dim, threads) : dot(theta1, C_eta, dim))
+                          : t2c;
+    const double within = 0.0; /* singleton blocks have no within rows */
+    const double infeas_raw = sqrt(within * within + cross_infeas * cross_infeas);
+    const double gap_norm = gap_raw / gap_div;
+    const double infeas_norm = infeas_raw / infeas_div;
+
+    if (cfg->record_history && res->history) { /* :210-222 */
+      double obj = 0, xx = 0;
+      for (int64_t i = 0; i < N; ++i) { const double d = c.ey[i] - ys[i]; obj += d * d; }
+      for (int64_t i = 0; i < N * n; ++i) xx += c.exi[i] * c.exi[i];
+      double *h = res->history + (ell - 1) * 8;
+      h[0] = (double)ell;
+      h[1] = 0.5 * obj;
+      h[2] = 0.5 * obj + 0.5 * cfg->gamma * xx;
+      h[3] = infeas_raw;
+      h[4] = infeas_norm;
+      h[5] = gap_raw;
+      h[6] = gap_norm;
+      h[7] = now_seconds() - start;
+    }
+    res->iters = ell;
+
+    int stop = 0; /* :225-236 */
+    if (fabs(gap_norm) <= cfg->gap_norm_tol && infeas_norm <= cfg->infeas_norm_tol) {
+      res->reason = CRO_THRESHOLDS;
+      stop = 1;
+    } else if (ell >= cfg->max_iters) {
+      res->reason = CRO_ITER_BUDGET;
+      stop = 1;
+    } else if (now_seconds() - start > cfg->max_seconds) {
+      res->reason = CRO_TIME_BUDGET;
+      stop = 1;
+    }
+    if (stop) { /* :238-254 */
+      const double n1 = sqrt(threads > 1 ? dot_omp(theta1, theta1, dim, threads) : dot(theta1, theta1, dim));
+      const int saturated = n1 > 0.99 * B_theta;
+      if (saturated && cfg->adaptive_B_theta && res->reason == CRO_THRESHOLDS &&
+          restarts < cfg->max_restarts) {
+        B_theta *= 2.0;
+        ++restarts;
+        memcpy(theta2, theta1, sizeof(double) * (size_t)dim);
+        memcpy(theta1_prev, theta1, sizeof(double) * (size_t)dim);
+        t = 1.0;
+        g_star_upper = INFINITY;
+        continue;
+      }
+      res->saturated = saturated;
+      break;
+    }
+    if (cfg->use_momentum) { /* :256-262 */
+      const double t_next = cro_momentum_next(t);
+      const double beta = (t - 1.0) / t_next;
+#pragma omp parallel for schedule(static) num_threads(threads) if (threads > 1)
+      for (int64_t i = 0; i < dim; ++i) theta2[i] = theta1[i] + beta * (theta1[i] - theta1_prev[i]);
+      t = t_next;
+    } else {
+      memcpy(theta2, theta1, sizeof(double) * (size_t)dim);
+    }
+  }
+
+  if (rc == 0) {
+    if (res->c_eta) memcpy(res->c_eta, C_eta, sizeof(double) * (size_t)dim);
+    /* :265-277 final re-solve at theta1 */
+    double ft = 1.0 / pow((double)ell, 3.0);
+    if (cfg->inner_tol_floor < ft) ft = cfg->inner_tol_floor;
+    if (cfg->final_resolve_tol < ft) ft = cfg->final_resolve_tol;
+    const double g_final = dual_gradient(&c, theta1, C_eta);
+    res->g_final = g_final;
+    const double d = g_star_upper - (g_final - 2.0 * ft * (double)K);
+    res->delta_estimate = d > 0 ? d : 0.0;
+    if (res->y) memcpy(res->y, c.ey, sizeof(double) * (size_t)N);
+    if (res->xi) memcpy(res->xi, c.exi, sizeof(double) * (size_t)(N * n));
+    if (res->theta) memcpy(res->theta, theta1, sizeof(double) * (size_t)dim);
+    res->B_theta = B_theta;
+    res->restarts = restarts;
+  }
+  res->wall_seconds = now_seconds() - start;
+  free(theta1); free(theta1_prev); free(theta2); free(C_eta);
+  free(c.q_y); free(c.q_xi); free(c.ey); free(c.exi);
+  return rc;
+}

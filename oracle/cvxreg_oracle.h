@@ -1,0 +1,118 @@
+/*
+ * cvxreg_oracle.h -- TEST INFRASTRUCTURE ONLY.
+ *
+ * CPU restatement of the reference solver path (arXiv 1407.7220, `cvxreg`,
+ * /root/reference/proj/core) in the singleton-block closed form. It is the
+ * parity checker for the CUDA path and the CPU baseline timed by bench.py.
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+ * --impl reference legs may load it. The product library never links it.
+ *
+ * Parity status: the reference cannot be compiled here (Eigen3 and vendor/
+ * headers absent, alcc.cpp:200-203 arity error) and cannot run singleton
+ * blocks (dataset.cpp:125-126). It ships no tests or golden vectors. This
+ * restatement is therefore pinned against the SPEC.md worked examples and
+ * analytic known-answer tests only ("parity unpinned" w.r.t. a reference
+ * binary; see DESIGN.md section "Oracle").
+ */
+#ifndef CVXREG_ORACLE_H
+#define CVXREG_ORACLE_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* generator kinds: 0..3 restate testgen.cpp:36-87; 10..12 are the BASELINE.json kinds */
+enum {
+  CRO_GEN_QUADRATIC = 0,
+  CRO_GEN_EXPONENTIAL = 1,
+  CRO_GEN_AFFINE_NOISELESS = 2,
+  CRO_GEN_CUSTOM_1D = 3,
+  CRO_GEN_SQNORM_UNIFORM = 10,    /* cfg 1, 4: y = |x|^2 + eps, x~U[-1,1]^n, eps~U[-a,a] */
+  CRO_GEN_MAXAFFINE_UNIFORM = 11, /* cfg 2, 5: y = max_i a_i.x + b_i + eps */
+  CRO_GEN_LSE_UNIFORM = 12        /* cfg 3:    y = log sum_k exp(a_k.x) + eps */
+};
+
+/* termination reasons, metrics.hpp:41 */
+enum { CRO_THRESHOLDS = 0, CRO_ITER_BUDGET = 1, CRO_TIME_BUDGET = 2, CRO_ERROR = 3 };
+
+typedef struct {
+  double gamma;            /* papg.hpp:8  */
+  double B_theta;          /* <= 0: adaptive 10 sqrt(N) (papg.cpp:149-150) */
+  int32_t adaptive_B_theta;
+  int32_t max_restarts;
+  double gap_norm_tol;
+  double infeas_norm_tol;
+  int64_t max_iters;
+  double max_seconds;
+  double inner_tol_floor;
+  double final_resolve_tol;
+  int32_t record_history;
+  int32_t use_momentum;    /* 1: papg_solve, 0: dual_gradient_ascent (papg.cpp:287-296) */
+  double sigma_C;          /* > 0: inject sigma_C (skips power iteration) */
+  int32_t threads;         /* <= 1: literal single-thread loops; > 1: OpenMP rows */
+  int32_t pad_;
+} cro_config;
+
+typedef struct {
+  /* caller-owned output arrays (may be NULL) */
+  double *y;       /* N */
+  double *xi;      /* N*n */
+  double *theta;   /* N(N-1)+N canonical [theta_cross; theta_pos] */
+  double *c_eta;   /* N(N-1)+N: C eta of the LAST loop iteration */
+  double *history; /* max_iters * 8: iter, objective, reg_objective, infeas_raw,
+                      infeas_norm, gap_raw, gap_norm, wall_time_s */
+  /* scalars */
+  int64_t iters;
+  int32_t reason;
+  int32_t restarts;
+  int32_t saturated;
+  int32_t sigma_iters;
+  int32_t sigma_converged;
+  int32_t pad_;
+  double g_final;
+  double delta_estimate;
+  double sigma_C;
+  double L_g;
+  double B_theta;
+  double wall_seconds;
+} cro_result;
+
+/* PRNG (rng.hpp:7-59) */
+uint64_t cro_rng_draws(uint64_t seed, uint64_t tag, int64_t count, int kind, double *out);
+
+/* generators; pieces = number of affine pieces / LSE terms for kinds 11/12.
+   returns 0 on success, -1 on invalid arguments, -2 on duplicate rows. */
+int cro_gen_instance(int kind, int64_t N, int64_t n, double noise, uint64_t seed,
+                     int64_t pieces, double *X /*N*n row-major*/, double *y /*N*/);
+
+/* preprocess.cpp:9-65. bounds4 = {B_theta, Bbar_y, Bbar_xi, gamma}.
+   feas_y (N) and feas_xi (N*n) are in the shifted frame. */
+int cro_prepare(const double *X, const double *y, int64_t N, int64_t n, double gamma,
+                double *ys_shifted, double *shift, double *feas_y, double *feas_xi,
+                double *bounds4, double *intercept, double *slope /*n*/);
+
+/* operators.cpp:128-180 in singleton order (K = N, nbar = 1) */
+void cro_apply_C(const double *X, int64_t N, int64_t n, const double *y, const double *xi,
+                 double *out /*N(N-1)+N*/);
+void cro_apply_C_T(const double *X, int64_t N, int64_t n, const double *theta,
+                   double *out_y /*N*/, double *out_xi /*N*n*/);
+
+/* operators.cpp:302-339 with op_C (:353-369) */
+int cro_sigma_C(const double *X, int64_t N, int64_t n, double tol, int max_iters,
+                double *sigma, int *iters, int *converged);
+
+/* papg.cpp:136-283 (singleton closed form). theta0: canonical or NULL. */
+int cro_papg(const double *X, const double *ys_shifted, int64_t N, int64_t n,
+             const cro_config *cfg, const double *theta0, cro_result *res);
+
+/* projections.hpp:9-13, engines.hpp:11-13, papg.cpp:298-303 */
+void cro_project_nonneg_ball(double *v, int64_t len, double radius);
+double cro_momentum_next(double t);
+void cro_certificate(double gamma, double delta, double B_xi, double sigma, double out2[2]);
+int64_t cro_cross_position(int64_t N, int64_t K, int64_t l1, int64_t l2);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

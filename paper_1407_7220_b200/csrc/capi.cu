@@ -1,0 +1,881 @@
+// capi.cu -- the C ABI (include/cvxreg_b200.h): handle lifetime, device
+// buffers, the device-resident dual loop (CUDA graphs or direct launches),
+// the power method for sigma_max(C), NCCL for row-sharded runs and the
+// canonical-order import/export of the dual point.
+//
+// The host loop of the reference (papg.cpp:136-283) is split: the per-
+// iteration scalar logic runs on the device (control_kernel), so the host
+// only enqueues work and polls a halt flag once per batch of iterations.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <chrono>
+#include <climits>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/cvxreg_b200.h"
+#include "device.cuh"
+#include "host.hpp"
+#include "kernels.cuh"
+
+using namespace crb;
+
+struct cr_handle {
+  int device = 0;
+  cudaStream_t st = nullptr;
+  int64_t N = 0, n = 0, r0 = 0, r1 = 0, R = 0, ld = 0;
+  int RP = 0;
+  double gamma = 1e-3;
+  SweepKernelInfo kp{}, kw{};
+  int S = 0, P = 0;
+  int k2_blocks = 0;
+  // device buffers
+  double *X = nullptr, *ybar = nullptr, *rowrec = nullptr, *colrec = nullptr;
+  double *V[2] = {nullptr, nullptr}, *vpos[2] = {nullptr, nullptr};
+  double *xbuf = nullptr, *aggsave = nullptr;
+  double *colpart = nullptr, *rowpart = nullptr, *scalpart = nullptr;
+  double *k2part = nullptr, *k2sum = nullptr, *hist = nullptr;
+  double *yout = nullptr, *xiout = nullptr;
+  double *pw_u = nullptr, *pw_v = nullptr, *pw_part = nullptr, *pw_sum = nullptr;
+  double *consts = nullptr;  // {1, 1, 0}
+  int *izero = nullptr;      // constant 0 (slot index / never halted)
+  double *stage = nullptr;
+  int64_t stage_elems = 0;
+  int64_t hist_cap = 0;
+  DevCtrl* ctrl_d = nullptr;
+  DevCtrl* ctrl_h = nullptr;     // pinned mirror (latest copy)
+  DevCtrl* ctrl_poll = nullptr;  // pinned, 2 polling slots
+  long long* pause_h = nullptr;  // pinned {pause_at, halt}
+  // NCCL
+  ncclComm_t comm = nullptr;
+  int rank = 0, world = 1;
+  // loop state
+  cr_papg_config cfg{};
+  bool begun = false;
+  int graph_iters = 0;  // 0: direct launches
+  cudaGraphExec_t gexec = nullptr;
+  double sigma_C = 0, L = 0, sigma_seconds = 0;
+  int sigma_iters = 0, sigma_conv = 1;
+  std::chrono::steady_clock::time_point t_begin;
+  double loop_seconds = 0;
+  // timing
+  cudaEvent_t ev_start = nullptr, ev_end = nullptr, ev_poll[2] = {nullptr, nullptr};
+  std::vector<cudaEvent_t> ev_sweep;  // pairs
+  double last_seconds = 0, last_sweep_seconds = 0;
+  int64_t last_launches = 0;
+  std::string err;
+};
+
+namespace {
+
+cr_status fail(cr_handle* h, cr_status s, const std::string& what) {
+  if (h) h->err = what;
+  return s;
+}
+
+#define CUDA_TRY(call)                                                                   \
+  do {                                                                                   \
+    cudaError_t e_ = (call);                                                             \
+    if (e_ != cudaSuccess)                                                               \
+      return fail(h, CR_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_));      \
+  } while (0)
+
+#define NCCL_TRY(call)                                                                   \
+  do {                                                                                   \
+    ncclResult_t r_ = (call);                                                            \
+    if (r_ != ncclSuccess)                                                               \
+      return fail(h, CR_ENCCL, std::string(#call) + ": " + ncclGetErrorString(r_));      \
+  } while (0)
+
+template <typename T>
+cudaError_t dalloc(T** p, size_t count) {
+  return cudaMalloc((void**)p, (count ? count : 1) * sizeof(T));
+}
+
+int64_t payload_len(const cr_handle* h) { return h->N * (h->n + 2) + kScal; }
+
+SweepArgs sweep_args(cr_handle* h, int mode, bool agg_only) {
+  SweepArgs a{};
+  a.V0 = h->V[0];
+  a.V1 = h->V[1];
+  a.cur = &h->ctrl_d->cur;
+  a.rowrec = h->rowrec;
+  a.colrec = h->colrec;
+  a.colpart = h->colpart;
+  a.rowpart = h->rowpart;
+  a.scalpart = h->scalpart;
+  a.coef = agg_only ? h->consts : &h->ctrl_d->s_cur;
+  a.stopped = (mode == kModePapg && !agg_only) ? &h->ctrl_d->halt : nullptr;
+  a.invL = agg_only ? 0.0 : 1.0 / h->L;
+  a.N = h->N;
+  a.R = h->R;
+  a.r0 = h->r0;
+  a.ld = h->ld;
+  a.S = h->S;
+  a.P = h->P;
+  return a;
+}
+
+ReduceArgs reduce_args(cr_handle* h, bool with_k2, const int* stopped) {
+  ReduceArgs a{};
+  a.colpart = h->colpart;
+  a.rowpart = h->rowpart;
+  a.scalpart = h->scalpart;
+  a.k2part = h->k2part;
+  a.agg_out = h->xbuf;
+  a.k2sum = with_k2 ? h->k2sum : nullptr;
+  a.stopped = stopped;
+  a.rank = h->rank;
+  a.N = h->N;
+  a.ld = h->ld;
+  a.R = h->R;
+  a.r0 = h->r0;
+  a.nw = (long long)h->S * h->P;
+  a.nk2 = with_k2 ? h->k2_blocks : 0;
+  a.n1 = (int)h->n + 1;
+  a.P = h->P;
+  a.S = h->S;
+  return a;
+}
+
+PrimalArgs primal_args(cr_handle* h, int mode) {
+  PrimalArgs a{};
+  a.X = h->X;
+  a.ybar = h->ybar;
+  a.rowrec = h->rowrec;
+  a.colrec = h->colrec;
+  a.aggc = h->xbuf;
+  a.aggp = h->aggsave;
+  a.vpos0 = h->vpos[0];
+  a.vpos1 = h->vpos[1];
+  a.cur = &h->ctrl_d->cur;
+  a.k2part = h->k2part;
+  a.coef = &h->ctrl_d->s_cur;
+  a.stopped = mode == 0 ? &h->ctrl_d->halt : nullptr;
+  a.yout = h->yout;
+  a.xiout = h->xiout;
+  a.invL = 1.0 / h->L;
+  a.gamma = h->cfg.gamma;
+  a.N = h->N;
+  a.n = (int)h->n;
+  a.mode = mode;
+  return a;
+}
+
+// Enqueue one dual iteration (papg.cpp:176-263). phase: 0 = all,
+// 1 = local part only (K2, K1, K3), 2 = finish only (control).
+cr_status enqueue_iteration(cr_handle* h, int phase, cudaEvent_t ev_a, cudaEvent_t ev_b,
+                            bool use_nccl) {
+  if (phase != 2) {
+    const PrimalArgs pa = primal_args(h, 0);
+    CUDA_TRY(launch_primal(pa, h->st));
+    const SweepArgs sa = sweep_args(h, kModePapg, false);
+    if (ev_a) CUDA_TRY(cudaEventRecord(ev_a, h->st));
+    CUDA_TRY((cudaError_t)launch_sweep(h->kp, sa, (int)h->n, h->st));
+    if (ev_b) CUDA_TRY(cudaEventRecord(ev_b, h->st));
+    const ReduceArgs ra = reduce_args(h, true, &h->ctrl_d->halt);
+    CUDA_TRY(launch_reduce(ra, h->st));
+    if (use_nccl && h->comm)
+      NCCL_TRY(ncclAllReduce(h->xbuf, h->xbuf, (size_t)payload_len(h), ncclDouble, ncclSum,
+                             h->comm, h->st));
+  }
+  if (phase != 1)
+    CUDA_TRY(launch_control(h->ctrl_d, h->xbuf + h->N * (h->n + 2), h->k2sum, h->hist, h->st));
+  return CR_OK;
+}
+
+int launches_per_iteration(const cr_handle* h) { return 4 + (h->comm ? 1 : 0); }
+
+cr_status build_graph(cr_handle* h) {
+  if (h->gexec) {
+    cudaGraphExecDestroy(h->gexec);
+    h->gexec = nullptr;
+  }
+  cudaGraph_t g = nullptr;
+  CUDA_TRY(cudaStreamBeginCapture(h->st, cudaStreamCaptureModeThreadLocal));
+  cr_status s = CR_OK;
+  for (int i = 0; i < h->graph_iters && s == CR_OK; ++i)
+    s = enqueue_iteration(h, 0, nullptr, nullptr, true);
+  cudaError_t e = cudaStreamEndCapture(h->st, &g);
+  if (s != CR_OK) {
+    if (g) cudaGraphDestroy(g);
+    return s;
+  }
+  CUDA_TRY(e);
+  e = cudaGraphInstantiate(&h->gexec, g, 0);
+  cudaGraphDestroy(g);
+  CUDA_TRY(e);
+  return CR_OK;
+}
+
+cr_status sync_ctrl(cr_handle* h) {
+  CUDA_TRY(cudaMemcpyAsync(h->ctrl_h, h->ctrl_d, sizeof(DevCtrl), cudaMemcpyDeviceToHost, h->st));
+  CUDA_TRY(cudaStreamSynchronize(h->st));
+  return CR_OK;
+}
+
+// one power step (operators.cpp:318-327); returns lambda and |u|
+cr_status power_step(cr_handle* h, double norm_u, double* lambda, double* nu) {
+  PowerArgs pa{};
+  pa.X = h->X;
+  pa.u = h->pw_u;
+  pa.v = h->pw_v;
+  pa.norm_u = norm_u;
+  pa.rowrec = h->rowrec;
+  pa.colrec = h->colrec;
+  pa.agg = h->xbuf;
+  pa.part = h->pw_part;
+  pa.N = h->N;
+  pa.n = (int)h->n;
+  CUDA_TRY(launch_power_prep(pa, h->st));
+  SweepArgs sa = sweep_args(h, kModePower, false);
+  sa.cur = h->izero;
+  CUDA_TRY((cudaError_t)launch_sweep(h->kw, sa, (int)h->n, h->st));
+  const ReduceArgs ra = reduce_args(h, false, nullptr);
+  CUDA_TRY(launch_reduce(ra, h->st));
+  if (h->comm)
+    NCCL_TRY(ncclAllReduce(h->xbuf, h->xbuf, (size_t)payload_len(h), ncclDouble, ncclSum, h->comm,
+                           h->st));
+  CUDA_TRY(launch_power_post(pa, h->st));
+  CUDA_TRY(launch_reduce_records(h->pw_part, primal_blocks(h->N), 2, h->pw_sum, h->st));
+  double host[3];
+  CUDA_TRY(cudaMemcpyAsync(host, h->xbuf + h->N * (h->n + 2), sizeof(double),
+                           cudaMemcpyDeviceToHost, h->st));
+  CUDA_TRY(cudaMemcpyAsync(host + 1, h->pw_sum, 2 * sizeof(double), cudaMemcpyDeviceToHost,
+                           h->st));
+  CUDA_TRY(cudaStreamSynchronize(h->st));
+  *lambda = host[0] + host[1];
+  *nu = std::sqrt(host[2]);
+  return CR_OK;
+}
+
+cr_status set_pause(cr_handle* h, long long pause_at) {
+  h->pause_h[0] = pause_at;
+  const int halt = (h->ctrl_h->stopped || h->ctrl_h->ell >= pause_at) ? 1 : 0;
+  reinterpret_cast<int*>(h->pause_h + 1)[0] = halt;
+  CUDA_TRY(cudaMemcpyAsync(&h->ctrl_d->pause_at, h->pause_h, sizeof(long long),
+                           cudaMemcpyHostToDevice, h->st));
+  CUDA_TRY(cudaMemcpyAsync(&h->ctrl_d->halt, h->pause_h + 1, sizeof(int), cudaMemcpyHostToDevice,
+                           h->st));
+  return CR_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* cr_status_string(cr_status s) {
+  switch (s) {
+    case CR_OK: return "ok";
+    case CR_EINVAL: return "invalid argument";
+    case CR_ENOMEM: return "out of memory";
+    case CR_ECUDA: return "CUDA error";
+    case CR_ENCCL: return "NCCL error";
+    case CR_ENONFINITE: return "papg: non-finite dual gradient";
+    case CR_ESTATE: return "call out of order";
+  }
+  return "unknown";
+}
+
+const char* cr_last_error(const cr_handle* h) { return h ? h->err.c_str() : "null handle"; }
+
+int64_t cr_exchange_len(const cr_handle* h) { return h ? payload_len(h) : 0; }
+
+cr_status cr_create(const double* Xh, const double* ybar_shifted, int64_t N, int64_t n,
+                    double gamma, int device, int64_t row_begin, int64_t row_end,
+                    cr_handle** out) {
+  if (!out) return CR_EINVAL;
+  *out = nullptr;
+  if (!Xh || !ybar_shifted || N < 2 || n < 1 || !(gamma > 0) || row_begin < 0 ||
+      row_end > N || row_begin >= row_end)
+    return CR_EINVAL;
+  if (n > kMaxN) return CR_EINVAL;
+  cr_handle* h = new cr_handle();
+  *out = h;
+  h->device = device;
+  h->N = N;
+  h->n = n;
+  h->r0 = row_begin;
+  h->r1 = row_end;
+  h->R = row_end - row_begin;
+  h->RP = (int)((n + 2) & ~1LL);
+  h->gamma = gamma;
+  h->cfg.gamma = gamma;
+  CUDA_TRY(cudaSetDevice(device));
+  CUDA_TRY(cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking));
+  h->kp = sweep_kernel_info((int)n, kModePapg);
+  h->kw = sweep_kernel_info((int)n, kModePower);
+  if (!h->kp.fn || !h->kw.fn || h->kp.max_blocks_per_sm < 1)
+    return fail(h, CR_EINVAL, "no sweep kernel for this n");
+  const int W = 32 * h->kp.C;
+  h->S = (int)((N + W - 1) / W);
+  h->ld = (int64_t)h->S * W;
+  int sms = 148;
+  CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+  const long long resident = (long long)sms * h->kp.max_blocks_per_sm * h->kp.warps_per_block;
+  long long P = resident / h->S;
+  const long long pmax = (h->R + 31) / 32;
+  if (P > pmax) P = pmax;
+  if (P < 1) P = 1;
+  h->P = (int)P;
+  h->k2_blocks = primal_blocks(N);
+
+  const size_t RP = (size_t)h->RP;
+  const size_t vlen = (size_t)h->R * (size_t)h->ld;
+  cudaError_t e = cudaSuccess;
+#define ALLOC(ptr, count)                                             \
+  if (e == cudaSuccess) e = dalloc(&(ptr), (size_t)(count));
+  ALLOC(h->X, N * n);
+  ALLOC(h->ybar, N);
+  ALLOC(h->rowrec, N * RP);
+  ALLOC(h->colrec, N * RP);
+  ALLOC(h->V[0], vlen);
+  ALLOC(h->V[1], vlen);
+  ALLOC(h->vpos[0], N);
+  ALLOC(h->vpos[1], N);
+  ALLOC(h->xbuf, payload_len(h));
+  ALLOC(h->aggsave, payload_len(h));
+  ALLOC(h->colpart, (size_t)h->P * h->ld * (n + 1));
+  ALLOC(h->rowpart, (size_t)h->S * h->R);
+  ALLOC(h->scalpart, (size_t)h->S * h->P * kScal);
+  ALLOC(h->k2part, (size_t)h->k2_blocks * kK2Scal);
+  ALLOC(h->k2sum, kK2Scal);
+  ALLOC(h->yout, N);
+  ALLOC(h->xiout, N * n);
+  ALLOC(h->pw_u, N * (n + 1));
+  ALLOC(h->pw_v, N * (n + 1));
+  ALLOC(h->pw_part, (size_t)h->k2_blocks * 2);
+  ALLOC(h->pw_sum, 2);
+  ALLOC(h->consts, 4);
+  ALLOC(h->izero, 1);
+  ALLOC(h->ctrl_d, 1);
+#undef ALLOC
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(h, CR_ENOMEM, std::string("device allocation failed: ") + cudaGetErrorString(e));
+  }
+  h->stage_elems = std::min<int64_t>((int64_t)1 << 25, h->R * (N - 1) + N);  // <= 256 MB
+  if (cudaMalloc(&h->stage, (size_t)h->stage_elems * sizeof(double)) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(h, CR_ENOMEM, "stage allocation failed");
+  }
+  CUDA_TRY(cudaMallocHost(&h->ctrl_h, sizeof(DevCtrl)));
+  CUDA_TRY(cudaMallocHost(&h->ctrl_poll, 2 * sizeof(DevCtrl)));
+  CUDA_TRY(cudaMallocHost(&h->pause_h, 2 * sizeof(long long)));
+  std::memset(h->ctrl_h, 0, sizeof(DevCtrl));
+  CUDA_TRY(cudaEventCreate(&h->ev_start));
+  CUDA_TRY(cudaEventCreate(&h->ev_end));
+  CUDA_TRY(cudaEventCreateWithFlags(&h->ev_poll[0], cudaEventDisableTiming));
+  CUDA_TRY(cudaEventCreateWithFlags(&h->ev_poll[1], cudaEventDisableTiming));
+
+  // static inputs: X, ybar, row records (y placeholder, x, pad)
+  CUDA_TRY(cudaMemcpyAsync(h->X, Xh, sizeof(double) * N * n, cudaMemcpyHostToDevice, h->st));
+  CUDA_TRY(cudaMemcpyAsync(h->ybar, ybar_shifted, sizeof(double) * N, cudaMemcpyHostToDevice,
+                           h->st));
+  std::vector<double> rec((size_t)N * RP, 0.0);
+  for (int64_t l = 0; l < N; ++l) {
+    rec[l * RP] = ybar_shifted[l];
+    for (int64_t j = 0; j < n; ++j) rec[l * RP + 1 + j] = Xh[l * n + j];
+  }
+  CUDA_TRY(cudaMemcpyAsync(h->rowrec, rec.data(), sizeof(double) * rec.size(),
+                           cudaMemcpyHostToDevice, h->st));
+  CUDA_TRY(cudaMemsetAsync(h->colrec, 0, sizeof(double) * N * RP, h->st));
+  const double consts[4] = {1.0, 1.0, 0.0, 0.0};
+  CUDA_TRY(cudaMemcpyAsync(h->consts, consts, sizeof(consts), cudaMemcpyHostToDevice, h->st));
+  CUDA_TRY(cudaMemsetAsync(h->izero, 0, sizeof(int), h->st));
+  CUDA_TRY(cudaMemsetAsync(h->ctrl_d, 0, sizeof(DevCtrl), h->st));
+  CUDA_TRY(cudaStreamSynchronize(h->st));
+  return CR_OK;
+}
+
+void cr_destroy(cr_handle* h) {
+  if (!h) return;
+  cudaSetDevice(h->device);
+  if (h->st) cudaStreamSynchronize(h->st);
+  if (h->gexec) cudaGraphExecDestroy(h->gexec);
+  if (h->comm) ncclCommDestroy(h->comm);
+  double* bufs[] = {h->X,       h->ybar,    h->rowrec,  h->colrec,   h->V[0],   h->V[1],
+                    h->vpos[0], h->vpos[1], h->xbuf,    h->aggsave,  h->colpart, h->rowpart,
+                    h->scalpart, h->k2part, h->k2sum,   h->hist,     h->yout,   h->xiout,
+                    h->pw_u,    h->pw_v,    h->pw_part, h->pw_sum,   h->consts, h->stage};
+  for (double* b : bufs)
+    if (b) cudaFree(b);
+  if (h->izero) cudaFree(h->izero);
+  if (h->ctrl_d) cudaFree(h->ctrl_d);
+  if (h->ctrl_h) cudaFreeHost(h->ctrl_h);
+  if (h->ctrl_poll) cudaFreeHost(h->ctrl_poll);
+  if (h->pause_h) cudaFreeHost(h->pause_h);
+  for (cudaEvent_t ev : h->ev_sweep) cudaEventDestroy(ev);
+  if (h->ev_start) cudaEventDestroy(h->ev_start);
+  if (h->ev_end) cudaEventDestroy(h->ev_end);
+  if (h->ev_poll[0]) cudaEventDestroy(h->ev_poll[0]);
+  if (h->ev_poll[1]) cudaEventDestroy(h->ev_poll[1]);
+  if (h->st) cudaStreamDestroy(h->st);
+  delete h;
+}
+
+cr_status cr_nccl_unique_id(uint8_t id_out[128]) {
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return CR_ENCCL;
+  std::memcpy(id_out, &id, 128);
+  return CR_OK;
+}
+
+cr_status cr_attach_nccl(cr_handle* h, const uint8_t id[128], int rank, int world) {
+  if (!h || !id || world < 1 || rank < 0 || rank >= world) return CR_EINVAL;
+  CUDA_TRY(cudaSetDevice(h->device));
+  ncclUniqueId uid;
+  std::memcpy(&uid, id, 128);
+  NCCL_TRY(ncclCommInitRank(&h->comm, world, uid, rank));
+  h->rank = rank;
+  h->world = world;
+  if (h->gexec) {
+    cudaGraphExecDestroy(h->gexec);
+    h->gexec = nullptr;
+  }
+  return CR_OK;
+}
+
+cr_status cr_sigma_C(cr_handle* h, double tol, int32_t max_iters, double* sigma, int32_t* iters,
+                     int32_t* converged) {
+  if (!h || !sigma || !iters || !converged || max_iters < 1) return CR_EINVAL;
+  CUDA_TRY(cudaSetDevice(h->device));
+  const auto t0 = std::chrono::steady_clock::now();
+  const int64_t cols = h->N * (h->n + 1);
+  // fixed seeded start (operators.cpp:309-313)
+  std::vector<double> v((size_t)cols);
+  host::normal_stream(0x5eedULL, 97, cols, v.data());
+  double ss = 0;
+  for (double x : v) ss += x * x;
+  const double nv = std::sqrt(ss);
+  for (double& x : v) x /= nv;
+  CUDA_TRY(cudaMemcpyAsync(h->pw_u, v.data(), sizeof(double) * cols, cudaMemcpyHostToDevice,
+                           h->st));
+  double norm_u = 1.0;  // v = u / 1 on the first step
+  double lambda_prev = 0;
+  *converged = 1;
+  for (int it = 1; it <= max_iters; ++it) {
+    double lambda = 0, nu = 0;
+    const cr_status s = power_step(h, norm_u, &lambda, &nu);
+    if (s != CR_OK) return s;
+    if (nu == 0 || lambda == 0) {
+      *sigma = 0;
+      *iters = it;
+      h->sigma_seconds =
+          std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      return CR_OK;
+    }
+    norm_u = nu;
+    *iters = it;
+    if (it > 1 && std::fabs(lambda - lambda_prev) <= tol * lambda) {
+      *sigma = std::sqrt(lambda) * 1.01;
+      *converged = 1;
+      h->sigma_seconds =
+          std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      return CR_OK;
+    }
+    lambda_prev = lambda;
+  }
+  *sigma = std::sqrt(lambda_prev) * 1.10;
+  *converged = 0;
+  h->sigma_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  return CR_OK;
+}
+
+cr_status cr_papg_begin(cr_handle* h, const cr_papg_config* cfg, const double* theta0) {
+  if (!h || !cfg) return CR_EINVAL;
+  if (!(cfg->gamma > 0) || cfg->max_iters < 1) return fail(h, CR_EINVAL, "papg: bad config");
+  CUDA_TRY(cudaSetDevice(h->device));
+  h->t_begin = std::chrono::steady_clock::now();
+  h->cfg = *cfg;
+  h->begun = false;
+  const int64_t N = h->N;
+  // clock origin of the time budget (papg.cpp:139) is set before sigma_C
+  DevCtrl c{};
+  std::memset(&c, 0, sizeof(c));
+  CUDA_TRY(cudaMemcpyAsync(h->ctrl_d, &c, sizeof(c), cudaMemcpyHostToDevice, h->st));
+  CUDA_TRY(launch_begin(h->ctrl_d, h->st));
+  CUDA_TRY(cudaStreamSynchronize(h->st));
+  h->sigma_iters = 0;
+  h->sigma_conv = 1;
+  h->sigma_seconds = 0;
+  if (cfg->sigma_C > 0) {
+    h->sigma_C = cfg->sigma_C;
+  } else {
+    int32_t it = 0, conv = 1;
+    double s = 0;
+    const cr_status st = cr_sigma_C(h, 1e-6, 5000, &s, &it, &conv);
+    if (st != CR_OK) return st;
+    h->sigma_C = s;
+    h->sigma_iters = it;
+    h->sigma_conv = conv;
+  }
+  if (!(h->sigma_C > 0)) return fail(h, CR_EINVAL, "papg: sigma_max(C) is zero");
+  h->L = h->sigma_C * h->sigma_C / cfg->gamma;  // papg.hpp:43
+
+  // history buffer
+  const int64_t want_hist = cfg->record_history ? std::min<int64_t>(cfg->max_iters, 4000000) : 0;
+  if (want_hist > h->hist_cap) {
+    if (h->hist) cudaFree(h->hist);
+    h->hist = nullptr;
+    h->hist_cap = 0;
+    if (cudaMalloc(&h->hist, sizeof(double) * 8 * want_hist) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(h, CR_ENOMEM, "history allocation failed");
+    }
+    h->hist_cap = want_hist;
+    if (h->gexec) {
+      cudaGraphExecDestroy(h->gexec);
+      h->gexec = nullptr;
+    }
+  }
+
+  // device control block (papg.cpp:148-175)
+  CUDA_TRY(cudaMemcpyAsync(&c, h->ctrl_d, sizeof(c), cudaMemcpyDeviceToHost, h->st));
+  CUDA_TRY(cudaStreamSynchronize(h->st));
+  const unsigned long long t0 = c.t_start_ns;
+  std::memset(&c, 0, sizeof(c));
+  c.t_start_ns = t0;
+  c.ell = 0;
+  c.max_iters = cfg->max_iters;
+  c.hist_cap = cfg->record_history ? h->hist_cap : 0;
+  c.cur = 0;
+  c.max_restarts = cfg->max_restarts;
+  c.adaptive = cfg->adaptive_B_theta ? 1 : 0;
+  c.use_momentum = cfg->use_momentum ? 1 : 0;
+  c.record_history = cfg->record_history ? 1 : 0;
+  c.pause_at = LLONG_MAX;
+  c.s_cur = 1.0;
+  c.s_prev = 1.0;
+  c.beta = 0.0;
+  c.t = 1.0;
+  c.B_theta = cfg->B_theta > 0 ? cfg->B_theta : 10.0 * std::sqrt((double)N);
+  c.g_star_upper = INFINITY;
+  c.invL = 1.0 / h->L;
+  c.gamma = cfg->gamma;
+  c.gap_tol = cfg->gap_norm_tol;
+  c.infeas_tol = cfg->infeas_norm_tol;
+  c.inner_tol_floor = cfg->inner_tol_floor;
+  c.max_seconds = cfg->max_seconds;
+  c.gap_div = (double)N * (double)(N - 1);
+  c.infeas_div = std::sqrt(c.gap_div);
+  c.K = (double)N;  // singleton partition
+  CUDA_TRY(cudaMemcpyAsync(h->ctrl_d, &c, sizeof(c), cudaMemcpyHostToDevice, h->st));
+  std::memcpy(h->ctrl_h, &c, sizeof(c));
+
+  const size_t vbytes = sizeof(double) * (size_t)h->R * (size_t)h->ld;
+  CUDA_TRY(cudaMemsetAsync(h->V[0], 0, vbytes, h->st));
+  CUDA_TRY(cudaMemsetAsync(h->V[1], 0, vbytes, h->st));
+  CUDA_TRY(cudaMemsetAsync(h->vpos[0], 0, sizeof(double) * N, h->st));
+  CUDA_TRY(cudaMemsetAsync(h->vpos[1], 0, sizeof(double) * N, h->st));
+  CUDA_TRY(cudaMemsetAsync(h->xbuf, 0, sizeof(double) * payload_len(h), h->st));
+  CUDA_TRY(cudaMemsetAsync(h->aggsave, 0, sizeof(double) * payload_len(h), h->st));
+
+  if (theta0) {  // warm start: theta1 = Pi_Q2(theta0) (papg.cpp:159-164)
+    const int64_t rowlen = N - 1;
+    const int64_t rows_per = std::max<int64_t>(1, h->stage_elems / rowlen);
+    for (int64_t ra = 0; ra < h->R; ra += rows_per) {
+      const int64_t rb = std::min(h->R, ra + rows_per);
+      CUDA_TRY(cudaMemcpyAsync(h->stage, theta0 + ra * rowlen,
+                               sizeof(double) * (rb - ra) * rowlen, cudaMemcpyHostToDevice,
+                               h->st));
+      CUDA_TRY(launch_theta_in(h->stage, h->V[0], N, h->ld, h->r0, ra, rb, h->st));
+    }
+    const double* tpos = theta0 + h->R * rowlen;
+    double pos_sq = 0;
+    for (int64_t l = 0; l < N; ++l) {
+      const double t = tpos[l] > 0 ? tpos[l] : 0.0;
+      pos_sq += t * t;
+    }
+    CUDA_TRY(cudaMemcpyAsync(h->stage, tpos, sizeof(double) * N, cudaMemcpyHostToDevice, h->st));
+    CUDA_TRY(launch_pos_in(h->vpos[0], h->stage, N, h->st));
+    // aggregates and |.|^2 of max(theta0, 0): a sweep with 1/L = 0 is a copy
+    const SweepArgs sa = sweep_args(h, kModePapg, true);
+    CUDA_TRY((cudaError_t)launch_sweep(h->kp, sa, (int)h->n, h->st));
+    const ReduceArgs ra = reduce_args(h, false, nullptr);
+    CUDA_TRY(launch_reduce(ra, h->st));
+    if (h->comm)
+      NCCL_TRY(ncclAllReduce(h->xbuf, h->xbuf, (size_t)payload_len(h), ncclDouble, ncclSum,
+                             h->comm, h->st));
+    CUDA_TRY(launch_warm_ctrl(h->ctrl_d, h->xbuf + N * (h->n + 2), pos_sq, h->st));
+  }
+
+  // batch size: graphs when an iteration is short, direct launches otherwise
+  if (cfg->graph_iters > 0) {
+    h->graph_iters = cfg->graph_iters;
+  } else if (cfg->graph_iters < 0) {
+    h->graph_iters = 0;
+  } else {
+    const double est_us = 24.0 * (double)h->R * (double)h->ld / 5.0e6 + 12.0;
+    h->graph_iters = est_us > 300.0 ? 0 : (int)std::min(256.0, std::ceil(2000.0 / est_us));
+  }
+  if (h->graph_iters > 0) {
+    const cr_status s = build_graph(h);
+    if (s != CR_OK) return s;
+  }
+  const cr_status s = sync_ctrl(h);
+  if (s != CR_OK) return s;
+  h->loop_seconds = 0;
+  h->begun = true;
+  return CR_OK;
+}
+
+cr_status cr_papg_iterate(cr_handle* h, int64_t max_steps, int64_t* done, int32_t* stopped) {
+  if (!h) return CR_EINVAL;
+  if (!h->begun) return fail(h, CR_ESTATE, "papg: iterate before begin");
+  CUDA_TRY(cudaSetDevice(h->device));
+  if (max_steps < 0) max_steps = 0;
+  const long long ell0 = h->ctrl_h->ell;
+  long long pause = ell0 + max_steps;
+  if (pause < ell0) pause = LLONG_MAX;
+  cr_status s = set_pause(h, pause);
+  if (s != CR_OK) return s;
+  const bool timed_sweeps = h->graph_iters == 0;
+  const int per_unit = h->graph_iters > 0 ? h->graph_iters : 4;
+  int64_t enq_iters = 0;
+  int64_t units = 0;
+  bool halted = h->ctrl_h->stopped || max_steps == 0;
+  if (timed_sweeps) {
+    const size_t need = (size_t)2 * (size_t)std::min<int64_t>(max_steps, 1 << 16);
+    while (h->ev_sweep.size() < need) {
+      cudaEvent_t e;
+      CUDA_TRY(cudaEventCreate(&e));
+      h->ev_sweep.push_back(e);
+    }
+  }
+  int64_t timed_pairs = 0;
+  CUDA_TRY(cudaEventRecord(h->ev_start, h->st));
+  const auto wall0 = std::chrono::steady_clock::now();
+  while (!halted) {
+    if (h->graph_iters > 0) {
+      CUDA_TRY(cudaGraphLaunch(h->gexec, h->st));
+    } else {
+      for (int i = 0; i < per_unit && enq_iters + i < max_steps; ++i) {
+        cudaEvent_t a = nullptr, b = nullptr;
+        if (timed_sweeps && (size_t)(2 * timed_pairs + 1) < h->ev_sweep.size()) {
+          a = h->ev_sweep[2 * timed_pairs];
+          b = h->ev_sweep[2 * timed_pairs + 1];
+          ++timed_pairs;
+        }
+        s = enqueue_iteration(h, 0, a, b, true);
+        if (s != CR_OK) return s;
+      }
+    }
+    enq_iters += per_unit;
+    const int slot = (int)(units & 1);
+    CUDA_TRY(cudaMemcpyAsync(&h->ctrl_poll[slot], h->ctrl_d, sizeof(DevCtrl),
+                             cudaMemcpyDeviceToHost, h->st));
+    CUDA_TRY(cudaEventRecord(h->ev_poll[slot], h->st));
+    if (units >= 1) {  // keep one unit in flight while polling the previous one
+      const int ps = (int)((units - 1) & 1);
+      CUDA_TRY(cudaEventSynchronize(h->ev_poll[ps]));
+      if (h->ctrl_poll[ps].halt) halted = true;
+    }
+    ++units;
+    if (!halted && h->graph_iters == 0 && enq_iters >= max_steps) {
+      CUDA_TRY(cudaEventSynchronize(h->ev_poll[slot]));
+      halted = true;
+    }
+  }
+  CUDA_TRY(cudaEventRecord(h->ev_end, h->st));
+  s = sync_ctrl(h);
+  if (s != CR_OK) return s;
+  float ms = 0;
+  CUDA_TRY(cudaEventElapsedTime(&ms, h->ev_start, h->ev_end));
+  h->last_seconds = units > 0 ? ms * 1e-3 : 0.0;
+  double sw = 0;
+  for (int64_t i = 0; i < timed_pairs; ++i) {
+    float m = 0;
+    CUDA_TRY(cudaEventElapsedTime(&m, h->ev_sweep[2 * i], h->ev_sweep[2 * i + 1]));
+    sw += m * 1e-3;
+  }
+  h->last_sweep_seconds = sw;
+  h->last_launches = (h->graph_iters > 0 ? units * h->graph_iters
+                                         : std::min<int64_t>(enq_iters, max_steps)) *
+                     launches_per_iteration(h);
+  h->loop_seconds +=
+      std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();
+  if (done) *done = h->ctrl_h->ell;
+  if (stopped) *stopped = h->ctrl_h->stopped;
+  if (h->ctrl_h->stopped && h->ctrl_h->reason == 3)
+    return fail(h, CR_ENONFINITE, "papg: non-finite dual gradient");
+  return CR_OK;
+}
+
+cr_status cr_iter_local(cr_handle* h) {
+  if (!h) return CR_EINVAL;
+  if (!h->begun) return fail(h, CR_ESTATE, "papg: iterate before begin");
+  CUDA_TRY(cudaSetDevice(h->device));
+  cr_status s = set_pause(h, LLONG_MAX);
+  if (s != CR_OK) return s;
+  s = enqueue_iteration(h, 1, nullptr, nullptr, false);
+  if (s != CR_OK) return s;
+  CUDA_TRY(cudaStreamSynchronize(h->st));
+  return CR_OK;
+}
+
+cr_status cr_exchange_get(cr_handle* h, double* buf) {
+  if (!h || !buf) return CR_EINVAL;
+  CUDA_TRY(cudaMemcpyAsync(buf, h->xbuf, sizeof(double) * payload_len(h), cudaMemcpyDeviceToHost,
+                           h->st));
+  CUDA_TRY(cudaStreamSynchronize(h->st));
+  return CR_OK;
+}
+
+cr_status cr_exchange_put(cr_handle* h, const double* buf) {
+  if (!h || !buf) return CR_EINVAL;
+  CUDA_TRY(cudaMemcpyAsync(h->xbuf, buf, sizeof(double) * payload_len(h), cudaMemcpyHostToDevice,
+                           h->st));
+  CUDA_TRY(cudaStreamSynchronize(h->st));
+  return CR_OK;
+}
+
+cr_status cr_iter_finish(cr_handle* h, int32_t* stopped) {
+  if (!h) return CR_EINVAL;
+  if (!h->begun) return fail(h, CR_ESTATE, "papg: iterate before begin");
+  cr_status s = enqueue_iteration(h, 2, nullptr, nullptr, false);
+  if (s != CR_OK) return s;
+  s = sync_ctrl(h);
+  if (s != CR_OK) return s;
+  if (stopped) *stopped = h->ctrl_h->stopped;
+  if (h->ctrl_h->stopped && h->ctrl_h->reason == 3)
+    return fail(h, CR_ENONFINITE, "papg: non-finite dual gradient");
+  return CR_OK;
+}
+
+cr_status cr_papg_finish(cr_handle* h, cr_papg_result* res, double* y, double* xi,
+                         cr_snapshot* history) {
+  if (!h || !res) return CR_EINVAL;
+  if (!h->begun) return fail(h, CR_ESTATE, "papg: finish before begin");
+  CUDA_TRY(cudaSetDevice(h->device));
+  cr_status s = sync_ctrl(h);
+  if (s != CR_OK) return s;
+  const DevCtrl& c = *h->ctrl_h;
+  // final re-solve at theta1 (papg.cpp:265-277): primal of s_cur * V[cur]
+  const PrimalArgs pa = primal_args(h, 1);
+  CUDA_TRY(launch_primal(pa, h->st));
+  CUDA_TRY(launch_reduce_records(h->k2part, h->k2_blocks, kK2Scal, h->k2sum, h->st));
+  double k2[kK2Scal];
+  CUDA_TRY(cudaMemcpyAsync(k2, h->k2sum, sizeof(k2), cudaMemcpyDeviceToHost, h->st));
+  if (y) CUDA_TRY(cudaMemcpyAsync(y, h->yout, sizeof(double) * h->N, cudaMemcpyDeviceToHost, h->st));
+  if (xi)
+    CUDA_TRY(cudaMemcpyAsync(xi, h->xiout, sizeof(double) * h->N * h->n, cudaMemcpyDeviceToHost,
+                             h->st));
+  const int64_t nh = std::min<int64_t>(c.ell, c.hist_cap);
+  if (history && nh > 0)
+    CUDA_TRY(cudaMemcpyAsync(history, h->hist, sizeof(double) * 8 * nh, cudaMemcpyDeviceToHost,
+                             h->st));
+  CUDA_TRY(cudaStreamSynchronize(h->st));
+  const double ell = (double)c.ell;
+  double ft = 1.0 / std::pow(ell, 3.0);
+  ft = std::min(ft, h->cfg.inner_tol_floor);
+  ft = std::min(ft, h->cfg.final_resolve_tol);
+  std::memset(res, 0, sizeof(*res));
+  res->iters = c.ell;
+  res->reason = c.reason;
+  res->restarts = c.restarts;
+  res->saturated = c.saturated;
+  res->sigma_iters = h->sigma_iters;
+  res->sigma_converged = h->sigma_conv;
+  res->g_final = k2[4];
+  res->delta_estimate = std::max(0.0, c.g_star_upper - (k2[4] - 2.0 * ft * c.K));
+  res->sigma_C = h->sigma_C;
+  res->L_g = h->L;
+  res->B_theta = c.B_theta;
+  res->wall_seconds =
+      std::chrono::duration<double>(std::chrono::steady_clock::now() - h->t_begin).count();
+  res->sigma_seconds = h->sigma_seconds;
+  res->loop_seconds = h->loop_seconds;
+  res->last_gap_norm = c.gap_norm;
+  res->last_infeas_norm = c.infeas_norm;
+  if (k2[7] != 0.0) return fail(h, CR_ENONFINITE, "papg: non-finite primal");
+  return CR_OK;
+}
+
+cr_status cr_papg_solve(cr_handle* h, const cr_papg_config* cfg, const double* theta0,
+                        cr_papg_result* res, double* y, double* xi, cr_snapshot* history) {
+  cr_status s = cr_papg_begin(h, cfg, theta0);
+  if (s != CR_OK) return s;
+  int64_t done = 0;
+  int32_t stopped = 0;
+  while (!stopped) {
+    s = cr_papg_iterate(h, INT64_MAX / 4, &done, &stopped);
+    if (s != CR_OK) return s;
+  }
+  return cr_papg_finish(h, res, y, xi, history);
+}
+
+cr_status cr_get_theta(cr_handle* h, double* out) {
+  if (!h || !out) return CR_EINVAL;
+  if (!h->begun) return fail(h, CR_ESTATE, "no dual state");
+  CUDA_TRY(cudaSetDevice(h->device));
+  cr_status s = sync_ctrl(h);
+  if (s != CR_OK) return s;
+  const int cur = h->ctrl_h->cur;
+  const double sc = h->ctrl_h->s_cur;
+  const int64_t rowlen = h->N - 1;
+  const int64_t rows_per = std::max<int64_t>(1, h->stage_elems / rowlen);
+  for (int64_t ra = 0; ra < h->R; ra += rows_per) {
+    const int64_t rb = std::min(h->R, ra + rows_per);
+    CUDA_TRY(launch_theta_out(h->stage, h->V[cur], sc, h->N, h->ld, h->r0, ra, rb, h->st));
+    CUDA_TRY(cudaMemcpyAsync(out + ra * rowlen, h->stage, sizeof(double) * (rb - ra) * rowlen,
+                             cudaMemcpyDeviceToHost, h->st));
+    CUDA_TRY(cudaStreamSynchronize(h->st));
+  }
+  CUDA_TRY(launch_scale_copy(h->stage, h->vpos[cur], sc, h->N, h->st));
+  CUDA_TRY(cudaMemcpyAsync(out + h->R * rowlen, h->stage, sizeof(double) * h->N,
+                           cudaMemcpyDeviceToHost, h->st));
+  CUDA_TRY(cudaStreamSynchronize(h->st));
+  return CR_OK;
+}
+
+cr_status cr_get_rows(cr_handle* h, double* out) {
+  if (!h || !out) return CR_EINVAL;
+  if (!h->begun) return fail(h, CR_ESTATE, "no dual state");
+  CUDA_TRY(cudaSetDevice(h->device));
+  const int64_t rowlen = h->N - 1;
+  const int64_t rows_per = std::max<int64_t>(1, h->stage_elems / rowlen);
+  for (int64_t ra = 0; ra < h->R; ra += rows_per) {
+    const int64_t rb = std::min(h->R, ra + rows_per);
+    CUDA_TRY(launch_rows_out(h->stage, h->rowrec, h->colrec, h->N, (int)h->n, h->r0, ra, rb, h->st));
+    CUDA_TRY(cudaMemcpyAsync(out + ra * rowlen, h->stage, sizeof(double) * (rb - ra) * rowlen,
+                             cudaMemcpyDeviceToHost, h->st));
+    CUDA_TRY(cudaStreamSynchronize(h->st));
+  }
+  std::vector<double> rec((size_t)h->N * h->RP);
+  CUDA_TRY(cudaMemcpy(rec.data(), h->rowrec, sizeof(double) * rec.size(), cudaMemcpyDeviceToHost));
+  for (int64_t l = 0; l < h->N; ++l) out[h->R * rowlen + l] = rec[(size_t)l * h->RP];  // apply_C :152
+  return CR_OK;
+}
+
+cr_status cr_last_timing(const cr_handle* h, double* seconds, int64_t* launches,
+                         double* sweep_seconds) {
+  if (!h) return CR_EINVAL;
+  if (seconds) *seconds = h->last_seconds;
+  if (launches) *launches = h->last_launches;
+  if (sweep_seconds) *sweep_seconds = h->last_sweep_seconds;
+  return CR_OK;
+}
+
+cr_status cr_time_sweep(cr_handle* h, int32_t k, double* avg_seconds) {
+  if (!h || k < 1 || !avg_seconds) return CR_EINVAL;
+  if (!h->begun) return fail(h, CR_ESTATE, "no dual state");
+  CUDA_TRY(cudaSetDevice(h->device));
+  SweepArgs sa = sweep_args(h, kModePapg, false);
+  sa.stopped = nullptr;
+  CUDA_TRY(cudaEventRecord(h->ev_start, h->st));
+  for (int i = 0; i < k; ++i) CUDA_TRY((cudaError_t)launch_sweep(h->kp, sa, (int)h->n, h->st));
+  CUDA_TRY(cudaEventRecord(h->ev_end, h->st));
+  CUDA_TRY(cudaEventSynchronize(h->ev_end));
+  float ms = 0;
+  CUDA_TRY(cudaEventElapsedTime(&ms, h->ev_start, h->ev_end));
+  *avg_seconds = ms * 1e-3 / k;
+  return CR_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,87 @@
+// device.cuh -- device-side data layout and launch interfaces of the
+// singleton-block P-APG pair sweep (arXiv 1407.7220 reference:
+// proj/core/src/papg.cpp:136-283, operators.cpp:128-180).
+//
+// HBM layout (one shard = global rows [r0, r0+R) of the N x N pair matrix):
+//   V[2]      : R x ld fp64, row-major, ld = N rounded up to the strip width.
+//               Unscaled projected multipliers v (theta1 = s * v, appendix A.3
+//               of SURVEY.md). Diagonal and pad columns are held at exactly 0.
+//   vpos[2]   : N fp64, the y >= 0 multipliers (replicated on every shard).
+//   xbuf      : [rowsum N | colagg N x (n+1) | sweep scalars 4] fp64 -- the
+//               aggregates of the newest V (linear, so aggregates of theta2
+//               are the same combination of xbuf and aggsave). xbuf is the
+//               NCCL allreduce payload of sharded runs.
+//   aggsave   : the same aggregates for the previous V.
+//   rowrec    : N x RP  (y_l, x_l[0..n-1], pad)   RP = round_up(n+1, 2)
+//   colrec    : N x RP  (c_l, xi_l[0..n-1], pad)  c_l = y_l - xi_l . x_l
+#pragma once
+#include <cstdint>
+
+namespace crb {
+
+constexpr int kMaxN = 24;    // templated register path covers n = 1..kMaxN
+constexpr int kScal = 4;     // sweep scalars: S_vv, S_vr, S_tr, S_nn
+constexpr int kK2Scal = 8;   // primal scalars, see primal_kernel
+
+// Device-resident solver state: papg.cpp:148-175 locals plus the deferred
+// ball scale (theta1 = s_cur * V[cur]).
+struct DevCtrl {
+  long long ell;        // completed iterations
+  long long max_iters;
+  long long hist_cap;
+  int cur;              // slot holding V_k
+  int stopped;
+  int reason;           // 0 thresholds, 1 iter budget, 2 time budget, 3 error
+  int restarts;
+  int max_restarts;
+  int adaptive;
+  int use_momentum;
+  int record_history;
+  int saturated;
+  int halt;             // stopped || ell >= pause_at: kernels become no-ops
+  long long pause_at;   // host-set iteration limit of the current iterate call
+  // coefficients of theta2 = th1 + beta (th1 - th1p), th1 = s_cur V[cur],
+  // th1p = s_prev V[1-cur]; read by the primal and sweep kernels
+  double s_cur, s_prev, beta;
+  double t;
+  double B_theta;
+  double g_star_upper;
+  double invL;
+  double gamma;
+  double gap_tol, infeas_tol, inner_tol_floor, max_seconds;
+  double gap_div, infeas_div, K;
+  unsigned long long t_start_ns;
+  // metrics of the last completed iteration (papg.cpp:191-208)
+  double gap_raw, gap_norm, infeas_raw, infeas_norm, g_value, fw, theta1_norm;
+  double objective, reg_objective;
+};
+
+struct SweepArgs {
+  double* V0;             // V[0]; V[cur] is read, V[1-cur] is read (theta1_prev)
+  double* V1;             // and then overwritten by v_{k+1}
+  const int* cur;         // device slot index (DevCtrl::cur)
+  const double* rowrec;   // N x RP
+  const double* colrec;   // N x RP
+  double* colpart;        // [P][ld][n+1]
+  double* rowpart;        // [S][R]
+  double* scalpart;       // [S*P][kScal]
+  const double* coef;     // {s_cur, s_prev, beta} (DevCtrl fields or constants)
+  const int* stopped;     // nullptr: always run
+  double invL;            // 1 / L_g (0 turns the step into a pure copy + aggregate)
+  long long N, R, r0, ld;
+  int S, P;               // strips, row chunks per strip
+};
+
+enum SweepMode { kModePapg = 0, kModePower = 1 };
+
+// returns the kernel attribute table entry for (n, mode); host side helpers
+struct SweepKernelInfo {
+  const void* fn;
+  int C;                  // columns per lane
+  int warps_per_block;
+  int max_blocks_per_sm;
+};
+SweepKernelInfo sweep_kernel_info(int n, int mode);
+int launch_sweep(const SweepKernelInfo& info, const SweepArgs& a, int n, void* stream);
+
+}  // namespace crb

@@ -1,0 +1,529 @@
+// kernels.cu -- the O(N n) kernels around the pair sweep:
+//   K2 primal closed form   (apply_C_T aggregation + block centres,
+//                            operators.cpp:155-180, alcc.cpp:233-235, :254-256)
+//   K3 fixed-order reduce   (deterministic second stage of the sweep partials)
+//   Kc control              (papg.cpp:187-262 scalar logic, one thread)
+//   K4 power-method helpers (operators.cpp:302-339 on op_C)
+//   K5 layout conversion    (canonical DualPoint order, indexing.hpp:30-37)
+#include <cuda_runtime.h>
+#include <math.h>
+
+#include "device.cuh"
+#include "kernels.cuh"
+
+namespace crb {
+
+namespace {
+
+constexpr int kBlock = 256;
+
+// deterministic block reduction of W values per thread (fixed tree)
+template <int W>
+__device__ void block_reduce_store(double (&v)[W], double* out /* W values */) {
+  __shared__ double sh[W][kBlock];
+#pragma unroll
+  for (int w = 0; w < W; ++w) sh[w][threadIdx.x] = v[w];
+  __syncthreads();
+  for (int s = kBlock / 2; s > 0; s >>= 1) {
+    if ((int)threadIdx.x < s) {
+#pragma unroll
+      for (int w = 0; w < W; ++w) sh[w][threadIdx.x] += sh[w][threadIdx.x + s];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int w = 0; w < W; ++w) out[w] = sh[w][0];
+  }
+}
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// theta2 (or theta1) combination of the two unscaled buffers
+__device__ __forceinline__ double combine(double zc, double zp, double s_c, double s_p,
+                                          double beta) {
+  const double th1 = s_c * zc;
+  const double th1p = s_p * zp;
+  return fma(beta, th1 - th1p, th1);
+}
+
+// K2. mode 0: iteration (primal at theta2, pos-row step, records);
+//     mode 1: final (primal at theta1 = s_cur V[cur], outputs y/xi, no writes
+//     to the dual state).
+__global__ void __launch_bounds__(kBlock) primal_kernel(const PrimalArgs a) {
+  if (a.stopped != nullptr && *a.stopped) return;
+  const long long N = a.N;
+  const int n = a.n;
+  const int RP = (n + 2) & ~1;
+  const double s_c = a.coef[0];
+  const double s_p = a.mode == 0 ? a.coef[1] : 0.0;
+  const double beta = a.mode == 0 ? a.coef[2] : 0.0;
+  const double* rowsum_c = a.aggc;
+  const double* colagg_c = a.aggc + N;
+  double* rowsum_p = a.aggp;
+  double* colagg_p = a.aggp + N;
+  const int cur = *a.cur;
+  const double* vposc = cur ? a.vpos1 : a.vpos0;
+  double* vposp = cur ? a.vpos0 : a.vpos1;
+  double acc[kK2Scal];
+#pragma unroll
+  for (int w = 0; w < kK2Scal; ++w) acc[w] = 0.0;
+
+  for (long long l = (long long)blockIdx.x * kBlock + threadIdx.x; l < N;
+       l += (long long)gridDim.x * kBlock) {
+    const double* x = a.X + l * n;
+    const double rsc = rowsum_c[l];
+    const double csc = colagg_c[l * (n + 1)];
+    const double rs = combine(rsc, rowsum_p[l], s_c, s_p, beta);
+    const double cs = combine(csc, colagg_p[l * (n + 1)], s_c, s_p, beta);
+    const double th2pos = combine(vposc[l], a.mode == 0 ? vposp[l] : 0.0, s_c, s_p, beta);
+    if (a.mode == 0) {  // aggregates of V[cur] become those of V[prev] next iteration
+      rowsum_p[l] = rsc;
+      colagg_p[l * (n + 1)] = csc;
+    }
+    const double qy = th2pos + rs - cs;  // operators.cpp:161-172
+    const double ybar = a.ybar[l];
+    const double y = ybar + qy;           // alcc.cpp:234
+    double cx = 0.0, xx = 0.0, qx = 0.0;
+    double* crec = a.colrec + l * RP;
+    for (int j = 0; j < n; ++j) {
+      const double vxc = colagg_c[l * (n + 1) + 1 + j];
+      const double vx = combine(vxc, a.mode == 0 ? colagg_p[l * (n + 1) + 1 + j] : 0.0, s_c, s_p,
+                                beta);
+      if (a.mode == 0) colagg_p[l * (n + 1) + 1 + j] = vxc;
+      const double qxi = cs * x[j] - vx;   // operators.cpp:173-175 summed over l1
+      const double xi = qxi / a.gamma;     // alcc.cpp:235
+      cx = fma(xi, x[j], cx);
+      xx = fma(xi, xi, xx);
+      qx = fma(qxi, xi, qx);
+      if (a.mode == 0) crec[1 + j] = xi;
+      else a.xiout[l * n + j] = xi;
+    }
+    const double dy = y - ybar;
+    if (a.mode == 0) {
+      crec[0] = y - cx;
+      a.rowrec[l * RP] = y;
+      // y >= 0 rows of C: theta1_pos = max(theta2_pos - y / L, 0) (papg.cpp:188-189)
+      const double vnew = fmax(fma(-y, a.invL, th2pos), 0.0);
+      vposp[l] = vnew;
+      acc[0] = fma(vnew, vnew, acc[0]);
+      acc[1] = fma(vnew, y, acc[1]);
+      acc[2] = fma(th2pos, y, acc[2]);
+    } else {
+      a.yout[l] = y;
+    }
+    const double m = fmin(y, 0.0);
+    acc[3] = fma(m, m, acc[3]);
+    // block objective at the closed-form minimiser (alcc.cpp:254-256)
+    acc[4] += 0.5 * (dy * dy) + 0.5 * a.gamma * xx - qy * y - qx;
+    acc[5] = fma(dy, dy, acc[5]);
+    acc[6] += xx;
+    acc[7] += isfinite(y) && isfinite(cx) ? 0.0 : 1.0;
+  }
+  block_reduce_store<kK2Scal>(acc, a.k2part + (long long)blockIdx.x * kK2Scal);
+}
+
+// K3: fixed-order reduction of the sweep partials
+__global__ void __launch_bounds__(kBlock) reduce_kernel(const ReduceArgs a) {
+  const long long N = a.N;
+  const int n1 = a.n1;
+  const long long ncol = N * n1;
+  if (a.stopped != nullptr && *a.stopped) {
+    // halted: keep the (already reduced) payload on rank 0, zero it elsewhere,
+    // so a trailing in-place allreduce leaves it unchanged on every rank
+    if (a.rank != 0) {
+      const long long total = N + ncol + kScal;
+      for (long long i = (long long)blockIdx.x * kBlock + threadIdx.x; i < total;
+           i += (long long)gridDim.x * kBlock)
+        a.agg_out[i] = 0.0;
+    }
+    return;
+  }
+  const long long nb_col = (ncol + kBlock - 1) / kBlock;
+  const long long nb_row = (N + kBlock - 1) / kBlock;
+  const long long b = blockIdx.x;
+  if (b < nb_col) {
+    const long long i = b * kBlock + threadIdx.x;
+    if (i < ncol) {
+      const long long stride = a.ld * n1;
+      double s = 0.0;
+      for (int p = 0; p < a.P; ++p) s += a.colpart[p * stride + i];
+      a.agg_out[N + i] = s;
+    }
+  } else if (b < nb_col + nb_row) {
+    const long long r = (b - nb_col) * kBlock + threadIdx.x;
+    if (r < N) {
+      double s = 0.0;
+      const long long lr = r - a.r0;
+      if (lr >= 0 && lr < a.R)
+        for (int st = 0; st < a.S; ++st) s += a.rowpart[st * a.R + lr];
+      a.agg_out[r] = s;
+    }
+  } else {
+    double v[kScal + kK2Scal];
+#pragma unroll
+    for (int w = 0; w < kScal + kK2Scal; ++w) v[w] = 0.0;
+    for (long long i = threadIdx.x; i < a.nw; i += kBlock) {
+#pragma unroll
+      for (int w = 0; w < kScal; ++w) v[w] += a.scalpart[i * kScal + w];
+    }
+    for (long long i = threadIdx.x; i < a.nk2; i += kBlock) {
+#pragma unroll
+      for (int w = 0; w < kK2Scal; ++w) v[kScal + w] += a.k2part[i * kK2Scal + w];
+    }
+    __shared__ double out[kScal + kK2Scal];
+    block_reduce_store<kScal + kK2Scal>(v, out);
+    __syncthreads();
+    if (threadIdx.x < kScal) a.agg_out[N + ncol + threadIdx.x] = out[threadIdx.x];
+    else if (threadIdx.x < kScal + kK2Scal && a.k2sum != nullptr)
+      a.k2sum[threadIdx.x - kScal] = out[threadIdx.x];
+  }
+}
+
+__device__ __forceinline__ double momentum_next(double t) {  // engines.hpp:11-13
+  return 0.5 * (1.0 + sqrt(1.0 + 4.0 * t * t));
+}
+
+// Kc: papg.cpp:187-262 on the reduced scalars. One thread.
+__device__ void control_step(DevCtrl* c, const double* scal, const double* k2, double* hist) {
+  const long long ell = c->ell + 1;
+  const double S_vv = scal[0] + k2[0];
+  const double S_vr = scal[1] + k2[1];
+  const double S_tr = scal[2] + k2[2];
+  const double S_nn_cross = scal[3];
+  const double S_nn_all = scal[3] + k2[3];
+  const double g_value = k2[4];
+  const double B = c->B_theta;
+
+  // projection scale (projections.hpp:10-12)
+  const double norm = sqrt(S_vv);
+  const double s_new = norm > B ? B / norm : 1.0;
+  // linearisation bound (papg.cpp:191-199)
+  const double cross_infeas = sqrt(S_nn_cross);
+  const double fw = B * sqrt(S_nn_all) + S_tr;
+  const double inv3 = 1.0 / ((double)ell * (double)ell * (double)ell);
+  const double inner_tol = fmin(c->inner_tol_floor, inv3);
+  const double cushion = 2.0 * inner_tol * c->K;
+  c->g_star_upper = fmin(c->g_star_upper, g_value + fw + cushion);
+  // gap / infeasibility (papg.cpp:201-208)
+  const double gap_raw = c->use_momentum ? s_new * S_vr : S_tr;
+  const double infeas_raw = cross_infeas;
+  const double gap_norm = gap_raw / c->gap_div;
+  const double infeas_norm = infeas_raw / c->infeas_div;
+  const double wall = (double)(globaltimer() - c->t_start_ns) * 1e-9;
+  c->gap_raw = gap_raw;
+  c->gap_norm = gap_norm;
+  c->infeas_raw = infeas_raw;
+  c->infeas_norm = infeas_norm;
+  c->g_value = g_value;
+  c->fw = fw;
+  c->objective = 0.5 * k2[5];
+  c->reg_objective = 0.5 * k2[5] + 0.5 * c->gamma * k2[6];
+  if (c->record_history && hist != nullptr && ell <= c->hist_cap) {  // papg.cpp:210-222
+    double* h = hist + (ell - 1) * 8;
+    h[0] = (double)ell;
+    h[1] = c->objective;
+    h[2] = c->reg_objective;
+    h[3] = infeas_raw;
+    h[4] = infeas_norm;
+    h[5] = gap_raw;
+    h[6] = gap_norm;
+    h[7] = wall;
+  }
+  c->ell = ell;
+  // theta1 = s_new * V[new]; the new buffer becomes "cur"
+  c->s_prev = c->s_cur;
+  c->s_cur = s_new;
+  c->cur = 1 - c->cur;
+  c->theta1_norm = s_new * norm;
+
+  if (!isfinite(S_tr) || !isfinite(S_vv) || k2[7] != 0.0) {  // papg.cpp:184-185
+    c->reason = 3;
+    c->stopped = 1;
+    return;
+  }
+  bool stop = false;  // papg.cpp:225-236
+  if (fabs(gap_norm) <= c->gap_tol && infeas_norm <= c->infeas_tol) {
+    c->reason = 0;
+    stop = true;
+  } else if (ell >= c->max_iters) {
+    c->reason = 1;
+    stop = true;
+  } else if (wall > c->max_seconds) {
+    c->reason = 2;
+    stop = true;
+  }
+  if (stop) {  // papg.cpp:238-254
+    const bool saturated = c->theta1_norm > 0.99 * B;
+    if (saturated && c->adaptive && c->reason == 0 && c->restarts < c->max_restarts) {
+      c->B_theta = B * 2.0;
+      c->restarts += 1;
+      c->t = 1.0;
+      c->beta = 0.0;  // theta2 = theta1
+      c->g_star_upper = INFINITY;
+      return;
+    }
+    c->saturated = saturated ? 1 : 0;
+    c->stopped = 1;
+    return;
+  }
+  if (c->use_momentum) {  // papg.cpp:256-262
+    const double t_next = momentum_next(c->t);
+    c->beta = (c->t - 1.0) / t_next;
+    c->t = t_next;
+  } else {
+    c->beta = 0.0;
+  }
+}
+
+__global__ void control_kernel(DevCtrl* c, const double* scal /* kScal, allreduced */,
+                               const double* k2 /* kK2Scal, replicated */, double* hist) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  if (c->halt) return;
+  control_step(c, scal, k2, hist);
+  c->halt = (c->stopped || c->ell >= c->pause_at) ? 1 : 0;
+}
+
+__global__ void begin_kernel(DevCtrl* c) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) c->t_start_ns = globaltimer();
+}
+
+__global__ void stamp_kernel(unsigned long long* out) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) *out = globaltimer();
+}
+
+// K4a: v = u / norm_u (operators.cpp:327) and the records of eta = v
+__global__ void __launch_bounds__(kBlock) power_prep_kernel(const PowerArgs a) {
+  const long long N = a.N;
+  const int n = a.n;
+  const int RP = (n + 2) & ~1;
+  double acc[1] = {0.0};
+  for (long long l = (long long)blockIdx.x * kBlock + threadIdx.x; l < N;
+       l += (long long)gridDim.x * kBlock) {
+    const double vy = a.u[l] / a.norm_u;
+    a.v[l] = vy;
+    double cx = 0.0;
+    const double* x = a.X + l * n;
+    double* crec = a.colrec + l * RP;
+    for (int j = 0; j < n; ++j) {
+      const double vxi = a.u[N + l * n + j] / a.norm_u;
+      a.v[N + l * n + j] = vxi;
+      cx = fma(vxi, x[j], cx);
+      crec[1 + j] = vxi;
+    }
+    crec[0] = vy - cx;
+    a.rowrec[l * RP] = vy;
+    acc[0] = fma(vy, vy, acc[0]);  // pos rows of C v = v_y
+  }
+  block_reduce_store<1>(acc, a.part + (long long)blockIdx.x * 2);
+}
+
+// K4b: u = C^T w from the reduced aggregates (operators.cpp:161-178)
+__global__ void __launch_bounds__(kBlock) power_post_kernel(const PowerArgs a) {
+  const long long N = a.N;
+  const int n = a.n;
+  double acc[1] = {0.0};
+  for (long long l = (long long)blockIdx.x * kBlock + threadIdx.x; l < N;
+       l += (long long)gridDim.x * kBlock) {
+    const double rs = a.agg[l];
+    const double cs = a.agg[N + l * (n + 1)];
+    const double uy = a.v[l] + rs - cs;
+    a.u[l] = uy;
+    double s = uy * uy;
+    const double* x = a.X + l * n;
+    for (int j = 0; j < n; ++j) {
+      const double ux = cs * x[j] - a.agg[N + l * (n + 1) + 1 + j];
+      a.u[N + l * n + j] = ux;
+      s = fma(ux, ux, s);
+    }
+    acc[0] += s;
+  }
+  block_reduce_store<1>(acc, a.part + (long long)blockIdx.x * 2 + 1);
+}
+
+// fixed-order sum of `count` records of width `width` -> out[width]
+__global__ void __launch_bounds__(kBlock) reduce_records_kernel(const double* part,
+                                                                long long count, int width,
+                                                                double* out) {
+  double v[kK2Scal];
+#pragma unroll
+  for (int w = 0; w < kK2Scal; ++w) v[w] = 0.0;
+  for (long long i = threadIdx.x; i < count; i += kBlock)
+#pragma unroll
+    for (int w = 0; w < kK2Scal; ++w)
+      if (w < width) v[w] += part[i * width + w];
+  __shared__ double o[kK2Scal];
+  block_reduce_store<kK2Scal>(v, o);
+  __syncthreads();
+  if ((int)threadIdx.x < width && threadIdx.x < kK2Scal) out[threadIdx.x] = o[threadIdx.x];
+}
+
+// K5: canonical theta rows [a, b) (local) <-> device V
+__global__ void theta_in_kernel(const double* stage, double* V, long long N, long long ld,
+                                long long r0, long long ra, long long rb) {
+  const long long total = (rb - ra) * ld;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long lr = i / ld, c = i % ld;
+    const long long r = ra + lr, gr = r0 + r;
+    double v = 0.0;
+    if (c < N && c != gr) {
+      const double t = stage[lr * (N - 1) + c - (c > gr ? 1 : 0)];
+      v = t > 0.0 ? t : 0.0;  // projections.hpp:10 (scale applied separately)
+    }
+    V[r * ld + c] = v;
+  }
+}
+
+__global__ void theta_out_kernel(double* stage, const double* V, double s, long long N,
+                                 long long ld, long long r0, long long ra, long long rb) {
+  const long long total = (rb - ra) * (N - 1);
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long lr = i / (N - 1), k = i % (N - 1);
+    const long long gr = r0 + ra + lr;
+    const long long c = k + (k >= gr ? 1 : 0);
+    stage[i] = s * V[(ra + lr) * ld + c];
+  }
+}
+
+__global__ void rows_out_kernel(double* stage, const double* rowrec, const double* colrec,
+                                long long N, int n, long long r0, long long ra, long long rb) {
+  const int RP = (n + 2) & ~1;
+  const long long total = (rb - ra) * (N - 1);
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long lr = i / (N - 1), k = i % (N - 1);
+    const long long gr = r0 + ra + lr;
+    const long long c = k + (k >= gr ? 1 : 0);
+    const double* xr = rowrec + gr * RP;
+    const double* cr = colrec + c * RP;
+    double row = xr[0] - cr[0];
+    for (int j = 0; j < n; ++j) row = fma(-xr[1 + j], cr[1 + j], row);
+    stage[i] = row;
+  }
+}
+
+__global__ void scale_copy_kernel(double* dst, const double* src, double s, long long len) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < len;
+       i += (long long)gridDim.x * blockDim.x)
+    dst[i] = s * src[i];
+}
+
+__global__ void pos_in_kernel(double* vpos, const double* src, long long N) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < N;
+       i += (long long)gridDim.x * blockDim.x)
+    vpos[i] = src[i] > 0.0 ? src[i] : 0.0;
+}
+
+// warm start: s = min(1, B / |max(theta0, 0)|) (papg.cpp:163), coefficient
+// state for iteration 1 (theta1 = theta1_prev = theta2, t = 1)
+__global__ void warm_ctrl_kernel(DevCtrl* c, const double* scal_cross, double pos_sq) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const double ss = scal_cross[0] + pos_sq;
+  const double norm = sqrt(ss);
+  const double s = norm > c->B_theta ? c->B_theta / norm : 1.0;
+  c->s_cur = s;
+  c->s_prev = s;
+  c->beta = 0.0;
+}
+
+unsigned grid_for(long long n, int block, int cap) {
+  long long g = (n + block - 1) / block;
+  if (g < 1) g = 1;
+  if (g > cap) g = cap;
+  return (unsigned)g;
+}
+
+}  // namespace
+
+int primal_blocks(long long N) { return (int)grid_for(N, kBlock, 1184); }
+
+cudaError_t launch_primal(const PrimalArgs& a, cudaStream_t s) {
+  primal_kernel<<<primal_blocks(a.N), kBlock, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_reduce(const ReduceArgs& a, cudaStream_t s) {
+  const long long nb = (a.N * a.n1 + kBlock - 1) / kBlock + (a.N + kBlock - 1) / kBlock + 1;
+  reduce_kernel<<<(unsigned)nb, kBlock, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_control(DevCtrl* c, const double* scal, const double* k2, double* hist,
+                           cudaStream_t s) {
+  control_kernel<<<1, 32, 0, s>>>(c, scal, k2, hist);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_begin(DevCtrl* c, cudaStream_t s) {
+  begin_kernel<<<1, 32, 0, s>>>(c);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_stamp(unsigned long long* out, cudaStream_t s) {
+  stamp_kernel<<<1, 32, 0, s>>>(out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_power_prep(const PowerArgs& a, cudaStream_t s) {
+  power_prep_kernel<<<primal_blocks(a.N), kBlock, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_power_post(const PowerArgs& a, cudaStream_t s) {
+  power_post_kernel<<<primal_blocks(a.N), kBlock, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_reduce_records(const double* part, long long count, int width, double* out,
+                                  cudaStream_t s) {
+  reduce_records_kernel<<<1, kBlock, 0, s>>>(part, count, width, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_theta_in(const double* stage, double* V, long long N, long long ld,
+                            long long r0, long long ra, long long rb, cudaStream_t s) {
+  theta_in_kernel<<<grid_for((rb - ra) * ld, 256, 4096), 256, 0, s>>>(stage, V, N, ld, r0, ra,
+                                                                       rb);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_theta_out(double* stage, const double* V, double sc, long long N,
+                             long long ld, long long r0, long long ra, long long rb,
+                             cudaStream_t s) {
+  theta_out_kernel<<<grid_for((rb - ra) * (N - 1), 256, 4096), 256, 0, s>>>(stage, V, sc, N, ld,
+                                                                            r0, ra, rb);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_rows_out(double* stage, const double* rowrec, const double* colrec,
+                            long long N, int n, long long r0, long long ra, long long rb,
+                            cudaStream_t s) {
+  rows_out_kernel<<<grid_for((rb - ra) * (N - 1), 256, 4096), 256, 0, s>>>(stage, rowrec, colrec,
+                                                                           N, n, r0, ra, rb);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_scale_copy(double* dst, const double* src, double sc, long long len,
+                              cudaStream_t s) {
+  scale_copy_kernel<<<grid_for(len, 256, 1024), 256, 0, s>>>(dst, src, sc, len);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pos_in(double* vpos, const double* src, long long N, cudaStream_t s) {
+  pos_in_kernel<<<grid_for(N, 256, 1024), 256, 0, s>>>(vpos, src, N);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_warm_ctrl(DevCtrl* c, const double* scal_cross, double pos_sq,
+                             cudaStream_t s) {
+  warm_ctrl_kernel<<<1, 32, 0, s>>>(c, scal_cross, pos_sq);
+  return cudaGetLastError();
+}
+
+}  // namespace crb

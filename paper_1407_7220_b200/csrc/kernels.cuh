@@ -1,0 +1,81 @@
+// kernels.cuh -- argument blocks and launchers of the O(N n) kernels (kernels.cu)
+#pragma once
+#include <cuda_runtime.h>
+
+#include "device.cuh"
+
+namespace crb {
+
+struct PrimalArgs {
+  const double* X;       // N x n
+  const double* ybar;    // N (shifted observations)
+  double* rowrec;        // N x RP (y written, x static)
+  double* colrec;        // N x RP
+  const double* aggc;    // aggregates of V[cur] (xbuf)
+  double* aggp;          // aggregates of V[prev] (aggsave); mode 0 refreshes it with aggc
+  double* vpos0;         // vpos[cur] is read, vpos[1-cur] is read and then
+  double* vpos1;         // overwritten with the new pos multipliers
+  const int* cur;
+  double* k2part;        // [blocks][kK2Scal]
+  const double* coef;    // {s_cur, s_prev, beta}
+  const int* stopped;
+  double* yout;          // mode 1
+  double* xiout;         // mode 1
+  double invL, gamma;
+  long long N;
+  int n;
+  int mode;              // 0 iteration, 1 final
+};
+
+struct ReduceArgs {
+  const double* colpart;  // [P][ld][n1]
+  const double* rowpart;  // [S][R]
+  const double* scalpart; // [nw][kScal]
+  const double* k2part;   // [nk2][kK2Scal]
+  double* agg_out;        // [N | N n1 | kScal]
+  double* k2sum;          // kK2Scal (may be null)
+  const int* stopped;     // halted: rank 0 keeps agg_out, other ranks zero it
+  int rank;
+  long long N, ld, R, r0, nw, nk2;
+  int n1, P, S;
+};
+
+struct PowerArgs {
+  const double* X;
+  double* u;       // N (n+1): [u_y | u_xi]
+  double* v;       // N (n+1)
+  double norm_u;
+  double* rowrec;
+  double* colrec;
+  const double* agg;
+  double* part;    // [blocks][2]
+  long long N;
+  int n;
+};
+
+int primal_blocks(long long N);
+cudaError_t launch_primal(const PrimalArgs& a, cudaStream_t s);
+cudaError_t launch_reduce(const ReduceArgs& a, cudaStream_t s);
+cudaError_t launch_control(DevCtrl* c, const double* scal, const double* k2, double* hist,
+                           cudaStream_t s);
+cudaError_t launch_begin(DevCtrl* c, cudaStream_t s);
+cudaError_t launch_stamp(unsigned long long* out, cudaStream_t s);
+cudaError_t launch_power_prep(const PowerArgs& a, cudaStream_t s);
+cudaError_t launch_power_post(const PowerArgs& a, cudaStream_t s);
+cudaError_t launch_reduce_records(const double* part, long long count, int width, double* out,
+                                  cudaStream_t s);
+cudaError_t launch_theta_in(const double* stage, double* V, long long N, long long ld,
+                            long long r0, long long ra, long long rb, cudaStream_t s);
+cudaError_t launch_theta_out(double* stage, const double* V, double sc, long long N,
+                             long long ld, long long r0, long long ra, long long rb,
+                             cudaStream_t s);
+cudaError_t launch_rows_out(double* stage, const double* rowrec, const double* colrec,
+                            long long N, int n, long long r0, long long ra, long long rb,
+                            cudaStream_t s);
+cudaError_t launch_scale_copy(double* dst, const double* src, double sc, long long len,
+                              cudaStream_t s);
+cudaError_t launch_pos_in(double* vpos, const double* src, long long N, cudaStream_t s);
+cudaError_t launch_warm_ctrl(DevCtrl* c, const double* scal_cross, double pos_sq,
+                             cudaStream_t s);
+
+}  // namespace crb
