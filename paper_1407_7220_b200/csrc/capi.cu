@@ -318,7 +318,7 @@ cr_status cr_create(const double* Xh, const double* ybar_shifted, int64_t N, int
   CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
   const long long resident = (long long)sms * h->kp.max_blocks_per_sm * h->kp.warps_per_block;
   long long P = resident / h->S;
-  const long long pmax = (h->R + 31) / 32;
+  const long long pmax = (h->R + 15) / 16;
   if (P > pmax) P = pmax;
   if (P < 1) P = 1;
   h->P = (int)P;
