@@ -13,6 +13,7 @@
 #include <climits>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -31,8 +32,14 @@ struct cr_handle {
   int RP = 0;
   double gamma = 1e-3;
   SweepKernelInfo kp{}, kw{};
-  int S = 0, P = 0;
+  int S = 0;            // column strips
+  int T = 0;            // sweep CTA column tiles = row-sum slices
+  int variant = 0;      // kSweepDfma / kSweepMma
+  int G = 0;            // sweep CTAs (one persistent wave)
+  int maxspan = 0;      // tiles one CTA's unit range can touch
+  long long U = 0;      // (tile, row) units per CTA
   int k2_blocks = 0;
+  unsigned int* counter = nullptr;
   // device buffers
   double *X = nullptr, *ybar = nullptr, *rowrec = nullptr, *colrec = nullptr;
   double *V[2] = {nullptr, nullptr}, *vpos[2] = {nullptr, nullptr};
@@ -116,11 +123,14 @@ SweepArgs sweep_args(cr_handle* h, int mode, bool agg_only) {
   a.r0 = h->r0;
   a.ld = h->ld;
   a.S = h->S;
-  a.P = h->P;
+  a.T = h->T;
+  a.G = h->G;
+  a.U = h->U;
+  a.maxspan = h->maxspan;
   return a;
 }
 
-ReduceArgs reduce_args(cr_handle* h, bool with_k2, const int* stopped) {
+ReduceArgs reduce_args(cr_handle* h, bool with_k2, const int* stopped, bool fuse_control) {
   ReduceArgs a{};
   a.colpart = h->colpart;
   a.rowpart = h->rowpart;
@@ -130,15 +140,21 @@ ReduceArgs reduce_args(cr_handle* h, bool with_k2, const int* stopped) {
   a.k2sum = with_k2 ? h->k2sum : nullptr;
   a.stopped = stopped;
   a.rank = h->rank;
+  a.ctrl = fuse_control ? h->ctrl_d : nullptr;
+  a.hist = h->hist;
+  a.counter = h->counter;
   a.N = h->N;
   a.ld = h->ld;
   a.R = h->R;
   a.r0 = h->r0;
-  a.nw = (long long)h->S * h->P;
+  a.nw = (long long)h->G * h->kp.warps_per_block;
   a.nk2 = with_k2 ? h->k2_blocks : 0;
   a.n1 = (int)h->n + 1;
-  a.P = h->P;
-  a.S = h->S;
+  a.S = h->T;
+  a.TC = h->kp.tile_cols;
+  a.G = h->G;
+  a.U = h->U;
+  a.maxspan = h->maxspan;
   return a;
 }
 
@@ -175,20 +191,23 @@ cr_status enqueue_iteration(cr_handle* h, int phase, cudaEvent_t ev_a, cudaEvent
     CUDA_TRY(launch_primal(pa, h->st));
     const SweepArgs sa = sweep_args(h, kModePapg, false);
     if (ev_a) CUDA_TRY(cudaEventRecord(ev_a, h->st));
-    CUDA_TRY((cudaError_t)launch_sweep(h->kp, sa, (int)h->n, h->st));
+    CUDA_TRY((cudaError_t)launch_sweep(h->kp, sa, h->st));
     if (ev_b) CUDA_TRY(cudaEventRecord(ev_b, h->st));
-    const ReduceArgs ra = reduce_args(h, true, &h->ctrl_d->halt);
+    // single GPU, full iteration: the reduce kernel's last block runs the control step
+    const bool fuse = phase == 0 && h->comm == nullptr;
+    const ReduceArgs ra = reduce_args(h, true, &h->ctrl_d->halt, fuse);
     CUDA_TRY(launch_reduce(ra, h->st));
     if (use_nccl && h->comm)
       NCCL_TRY(ncclAllReduce(h->xbuf, h->xbuf, (size_t)payload_len(h), ncclDouble, ncclSum,
                              h->comm, h->st));
+    if (fuse) return CR_OK;
   }
   if (phase != 1)
     CUDA_TRY(launch_control(h->ctrl_d, h->xbuf + h->N * (h->n + 2), h->k2sum, h->hist, h->st));
   return CR_OK;
 }
 
-int launches_per_iteration(const cr_handle* h) { return 4 + (h->comm ? 1 : 0); }
+int launches_per_iteration(const cr_handle* h) { return h->comm ? 5 : 3; }
 
 cr_status build_graph(cr_handle* h) {
   if (h->gexec) {
@@ -234,8 +253,8 @@ cr_status power_step(cr_handle* h, double norm_u, double* lambda, double* nu) {
   CUDA_TRY(launch_power_prep(pa, h->st));
   SweepArgs sa = sweep_args(h, kModePower, false);
   sa.cur = h->izero;
-  CUDA_TRY((cudaError_t)launch_sweep(h->kw, sa, (int)h->n, h->st));
-  const ReduceArgs ra = reduce_args(h, false, nullptr);
+  CUDA_TRY((cudaError_t)launch_sweep(h->kw, sa, h->st));
+  const ReduceArgs ra = reduce_args(h, false, nullptr, false);
   CUDA_TRY(launch_reduce(ra, h->st));
   if (h->comm)
     NCCL_TRY(ncclAllReduce(h->xbuf, h->xbuf, (size_t)payload_len(h), ncclDouble, ncclSum, h->comm,
@@ -302,26 +321,42 @@ cr_status cr_create(const double* Xh, const double* ybar_shifted, int64_t N, int
   h->r0 = row_begin;
   h->r1 = row_end;
   h->R = row_end - row_begin;
-  h->RP = (int)((n + 2) & ~1LL);
+  h->RP = rec_pitch((int)n);
   h->gamma = gamma;
   h->cfg.gamma = gamma;
   CUDA_TRY(cudaSetDevice(device));
   CUDA_TRY(cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking));
-  h->kp = sweep_kernel_info((int)n, kModePapg);
-  h->kw = sweep_kernel_info((int)n, kModePower);
+  // sweep variant (measured on B200, profiles/): CUDA-core DFMA for small n,
+  // DMMA tensor cores once the two rank-n contractions dominate the issue slots.
+  // CRB_SWEEP=dfma|mma overrides.
+  const char* var = std::getenv("CRB_SWEEP");
+  h->variant = n <= 6 ? kSweepDfma : kSweepMma;
+  if (var && std::strcmp(var, "dfma") == 0) h->variant = kSweepDfma;
+  if (var && std::strcmp(var, "mma") == 0) h->variant = kSweepMma;
+  if (h->variant == kSweepMma) {
+    h->kp = sweep_mma_info((int)n, kModePapg);
+    h->kw = sweep_mma_info((int)n, kModePower);
+  } else {
+    h->kp = sweep_dfma_info((int)n, kModePapg);
+    h->kw = sweep_dfma_info((int)n, kModePower);
+  }
   if (!h->kp.fn || !h->kw.fn || h->kp.max_blocks_per_sm < 1)
     return fail(h, CR_EINVAL, "no sweep kernel for this n");
-  const int W = 32 * h->kp.C;
+  const int W = h->kp.strip_cols;
   h->S = (int)((N + W - 1) / W);
   h->ld = (int64_t)h->S * W;
   int sms = 148;
   CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
-  const long long resident = (long long)sms * h->kp.max_blocks_per_sm * h->kp.warps_per_block;
-  long long P = resident / h->S;
-  const long long pmax = (h->R + 15) / 16;
-  if (P > pmax) P = pmax;
-  if (P < 1) P = 1;
-  h->P = (int)P;
+  // one persistent wave; each CTA gets an equal contiguous share of the
+  // T x R (tile, row) units, at least 64 rows
+  h->T = (h->S + h->kp.warps_per_block - 1) / h->kp.warps_per_block;
+  const long long units = (long long)h->T * h->R;
+  long long G = (long long)sms * h->kp.max_blocks_per_sm;
+  G = std::min<long long>(G, (units + 63) / 64);
+  if (G < 1) G = 1;
+  h->U = (units + G - 1) / G;
+  h->G = (int)((units + h->U - 1) / h->U);
+  h->maxspan = (int)((h->U - 1) / h->R + 2);
   h->k2_blocks = primal_blocks(N);
 
   const size_t RP = (size_t)h->RP;
@@ -339,9 +374,9 @@ cr_status cr_create(const double* Xh, const double* ybar_shifted, int64_t N, int
   ALLOC(h->vpos[1], N);
   ALLOC(h->xbuf, payload_len(h));
   ALLOC(h->aggsave, payload_len(h));
-  ALLOC(h->colpart, (size_t)h->P * h->ld * (n + 1));
-  ALLOC(h->rowpart, (size_t)h->S * h->R);
-  ALLOC(h->scalpart, (size_t)h->S * h->P * kScal);
+  ALLOC(h->colpart, (size_t)h->G * h->maxspan * h->kp.tile_cols * (n + 1));
+  ALLOC(h->rowpart, (size_t)h->T * h->R);
+  ALLOC(h->scalpart, (size_t)h->G * h->kp.warps_per_block * kScal);
   ALLOC(h->k2part, (size_t)h->k2_blocks * kK2Scal);
   ALLOC(h->k2sum, kK2Scal);
   ALLOC(h->yout, N);
@@ -352,6 +387,7 @@ cr_status cr_create(const double* Xh, const double* ybar_shifted, int64_t N, int
   ALLOC(h->pw_sum, 2);
   ALLOC(h->consts, 4);
   ALLOC(h->izero, 1);
+  ALLOC(h->counter, 1);
   ALLOC(h->ctrl_d, 1);
 #undef ALLOC
   if (e != cudaSuccess) {
@@ -378,8 +414,9 @@ cr_status cr_create(const double* Xh, const double* ybar_shifted, int64_t N, int
                            h->st));
   std::vector<double> rec((size_t)N * RP, 0.0);
   for (int64_t l = 0; l < N; ++l) {
-    rec[l * RP] = ybar_shifted[l];
-    for (int64_t j = 0; j < n; ++j) rec[l * RP + 1 + j] = Xh[l * n + j];
+    for (int64_t j = 0; j < n; ++j) rec[l * RP + j] = Xh[l * n + j];  // (x, 1, y)
+    rec[l * RP + n] = 1.0;
+    rec[l * RP + n + 1] = ybar_shifted[l];
   }
   CUDA_TRY(cudaMemcpyAsync(h->rowrec, rec.data(), sizeof(double) * rec.size(),
                            cudaMemcpyHostToDevice, h->st));
@@ -387,6 +424,7 @@ cr_status cr_create(const double* Xh, const double* ybar_shifted, int64_t N, int
   const double consts[4] = {1.0, 1.0, 0.0, 0.0};
   CUDA_TRY(cudaMemcpyAsync(h->consts, consts, sizeof(consts), cudaMemcpyHostToDevice, h->st));
   CUDA_TRY(cudaMemsetAsync(h->izero, 0, sizeof(int), h->st));
+  CUDA_TRY(cudaMemsetAsync(h->counter, 0, sizeof(unsigned int), h->st));
   CUDA_TRY(cudaMemsetAsync(h->ctrl_d, 0, sizeof(DevCtrl), h->st));
   CUDA_TRY(cudaStreamSynchronize(h->st));
   return CR_OK;
@@ -405,6 +443,7 @@ void cr_destroy(cr_handle* h) {
   for (double* b : bufs)
     if (b) cudaFree(b);
   if (h->izero) cudaFree(h->izero);
+  if (h->counter) cudaFree(h->counter);
   if (h->ctrl_d) cudaFree(h->ctrl_d);
   if (h->ctrl_h) cudaFreeHost(h->ctrl_h);
   if (h->ctrl_poll) cudaFreeHost(h->ctrl_poll);
@@ -596,8 +635,8 @@ cr_status cr_papg_begin(cr_handle* h, const cr_papg_config* cfg, const double* t
     CUDA_TRY(launch_pos_in(h->vpos[0], h->stage, N, h->st));
     // aggregates and |.|^2 of max(theta0, 0): a sweep with 1/L = 0 is a copy
     const SweepArgs sa = sweep_args(h, kModePapg, true);
-    CUDA_TRY((cudaError_t)launch_sweep(h->kp, sa, (int)h->n, h->st));
-    const ReduceArgs ra = reduce_args(h, false, nullptr);
+    CUDA_TRY((cudaError_t)launch_sweep(h->kp, sa, h->st));
+    const ReduceArgs ra = reduce_args(h, false, nullptr, false);
     CUDA_TRY(launch_reduce(ra, h->st));
     if (h->comm)
       NCCL_TRY(ncclAllReduce(h->xbuf, h->xbuf, (size_t)payload_len(h), ncclDouble, ncclSum,
@@ -849,7 +888,8 @@ cr_status cr_get_rows(cr_handle* h, double* out) {
   }
   std::vector<double> rec((size_t)h->N * h->RP);
   CUDA_TRY(cudaMemcpy(rec.data(), h->rowrec, sizeof(double) * rec.size(), cudaMemcpyDeviceToHost));
-  for (int64_t l = 0; l < h->N; ++l) out[h->R * rowlen + l] = rec[(size_t)l * h->RP];  // apply_C :152
+  for (int64_t l = 0; l < h->N; ++l)  // apply_C :152, y of eta
+    out[h->R * rowlen + l] = rec[(size_t)l * h->RP + h->n + 1];
   return CR_OK;
 }
 
@@ -869,7 +909,7 @@ cr_status cr_time_sweep(cr_handle* h, int32_t k, double* avg_seconds) {
   SweepArgs sa = sweep_args(h, kModePapg, false);
   sa.stopped = nullptr;
   CUDA_TRY(cudaEventRecord(h->ev_start, h->st));
-  for (int i = 0; i < k; ++i) CUDA_TRY((cudaError_t)launch_sweep(h->kp, sa, (int)h->n, h->st));
+  for (int i = 0; i < k; ++i) CUDA_TRY((cudaError_t)launch_sweep(h->kp, sa, h->st));
   CUDA_TRY(cudaEventRecord(h->ev_end, h->st));
   CUDA_TRY(cudaEventSynchronize(h->ev_end));
   float ms = 0;

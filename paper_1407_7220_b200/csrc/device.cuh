@@ -12,14 +12,20 @@
 //               are the same combination of xbuf and aggsave). xbuf is the
 //               NCCL allreduce payload of sharded runs.
 //   aggsave   : the same aggregates for the previous V.
-//   rowrec    : N x RP  (y_l, x_l[0..n-1], pad)   RP = round_up(n+1, 2)
-//   colrec    : N x RP  (c_l, xi_l[0..n-1], pad)  c_l = y_l - xi_l . x_l
+//   rowrec    : N x RQ  (x_l[0..n-1], 1, y_l, 0...)
+//   colrec    : N x RQ  (xi_l[0..n-1], c_l, -1, 0...)   c_l = y_l - xi_l . x_l
+//               so that -(C eta)_{l1 l2} = colrec[l2] . rowrec[l1] (the MMA
+//               residual), RQ = max(round_up(n+2, 4), round_up(n+1, 8)).
 #pragma once
 #include <cstdint>
 
 namespace crb {
 
 constexpr int kMaxN = 24;    // templated register path covers n = 1..kMaxN
+
+__host__ __device__ constexpr int rec_pitch(int n) {
+  return ((n + 5) & ~3) > ((n + 8) & ~7) ? ((n + 5) & ~3) : ((n + 8) & ~7);
+}
 constexpr int kScal = 4;     // sweep scalars: S_vv, S_vr, S_tr, S_nn
 constexpr int kK2Scal = 8;   // primal scalars, see primal_kernel
 
@@ -62,14 +68,18 @@ struct SweepArgs {
   const int* cur;         // device slot index (DevCtrl::cur)
   const double* rowrec;   // N x RP
   const double* colrec;   // N x RP
-  double* colpart;        // [P][ld][n+1]
-  double* rowpart;        // [S][R]
-  double* scalpart;       // [S*P][kScal]
+  double* colpart;        // [G*maxspan][TC][n+1]: one slot per (CTA, segment)
+  double* rowpart;        // [T][R]: one row-sum slice per column tile
+  double* scalpart;       // [G*CW][kScal]
   const double* coef;     // {s_cur, s_prev, beta} (DevCtrl fields or constants)
   const int* stopped;     // nullptr: always run
   double invL;            // 1 / L_g (0 turns the step into a pure copy + aggregate)
   long long N, R, r0, ld;
-  int S, P;               // strips, row chunks per strip
+  long long U;            // rows of the (tile, row) unit space per CTA
+  int S;                  // column strips (32*C columns each)
+  int T;                  // column tiles (CW strips each)
+  int G;                  // CTAs (persistent, one wave)
+  int maxspan;            // max segments (tiles) one CTA can touch
 };
 
 enum SweepMode { kModePapg = 0, kModePower = 1 };
@@ -77,11 +87,16 @@ enum SweepMode { kModePapg = 0, kModePower = 1 };
 // returns the kernel attribute table entry for (n, mode); host side helpers
 struct SweepKernelInfo {
   const void* fn;
-  int C;                  // columns per lane
-  int warps_per_block;
+  int strip_cols;         // columns per consumer warp (W)
+  int warps_per_block;    // consumer warps
   int max_blocks_per_sm;
+  int tile_cols;          // TC = warps_per_block * strip_cols
+  int threads;
+  int smem_bytes;
 };
-SweepKernelInfo sweep_kernel_info(int n, int mode);
-int launch_sweep(const SweepKernelInfo& info, const SweepArgs& a, int n, void* stream);
+enum SweepVariant { kSweepDfma = 0, kSweepMma = 1 };
+SweepKernelInfo sweep_dfma_info(int n, int mode);  // sweep.cu (CUDA-core DFMA)
+SweepKernelInfo sweep_mma_info(int n, int mode);   // sweep_mma.cu (DMMA tensor cores)
+int launch_sweep(const SweepKernelInfo& info, const SweepArgs& a, void* stream);
 
 }  // namespace crb

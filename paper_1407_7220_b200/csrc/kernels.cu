@@ -16,15 +16,16 @@ namespace crb {
 namespace {
 
 constexpr int kBlock = 256;
+constexpr int kPBlock = 64;  // O(N) kernels: small blocks so N = 1e4 still spans every SM
 
 // deterministic block reduction of W values per thread (fixed tree)
-template <int W>
+template <int W, int BS = kBlock>
 __device__ void block_reduce_store(double (&v)[W], double* out /* W values */) {
-  __shared__ double sh[W][kBlock];
+  __shared__ double sh[W][BS];
 #pragma unroll
   for (int w = 0; w < W; ++w) sh[w][threadIdx.x] = v[w];
   __syncthreads();
-  for (int s = kBlock / 2; s > 0; s >>= 1) {
+  for (int s = BS / 2; s > 0; s >>= 1) {
     if ((int)threadIdx.x < s) {
 #pragma unroll
       for (int w = 0; w < W; ++w) sh[w][threadIdx.x] += sh[w][threadIdx.x + s];
@@ -53,12 +54,13 @@ __device__ __forceinline__ double combine(double zc, double zp, double s_c, doub
 
 // K2. mode 0: iteration (primal at theta2, pos-row step, records);
 //     mode 1: final (primal at theta1 = s_cur V[cur], outputs y/xi, no writes
-//     to the dual state).
-__global__ void __launch_bounds__(kBlock) primal_kernel(const PrimalArgs a) {
+//     to the dual state). NN = n is a template parameter so every load of a
+//     point is issued up front.
+template <int NN>
+__global__ void __launch_bounds__(kPBlock) primal_kernel(const PrimalArgs a) {
   if (a.stopped != nullptr && *a.stopped) return;
+  constexpr int RP = rec_pitch(NN);
   const long long N = a.N;
-  const int n = a.n;
-  const int RP = (n + 2) & ~1;
   const double s_c = a.coef[0];
   const double s_p = a.mode == 0 ? a.coef[1] : 0.0;
   const double beta = a.mode == 0 ? a.coef[2] : 0.0;
@@ -73,40 +75,53 @@ __global__ void __launch_bounds__(kBlock) primal_kernel(const PrimalArgs a) {
 #pragma unroll
   for (int w = 0; w < kK2Scal; ++w) acc[w] = 0.0;
 
-  for (long long l = (long long)blockIdx.x * kBlock + threadIdx.x; l < N;
-       l += (long long)gridDim.x * kBlock) {
-    const double* x = a.X + l * n;
+  for (long long l = (long long)blockIdx.x * kPBlock + threadIdx.x; l < N;
+       l += (long long)gridDim.x * kPBlock) {
+    const double* x = a.X + l * NN;
+    const double* ac = colagg_c + l * (NN + 1);
+    double* ap = colagg_p + l * (NN + 1);
+    double agc[NN + 1], agp[NN + 1], xv[NN];
+#pragma unroll
+    for (int j = 0; j <= NN; ++j) {
+      agc[j] = ac[j];
+      agp[j] = a.mode == 0 ? ap[j] : 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < NN; ++j) xv[j] = x[j];
     const double rsc = rowsum_c[l];
-    const double csc = colagg_c[l * (n + 1)];
-    const double rs = combine(rsc, rowsum_p[l], s_c, s_p, beta);
-    const double cs = combine(csc, colagg_p[l * (n + 1)], s_c, s_p, beta);
-    const double th2pos = combine(vposc[l], a.mode == 0 ? vposp[l] : 0.0, s_c, s_p, beta);
+    const double rsp = a.mode == 0 ? rowsum_p[l] : 0.0;
+    const double vpc = vposc[l];
+    const double vpp = a.mode == 0 ? vposp[l] : 0.0;
+    const double ybar = a.ybar[l];
     if (a.mode == 0) {  // aggregates of V[cur] become those of V[prev] next iteration
       rowsum_p[l] = rsc;
-      colagg_p[l * (n + 1)] = csc;
+#pragma unroll
+      for (int j = 0; j <= NN; ++j) ap[j] = agc[j];
     }
+    const double rs = combine(rsc, rsp, s_c, s_p, beta);
+    const double cs = combine(agc[0], agp[0], s_c, s_p, beta);
+    const double th2pos = combine(vpc, vpp, s_c, s_p, beta);
     const double qy = th2pos + rs - cs;  // operators.cpp:161-172
-    const double ybar = a.ybar[l];
-    const double y = ybar + qy;           // alcc.cpp:234
+    const double y = ybar + qy;          // alcc.cpp:234
     double cx = 0.0, xx = 0.0, qx = 0.0;
-    double* crec = a.colrec + l * RP;
-    for (int j = 0; j < n; ++j) {
-      const double vxc = colagg_c[l * (n + 1) + 1 + j];
-      const double vx = combine(vxc, a.mode == 0 ? colagg_p[l * (n + 1) + 1 + j] : 0.0, s_c, s_p,
-                                beta);
-      if (a.mode == 0) colagg_p[l * (n + 1) + 1 + j] = vxc;
-      const double qxi = cs * x[j] - vx;   // operators.cpp:173-175 summed over l1
-      const double xi = qxi / a.gamma;     // alcc.cpp:235
-      cx = fma(xi, x[j], cx);
-      xx = fma(xi, xi, xx);
-      qx = fma(qxi, xi, qx);
-      if (a.mode == 0) crec[1 + j] = xi;
-      else a.xiout[l * n + j] = xi;
+    double xi[NN];
+#pragma unroll
+    for (int j = 0; j < NN; ++j) {
+      const double vx = combine(agc[1 + j], agp[1 + j], s_c, s_p, beta);
+      const double qxi = cs * xv[j] - vx;  // operators.cpp:173-175 summed over l1
+      xi[j] = qxi / a.gamma;               // alcc.cpp:235
+      cx = fma(xi[j], xv[j], cx);
+      xx = fma(xi[j], xi[j], xx);
+      qx = fma(qxi, xi[j], qx);
     }
     const double dy = y - ybar;
     if (a.mode == 0) {
-      crec[0] = y - cx;
-      a.rowrec[l * RP] = y;
+      double* crec = a.colrec + l * RP;  // (xi, c, -1)
+#pragma unroll
+      for (int j = 0; j < NN; ++j) crec[j] = xi[j];
+      crec[NN] = y - cx;
+      crec[NN + 1] = -1.0;
+      a.rowrec[l * RP + NN + 1] = y;     // (x, 1, y)
       // y >= 0 rows of C: theta1_pos = max(theta2_pos - y / L, 0) (papg.cpp:188-189)
       const double vnew = fmax(fma(-y, a.invL, th2pos), 0.0);
       vposp[l] = vnew;
@@ -115,6 +130,8 @@ __global__ void __launch_bounds__(kBlock) primal_kernel(const PrimalArgs a) {
       acc[2] = fma(th2pos, y, acc[2]);
     } else {
       a.yout[l] = y;
+#pragma unroll
+      for (int j = 0; j < NN; ++j) a.xiout[l * NN + j] = xi[j];
     }
     const double m = fmin(y, 0.0);
     acc[3] = fma(m, m, acc[3]);
@@ -124,64 +141,7 @@ __global__ void __launch_bounds__(kBlock) primal_kernel(const PrimalArgs a) {
     acc[6] += xx;
     acc[7] += isfinite(y) && isfinite(cx) ? 0.0 : 1.0;
   }
-  block_reduce_store<kK2Scal>(acc, a.k2part + (long long)blockIdx.x * kK2Scal);
-}
-
-// K3: fixed-order reduction of the sweep partials
-__global__ void __launch_bounds__(kBlock) reduce_kernel(const ReduceArgs a) {
-  const long long N = a.N;
-  const int n1 = a.n1;
-  const long long ncol = N * n1;
-  if (a.stopped != nullptr && *a.stopped) {
-    // halted: keep the (already reduced) payload on rank 0, zero it elsewhere,
-    // so a trailing in-place allreduce leaves it unchanged on every rank
-    if (a.rank != 0) {
-      const long long total = N + ncol + kScal;
-      for (long long i = (long long)blockIdx.x * kBlock + threadIdx.x; i < total;
-           i += (long long)gridDim.x * kBlock)
-        a.agg_out[i] = 0.0;
-    }
-    return;
-  }
-  const long long nb_col = (ncol + kBlock - 1) / kBlock;
-  const long long nb_row = (N + kBlock - 1) / kBlock;
-  const long long b = blockIdx.x;
-  if (b < nb_col) {
-    const long long i = b * kBlock + threadIdx.x;
-    if (i < ncol) {
-      const long long stride = a.ld * n1;
-      double s = 0.0;
-      for (int p = 0; p < a.P; ++p) s += a.colpart[p * stride + i];
-      a.agg_out[N + i] = s;
-    }
-  } else if (b < nb_col + nb_row) {
-    const long long r = (b - nb_col) * kBlock + threadIdx.x;
-    if (r < N) {
-      double s = 0.0;
-      const long long lr = r - a.r0;
-      if (lr >= 0 && lr < a.R)
-        for (int st = 0; st < a.S; ++st) s += a.rowpart[st * a.R + lr];
-      a.agg_out[r] = s;
-    }
-  } else {
-    double v[kScal + kK2Scal];
-#pragma unroll
-    for (int w = 0; w < kScal + kK2Scal; ++w) v[w] = 0.0;
-    for (long long i = threadIdx.x; i < a.nw; i += kBlock) {
-#pragma unroll
-      for (int w = 0; w < kScal; ++w) v[w] += a.scalpart[i * kScal + w];
-    }
-    for (long long i = threadIdx.x; i < a.nk2; i += kBlock) {
-#pragma unroll
-      for (int w = 0; w < kK2Scal; ++w) v[kScal + w] += a.k2part[i * kK2Scal + w];
-    }
-    __shared__ double out[kScal + kK2Scal];
-    block_reduce_store<kScal + kK2Scal>(v, out);
-    __syncthreads();
-    if (threadIdx.x < kScal) a.agg_out[N + ncol + threadIdx.x] = out[threadIdx.x];
-    else if (threadIdx.x < kScal + kK2Scal && a.k2sum != nullptr)
-      a.k2sum[threadIdx.x - kScal] = out[threadIdx.x];
-  }
+  block_reduce_store<kK2Scal, kPBlock>(acc, a.k2part + (long long)blockIdx.x * kK2Scal);
 }
 
 __device__ __forceinline__ double momentum_next(double t) {  // engines.hpp:11-13
@@ -288,6 +248,92 @@ __global__ void control_kernel(DevCtrl* c, const double* scal /* kScal, allreduc
   c->halt = (c->stopped || c->ell >= c->pause_at) ? 1 : 0;
 }
 
+// K3: fixed-order reduction of the sweep partials. On a single GPU the last
+// block to finish also runs the control step (no separate launch); sharded
+// runs call control_kernel after the allreduce instead.
+__global__ void __launch_bounds__(kBlock) reduce_kernel(const ReduceArgs a) {
+  const long long N = a.N;
+  const int n1 = a.n1;
+  const long long ncol = N * n1;
+  if (a.stopped != nullptr && *a.stopped) {
+    // halted: keep the (already reduced) payload on rank 0, zero it elsewhere,
+    // so a trailing in-place allreduce leaves it unchanged on every rank
+    if (a.rank != 0) {
+      const long long total = N + ncol + kScal;
+      for (long long i = (long long)blockIdx.x * kBlock + threadIdx.x; i < total;
+           i += (long long)gridDim.x * kBlock)
+        a.agg_out[i] = 0.0;
+    }
+    return;
+  }
+  const long long nb_col = (ncol + kBlock - 1) / kBlock;
+  const long long nb_row = (N + kBlock - 1) / kBlock;
+  const long long b = blockIdx.x;
+  if (b < nb_col) {
+    const long long i = b * kBlock + threadIdx.x;
+    if (i < ncol) {
+      // column c of tile t was swept by CTAs g_lo..g_hi (contiguous unit ranges)
+      const long long c = i / n1, j = i % n1;
+      const long long t = c / a.TC, off = c % a.TC;
+      const long long g_lo = (t * a.R) / a.U;
+      long long g_hi = ((t + 1) * a.R - 1) / a.U;
+      if (g_hi > a.G - 1) g_hi = a.G - 1;
+      double s = 0.0;
+      for (long long g = g_lo; g <= g_hi; ++g) {
+        const long long slot = g * a.maxspan + (t - (g * a.U) / a.R);
+        s += a.colpart[(slot * a.TC + off) * n1 + j];
+      }
+      a.agg_out[N + i] = s;
+    }
+  } else if (b < nb_col + nb_row) {
+    const long long r = (b - nb_col) * kBlock + threadIdx.x;
+    if (r < N) {
+      double s = 0.0;
+      const long long lr = r - a.r0;
+      if (lr >= 0 && lr < a.R)
+        for (int st = 0; st < a.S; ++st) s += a.rowpart[st * a.R + lr];
+      a.agg_out[r] = s;
+    }
+  } else {
+    double v[kScal + kK2Scal];
+#pragma unroll
+    for (int w = 0; w < kScal + kK2Scal; ++w) v[w] = 0.0;
+    for (long long i = threadIdx.x; i < a.nw; i += kBlock) {
+#pragma unroll
+      for (int w = 0; w < kScal; ++w) v[w] += a.scalpart[i * kScal + w];
+    }
+    for (long long i = threadIdx.x; i < a.nk2; i += kBlock) {
+#pragma unroll
+      for (int w = 0; w < kK2Scal; ++w) v[kScal + w] += a.k2part[i * kK2Scal + w];
+    }
+    __shared__ double out[kScal + kK2Scal];
+    block_reduce_store<kScal + kK2Scal>(v, out);
+    __syncthreads();
+    if (threadIdx.x < kScal) a.agg_out[N + ncol + threadIdx.x] = out[threadIdx.x];
+    else if (threadIdx.x < kScal + kK2Scal && a.k2sum != nullptr)
+      a.k2sum[threadIdx.x - kScal] = out[threadIdx.x];
+  }
+  if (a.ctrl == nullptr) return;
+  // last block done -> control step (all blocks read the halt flag above
+  // before any block can get here, so the update cannot race with them)
+  __shared__ bool last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(a.counter, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    __threadfence();
+    *a.counter = 0u;
+    DevCtrl* c = a.ctrl;
+    if (!c->halt) {
+      control_step(c, a.agg_out + N + ncol, a.k2sum, a.hist);
+      c->halt = (c->stopped || c->ell >= c->pause_at) ? 1 : 0;
+    }
+  }
+}
+
 __global__ void begin_kernel(DevCtrl* c) {
   if (threadIdx.x == 0 && blockIdx.x == 0) c->t_start_ns = globaltimer();
 }
@@ -297,13 +343,13 @@ __global__ void stamp_kernel(unsigned long long* out) {
 }
 
 // K4a: v = u / norm_u (operators.cpp:327) and the records of eta = v
-__global__ void __launch_bounds__(kBlock) power_prep_kernel(const PowerArgs a) {
+__global__ void __launch_bounds__(kPBlock) power_prep_kernel(const PowerArgs a) {
   const long long N = a.N;
   const int n = a.n;
-  const int RP = (n + 2) & ~1;
+  const int RP = rec_pitch(n);
   double acc[1] = {0.0};
-  for (long long l = (long long)blockIdx.x * kBlock + threadIdx.x; l < N;
-       l += (long long)gridDim.x * kBlock) {
+  for (long long l = (long long)blockIdx.x * kPBlock + threadIdx.x; l < N;
+       l += (long long)gridDim.x * kPBlock) {
     const double vy = a.u[l] / a.norm_u;
     a.v[l] = vy;
     double cx = 0.0;
@@ -313,22 +359,23 @@ __global__ void __launch_bounds__(kBlock) power_prep_kernel(const PowerArgs a) {
       const double vxi = a.u[N + l * n + j] / a.norm_u;
       a.v[N + l * n + j] = vxi;
       cx = fma(vxi, x[j], cx);
-      crec[1 + j] = vxi;
+      crec[j] = vxi;
     }
-    crec[0] = vy - cx;
-    a.rowrec[l * RP] = vy;
+    crec[n] = vy - cx;
+    crec[n + 1] = -1.0;
+    a.rowrec[l * RP + n + 1] = vy;
     acc[0] = fma(vy, vy, acc[0]);  // pos rows of C v = v_y
   }
-  block_reduce_store<1>(acc, a.part + (long long)blockIdx.x * 2);
+  block_reduce_store<1, kPBlock>(acc, a.part + (long long)blockIdx.x * 2);
 }
 
 // K4b: u = C^T w from the reduced aggregates (operators.cpp:161-178)
-__global__ void __launch_bounds__(kBlock) power_post_kernel(const PowerArgs a) {
+__global__ void __launch_bounds__(kPBlock) power_post_kernel(const PowerArgs a) {
   const long long N = a.N;
   const int n = a.n;
   double acc[1] = {0.0};
-  for (long long l = (long long)blockIdx.x * kBlock + threadIdx.x; l < N;
-       l += (long long)gridDim.x * kBlock) {
+  for (long long l = (long long)blockIdx.x * kPBlock + threadIdx.x; l < N;
+       l += (long long)gridDim.x * kPBlock) {
     const double rs = a.agg[l];
     const double cs = a.agg[N + l * (n + 1)];
     const double uy = a.v[l] + rs - cs;
@@ -342,7 +389,7 @@ __global__ void __launch_bounds__(kBlock) power_post_kernel(const PowerArgs a) {
     }
     acc[0] += s;
   }
-  block_reduce_store<1>(acc, a.part + (long long)blockIdx.x * 2 + 1);
+  block_reduce_store<1, kPBlock>(acc, a.part + (long long)blockIdx.x * 2 + 1);
 }
 
 // fixed-order sum of `count` records of width `width` -> out[width]
@@ -393,7 +440,7 @@ __global__ void theta_out_kernel(double* stage, const double* V, double s, long 
 
 __global__ void rows_out_kernel(double* stage, const double* rowrec, const double* colrec,
                                 long long N, int n, long long r0, long long ra, long long rb) {
-  const int RP = (n + 2) & ~1;
+  const int RP = rec_pitch(n);
   const long long total = (rb - ra) * (N - 1);
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
        i += (long long)gridDim.x * blockDim.x) {
@@ -402,8 +449,8 @@ __global__ void rows_out_kernel(double* stage, const double* rowrec, const doubl
     const long long c = k + (k >= gr ? 1 : 0);
     const double* xr = rowrec + gr * RP;
     const double* cr = colrec + c * RP;
-    double row = xr[0] - cr[0];
-    for (int j = 0; j < n; ++j) row = fma(-xr[1 + j], cr[1 + j], row);
+    double row = xr[n + 1] - cr[n];  // y_l1 - c_l2 - x_l1 . xi_l2
+    for (int j = 0; j < n; ++j) row = fma(-xr[j], cr[j], row);
     stage[i] = row;
   }
 }
@@ -441,10 +488,23 @@ unsigned grid_for(long long n, int block, int cap) {
 
 }  // namespace
 
-int primal_blocks(long long N) { return (int)grid_for(N, kBlock, 1184); }
+int primal_blocks(long long N) { return (int)grid_for(N, kPBlock, 4736); }
 
+template <int NN>
+void launch_primal_n(const PrimalArgs& a, cudaStream_t s) {
+  primal_kernel<NN><<<primal_blocks(a.N), kPBlock, 0, s>>>(a);
+}
+using PrimalLauncher = void (*)(const PrimalArgs&, cudaStream_t);
 cudaError_t launch_primal(const PrimalArgs& a, cudaStream_t s) {
-  primal_kernel<<<primal_blocks(a.N), kBlock, 0, s>>>(a);
+  static constexpr PrimalLauncher tab[kMaxN] = {
+      launch_primal_n<1>,  launch_primal_n<2>,  launch_primal_n<3>,  launch_primal_n<4>,
+      launch_primal_n<5>,  launch_primal_n<6>,  launch_primal_n<7>,  launch_primal_n<8>,
+      launch_primal_n<9>,  launch_primal_n<10>, launch_primal_n<11>, launch_primal_n<12>,
+      launch_primal_n<13>, launch_primal_n<14>, launch_primal_n<15>, launch_primal_n<16>,
+      launch_primal_n<17>, launch_primal_n<18>, launch_primal_n<19>, launch_primal_n<20>,
+      launch_primal_n<21>, launch_primal_n<22>, launch_primal_n<23>, launch_primal_n<24>};
+  if (a.n < 1 || a.n > kMaxN) return cudaErrorInvalidValue;
+  tab[a.n - 1](a, s);
   return cudaGetLastError();
 }
 
@@ -471,12 +531,12 @@ cudaError_t launch_stamp(unsigned long long* out, cudaStream_t s) {
 }
 
 cudaError_t launch_power_prep(const PowerArgs& a, cudaStream_t s) {
-  power_prep_kernel<<<primal_blocks(a.N), kBlock, 0, s>>>(a);
+  power_prep_kernel<<<primal_blocks(a.N), kPBlock, 0, s>>>(a);
   return cudaGetLastError();
 }
 
 cudaError_t launch_power_post(const PowerArgs& a, cudaStream_t s) {
-  power_post_kernel<<<primal_blocks(a.N), kBlock, 0, s>>>(a);
+  power_post_kernel<<<primal_blocks(a.N), kPBlock, 0, s>>>(a);
   return cudaGetLastError();
 }
 

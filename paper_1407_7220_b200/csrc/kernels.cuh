@@ -28,16 +28,19 @@ struct PrimalArgs {
 };
 
 struct ReduceArgs {
-  const double* colpart;  // [P][ld][n1]
-  const double* rowpart;  // [S][R]
+  const double* colpart;  // [G*maxspan][TC][n1] (sweep CTA, segment) slots
+  const double* rowpart;  // [S][R], S = number of row-sum slices (CTA column tiles)
   const double* scalpart; // [nw][kScal]
   const double* k2part;   // [nk2][kK2Scal]
   double* agg_out;        // [N | N n1 | kScal]
   double* k2sum;          // kK2Scal (may be null)
   const int* stopped;     // halted: rank 0 keeps agg_out, other ranks zero it
+  DevCtrl* ctrl;          // non-null: the last block runs the control step
+  double* hist;
+  unsigned int* counter;  // last-block detection (self-resetting)
   int rank;
-  long long N, ld, R, r0, nw, nk2;
-  int n1, P, S;
+  long long N, ld, R, r0, nw, nk2, U;
+  int n1, S, TC, G, maxspan;
 };
 
 struct PowerArgs {

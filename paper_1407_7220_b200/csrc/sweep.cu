@@ -29,6 +29,7 @@
 #include <cstdint>
 
 #include "device.cuh"
+#include "pipeline.cuh"
 
 namespace crb {
 
@@ -44,8 +45,6 @@ __host__ __device__ constexpr int consumer_warps() { return NN <= 10 ? 8 : 4; }
 template <int NN>
 __host__ __device__ constexpr int threads_per_cta() { return (consumer_warps<NN>() + 1) * 32; }
 template <int NN>
-__host__ __device__ constexpr int rec_pitch() { return (NN + 2) & ~1; }
-template <int NN>
 __host__ __device__ constexpr int rows_per_stage() { return cols_per_lane<NN>() == 2 ? 4 : 8; }
 template <int NN>
 __host__ __device__ constexpr int tile_cols() {
@@ -54,12 +53,13 @@ __host__ __device__ constexpr int tile_cols() {
 // doubles per stage: V and V' rows for the tile + row records
 template <int NN>
 __host__ __device__ constexpr int stage_doubles() {
-  return 2 * rows_per_stage<NN>() * tile_cols<NN>() + rows_per_stage<NN>() * rec_pitch<NN>();
+  return 2 * rows_per_stage<NN>() * tile_cols<NN>() + rows_per_stage<NN>() * rec_pitch(NN);
 }
 constexpr int kRsPitch = 17;  // per-warp row-sum transpose: 32 rows x 16 lanes (+1 pad)
 template <int NN>
 __host__ __device__ constexpr int smem_bytes() {
-  return kNS * stage_doubles<NN>() * 8 + consumer_warps<NN>() * 32 * kRsPitch * 8 + 2 * kNS * 8;
+  return kNS * stage_doubles<NN>() * 8 + consumer_warps<NN>() * 32 * kRsPitch * 8 +
+         2 * consumer_warps<NN>() * 32 * 8 + 2 * kNS * 8;
 }
 
 template <int C> struct VecT;
@@ -71,58 +71,6 @@ __device__ __forceinline__ double vget(const double2& v, int k) { return k == 0 
 __device__ __forceinline__ void vset(double& v, int, double x) { v = x; }
 __device__ __forceinline__ void vset(double2& v, int k, double x) {
   if (k == 0) v.x = x; else v.y = x;
-}
-
-__device__ __forceinline__ void st_stream(double* p, double v) {
-  asm volatile("st.global.cs.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
-}
-__device__ __forceinline__ void st_stream(double2* p, double2 v) {
-  asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v.x), "d"(v.y) : "memory");
-}
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-// TMA bulk copy global -> shared, completion counted on an mbarrier
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
-                                         uint64_t* bar, uint64_t policy) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
-      " [%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
-      : "memory");
-}
-__device__ __forceinline__ uint64_t policy_evict_first() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-__device__ __forceinline__ uint64_t policy_evict_last() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-  return p;
 }
 
 // ---- consumer building blocks ---------------------------------------------
@@ -150,33 +98,21 @@ struct StageView {
   double* srs;        // row-sum transpose slot of stage row 0
 };
 
-// max(u, 0) and min(r, 0) on the sign bit: three integer ops, no FSEL chains
-__device__ __forceinline__ double keep_if_nonneg(double u) {
-  const int hi = __double2hiint(u), lo = __double2loint(u);
-  const int m = ~(hi >> 31);
-  return __hiloint2double(hi & m, lo & m);
-}
-__device__ __forceinline__ double keep_if_neg(double r) {
-  const int hi = __double2hiint(r), lo = __double2loint(r);
-  const int m = hi >> 31;
-  return __hiloint2double(hi & m, lo & m);
-}
-
 template <int NN, int MODE, int TR, int TC, bool MASK, bool UNIT>
 __device__ __forceinline__ void run_stage(const StageView& sv, int nr, int lane,
                                           ColState<NN, cols_per_lane<NN>()>& cs, const Coef& cf,
                                           Scal& sc) {
   constexpr int C = cols_per_lane<NN>();
-  constexpr int RP = rec_pitch<NN>();
+  constexpr int RP = rec_pitch(NN);
   using VT = typename VecT<C>::T;
 #pragma unroll
   for (int q = 0; q < TR; ++q) {
     if (q < nr) {
-      const double* xr = sv.rec + q * RP;
+      const double* xr = sv.rec + q * RP;  // (x, 1, y)
       double x[NN];
-      const double y1 = xr[0];
+      const double y1 = xr[NN + 1];
 #pragma unroll
-      for (int j = 0; j < NN; ++j) x[j] = xr[1 + j];
+      for (int j = 0; j < NN; ++j) x[j] = xr[j];
       VT vc, vp, out;
       if (MODE == kModePapg) {
         vc = *reinterpret_cast<const VT*>(sv.vc + q * TC);
@@ -231,15 +167,15 @@ __global__ void __launch_bounds__(threads_per_cta<NN>()) sweep_kernel(const Swee
   constexpr int kCW = consumer_warps<NN>();
   constexpr int C = cols_per_lane<NN>();
   constexpr int W = 32 * C;
-  constexpr int RP = rec_pitch<NN>();
+  constexpr int RP = rec_pitch(NN);
   constexpr int TR = rows_per_stage<NN>();
   constexpr int TC = tile_cols<NN>();
   constexpr int SD = stage_doubles<NN>();
-  using VT = typename VecT<C>::T;
   extern __shared__ __align__(128) double smem[];
   double* stages = smem;
   double* srs_all = smem + kNS * SD;
-  uint64_t* full = reinterpret_cast<uint64_t*>(srs_all + kCW * 32 * kRsPitch);
+  double* rowacc = srs_all + kCW * 32 * kRsPitch;  // [2][kCW][32] CTA row-sum combine
+  uint64_t* full = reinterpret_cast<uint64_t*>(rowacc + 2 * kCW * 32);
   uint64_t* empty = full + kNS;
 
   if (a.stopped != nullptr && *a.stopped) return;
@@ -247,14 +183,15 @@ __global__ void __launch_bounds__(threads_per_cta<NN>()) sweep_kernel(const Swee
   const double* Vc = cur ? a.V1 : a.V0;
   double* Vp = cur ? a.V0 : a.V1;
 
-  const int T = (a.S + kCW - 1) / kCW;  // column tiles
-  const int ct = blockIdx.x % T;
-  const int chunk = blockIdx.x / T;
-  const long long rlo = a.R * chunk / a.P;
-  const long long rhi = a.R * (chunk + 1) / a.P;
-  const int nstage = (int)((rhi - rlo + TR - 1) / TR);
-  const long long c0 = (long long)ct * TC;
-  const int tile_w = (int)min((long long)TC, a.ld - c0);  // columns actually present
+  // Persistent balanced split: the (tile, row) unit space of T * R rows is
+  // cut into G equal contiguous ranges, one per CTA; a range covers one or a
+  // few "segments" (a row range of one column tile).
+  const long long units = (long long)a.T * a.R;
+  const long long u0 = (long long)blockIdx.x * a.U;
+  const long long u1 = min(u0 + a.U, units);
+  if (u0 >= u1) return;
+  const int t_first = (int)(u0 / a.R);
+  const int t_last = (int)((u1 - 1) / a.R);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -271,51 +208,38 @@ __global__ void __launch_bounds__(threads_per_cta<NN>()) sweep_kernel(const Swee
     if (lane == 0) {
       const uint64_t pol_stream = policy_evict_first();
       const uint64_t pol_keep = policy_evict_last();
-      const uint32_t vbytes = (uint32_t)tile_w * 8u;
-      for (int i = 0; i < nstage; ++i) {
-        const int s = i % kNS;
-        if (i >= kNS) mbar_wait(&empty[s], (uint32_t)(((i / kNS) - 1) & 1));
-        const long long r = rlo + (long long)i * TR;
-        const int nr = (int)min((long long)TR, rhi - r);
-        double* st = stages + s * SD;
-        const uint32_t bytes =
-            (MODE == kModePapg ? 2u * nr * vbytes : 0u) + (uint32_t)nr * RP * 8u;
-        mbar_arrive_expect_tx(&full[s], bytes);
-        if (MODE == kModePapg) {
-          for (int q = 0; q < nr; ++q) {
-            const long long off = (r + q) * a.ld + c0;
-            bulk_g2s(st + q * TC, Vc + off, vbytes, &full[s], pol_stream);
-            bulk_g2s(st + (TR + q) * TC, Vp + off, vbytes, &full[s], pol_stream);
+      int i = 0;  // global stage counter
+      for (int t = t_first; t <= t_last; ++t) {
+        const long long rlo = max(u0, (long long)t * a.R) - (long long)t * a.R;
+        const long long rhi = min(u1, (long long)(t + 1) * a.R) - (long long)t * a.R;
+        const long long c0 = (long long)t * TC;
+        const uint32_t vbytes = (uint32_t)min((long long)TC, a.ld - c0) * 8u;
+        for (long long r = rlo; r < rhi; r += TR, ++i) {
+          const int s = i % kNS;
+          if (i >= kNS) mbar_wait(&empty[s], (uint32_t)(((i / kNS) - 1) & 1));
+          const int nr = (int)min((long long)TR, rhi - r);
+          double* st = stages + s * SD;
+          const uint32_t bytes =
+              (MODE == kModePapg ? 2u * nr * vbytes : 0u) + (uint32_t)nr * RP * 8u;
+          mbar_arrive_expect_tx(&full[s], bytes);
+          if (MODE == kModePapg) {
+            for (int q = 0; q < nr; ++q) {
+              const long long off = (r + q) * a.ld + c0;
+              bulk_g2s(st + q * TC, Vc + off, vbytes, &full[s], pol_stream);
+              bulk_g2s(st + (TR + q) * TC, Vp + off, vbytes, &full[s], pol_stream);
+            }
           }
+          bulk_g2s(st + 2 * TR * TC, a.rowrec + (a.r0 + r) * RP, (uint32_t)nr * RP * 8u,
+                   &full[s], pol_keep);
         }
-        bulk_g2s(st + 2 * TR * TC, a.rowrec + (a.r0 + r) * RP, (uint32_t)nr * RP * 8u, &full[s],
-                 pol_keep);
       }
     }
     return;
   }
 
   // ---------------------------------------------------------------- consumers
-  const int strip = ct * kCW + warp;
-  const bool active = strip < a.S;
-  const long long col0 = c0 + warp * W + lane * C;  // first column of this lane
   double* srs = srs_all + warp * 32 * kRsPitch;
-
-  ColState<NN, C> cs;
-#pragma unroll
-  for (int k = 0; k < C; ++k) {
-    const long long col = col0 + k;
-    cs.valid[k] = active && col < a.N;
-    const double* rec = a.colrec + (cs.valid[k] ? col : 0) * RP;
-    cs.cc[k] = cs.valid[k] ? __ldg(rec) : 0.0;
-#pragma unroll
-    for (int j = 0; j < NN; ++j) cs.xi[k][j] = cs.valid[k] ? __ldg(rec + 1 + j) : 0.0;
-#pragma unroll
-    for (int j = 0; j <= NN; ++j) cs.acc[k][j] = 0.0;
-  }
-  // warp-uniform: every column of the strip is a real column
-  const bool strip_full = active && (c0 + (long long)(warp + 1) * W <= a.N);
-  const long long strip_lo = c0 + (long long)warp * W;
+  const int lane_off = warp * W + lane * C;
   Coef cf{1.0, 0.0, 0.0, a.invL};
   if (MODE == kModePapg) {
     cf.s_c = a.coef[0];
@@ -324,54 +248,91 @@ __global__ void __launch_bounds__(threads_per_cta<NN>()) sweep_kernel(const Swee
   }
   const bool unit_scale = (cf.s_c == 1.0) && (cf.s_p == 1.0);
   Scal sc{0.0, 0.0, 0.0, 0.0};
-  int win = 0;               // rows held in the row-sum transpose window
-  long long win_base = rlo;  // local row of window slot 0
-  const int lane_off = warp * W + lane * C;
+  int i = 0;        // global stage counter (matches the producer)
+  int flushes = 0;  // row-sum combine buffer parity
 
-  for (int i = 0; i < nstage; ++i) {
-    const int s = i % kNS;
-    mbar_wait(&full[s], (uint32_t)((i / kNS) & 1));
-    const long long r = rlo + (long long)i * TR;
-    const int nr = (int)min((long long)TR, rhi - r);
-    if (active) {
-      const double* st = stages + s * SD;
-      StageView sv{st + lane_off, st + TR * TC + lane_off, st + 2 * TR * TC,
-                   Vp + r * a.ld + col0, a.ld, col0, a.r0 + r, srs + win * kRsPitch};
-      // the diagonal or a pad column touches this stage: per-pair masks
-      const bool clean =
-          strip_full && (sv.g0 + nr <= strip_lo || sv.g0 >= strip_lo + W);
-      if (clean) {
-        if (unit_scale) run_stage<NN, MODE, TR, TC, false, true>(sv, nr, lane, cs, cf, sc);
-        else run_stage<NN, MODE, TR, TC, false, false>(sv, nr, lane, cs, cf, sc);
-      } else {
-        if (unit_scale) run_stage<NN, MODE, TR, TC, true, true>(sv, nr, lane, cs, cf, sc);
-        else run_stage<NN, MODE, TR, TC, true, false>(sv, nr, lane, cs, cf, sc);
-      }
-      win += nr;
-      if (win == 32 || i == nstage - 1) {  // fixed-order row reduction of the window
-        __syncwarp();
-        if (lane < win) {
-          double t = 0.0;
+  for (int t = t_first; t <= t_last; ++t) {
+    const long long rlo = max(u0, (long long)t * a.R) - (long long)t * a.R;
+    const long long rhi = min(u1, (long long)(t + 1) * a.R) - (long long)t * a.R;
+    const long long c0 = (long long)t * TC;
+    const int strip = t * kCW + warp;
+    const bool active = strip < a.S;
+    const long long col0 = c0 + warp * W + lane * C;  // first column of this lane
+
+    ColState<NN, C> cs;
 #pragma unroll
-          for (int l = 0; l < 16; ++l) t += srs[lane * kRsPitch + l];
-          a.rowpart[(long long)strip * a.R + win_base + lane] = t;
+    for (int k = 0; k < C; ++k) {
+      const long long col = col0 + k;
+      cs.valid[k] = active && col < a.N;
+      const double* rec = a.colrec + (cs.valid[k] ? col : 0) * RP;  // (xi, c, -1)
+      cs.cc[k] = cs.valid[k] ? __ldg(rec + NN) : 0.0;
+#pragma unroll
+      for (int j = 0; j < NN; ++j) cs.xi[k][j] = cs.valid[k] ? __ldg(rec + j) : 0.0;
+#pragma unroll
+      for (int j = 0; j <= NN; ++j) cs.acc[k][j] = 0.0;
+    }
+    // warp-uniform: every column of the strip is a real column
+    const bool strip_full = active && (c0 + (long long)(warp + 1) * W <= a.N);
+    const long long strip_lo = c0 + (long long)warp * W;
+    int win = 0;               // rows held in the row-sum transpose window
+    long long win_base = rlo;  // local row of window slot 0
+
+    for (long long r = rlo; r < rhi; r += TR, ++i) {
+      const int s = i % kNS;
+      mbar_wait(&full[s], (uint32_t)((i / kNS) & 1));
+      const int nr = (int)min((long long)TR, rhi - r);
+      if (active) {
+        const double* st = stages + s * SD;
+        StageView sv{st + lane_off, st + TR * TC + lane_off, st + 2 * TR * TC,
+                     Vp + r * a.ld + col0, a.ld, col0, a.r0 + r, srs + win * kRsPitch};
+        // the diagonal or a pad column touches this stage: per-pair masks
+        const bool clean = strip_full && (sv.g0 + nr <= strip_lo || sv.g0 >= strip_lo + W);
+        if (clean) {
+          if (unit_scale) run_stage<NN, MODE, TR, TC, false, true>(sv, nr, lane, cs, cf, sc);
+          else run_stage<NN, MODE, TR, TC, false, false>(sv, nr, lane, cs, cf, sc);
+        } else {
+          if (unit_scale) run_stage<NN, MODE, TR, TC, true, true>(sv, nr, lane, cs, cf, sc);
+          else run_stage<NN, MODE, TR, TC, true, false>(sv, nr, lane, cs, cf, sc);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+      win += nr;
+      if (win == 32 || r + TR >= rhi) {
+        // per-warp row sums of the window (lane i <-> row i), then a
+        // fixed-order sum over the CTA's warps into the tile's row-sum slice
+        double tsum = 0.0;
+        if (active && lane < win) {
+#pragma unroll
+          for (int l = 0; l < 16; ++l) tsum += srs[lane * kRsPitch + l];
+        }
+        double* ra = rowacc + (flushes & 1) * kCW * 32;
+        ra[warp * 32 + lane] = tsum;
+        asm volatile("bar.sync 1, %0;" ::"r"(kCW * 32) : "memory");
+        if (warp == 0 && lane < win) {
+          double u = 0.0;
+#pragma unroll
+          for (int w = 0; w < kCW; ++w) u += ra[w * 32 + lane];
+          a.rowpart[(long long)t * a.R + win_base + lane] = u;
         }
         __syncwarp();
         win_base += win;
         win = 0;
+        ++flushes;
       }
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
+    // column partials of this segment: slot (CTA, segment index)
+    if (active) {
+      const long long slot = (long long)blockIdx.x * a.maxspan + (t - t_first);
+#pragma unroll
+      for (int k = 0; k < C; ++k) {
+        double* dst = a.colpart + (slot * TC + warp * W + lane * C + k) * (NN + 1);
+#pragma unroll
+        for (int j = 0; j <= NN; ++j) dst[j] = cs.acc[k][j];
+      }
+    }
   }
-  if (!active) return;
 
-#pragma unroll
-  for (int k = 0; k < C; ++k) {
-    double* dst = a.colpart + ((long long)chunk * a.ld + col0 + k) * (NN + 1);
-#pragma unroll
-    for (int j = 0; j <= NN; ++j) dst[j] = cs.acc[k][j];
-  }
   double vv = sc.vv, vr = sc.vr, tr = sc.tr, nn = sc.nn;
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) {  // fixed butterfly: deterministic
@@ -381,7 +342,7 @@ __global__ void __launch_bounds__(threads_per_cta<NN>()) sweep_kernel(const Swee
     nn += __shfl_xor_sync(0xffffffffu, nn, off);
   }
   if (lane == 0) {
-    double* sp = a.scalpart + ((long long)chunk * a.S + strip) * kScal;
+    double* sp = a.scalpart + ((long long)blockIdx.x * kCW + warp) * kScal;
     sp[0] = vv;
     sp[1] = vr;
     sp[2] = tr;
@@ -391,29 +352,21 @@ __global__ void __launch_bounds__(threads_per_cta<NN>()) sweep_kernel(const Swee
 
 template <int NN>
 SweepKernelInfo info_for(int mode) {
-  SweepKernelInfo inf;
+  SweepKernelInfo inf{};
   inf.fn = mode == kModePapg ? (const void*)sweep_kernel<NN, kModePapg>
                              : (const void*)sweep_kernel<NN, kModePower>;
-  inf.C = cols_per_lane<NN>();
+  inf.strip_cols = 32 * cols_per_lane<NN>();
   inf.warps_per_block = consumer_warps<NN>();
-  const int smem = smem_bytes<NN>();
-  cudaFuncSetAttribute(inf.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  inf.tile_cols = tile_cols<NN>();
+  inf.threads = threads_per_cta<NN>();
+  inf.smem_bytes = smem_bytes<NN>();
+  cudaFuncSetAttribute(inf.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, inf.smem_bytes);
   int bps = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, inf.fn, threads_per_cta<NN>(), smem) !=
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, inf.fn, inf.threads, inf.smem_bytes) !=
       cudaSuccess)
     bps = 0;
   inf.max_blocks_per_sm = bps;
   return inf;
-}
-
-template <int NN>
-int launch_for(const SweepKernelInfo& info, const SweepArgs& a, cudaStream_t s) {
-  constexpr int kCW = consumer_warps<NN>();
-  const int T = (a.S + kCW - 1) / kCW;
-  const unsigned grid = (unsigned)((long long)T * a.P);
-  void* args[] = {const_cast<SweepArgs*>(&a)};
-  return (int)cudaLaunchKernel(info.fn, dim3(grid), dim3(threads_per_cta<NN>()), args,
-                               smem_bytes<NN>(), s);
 }
 
 template <int... Ns> struct Table;
@@ -421,25 +374,21 @@ template <int N0, int... Ns> struct Table<N0, Ns...> {
   static SweepKernelInfo info(int n, int mode) {
     return n == N0 ? info_for<N0>(mode) : Table<Ns...>::info(n, mode);
   }
-  static int launch(int n, const SweepKernelInfo& i, const SweepArgs& a, cudaStream_t s) {
-    return n == N0 ? launch_for<N0>(i, a, s) : Table<Ns...>::launch(n, i, a, s);
-  }
 };
 template <> struct Table<> {
-  static SweepKernelInfo info(int, int) { return SweepKernelInfo{nullptr, 0, 0, 0}; }
-  static int launch(int, const SweepKernelInfo&, const SweepArgs&, cudaStream_t) {
-    return (int)cudaErrorInvalidValue;
-  }
+  static SweepKernelInfo info(int, int) { return SweepKernelInfo{}; }
 };
 using AllN = Table<1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16, 17, 18, 19, 20, 21, 22,
                    23, 24>;
 
 }  // namespace
 
-SweepKernelInfo sweep_kernel_info(int n, int mode) { return AllN::info(n, mode); }
+SweepKernelInfo sweep_dfma_info(int n, int mode) { return AllN::info(n, mode); }
 
-int launch_sweep(const SweepKernelInfo& info, const SweepArgs& a, int n, void* stream) {
-  return AllN::launch(n, info, a, (cudaStream_t)stream);
+int launch_sweep(const SweepKernelInfo& info, const SweepArgs& a, void* stream) {
+  void* args[] = {const_cast<SweepArgs*>(&a)};
+  return (int)cudaLaunchKernel(info.fn, dim3((unsigned)a.G), dim3(info.threads), args,
+                               info.smem_bytes, (cudaStream_t)stream);
 }
 
 }  // namespace crb

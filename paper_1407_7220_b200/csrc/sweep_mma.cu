@@ -1,0 +1,375 @@
+// sweep_mma.cu -- K1 on the FP64 tensor cores (mma.sync m8n8k4 f64 -> DMMA).
+//
+// Same contract as sweep.cu (one HBM pass per dual iteration, 24 B per pair;
+// reference: operators.cpp:128-180, papg.cpp:187-208) but the two rank-n
+// contractions of the pair sweep run as 8x8x4 fp64 MMAs:
+//
+//   residual     -row^T (8 cols x 8 rows) = Xi'(8 x K) . X'^T(K x 8)
+//                with Xi'_l = (xi_l, c_l, -1), X'_l = (x_l, 1, y_l), K = n+2 -> mult. of 4
+//   aggregation  (V^T [X 1])^T (F x 8 cols) += [X 1]^T(F x 4 rows) . V(4 rows x 8 cols)
+//
+// The residual's accumulator fragment puts (col = lane/4, rows 2(lane%4)+{0,1})
+// in each thread. Splitting the 8 rows of a tile into the k-steps {0,2,4,6}
+// and {1,3,5,7} makes exactly those two values the B fragments of the two
+// aggregation MMAs (B[k=lane%4][n=lane/4]), so v never moves between lanes.
+//
+// CTA: 7 consumer warps x (4 tiles of 8 columns) = 224 columns, 1 producer
+// warp streaming 8-row stages of V, V' and the row records through a 4-deep
+// cp.async.bulk / mbarrier ring (row pitch padded by 16 B: conflict-free
+// column-fragment reads). Work split, partial layouts and row-sum combine are
+// identical to sweep.cu.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "device.cuh"
+#include "pipeline.cuh"
+
+namespace crb {
+
+namespace {
+
+constexpr int kCW = 7;                 // consumer warps (+1 producer = 8: 255-register cap)
+constexpr int kCT = 4;                 // 8-column MMA tiles per warp
+constexpr int kW = 8 * kCT;            // columns per warp
+constexpr int kTC = kCW * kW;          // columns per CTA tile (224)
+constexpr int kTCP = kTC + 2;          // smem row pitch of V stages (doubles)
+constexpr int kTR = 8;                 // rows per stage (one MMA row block)
+constexpr int kNS = 4;                 // stages
+constexpr int kThreads = (kCW + 1) * 32;
+constexpr int kWin = 32;               // row-sum window (rows)
+
+template <int NN>
+__host__ __device__ constexpr int ksteps() { return ((NN + 2) + 3) / 4; }
+template <int NN>
+__host__ __device__ constexpr int fblocks() { return ((NN + 1) + 7) / 8; }
+template <int NN>
+__host__ __device__ constexpr int stage_doubles() {
+  return 2 * kTR * kTCP + kTR * rec_pitch(NN);
+}
+template <int NN>
+__host__ __device__ constexpr int smem_bytes() {
+  return kNS * stage_doubles<NN>() * 8 + 2 * kCW * kWin * 8 + 2 * kNS * 8;
+}
+
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+struct MCoef {
+  double s_c, s_p, beta, invL;
+};
+struct MScal {
+  double vv, vr, tr, nn;
+};
+
+// One 8-row stage for one warp. MASK: diagonal / partial-stage masking.
+template <int NN, int MODE, bool MASK, bool UNIT>
+__device__ __forceinline__ void mma_stage(const double* __restrict__ sv, const double* __restrict__ svp,
+                                          const double* __restrict__ srec, double* gout,
+                                          long long ld, long long gcol0, long long grow0, int nr,
+                                          int lane, const double (&A)[kCT][ksteps<NN>()],
+                                          double (&D)[kCT][fblocks<NN>()][2], const MCoef& cf,
+                                          MScal& sc, double (&rs)[2]) {
+  constexpr int KS = ksteps<NN>();
+  constexpr int FB = fblocks<NN>();
+  constexpr int RQ = rec_pitch(NN);
+  const int q = lane & 3;
+  const int c8 = lane >> 2;
+  // residual B fragments: X'[row c8][k]
+  double B[KS];
+#pragma unroll
+  for (int ks = 0; ks < KS; ++ks) B[ks] = srec[c8 * RQ + ks * 4 + q];
+  // aggregation A fragments: [X 1][row 2q+j][feature fb*8 + c8]
+  double Ag[2][FB];
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const bool rv = !MASK || (2 * q + j < nr);
+#pragma unroll
+    for (int fb = 0; fb < FB; ++fb) Ag[j][fb] = rv ? srec[(2 * q + j) * RQ + fb * 8 + c8] : 0.0;
+  }
+  rs[0] = 0.0;
+  rs[1] = 0.0;
+#pragma unroll
+  for (int ct = 0; ct < kCT; ++ct) {
+    double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) dmma(d0, d1, A[ct][ks], B[ks]);
+    const int cl = ct * 8 + c8;  // column within the warp's strip
+    double v[2];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int rr = 2 * q + j;
+      const bool rv = !MASK || rr < nr;  // row present in this (partial) stage
+      double row = -(j == 0 ? d0 : d1);
+      if (MASK && (gcol0 + cl == grow0 + rr || !rv)) row = 0.0;
+      if (MODE == kModePapg) {
+        const double c1 = sv[rr * kTCP + cl];
+        const double p1 = svp[rr * kTCP + cl];
+        double th2;
+        if (UNIT) {
+          th2 = fma(cf.beta, c1 - p1, c1);
+        } else {
+          const double th1 = cf.s_c * c1;
+          th2 = fma(cf.beta, th1 - cf.s_p * p1, th1);
+        }
+        if (MASK && !rv) th2 = 0.0;
+        v[j] = keep_if_nonneg(fma(-row, cf.invL, th2));
+        sc.vv = fma(v[j], v[j], sc.vv);
+        sc.vr = fma(v[j], row, sc.vr);
+        sc.tr = fma(th2, row, sc.tr);
+        const double m = keep_if_neg(row);
+        sc.nn = fma(m, m, sc.nn);
+        if (rv) st_stream(gout + rr * ld + cl, v[j]);
+      } else {
+        v[j] = row;
+        sc.vv = fma(row, row, sc.vv);
+      }
+      rs[j] += v[j];
+    }
+#pragma unroll
+    for (int fb = 0; fb < FB; ++fb) {
+      dmma(D[ct][fb][0], D[ct][fb][1], Ag[0][fb], v[0]);
+      dmma(D[ct][fb][0], D[ct][fb][1], Ag[1][fb], v[1]);
+    }
+  }
+}
+
+template <int NN, int MODE>
+__global__ void __launch_bounds__(kThreads) sweep_mma_kernel(const SweepArgs a) {
+  constexpr int KS = ksteps<NN>();
+  constexpr int FB = fblocks<NN>();
+  constexpr int RQ = rec_pitch(NN);
+  constexpr int SD = stage_doubles<NN>();
+  extern __shared__ __align__(128) double smem[];
+  double* stages = smem;
+  double* rowacc = smem + kNS * SD;  // [2][kCW][kWin]
+  uint64_t* full = reinterpret_cast<uint64_t*>(rowacc + 2 * kCW * kWin);
+  uint64_t* empty = full + kNS;
+
+  if (a.stopped != nullptr && *a.stopped) return;
+  const int cur = (MODE == kModePapg) ? *a.cur : 0;
+  const double* Vc = cur ? a.V1 : a.V0;
+  double* Vp = cur ? a.V0 : a.V1;
+
+  const long long units = (long long)a.T * a.R;
+  const long long u0 = (long long)blockIdx.x * a.U;
+  const long long u1 = min(u0 + a.U, units);
+  if (u0 >= u1) return;
+  const int t_first = (int)(u0 / a.R);
+  const int t_last = (int)((u1 - 1) / a.R);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kNS; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kCW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == kCW) {  // ------------------------------------------ producer
+    if (lane == 0) {
+      const uint64_t pol_stream = policy_evict_first();
+      const uint64_t pol_keep = policy_evict_last();
+      int i = 0;
+      for (int t = t_first; t <= t_last; ++t) {
+        const long long rlo = max(u0, (long long)t * a.R) - (long long)t * a.R;
+        const long long rhi = min(u1, (long long)(t + 1) * a.R) - (long long)t * a.R;
+        const long long c0 = (long long)t * kTC;
+        const uint32_t vbytes = (uint32_t)min((long long)kTC, a.ld - c0) * 8u;
+        for (long long r = rlo; r < rhi; r += kTR, ++i) {
+          const int s = i % kNS;
+          if (i >= kNS) mbar_wait(&empty[s], (uint32_t)(((i / kNS) - 1) & 1));
+          const int nr = (int)min((long long)kTR, rhi - r);
+          double* st = stages + s * SD;
+          const uint32_t bytes =
+              (MODE == kModePapg ? 2u * nr * vbytes : 0u) + (uint32_t)nr * RQ * 8u;
+          mbar_arrive_expect_tx(&full[s], bytes);
+          if (MODE == kModePapg) {
+            for (int qq = 0; qq < nr; ++qq) {
+              const long long off = (r + qq) * a.ld + c0;
+              bulk_g2s(st + qq * kTCP, Vc + off, vbytes, &full[s], pol_stream);
+              bulk_g2s(st + (kTR + qq) * kTCP, Vp + off, vbytes, &full[s], pol_stream);
+            }
+          }
+          bulk_g2s(st + 2 * kTR * kTCP, a.rowrec + (a.r0 + r) * RQ, (uint32_t)nr * RQ * 8u,
+                   &full[s], pol_keep);
+        }
+      }
+    }
+    return;
+  }
+
+  // ---------------------------------------------------------------- consumers
+  const int q = lane & 3;
+  const int c8 = lane >> 2;
+  MCoef cf{1.0, 0.0, 0.0, a.invL};
+  if (MODE == kModePapg) {
+    cf.s_c = a.coef[0];
+    cf.s_p = a.coef[1];
+    cf.beta = a.coef[2];
+  }
+  const bool unit_scale = (cf.s_c == 1.0) && (cf.s_p == 1.0);
+  MScal sc{0.0, 0.0, 0.0, 0.0};
+  int i = 0;
+  int flushes = 0;
+
+  for (int t = t_first; t <= t_last; ++t) {
+    const long long rlo = max(u0, (long long)t * a.R) - (long long)t * a.R;
+    const long long rhi = min(u1, (long long)(t + 1) * a.R) - (long long)t * a.R;
+    const long long gcol0 = (long long)t * kTC + warp * kW;  // first column of the warp
+    const bool active = gcol0 < a.N;
+    // residual A fragments: Xi'[col][k] (zero for pad columns -> row = 0 there)
+    double A[kCT][KS];
+    double D[kCT][FB][2];
+#pragma unroll
+    for (int ct = 0; ct < kCT; ++ct) {
+      const long long col = gcol0 + ct * 8 + c8;
+      const bool cv = active && col < a.N;
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks)
+        A[ct][ks] = cv ? __ldg(a.colrec + col * RQ + ks * 4 + q) : 0.0;
+#pragma unroll
+      for (int fb = 0; fb < FB; ++fb) D[ct][fb][0] = D[ct][fb][1] = 0.0;
+    }
+    int win = 0;
+    long long win_base = rlo;
+    for (long long r = rlo; r < rhi; r += kTR, ++i) {
+      const int s = i % kNS;
+      mbar_wait(&full[s], (uint32_t)((i / kNS) & 1));
+      const int nr = (int)min((long long)kTR, rhi - r);
+      double rsj[2] = {0.0, 0.0};
+      if (active) {
+        const double* st = stages + s * SD;
+        const double* sv = st + warp * kW;
+        const double* svp = st + kTR * kTCP + warp * kW;
+        const double* srec = st + 2 * kTR * kTCP;
+        double* gout = Vp + r * a.ld + gcol0;
+        const long long grow0 = a.r0 + r;
+        // warp-uniform: no diagonal in this 8 x 32 block and a full stage
+        const bool clean = nr == kTR && (grow0 + kTR <= gcol0 || grow0 >= gcol0 + kW);
+        if (clean) {
+          if (unit_scale)
+            mma_stage<NN, MODE, false, true>(sv, svp, srec, gout, a.ld, gcol0, grow0, nr, lane, A,
+                                             D, cf, sc, rsj);
+          else
+            mma_stage<NN, MODE, false, false>(sv, svp, srec, gout, a.ld, gcol0, grow0, nr, lane,
+                                              A, D, cf, sc, rsj);
+        } else {
+          if (unit_scale)
+            mma_stage<NN, MODE, true, true>(sv, svp, srec, gout, a.ld, gcol0, grow0, nr, lane, A,
+                                            D, cf, sc, rsj);
+          else
+            mma_stage<NN, MODE, true, false>(sv, svp, srec, gout, a.ld, gcol0, grow0, nr, lane, A,
+                                             D, cf, sc, rsj);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+      // row sums over the warp's 32 columns: lanes sharing q hold the same rows
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        rsj[j] += __shfl_xor_sync(0xffffffffu, rsj[j], 4);
+        rsj[j] += __shfl_xor_sync(0xffffffffu, rsj[j], 8);
+        rsj[j] += __shfl_xor_sync(0xffffffffu, rsj[j], 16);
+      }
+      double* ra = rowacc + (flushes & 1) * kCW * kWin + warp * kWin;
+      if (c8 == 0) {
+        ra[win + 2 * q] = rsj[0];
+        ra[win + 2 * q + 1] = rsj[1];
+      }
+      win += kTR;
+      if (win == kWin || r + kTR >= rhi) {
+        // fixed-order sum over the CTA's warps into the tile's row-sum slice
+        asm volatile("bar.sync 1, %0;" ::"r"(kCW * 32) : "memory");
+        const int valid_rows = (int)min((long long)win, rhi - win_base);
+        if (warp == 0 && lane < valid_rows) {
+          const double* rb = rowacc + (flushes & 1) * kCW * kWin;
+          double u = 0.0;
+#pragma unroll
+          for (int w = 0; w < kCW; ++w) u += rb[w * kWin + lane];
+          a.rowpart[(long long)t * a.R + win_base + lane] = u;
+        }
+        win_base += win;
+        win = 0;
+        ++flushes;
+      }
+    }
+    if (active) {  // column partials: thread holds (feature fb*8+c8, cols 2q+{0,1})
+      const long long slot = (long long)blockIdx.x * a.maxspan + (t - t_first);
+#pragma unroll
+      for (int ct = 0; ct < kCT; ++ct) {
+#pragma unroll
+        for (int fb = 0; fb < FB; ++fb) {
+          const int f = fb * 8 + c8;
+          if (f <= NN) {
+            const int slotf = (f == NN) ? 0 : 1 + f;  // colagg = (colsum, V^T X)
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+              const long long coff = (long long)warp * kW + ct * 8 + 2 * q + j;
+              a.colpart[(slot * kTC + coff) * (NN + 1) + slotf] = D[ct][fb][j];
+            }
+          }
+        }
+      }
+    }
+  }
+
+  double vv = sc.vv, vr = sc.vr, tr = sc.tr, nn = sc.nn;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    vv += __shfl_xor_sync(0xffffffffu, vv, off);
+    vr += __shfl_xor_sync(0xffffffffu, vr, off);
+    tr += __shfl_xor_sync(0xffffffffu, tr, off);
+    nn += __shfl_xor_sync(0xffffffffu, nn, off);
+  }
+  if (lane == 0) {
+    double* sp = a.scalpart + ((long long)blockIdx.x * kCW + warp) * kScal;
+    sp[0] = vv;
+    sp[1] = vr;
+    sp[2] = tr;
+    sp[3] = nn;
+  }
+}
+
+template <int NN>
+SweepKernelInfo info_for(int mode) {
+  SweepKernelInfo inf{};
+  inf.fn = mode == kModePapg ? (const void*)sweep_mma_kernel<NN, kModePapg>
+                             : (const void*)sweep_mma_kernel<NN, kModePower>;
+  inf.strip_cols = kW;
+  inf.warps_per_block = kCW;
+  inf.tile_cols = kTC;
+  inf.threads = kThreads;
+  inf.smem_bytes = smem_bytes<NN>();
+  cudaFuncSetAttribute(inf.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, inf.smem_bytes);
+  int bps = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, inf.fn, inf.threads, inf.smem_bytes) !=
+      cudaSuccess)
+    bps = 0;
+  inf.max_blocks_per_sm = bps;
+  return inf;
+}
+
+template <int... Ns> struct Table;
+template <int N0, int... Ns> struct Table<N0, Ns...> {
+  static SweepKernelInfo info(int n, int mode) {
+    return n == N0 ? info_for<N0>(mode) : Table<Ns...>::info(n, mode);
+  }
+};
+template <> struct Table<> {
+  static SweepKernelInfo info(int, int) { return SweepKernelInfo{}; }
+};
+using AllN = Table<1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16, 17, 18, 19, 20, 21, 22,
+                   23, 24>;
+
+}  // namespace
+
+SweepKernelInfo sweep_mma_info(int n, int mode) { return AllN::info(n, mode); }
+
+}  // namespace crb
