@@ -75,6 +75,13 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if force or jobs or _stale(LIB, objs):
         run([_nvcc(), *ARCH, "-shared", "-o", LIB, *objs, "-lnccl", "-lcudart_static", "-lrt",
              "-lpthread", "-ldl"])
+    # C++ drop-in demo (include/cvxreg_b200/papg.hpp over the C ABI), used by the GPU tests
+    demo_src = os.path.join(ROOT, "tests", "cpp", "dropin_demo.cpp")
+    demo = os.path.join(PKG, "cxx_dropin_demo")
+    hpp = os.path.join(ROOT, "include", "cvxreg_b200", "papg.hpp")
+    if os.path.exists(demo_src) and (force or _stale(demo, [demo_src, hpp, LIB])):
+        run([_cxx(), "-O2", "-std=c++17", "-Wall", "-Wextra", "-I" + os.path.join(ROOT, "include"),
+             demo_src, "-o", demo, "-L" + PKG, "-lcvxreg_b200", "-Wl,-rpath,$ORIGIN"])
     return LIB
 
 

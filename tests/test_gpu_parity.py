@@ -1,0 +1,295 @@
+"""GPU parity of the B200 pair-sweep solver against the CPU oracle.
+
+Tolerances (BASELINE.json north_star): after k iterations the dual iterate
+theta and the per-pair residuals C eta agree within 1e-12 relative (normwise),
+the fitted y within 1e-8 relative, with identical iteration counts and
+termination reasons. sigma_max(C) is injected identically into both paths
+except in the sigma tests themselves.
+"""
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+import paper_1407_7220_b200 as crb
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+GOLDEN = os.path.join(ROOT, "tests", "golden")
+TOL_THETA = 1e-12
+TOL_ROWS = 1e-12
+TOL_Y = 1e-8
+
+
+def rel(a, b):
+    nb = np.linalg.norm(b)
+    return np.linalg.norm(np.asarray(a) - np.asarray(b)) / (nb if nb > 0 else 1.0)
+
+
+def gpu_run(X, ys, *, momentum=True, theta0=None, device_rows=None, **kw):
+    cfg = crb.PapgConfig(**kw)
+    with crb.DualSolver(X, ys, cfg.gamma) as s:
+        s.begin(cfg, momentum, theta0)
+        stopped = False
+        while not stopped:
+            _, stopped = s.iterate(1 << 40)
+        res, y, xi, hist = s.finish()
+        return dict(res=res, y=y, xi=xi, hist=hist, theta=s.theta(), rows=s.rows())
+
+
+def oracle_run(O, X, ys, *, momentum=True, theta0=None, **kw):
+    kw = dict(kw)
+    kw.pop("graph_iters", None)
+    return O.papg(X, ys, use_momentum=momentum, theta0=theta0, want_c_eta=True, **kw)
+
+
+def instance(O, kind, N, n, noise, seed, pieces=0):
+    X, y = O.gen_instance(kind, N, n, noise, seed, pieces)
+    p = O.prepare(X, y)
+    return X, p.ys
+
+
+def assert_parity(g, o, hist_rtol=1e-9):
+    assert g["res"].iters == o.iters
+    assert g["res"].reason == {"thresholds": 0, "iter_budget": 1, "time_budget": 2,
+                               "error": 3}[o.reason]
+    assert g["res"].restarts == o.restarts
+    assert rel(g["theta"], o.theta) <= TOL_THETA, rel(g["theta"], o.theta)
+    assert rel(g["rows"], o.c_eta) <= TOL_ROWS, rel(g["rows"], o.c_eta)
+    assert rel(g["y"], o.y) <= TOL_Y, rel(g["y"], o.y)
+    assert rel(g["xi"], o.xi.reshape(-1)) <= 1e-8
+    h, ho = g["hist"], o.history
+    for col in (1, 2, 3, 4):  # objective, reg_objective, infeas_raw, infeas_norm
+        assert np.allclose(h[:, col], ho[:, col], rtol=hist_rtol, atol=1e-300)
+    for col in (5, 6):  # gap may cross zero: compare against its scale
+        scale = np.abs(ho[:, col]).max()
+        assert np.abs(h[:, col] - ho[:, col]).max() <= hist_rtol * max(scale, 1e-300)
+    assert g["res"].g_final == pytest.approx(o.g_final, rel=1e-9, abs=1e-12)
+
+
+def test_smoke_parity(oracle):
+    X, ys = instance(oracle, "sqnorm-uniform", 300, 5, 0.1, 7)
+    s, _, _ = oracle.sigma_C(X)
+    kw = dict(max_iters=60, gap_norm_tol=-1.0, infeas_norm_tol=-1.0, sigma_C=s)
+    assert_parity(gpu_run(X, ys, **kw), oracle_run(oracle, X, ys, **kw))
+
+
+def test_golden_fixtures():
+    g = np.load(os.path.join(GOLDEN, "papg_small.npz"))
+    for i in range(int(g["count"])):
+        X, ys = g[f"X{i}"], g[f"ys{i}"]
+        it, s, gt, ft, B, mom = g[f"meta{i}"]
+        r = gpu_run(X, ys, momentum=bool(mom), max_iters=int(it), sigma_C=float(s),
+                    gap_norm_tol=float(gt), infeas_norm_tol=float(ft), B_theta=float(B))
+        assert r["res"].iters == int(g[f"iters{i}"][0])
+        assert rel(r["theta"], g[f"theta{i}"]) <= TOL_THETA
+        assert rel(r["rows"], g[f"c_eta{i}"]) <= TOL_ROWS
+        assert rel(r["y"], g[f"y{i}"]) <= TOL_Y
+        assert rel(r["xi"], g[f"xi{i}"].reshape(-1)) <= 1e-8
+
+
+@pytest.mark.parametrize("variant", ["dfma", "mma"])
+@pytest.mark.parametrize("n", list(range(1, 25)))
+def test_every_n_both_sweep_variants(oracle, monkeypatch, variant, n):
+    monkeypatch.setenv("CRB_SWEEP", variant)
+    N = 67 + 3 * n  # ragged: not a multiple of any strip or tile width
+    X, ys = instance(oracle, "maxaffine-uniform", N, n, 0.1, 100 + n, 6)
+    s, _, _ = oracle.sigma_C(X)
+    kw = dict(max_iters=15, gap_norm_tol=-1.0, infeas_norm_tol=-1.0, sigma_C=s)
+    assert_parity(gpu_run(X, ys, **kw), oracle_run(oracle, X, ys, **kw))
+
+
+def test_config1_full_2000_iterations(oracle):
+    """BASELINE config 1: N=1000, n=5, |x|^2 + U[-0.1, 0.1] noise, 2000 iterations."""
+    X, ys = instance(oracle, "sqnorm-uniform", 1000, 5, 0.1, 1)
+    s, _, _ = oracle.sigma_C(X)
+    kw = dict(max_iters=2000, gap_norm_tol=-1.0, infeas_norm_tol=-1.0, sigma_C=s)
+    o = oracle_run(oracle, X, ys, threads=8, **kw)
+    assert_parity(gpu_run(X, ys, **kw), o, hist_rtol=1e-8)
+
+
+def test_sigma_C_parity(oracle):
+    for kind, N, n, pieces in [("sqnorm-uniform", 400, 5, 0), ("maxaffine-uniform", 300, 10, 20),
+                               ("lse-uniform", 250, 20, 50)]:
+        X, ys = instance(oracle, kind, N, n, 0.1, 3, pieces)
+        so, ito, co = oracle.sigma_C(X)
+        with crb.DualSolver(X, ys) as d:
+            sg, itg, cg = d.sigma_C()
+        assert itg == ito and cg == co
+        assert sg == pytest.approx(so, rel=1e-10)
+
+
+def test_default_thresholds_termination(oracle):
+    X, ys = instance(oracle, "sqnorm-uniform", 1000, 5, 0.1, 1)
+    s, _, _ = oracle.sigma_C(X)
+    g = gpu_run(X, ys, sigma_C=s)
+    o = oracle_run(oracle, X, ys, sigma_C=s)
+    assert o.reason == "thresholds"
+    assert_parity(g, o)
+    # delta estimate and final dual value (papg.cpp:272-275)
+    assert g["res"].delta_estimate == pytest.approx(o.delta_estimate, rel=1e-8)
+
+
+def test_dual_gradient_ascent_parity(oracle):
+    X, ys = instance(oracle, "maxaffine-uniform", 500, 10, 0.1, 9, 20)
+    s, _, _ = oracle.sigma_C(X)
+    kw = dict(max_iters=120, gap_norm_tol=-1.0, infeas_norm_tol=-1.0, sigma_C=s)
+    assert_parity(gpu_run(X, ys, momentum=False, **kw), oracle_run(oracle, X, ys, momentum=False, **kw))
+
+
+def test_ball_binding_adaptive_restarts(oracle):
+    """Tiny B_theta: Q2 clips every iterate; loose thresholds stop at once, the
+    saturated norm triggers the doubling warm restarts (papg.cpp:238-251)."""
+    X, ys = instance(oracle, "sqnorm-uniform", 200, 3, 0.1, 5)
+    s, _, _ = oracle.sigma_C(X)
+    kw = dict(max_iters=400, gap_norm_tol=1e9, infeas_norm_tol=1e9, sigma_C=s, B_theta=1e-5)
+    g, o = gpu_run(X, ys, **kw), oracle_run(oracle, X, ys, **kw)
+    assert o.restarts >= 3
+    assert_parity(g, o)
+    assert g["res"].B_theta == o.B_theta == pytest.approx(1e-5 * 2 ** o.restarts)
+    kw.update(gap_norm_tol=-1.0, infeas_norm_tol=-1.0, max_iters=80, adaptive_B_theta=False)
+    assert_parity(gpu_run(X, ys, **kw), oracle_run(oracle, X, ys, **kw))
+
+
+def test_warm_start_parity(oracle):
+    X, ys = instance(oracle, "maxaffine-uniform", 260, 6, 0.1, 12, 8)
+    s, _, _ = oracle.sigma_C(X)
+    kw = dict(max_iters=30, gap_norm_tol=-1.0, infeas_norm_tol=-1.0, sigma_C=s)
+    first = oracle_run(oracle, X, ys, **kw)
+    rng = np.random.default_rng(0)
+    theta0 = first.theta * 3e4 + rng.normal(size=first.theta.size) * 1e-3  # forces clipping
+    kw["B_theta"] = 20.0
+    assert_parity(gpu_run(X, ys, theta0=theta0, **kw),
+                  oracle_run(oracle, X, ys, theta0=theta0, **kw))
+
+
+def test_graph_and_direct_modes_bitwise_identical(oracle):
+    X, ys = instance(oracle, "sqnorm-uniform", 700, 5, 0.1, 4)
+    s, _, _ = oracle.sigma_C(X)
+    kw = dict(max_iters=150, gap_norm_tol=-1.0, infeas_norm_tol=-1.0, sigma_C=s)
+    a = gpu_run(X, ys, graph_iters=16, **kw)
+    b = gpu_run(X, ys, graph_iters=-1, **kw)
+    c = gpu_run(X, ys, graph_iters=-1, **kw)
+    assert np.array_equal(a["theta"], b["theta"]) and np.array_equal(a["y"], b["y"])
+    assert np.array_equal(b["theta"], c["theta"])  # run-to-run determinism
+
+
+def test_iterate_in_pieces_matches_one_call(oracle):
+    X, ys = instance(oracle, "sqnorm-uniform", 500, 4, 0.1, 8)
+    s, _, _ = oracle.sigma_C(X)
+    cfg = crb.PapgConfig(max_iters=97, gap_norm_tol=-1.0, infeas_norm_tol=-1.0, sigma_C=s)
+    with crb.DualSolver(X, ys) as d:
+        d.begin(cfg)
+        done = 0
+        for k in (1, 2, 7, 30, 100):
+            done, stopped = d.iterate(k)
+        assert done == 97 and stopped
+        piecewise = d.theta()
+    whole = gpu_run(X, ys, max_iters=97, gap_norm_tol=-1.0, infeas_norm_tol=-1.0, sigma_C=s)
+    assert np.array_equal(piecewise, whole["theta"])
+
+
+def test_row_sharded_emulation_on_one_gpu(oracle):
+    """Two handles own row blocks [0, N/2) and [N/2, N) of the pair matrix; the
+    per-iteration aggregate exchange (the NCCL allreduce payload) is summed on
+    the host. The sharded iterates must match the unsharded ones."""
+    X, ys = instance(oracle, "maxaffine-uniform", 420, 10, 0.1, 21, 20)
+    s, _, _ = oracle.sigma_C(X)
+    N = X.shape[0]
+    cfg = crb.PapgConfig(max_iters=40, gap_norm_tol=-1.0, infeas_norm_tol=-1.0, sigma_C=s)
+    cut = 173
+    shards = [crb.DualSolver(X, ys, row_begin=0, row_end=cut),
+              crb.DualSolver(X, ys, row_begin=cut, row_end=N)]
+    try:
+        for d in shards:
+            d.begin(cfg)
+        for _ in range(40):
+            for d in shards:
+                d.iter_local()
+            total = shards[0].exchange_get() + shards[1].exchange_get()
+            for d in shards:
+                d.exchange_put(total)
+            stops = [d.iter_finish() for d in shards]
+            assert stops[0] == stops[1]
+        th = [d.theta() for d in shards]
+        theta = np.concatenate([th[0][: cut * (N - 1)], th[1][: (N - cut) * (N - 1)], th[0][-N:]])
+        res = [d.finish() for d in shards]
+    finally:
+        for d in shards:
+            d.close()
+    o = oracle_run(oracle, X, ys, max_iters=40, gap_norm_tol=-1.0, infeas_norm_tol=-1.0, sigma_C=s)
+    assert rel(theta, o.theta) <= TOL_THETA
+    assert rel(res[0][1], o.y) <= TOL_Y and np.array_equal(res[0][1], res[1][1])
+
+
+def test_nonfinite_gradient_raises():
+    rng = np.random.default_rng(1)
+    X = rng.uniform(-1, 1, size=(50, 3))
+    ys = rng.uniform(1, 2, size=50)
+    ys[7] = 1e308  # rows overflow to inf
+    with pytest.raises(RuntimeError, match="non-finite"):
+        gpu_run(X, ys, max_iters=5, gap_norm_tol=-1.0, infeas_norm_tol=-1.0, sigma_C=50.0)
+
+
+def test_iterate_before_begin_raises():
+    rng = np.random.default_rng(1)
+    X = rng.uniform(-1, 1, size=(20, 2))
+    with crb.DualSolver(X, np.ones(20)) as d:
+        with pytest.raises((ValueError, RuntimeError)):
+            d.iterate(1)  # before begin
+
+
+def _numpy_primal(theta, X, ys, gamma, N):
+    th = theta[: N * (N - 1)].reshape(N, N - 1)
+    full = np.zeros((N, N))
+    mask = ~np.eye(N, dtype=bool)
+    full[mask] = th.reshape(-1)
+    rows, cols = full.sum(1), full.sum(0)
+    y = ys + theta[N * (N - 1):] + rows - cols
+    xi = (cols[:, None] * X - full.T @ X) / gamma
+    return y, xi
+
+
+@pytest.mark.parametrize("kind,N,n,noise,pieces,iters", [
+    ("maxaffine-uniform", 10000, 10, 0.1, 20, 25),   # BASELINE config 2
+    ("lse-uniform", 20000, 20, 0.05, 50, 10),        # BASELINE config 3
+])
+def test_full_size_properties(kind, N, n, noise, pieces, iters):
+    """At BASELINE sizes the oracle is too slow; size-independent properties:
+    theta in Q2, diagonal-free, the returned primal equals the closed form of
+    the exported theta (aggregation identity), history consistent."""
+    d = crb.gen_instance(crb.GeneratorSpec(kind, n, N, noise, 1, pieces))
+    p = crb.prepare_problem(d)
+    g = gpu_run(p.data.xs, p.data.ys, max_iters=iters, gap_norm_tol=-1.0, infeas_norm_tol=-1.0)
+    th = g["theta"]
+    assert th.min() >= 0.0
+    assert np.linalg.norm(th) <= g["res"].B_theta * (1 + 1e-12)
+    y, xi = _numpy_primal(th, p.data.xs, p.data.ys, 1e-3, N)
+    assert rel(g["y"], y) <= 1e-10
+    assert rel(g["xi"], xi.reshape(-1)) <= 1e-9
+    h = g["hist"]
+    assert h.shape[0] == iters and np.all(np.isfinite(h))
+    assert np.all(np.diff(h[:, 0]) == 1)
+    # infeasibility of the last eta from the exported rows
+    r = g["rows"]
+    infeas = np.linalg.norm(np.minimum(r[: N * (N - 1)], 0))
+    assert infeas == pytest.approx(h[-1, 3], rel=1e-9)
+
+
+def test_cpp_dropin_binary(oracle, tmp_path):
+    exe = os.path.join(ROOT, "paper_1407_7220_b200", "cxx_dropin_demo")
+    assert os.path.exists(exe), "built by __graft_entry__.build()"
+    X, ys = instance(oracle, "maxaffine-uniform", 240, 5, 0.1, 3, 8)
+    s, _, _ = oracle.sigma_C(X)
+    inp = tmp_path / "in.bin"
+    out = tmp_path / "out.bin"
+    np.concatenate([[X.shape[0], X.shape[1], 50, s], X.reshape(-1), ys]).astype(np.float64).tofile(inp)
+    subprocess.run([exe, str(inp), str(out)], check=True)
+    res = np.fromfile(out, dtype=np.float64)
+    N = X.shape[0]
+    iters, y, theta = int(res[0]), res[1:1 + N], res[1 + N:]
+    o = oracle_run(oracle, X, ys, max_iters=50, gap_norm_tol=-1.0, infeas_norm_tol=-1.0, sigma_C=s)
+    assert iters == o.iters
+    assert rel(theta, o.theta) <= TOL_THETA and rel(y, o.y) <= TOL_Y
