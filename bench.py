@@ -1,0 +1,331 @@
+#!/usr/bin/env python
+"""bench.py -- pair-constraint updates/s of the B200 P-APG pair sweep.
+
+Metric (BASELINE.json): pair-constraint updates/s = N^2 * iterations / s, and
+time-to-tolerance. A step is one dual iteration of papg_solve over the whole
+N x N pair matrix (primal closed form + fused pair sweep + fixed-order reduce
++ control). Workload at 1 GPU: BASELINE config 2 (N = 10000, n = 10,
+x ~ U[-1,1]^10, y = max of 20 affine pieces + U[-0.1,0.1] noise, fp64).
+With --gpus p > 1 the run is weak-scaled: N = round(1e4 sqrt(p)), so every
+GPU sweeps the same 1e8 pairs per iteration over its row block.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+--impl reference times the reference's algorithm on the host CPU (the
+oracle port, oracle/cvxreg_oracle.c, all host threads; the reference itself
+cannot be built here) on the same config and metric.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+BYTES_PER_PAIR = 24  # read V, read V', write v (fp64)
+CONFIGS = {  # BASELINE.json configs
+    "cfg1": dict(kind="sqnorm-uniform", N=1000, n=5, noise=0.1, pieces=0),
+    "cfg2": dict(kind="maxaffine-uniform", N=10000, n=10, noise=0.1, pieces=20),
+    "cfg3": dict(kind="lse-uniform", N=20000, n=20, noise=0.05, pieces=50),
+    "cfg4": dict(kind="sqnorm-uniform", N=50000, n=10, noise=0.2, pieces=0),
+    "cfg5": dict(kind="maxaffine-uniform", N=100000, n=5, noise=0.1, pieces=10),
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2000)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="cfg2")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip time-to-tolerance and e2e")
+    return ap.parse_args()
+
+
+def workload(name, world):
+    c = dict(CONFIGS[name])
+    if world > 1:
+        c["N"] = int(round(c["N"] * math.sqrt(world)))
+    return c
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0}, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(cfgname, variant):
+    """dram bytes (read + write) per sweep launch from the committed ncu capture."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "sweep_traffic.json")) as f:
+            d = json.load(f)
+        e = d.get(f"{cfgname}:{variant}")
+        return None if e is None else float(e["dram_bytes_per_launch"])
+    except (OSError, ValueError, KeyError):
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        time.sleep(0.15)
+        return self
+
+    def __exit__(self, *exc):
+        time.sleep(0.1)
+        self.samples = []
+        if self.proc is None:
+            return
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        for line in out.splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.samples.append(parts)
+
+    def summary(self):
+        if not getattr(self, "samples", None):
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if s[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def cpu_oracle_rate(cfg, threads, k_lo=1, k_hi=4):
+    """Oracle (CPU restatement of papg.cpp) per-iteration rate on the config:
+    difference of two runs (k_lo, k_hi iterations) removes setup and the final
+    re-solve. Returns (pair-updates/s, seconds of CPU work, sample text)."""
+    from oracle import oracle as O
+
+    X, y = O.gen_instance(cfg["kind"], cfg["N"], cfg["n"], cfg["noise"], 1, cfg["pieces"])
+    p = O.prepare(X, y)
+    sigma = 300.0  # step size does not change the cost of an iteration
+    kw = dict(sigma_C=sigma, gap_norm_tol=-1.0, infeas_norm_tol=-1.0, threads=threads,
+              record_history=False, want_theta=False)
+    t0 = time.perf_counter()
+    a = O.papg(X, p.ys, max_iters=k_lo, **kw).wall_seconds
+    b = O.papg(X, p.ys, max_iters=k_hi, **kw).wall_seconds
+    spent = time.perf_counter() - t0
+    per_iter = max(b - a, 1e-9) / (k_hi - k_lo)
+    N = cfg["N"]
+    sample = (f"{cfg['kind']} N={N} n={cfg['n']}: {k_hi - k_lo} dual iterations "
+              f"(runs of {k_lo} and {k_hi}), {threads} thread(s), {per_iter:.3f} s/iteration")
+    return N * N / per_iter, spent, sample
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    cfg = workload(args.config, 1)
+    threads = os.cpu_count() or 1
+    k_hi = 1 + max(1, min(args.steps, 4))
+    rate, spent, sample = cpu_oracle_rate(cfg, threads, 1, k_hi)
+    line = {
+        "impl": "reference", "metric": "pair-constraint updates/s", "value": rate,
+        "unit": "pair-updates/s", "n_gpus": args.gpus, "steps": k_hi - 1, "warmup": 1,
+        "ms_per_step": cfg["N"] ** 2 / rate * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{args.config}: {cfg['kind']} N={cfg['N']} n={cfg['n']}",
+                   "N": cfg["N"], "n": cfg["n"], "pairs_per_step": cfg["N"] ** 2},
+        "cpu_baseline": {"value": rate, "unit": "pair-updates/s", "cores": threads,
+                         "kind": "port", "sample": sample},
+        "e2e": {"value": rate, "unit": "pair-updates/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "note": "oracle/cvxreg_oracle.c (CPU restatement of papg.cpp:136-283, OpenMP rows); "
+                "the reference does not build here (Eigen3/vendor absent, alcc.cpp:200-203)",
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args):
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        world = max(world, 1)
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    import paper_1407_7220_b200 as crb
+    from paper_1407_7220_b200.dist import sharded_solver
+
+    cfg = workload(args.config, world)
+    N, n = cfg["N"], cfg["n"]
+    data = crb.gen_instance(crb.GeneratorSpec(cfg["kind"], n, N, cfg["noise"], 1, cfg["pieces"]))
+    prep = crb.prepare_problem(data)
+
+    if world > 1:
+        solver = sharded_solver(prep.data.xs, prep.data.ys, group=None, device=local)
+    else:
+        solver = crb.DualSolver(prep.data.xs, prep.data.ys, device=local)
+    sigma, sig_iters, _ = solver.sigma_C()
+    W, K = max(args.warmup, 3), args.steps
+    pc = crb.PapgConfig(max_iters=W + K + 16, gap_norm_tol=-1.0, infeas_norm_tol=-1.0,
+                        sigma_C=sigma, device=local)
+    solver.begin(pc)
+    solver.iterate(W)
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    with ClockSampler(local) as clk:
+        barrier()
+        torch.cuda.synchronize()
+        done0 = solver.iterate(0)[0]
+        t_wall0 = time.perf_counter()
+        done, stopped = solver.iterate(K)
+        t_wall = time.perf_counter() - t_wall0
+        torch.cuda.synchronize()
+        barrier()
+    dev_s, launches, sweep_s = solver.last_timing()
+    assert done - done0 == K and not stopped, (done, done0, stopped)
+    t = torch.tensor([dev_s, sweep_s], dtype=torch.float64, device="cuda")
+    if dist is not None:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dev_max, sweep_max = float(t[0]), float(t[1])
+    rows = solver.row_end - solver.row_begin
+    variant = solver.sweep_variant
+    solver.close()
+
+    pairs_step = N * N  # metric unit: N^2 pair-constraint updates per iteration
+    value = pairs_step * K / dev_max
+    peaks, peak_kind = measured_peaks()
+    sweep_avg = sweep_s / K if sweep_s > 0 else None
+    achieved = (BYTES_PER_PAIR * rows * N / sweep_avg / 1e9) if sweep_avg else None
+    roofline = {
+        "bound": "hbm", "unit": "GB/s", "achieved": achieved, "peak": peaks["hbm_gbs"],
+        "frac": (achieved / peaks["hbm_gbs"]) if achieved else None,
+        "traffic": ncu_traffic(args.config if world == 1 else "", variant),
+        "peak_kind": peak_kind, "kernel": f"sweep ({variant})",
+        "algorithmic_bytes_per_launch": BYTES_PER_PAIR * rows * N,
+        "sweep_share_of_step": (sweep_s / dev_s) if dev_s > 0 else None,
+    }
+
+    extras = {}
+    if not args.no_extras:
+        # e2e: the public API call from host arrays, K iterations, sigma estimated inside
+        ecfg = crb.PapgConfig(max_iters=K, gap_norm_tol=-1.0, infeas_norm_tol=-1.0, device=local,
+                              record_history=False)
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        if world > 1:
+            from paper_1407_7220_b200.dist import papg_solve_sharded
+
+            er = papg_solve_sharded(prep, ecfg)
+        else:
+            er = crb.papg_solve(prep, ecfg, want_dual=False)
+        torch.cuda.synchronize()
+        barrier()
+        e_s = time.perf_counter() - t0
+        te = torch.tensor([e_s], dtype=torch.float64, device="cuda")
+        if dist is not None:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e_s = float(te[0])
+        h2d = 8 * (N * n + N)  # X and shifted ybar, once per call
+        d2h = 8 * (N + N * n)  # fitted y and xi
+        extras["e2e"] = {"value": pairs_step * er.report.iters / e_s, "unit": "pair-updates/s",
+                         "h2d_bytes_per_step": h2d / K, "d2h_bytes_per_step": d2h / K,
+                         "seconds": e_s, "iterations": er.report.iters,
+                         "includes": "handle create + H2D, sigma_C power iteration, K iterations,"
+                                     " final re-solve, D2H of (y, xi)"}
+        if world == 1 and args.config == "cfg2":
+            # time to tolerance: BASELINE cfg 2 runs to |gap_norm| <= 1e-4 (and infeas <= 1e-1)
+            tcfg = crb.PapgConfig(gap_norm_tol=1e-4, device=local)
+            t0 = time.perf_counter()
+            tr = crb.papg_solve(prep, tcfg, want_dual=False)
+            tt = time.perf_counter() - t0
+            extras["time_to_tolerance"] = {
+                "seconds": tt, "iterations": tr.report.iters, "reason": tr.report.reason.name,
+                "sigma_seconds": tr.sigma_seconds, "sigma_power_steps": tr.sigma_iters,
+                "loop_seconds": tr.loop_seconds, "gap_norm_tol": 1e-4, "infeas_norm_tol": 0.1}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        rate, spent, sample = cpu_oracle_rate(cfg, threads)
+        cpu = {"value": rate, "unit": "pair-updates/s", "cores": threads, "kind": "port",
+               "sample": sample}
+        if "time_to_tolerance" in extras:
+            extras["time_to_tolerance"]["cpu_port_estimate_s"] = (
+                extras["time_to_tolerance"]["iterations"] * N * N / rate)
+
+    if rank == 0:
+        line = {
+            "metric": "pair-constraint updates/s", "value": value, "unit": "pair-updates/s",
+            "n_gpus": world, "steps": K, "warmup": W, "ms_per_step": dev_max / K * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded BASELINE generator)",
+            "config": {"workload": f"{args.config}: {cfg['kind']} N={N} n={n} "
+                                   f"pieces={cfg['pieces']} noise={cfg['noise']}"
+                                   + (" (weak scaling N=1e4*sqrt(p))" if world > 1 else ""),
+                       "N": N, "n": n, "pairs_per_step": pairs_step,
+                       "rows_per_gpu": rows, "sweep_variant": variant,
+                       "l2": "inputs > L2 (V, V' = 1.6 GB per GPU), no flush",
+                       "sigma_C": sigma, "sigma_power_steps": sig_iters,
+                       "timing": "CUDA events on the solver stream, max over ranks",
+                       "wall_s": t_wall},
+            "roofline": roofline, "cpu_baseline": cpu, "gpu_launches": launches,
+            "clocks": clk.summary(),
+        }
+        line.update(extras)
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -146,6 +146,9 @@ cr_status cr_get_rows(cr_handle *h, double *out);
    launches it issued (for bench.py) */
 cr_status cr_last_timing(const cr_handle *h, double *seconds, int64_t *launches,
                          double *sweep_seconds);
+/* sweep kernel variant chosen for this handle: 0 = CUDA-core DFMA,
+   1 = FP64 tensor-core DMMA (override with CRB_SWEEP=dfma|mma) */
+int32_t cr_sweep_variant(const cr_handle *h);
 /* Time k sweep-kernel launches alone on the handle's stream with CUDA events
    (the dominant kernel in isolation, for the roofline). */
 cr_status cr_time_sweep(cr_handle *h, int32_t k, double *avg_seconds);

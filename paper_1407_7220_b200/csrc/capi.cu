@@ -207,7 +207,8 @@ cr_status enqueue_iteration(cr_handle* h, int phase, cudaEvent_t ev_a, cudaEvent
   return CR_OK;
 }
 
-int launches_per_iteration(const cr_handle* h) { return h->comm ? 5 : 3; }
+// our kernels per iteration (the NCCL allreduce kernel is not counted)
+int launches_per_iteration(const cr_handle* h) { return h->comm ? 4 : 3; }
 
 cr_status build_graph(cr_handle* h) {
   if (h->gexec) {
@@ -901,6 +902,8 @@ cr_status cr_last_timing(const cr_handle* h, double* seconds, int64_t* launches,
   if (sweep_seconds) *sweep_seconds = h->last_sweep_seconds;
   return CR_OK;
 }
+
+int32_t cr_sweep_variant(const cr_handle* h) { return h ? h->variant : -1; }
 
 cr_status cr_time_sweep(cr_handle* h, int32_t k, double* avg_seconds) {
   if (!h || k < 1 || !avg_seconds) return CR_EINVAL;

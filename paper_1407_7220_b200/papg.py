@@ -258,6 +258,10 @@ class DualSolver:
         _raise(self._L.cr_attach_nccl(self.h, uid, rank, world), self.h)
 
     @property
+    def sweep_variant(self) -> str:
+        return {0: "dfma", 1: "mma"}.get(int(self._L.cr_sweep_variant(self.h)), "?")
+
+    @property
     def exchange_len(self):
         return int(self._L.cr_exchange_len(self.h))
 
