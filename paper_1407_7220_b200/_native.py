@@ -9,7 +9,7 @@ import ctypes as C
 import os
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libcvxreg_b200.so")
+LIB_PATH = os.environ.get("CRB_LIB") or os.path.join(PKG, "libcvxreg_b200.so")
 
 CR_STATUS = {0: "CR_OK", 1: "CR_EINVAL", 2: "CR_ENOMEM", 3: "CR_ECUDA", 4: "CR_ENCCL",
              5: "CR_ENONFINITE", 6: "CR_ESTATE"}

@@ -13,8 +13,8 @@
 //               NCCL allreduce payload of sharded runs.
 //   aggsave   : the same aggregates for the previous V.
 //   rowrec    : N x RQ  (x_l[0..n-1], 1, y_l, 0...)
-//   colrec    : N x RQ  (xi_l[0..n-1], c_l, -1, 0...)   c_l = y_l - xi_l . x_l
-//               so that -(C eta)_{l1 l2} = colrec[l2] . rowrec[l1] (the MMA
+//   colrec    : N x RQ  (-xi_l[0..n-1], -c_l, 1, 0...)   c_l = y_l - xi_l . x_l
+//               so that (C eta)_{l1 l2} = colrec[l2] . rowrec[l1] (the MMA
 //               residual), RQ = max(round_up(n+2, 4), round_up(n+1, 8)).
 #pragma once
 #include <cstdint>

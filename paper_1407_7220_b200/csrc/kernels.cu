@@ -116,11 +116,11 @@ __global__ void __launch_bounds__(kPBlock) primal_kernel(const PrimalArgs a) {
     }
     const double dy = y - ybar;
     if (a.mode == 0) {
-      double* crec = a.colrec + l * RP;  // (xi, c, -1)
+      double* crec = a.colrec + l * RP;  // (-xi, -c, 1)
 #pragma unroll
-      for (int j = 0; j < NN; ++j) crec[j] = xi[j];
-      crec[NN] = y - cx;
-      crec[NN + 1] = -1.0;
+      for (int j = 0; j < NN; ++j) crec[j] = -xi[j];
+      crec[NN] = -(y - cx);
+      crec[NN + 1] = 1.0;
       a.rowrec[l * RP + NN + 1] = y;     // (x, 1, y)
       // y >= 0 rows of C: theta1_pos = max(theta2_pos - y / L, 0) (papg.cpp:188-189)
       const double vnew = fmax(fma(-y, a.invL, th2pos), 0.0);
@@ -359,10 +359,10 @@ __global__ void __launch_bounds__(kPBlock) power_prep_kernel(const PowerArgs a) 
       const double vxi = a.u[N + l * n + j] / a.norm_u;
       a.v[N + l * n + j] = vxi;
       cx = fma(vxi, x[j], cx);
-      crec[j] = vxi;
+      crec[j] = -vxi;
     }
-    crec[n] = vy - cx;
-    crec[n + 1] = -1.0;
+    crec[n] = -(vy - cx);
+    crec[n + 1] = 1.0;
     a.rowrec[l * RP + n + 1] = vy;
     acc[0] = fma(vy, vy, acc[0]);  // pos rows of C v = v_y
   }
@@ -449,8 +449,8 @@ __global__ void rows_out_kernel(double* stage, const double* rowrec, const doubl
     const long long c = k + (k >= gr ? 1 : 0);
     const double* xr = rowrec + gr * RP;
     const double* cr = colrec + c * RP;
-    double row = xr[n + 1] - cr[n];  // y_l1 - c_l2 - x_l1 . xi_l2
-    for (int j = 0; j < n; ++j) row = fma(-xr[j], cr[j], row);
+    double row = xr[n + 1] + cr[n];  // y_l1 - c_l2 - x_l1 . xi_l2
+    for (int j = 0; j < n; ++j) row = fma(xr[j], cr[j], row);
     stage[i] = row;
   }
 }

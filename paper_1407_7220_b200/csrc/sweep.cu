@@ -121,11 +121,12 @@ __device__ __forceinline__ void run_stage(const StageView& sv, int nr, int lane,
       double rs = 0.0;
 #pragma unroll
       for (int k = 0; k < C; ++k) {
-        double ra = y1 - cs.cc[k], rb = 0.0;  // two FMA chains for ILP
+        // colrec holds (-xi, -c): row = y1 - c - x.xi, two FMA chains for ILP
+        double ra = y1 + cs.cc[k], rb = 0.0;
 #pragma unroll
         for (int j = 0; j < NN; j += 2) {
-          ra = fma(-x[j], cs.xi[k][j], ra);
-          if (j + 1 < NN) rb = fma(-x[j + 1], cs.xi[k][j + 1], rb);
+          ra = fma(x[j], cs.xi[k][j], ra);
+          if (j + 1 < NN) rb = fma(x[j + 1], cs.xi[k][j + 1], rb);
         }
         double row = ra + rb;
         if (MASK && (!cs.valid[k] || sv.col0 + k == sv.g0 + q)) row = 0.0;
@@ -264,7 +265,7 @@ __global__ void __launch_bounds__(threads_per_cta<NN>()) sweep_kernel(const Swee
     for (int k = 0; k < C; ++k) {
       const long long col = col0 + k;
       cs.valid[k] = active && col < a.N;
-      const double* rec = a.colrec + (cs.valid[k] ? col : 0) * RP;  // (xi, c, -1)
+      const double* rec = a.colrec + (cs.valid[k] ? col : 0) * RP;  // (-xi, -c, 1)
       cs.cc[k] = cs.valid[k] ? __ldg(rec + NN) : 0.0;
 #pragma unroll
       for (int j = 0; j < NN; ++j) cs.xi[k][j] = cs.valid[k] ? __ldg(rec + j) : 0.0;

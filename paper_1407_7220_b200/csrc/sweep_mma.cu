@@ -4,8 +4,8 @@
 // reference: operators.cpp:128-180, papg.cpp:187-208) but the two rank-n
 // contractions of the pair sweep run as 8x8x4 fp64 MMAs:
 //
-//   residual     -row^T (8 cols x 8 rows) = Xi'(8 x K) . X'^T(K x 8)
-//                with Xi'_l = (xi_l, c_l, -1), X'_l = (x_l, 1, y_l), K = n+2 -> mult. of 4
+//   residual     row^T (8 cols x 8 rows) = Xi'(8 x K) . X'^T(K x 8)
+//                with Xi'_l = (-xi_l, -c_l, 1), X'_l = (x_l, 1, y_l), K = n+2 -> mult. of 4
 //   aggregation  (V^T [X 1])^T (F x 8 cols) += [X 1]^T(F x 4 rows) . V(4 rows x 8 cols)
 //
 // The residual's accumulator fragment puts (col = lane/4, rows 2(lane%4)+{0,1})
@@ -35,7 +35,11 @@ constexpr int kW = 8 * kCT;            // columns per warp
 constexpr int kTC = kCW * kW;          // columns per CTA tile (224)
 constexpr int kTCP = kTC + 2;          // smem row pitch of V stages (doubles)
 constexpr int kTR = 8;                 // rows per stage (one MMA row block)
-constexpr int kNS = 4;                 // stages
+#ifndef CRB_MMA_CTAS_PER_SM
+#define CRB_MMA_CTAS_PER_SM 1
+#endif
+constexpr int kMinCtas = CRB_MMA_CTAS_PER_SM;  // 2: 128-register cap, 3-stage ring
+constexpr int kNS = kMinCtas == 2 ? 3 : 4;     // stages
 constexpr int kThreads = (kCW + 1) * 32;
 constexpr int kWin = 32;               // row-sum window (rows)
 
@@ -103,7 +107,7 @@ __device__ __forceinline__ void mma_stage(const double* __restrict__ sv, const d
     for (int j = 0; j < 2; ++j) {
       const int rr = 2 * q + j;
       const bool rv = !MASK || rr < nr;  // row present in this (partial) stage
-      double row = -(j == 0 ? d0 : d1);
+      double row = j == 0 ? d0 : d1;
       if (MASK && (gcol0 + cl == grow0 + rr || !rv)) row = 0.0;
       if (MODE == kModePapg) {
         const double c1 = sv[rr * kTCP + cl];
@@ -138,7 +142,7 @@ __device__ __forceinline__ void mma_stage(const double* __restrict__ sv, const d
 }
 
 template <int NN, int MODE>
-__global__ void __launch_bounds__(kThreads) sweep_mma_kernel(const SweepArgs a) {
+__global__ void __launch_bounds__(kThreads, kMinCtas) sweep_mma_kernel(const SweepArgs a) {
   constexpr int KS = ksteps<NN>();
   constexpr int FB = fblocks<NN>();
   constexpr int RQ = rec_pitch(NN);
