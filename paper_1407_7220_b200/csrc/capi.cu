@@ -48,6 +48,8 @@ struct cr_handle {
   double *k2part = nullptr, *k2sum = nullptr, *hist = nullptr;
   double *yout = nullptr, *xiout = nullptr;
   double *pw_u = nullptr, *pw_v = nullptr, *pw_part = nullptr, *pw_sum = nullptr;
+  double *gram = nullptr, *ps_sums = nullptr, *ps_part = nullptr;  // closed-form power step
+  bool sigma_by_sweep = false;  // CRB_SIGMA=sweep: O(N^2 n) power steps through the sweep
   double *consts = nullptr;  // {1, 1, 0}
   int *izero = nullptr;      // constant 0 (slot index / never halted)
   double *stage = nullptr;
@@ -238,8 +240,33 @@ cr_status sync_ctrl(cr_handle* h) {
   return CR_OK;
 }
 
-// one power step (operators.cpp:318-327); returns lambda and |u|
+// one power step in closed form (see kernels.cu K4'): replicated O(N n^2)
+// work, no pair sweep and no exchange
+cr_status power_step_struct(cr_handle* h, double norm_u, double* lambda, double* nu) {
+  PowerStructArgs a{};
+  a.u = h->pw_u;
+  a.v = h->pw_v;
+  a.norm_u = norm_u;
+  a.X = h->X;
+  a.gram = h->gram;
+  a.sums = h->ps_sums;
+  a.part = h->ps_part;
+  a.part2 = h->pw_part;
+  a.out2 = h->pw_sum;
+  a.N = h->N;
+  a.n = (int)h->n;
+  CUDA_TRY(launch_power_struct(a, h->st));
+  double host[2];
+  CUDA_TRY(cudaMemcpyAsync(host, h->pw_sum, 2 * sizeof(double), cudaMemcpyDeviceToHost, h->st));
+  CUDA_TRY(cudaStreamSynchronize(h->st));
+  *nu = std::sqrt(host[0]);
+  *lambda = host[1];
+  return CR_OK;
+}
+
+// one power step (operators.cpp:318-327) through the pair sweep; returns lambda and |u|
 cr_status power_step(cr_handle* h, double norm_u, double* lambda, double* nu) {
+  if (!h->sigma_by_sweep) return power_step_struct(h, norm_u, lambda, nu);
   PowerArgs pa{};
   pa.X = h->X;
   pa.u = h->pw_u;
@@ -386,6 +413,9 @@ cr_status cr_create(const double* Xh, const double* ybar_shifted, int64_t N, int
   ALLOC(h->pw_v, N * (n + 1));
   ALLOC(h->pw_part, (size_t)h->k2_blocks * 2);
   ALLOC(h->pw_sum, 2);
+  ALLOC(h->gram, n * n + n);
+  ALLOC(h->ps_sums, 2 + 2 * n);
+  ALLOC(h->ps_part, (size_t)h->k2_blocks * (2 + 2 * n));
   ALLOC(h->consts, 4);
   ALLOC(h->izero, 1);
   ALLOC(h->counter, 1);
@@ -427,6 +457,9 @@ cr_status cr_create(const double* Xh, const double* ybar_shifted, int64_t N, int
   CUDA_TRY(cudaMemsetAsync(h->izero, 0, sizeof(int), h->st));
   CUDA_TRY(cudaMemsetAsync(h->counter, 0, sizeof(unsigned int), h->st));
   CUDA_TRY(cudaMemsetAsync(h->ctrl_d, 0, sizeof(DevCtrl), h->st));
+  CUDA_TRY(launch_gram(h->X, N, (int)n, h->gram, h->st));
+  const char* sig = std::getenv("CRB_SIGMA");
+  h->sigma_by_sweep = sig && std::strcmp(sig, "sweep") == 0;
   CUDA_TRY(cudaStreamSynchronize(h->st));
   return CR_OK;
 }
@@ -440,7 +473,8 @@ void cr_destroy(cr_handle* h) {
   double* bufs[] = {h->X,       h->ybar,    h->rowrec,  h->colrec,   h->V[0],   h->V[1],
                     h->vpos[0], h->vpos[1], h->xbuf,    h->aggsave,  h->colpart, h->rowpart,
                     h->scalpart, h->k2part, h->k2sum,   h->hist,     h->yout,   h->xiout,
-                    h->pw_u,    h->pw_v,    h->pw_part, h->pw_sum,   h->consts, h->stage};
+                    h->pw_u,    h->pw_v,    h->pw_part, h->pw_sum,   h->consts, h->stage,
+                    h->gram,    h->ps_sums, h->ps_part};
   for (double* b : bufs)
     if (b) cudaFree(b);
   if (h->izero) cudaFree(h->izero);

@@ -110,9 +110,16 @@ def test_config1_full_2000_iterations(oracle):
     assert_parity(gpu_run(X, ys, **kw), o, hist_rtol=1e-8)
 
 
-def test_sigma_C_parity(oracle):
+@pytest.mark.parametrize("method", ["closed-form", "sweep"])
+def test_sigma_C_parity(oracle, monkeypatch, method):
+    """Power iteration on C^T C (operators.cpp:302-339): the default O(N n^2)
+    closed-form step and the O(N^2 n) pair-sweep step both reproduce the
+    oracle's sigma and iteration count."""
+    if method == "sweep":
+        monkeypatch.setenv("CRB_SIGMA", "sweep")
     for kind, N, n, pieces in [("sqnorm-uniform", 400, 5, 0), ("maxaffine-uniform", 300, 10, 20),
-                               ("lse-uniform", 250, 20, 50)]:
+                               ("lse-uniform", 250, 20, 50), ("quadratic", 333, 1, 0),
+                               ("exponential", 150, 24, 0)]:
         X, ys = instance(oracle, kind, N, n, 0.1, 3, pieces)
         so, ito, co = oracle.sigma_C(X)
         with crb.DualSolver(X, ys) as d:
