@@ -300,3 +300,22 @@ def test_cpp_dropin_binary(oracle, tmp_path):
     o = oracle_run(oracle, X, ys, max_iters=50, gap_norm_tol=-1.0, infeas_norm_tol=-1.0, sigma_C=s)
     assert iters == o.iters
     assert rel(theta, o.theta) <= TOL_THETA and rel(y, o.y) <= TOL_Y
+
+
+def test_nccl_attached_single_rank(oracle):
+    """The NCCL exchange path (in-graph allreduce + separate control launch) with
+    a one-rank communicator reproduces the unsharded iterates."""
+    X, ys = instance(oracle, "maxaffine-uniform", 300, 7, 0.1, 31, 9)
+    s, _, _ = oracle.sigma_C(X)
+    o = oracle_run(oracle, X, ys, max_iters=50, gap_norm_tol=-1.0, infeas_norm_tol=-1.0, sigma_C=s)
+    for graph_iters in (8, -1):
+        cfg = crb.PapgConfig(max_iters=50, gap_norm_tol=-1.0, infeas_norm_tol=-1.0, sigma_C=s,
+                             graph_iters=graph_iters)
+        with crb.DualSolver(X, ys) as d:
+            d.attach_nccl(crb.DualSolver.nccl_unique_id(), 0, 1)
+            d.begin(cfg)
+            done, stopped = d.iterate(1 << 30)
+            assert done == 50 and stopped
+            res, y, xi, hist = d.finish()
+            assert rel(d.theta(), o.theta) <= TOL_THETA
+            assert rel(y, o.y) <= TOL_Y
