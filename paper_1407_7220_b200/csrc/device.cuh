@@ -15,7 +15,7 @@
 //   rowrec    : N x RQ  (x_l[0..n-1], 1, y_l, 0...)
 //   colrec    : N x RQ  (-xi_l[0..n-1], -c_l, 1, 0...)   c_l = y_l - xi_l . x_l
 //               so that (C eta)_{l1 l2} = colrec[l2] . rowrec[l1] (the MMA
-//               residual), RQ = max(round_up(n+2, 4), round_up(n+1, 8)).
+//               residual), RQ = max(round_up(n+2, 4), round_up(n+1, 8)) + 2.
 #pragma once
 #include <cstdint>
 
@@ -23,8 +23,11 @@ namespace crb {
 
 constexpr int kMaxN = 24;    // templated register path covers n = 1..kMaxN
 
+// max(round_up(n+2, 4), round_up(n+1, 8)) + 2: the +2 makes the row pitch an odd
+// multiple of 16 B, so the MMA aggregation fragment reads (8 lanes per row, 4 rows)
+// are bank-conflict free and the residual fragment reads at most 2-way.
 __host__ __device__ constexpr int rec_pitch(int n) {
-  return ((n + 5) & ~3) > ((n + 8) & ~7) ? ((n + 5) & ~3) : ((n + 8) & ~7);
+  return (((n + 5) & ~3) > ((n + 8) & ~7) ? ((n + 5) & ~3) : ((n + 8) & ~7)) + 2;
 }
 constexpr int kScal = 4;     // sweep scalars: S_vv, S_vr, S_tr, S_nn
 constexpr int kK2Scal = 8;   // primal scalars, see primal_kernel
