@@ -126,6 +126,24 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
+def host_mem_available():
+    try:
+        for line in open("/proc/meminfo"):
+            if line.startswith("MemAvailable:"):
+                return int(line.split()[1]) * 1024
+    except OSError:
+        pass
+    return 0
+
+
+def cpu_feasible(cfg):
+    """BASELINE.md CPU-baseline rule: the oracle holds 4 N^2 doubles (theta1,
+    theta1_prev, theta2, C eta); skip when that exceeds 0.8 x MemAvailable."""
+    need = 4 * 8 * cfg["N"] ** 2
+    avail = host_mem_available()
+    return need <= 0.8 * avail, need, avail
+
+
 def cpu_oracle_rate(cfg, threads, k_lo=1, k_hi=4):
     """Oracle (CPU restatement of papg.cpp) per-iteration rate on the config:
     difference of two runs (k_lo, k_hi iterations) removes setup and the final
@@ -154,6 +172,12 @@ def run_reference(args):
         return 0
     cfg = workload(args.config, 1)
     threads = os.cpu_count() or 1
+    ok, need, avail = cpu_feasible(cfg)
+    if not ok:
+        print(json.dumps({"impl": "reference", "unavailable":
+                          f"CPU restatement needs {need / 1e9:.0f} GB (4 N^2 doubles) > 0.8 x "
+                          f"MemAvailable {avail / 1e9:.0f} GB (BASELINE.md feasibility rule)"}))
+        return 0
     k_hi = 1 + max(1, min(args.steps, 4))
     rate, spent, sample = cpu_oracle_rate(cfg, threads, 1, k_hi)
     line = {
@@ -285,7 +309,12 @@ def run_ours(args):
                 "loop_seconds": tr.loop_seconds, "gap_norm_tol": 1e-4, "infeas_norm_tol": 0.1}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    ok, need, avail = cpu_feasible(cfg)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and not ok:
+        cpu = {"value": None, "unit": "pair-updates/s", "cores": os.cpu_count(), "kind": "port",
+               "sample": f"skipped: needs {need / 1e9:.0f} GB > 0.8 x MemAvailable "
+                         f"{avail / 1e9:.0f} GB"}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and ok:
         threads = os.cpu_count() or 1
         rate, spent, sample = cpu_oracle_rate(cfg, threads)
         cpu = {"value": rate, "unit": "pair-updates/s", "cores": threads, "kind": "port",
