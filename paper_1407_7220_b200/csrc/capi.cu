@@ -22,6 +22,7 @@
 #include "device.cuh"
 #include "host.hpp"
 #include "kernels.cuh"
+#include "small.cuh"
 
 using namespace crb;
 
@@ -35,6 +36,11 @@ struct cr_handle {
   int S = 0;            // column strips
   int T = 0;            // sweep CTA column tiles = row-sum slices
   int variant = 0;      // kSweepDfma / kSweepMma
+  // persistent small-N loop (small.cu)
+  bool small_mode = false;
+  SmallInfo ks{};
+  int small_grid = 0, small_S = 0, small_P = 0;
+  double *s_colpart = nullptr, *s_rowpart = nullptr, *s_scalpart = nullptr, *s_k2part = nullptr;
   int G = 0;            // sweep CTAs (one persistent wave)
   int maxspan = 0;      // tiles one CTA's unit range can touch
   long long U = 0;      // (tile, row) units per CTA
@@ -477,6 +483,8 @@ void cr_destroy(cr_handle* h) {
                     h->gram,    h->ps_sums, h->ps_part};
   for (double* b : bufs)
     if (b) cudaFree(b);
+  for (double* b : {h->s_colpart, h->s_rowpart, h->s_scalpart, h->s_k2part})
+    if (b) cudaFree(b);
   if (h->izero) cudaFree(h->izero);
   if (h->counter) cudaFree(h->counter);
   if (h->ctrl_d) cudaFree(h->ctrl_d);
@@ -679,6 +687,44 @@ cr_status cr_papg_begin(cr_handle* h, const cr_papg_config* cfg, const double* t
     CUDA_TRY(launch_warm_ctrl(h->ctrl_d, h->xbuf + N * (h->n + 2), pos_sq, h->st));
   }
 
+  // small N (V, V' L2-resident, one GPU): one persistent cooperative launch runs
+  // many iterations (small.cu). CRB_SMALL=0 disables, CRB_SMALL=1 forces.
+  {
+    const char* sm = std::getenv("CRB_SMALL");
+    const double vbytes2 = 2.0 * 8.0 * (double)h->R * (double)h->ld;
+    bool want = h->comm == nullptr && cfg->graph_iters == 0 && vbytes2 <= 48e6;
+    if (sm && sm[0] == '0') want = false;
+    if (sm && sm[0] == '1' && h->comm == nullptr && h->R == h->N) want = true;
+    h->small_mode = false;
+    if (want) {
+      h->ks = small_loop_info((int)h->n);
+      int sms = 148;
+      CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
+      const int bps = std::min(h->ks.max_blocks_per_sm, 2);
+      if (h->ks.fn && bps >= 1) {
+        h->small_grid = sms * bps;
+        h->small_S = (int)((h->N + 31) / 32);
+        const long long warps = (long long)h->small_grid * (h->ks.threads / 32);
+        h->small_P = (int)std::max<long long>(1, std::min<long long>(h->N, warps / h->small_S));
+        for (double* b : {h->s_colpart, h->s_rowpart, h->s_scalpart, h->s_k2part})
+          if (b) cudaFree(b);
+        h->s_colpart = h->s_rowpart = h->s_scalpart = h->s_k2part = nullptr;
+        cudaError_t e = cudaSuccess;
+        if (e == cudaSuccess)
+          e = dalloc(&h->s_colpart, (size_t)h->small_P * h->ld * (h->n + 1));
+        if (e == cudaSuccess) e = dalloc(&h->s_rowpart, (size_t)h->small_S * h->N);
+        if (e == cudaSuccess)
+          e = dalloc(&h->s_scalpart, (size_t)h->small_grid * kScal);
+        if (e == cudaSuccess) e = dalloc(&h->s_k2part, (size_t)h->small_grid * kK2Scal);
+        if (e != cudaSuccess) {
+          cudaGetLastError();
+          return fail(h, CR_ENOMEM, "small-N buffers");
+        }
+        h->small_mode = true;
+      }
+    }
+  }
+
   // batch size: graphs when an iteration is short, direct launches otherwise
   if (cfg->graph_iters > 0) {
     h->graph_iters = cfg->graph_iters;
@@ -688,7 +734,7 @@ cr_status cr_papg_begin(cr_handle* h, const cr_papg_config* cfg, const double* t
     const double est_us = 24.0 * (double)h->R * (double)h->ld / 5.0e6 + 12.0;
     h->graph_iters = est_us > 300.0 ? 0 : (int)std::min(256.0, std::ceil(2000.0 / est_us));
   }
-  if (h->graph_iters > 0) {
+  if (h->graph_iters > 0 && !h->small_mode) {
     const cr_status s = build_graph(h);
     if (s != CR_OK) return s;
   }
@@ -709,6 +755,67 @@ cr_status cr_papg_iterate(cr_handle* h, int64_t max_steps, int64_t* done, int32_
   if (pause < ell0) pause = LLONG_MAX;
   cr_status s = set_pause(h, pause);
   if (s != CR_OK) return s;
+  if (h->small_mode) {  // one persistent launch, halts on termination or pause
+    if (h->ctrl_h->stopped || max_steps == 0) {
+      h->last_seconds = 0;
+      h->last_launches = 0;
+      h->last_sweep_seconds = 0;
+    } else {
+      SmallArgs sa{};
+      sa.pa = primal_args(h, 0);
+      sa.V0 = h->V[0];
+      sa.V1 = h->V[1];
+      sa.colpart = h->s_colpart;
+      sa.rowpart = h->s_rowpart;
+      sa.scalpart = h->s_scalpart;
+      sa.k2part = h->s_k2part;
+      sa.xbuf = h->xbuf;
+      sa.k2sum = h->k2sum;
+      sa.hist = h->hist;
+      sa.ctrl = h->ctrl_d;
+      sa.N = h->N;
+      sa.ld = h->ld;
+      sa.max_iters = max_steps;
+      sa.S = h->small_S;
+      sa.P = h->small_P;
+      unsigned long long* trace = nullptr;
+      if (std::getenv("CRB_TRACE")) {
+        CUDA_TRY(cudaMalloc(&trace, 64 * 8 * sizeof(unsigned long long)));
+        CUDA_TRY(cudaMemsetAsync(trace, 0, 64 * 8 * sizeof(unsigned long long), h->st));
+      }
+      sa.trace = trace;
+      const auto wall0 = std::chrono::steady_clock::now();
+      CUDA_TRY(cudaEventRecord(h->ev_start, h->st));
+      CUDA_TRY(launch_small_loop(h->ks, sa, h->small_grid, h->st));
+      CUDA_TRY(cudaEventRecord(h->ev_end, h->st));
+      s = sync_ctrl(h);
+      if (s != CR_OK) return s;
+      float ms = 0;
+      CUDA_TRY(cudaEventElapsedTime(&ms, h->ev_start, h->ev_end));
+      h->last_seconds = ms * 1e-3;
+      h->last_launches = 1;
+      h->last_sweep_seconds = 0;
+      if (trace) {  // dev aid: mean phase durations of the first iterations
+        unsigned long long tb[64 * 8];
+        CUDA_TRY(cudaMemcpy(tb, trace, sizeof(tb), cudaMemcpyDeviceToHost));
+        double acc[7] = {0};
+        int cnt = 0;
+        for (int it = 1; it < 64 && tb[it * 8 + 7] != 0; ++it, ++cnt)
+          for (int k = 0; k < 7; ++k) acc[k] += (double)(tb[it * 8 + k + 1] - tb[it * 8 + k]);
+        std::fprintf(stderr, "small-loop phases (ns, mean of %d): A %.0f syncA %.0f B %.0f syncB %.0f C %.0f ctl %.0f syncC %.0f\n",
+                     cnt, acc[0] / cnt, acc[1] / cnt, acc[2] / cnt, acc[3] / cnt, acc[4] / cnt,
+                     acc[5] / cnt, acc[6] / cnt);
+        cudaFree(trace);
+      }
+      h->loop_seconds +=
+          std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();
+    }
+    if (done) *done = h->ctrl_h->ell;
+    if (stopped) *stopped = h->ctrl_h->stopped;
+    if (h->ctrl_h->stopped && h->ctrl_h->reason == 3)
+      return fail(h, CR_ENONFINITE, "papg: non-finite dual gradient");
+    return CR_OK;
+  }
   const bool timed_sweeps = h->graph_iters == 0;
   const int per_unit = h->graph_iters > 0 ? h->graph_iters : 4;
   int64_t enq_iters = 0;

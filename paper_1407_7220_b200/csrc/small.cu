@@ -1,0 +1,255 @@
+// small.cu -- persistent cooperative dual loop for small N (V, V' L2-resident).
+//
+// For N ~ 1e3 (BASELINE config 1: 24 MB per iteration, L2-resident) a dual
+// iteration is a few microseconds of work and the per-kernel path is bound by
+// launch and pipeline-fill latency. Here one cooperative launch runs many
+// iterations of papg.cpp:176-263; grid-wide barriers separate the phases:
+//   A  primal closed form of every point (K2, iteration.cuh)
+//   B  pair sweep: a warp owns 32 columns (one per lane) and a chunk of rows
+//   C  fixed-order reduction of the partials; block 0 also reduces the
+//      scalars and runs the control step (papg.cpp:187-262)
+// Data produced inside the launch is read with L2-coherent loads (ld.cg).
+// Same math, same partial layout and same fixed-order sums as the per-kernel
+// path; results are deterministic.
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+
+#include "device.cuh"
+#include "iteration.cuh"
+#include "kernels.cuh"
+#include "small.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace crb {
+
+namespace {
+
+constexpr int kSBlock = 256;
+
+template <int NN>
+__global__ void __launch_bounds__(kSBlock) small_loop_kernel(const SmallArgs a) {
+  constexpr int RP = rec_pitch(NN);
+  cg::grid_group grid = cg::this_grid();
+  const long long tid = (long long)blockIdx.x * kSBlock + threadIdx.x;
+  const long long nthreads = (long long)gridDim.x * kSBlock;
+  const int lane = threadIdx.x & 31;
+  const long long gwarp = tid >> 5;
+  const long long nwarps = nthreads >> 5;
+  const long long N = a.N;
+  DevCtrl* c = a.ctrl;
+  const bool tr0 = a.trace != nullptr && blockIdx.x == 0 && threadIdx.x == 0;
+  auto stamp = [&](long long it, int k) {
+    if (tr0 && it < 64) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      a.trace[it * 8 + k] = t;
+    }
+  };
+
+  for (long long it = 0; it < a.max_iters; ++it) {
+    stamp(it, 0);
+    if (__ldcg(&c->halt)) break;  // written before the last grid barrier
+    const int cur = __ldcg(&c->cur);
+    const double s_c = __ldcg(&c->s_cur), s_p = __ldcg(&c->s_prev), beta = __ldcg(&c->beta);
+    const double* vposc = cur ? a.pa.vpos1 : a.pa.vpos0;
+    double* vposp = cur ? a.pa.vpos0 : a.pa.vpos1;
+
+    // ---- A: primal closed form (K2)
+    {
+      double acc[kK2Scal];
+#pragma unroll
+      for (int w = 0; w < kK2Scal; ++w) acc[w] = 0.0;
+      for (long long l = tid; l < N; l += nthreads)
+        primal_point<NN>(a.pa, l, s_c, s_p, beta, vposc, vposp, acc);
+      block_reduce_store<kK2Scal, kSBlock>(acc, a.k2part + (long long)blockIdx.x * kK2Scal);
+    }
+    stamp(it, 1);
+    grid.sync();
+    stamp(it, 2);
+
+    // ---- B: pair sweep
+    {
+      const double* Vc = cur ? a.V1 : a.V0;
+      double* Vp = cur ? a.V0 : a.V1;
+      const double invL = a.pa.invL;
+      const bool unit = (s_c == 1.0) && (s_p == 1.0);
+      double wsc[kScal] = {0.0, 0.0, 0.0, 0.0};
+      for (long long w = gwarp; w < (long long)a.S * a.P; w += nwarps) {
+        const int strip = (int)(w % a.S);
+        const int chunk = (int)(w / a.S);
+        const long long rlo = N * chunk / a.P, rhi = N * (chunk + 1) / a.P;
+        const long long col = (long long)strip * 32 + lane;
+        const bool valid = col < N;
+        const double* rec = a.pa.colrec + (valid ? col : 0) * RP;  // (-xi, -c, 1)
+        double xi[NN], acc[NN + 1];
+        const double cc = valid ? __ldcg(rec + NN) : 0.0;
+#pragma unroll
+        for (int j = 0; j < NN; ++j) xi[j] = valid ? __ldcg(rec + j) : 0.0;
+#pragma unroll
+        for (int j = 0; j <= NN; ++j) acc[j] = 0.0;
+        double vv = 0.0, vr = 0.0, tr = 0.0, nn = 0.0;
+        // U rows in flight: all loads of a batch are issued before its math
+        constexpr int U = (NN + 3) <= 8 ? 4 : ((NN + 3) <= 16 ? 2 : 1);
+        for (long long r0 = rlo; r0 < rhi; r0 += U) {
+          double xb[U][NN], yb[U], cb[U], pb[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const long long r = r0 + u < rhi ? r0 + u : rhi - 1;
+            const double* xr = a.pa.rowrec + r * RP;  // (x, 1, y)
+#pragma unroll
+            for (int j = 0; j < NN; ++j) xb[u][j] = __ldcg(xr + j);
+            yb[u] = __ldcg(xr + NN + 1);
+            cb[u] = __ldcg(Vc + r * a.ld + col);
+            pb[u] = __ldcg(Vp + r * a.ld + col);
+          }
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const long long r = r0 + u;
+            if (r >= rhi) break;
+            double row = yb[u] + cc;
+#pragma unroll
+            for (int j = 0; j < NN; ++j) row = fma(xb[u][j], xi[j], row);
+            if (!valid || col == r) row = 0.0;
+            const double c1 = cb[u], p1 = pb[u];
+            double th2;
+            if (unit) {
+              th2 = fma(beta, c1 - p1, c1);
+            } else {
+              const double th1 = s_c * c1;
+              th2 = fma(beta, th1 - s_p * p1, th1);
+            }
+            const double uu = fma(-row, invL, th2);
+            const double v = uu > 0.0 ? uu : 0.0;
+            __stcg(Vp + r * a.ld + col, v);
+            vv = fma(v, v, vv);
+            vr = fma(v, row, vr);
+            tr = fma(th2, row, tr);
+            const double m = row < 0.0 ? row : 0.0;
+            nn = fma(m, m, nn);
+            acc[0] += v;
+#pragma unroll
+            for (int j = 0; j < NN; ++j) acc[1 + j] = fma(v, xb[u][j], acc[1 + j]);
+            double rs = v;  // fixed butterfly over the strip's 32 columns
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) rs += __shfl_xor_sync(0xffffffffu, rs, o);
+            if (lane == 0) __stcg(a.rowpart + r * a.S + strip, rs);  // [N][S]
+          }
+        }
+        // [ld][n+1][P]: the P partials of one column entry are contiguous
+        double* dst = a.colpart + (col * (NN + 1)) * a.P + chunk;
+#pragma unroll
+        for (int j = 0; j <= NN; ++j) __stcg(dst + (long long)j * a.P, acc[j]);
+        wsc[0] += vv;
+        wsc[1] += vr;
+        wsc[2] += tr;
+        wsc[3] += nn;
+      }
+      // scalars: lanes, then the block's warps, in a fixed order -> one record per block
+#pragma unroll
+      for (int k = 0; k < kScal; ++k) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) wsc[k] += __shfl_xor_sync(0xffffffffu, wsc[k], o);
+      }
+      __shared__ double bsc[kSBlock / 32][kScal];
+      if (lane == 0) {
+#pragma unroll
+        for (int k = 0; k < kScal; ++k) bsc[threadIdx.x >> 5][k] = wsc[k];
+      }
+      __syncthreads();
+      if (threadIdx.x < kScal) {
+        double t = 0.0;
+#pragma unroll
+        for (int w8 = 0; w8 < kSBlock / 32; ++w8) t += bsc[w8][threadIdx.x];
+        __stcg(a.scalpart + (long long)blockIdx.x * kScal + threadIdx.x, t);
+      }
+    }
+    stamp(it, 3);
+    grid.sync();
+    stamp(it, 4);
+
+    // ---- C: fixed-order reduction (+ scalars and control in block 0)
+    {
+      // one warp per output element: lanes split the partials, fixed butterfly
+      const long long ncol = N * (NN + 1);
+      for (long long e = gwarp; e < ncol + N; e += nwarps) {
+        double s = 0.0;
+        if (e < ncol) {
+          const double* src = a.colpart + e * a.P;  // contiguous over the chunks
+          for (int p = lane; p < a.P; p += 32) s += __ldcg(src + p);
+        } else {
+          const double* src = a.rowpart + (e - ncol) * a.S;  // contiguous over the strips
+          for (int st = lane; st < a.S; st += 32) s += __ldcg(src + st);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) __stcg(a.xbuf + (e < ncol ? N + e : e - ncol), s);
+      }
+      stamp(it, 5);
+      if (blockIdx.x == 0) {
+        double v[kScal + kK2Scal];
+#pragma unroll
+        for (int w = 0; w < kScal + kK2Scal; ++w) v[w] = 0.0;
+        const long long nw = gridDim.x;  // one scalar record per block
+        for (long long i = threadIdx.x; i < nw; i += kSBlock) {
+#pragma unroll
+          for (int w = 0; w < kScal; ++w) v[w] += __ldcg(a.scalpart + i * kScal + w);
+        }
+        for (long long i = threadIdx.x; i < gridDim.x; i += kSBlock) {
+#pragma unroll
+          for (int w = 0; w < kK2Scal; ++w) v[kScal + w] += __ldcg(a.k2part + i * kK2Scal + w);
+        }
+        __shared__ double out[kScal + kK2Scal];
+        block_reduce_store<kScal + kK2Scal, kSBlock>(v, out);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          double* scal = a.xbuf + N + ncol;
+          for (int w = 0; w < kScal; ++w) scal[w] = out[w];
+          for (int w = 0; w < kK2Scal; ++w) a.k2sum[w] = out[kScal + w];
+          if (!c->halt) {
+            control_step(c, scal, a.k2sum, a.hist);
+          }
+          __threadfence();
+        }
+      }
+    }
+    stamp(it, 6);
+    grid.sync();
+    stamp(it, 7);
+  }
+}
+
+template <int NN>
+SmallInfo small_info_for() {
+  SmallInfo inf{};
+  inf.fn = (const void*)small_loop_kernel<NN>;
+  inf.threads = kSBlock;
+  int bps = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, inf.fn, kSBlock, 0) != cudaSuccess)
+    bps = 0;
+  inf.max_blocks_per_sm = bps;
+  return inf;
+}
+
+template <int... Ns> struct STable;
+template <int N0, int... Ns> struct STable<N0, Ns...> {
+  static SmallInfo info(int n) { return n == N0 ? small_info_for<N0>() : STable<Ns...>::info(n); }
+};
+template <> struct STable<> {
+  static SmallInfo info(int) { return SmallInfo{}; }
+};
+using AllS = STable<1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16, 17, 18, 19, 20, 21, 22,
+                    23, 24>;
+
+}  // namespace
+
+SmallInfo small_loop_info(int n) { return AllS::info(n); }
+
+cudaError_t launch_small_loop(const SmallInfo& info, const SmallArgs& a, int grid,
+                              cudaStream_t s) {
+  void* args[] = {const_cast<SmallArgs*>(&a)};
+  return cudaLaunchCooperativeKernel(info.fn, dim3((unsigned)grid), dim3(info.threads), args, 0,
+                                     s);
+}
+
+}  // namespace crb

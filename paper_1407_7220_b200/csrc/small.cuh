@@ -1,0 +1,38 @@
+// small.cuh -- persistent cooperative dual loop for small N (small.cu)
+#pragma once
+#include <cuda_runtime.h>
+
+#include "device.cuh"
+#include "kernels.cuh"
+
+namespace crb {
+
+struct SmallArgs {
+  PrimalArgs pa;       // K2 arguments (mode 0): records, aggregates, vpos, k2part
+  double* V0;
+  double* V1;
+  double* colpart;     // [ld][n+1][P]
+  double* rowpart;     // [N][S]
+  double* scalpart;    // [grid][kScal]
+  double* k2part;      // [grid][kK2Scal]
+  double* xbuf;        // aggregates of the newest V (also read by K2 as aggc)
+  double* k2sum;
+  double* hist;
+  DevCtrl* ctrl;
+  long long N, ld;
+  long long max_iters; // iterations this launch may run (halts earlier on termination)
+  int S, P;            // 32-column strips, row chunks
+  unsigned long long* trace;  // optional: block 0 phase timestamps (CRB_TRACE), 8 per iteration
+};
+
+struct SmallInfo {
+  const void* fn;
+  int threads;
+  int max_blocks_per_sm;
+};
+
+SmallInfo small_loop_info(int n);
+cudaError_t launch_small_loop(const SmallInfo& info, const SmallArgs& a, int grid,
+                              cudaStream_t s);
+
+}  // namespace crb

@@ -90,10 +90,16 @@ def test_golden_fixtures():
         assert rel(r["xi"], g[f"xi{i}"].reshape(-1)) <= 1e-8
 
 
-@pytest.mark.parametrize("variant", ["dfma", "mma"])
+@pytest.mark.parametrize("variant", ["dfma", "mma", "small"])
 @pytest.mark.parametrize("n", list(range(1, 25)))
-def test_every_n_both_sweep_variants(oracle, monkeypatch, variant, n):
-    monkeypatch.setenv("CRB_SWEEP", variant)
+def test_every_n_every_sweep_path(oracle, monkeypatch, variant, n):
+    """Every n on each sweep implementation: the TMA-pipelined DFMA and DMMA
+    kernels (per-kernel iteration) and the persistent small-N loop."""
+    if variant == "small":
+        monkeypatch.setenv("CRB_SMALL", "1")
+    else:
+        monkeypatch.setenv("CRB_SMALL", "0")
+        monkeypatch.setenv("CRB_SWEEP", variant)
     N = 67 + 3 * n  # ragged: not a multiple of any strip or tile width
     X, ys = instance(oracle, "maxaffine-uniform", N, n, 0.1, 100 + n, 6)
     s, _, _ = oracle.sigma_C(X)
@@ -101,8 +107,11 @@ def test_every_n_both_sweep_variants(oracle, monkeypatch, variant, n):
     assert_parity(gpu_run(X, ys, **kw), oracle_run(oracle, X, ys, **kw))
 
 
-def test_config1_full_2000_iterations(oracle):
-    """BASELINE config 1: N=1000, n=5, |x|^2 + U[-0.1, 0.1] noise, 2000 iterations."""
+@pytest.mark.parametrize("small", ["1", "0"])
+def test_config1_full_2000_iterations(oracle, monkeypatch, small):
+    """BASELINE config 1: N=1000, n=5, |x|^2 + U[-0.1, 0.1] noise, 2000 iterations
+    (persistent small-N loop and per-kernel path)."""
+    monkeypatch.setenv("CRB_SMALL", small)
     X, ys = instance(oracle, "sqnorm-uniform", 1000, 5, 0.1, 1)
     s, _, _ = oracle.sigma_C(X)
     kw = dict(max_iters=2000, gap_norm_tol=-1.0, infeas_norm_tol=-1.0, sigma_C=s)
