@@ -54,7 +54,8 @@ struct cr_handle {
   double *k2part = nullptr, *k2sum = nullptr, *hist = nullptr;
   double *yout = nullptr, *xiout = nullptr;
   double *pw_u = nullptr, *pw_v = nullptr, *pw_part = nullptr, *pw_sum = nullptr;
-  double *gram = nullptr, *ps_sums = nullptr, *ps_part = nullptr;  // closed-form power step
+  double *gram = nullptr, *ps_part = nullptr, *ps_part2 = nullptr, *ps_state = nullptr;
+  int power_grid = 0;  // closed-form power iteration (power.cu)
   bool sigma_by_sweep = false;  // CRB_SIGMA=sweep: O(N^2 n) power steps through the sweep
   double *consts = nullptr;  // {1, 1, 0}
   int *izero = nullptr;      // constant 0 (slot index / never halted)
@@ -106,9 +107,23 @@ cr_status fail(cr_handle* h, cr_status s, const std::string& what) {
       return fail(h, CR_ENCCL, std::string(#call) + ": " + ncclGetErrorString(r_));      \
   } while (0)
 
+// Device buffers come from the device's stream-ordered memory pool, which is
+// told to keep freed memory: a service that creates a handle per solve reuses
+// the mapping instead of paying cudaMalloc/cudaFree of gigabytes each time.
+cudaStream_t g_alloc_stream = nullptr;  // stream of the handle being created
 template <typename T>
 cudaError_t dalloc(T** p, size_t count) {
-  return cudaMalloc((void**)p, (count ? count : 1) * sizeof(T));
+  return cudaMallocAsync((void**)p, (count ? count : 1) * sizeof(T), g_alloc_stream);
+}
+void dfree(void* p, cudaStream_t s) {
+  if (p) cudaFreeAsync(p, s);
+}
+void keep_pool_memory(int device) {
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
 }
 
 int64_t payload_len(const cr_handle* h) { return h->N * (h->n + 2) + kScal; }
@@ -246,33 +261,8 @@ cr_status sync_ctrl(cr_handle* h) {
   return CR_OK;
 }
 
-// one power step in closed form (see kernels.cu K4'): replicated O(N n^2)
-// work, no pair sweep and no exchange
-cr_status power_step_struct(cr_handle* h, double norm_u, double* lambda, double* nu) {
-  PowerStructArgs a{};
-  a.u = h->pw_u;
-  a.v = h->pw_v;
-  a.norm_u = norm_u;
-  a.X = h->X;
-  a.gram = h->gram;
-  a.sums = h->ps_sums;
-  a.part = h->ps_part;
-  a.part2 = h->pw_part;
-  a.out2 = h->pw_sum;
-  a.N = h->N;
-  a.n = (int)h->n;
-  CUDA_TRY(launch_power_struct(a, h->st));
-  double host[2];
-  CUDA_TRY(cudaMemcpyAsync(host, h->pw_sum, 2 * sizeof(double), cudaMemcpyDeviceToHost, h->st));
-  CUDA_TRY(cudaStreamSynchronize(h->st));
-  *nu = std::sqrt(host[0]);
-  *lambda = host[1];
-  return CR_OK;
-}
-
 // one power step (operators.cpp:318-327) through the pair sweep; returns lambda and |u|
 cr_status power_step(cr_handle* h, double norm_u, double* lambda, double* nu) {
-  if (!h->sigma_by_sweep) return power_step_struct(h, norm_u, lambda, nu);
   PowerArgs pa{};
   pa.X = h->X;
   pa.u = h->pw_u;
@@ -360,6 +350,8 @@ cr_status cr_create(const double* Xh, const double* ybar_shifted, int64_t N, int
   h->cfg.gamma = gamma;
   CUDA_TRY(cudaSetDevice(device));
   CUDA_TRY(cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking));
+  keep_pool_memory(device);
+  g_alloc_stream = h->st;
   // sweep variant (measured on B200, profiles/): CUDA-core DFMA for small n,
   // DMMA tensor cores once the two rank-n contractions dominate the issue slots.
   // CRB_SWEEP=dfma|mma overrides.
@@ -419,9 +411,11 @@ cr_status cr_create(const double* Xh, const double* ybar_shifted, int64_t N, int
   ALLOC(h->pw_v, N * (n + 1));
   ALLOC(h->pw_part, (size_t)h->k2_blocks * 2);
   ALLOC(h->pw_sum, 2);
+  h->power_grid = power_loop_grid(sms);
   ALLOC(h->gram, n * n + n);
-  ALLOC(h->ps_sums, 2 + 2 * n);
-  ALLOC(h->ps_part, (size_t)h->k2_blocks * (2 + 2 * n));
+  ALLOC(h->ps_part, (size_t)h->power_grid * (2 + 2 * n));
+  ALLOC(h->ps_part2, (size_t)h->power_grid * 2);
+  ALLOC(h->ps_state, 4);
   ALLOC(h->consts, 4);
   ALLOC(h->izero, 1);
   ALLOC(h->counter, 1);
@@ -432,7 +426,7 @@ cr_status cr_create(const double* Xh, const double* ybar_shifted, int64_t N, int
     return fail(h, CR_ENOMEM, std::string("device allocation failed: ") + cudaGetErrorString(e));
   }
   h->stage_elems = std::min<int64_t>((int64_t)1 << 25, h->R * (N - 1) + N);  // <= 256 MB
-  if (cudaMalloc(&h->stage, (size_t)h->stage_elems * sizeof(double)) != cudaSuccess) {
+  if (dalloc(&h->stage, (size_t)h->stage_elems) != cudaSuccess) {
     cudaGetLastError();
     return fail(h, CR_ENOMEM, "stage allocation failed");
   }
@@ -480,14 +474,13 @@ void cr_destroy(cr_handle* h) {
                     h->vpos[0], h->vpos[1], h->xbuf,    h->aggsave,  h->colpart, h->rowpart,
                     h->scalpart, h->k2part, h->k2sum,   h->hist,     h->yout,   h->xiout,
                     h->pw_u,    h->pw_v,    h->pw_part, h->pw_sum,   h->consts, h->stage,
-                    h->gram,    h->ps_sums, h->ps_part};
-  for (double* b : bufs)
-    if (b) cudaFree(b);
-  for (double* b : {h->s_colpart, h->s_rowpart, h->s_scalpart, h->s_k2part})
-    if (b) cudaFree(b);
-  if (h->izero) cudaFree(h->izero);
-  if (h->counter) cudaFree(h->counter);
-  if (h->ctrl_d) cudaFree(h->ctrl_d);
+                    h->gram,    h->ps_part, h->ps_part2, h->ps_state};
+  for (double* b : bufs) dfree(b, h->st);
+  for (double* b : {h->s_colpart, h->s_rowpart, h->s_scalpart, h->s_k2part}) dfree(b, h->st);
+  dfree(h->izero, h->st);
+  dfree(h->counter, h->st);
+  dfree(h->ctrl_d, h->st);
+  if (h->st) cudaStreamSynchronize(h->st);
   if (h->ctrl_h) cudaFreeHost(h->ctrl_h);
   if (h->ctrl_poll) cudaFreeHost(h->ctrl_poll);
   if (h->pause_h) cudaFreeHost(h->pause_h);
@@ -538,6 +531,30 @@ cr_status cr_sigma_C(cr_handle* h, double tol, int32_t max_iters, double* sigma,
   for (double& x : v) x /= nv;
   CUDA_TRY(cudaMemcpyAsync(h->pw_u, v.data(), sizeof(double) * cols, cudaMemcpyHostToDevice,
                            h->st));
+  if (!h->sigma_by_sweep) {  // whole power iteration in one cooperative launch
+    PowerLoopArgs pa{};
+    pa.u = h->pw_u;
+    pa.v = h->pw_v;
+    pa.X = h->X;
+    pa.gram = h->gram;
+    pa.part = h->ps_part;
+    pa.part2 = h->ps_part2;
+    pa.state = h->ps_state;
+    pa.N = h->N;
+    pa.n = (int)h->n;
+    pa.max_iters = max_iters;
+    pa.tol = tol;
+    CUDA_TRY(launch_power_loop(pa, h->power_grid, h->st));
+    double st[3];
+    CUDA_TRY(cudaMemcpyAsync(st, h->ps_state, sizeof(st), cudaMemcpyDeviceToHost, h->st));
+    CUDA_TRY(cudaStreamSynchronize(h->st));
+    *sigma = st[0];
+    *iters = (int32_t)st[1];
+    *converged = (int32_t)st[2];
+    h->sigma_seconds =
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    return CR_OK;
+  }
   double norm_u = 1.0;  // v = u / 1 on the first step
   double lambda_prev = 0;
   *converged = 1;
@@ -603,10 +620,11 @@ cr_status cr_papg_begin(cr_handle* h, const cr_papg_config* cfg, const double* t
   // history buffer
   const int64_t want_hist = cfg->record_history ? std::min<int64_t>(cfg->max_iters, 4000000) : 0;
   if (want_hist > h->hist_cap) {
-    if (h->hist) cudaFree(h->hist);
+    dfree(h->hist, h->st);
     h->hist = nullptr;
     h->hist_cap = 0;
-    if (cudaMalloc(&h->hist, sizeof(double) * 8 * want_hist) != cudaSuccess) {
+    g_alloc_stream = h->st;
+    if (dalloc(&h->hist, (size_t)(8 * want_hist)) != cudaSuccess) {
       cudaGetLastError();
       return fail(h, CR_ENOMEM, "history allocation failed");
     }
@@ -707,8 +725,9 @@ cr_status cr_papg_begin(cr_handle* h, const cr_papg_config* cfg, const double* t
         const long long warps = (long long)h->small_grid * (h->ks.threads / 32);
         h->small_P = (int)std::max<long long>(1, std::min<long long>(h->N, warps / h->small_S));
         for (double* b : {h->s_colpart, h->s_rowpart, h->s_scalpart, h->s_k2part})
-          if (b) cudaFree(b);
+          dfree(b, h->st);
         h->s_colpart = h->s_rowpart = h->s_scalpart = h->s_k2part = nullptr;
+        g_alloc_stream = h->st;
         cudaError_t e = cudaSuccess;
         if (e == cudaSuccess)
           e = dalloc(&h->s_colpart, (size_t)h->small_P * h->ld * (h->n + 1));
@@ -821,14 +840,6 @@ cr_status cr_papg_iterate(cr_handle* h, int64_t max_steps, int64_t* done, int32_
   int64_t enq_iters = 0;
   int64_t units = 0;
   bool halted = h->ctrl_h->stopped || max_steps == 0;
-  if (timed_sweeps) {
-    const size_t need = (size_t)2 * (size_t)std::min<int64_t>(max_steps, 1 << 16);
-    while (h->ev_sweep.size() < need) {
-      cudaEvent_t e;
-      CUDA_TRY(cudaEventCreate(&e));
-      h->ev_sweep.push_back(e);
-    }
-  }
   int64_t timed_pairs = 0;
   CUDA_TRY(cudaEventRecord(h->ev_start, h->st));
   const auto wall0 = std::chrono::steady_clock::now();
@@ -838,7 +849,12 @@ cr_status cr_papg_iterate(cr_handle* h, int64_t max_steps, int64_t* done, int32_
     } else {
       for (int i = 0; i < per_unit && enq_iters + i < max_steps; ++i) {
         cudaEvent_t a = nullptr, b = nullptr;
-        if (timed_sweeps && (size_t)(2 * timed_pairs + 1) < h->ev_sweep.size()) {
+        if (timed_sweeps && timed_pairs < (1 << 16)) {  // event pairs created on demand
+          while (h->ev_sweep.size() < (size_t)(2 * timed_pairs + 2)) {
+            cudaEvent_t e;
+            CUDA_TRY(cudaEventCreate(&e));
+            h->ev_sweep.push_back(e);
+          }
           a = h->ev_sweep[2 * timed_pairs];
           b = h->ev_sweep[2 * timed_pairs + 1];
           ++timed_pairs;

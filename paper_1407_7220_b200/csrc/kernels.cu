@@ -189,128 +189,6 @@ __global__ void __launch_bounds__(kPBlock) power_post_kernel(const PowerArgs a) 
   block_reduce_store<1, kPBlock>(acc, a.part + (long long)blockIdx.x * 2 + 1);
 }
 
-// ---- K4': sigma_max(C) power step in closed form ---------------------------
-// C^T C has O(N n^2) structure: with a = v_y, b_l = v_xi[l], c_l = a_l - b_l.x_l
-// and w(l1, l2) = a_l1 - c_l2 - b_l2.x_l1 (operators.cpp:143-147),
-//   sum_{l2 != l} w(l, l2) = (N-1) a_l - (Cs - c_l) - (B - b_l).x_l
-//   sum_{l1 != l} w(l1, l) = (A - a_l) - (N-1) c_l - b_l.(s - x_l)
-//   sum_{l1 != l} w(l1, l) x_l1 = (AX - a_l x_l) - c_l (s - x_l) - (S - x_l x_l^T) b_l
-// with A = sum a, Cs = sum c, B = sum b, AX = sum a x, s = sum x, S = sum x x^T.
-// So u = C^T C v (apply_C then apply_C_T, operators.cpp:128-180) and
-// lambda = |C v|^2 = v.u (v normalised) cost O(N n^2) instead of O(N^2 n).
-
-// Gram sums S (n x n) and s (n) of the points, one block per entry (fixed order)
-__global__ void __launch_bounds__(kBlock) gram_kernel(const double* X, long long N, int n,
-                                                      double* out) {
-  const int e = blockIdx.x;
-  const int i = e < n * n ? e / n : e - n * n;
-  const int j = e < n * n ? e % n : -1;
-  double v[1] = {0.0};
-  for (long long l = threadIdx.x; l < N; l += kBlock)
-    v[0] += j >= 0 ? X[l * n + i] * X[l * n + j] : X[l * n + i];
-  __shared__ double o[1];
-  block_reduce_store<1>(v, o);
-  __syncthreads();
-  if (threadIdx.x == 0) out[e] = o[0];
-}
-
-// v = u / norm_u and per-block partials of (A, Cs, B[n], AX[n])
-template <int NN>
-__global__ void __launch_bounds__(kPBlock) pstruct_sums_kernel(const double* u, double* v,
-                                                               double norm_u, const double* X,
-                                                               long long N, double* part) {
-  constexpr int W = 2 + 2 * NN;
-  double acc[W];
-#pragma unroll
-  for (int w = 0; w < W; ++w) acc[w] = 0.0;
-  for (long long l = (long long)blockIdx.x * kPBlock + threadIdx.x; l < N;
-       l += (long long)gridDim.x * kPBlock) {
-    const double a = u[l] / norm_u;  // operators.cpp:327
-    v[l] = a;
-    double bx = 0.0;
-#pragma unroll
-    for (int j = 0; j < NN; ++j) {
-      const double b = u[N + l * NN + j] / norm_u;
-      v[N + l * NN + j] = b;
-      const double x = X[l * NN + j];
-      bx = fma(b, x, bx);
-      acc[2 + j] += b;
-      acc[2 + NN + j] = fma(a, x, acc[2 + NN + j]);
-    }
-    acc[0] += a;
-    acc[1] += a - bx;
-  }
-  block_reduce_store<W, kPBlock>(acc, part + (long long)blockIdx.x * W);
-}
-
-// u = C^T C v per point, partials of (|u|^2, v.u)
-template <int NN>
-__global__ void __launch_bounds__(kPBlock) pstruct_apply_kernel(const double* v, const double* X,
-                                                                const double* gram,
-                                                                const double* sums, long long N,
-                                                                double* u, double* part) {
-  const double A = sums[0], Cs = sums[1];
-  const double* B = sums + 2;
-  const double* AX = sums + 2 + NN;
-  const double* S = gram;
-  const double* sx = gram + NN * NN;
-  const double Nm1 = (double)(N - 1);
-  double acc[2] = {0.0, 0.0};
-  for (long long l = (long long)blockIdx.x * kPBlock + threadIdx.x; l < N;
-       l += (long long)gridDim.x * kPBlock) {
-    const double a = v[l];
-    double b[NN], x[NN];
-    double bx = 0.0;
-#pragma unroll
-    for (int j = 0; j < NN; ++j) {
-      b[j] = v[N + l * NN + j];
-      x[j] = X[l * NN + j];
-      bx = fma(b[j], x[j], bx);
-    }
-    const double c = a - bx;
-    double Bx = 0.0, bs = 0.0;
-#pragma unroll
-    for (int j = 0; j < NN; ++j) {
-      Bx = fma(B[j] - b[j], x[j], Bx);
-      bs = fma(b[j], sx[j] - x[j], bs);
-    }
-    const double R = Nm1 * a - (Cs - c) - Bx;
-    const double Col = (A - a) - Nm1 * c - bs;
-    const double uy = a + R - Col;  // pos rows + row sums - column sums
-    u[l] = uy;
-    double uu = uy * uy, vu = a * uy;
-#pragma unroll
-    for (int j = 0; j < NN; ++j) {
-      double Sb = 0.0;
-#pragma unroll
-      for (int k = 0; k < NN; ++k) Sb = fma(S[j * NN + k], b[k], Sb);
-      const double T = (AX[j] - a * x[j]) - c * (sx[j] - x[j]) - (Sb - x[j] * bx);
-      const double ux = Col * x[j] - T;
-      u[N + l * NN + j] = ux;
-      uu = fma(ux, ux, uu);
-      vu = fma(b[j], ux, vu);
-    }
-    acc[0] += uu;
-    acc[1] += vu;
-  }
-  block_reduce_store<2, kPBlock>(acc, part + (long long)blockIdx.x * 2);
-}
-
-// fixed-order column sums of a [count][width] record array (width <= 64)
-__global__ void __launch_bounds__(kBlock) reduce_columns_kernel(const double* part,
-                                                                long long count, int width,
-                                                                double* out) {
-  for (int w = 0; w < width; ++w) {
-    double v[1] = {0.0};
-    for (long long i = threadIdx.x; i < count; i += kBlock) v[0] += part[i * width + w];
-    __shared__ double o[1];
-    block_reduce_store<1>(v, o);
-    __syncthreads();
-    if (threadIdx.x == 0) out[w] = o[0];
-    __syncthreads();
-  }
-}
-
 // fixed-order sum of `count` records of width `width` -> out[width]
 __global__ void __launch_bounds__(kBlock) reduce_records_kernel(const double* part,
                                                                 long long count, int width,
@@ -456,35 +334,6 @@ cudaError_t launch_power_prep(const PowerArgs& a, cudaStream_t s) {
 
 cudaError_t launch_power_post(const PowerArgs& a, cudaStream_t s) {
   power_post_kernel<<<primal_blocks(a.N), kPBlock, 0, s>>>(a);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_gram(const double* X, long long N, int n, double* out, cudaStream_t s) {
-  gram_kernel<<<n * n + n, kBlock, 0, s>>>(X, N, n, out);
-  return cudaGetLastError();
-}
-
-template <int NN>
-void pstruct_n(const double* u, double* v, double norm_u, const double* X, const double* gram,
-               double* sums, double* part, double* part2, double* out2, long long N, cudaStream_t s) {
-  const int nb = primal_blocks(N);
-  pstruct_sums_kernel<NN><<<nb, kPBlock, 0, s>>>(u, v, norm_u, X, N, part);
-  reduce_columns_kernel<<<1, kBlock, 0, s>>>(part, nb, 2 + 2 * NN, sums);
-  pstruct_apply_kernel<NN><<<nb, kPBlock, 0, s>>>(v, X, gram, sums, N, const_cast<double*>(u),
-                                                  part2);
-  reduce_columns_kernel<<<1, kBlock, 0, s>>>(part2, nb, 2, out2);
-}
-using PstructFn = void (*)(const double*, double*, double, const double*, const double*, double*,
-                           double*, double*, double*, long long, cudaStream_t);
-
-cudaError_t launch_power_struct(const PowerStructArgs& a, cudaStream_t s) {
-  static constexpr PstructFn tab[kMaxN] = {
-      pstruct_n<1>,  pstruct_n<2>,  pstruct_n<3>,  pstruct_n<4>,  pstruct_n<5>,  pstruct_n<6>,
-      pstruct_n<7>,  pstruct_n<8>,  pstruct_n<9>,  pstruct_n<10>, pstruct_n<11>, pstruct_n<12>,
-      pstruct_n<13>, pstruct_n<14>, pstruct_n<15>, pstruct_n<16>, pstruct_n<17>, pstruct_n<18>,
-      pstruct_n<19>, pstruct_n<20>, pstruct_n<21>, pstruct_n<22>, pstruct_n<23>, pstruct_n<24>};
-  if (a.n < 1 || a.n > kMaxN) return cudaErrorInvalidValue;
-  tab[a.n - 1](a.u, a.v, a.norm_u, a.X, a.gram, a.sums, a.part, a.part2, a.out2, a.N, s);
   return cudaGetLastError();
 }
 

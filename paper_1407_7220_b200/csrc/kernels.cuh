@@ -56,24 +56,25 @@ struct PowerArgs {
   int n;
 };
 
-// closed-form power step (u = C^T C v in O(N n^2)); u is updated in place
-struct PowerStructArgs {
-  double* u;            // N (n+1): in = previous u, out = C^T C v
-  double* v;            // N (n+1): v = u_in / norm_u
-  double norm_u;
+// closed-form power iteration for sigma_max(C) in one cooperative launch (power.cu)
+struct PowerLoopArgs {
+  double* u;            // N (n+1): in = normalised start vector, scratch afterwards
+  double* v;            // N (n+1) scratch
   const double* X;
   const double* gram;   // [S (n x n) | s (n)]
-  double* sums;         // 2 + 2n
-  double* part;         // [blocks][2 + 2n]
-  double* part2;        // [blocks][2]
-  double* out2;         // (|u|^2, v.u)
+  double* part;         // [grid][2 + 2n]
+  double* part2;        // [grid][2]
+  double* state;        // out: sigma, iterations, converged
   long long N;
   int n;
+  int max_iters;
+  double tol;
 };
 
 int primal_blocks(long long N);
 cudaError_t launch_gram(const double* X, long long N, int n, double* out, cudaStream_t s);
-cudaError_t launch_power_struct(const PowerStructArgs& a, cudaStream_t s);
+int power_loop_grid(int sms);
+cudaError_t launch_power_loop(const PowerLoopArgs& a, int grid, cudaStream_t s);
 cudaError_t launch_primal(const PrimalArgs& a, cudaStream_t s);
 cudaError_t launch_reduce(const ReduceArgs& a, cudaStream_t s);
 cudaError_t launch_control(DevCtrl* c, const double* scal, const double* k2, double* hist,

@@ -1,0 +1,246 @@
+// power.cu -- K4': sigma_max(C) by the power method (operators.cpp:302-339 on
+// op_C, :353-369) with a closed-form O(N n^2) step, the whole iteration in one
+// cooperative launch.
+//
+// C^T C has structure: with a = v_y, b_l = v_xi[l], c_l = a_l - b_l.x_l and
+// w(l1, l2) = a_l1 - c_l2 - b_l2.x_l1 (operators.cpp:143-147),
+//   sum_{l2 != l} w(l, l2) = (N-1) a_l - (Cs - c_l) - (B - b_l).x_l
+//   sum_{l1 != l} w(l1, l) = (A - a_l) - (N-1) c_l - b_l.(s - x_l)
+//   sum_{l1 != l} w(l1, l) x_l1 = (AX - a_l x_l) - c_l (s - x_l) - (S - x_l x_l^T) b_l
+// with A = sum a, Cs = sum c, B = sum b, AX = sum a x, s = sum x, S = sum x x^T.
+// So u = C^T C v (apply_C then apply_C_T, operators.cpp:128-180) and
+// lambda = |C v|^2 = v.u (v normalised) cost O(N n^2) instead of two O(N^2 n)
+// operator passes. Step, start vector (rng_stream(0x5eed, 97)) and stopping
+// rule are the reference's; every block reduces the partials redundantly in
+// the same fixed order, so all blocks take identical decisions with two grid
+// barriers per step. The computation is replicated on every rank of a
+// sharded run (no exchange).
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+#include <math.h>
+
+#include "device.cuh"
+#include "iteration.cuh"
+#include "kernels.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace crb {
+
+namespace {
+
+constexpr int kQBlock = 256;
+
+// Gram sums S (n x n) and s (n) of the points, one block per entry (fixed order)
+__global__ void __launch_bounds__(kBlock) gram_kernel(const double* X, long long N, int n,
+                                                      double* out) {
+  const int e = blockIdx.x;
+  const int i = e < n * n ? e / n : e - n * n;
+  const int j = e < n * n ? e % n : -1;
+  double v[1] = {0.0};
+  for (long long l = threadIdx.x; l < N; l += kBlock)
+    v[0] += j >= 0 ? X[l * n + i] * X[l * n + j] : X[l * n + i];
+  __shared__ double o[1];
+  block_reduce_store<1>(v, o);
+  __syncthreads();
+  if (threadIdx.x == 0) out[e] = o[0];
+}
+
+// v_l = u_l / norm_u (operators.cpp:327); accumulates (A, Cs, B[n], AX[n])
+template <int NN>
+__device__ __forceinline__ void sums_point(const double* u, double* v, double norm_u,
+                                           const double* X, long long N, long long l,
+                                           double (&acc)[2 + 2 * NN]) {
+  const double a = __ldcg(u + l) / norm_u;
+  __stcg(v + l, a);
+  double bx = 0.0;
+#pragma unroll
+  for (int j = 0; j < NN; ++j) {
+    const double b = __ldcg(u + N + l * NN + j) / norm_u;
+    __stcg(v + N + l * NN + j, b);
+    const double x = X[l * NN + j];
+    bx = fma(b, x, bx);
+    acc[2 + j] += b;
+    acc[2 + NN + j] = fma(a, x, acc[2 + NN + j]);
+  }
+  acc[0] += a;
+  acc[1] += a - bx;
+}
+
+// u_l = (C^T C v)_l; accumulates (|u|^2, v.u)
+template <int NN>
+__device__ __forceinline__ void apply_point(const double* v, const double* X, const double* gram,
+                                            const double* sums, long long N, long long l,
+                                            double* u, double (&acc)[2]) {
+  const double A = sums[0], Cs = sums[1];
+  const double* B = sums + 2;
+  const double* AX = sums + 2 + NN;
+  const double* S = gram;
+  const double* sx = gram + NN * NN;
+  const double Nm1 = (double)(N - 1);
+  const double a = __ldcg(v + l);
+  double b[NN], x[NN];
+  double bx = 0.0;
+#pragma unroll
+  for (int j = 0; j < NN; ++j) {
+    b[j] = __ldcg(v + N + l * NN + j);
+    x[j] = X[l * NN + j];
+    bx = fma(b[j], x[j], bx);
+  }
+  const double c = a - bx;
+  double Bx = 0.0, bs = 0.0;
+#pragma unroll
+  for (int j = 0; j < NN; ++j) {
+    Bx = fma(B[j] - b[j], x[j], Bx);
+    bs = fma(b[j], sx[j] - x[j], bs);
+  }
+  const double R = Nm1 * a - (Cs - c) - Bx;
+  const double Col = (A - a) - Nm1 * c - bs;
+  const double uy = a + R - Col;  // pos rows + row sums - column sums
+  __stcg(u + l, uy);
+  double uu = uy * uy, vu = a * uy;
+#pragma unroll
+  for (int j = 0; j < NN; ++j) {
+    double Sb = 0.0;
+#pragma unroll
+    for (int k = 0; k < NN; ++k) Sb = fma(S[j * NN + k], b[k], Sb);
+    const double T = (AX[j] - a * x[j]) - c * (sx[j] - x[j]) - (Sb - x[j] * bx);
+    const double ux = Col * x[j] - T;
+    __stcg(u + N + l * NN + j, ux);
+    uu = fma(ux, ux, uu);
+    vu = fma(b[j], ux, vu);
+  }
+  acc[0] += uu;
+  acc[1] += vu;
+}
+
+// fixed-order block sum of W per-thread values with warp butterflies (small smem)
+template <int W>
+__device__ __forceinline__ void block_sum_store(double (&v)[W], double* out) {
+  __shared__ double sh[kQBlock / 32][W];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int w = 0; w < W; ++w) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v[w] += __shfl_xor_sync(0xffffffffu, v[w], o);
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int w = 0; w < W; ++w) sh[warp][w] = v[w];
+  }
+  __syncthreads();
+  for (int w = threadIdx.x; w < W; w += kQBlock) {
+    double t = 0.0;
+#pragma unroll
+    for (int k = 0; k < kQBlock / 32; ++k) t += sh[k][w];
+    __stcg(out + w, t);
+  }
+  __syncthreads();
+}
+
+// every block: out[w] = sum over the grid's records part[g][w], fixed order
+// (warp-per-column, lanes over records, butterfly)
+template <int W>
+__device__ __forceinline__ void grid_records_sum(const double* part, int nrec, double* out) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int w = warp; w < W; w += kQBlock / 32) {
+    double s = 0.0;
+    for (int g = lane; g < nrec; g += 32) s += __ldcg(part + (long long)g * W + w);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) out[w] = s;
+  }
+  __syncthreads();
+}
+
+template <int NN>
+__global__ void __launch_bounds__(kQBlock) power_loop_kernel(const PowerLoopArgs a) {
+  constexpr int W = 2 + 2 * NN;
+  cg::grid_group grid = cg::this_grid();
+  const long long tid = (long long)blockIdx.x * kQBlock + threadIdx.x;
+  const long long nthreads = (long long)gridDim.x * kQBlock;
+  const long long N = a.N;
+  __shared__ double sums[W];
+  __shared__ double red2[2];
+  double norm_u = 1.0;  // the host stored the normalised start vector in u
+  double lambda_prev = 0.0;
+  for (int it = 1; it <= a.max_iters; ++it) {
+    {
+      double acc[W];
+#pragma unroll
+      for (int w = 0; w < W; ++w) acc[w] = 0.0;
+      for (long long l = tid; l < N; l += nthreads) sums_point<NN>(a.u, a.v, norm_u, a.X, N, l, acc);
+      block_sum_store<W>(acc, a.part + (long long)blockIdx.x * W);
+    }
+    grid.sync();
+    grid_records_sum<W>(a.part, gridDim.x, sums);
+    {
+      double acc[2] = {0.0, 0.0};
+      for (long long l = tid; l < N; l += nthreads)
+        apply_point<NN>(a.v, a.X, a.gram, sums, N, l, a.u, acc);
+      block_sum_store<2>(acc, a.part2 + (long long)blockIdx.x * 2);
+    }
+    grid.sync();
+    grid_records_sum<2>(a.part2, gridDim.x, red2);
+    // identical in every block: operators.cpp:318-334
+    const double lambda = red2[1];  // |C v|^2 = v . C^T C v
+    const double nu = sqrt(red2[0]);
+    bool done = false;
+    double sigma = 0.0;
+    int conv = 1;
+    if (nu == 0.0 || lambda == 0.0) {
+      done = true;
+    } else {
+      norm_u = nu;
+      if (it > 1 && fabs(lambda - lambda_prev) <= a.tol * lambda) {
+        sigma = sqrt(lambda) * 1.01;
+        done = true;
+      } else if (it == a.max_iters) {
+        sigma = sqrt(lambda) * 1.10;  // the reference inflates lambda_prev = lambda here
+        conv = 0;
+        done = true;
+      }
+      lambda_prev = lambda;
+    }
+    if (done) {
+      if (blockIdx.x == 0 && threadIdx.x == 0) {
+        a.state[0] = sigma;
+        a.state[1] = (double)it;
+        a.state[2] = (double)conv;
+      }
+      return;
+    }
+  }
+}
+
+template <int NN>
+void power_loop_n(const PowerLoopArgs& a, int grid, cudaStream_t s, cudaError_t* err) {
+  void* args[] = {const_cast<PowerLoopArgs*>(&a)};
+  *err = cudaLaunchCooperativeKernel((const void*)power_loop_kernel<NN>, dim3((unsigned)grid),
+                                     dim3(kQBlock), args, 0, s);
+}
+using PowerLoopFn = void (*)(const PowerLoopArgs&, int, cudaStream_t, cudaError_t*);
+
+}  // namespace
+
+cudaError_t launch_gram(const double* X, long long N, int n, double* out, cudaStream_t s) {
+  gram_kernel<<<n * n + n, kBlock, 0, s>>>(X, N, n, out);
+  return cudaGetLastError();
+}
+
+int power_loop_grid(int sms) { return sms; }  // one 256-thread block per SM
+
+cudaError_t launch_power_loop(const PowerLoopArgs& a, int grid, cudaStream_t s) {
+  static constexpr PowerLoopFn tab[kMaxN] = {
+      power_loop_n<1>,  power_loop_n<2>,  power_loop_n<3>,  power_loop_n<4>,  power_loop_n<5>,
+      power_loop_n<6>,  power_loop_n<7>,  power_loop_n<8>,  power_loop_n<9>,  power_loop_n<10>,
+      power_loop_n<11>, power_loop_n<12>, power_loop_n<13>, power_loop_n<14>, power_loop_n<15>,
+      power_loop_n<16>, power_loop_n<17>, power_loop_n<18>, power_loop_n<19>, power_loop_n<20>,
+      power_loop_n<21>, power_loop_n<22>, power_loop_n<23>, power_loop_n<24>};
+  if (a.n < 1 || a.n > kMaxN) return cudaErrorInvalidValue;
+  cudaError_t e = cudaSuccess;
+  tab[a.n - 1](a, grid, s, &e);
+  return e;
+}
+
+}  // namespace crb
