@@ -132,6 +132,12 @@ cr_status cr_iter_finish(cr_handle *h, int32_t *stopped);
    when history != NULL, res->iters snapshots. */
 cr_status cr_papg_finish(cr_handle *h, cr_papg_result *res, double *y, double *xi,
                          cr_snapshot *history);
+/* Begin a new solve warm-started from this handle's device-resident theta1
+   (papg.cpp:159-164; the gamma continuation of runner.cpp:258-259, 305, 322
+   without a host round trip of the N^2 multipliers). */
+cr_status cr_papg_begin_resume(cr_handle *h, const cr_papg_config *cfg);
+/* Replace the shifted observations (e.g. prepare_problem at the next gamma). */
+cr_status cr_set_observations(cr_handle *h, const double *ybar_shifted);
 /* begin + iterate to termination + finish */
 cr_status cr_papg_solve(cr_handle *h, const cr_papg_config *cfg, const double *theta0,
                         cr_papg_result *res, double *y, double *xi, cr_snapshot *history);
@@ -152,6 +158,18 @@ int32_t cr_sweep_variant(const cr_handle *h);
 /* Time k sweep-kernel launches alone on the handle's stream with CUDA events
    (the dominant kernel in isolation, for the roofline). */
 cr_status cr_time_sweep(cr_handle *h, int32_t k, double *avg_seconds);
+
+/* ---- one-shot metric sweeps on a given point (metrics.cpp) --------------- */
+/* |(A1 y + A2 xi)_-|_2 over all N(N-1) rows and its /sqrt(N^2-N) form
+   (metrics.cpp:8-15); shift-invariant, so original or shifted y both work. */
+cr_status cr_infeasibility(cr_handle *h, const double *y, const double *xi, double out2[2]);
+/* theta1 . C eta with the handle's current theta1 (metrics.cpp:17-30). */
+cr_status cr_duality_gap(cr_handle *h, const double *y, const double *xi, double out2[2]);
+/* max_l y_l + xi_l.(x_q - x_l) for Q query points Xq (Q x n) (metrics.cpp:32-48). */
+cr_status cr_evaluate_estimator(cr_handle *h, const double *y, const double *xi,
+                                const double *Xq, int64_t Q, double *out);
+/* y'_l = estimator(x_l), an exactly feasible point (metrics.cpp:50-56). */
+cr_status cr_repair_feasibility(cr_handle *h, const double *y, const double *xi, double *y_out);
 
 /* ---- host utilities (no device) ----------------------------------------- */
 /* kinds: 0 quadratic, 1 exponential, 2 affine-noiseless, 3 custom-1d

@@ -231,6 +231,46 @@ inline PapgResult dual_gradient_ascent(const PreparedProblem& prep, const PapgCo
   return detail::solve(prep, cfg, theta0, false);
 }
 
+// metrics.cpp:8-15 -- (raw, normalised) infeasibility over all N(N-1) rows
+inline std::pair<double, double> infeasibility(const Dataset& data, const PrimalPoint& eta,
+                                               int device = 0) {
+  detail::Handle hd;
+  detail::check(cr_create(data.xs.data(), data.ys.data(), data.N(), data.n(), 1e-3, device, 0,
+                          data.N(), &hd.h),
+                hd.h);
+  double out[2];
+  detail::check(cr_infeasibility(hd.h, eta.y.data(), eta.xi.data(), out), hd.h);
+  return {out[0], out[1]};
+}
+
+// metrics.cpp:32-48 -- fhat(x) = max_l y_l + xi_l.(x - x_l) at Q query points (Q x n)
+inline std::vector<double> evaluate_estimator(const PrimalPoint& eta, const Dataset& data,
+                                              const std::vector<double>& x_query,
+                                              int device = 0) {
+  detail::Handle hd;
+  detail::check(cr_create(data.xs.data(), data.ys.data(), data.N(), data.n(), 1e-3, device, 0,
+                          data.N(), &hd.h),
+                hd.h);
+  const Index Q = static_cast<Index>(x_query.size()) / data.n();
+  std::vector<double> out(static_cast<size_t>(Q));
+  detail::check(cr_evaluate_estimator(hd.h, eta.y.data(), eta.xi.data(), x_query.data(), Q,
+                                      out.data()),
+                hd.h);
+  return out;
+}
+
+// metrics.cpp:50-56 -- y'_l = fhat(x_l)
+inline PrimalPoint repair_feasibility(const PrimalPoint& eta, const Dataset& data,
+                                      int device = 0) {
+  detail::Handle hd;
+  detail::check(cr_create(data.xs.data(), data.ys.data(), data.N(), data.n(), 1e-3, device, 0,
+                          data.N(), &hd.h),
+                hd.h);
+  PrimalPoint out = eta;
+  detail::check(cr_repair_feasibility(hd.h, eta.y.data(), eta.xi.data(), out.y.data()), hd.h);
+  return out;
+}
+
 inline std::pair<double, double> certificate_for_iterate(double gamma, double delta,
                                                          double B_xi_estimate,
                                                          double sigma_max_C) {

@@ -523,6 +523,60 @@ int cro_sigma_C(const double *X, int64_t N, int64_t n, double tol, int max_iters
   return 0;
 }
 
+/* --------------------------------------------------------------- metrics */
+/* metrics.cpp:8-15: apply_rows (operators.cpp:87-105) then |(-r)_+| */
+void cro_infeasibility(const double *X, int64_t N, int64_t n, const double *y, const double *xi,
+                       double out2[2]) {
+  double ss = 0;
+  for (int64_t l1 = 0; l1 < N; ++l1) {
+    const double *x1 = X + l1 * n;
+    for (int64_t l2 = 0; l2 < N; ++l2) {
+      if (l1 == l2) continue;
+      double acc = y[l1] - y[l2];
+      const double *xi2 = xi + l2 * n;
+      const double *x2 = X + l2 * n;
+      for (int64_t j = 0; j < n; ++j) acc -= xi2[j] * (x1[j] - x2[j]);
+      const double m = -acc > 0.0 ? -acc : 0.0;
+      ss += m * m;
+    }
+  }
+  out2[0] = sqrt(ss);
+  out2[1] = out2[0] / sqrt((double)(N * (N - 1)));
+}
+
+/* metrics.cpp:17-30 */
+void cro_duality_gap(const double *X, int64_t N, int64_t n, const double *theta, const double *y,
+                     const double *xi, double out2[2]) {
+  const int64_t dim = N * (N - 1) + N;
+  double *ce = (double *)malloc(sizeof(double) * (size_t)dim);
+  cro_apply_C(X, N, n, y, xi, ce);
+  double a = 0, b = 0;
+  for (int64_t i = 0; i < N * (N - 1); ++i) a += theta[i] * ce[i];
+  for (int64_t i = 0; i < N; ++i) b += theta[N * (N - 1) + i] * ce[N * (N - 1) + i];
+  free(ce);
+  out2[0] = a + b;
+  out2[1] = out2[0] / (double)(N * (N - 1));
+}
+
+/* metrics.cpp:32-48 */
+double cro_evaluate_estimator(const double *X, int64_t N, int64_t n, const double *y,
+                              const double *xi, const double *xq) {
+  double best = -INFINITY;
+  for (int64_t l = 0; l < N; ++l) {
+    double v = y[l];
+    const double *xil = xi + l * n;
+    for (int64_t j = 0; j < n; ++j) v += xil[j] * (xq[j] - X[l * n + j]);
+    if (v > best) best = v;
+  }
+  return best;
+}
+
+/* metrics.cpp:50-56 */
+void cro_repair_feasibility(const double *X, int64_t N, int64_t n, const double *y,
+                            const double *xi, double *y_out) {
+  for (int64_t l = 0; l < N; ++l) y_out[l] = cro_evaluate_estimator(X, N, n, y, xi, X + l * n);
+}
+
 /* ----------------------------------------------------------- small ops */
 void cro_project_nonneg_ball(double *v, int64_t len, double radius) { /* projections.hpp:9-13 */
   for (int64_t i = 0; i < len; ++i) v[i] = v[i] > 0.0 ? v[i] : 0.0;

@@ -106,6 +106,16 @@ int cro_sigma_C(const double *X, int64_t N, int64_t n, double tol, int max_iters
 int cro_papg(const double *X, const double *ys_shifted, int64_t N, int64_t n,
              const cro_config *cfg, const double *theta0, cro_result *res);
 
+/* metrics.cpp:8-56 (full row set, canonical order) */
+void cro_infeasibility(const double *X, int64_t N, int64_t n, const double *y, const double *xi,
+                       double out2[2]);
+void cro_duality_gap(const double *X, int64_t N, int64_t n, const double *theta, const double *y,
+                     const double *xi, double out2[2]);
+double cro_evaluate_estimator(const double *X, int64_t N, int64_t n, const double *y,
+                              const double *xi, const double *xq);
+void cro_repair_feasibility(const double *X, int64_t N, int64_t n, const double *y,
+                            const double *xi, double *y_out);
+
 /* projections.hpp:9-13, engines.hpp:11-13, papg.cpp:298-303 */
 void cro_project_nonneg_ball(double *v, int64_t len, double radius);
 double cro_momentum_next(double t);

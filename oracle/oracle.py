@@ -80,6 +80,14 @@ def lib():
         L.cro_momentum_next.restype = d
         L.cro_certificate.argtypes = [d, d, d, d, _P]
         L.cro_certificate.restype = None
+        L.cro_infeasibility.argtypes = [_P, i64, i64, _P, _P, _P]
+        L.cro_infeasibility.restype = None
+        L.cro_duality_gap.argtypes = [_P, i64, i64, _P, _P, _P, _P]
+        L.cro_duality_gap.restype = None
+        L.cro_evaluate_estimator.argtypes = [_P, i64, i64, _P, _P, _P]
+        L.cro_evaluate_estimator.restype = d
+        L.cro_repair_feasibility.argtypes = [_P, i64, i64, _P, _P, _P]
+        L.cro_repair_feasibility.restype = None
         L.cro_cross_position.argtypes = [i64, i64, i64, i64]
         L.cro_cross_position.restype = i64
         _lib = L
@@ -218,6 +226,39 @@ def papg(X, ys, *, gamma=1e-3, B_theta=0.0, adaptive_B_theta=True, max_restarts=
                         REASONS[res.reason], res.restarts, bool(res.saturated), res.g_final,
                         res.delta_estimate, res.sigma_C, res.L_g, res.B_theta, res.wall_seconds,
                         res.sigma_iters)
+
+
+def _c(a):
+    return np.ascontiguousarray(a, np.float64)
+
+
+def infeasibility(X, y, xi):
+    X = _c(X)
+    out = np.empty(2)
+    lib().cro_infeasibility(_p(X), X.shape[0], X.shape[1], _p(_c(y)), _p(_c(xi).reshape(-1)), _p(out))
+    return float(out[0]), float(out[1])
+
+
+def duality_gap(X, theta, y, xi):
+    X = _c(X)
+    out = np.empty(2)
+    lib().cro_duality_gap(_p(X), X.shape[0], X.shape[1], _p(_c(theta)), _p(_c(y)),
+                          _p(_c(xi).reshape(-1)), _p(out))
+    return float(out[0]), float(out[1])
+
+
+def evaluate_estimator(X, y, xi, xq):
+    X = _c(X)
+    return lib().cro_evaluate_estimator(_p(X), X.shape[0], X.shape[1], _p(_c(y)),
+                                        _p(_c(xi).reshape(-1)), _p(_c(xq)))
+
+
+def repair_feasibility(X, y, xi):
+    X = _c(X)
+    out = np.empty(X.shape[0])
+    lib().cro_repair_feasibility(_p(X), X.shape[0], X.shape[1], _p(_c(y)), _p(_c(xi).reshape(-1)),
+                                 _p(out))
+    return out
 
 
 def project_nonneg_ball(v, radius):

@@ -3,5 +3,5 @@ regression (arXiv 1407.7220, reference `cvxreg` proj/core)."""
 from .papg import (Dataset, DualPoint, DualSolver, GeneratorSpec,  # noqa: F401
                    MetricsSnapshot, PapgConfig, PapgResult, PreparedProblem, PrimalPoint,
                    ProblemBounds, SolveReport, TermReason, certificate_for_iterate,
-                   dual_gradient_ascent, gen_instance, momentum_next, papg_solve,
-                   prepare_problem)
+                   dual_gradient_ascent, evaluate_estimator, gen_instance, infeasibility,
+                   momentum_next, papg_solve, prepare_problem, repair_feasibility)

@@ -47,7 +47,8 @@ EXPORTS = [
     "cr_attach_nccl", "cr_exchange_len", "cr_sigma_C", "cr_papg_begin", "cr_papg_iterate",
     "cr_iter_local", "cr_exchange_get", "cr_exchange_put", "cr_iter_finish", "cr_papg_finish",
     "cr_papg_solve", "cr_get_theta", "cr_get_rows", "cr_last_timing", "cr_time_sweep",
-    "cr_sweep_variant",
+    "cr_sweep_variant", "cr_papg_begin_resume", "cr_set_observations", "cr_infeasibility",
+    "cr_duality_gap", "cr_evaluate_estimator", "cr_repair_feasibility",
     "cr_gen_instance", "cr_prepare_problem", "cr_certificate", "cr_momentum_next",
 ]
 
@@ -92,6 +93,12 @@ def load():
         "cr_last_timing": (st, [vp, _P, C.POINTER(i64), _P]),
         "cr_time_sweep": (st, [vp, i32, _P]),
         "cr_sweep_variant": (i32, [vp]),
+        "cr_papg_begin_resume": (st, [vp, C.POINTER(PapgConfigC)]),
+        "cr_set_observations": (st, [vp, _P]),
+        "cr_infeasibility": (st, [vp, _P, _P, _P]),
+        "cr_duality_gap": (st, [vp, _P, _P, _P]),
+        "cr_evaluate_estimator": (st, [vp, _P, _P, _P, i64, _P]),
+        "cr_repair_feasibility": (st, [vp, _P, _P, _P]),
         "cr_gen_instance": (st, [i32, i64, i64, d, u64, i64, _P, _P]),
         "cr_prepare_problem": (st, [_P, _P, i64, i64, d, _P, _P, _P, _P, _P]),
         "cr_certificate": (None, [d, d, d, d, _P]),

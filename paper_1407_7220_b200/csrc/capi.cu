@@ -586,10 +586,23 @@ cr_status cr_sigma_C(cr_handle* h, double tol, int32_t max_iters, double* sigma,
   return CR_OK;
 }
 
-cr_status cr_papg_begin(cr_handle* h, const cr_papg_config* cfg, const double* theta0) {
+}  // extern "C"
+
+namespace {
+// resume: warm start from the handle's device-resident theta1 (papg.cpp:159-164
+// with theta0 = the previous solve's theta1, e.g. the gamma continuation of
+// runner.cpp:258-259, 305, 322) without a host round trip.
+cr_status begin_impl(cr_handle* h, const cr_papg_config* cfg, const double* theta0, bool resume) {
   if (!h || !cfg) return CR_EINVAL;
   if (!(cfg->gamma > 0) || cfg->max_iters < 1) return fail(h, CR_EINVAL, "papg: bad config");
+  if (resume && (!h->begun || theta0 != nullptr))
+    return fail(h, CR_ESTATE, "papg: resume needs a previous solve on this handle");
   CUDA_TRY(cudaSetDevice(h->device));
+  if (resume) {
+    const cr_status s0 = sync_ctrl(h);
+    if (s0 != CR_OK) return s0;
+  }
+  const DevCtrl prev = *h->ctrl_h;
   h->t_begin = std::chrono::steady_clock::now();
   h->cfg = *cfg;
   h->begun = false;
@@ -605,6 +618,8 @@ cr_status cr_papg_begin(cr_handle* h, const cr_papg_config* cfg, const double* t
   h->sigma_seconds = 0;
   if (cfg->sigma_C > 0) {
     h->sigma_C = cfg->sigma_C;
+  } else if (resume && h->sigma_C > 0) {
+    // same X -> the same power iteration and sigma; keep the cached value
   } else {
     int32_t it = 0, conv = 1;
     double s = 0;
@@ -644,7 +659,7 @@ cr_status cr_papg_begin(cr_handle* h, const cr_papg_config* cfg, const double* t
   c.ell = 0;
   c.max_iters = cfg->max_iters;
   c.hist_cap = cfg->record_history ? h->hist_cap : 0;
-  c.cur = 0;
+  c.cur = resume ? prev.cur : 0;
   c.max_restarts = cfg->max_restarts;
   c.adaptive = cfg->adaptive_B_theta ? 1 : 0;
   c.use_momentum = cfg->use_momentum ? 1 : 0;
@@ -665,16 +680,24 @@ cr_status cr_papg_begin(cr_handle* h, const cr_papg_config* cfg, const double* t
   c.gap_div = (double)N * (double)(N - 1);
   c.infeas_div = std::sqrt(c.gap_div);
   c.K = (double)N;  // singleton partition
+  if (resume) {  // theta1 = Pi_Q2(theta0), theta0 = s V[cur] >= 0: a rescale only
+    const double nrm = prev.theta1_norm;
+    const double sc = nrm > c.B_theta ? c.B_theta / nrm : 1.0;
+    c.s_cur = prev.s_cur * sc;
+    c.s_prev = c.s_cur;
+  }
   CUDA_TRY(cudaMemcpyAsync(h->ctrl_d, &c, sizeof(c), cudaMemcpyHostToDevice, h->st));
   std::memcpy(h->ctrl_h, &c, sizeof(c));
 
   const size_t vbytes = sizeof(double) * (size_t)h->R * (size_t)h->ld;
-  CUDA_TRY(cudaMemsetAsync(h->V[0], 0, vbytes, h->st));
-  CUDA_TRY(cudaMemsetAsync(h->V[1], 0, vbytes, h->st));
-  CUDA_TRY(cudaMemsetAsync(h->vpos[0], 0, sizeof(double) * N, h->st));
-  CUDA_TRY(cudaMemsetAsync(h->vpos[1], 0, sizeof(double) * N, h->st));
-  CUDA_TRY(cudaMemsetAsync(h->xbuf, 0, sizeof(double) * payload_len(h), h->st));
-  CUDA_TRY(cudaMemsetAsync(h->aggsave, 0, sizeof(double) * payload_len(h), h->st));
+  if (!resume) {
+    CUDA_TRY(cudaMemsetAsync(h->V[0], 0, vbytes, h->st));
+    CUDA_TRY(cudaMemsetAsync(h->V[1], 0, vbytes, h->st));
+    CUDA_TRY(cudaMemsetAsync(h->vpos[0], 0, sizeof(double) * N, h->st));
+    CUDA_TRY(cudaMemsetAsync(h->vpos[1], 0, sizeof(double) * N, h->st));
+    CUDA_TRY(cudaMemsetAsync(h->xbuf, 0, sizeof(double) * payload_len(h), h->st));
+    CUDA_TRY(cudaMemsetAsync(h->aggsave, 0, sizeof(double) * payload_len(h), h->st));
+  }
 
   if (theta0) {  // warm start: theta1 = Pi_Q2(theta0) (papg.cpp:159-164)
     const int64_t rowlen = N - 1;
@@ -761,6 +784,26 @@ cr_status cr_papg_begin(cr_handle* h, const cr_papg_config* cfg, const double* t
   if (s != CR_OK) return s;
   h->loop_seconds = 0;
   h->begun = true;
+  return CR_OK;
+}
+}  // namespace
+
+extern "C" {
+
+cr_status cr_papg_begin(cr_handle* h, const cr_papg_config* cfg, const double* theta0) {
+  return begin_impl(h, cfg, theta0, false);
+}
+
+cr_status cr_papg_begin_resume(cr_handle* h, const cr_papg_config* cfg) {
+  return begin_impl(h, cfg, nullptr, true);
+}
+
+cr_status cr_set_observations(cr_handle* h, const double* ybar_shifted) {
+  if (!h || !ybar_shifted) return CR_EINVAL;
+  CUDA_TRY(cudaSetDevice(h->device));
+  CUDA_TRY(cudaMemcpyAsync(h->ybar, ybar_shifted, sizeof(double) * h->N, cudaMemcpyHostToDevice,
+                           h->st));
+  CUDA_TRY(cudaStreamSynchronize(h->st));
   return CR_OK;
 }
 
@@ -1076,6 +1119,157 @@ cr_status cr_time_sweep(cr_handle* h, int32_t k, double* avg_seconds) {
   CUDA_TRY(cudaEventElapsedTime(&ms, h->ev_start, h->ev_end));
   *avg_seconds = ms * 1e-3 / k;
   return CR_OK;
+}
+
+}  // extern "C"
+
+// ---- one-shot metric sweeps (metrics.cpp) ---------------------------------
+namespace {
+struct PointBufs {
+  double *y = nullptr, *xi = nullptr, *rowrec = nullptr, *colrec = nullptr, *part = nullptr;
+  cudaStream_t st = nullptr;
+  ~PointBufs() {
+    for (double* b : {y, xi, rowrec, colrec, part}) dfree(b, st);
+    if (st) cudaStreamSynchronize(st);
+  }
+};
+
+cr_status upload_point(cr_handle* h, const double* y, const double* xi, PointBufs& b) {
+  b.st = h->st;
+  g_alloc_stream = h->st;
+  const size_t RP = (size_t)h->RP;
+  if (dalloc(&b.y, h->N) != cudaSuccess || dalloc(&b.xi, h->N * h->n) != cudaSuccess ||
+      dalloc(&b.rowrec, h->N * RP) != cudaSuccess || dalloc(&b.colrec, h->N * RP) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(h, CR_ENOMEM, "metric buffers");
+  }
+  CUDA_TRY(cudaMemcpyAsync(b.y, y, sizeof(double) * h->N, cudaMemcpyHostToDevice, h->st));
+  CUDA_TRY(cudaMemcpyAsync(b.xi, xi, sizeof(double) * h->N * h->n, cudaMemcpyHostToDevice, h->st));
+  CUDA_TRY(launch_records(h->X, b.y, b.xi, h->N, (int)h->n, b.rowrec, b.colrec, h->st));
+  return CR_OK;
+}
+
+// (sum min(row,0)^2, sum theta1.row) over all shards' rows
+cr_status pair_metrics(cr_handle* h, PointBufs& b, bool with_theta, double out[2]) {
+  int sms = 148;
+  CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
+  const int grid = sms * 4;
+  if (dalloc(&b.part, (size_t)grid * 2 + 2) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(h, CR_ENOMEM, "metric buffers");
+  }
+  MetricsArgs a{};
+  a.rowrec = b.rowrec;
+  a.colrec = b.colrec;
+  a.V = with_theta ? h->V[h->ctrl_h->cur] : nullptr;
+  a.s = h->ctrl_h->s_cur;
+  a.part = b.part;
+  a.N = h->N;
+  a.R = h->R;
+  a.r0 = h->r0;
+  a.ld = h->ld;
+  a.n = (int)h->n;
+  a.S = (int)((h->N + 31) / 32);
+  a.P = (int)std::max<long long>(1, std::min<long long>(h->R, (long long)grid * 8 / a.S));
+  CUDA_TRY(launch_pair_metrics(a, grid, h->st));
+  CUDA_TRY(launch_reduce_records(b.part, grid, 2, b.part + (size_t)grid * 2, h->st));
+  if (h->comm)
+    NCCL_TRY(ncclAllReduce(b.part + (size_t)grid * 2, b.part + (size_t)grid * 2, 2, ncclDouble,
+                           ncclSum, h->comm, h->st));
+  CUDA_TRY(cudaMemcpyAsync(out, b.part + (size_t)grid * 2, 2 * sizeof(double),
+                           cudaMemcpyDeviceToHost, h->st));
+  CUDA_TRY(cudaStreamSynchronize(h->st));
+  return CR_OK;
+}
+}  // namespace
+
+extern "C" {
+
+cr_status cr_infeasibility(cr_handle* h, const double* y, const double* xi, double out2[2]) {
+  if (!h || !y || !xi || !out2) return CR_EINVAL;
+  CUDA_TRY(cudaSetDevice(h->device));
+  PointBufs b;
+  cr_status s = upload_point(h, y, xi, b);
+  if (s != CR_OK) return s;
+  double r[2];
+  s = pair_metrics(h, b, false, r);
+  if (s != CR_OK) return s;
+  out2[0] = std::sqrt(r[0]);  // metrics.cpp:12-14
+  out2[1] = out2[0] / std::sqrt((double)h->N * (double)(h->N - 1));
+  return CR_OK;
+}
+
+cr_status cr_duality_gap(cr_handle* h, const double* y, const double* xi, double out2[2]) {
+  if (!h || !y || !xi || !out2) return CR_EINVAL;
+  if (!h->begun) return fail(h, CR_ESTATE, "no dual state");
+  CUDA_TRY(cudaSetDevice(h->device));
+  cr_status s = sync_ctrl(h);
+  if (s != CR_OK) return s;
+  PointBufs b;
+  s = upload_point(h, y, xi, b);
+  if (s != CR_OK) return s;
+  double r[2];
+  s = pair_metrics(h, b, true, r);
+  if (s != CR_OK) return s;
+  // identity rows: theta_pos . y (metrics.cpp:26-27), replicated on every shard
+  std::vector<double> vp((size_t)h->N);
+  CUDA_TRY(cudaMemcpy(vp.data(), h->vpos[h->ctrl_h->cur], sizeof(double) * h->N,
+                      cudaMemcpyDeviceToHost));
+  double pos = 0.0;
+  for (int64_t l = 0; l < h->N; ++l) pos += (h->ctrl_h->s_cur * vp[l]) * y[l];
+  out2[0] = r[1] + pos;
+  out2[1] = out2[0] / ((double)h->N * (double)(h->N - 1));
+  return CR_OK;
+}
+
+}  // extern "C"
+
+namespace {
+// Xq: host queries, or nullptr to evaluate at the data points themselves
+cr_status estimator_impl(cr_handle* h, const double* y, const double* xi, const double* Xq,
+                         int64_t Q, double* out) {
+  CUDA_TRY(cudaSetDevice(h->device));
+  PointBufs b;
+  cr_status s = upload_point(h, y, xi, b);
+  if (s != CR_OK) return s;
+  double *dq = nullptr, *dout = nullptr;
+  g_alloc_stream = h->st;
+  if ((Xq && dalloc(&dq, (size_t)(Q * h->n)) != cudaSuccess) ||
+      dalloc(&dout, (size_t)Q) != cudaSuccess) {
+    cudaGetLastError();
+    dfree(dq, h->st);
+    return fail(h, CR_ENOMEM, "estimator buffers");
+  }
+  cudaError_t e = cudaSuccess;
+  if (Xq) e = cudaMemcpyAsync(dq, Xq, sizeof(double) * Q * h->n, cudaMemcpyHostToDevice, h->st);
+  const double* qsrc = Xq ? dq : h->X;
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device);
+  if (e == cudaSuccess)
+    e = launch_estimator(qsrc, Q, h->X, b.y, b.xi, h->N, (int)h->n, dout, sms * 8, h->st);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(out, dout, sizeof(double) * Q, cudaMemcpyDeviceToHost, h->st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(h->st);
+  dfree(dq, h->st);
+  dfree(dout, h->st);
+  CUDA_TRY(e);
+  return CR_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+cr_status cr_evaluate_estimator(cr_handle* h, const double* y, const double* xi,
+                                const double* Xq, int64_t Q, double* out) {
+  if (!h || !y || !xi || !Xq || !out || Q < 0) return CR_EINVAL;
+  if (Q == 0) return CR_OK;
+  return estimator_impl(h, y, xi, Xq, Q, out);
+}
+
+cr_status cr_repair_feasibility(cr_handle* h, const double* y, const double* xi, double* y_out) {
+  if (!h || !y || !xi || !y_out) return CR_EINVAL;
+  return estimator_impl(h, y, xi, nullptr, h->N, y_out);  // metrics.cpp:50-56
 }
 
 }  // extern "C"

@@ -71,6 +71,23 @@ struct PowerLoopArgs {
   double tol;
 };
 
+// one-shot metric sweeps over a given point (metrics.cu)
+struct MetricsArgs {
+  const double* rowrec;  // N x RQ records of the point (x, 1, y)
+  const double* colrec;  // N x RQ (-xi, -c, 1)
+  const double* V;       // optional: theta1 = s V (local rows) for the duality gap
+  double s;
+  double* part;          // [grid][2]: (sum min(row,0)^2, sum theta.row)
+  long long N, R, r0, ld;
+  int n, S, P;
+};
+cudaError_t launch_records(const double* X, const double* y, const double* xi, long long N, int n,
+                           double* rowrec, double* colrec, cudaStream_t s);
+cudaError_t launch_pair_metrics(const MetricsArgs& a, int grid, cudaStream_t s);
+cudaError_t launch_estimator(const double* Xq, long long Q, const double* X, const double* y,
+                             const double* xi, long long N, int n, double* out, int grid,
+                             cudaStream_t s);
+
 int primal_blocks(long long N);
 cudaError_t launch_gram(const double* X, long long N, int n, double* out, cudaStream_t s);
 int power_loop_grid(int sms);

@@ -154,6 +154,10 @@ class PapgResult:  # papg.hpp:60-69
     loop_seconds: float = 0.0
 
 
+def _f64(a):
+    return np.ascontiguousarray(a, np.float64).reshape(-1)
+
+
 def _raise(status, handle=None, what=""):
     if status == 0:
         return
@@ -317,6 +321,44 @@ class DualSolver:
                                       nat.ptr(hist) if cap else None), self.h)
         return res, y, xi, hist[: min(res.iters, cap)] if cap else np.zeros((0, 8))
 
+    def begin_resume(self, cfg: PapgConfig, use_momentum=True):
+        """Warm start from this handle's theta1 (device-resident), e.g. the next
+        gamma stage of a continuation (runner.cpp:258-259, 305, 322)."""
+        self.cfg = cfg
+        c = cfg.to_c(use_momentum)
+        _raise(self._L.cr_papg_begin_resume(self.h, C.byref(c)), self.h)
+
+    def set_observations(self, ys_shifted):
+        self.ys = np.ascontiguousarray(ys_shifted, np.float64)
+        _raise(self._L.cr_set_observations(self.h, nat.ptr(self.ys)), self.h)
+
+    # -- one-shot metric sweeps (metrics.cpp) --------------------------------
+    def infeasibility(self, y, xi):
+        out = np.empty(2)
+        _raise(self._L.cr_infeasibility(self.h, nat.ptr(_f64(y)), nat.ptr(_f64(xi)),
+                                        nat.ptr(out)), self.h)
+        return float(out[0]), float(out[1])
+
+    def duality_gap(self, y, xi):
+        """theta1 . C eta with this handle's current theta1 (metrics.cpp:17-30)."""
+        out = np.empty(2)
+        _raise(self._L.cr_duality_gap(self.h, nat.ptr(_f64(y)), nat.ptr(_f64(xi)), nat.ptr(out)),
+               self.h)
+        return float(out[0]), float(out[1])
+
+    def evaluate_estimator(self, y, xi, Xq):
+        Xq = _f64(Xq).reshape(-1, self.n)
+        out = np.empty(Xq.shape[0])
+        _raise(self._L.cr_evaluate_estimator(self.h, nat.ptr(_f64(y)), nat.ptr(_f64(xi)),
+                                             nat.ptr(Xq), Xq.shape[0], nat.ptr(out)), self.h)
+        return out
+
+    def repair_feasibility(self, y, xi):
+        out = np.empty(self.N)
+        _raise(self._L.cr_repair_feasibility(self.h, nat.ptr(_f64(y)), nat.ptr(_f64(xi)),
+                                             nat.ptr(out)), self.h)
+        return out
+
     def theta(self):
         out = np.empty((self.row_end - self.row_begin) * (self.N - 1) + self.N)
         _raise(self._L.cr_get_theta(self.h, nat.ptr(out)), self.h)
@@ -372,3 +414,23 @@ def dual_gradient_ascent(prep: PreparedProblem, cfg: PapgConfig | None = None, t
                          want_dual=True) -> PapgResult:
     """Projected dual gradient ascent baseline (papg.cpp:292-296)."""
     return _solve(prep, cfg or PapgConfig(), theta0, False, want_dual)
+
+
+def infeasibility(data: Dataset, eta: PrimalPoint, device=0):
+    """(raw, normalised) |(A1 y + A2 xi)_-| over all N(N-1) rows (metrics.cpp:8-15)."""
+    with DualSolver(data.xs, data.ys, device=device) as s:
+        return s.infeasibility(eta.y, eta.xi)
+
+
+def evaluate_estimator(eta: PrimalPoint, data: Dataset, x_query, device=0):
+    """max_l y_l + xi_l.(x - x_l) (metrics.cpp:32-48); x_query (n,) or (Q, n)."""
+    xq = np.asarray(x_query, np.float64)
+    with DualSolver(data.xs, data.ys, device=device) as s:
+        out = s.evaluate_estimator(eta.y, eta.xi, xq)
+    return float(out[0]) if xq.ndim == 1 else out
+
+
+def repair_feasibility(eta: PrimalPoint, data: Dataset, device=0) -> PrimalPoint:
+    """y'_l = estimator(x_l): an exactly feasible point (metrics.cpp:50-56)."""
+    with DualSolver(data.xs, data.ys, device=device) as s:
+        return PrimalPoint(s.repair_feasibility(eta.y, eta.xi), np.array(eta.xi, copy=True))

@@ -328,3 +328,54 @@ def test_nccl_attached_single_rank(oracle):
             res, y, xi, hist = d.finish()
             assert rel(d.theta(), o.theta) <= TOL_THETA
             assert rel(y, o.y) <= TOL_Y
+
+
+def test_metric_sweeps_match_oracle(oracle):
+    """f3: infeasibility, duality gap, estimator and repair (metrics.cpp:8-56)."""
+    X, ys = instance(oracle, "maxaffine-uniform", 347, 6, 0.1, 41, 7)
+    s, _, _ = oracle.sigma_C(X)
+    o = oracle_run(oracle, X, ys, max_iters=40, gap_norm_tol=-1.0, infeas_norm_tol=-1.0, sigma_C=s)
+    rng = np.random.default_rng(3)
+    with crb.DualSolver(X, ys) as d:
+        d.begin(crb.PapgConfig(max_iters=40, gap_norm_tol=-1.0, infeas_norm_tol=-1.0, sigma_C=s))
+        d.iterate(100)
+        res, y, xi, _ = d.finish()
+        for (py, pxi) in [(o.y, o.xi.reshape(-1)), (rng.normal(size=347), rng.normal(size=347 * 6))]:
+            gi = d.infeasibility(py, pxi)
+            oi = oracle.infeasibility(X, py, pxi)
+            assert gi[0] == pytest.approx(oi[0], rel=1e-11) and gi[1] == pytest.approx(oi[1], rel=1e-11)
+            gg = d.duality_gap(py, pxi)
+            og = oracle.duality_gap(X, o.theta, py, pxi)
+            assert gg[0] == pytest.approx(og[0], rel=1e-9, abs=1e-12 * abs(og[0]) + 1e-300)
+        Xq = rng.uniform(-1.2, 1.2, size=(50, 6))
+        est = d.evaluate_estimator(o.y, o.xi, Xq)
+        ref = np.array([oracle.evaluate_estimator(X, o.y, o.xi, q) for q in Xq])
+        assert np.allclose(est, ref, rtol=1e-13, atol=1e-13)
+        rep = d.repair_feasibility(o.y, o.xi)
+        assert np.allclose(rep, oracle.repair_feasibility(X, o.y, o.xi), rtol=1e-13, atol=1e-13)
+        assert np.all(rep >= o.y - 1e-12)
+
+
+def test_gamma_continuation_resume(oracle):
+    """Device-resident warm start across a gamma stage (runner.cpp:258-259, 305,
+    322): stage 2 at gamma/10 from stage 1's theta1 equals the oracle with
+    theta0 = stage-1 theta."""
+    X, y = oracle.gen_instance("lse-uniform", 240, 5, 0.05, 8, 9)
+    p1 = oracle.prepare(X, y, 1e-3)
+    p2 = oracle.prepare(X, y, 1e-4)
+    s, _, _ = oracle.sigma_C(X)
+    kw1 = dict(max_iters=30, gap_norm_tol=-1.0, infeas_norm_tol=-1.0, sigma_C=s)
+    o1 = oracle_run(oracle, X, p1.ys, gamma=1e-3, **kw1)
+    o2 = oracle_run(oracle, X, p2.ys, gamma=1e-4, theta0=o1.theta, B_theta=0.5, **kw1)
+    with crb.DualSolver(X, p1.ys) as d:
+        d.begin(crb.PapgConfig(gamma=1e-3, **kw1))
+        d.iterate(1 << 20)
+        d.finish()
+        assert rel(d.theta(), o1.theta) <= TOL_THETA
+        d.set_observations(p2.ys)
+        d.begin_resume(crb.PapgConfig(gamma=1e-4, B_theta=0.5, **kw1))
+        done, stopped = d.iterate(1 << 20)
+        res, y2, xi2, _ = d.finish()
+        assert done == o2.iters
+        assert rel(d.theta(), o2.theta) <= TOL_THETA
+        assert rel(y2, o2.y) <= TOL_Y

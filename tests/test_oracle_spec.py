@@ -280,3 +280,29 @@ def test_rng_streams_golden(oracle):
     assert np.array_equal(oracle.rng_draws(1, 2, 8, "raw53"), g["raw_1_2"])
     assert np.array_equal(oracle.rng_draws(0x5EED, 97, 8, "normal"), g["normal_5eed_97"])
     assert np.array_equal(oracle.rng_draws(7, 3, 8, "uniform"), g["uniform_7_3"])
+
+
+# ------------------------------------------------------------- metrics.cpp
+def test_metrics_examples(oracle):  # SPEC.md:425-440 (metrics.cpp:8-56)
+    X = np.array([[0.0], [1.0]])
+    raw, norm = oracle.infeasibility(X, np.zeros(2), np.array([0.0, -1.0]))
+    assert raw == 1.0 and norm == pytest.approx(1 / np.sqrt(2))
+    rng = np.random.default_rng(5)
+    X = rng.normal(size=(15, 3))
+    b = rng.normal(size=3)
+    y = 0.3 + X @ b  # affine point: feasible, estimator reproduces the affine function
+    assert oracle.infeasibility(X, y, np.tile(b, 15))[0] < 1e-12
+    q = rng.normal(size=3)
+    assert oracle.evaluate_estimator(X, y, np.tile(b, 15), q) == pytest.approx(0.3 + q @ b)
+    # repair: y'_l = fhat(x_l) >= y_l. metrics.hpp:38 claims (y', xi) is then
+    # exactly feasible; that holds only when xi_l is the active slope of fhat at
+    # x_l, so we check y' >= y and that it is exact on a consistent point.
+    y2, xi2 = rng.normal(size=15), rng.normal(size=45)
+    yr = oracle.repair_feasibility(X, y2, xi2)
+    assert np.all(yr >= y2 - 1e-12)
+    assert np.allclose(oracle.repair_feasibility(X, y, np.tile(b, 15)), y, atol=1e-12)
+    # duality gap = theta . C eta (metrics.cpp:17-30)
+    th = np.abs(rng.normal(size=15 * 14 + 15))
+    g, gn = oracle.duality_gap(X, th, y2, xi2)
+    assert g == pytest.approx(th @ oracle.apply_C(X, y2, xi2), rel=1e-12)
+    assert gn == pytest.approx(g / (15 * 14))
