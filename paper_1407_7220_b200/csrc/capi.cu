@@ -753,7 +753,7 @@ cr_status begin_impl(cr_handle* h, const cr_papg_config* cfg, const double* thet
         g_alloc_stream = h->st;
         cudaError_t e = cudaSuccess;
         if (e == cudaSuccess)
-          e = dalloc(&h->s_colpart, (size_t)h->small_P * h->ld * (h->n + 1));
+          e = dalloc(&h->s_colpart, (size_t)h->small_P * h->N * (h->n + 1));
         if (e == cudaSuccess) e = dalloc(&h->s_rowpart, (size_t)h->small_S * h->N);
         if (e == cudaSuccess)
           e = dalloc(&h->s_scalpart, (size_t)h->small_grid * kScal);

@@ -100,8 +100,10 @@ __global__ void __launch_bounds__(kSBlock) small_loop_kernel(const SmallArgs a) 
 #pragma unroll
             for (int j = 0; j < NN; ++j) xb[u][j] = __ldcg(xr + j);
             yb[u] = __ldcg(xr + NN + 1);
-            cb[u] = __ldcg(Vc + r * a.ld + col);
-            pb[u] = __ldcg(Vp + r * a.ld + col);
+            // the V pitch ld comes from the TMA kernels' strip width and may be
+            // narrower than this kernel's 32-column strips: touch real columns only
+            cb[u] = valid ? __ldcg(Vc + r * a.ld + col) : 0.0;
+            pb[u] = valid ? __ldcg(Vp + r * a.ld + col) : 0.0;
           }
 #pragma unroll
           for (int u = 0; u < U; ++u) {
@@ -121,7 +123,7 @@ __global__ void __launch_bounds__(kSBlock) small_loop_kernel(const SmallArgs a) 
             }
             const double uu = fma(-row, invL, th2);
             const double v = uu > 0.0 ? uu : 0.0;
-            __stcg(Vp + r * a.ld + col, v);
+            if (valid) __stcg(Vp + r * a.ld + col, v);
             vv = fma(v, v, vv);
             vr = fma(v, row, vr);
             tr = fma(th2, row, tr);
@@ -136,10 +138,12 @@ __global__ void __launch_bounds__(kSBlock) small_loop_kernel(const SmallArgs a) 
             if (lane == 0) __stcg(a.rowpart + r * a.S + strip, rs);  // [N][S]
           }
         }
-        // [ld][n+1][P]: the P partials of one column entry are contiguous
-        double* dst = a.colpart + (col * (NN + 1)) * a.P + chunk;
+        // [N][n+1][P]: the P partials of one column entry are contiguous
+        if (valid) {
+          double* dst = a.colpart + (col * (NN + 1)) * a.P + chunk;
 #pragma unroll
-        for (int j = 0; j <= NN; ++j) __stcg(dst + (long long)j * a.P, acc[j]);
+          for (int j = 0; j <= NN; ++j) __stcg(dst + (long long)j * a.P, acc[j]);
+        }
         wsc[0] += vv;
         wsc[1] += vr;
         wsc[2] += tr;

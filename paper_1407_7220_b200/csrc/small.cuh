@@ -11,7 +11,7 @@ struct SmallArgs {
   PrimalArgs pa;       // K2 arguments (mode 0): records, aggregates, vpos, k2part
   double* V0;
   double* V1;
-  double* colpart;     // [ld][n+1][P]
+  double* colpart;     // [N][n+1][P]
   double* rowpart;     // [N][S]
   double* scalpart;    // [grid][kScal]
   double* k2part;      // [grid][kK2Scal]

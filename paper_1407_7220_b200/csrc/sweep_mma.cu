@@ -13,7 +13,7 @@
 // and {1,3,5,7} makes exactly those two values the B fragments of the two
 // aggregation MMAs (B[k=lane%4][n=lane/4]), so v never moves between lanes.
 //
-// CTA: 7 consumer warps x (4 tiles of 8 columns) = 224 columns, 1 producer
+// CTA: 15 consumer warps x (2 tiles of 8 columns) = 240 columns, 1 producer
 // warp streaming 8-row stages of V, V' and the row records through a 4-deep
 // cp.async.bulk / mbarrier ring (row pitch padded by 16 B: conflict-free
 // column-fragment reads). Work split, partial layouts and row-sum combine are
@@ -29,18 +29,30 @@ namespace crb {
 
 namespace {
 
-constexpr int kCW = 7;                 // consumer warps (+1 producer = 8: 255-register cap)
-constexpr int kCT = 4;                 // 8-column MMA tiles per warp
-constexpr int kW = 8 * kCT;            // columns per warp
-constexpr int kTC = kCW * kW;          // columns per CTA tile (224)
-constexpr int kTCP = kTC + 2;          // smem row pitch of V stages (doubles)
+// CTA geometry per n (measured, profiles/): n <= 12: 7 consumer warps x 4
+// tiles (8 warps -> 255-register cap); n > 12: 15 consumer warps x 2 tiles
+// (16 warps, 128 registers) -- more warps hide the longer DMMA chains.
+template <int NN>
+__host__ __device__ constexpr int mma_cw() { return NN <= 12 ? 7 : 15; }  // consumer warps
+template <int NN>
+__host__ __device__ constexpr int mma_ct() { return NN <= 12 ? 4 : 2; }   // 8-col tiles / warp
+template <int NN>
+__host__ __device__ constexpr int mma_threads() { return (mma_cw<NN>() + 1) * 32; }
+// kW columns per warp, kTC per CTA tile, kTCP smem row pitch (+16 B: conflict-free)
+#define CRB_GEO(NN)                              \
+  constexpr int kCW = mma_cw<NN>();              \
+  constexpr int kCT = mma_ct<NN>();              \
+  constexpr int kW = 8 * kCT;                    \
+  constexpr int kTC = kCW * kW;                  \
+  constexpr int kTCP = kTC + 2;                  \
+  constexpr int kThreads = (kCW + 1) * 32;       \
+  (void)kThreads;
 constexpr int kTR = 8;                 // rows per stage (one MMA row block)
 #ifndef CRB_MMA_CTAS_PER_SM
 #define CRB_MMA_CTAS_PER_SM 1
 #endif
 constexpr int kMinCtas = CRB_MMA_CTAS_PER_SM;  // 2: 128-register cap, 3-stage ring
 constexpr int kNS = kMinCtas == 2 ? 3 : 4;     // stages
-constexpr int kThreads = (kCW + 1) * 32;
 constexpr int kWin = 32;               // row-sum window (rows)
 
 template <int NN>
@@ -49,11 +61,11 @@ template <int NN>
 __host__ __device__ constexpr int fblocks() { return ((NN + 1) + 7) / 8; }
 template <int NN>
 __host__ __device__ constexpr int stage_doubles() {
-  return 2 * kTR * kTCP + kTR * rec_pitch(NN);
+  return 2 * kTR * (mma_cw<NN>() * 8 * mma_ct<NN>() + 2) + kTR * rec_pitch(NN);
 }
 template <int NN>
 __host__ __device__ constexpr int smem_bytes() {
-  return kNS * stage_doubles<NN>() * 8 + 2 * kCW * kWin * 8 + 2 * kNS * 8;
+  return kNS * stage_doubles<NN>() * 8 + 2 * mma_cw<NN>() * kWin * 8 + 2 * kNS * 8;
 }
 
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
@@ -74,9 +86,10 @@ template <int NN, int MODE, bool MASK, bool UNIT>
 __device__ __forceinline__ void mma_stage(const double* __restrict__ sv, const double* __restrict__ svp,
                                           const double* __restrict__ srec, double* gout,
                                           long long ld, long long gcol0, long long grow0, int nr,
-                                          int lane, const double (&A)[kCT][ksteps<NN>()],
-                                          double (&D)[kCT][fblocks<NN>()][2], const MCoef& cf,
-                                          MScal& sc, double (&rs)[2]) {
+                                          int lane, const double (&A)[mma_ct<NN>()][ksteps<NN>()],
+                                          double (&D)[mma_ct<NN>()][fblocks<NN>()][2],
+                                          const MCoef& cf, MScal& sc, double (&rs)[2]) {
+  CRB_GEO(NN)
   constexpr int KS = ksteps<NN>();
   constexpr int FB = fblocks<NN>();
   constexpr int RQ = rec_pitch(NN);
@@ -142,7 +155,8 @@ __device__ __forceinline__ void mma_stage(const double* __restrict__ sv, const d
 }
 
 template <int NN, int MODE>
-__global__ void __launch_bounds__(kThreads, kMinCtas) sweep_mma_kernel(const SweepArgs a) {
+__global__ void __launch_bounds__(mma_threads<NN>(), kMinCtas) sweep_mma_kernel(const SweepArgs a) {
+  CRB_GEO(NN)
   constexpr int KS = ksteps<NN>();
   constexpr int FB = fblocks<NN>();
   constexpr int RQ = rec_pitch(NN);
@@ -343,6 +357,7 @@ __global__ void __launch_bounds__(kThreads, kMinCtas) sweep_mma_kernel(const Swe
 
 template <int NN>
 SweepKernelInfo info_for(int mode) {
+  CRB_GEO(NN)
   SweepKernelInfo inf{};
   inf.fn = mode == kModePapg ? (const void*)sweep_mma_kernel<NN, kModePapg>
                              : (const void*)sweep_mma_kernel<NN, kModePower>;

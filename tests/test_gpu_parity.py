@@ -379,3 +379,16 @@ def test_gamma_continuation_resume(oracle):
         assert done == o2.iters
         assert rel(d.theta(), o2.theta) <= TOL_THETA
         assert rel(y2, o2.y) <= TOL_Y
+
+
+@pytest.mark.parametrize("path", ["small", "dfma", "mma"])
+@pytest.mark.parametrize("N,n", [(2, 1), (3, 2), (17, 16), (21, 20), (25, 24), (33, 5), (65, 13)])
+def test_tiny_and_ragged_sizes(oracle, monkeypatch, path, N, n):
+    """Edge sizes: N = n + 1, N below one strip/tile, ragged last strips."""
+    monkeypatch.setenv("CRB_SMALL", "1" if path == "small" else "0")
+    if path != "small":
+        monkeypatch.setenv("CRB_SWEEP", path)
+    X, ys = instance(oracle, "sqnorm-uniform", N, n, 0.1, 77)
+    s, _, _ = oracle.sigma_C(X)
+    kw = dict(max_iters=25, gap_norm_tol=-1.0, infeas_norm_tol=-1.0, sigma_C=s)
+    assert_parity(gpu_run(X, ys, **kw), oracle_run(oracle, X, ys, **kw))
