@@ -55,8 +55,12 @@ constexpr int kMinCtas = CRB_MMA_CTAS_PER_SM;  // 2: 128-register cap, 3-stage r
 constexpr int kNS = kMinCtas == 2 ? 3 : 4;     // stages
 constexpr int kWin = 32;               // row-sum window (rows)
 
+// Residual K: the n features plus (1, y) with (-c, 1) folded in -- unless
+// dropping those two columns saves a k-step, then y - c is added with DADDs.
 template <int NN>
-__host__ __device__ constexpr int ksteps() { return ((NN + 2) + 3) / 4; }
+__host__ __device__ constexpr bool split_yc() { return (NN + 3) / 4 < (NN + 5) / 4; }
+template <int NN>
+__host__ __device__ constexpr int ksteps() { return split_yc<NN>() ? (NN + 3) / 4 : (NN + 5) / 4; }
 template <int NN>
 __host__ __device__ constexpr int fblocks() { return ((NN + 1) + 7) / 8; }
 template <int NN>
@@ -88,13 +92,20 @@ __device__ __forceinline__ void mma_stage(const double* __restrict__ sv, const d
                                           long long ld, long long gcol0, long long grow0, int nr,
                                           int lane, const double (&A)[mma_ct<NN>()][ksteps<NN>()],
                                           double (&D)[mma_ct<NN>()][fblocks<NN>()][2],
-                                          const MCoef& cf, MScal& sc, double (&rs)[2]) {
+                                          const double (&Cc)[mma_ct<NN>()], const MCoef& cf,
+                                          MScal& sc, double (&rs)[2]) {
   CRB_GEO(NN)
   constexpr int KS = ksteps<NN>();
   constexpr int FB = fblocks<NN>();
   constexpr int RQ = rec_pitch(NN);
+  constexpr bool SPLIT = split_yc<NN>();
   const int q = lane & 3;
   const int c8 = lane >> 2;
+  double yr[2] = {0.0, 0.0};  // y of rows 2q, 2q+1 (split form)
+  if (SPLIT) {
+    yr[0] = srec[(2 * q) * RQ + NN + 1];
+    yr[1] = srec[(2 * q + 1) * RQ + NN + 1];
+  }
   // residual B fragments: X'[row c8][k]
   double B[KS];
 #pragma unroll
@@ -121,6 +132,7 @@ __device__ __forceinline__ void mma_stage(const double* __restrict__ sv, const d
       const int rr = 2 * q + j;
       const bool rv = !MASK || rr < nr;  // row present in this (partial) stage
       double row = j == 0 ? d0 : d1;
+      if (SPLIT) row += yr[j] + Cc[ct];  // y_l1 - c_l2 (Cc holds -c_l2)
       if (MASK && (gcol0 + cl == grow0 + rr || !rv)) row = 0.0;
       if (MODE == kModePapg) {
         const double c1 = sv[rr * kTCP + cl];
@@ -245,13 +257,17 @@ __global__ void __launch_bounds__(mma_threads<NN>(), kMinCtas) sweep_mma_kernel(
     // residual A fragments: Xi'[col][k] (zero for pad columns -> row = 0 there)
     double A[kCT][KS];
     double D[kCT][FB][2];
+    double Cc[kCT];
 #pragma unroll
     for (int ct = 0; ct < kCT; ++ct) {
       const long long col = gcol0 + ct * 8 + c8;
       const bool cv = active && col < a.N;
 #pragma unroll
-      for (int ks = 0; ks < KS; ++ks)
-        A[ct][ks] = cv ? __ldg(a.colrec + col * RQ + ks * 4 + q) : 0.0;
+      for (int ks = 0; ks < KS; ++ks) {
+        const int k = ks * 4 + q;
+        A[ct][ks] = (cv && (!split_yc<NN>() || k < NN)) ? __ldg(a.colrec + col * RQ + k) : 0.0;
+      }
+      Cc[ct] = cv ? __ldg(a.colrec + col * RQ + NN) : 0.0;
 #pragma unroll
       for (int fb = 0; fb < FB; ++fb) D[ct][fb][0] = D[ct][fb][1] = 0.0;
     }
@@ -269,22 +285,22 @@ __global__ void __launch_bounds__(mma_threads<NN>(), kMinCtas) sweep_mma_kernel(
         const double* srec = st + 2 * kTR * kTCP;
         double* gout = Vp + r * a.ld + gcol0;
         const long long grow0 = a.r0 + r;
-        // warp-uniform: no diagonal in this 8 x 32 block and a full stage
+        // warp-uniform: no diagonal in this 8-row block of the warp's columns, full stage
         const bool clean = nr == kTR && (grow0 + kTR <= gcol0 || grow0 >= gcol0 + kW);
         if (clean) {
           if (unit_scale)
             mma_stage<NN, MODE, false, true>(sv, svp, srec, gout, a.ld, gcol0, grow0, nr, lane, A,
-                                             D, cf, sc, rsj);
+                                             D, Cc, cf, sc, rsj);
           else
             mma_stage<NN, MODE, false, false>(sv, svp, srec, gout, a.ld, gcol0, grow0, nr, lane,
-                                              A, D, cf, sc, rsj);
+                                              A, D, Cc, cf, sc, rsj);
         } else {
           if (unit_scale)
             mma_stage<NN, MODE, true, true>(sv, svp, srec, gout, a.ld, gcol0, grow0, nr, lane, A,
-                                            D, cf, sc, rsj);
+                                             D, Cc, cf, sc, rsj);
           else
             mma_stage<NN, MODE, true, false>(sv, svp, srec, gout, a.ld, gcol0, grow0, nr, lane, A,
-                                             D, cf, sc, rsj);
+                                             D, Cc, cf, sc, rsj);
         }
       }
       __syncwarp();
