@@ -320,7 +320,7 @@ def run_ours(args):
         cpu = {"value": rate, "unit": "pair-updates/s", "cores": threads, "kind": "port",
                "sample": sample}
         if "time_to_tolerance" in extras:
-            extras["time_to_tolerance"]["cpu_port_estimate_s"] = (
+            extras["time_to_tolerance"]["cpu_port_iterations_only_s"] = (
                 extras["time_to_tolerance"]["iterations"] * N * N / rate)
 
     if rank == 0:
