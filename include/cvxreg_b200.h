@@ -18,6 +18,10 @@
  *   cr_gen_instance      gen_instance                            src/testgen.cpp:36-87
  *   cr_prepare_problem   prepare_problem                         src/preprocess.cpp:50-65
  *   cr_certificate       certificate_for_iterate                 src/papg.cpp:298-303
+ *   cr_alcc_solve        alcc_solve (standalone ALCC)            include/cvxreg/alcc.hpp:134-136
+ *                        (alcc_core src/alcc.cpp:54-191, MAPG src/engines.cpp:57-106)
+ *   cr_alcc_multiplier   AlccResult::multiplier                  include/cvxreg/alcc.hpp:110-118
+ *   cr_sigma_A           estimate_sigma_max(op_A1 / op_A2)       src/operators.cpp:341-351
  *
  * Threading: a handle is confined to one host thread. Distinct handles may
  * be driven concurrently. Sharded runs use one handle (and one process) per
@@ -170,6 +174,61 @@ cr_status cr_evaluate_estimator(cr_handle *h, const double *y, const double *xi,
                                 const double *Xq, int64_t Q, double *out);
 /* y'_l = estimator(x_l), an exactly feasible point (metrics.cpp:50-56). */
 cr_status cr_repair_feasibility(cr_handle *h, const double *y, const double *xi, double *y_out);
+
+/* ---- standalone ALCC (alcc_solve) ------------------ */
+/* AlccConfig (alcc.hpp:71-83) plus the solve's inputs that the reference
+   takes from ProblemBounds / estimate_sigma_max. */
+typedef struct {
+  double mu1;              /* 1 */
+  double tau1_scale;       /* 1e-2 */
+  double alpha1_scale;     /* 1e-3 */
+  double c;                /* 5 (> 1) */
+  double kappa;            /* 0.5 (> 0) */
+  int64_t max_outer;       /* 30 */
+  int64_t mapg_cap;        /* 200000 */
+  double infeas_norm_tol;  /* 1e-1 */
+  double gap_norm_tol;     /* 1e-6 */
+  double max_seconds;      /* inf */
+  int32_t record_history;  /* 1 */
+  int32_t pad_;
+  double sigma_A1;         /* > 0: inject sigma_max(A1), else estimated on the device */
+  double sigma_A2;         /* > 0: inject sigma_max(A2) */
+  double Bbar_y;           /* ball radii (ProblemBounds, preprocess.cpp:9-48) */
+  double Bbar_xi;
+} cr_alcc_config;
+
+/* AlccResult scalars (alcc.hpp:110-118) + SolveReport */
+typedef struct {
+  int64_t outer_iters;
+  int64_t mapg_iters_total;
+  int32_t reason;
+  int32_t hit_cap_any;     /* some MAPG call ran to its l_max */
+  int32_t sigma_A1_iters;  /* power iterations (0 if injected) */
+  int32_t sigma_A2_iters;
+  double certified_gap;
+  double infeas_raw;
+  double gap_raw;
+  double objective;
+  double wall_seconds;
+  double sigma_A1;
+  double sigma_A2;
+  double sigma_seconds;
+} cr_alcc_result;
+
+/* sigma_max(A1) (which = 1) or sigma_max(A2) (which = 2) by the reference's
+   power method on the full row set (closed-form O(N n^2) steps). */
+cr_status cr_sigma_A(cr_handle *h, int32_t which, double tol, int32_t max_iters, double *sigma,
+                     int32_t *iters, int32_t *converged);
+/* alcc_solve from the warm point (warm_y: N shifted frame, warm_xi: N*n),
+   centres (ybar, 0). Unsharded handles only; overwrites any P-APG state on the
+   handle. y_out / xi_out / history (max_outer) / mapg_iters (max_outer) may be
+   NULL. */
+cr_status cr_alcc_solve(cr_handle *h, const cr_alcc_config *cfg, const double *warm_y,
+                        const double *warm_xi, double *y_out, double *xi_out,
+                        cr_snapshot *history, int64_t *mapg_iters, cr_alcc_result *res);
+/* lambda = mu_k (theta_k - R(y, xi))_+ of the last outer step for pair rows
+   l1 in [row_begin, row_end), canonical order ((row_end-row_begin) x (N-1)). */
+cr_status cr_alcc_multiplier(cr_handle *h, int64_t row_begin, int64_t row_end, double *out);
 
 /* ---- host utilities (no device) ----------------------------------------- */
 /* kinds: 0 quadratic, 1 exponential, 2 affine-noiseless, 3 custom-1d

@@ -821,3 +821,304 @@ int cro_papg(const double *X, const double *ys, int64_t N, int64_t n, const cro_
   free(c.q_y); free(c.q_xi); free(c.ey); free(c.exi);
   return rc;
 }
+
+/* ================================================= standalone ALCC (f1) */
+/* Row set of alcc_solve (alcc.cpp:193-208): all N(N-1) cross rows
+   R(y, xi) = A1 y + A2 xi in canonical (l1, l2) order (FullRows,
+   alcc.hpp:32-48 -> operators.cpp apply_rows / rows_adjoint). The forward and
+   adjoint reuse the op_C restatement: C's pos rows are dropped on the way out
+   and fed zeros on the way in. */
+typedef struct {
+  const double *X;
+  int64_t N, n;
+  int threads;
+  double *rowbuf; /* N(N-1) + N */
+  double *zbuf;   /* N(N-1) + N, pos part held at 0 */
+} rows_ctx;
+
+static void rows_forward(rows_ctx *r, const double *y, const double *xi, double *out) {
+  if (r->threads > 1) apply_C_omp(r->X, r->N, r->n, y, xi, r->rowbuf, r->threads);
+  else cro_apply_C(r->X, r->N, r->n, y, xi, r->rowbuf);
+  memcpy(out, r->rowbuf, sizeof(double) * (size_t)(r->N * (r->N - 1)));
+}
+static void rows_adjoint(rows_ctx *r, const double *z, double *out_y, double *out_xi) {
+  const int64_t m = r->N * (r->N - 1);
+  memcpy(r->zbuf, z, sizeof(double) * (size_t)m);
+  memset(r->zbuf + m, 0, sizeof(double) * (size_t)r->N);
+  if (r->threads > 1) apply_C_T_omp(r->X, r->N, r->n, r->zbuf, out_y, out_xi, r->threads);
+  else cro_apply_C_T(r->X, r->N, r->n, r->zbuf, out_y, out_xi);
+}
+
+/* operators.cpp:302-339 on op_A1 (:341-345, cols N) or op_A2 (:347-351, cols N n) */
+int cro_sigma_A(const double *X, int64_t N, int64_t n, int which, double tol, int max_iters,
+                double *sigma, int *iters, int *converged) {
+  if (N < 2 || n < 1 || (which != 1 && which != 2)) return -1;
+  const int64_t m = N * (N - 1);
+  const int64_t cols = which == 1 ? N : N * n;
+  double *v = (double *)malloc(sizeof(double) * (size_t)cols);
+  double *u = (double *)malloc(sizeof(double) * (size_t)(N * (n + 1)));
+  double *w = (double *)malloc(sizeof(double) * (size_t)m);
+  double *zy = (double *)calloc((size_t)N, sizeof(double));
+  double *zxi = (double *)calloc((size_t)(N * n), sizeof(double));
+  rows_ctx rc = {X, N, n, 1, (double *)malloc(sizeof(double) * (size_t)(m + N)),
+                 (double *)malloc(sizeof(double) * (size_t)(m + N))};
+  int ret = 0;
+  if (!v || !u || !w || !zy || !zxi || !rc.rowbuf || !rc.zbuf) { ret = -2; goto done; }
+  {
+    xo256 g = rng_stream(0x5eedULL, 97);
+    for (int64_t k = 0; k < cols; ++k) v[k] = xo_normal(&g);
+    const double nv = sqrt(dot(v, v, cols));
+    for (int64_t k = 0; k < cols; ++k) v[k] /= nv;
+    double lambda_prev = 0;
+    *iters = 0;
+    *converged = 1;
+    for (int it = 1; it <= max_iters; ++it) {
+      /* op.forward: A1 v = R(v, 0) or A2 v = R(0, v) */
+      if (which == 1) rows_forward(&rc, v, zxi, w);
+      else rows_forward(&rc, zy, v, w);
+      const double lambda = dot(w, w, m);
+      rows_adjoint(&rc, w, u, u + N); /* A1^T w = u[0..N), A2^T w = u[N..) */
+      const double *uu = which == 1 ? u : u + N;
+      const double norm_u = sqrt(dot(uu, uu, cols));
+      if (norm_u == 0 || lambda == 0) {
+        *sigma = 0;
+        *iters = it;
+        goto done;
+      }
+      for (int64_t k = 0; k < cols; ++k) v[k] = uu[k] / norm_u;
+      *iters = it;
+      if (it > 1 && fabs(lambda - lambda_prev) <= tol * lambda) {
+        *sigma = sqrt(lambda) * 1.01;
+        *converged = 1;
+        goto done;
+      }
+      lambda_prev = lambda;
+    }
+    *sigma = sqrt(lambda_prev) * 1.10;
+    *converged = 0;
+  }
+done:
+  free(v); free(u); free(w); free(zy); free(zxi); free(rc.rowbuf); free(rc.zbuf);
+  return ret;
+}
+
+/* projections.hpp:22-26 */
+static void project_ball_c(double *v, const double *center, int64_t len, double radius) {
+  double ss = 0;
+  for (int64_t i = 0; i < len; ++i) {
+    const double d = v[i] - (center ? center[i] : 0.0);
+    ss += d * d;
+  }
+  const double dist = sqrt(ss);
+  if (dist > radius) {
+    const double f = radius / dist;
+    for (int64_t i = 0; i < len; ++i) {
+      const double c = center ? center[i] : 0.0;
+      v[i] = c + f * (v[i] - c);
+    }
+  }
+}
+
+/* PenaltyOracle::eval (alcc.cpp:33-47), standalone centres (ybar, 0) */
+typedef struct {
+  rows_ctx *rows;
+  const double *cy;
+  const double *theta; /* m */
+  double mu, gamma;
+  int64_t N, n;
+  double *res, *vneg, *ay, *axi; /* scratch */
+} pen_ctx;
+
+static void penalty_grad(pen_ctx *p, const double *y, const double *xi, double *gy,
+                         double *gxi) {
+  const int64_t m = p->N * (p->N - 1);
+  rows_forward(p->rows, y, xi, p->res);
+  for (int64_t i = 0; i < m; ++i) {
+    const double r = p->res[i] - p->theta[i];
+    p->vneg[i] = -r > 0.0 ? -r : 0.0;
+  }
+  rows_adjoint(p->rows, p->vneg, p->ay, p->axi);
+  for (int64_t i = 0; i < p->N; ++i) gy[i] = (y[i] - p->cy[i]) / p->mu - p->ay[i];
+  const double gm = p->gamma / p->mu;
+  for (int64_t i = 0; i < p->N * p->n; ++i) gxi[i] = gm * xi[i] - p->axi[i];
+}
+
+int cro_alcc(const double *X, const double *ys, int64_t N, int64_t n, double gamma,
+             double Bbar_y, double Bbar_xi, double sigma_A1, double sigma_A2,
+             const double *warm_y, const double *warm_xi, const cro_alcc_config *cfg,
+             cro_alcc_result *res) {
+  const double start = now_seconds();
+  if (N < 2 || n < 1 || !(gamma > 0)) return -1;
+  if (!(cfg->c > 1) || !(cfg->kappa > 0) || !(cfg->mu1 > 0)) return -1; /* alcc.cpp:59-61 */
+  const int threads = cfg->threads > 1 ? cfg->threads : 1;
+  const int64_t m = N * (N - 1);
+  const int64_t Nn = N * n;
+  if (!(sigma_A1 > 0)) {
+    int it, cv;
+    if (cro_sigma_A(X, N, n, 1, 1e-6, 5000, &sigma_A1, &it, &cv)) return -2;
+  }
+  if (!(sigma_A2 > 0)) {
+    int it, cv;
+    if (cro_sigma_A(X, N, n, 2, 1e-6, 5000, &sigma_A2, &it, &cv)) return -2;
+  }
+  res->sigma_A1 = sigma_A1;
+  res->sigma_A2 = sigma_A2;
+
+  rows_ctx rc = {X, N, n, threads, (double *)malloc(sizeof(double) * (size_t)(m + N)),
+                 (double *)malloc(sizeof(double) * (size_t)(m + N))};
+  double *theta = (double *)calloc((size_t)m, sizeof(double));
+  double *res_v = (double *)malloc(sizeof(double) * (size_t)m);
+  double *vneg = (double *)malloc(sizeof(double) * (size_t)m);
+  double *work = (double *)malloc(sizeof(double) * (size_t)m);
+  /* point buffers: y, xi, y1, y1_prev, y2, xi1, xi1_prev, xi2, gy, gxi, ay, axi */
+  double *pb = (double *)malloc(sizeof(double) * (size_t)(6 * N + 6 * Nn));
+  if (!rc.rowbuf || !rc.zbuf || !theta || !res_v || !vneg || !work || !pb) return -3;
+  double *y = pb, *y1 = pb + N, *y1p = pb + 2 * N, *y2 = pb + 3 * N, *gy = pb + 4 * N,
+         *ay = pb + 5 * N;
+  double *xi = pb + 6 * N, *xi1 = xi + Nn, *xi1p = xi + 2 * Nn, *xi2 = xi + 3 * Nn,
+         *gxi = xi + 4 * Nn, *axi = xi + 5 * Nn;
+
+  double mu = cfg->mu1;
+  memcpy(y, warm_y, sizeof(double) * (size_t)N); /* alcc.cpp:68-69 */
+  memcpy(xi, warm_xi, sizeof(double) * (size_t)Nn);
+  project_ball_c(y, ys, N, Bbar_y);
+  project_ball_c(xi, NULL, Nn, Bbar_xi);
+
+  pen_ctx pen = {&rc, ys, theta, mu, gamma, N, n, work, vneg, ay, axi};
+  double tau, alpha_y, alpha_xi;
+  { /* alcc.cpp:75-84: P_1 at the start point */
+    penalty_grad(&pen, y, xi, gy, gxi);
+    double sy = 0, sx = 0, sv = 0;
+    for (int64_t i = 0; i < N; ++i) sy += (y[i] - ys[i]) * (y[i] - ys[i]);
+    for (int64_t i = 0; i < Nn; ++i) sx += xi[i] * xi[i];
+    for (int64_t i = 0; i < m; ++i) sv += vneg[i] * vneg[i];
+    const double p1 = sy / (2.0 * mu) + gamma * sx / (2.0 * mu) + 0.5 * sv;
+    if (!isfinite(p1)) return -4;
+    tau = cfg->tau1_scale * p1;
+    if (tau < 1e-16) tau = 1e-16;
+    alpha_y = alpha_xi = cfg->alpha1_scale * (Bbar_y + Bbar_xi);
+  }
+  /* rows_center = R(ybar, 0): needed only through lambda . rows_center */
+  double *rows_center = (double *)malloc(sizeof(double) * (size_t)m);
+  memset(gxi, 0, sizeof(double) * (size_t)Nn);
+  rows_forward(&rc, ys, gxi, rows_center);
+
+  res->reason = CRO_ITER_BUDGET;
+  res->mapg_iters_total = 0;
+  res->outer_iters = 0;
+  res->hit_cap_any = 0;
+  int rcode = 0;
+  for (int64_t k = 1; k <= cfg->max_outer; ++k) {
+    const double L_y = 1.0 / mu + sigma_A1 * sigma_A1; /* :101-102 */
+    const double L_xi = gamma / mu + sigma_A2 * sigma_A2;
+    const double lmax_real = 4.0 * sqrt((L_y * Bbar_y * Bbar_y + L_xi * Bbar_xi * Bbar_xi) / tau);
+    int64_t lmax = (int64_t)ceil(lmax_real);
+    if (lmax < 10) lmax = 10;
+    if (lmax > cfg->mapg_cap) lmax = cfg->mapg_cap;
+    pen.mu = mu;
+
+    /* mapg (engines.cpp:57-106) from (y, xi) */
+    memcpy(y1, y, sizeof(double) * (size_t)N);
+    memcpy(y1p, y, sizeof(double) * (size_t)N);
+    memcpy(y2, y, sizeof(double) * (size_t)N);
+    memcpy(xi1, xi, sizeof(double) * (size_t)Nn);
+    memcpy(xi1p, xi, sizeof(double) * (size_t)Nn);
+    memcpy(xi2, xi, sizeof(double) * (size_t)Nn);
+    double t = 1.0;
+    int64_t inner = 0;
+    for (int64_t ell = 1; ell <= lmax; ++ell) {
+      penalty_grad(&pen, y2, xi2, gy, gxi);
+      for (int64_t i = 0; i < N; ++i) if (!isfinite(gy[i])) { rcode = -5; goto out; }
+      for (int64_t i = 0; i < Nn; ++i) if (!isfinite(gxi[i])) { rcode = -5; goto out; }
+      { double *tmp = y1p; y1p = y1; y1 = tmp; }
+      for (int64_t i = 0; i < N; ++i) y1[i] = y2[i] - gy[i] / L_y;
+      project_ball_c(y1, ys, N, Bbar_y);
+      { double *tmp = xi1p; xi1p = xi1; xi1 = tmp; }
+      for (int64_t i = 0; i < Nn; ++i) xi1[i] = xi2[i] - gxi[i] / L_xi;
+      project_ball_c(xi1, NULL, Nn, Bbar_xi);
+      inner = ell;
+      double dy = 0, dx = 0;
+      for (int64_t i = 0; i < N; ++i) dy += (y1[i] - y2[i]) * (y1[i] - y2[i]);
+      for (int64_t i = 0; i < Nn; ++i) dx += (xi1[i] - xi2[i]) * (xi1[i] - xi2[i]);
+      const double disp_y = sqrt(dy), disp_xi = sqrt(dx);
+      const double t_next = cro_momentum_next(t);
+      const double beta = (t - 1.0) / t_next;
+      for (int64_t i = 0; i < N; ++i) y2[i] = y1[i] + beta * (y1[i] - y1p[i]);
+      for (int64_t i = 0; i < Nn; ++i) xi2[i] = xi1[i] + beta * (xi1[i] - xi1p[i]);
+      t = t_next;
+      if (disp_y <= alpha_y && disp_xi <= alpha_xi) break;
+      if (ell == lmax) res->hit_cap_any = 1;
+    }
+    memcpy(y, y1, sizeof(double) * (size_t)N);
+    memcpy(xi, xi1, sizeof(double) * (size_t)Nn);
+    res->mapg_iters_total += inner;
+    if (res->mapg_iters) res->mapg_iters[k - 1] = inner;
+
+    /* :124-160 */
+    rows_forward(&rc, y, xi, res_v);
+    double nn = 0, gap_raw = 0, lc = 0;
+    for (int64_t i = 0; i < m; ++i) {
+      const double d = theta[i] - res_v[i];
+      vneg[i] = d > 0.0 ? d : 0.0;
+      const double lam = mu * vneg[i];
+      work[i] = lam;
+      const double neg = -res_v[i] > 0.0 ? -res_v[i] : 0.0;
+      nn += neg * neg;
+      gap_raw += lam * res_v[i];
+      lc += lam * rows_center[i];
+    }
+    const double infeas_raw = sqrt(nn);
+    rows_adjoint(&rc, work, ay, axi);
+    const double dual_value = -0.5 * dot(ay, ay, N) - dot(axi, axi, Nn) / (2.0 * gamma) - lc;
+    double sy = 0, sx = 0;
+    for (int64_t i = 0; i < N; ++i) sy += (y[i] - ys[i]) * (y[i] - ys[i]);
+    for (int64_t i = 0; i < Nn; ++i) sx += xi[i] * xi[i];
+    const double primal_value = 0.5 * sy + 0.5 * gamma * sx;
+    res->certified_gap = primal_value - dual_value;
+    res->infeas_raw = infeas_raw;
+    res->gap_raw = gap_raw;
+    res->outer_iters = k;
+    const double infeas_norm = infeas_raw / sqrt((double)m);
+    const double gap_norm = gap_raw / (double)m;
+    if (cfg->record_history && res->history) {
+      double *h = res->history + (k - 1) * 8;
+      h[0] = (double)k;
+      h[1] = 0.5 * sy;
+      h[2] = primal_value;
+      h[3] = infeas_raw;
+      h[4] = infeas_norm;
+      h[5] = gap_raw;
+      h[6] = gap_norm;
+      h[7] = now_seconds() - start;
+    }
+    if (res->multiplier) memcpy(res->multiplier, work, sizeof(double) * (size_t)m);
+    if (infeas_norm <= cfg->infeas_norm_tol && fabs(gap_norm) <= cfg->gap_norm_tol) {
+      res->reason = CRO_THRESHOLDS;
+      break;
+    }
+    if (now_seconds() - start > cfg->max_seconds) {
+      res->reason = CRO_TIME_BUDGET;
+      break;
+    }
+    for (int64_t i = 0; i < m; ++i) theta[i] = vneg[i] / cfg->c; /* :176-183 */
+    mu *= cfg->c;
+    const double decay = pow(cfg->c * pow((double)k, 1.0 + cfg->kappa), 2.0);
+    tau /= decay;
+    alpha_y /= decay;
+    alpha_xi /= decay;
+  }
+out:
+  if (rcode == 0) {
+    if (res->y) memcpy(res->y, y, sizeof(double) * (size_t)N);
+    if (res->xi) memcpy(res->xi, xi, sizeof(double) * (size_t)Nn);
+    double sy = 0;
+    for (int64_t i = 0; i < N; ++i) sy += (y[i] - ys[i]) * (y[i] - ys[i]);
+    res->objective = 0.5 * sy;
+  } else {
+    res->reason = CRO_ERROR;
+  }
+  res->wall_seconds = now_seconds() - start;
+  free(rc.rowbuf); free(rc.zbuf); free(theta); free(res_v); free(vneg); free(work); free(pb);
+  free(rows_center);
+  return rcode;
+}

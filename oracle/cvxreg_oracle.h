@@ -122,6 +122,36 @@ double cro_momentum_next(double t);
 void cro_certificate(double gamma, double delta, double B_xi, double sigma, double out2[2]);
 int64_t cro_cross_position(int64_t N, int64_t K, int64_t l1, int64_t l2);
 
+/* ---- standalone ALCC (alcc.cpp:54-208, engines.cpp:57-106) ---- */
+typedef struct {           /* alcc.hpp:71-83 */
+  double mu1, tau1_scale, alpha1_scale, c, kappa;
+  int64_t max_outer, mapg_cap;
+  double infeas_norm_tol, gap_norm_tol, max_seconds;
+  int32_t record_history;
+  int32_t threads;         /* <= 1: literal loops; > 1: OpenMP rows */
+} cro_alcc_config;
+
+typedef struct {
+  double *y, *xi;          /* N, N*n (caller-owned, may be NULL) */
+  double *multiplier;      /* N(N-1): lambda = mu (theta - R)_+ of the last outer step */
+  double *history;         /* max_outer * 8 */
+  int64_t *mapg_iters;     /* max_outer: MAPG iterations per outer step */
+  int64_t outer_iters, mapg_iters_total;
+  int32_t reason, hit_cap_any;
+  double certified_gap, infeas_raw, gap_raw, objective, wall_seconds, sigma_A1, sigma_A2;
+} cro_alcc_result;
+
+/* operators.cpp:302-339 on op_A1 (which = 1) / op_A2 (which = 2) */
+int cro_sigma_A(const double *X, int64_t N, int64_t n, int which, double tol, int max_iters,
+                double *sigma, int *iters, int *converged);
+/* alcc_solve (alcc.cpp:193-208, arity fixed) -> alcc_core with centres (ybar, 0).
+   sigma_A1/2 <= 0: estimated. returns 0, -1 invalid, -4 non-finite P_1,
+   -5 non-finite MAPG gradient. */
+int cro_alcc(const double *X, const double *ys, int64_t N, int64_t n, double gamma,
+             double Bbar_y, double Bbar_xi, double sigma_A1, double sigma_A2,
+             const double *warm_y, const double *warm_xi, const cro_alcc_config *cfg,
+             cro_alcc_result *res);
+
 #ifdef __cplusplus
 }
 #endif

@@ -50,6 +50,27 @@ class CroResult(C.Structure):
     ]
 
 
+class CroAlccConfig(C.Structure):
+    _fields_ = [
+        ("mu1", C.c_double), ("tau1_scale", C.c_double), ("alpha1_scale", C.c_double),
+        ("c", C.c_double), ("kappa", C.c_double), ("max_outer", C.c_int64),
+        ("mapg_cap", C.c_int64), ("infeas_norm_tol", C.c_double), ("gap_norm_tol", C.c_double),
+        ("max_seconds", C.c_double), ("record_history", C.c_int32), ("threads", C.c_int32),
+    ]
+
+
+class CroAlccResult(C.Structure):
+    _fields_ = [
+        ("y", _P), ("xi", _P), ("multiplier", _P), ("history", _P),
+        ("mapg_iters", C.POINTER(C.c_int64)),
+        ("outer_iters", C.c_int64), ("mapg_iters_total", C.c_int64),
+        ("reason", C.c_int32), ("hit_cap_any", C.c_int32),
+        ("certified_gap", C.c_double), ("infeas_raw", C.c_double), ("gap_raw", C.c_double),
+        ("objective", C.c_double), ("wall_seconds", C.c_double), ("sigma_A1", C.c_double),
+        ("sigma_A2", C.c_double),
+    ]
+
+
 _lib = None
 
 
@@ -88,6 +109,9 @@ def lib():
         L.cro_evaluate_estimator.restype = d
         L.cro_repair_feasibility.argtypes = [_P, i64, i64, _P, _P, _P]
         L.cro_repair_feasibility.restype = None
+        L.cro_sigma_A.argtypes = [_P, i64, i64, i32, d, i32, _P, C.POINTER(i32), C.POINTER(i32)]
+        L.cro_alcc.argtypes = [_P, _P, i64, i64, d, d, d, d, d, _P, _P,
+                               C.POINTER(CroAlccConfig), C.POINTER(CroAlccResult)]
         L.cro_cross_position.argtypes = [i64, i64, i64, i64]
         L.cro_cross_position.restype = i64
         _lib = L
@@ -282,3 +306,67 @@ def cross_position(N, K, l1, l2):
     if r < 0:
         raise ValueError("not a cross-block pair")
     return r
+
+
+def sigma_A(X, which, tol=1e-6, max_iters=5000):
+    """operators.cpp:302-339 on op_A1 (which=1) or op_A2 (which=2)."""
+    X = _c(X)
+    s = np.zeros(1)
+    it = C.c_int(0)
+    cv = C.c_int(0)
+    rc = lib().cro_sigma_A(_p(X), X.shape[0], X.shape[1], which, tol, max_iters, _p(s),
+                           C.byref(it), C.byref(cv))
+    if rc != 0:
+        raise ValueError(f"oracle sigma_A failed ({rc})")
+    return float(s[0]), it.value, bool(cv.value)
+
+
+@dataclass
+class AlccResult:
+    y: np.ndarray
+    xi: np.ndarray
+    multiplier: np.ndarray | None
+    history: np.ndarray
+    mapg_iters: np.ndarray
+    outer_iters: int
+    mapg_iters_total: int
+    reason: str
+    hit_cap_any: bool
+    certified_gap: float
+    infeas_raw: float
+    gap_raw: float
+    objective: float
+    wall_seconds: float
+    sigma_A1: float
+    sigma_A2: float
+
+
+def alcc(X, ys, *, gamma, Bbar_y, Bbar_xi, warm_y, warm_xi, sigma_A1=0.0, sigma_A2=0.0,
+         mu1=1.0, tau1_scale=1e-2, alpha1_scale=1e-3, c=5.0, kappa=0.5, max_outer=30,
+         mapg_cap=200000, infeas_norm_tol=1e-1, gap_norm_tol=1e-6, max_seconds=float("inf"),
+         record_history=True, threads=1, want_multiplier=False):
+    """alcc_solve (alcc.cpp:193-208) -> alcc_core (alcc.cpp:54-191), standalone mode."""
+    X = _c(X)
+    ys = _c(ys)
+    N, n = X.shape
+    cfg = CroAlccConfig(mu1, tau1_scale, alpha1_scale, c, kappa, max_outer, mapg_cap,
+                        infeas_norm_tol, gap_norm_tol, max_seconds, int(record_history), threads)
+    y = np.empty(N)
+    xi = np.empty(N * n)
+    mult = np.empty(N * (N - 1)) if want_multiplier else None
+    hist = np.zeros((max_outer, 8))
+    mi = np.zeros(max_outer, np.int64)
+    res = CroAlccResult()
+    res.y, res.xi, res.multiplier, res.history = _p(y), _p(xi), _p(mult), _p(hist)
+    res.mapg_iters = mi.ctypes.data_as(C.POINTER(C.c_int64))
+    rc = lib().cro_alcc(_p(X), _p(ys), N, n, gamma, Bbar_y, Bbar_xi, sigma_A1, sigma_A2,
+                        _p(_c(warm_y)), _p(_c(warm_xi).reshape(-1)), C.byref(cfg), C.byref(res))
+    if rc == -5:
+        raise RuntimeError("mapg: non-finite gradient")
+    if rc != 0:
+        raise RuntimeError(f"oracle alcc failed ({rc})")
+    k = int(res.outer_iters)
+    return AlccResult(y, xi.reshape(N, n), mult, hist[:k], mi[:k], k, int(res.mapg_iters_total),
+                      REASONS[res.reason], bool(res.hit_cap_any), res.certified_gap,
+                      res.infeas_raw, res.gap_raw, res.objective, res.wall_seconds,
+                      res.sigma_A1, res.sigma_A2)

@@ -41,6 +41,27 @@ class PapgResultC(C.Structure):
     ]
 
 
+class AlccConfigC(C.Structure):
+    _fields_ = [
+        ("mu1", C.c_double), ("tau1_scale", C.c_double), ("alpha1_scale", C.c_double),
+        ("c", C.c_double), ("kappa", C.c_double), ("max_outer", C.c_int64),
+        ("mapg_cap", C.c_int64), ("infeas_norm_tol", C.c_double), ("gap_norm_tol", C.c_double),
+        ("max_seconds", C.c_double), ("record_history", C.c_int32), ("pad_", C.c_int32),
+        ("sigma_A1", C.c_double), ("sigma_A2", C.c_double), ("Bbar_y", C.c_double),
+        ("Bbar_xi", C.c_double),
+    ]
+
+
+class AlccResultC(C.Structure):
+    _fields_ = [
+        ("outer_iters", C.c_int64), ("mapg_iters_total", C.c_int64), ("reason", C.c_int32),
+        ("hit_cap_any", C.c_int32), ("sigma_A1_iters", C.c_int32), ("sigma_A2_iters", C.c_int32),
+        ("certified_gap", C.c_double), ("infeas_raw", C.c_double), ("gap_raw", C.c_double),
+        ("objective", C.c_double), ("wall_seconds", C.c_double), ("sigma_A1", C.c_double),
+        ("sigma_A2", C.c_double), ("sigma_seconds", C.c_double),
+    ]
+
+
 # every symbol declared in include/cvxreg_b200.h
 EXPORTS = [
     "cr_create", "cr_destroy", "cr_last_error", "cr_status_string", "cr_nccl_unique_id",
@@ -50,6 +71,7 @@ EXPORTS = [
     "cr_sweep_variant", "cr_papg_begin_resume", "cr_set_observations", "cr_infeasibility",
     "cr_duality_gap", "cr_evaluate_estimator", "cr_repair_feasibility",
     "cr_gen_instance", "cr_prepare_problem", "cr_certificate", "cr_momentum_next",
+    "cr_sigma_A", "cr_alcc_solve", "cr_alcc_multiplier",
 ]
 
 _lib = None
@@ -103,6 +125,10 @@ def load():
         "cr_prepare_problem": (st, [_P, _P, i64, i64, d, _P, _P, _P, _P, _P]),
         "cr_certificate": (None, [d, d, d, d, _P]),
         "cr_momentum_next": (d, [d]),
+        "cr_sigma_A": (st, [vp, i32, d, i32, _P, C.POINTER(i32), C.POINTER(i32)]),
+        "cr_alcc_solve": (st, [vp, C.POINTER(AlccConfigC), _P, _P, _P, _P, _P,
+                               C.POINTER(i64), C.POINTER(AlccResultC)]),
+        "cr_alcc_multiplier": (st, [vp, i64, i64, _P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

@@ -21,9 +21,11 @@ NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
                      "-Xcompiler", "-ffp-contract=off", "-I" + os.path.join(ROOT, "include")]
 CXX_FLAGS = ["-O2", "-std=c++17", "-fPIC", "-ffp-contract=off", "-Wall", "-Wextra",
              "-I" + os.path.join(ROOT, "include")]
-CU_SOURCES = ["sweep.cu", "sweep_mma.cu", "kernels.cu", "small.cu", "power.cu", "metrics.cu", "capi.cu"]
+CU_SOURCES = ["sweep.cu", "sweep_mma.cu", "kernels.cu", "small.cu", "power.cu", "metrics.cu", "capi.cu",
+              "alcc.cu"]
 CXX_SOURCES = ["host.cpp"]
-HEADERS = ["device.cuh", "kernels.cuh", "host.hpp", "pipeline.cuh", "iteration.cuh", "small.cuh"]
+HEADERS = ["device.cuh", "kernels.cuh", "host.hpp", "pipeline.cuh", "iteration.cuh", "small.cuh",
+           "handle.cuh"]
 
 
 def _nvcc():

@@ -1,0 +1,759 @@
+// alcc.cu -- the standalone augmented-Lagrangian solver:
+// alcc_solve (alcc.cpp:193-208) -> alcc_core (alcc.cpp:54-191) with the
+// PenaltyOracle (alcc.cpp:33-47) and the MAPG inner loop (engines.cpp:57-106),
+// over all N(N-1) pair rows R(y, xi) = A1 y + A2 xi (FullRows, alcc.hpp:32-48).
+//
+// Device layout: the outer multiplier theta_k is an N x ld pair matrix in
+// V[cur] (the P-APG dual buffers are reused; a solve invalidates any P-APG
+// state on the handle), theta_{k+1} = v / c is written into V[1-cur] by the
+// outer sweep. Points are [y (N) | xi (N n)] vectors: p1 = y1, p1p = y1_prev,
+// p2 = y2 of the MAPG recursion.
+//
+// One MAPG iteration = 4 launches, captured in a CUDA graph and halted on
+// the device:
+//   K1p  penalty sweep (sweep.cu / sweep_mma.cu, kModePenalty): per pair
+//        v = max(theta - row(y2, xi2), 0), aggregates (rowsum, colsum, V^T X)
+//        -- 8 B of HBM per pair (theta read once)
+//   K3   fixed-order reduce of the sweep partials (kernels.cu)
+//   Kg   gradient step: grad = (y2 - ybar)/mu - A1^T v, (gamma/mu) xi2 - A2^T v
+//        with A1^T v = rowsum - colsum, (A2^T v)_l = colsum_l x_l - (V^T X)_l;
+//        y1 = y2 - grad / L (engines.cpp:83-88); partial ball distances
+//   Ks   ball projections (projections.hpp:22-26), displacements, momentum
+//        (engines.cpp:97-103), records of y2 for the next sweep; the last
+//        block applies the stop test (engines.cpp:104-105) and halts.
+// One outer step (alcc.cpp:124-183) = records(y1) + kModePenaltyUpdate sweep
+// (stats + theta_{k+1}) + reduce + one stats block; the scalar logic runs on
+// the host exactly as in the reference.
+#include <cuda_runtime.h>
+#include <math.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "handle.cuh"
+#include "host.hpp"
+#include "iteration.cuh"
+
+namespace crb {
+
+struct AlccDev {
+  long long ell;   // MAPG iterations of the current outer step
+  long long lmax;
+  int halt;
+  int hit_cap;
+  int cur;         // slot of theta_k
+  int nonfinite;
+  double t;        // momentum
+  double mu, gamma, L_y, L_xi, alpha_y, alpha_xi, Bbar_y, Bbar_xi;
+  double disp_y, disp_xi;
+  // stats block: |y-ybar|^2, |xi|^2, |A1^T v|^2, |A2^T v|^2, ybar.A1^T v, S_vv, S_vr, S_nn
+  double stats[8];
+};
+
+namespace {
+
+constexpr int kSBlock = 1024;  // single-block kernels
+
+struct AlccArgs {
+  AlccDev* d;
+  const double* X;
+  const double* cy;     // ybar (ball centre of y; xi centre is 0)
+  const double* agg;    // [rowsum N | colagg N (n+1) | scalars]
+  double *p1, *p1p, *p2;
+  double *rowrec, *colrec;
+  double *part1, *part2;
+  unsigned int* counter;
+  long long N;
+  int n;
+};
+
+// fixed-order block sum of W values (warp butterflies, then warps in order);
+// the result is valid in every thread
+template <int W, int BS>
+__device__ __forceinline__ void block_sum_all(double (&v)[W]) {
+  __shared__ double sh[BS / 32][W];
+  __shared__ double tot[W];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int w = 0; w < W; ++w) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v[w] += __shfl_xor_sync(0xffffffffu, v[w], o);
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int w = 0; w < W; ++w) sh[warp][w] = v[w];
+  }
+  __syncthreads();
+  if (threadIdx.x < W) {
+    double t = 0.0;
+#pragma unroll
+    for (int k = 0; k < BS / 32; ++k) t += sh[k][threadIdx.x];
+    tot[threadIdx.x] = t;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int w = 0; w < W; ++w) v[w] = tot[w];
+  __syncthreads();
+}
+
+// sum of `count` records part[g][2] in a fixed order, valid in every thread
+template <int BS>
+__device__ __forceinline__ void records_sum2(const double* part, int count, double (&out)[2]) {
+  double v[2] = {0.0, 0.0};
+  for (int g = threadIdx.x; g < count; g += BS) {
+    v[0] += __ldcg(part + 2 * g);
+    v[1] += __ldcg(part + 2 * g + 1);
+  }
+  block_sum_all<2, BS>(v);
+  out[0] = v[0];
+  out[1] = v[1];
+}
+
+template <int NN>
+__device__ __forceinline__ void write_records(const AlccArgs& a, long long l, double y,
+                                              const double* xi /* NN */) {
+  constexpr int RP = rec_pitch(NN);
+  double cx = 0.0;
+  double* cr = a.colrec + l * RP;
+#pragma unroll
+  for (int j = 0; j < NN; ++j) {
+    cx = fma(xi[j], a.X[l * NN + j], cx);
+    cr[j] = -xi[j];
+  }
+  cr[NN] = -(y - cx);
+  cr[NN + 1] = 1.0;
+  a.rowrec[l * RP + NN + 1] = y;
+}
+
+// project_ball(warm, centre, B) for y and xi (alcc.cpp:68-69); one block
+template <int NN>
+__global__ void __launch_bounds__(kSBlock) project_start_kernel(const AlccArgs a) {
+  const long long N = a.N;
+  double v[2] = {0.0, 0.0};
+  for (long long l = threadIdx.x; l < N; l += kSBlock) {
+    const double d = a.p1[l] - a.cy[l];
+    v[0] = fma(d, d, v[0]);
+  }
+  for (long long i = threadIdx.x; i < N * NN; i += kSBlock) v[1] = fma(a.p1[N + i], a.p1[N + i], v[1]);
+  block_sum_all<2, kSBlock>(v);
+  const double dy = sqrt(v[0]), dx = sqrt(v[1]);
+  const double By = a.d->Bbar_y, Bx = a.d->Bbar_xi;
+  if (dy > By) {
+    const double f = By / dy;
+    for (long long l = threadIdx.x; l < N; l += kSBlock) a.p1[l] = a.cy[l] + f * (a.p1[l] - a.cy[l]);
+  }
+  if (dx > Bx) {
+    const double f = Bx / dx;
+    for (long long i = threadIdx.x; i < N * NN; i += kSBlock) a.p1[N + i] = 0.0 + f * (a.p1[N + i] - 0.0);
+  }
+}
+
+// MAPG start (engines.cpp:65-66): y1_prev = y1 = y2 = y0; records of y2
+template <int NN>
+__global__ void __launch_bounds__(kPBlock) mapg_reset_kernel(const AlccArgs a) {
+  const long long N = a.N;
+  for (long long l = (long long)blockIdx.x * kPBlock + threadIdx.x; l < N;
+       l += (long long)gridDim.x * kPBlock) {
+    const double y = a.p1[l];
+    a.p1p[l] = y;
+    a.p2[l] = y;
+    double xi[NN];
+#pragma unroll
+    for (int j = 0; j < NN; ++j) {
+      xi[j] = a.p1[N + l * NN + j];
+      a.p1p[N + l * NN + j] = xi[j];
+      a.p2[N + l * NN + j] = xi[j];
+    }
+    write_records<NN>(a, l, y, xi);
+  }
+}
+
+// records of y1 (the MAPG result) for the outer sweep
+template <int NN>
+__global__ void __launch_bounds__(kPBlock) point_records_kernel(const AlccArgs a) {
+  const long long N = a.N;
+  for (long long l = (long long)blockIdx.x * kPBlock + threadIdx.x; l < N;
+       l += (long long)gridDim.x * kPBlock) {
+    double xi[NN];
+#pragma unroll
+    for (int j = 0; j < NN; ++j) xi[j] = a.p1[N + l * NN + j];
+    write_records<NN>(a, l, a.p1[l], xi);
+  }
+}
+
+// Kg: gradient at y2 (alcc.cpp:38-41), y1 = y2 - g / L (engines.cpp:82-88)
+template <int NN>
+__global__ void __launch_bounds__(kPBlock) mapg_grad_kernel(const AlccArgs a) {
+  AlccDev* d = a.d;
+  if (d->halt) return;
+  const long long N = a.N;
+  const double mu = d->mu, gm = d->gamma / d->mu, Ly = d->L_y, Lx = d->L_xi;
+  double acc[2] = {0.0, 0.0};
+  bool bad = false;
+  for (long long l = (long long)blockIdx.x * kPBlock + threadIdx.x; l < N;
+       l += (long long)gridDim.x * kPBlock) {
+    const double* ca = a.agg + N + l * (NN + 1);
+    const double rs = a.agg[l], cs = ca[0];
+    const double gy = (a.p2[l] - a.cy[l]) / mu - (rs - cs);
+    bad |= !isfinite(gy);
+    const double y1 = a.p2[l] - gy / Ly;
+    a.p1p[l] = a.p1[l];
+    a.p1[l] = y1;
+    const double dy = y1 - a.cy[l];
+    acc[0] = fma(dy, dy, acc[0]);
+#pragma unroll
+    for (int j = 0; j < NN; ++j) {
+      const long long k = N + l * NN + j;
+      const double adj = cs * a.X[l * NN + j] - ca[1 + j];
+      const double g = gm * a.p2[k] - adj;
+      bad |= !isfinite(g);
+      const double x1 = a.p2[k] - g / Lx;
+      a.p1p[k] = a.p1[k];
+      a.p1[k] = x1;
+      acc[1] = fma(x1, x1, acc[1]);
+    }
+  }
+  if (bad) d->nonfinite = 1;
+  block_sum_all<2, kPBlock>(acc);
+  if (threadIdx.x == 0) {
+    a.part1[2 * blockIdx.x] = acc[0];
+    a.part1[2 * blockIdx.x + 1] = acc[1];
+  }
+}
+
+// Ks: projections, displacements, momentum, records; last block: stop test
+template <int NN>
+__global__ void __launch_bounds__(kPBlock) mapg_step_kernel(const AlccArgs a) {
+  AlccDev* d = a.d;
+  if (d->halt) return;
+  const long long N = a.N;
+  double dist2[2];
+  records_sum2<kPBlock>(a.part1, gridDim.x, dist2);
+  const double dy = sqrt(dist2[0]), dx = sqrt(dist2[1]);
+  const bool sy = dy > d->Bbar_y, sx = dx > d->Bbar_xi;
+  const double fy = sy ? d->Bbar_y / dy : 1.0, fx = sx ? d->Bbar_xi / dx : 1.0;
+  const double t = d->t;
+  const double t_next = 0.5 * (1.0 + sqrt(1.0 + 4.0 * t * t));  // engines.hpp:11-13
+  const double beta = (t - 1.0) / t_next;
+  double acc[2] = {0.0, 0.0};
+  for (long long l = (long long)blockIdx.x * kPBlock + threadIdx.x; l < N;
+       l += (long long)gridDim.x * kPBlock) {
+    double y1 = a.p1[l];
+    if (sy) {
+      y1 = a.cy[l] + fy * (y1 - a.cy[l]);
+      a.p1[l] = y1;
+    }
+    const double e = y1 - a.p2[l];
+    acc[0] = fma(e, e, acc[0]);
+    const double y2 = y1 + beta * (y1 - a.p1p[l]);
+    a.p2[l] = y2;
+    double xi2[NN];
+#pragma unroll
+    for (int j = 0; j < NN; ++j) {
+      const long long k = N + l * NN + j;
+      double x1 = a.p1[k];
+      if (sx) {
+        x1 = 0.0 + fx * (x1 - 0.0);
+        a.p1[k] = x1;
+      }
+      const double ex = x1 - a.p2[k];
+      acc[1] = fma(ex, ex, acc[1]);
+      xi2[j] = x1 + beta * (x1 - a.p1p[k]);
+      a.p2[k] = xi2[j];
+    }
+    write_records<NN>(a, l, y2, xi2);
+  }
+  block_sum_all<2, kPBlock>(acc);
+  __shared__ bool last;
+  if (threadIdx.x == 0) {
+    a.part2[2 * blockIdx.x] = acc[0];
+    a.part2[2 * blockIdx.x + 1] = acc[1];
+    __threadfence();
+    last = atomicAdd(a.counter, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  double disp2[2];
+  records_sum2<kPBlock>(a.part2, gridDim.x, disp2);
+  if (threadIdx.x == 0) {
+    *a.counter = 0u;
+    const double disp_y = sqrt(disp2[0]), disp_x = sqrt(disp2[1]);
+    d->disp_y = disp_y;
+    d->disp_xi = disp_x;
+    d->t = t_next;
+    const long long ell = d->ell + 1;
+    d->ell = ell;
+    const bool stop = disp_y <= d->alpha_y && disp_x <= d->alpha_xi;
+    if (!stop && ell == d->lmax) d->hit_cap = 1;
+    if (stop || ell >= d->lmax || d->nonfinite) d->halt = 1;
+  }
+}
+
+// outer-step statistics (alcc.cpp:124-145) from the aggregates of v and y1
+template <int NN>
+__global__ void __launch_bounds__(kSBlock) alcc_stats_kernel(const AlccArgs a) {
+  const long long N = a.N;
+  double v[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+  for (long long l = threadIdx.x; l < N; l += kSBlock) {
+    const double* ca = a.agg + N + l * (NN + 1);
+    const double dy = a.p1[l] - a.cy[l];
+    v[0] = fma(dy, dy, v[0]);
+    const double ay = a.agg[l] - ca[0];
+    v[2] = fma(ay, ay, v[2]);
+    v[4] = fma(a.cy[l], ay, v[4]);
+#pragma unroll
+    for (int j = 0; j < NN; ++j) {
+      const double xi = a.p1[N + l * NN + j];
+      v[1] = fma(xi, xi, v[1]);
+      const double ax = ca[0] * a.X[l * NN + j] - ca[1 + j];
+      v[3] = fma(ax, ax, v[3]);
+    }
+  }
+  block_sum_all<5, kSBlock>(v);
+  if (threadIdx.x == 0) {
+    AlccDev* d = a.d;
+    for (int w = 0; w < 5; ++w) d->stats[w] = v[w];
+    const double* sc = a.agg + N + N * (NN + 1);
+    d->stats[5] = sc[0];  // S_vv
+    d->stats[6] = sc[1];  // S_vr
+    d->stats[7] = sc[3];  // S_nn
+  }
+}
+
+// lambda = mu (theta - row)_+ of rows [ra, rb) in canonical order (alcc.cpp:125-126)
+__global__ void multiplier_out_kernel(double* stage, const double* V, double mu,
+                                      const double* rowrec, const double* colrec, long long N,
+                                      int n, long long ld, long long ra, long long rb) {
+  const int RP = rec_pitch(n);
+  const long long total = (rb - ra) * (N - 1);
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long lr = i / (N - 1), k = i % (N - 1);
+    const long long gr = ra + lr;
+    const long long c = k + (k >= gr ? 1 : 0);
+    const double* xr = rowrec + gr * RP;
+    const double* cr = colrec + c * RP;
+    double row = xr[n + 1] + cr[n];
+    for (int j = 0; j < n; ++j) row = fma(xr[j], cr[j], row);
+    const double th = V[gr * ld + c];
+    const double vn = th - row > 0.0 ? th - row : 0.0;
+    stage[i] = mu * vn;
+  }
+}
+
+using AlccKernel = void (*)(const AlccArgs);
+template <int NN>
+struct AlccTab {
+  static constexpr AlccKernel project = project_start_kernel<NN>;
+  static constexpr AlccKernel reset = mapg_reset_kernel<NN>;
+  static constexpr AlccKernel records = point_records_kernel<NN>;
+  static constexpr AlccKernel grad = mapg_grad_kernel<NN>;
+  static constexpr AlccKernel step = mapg_step_kernel<NN>;
+  static constexpr AlccKernel stats = alcc_stats_kernel<NN>;
+};
+struct AlccFns {
+  AlccKernel project, reset, records, grad, step, stats;
+};
+template <int NN>
+constexpr AlccFns fns_for() {
+  return {AlccTab<NN>::project, AlccTab<NN>::reset, AlccTab<NN>::records,
+          AlccTab<NN>::grad,    AlccTab<NN>::step,  AlccTab<NN>::stats};
+}
+constexpr AlccFns kFns[kMaxN] = {
+    fns_for<1>(),  fns_for<2>(),  fns_for<3>(),  fns_for<4>(),  fns_for<5>(),  fns_for<6>(),
+    fns_for<7>(),  fns_for<8>(),  fns_for<9>(),  fns_for<10>(), fns_for<11>(), fns_for<12>(),
+    fns_for<13>(), fns_for<14>(), fns_for<15>(), fns_for<16>(), fns_for<17>(), fns_for<18>(),
+    fns_for<19>(), fns_for<20>(), fns_for<21>(), fns_for<22>(), fns_for<23>(), fns_for<24>()};
+
+AlccArgs alcc_args(cr_handle* h) {
+  AlccArgs a{};
+  a.d = h->alcc.dev;
+  a.X = h->X;
+  a.cy = h->ybar;
+  a.agg = h->xbuf;
+  a.p1 = h->alcc.p1;
+  a.p1p = h->alcc.p1p;
+  a.p2 = h->alcc.p2;
+  a.rowrec = h->rowrec;
+  a.colrec = h->colrec;
+  a.part1 = h->alcc.part1;
+  a.part2 = h->alcc.part2;
+  a.counter = h->alcc.counter;
+  a.N = h->N;
+  a.n = (int)h->n;
+  return a;
+}
+
+cudaError_t launch_alcc(AlccKernel k, int grid, int block, const AlccArgs& a, cudaStream_t s) {
+  void* args[] = {const_cast<AlccArgs*>(&a)};
+  return cudaLaunchKernel((const void*)k, dim3((unsigned)grid), dim3((unsigned)block), args, 0, s);
+}
+
+SweepArgs penalty_sweep_args(cr_handle* h, double cdiv) {
+  SweepArgs a = sweep_args(h, kModePenalty, false);
+  a.cur = &h->alcc.dev->cur;
+  a.stopped = nullptr;
+  a.coef = h->consts;
+  a.invL = 1.0;
+  a.cdiv = cdiv;
+  return a;
+}
+
+cr_status ensure_alcc(cr_handle* h) {
+  AlccBufs& b = h->alcc;
+  if (b.dev) return CR_OK;
+  const int64_t P = h->N * (h->n + 1);
+  b.blocks = primal_blocks(h->N);
+  g_alloc_stream = h->st;
+  cudaError_t e = cudaSuccess;
+  if (e == cudaSuccess) e = dalloc(&b.dev, 1);
+  if (e == cudaSuccess) e = dalloc(&b.p1, (size_t)P);
+  if (e == cudaSuccess) e = dalloc(&b.p1p, (size_t)P);
+  if (e == cudaSuccess) e = dalloc(&b.p2, (size_t)P);
+  if (e == cudaSuccess) e = dalloc(&b.part1, (size_t)2 * b.blocks);
+  if (e == cudaSuccess) e = dalloc(&b.part2, (size_t)2 * b.blocks);
+  if (e == cudaSuccess) e = dalloc(&b.counter, 1);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(h, CR_ENOMEM, std::string("alcc allocation failed: ") + cudaGetErrorString(e));
+  }
+  CUDA_TRY(cudaMallocHost(&b.host, sizeof(AlccDev)));
+  std::memset(b.host, 0, sizeof(AlccDev));
+  CUDA_TRY(cudaMemsetAsync(b.counter, 0, sizeof(unsigned int), h->st));
+  const int pen = kModePenalty, upd = kModePenaltyUpdate;
+  if (h->variant == kSweepMma) {
+    b.kpen = sweep_mma_info((int)h->n, pen);
+    b.kupd = sweep_mma_info((int)h->n, upd);
+  } else {
+    b.kpen = sweep_dfma_info((int)h->n, pen);
+    b.kupd = sweep_dfma_info((int)h->n, upd);
+  }
+  if (!b.kpen.fn || !b.kupd.fn || b.kpen.max_blocks_per_sm < 1 || b.kupd.max_blocks_per_sm < 1)
+    return fail(h, CR_EINVAL, "alcc: no penalty sweep kernel for this n");
+  return CR_OK;
+}
+
+// one MAPG iteration (4 launches)
+cr_status enqueue_mapg(cr_handle* h, const AlccFns& f, const AlccArgs& aa, double cdiv) {
+  SweepArgs sa = penalty_sweep_args(h, cdiv);
+  sa.stopped = &h->alcc.dev->halt;
+  CUDA_TRY((cudaError_t)launch_sweep(h->alcc.kpen, sa, h->st));
+  const ReduceArgs ra = reduce_args(h, false, &h->alcc.dev->halt, false);
+  CUDA_TRY(launch_reduce(ra, h->st));
+  CUDA_TRY(launch_alcc(f.grad, h->alcc.blocks, kPBlock, aa, h->st));
+  CUDA_TRY(launch_alcc(f.step, h->alcc.blocks, kPBlock, aa, h->st));
+  return CR_OK;
+}
+
+cr_status build_mapg_graph(cr_handle* h, const AlccFns& f, const AlccArgs& aa, int iters) {
+  AlccBufs& b = h->alcc;
+  if (b.gexec) {
+    cudaGraphExecDestroy(b.gexec);
+    b.gexec = nullptr;
+  }
+  cudaGraph_t g = nullptr;
+  CUDA_TRY(cudaStreamBeginCapture(h->st, cudaStreamCaptureModeThreadLocal));
+  cr_status s = CR_OK;
+  for (int i = 0; i < iters && s == CR_OK; ++i) s = enqueue_mapg(h, f, aa, 1.0);
+  cudaError_t e = cudaStreamEndCapture(h->st, &g);
+  if (s != CR_OK) {
+    if (g) cudaGraphDestroy(g);
+    return s;
+  }
+  CUDA_TRY(e);
+  e = cudaGraphInstantiate(&b.gexec, g, 0);
+  cudaGraphDestroy(g);
+  CUDA_TRY(e);
+  b.graph_iters = iters;
+  return CR_OK;
+}
+
+cr_status push_dev(cr_handle* h) {
+  CUDA_TRY(cudaMemcpyAsync(h->alcc.dev, h->alcc.host, sizeof(AlccDev), cudaMemcpyHostToDevice,
+                           h->st));
+  return CR_OK;
+}
+cr_status pull_dev(cr_handle* h) {
+  CUDA_TRY(cudaMemcpyAsync(h->alcc.host, h->alcc.dev, sizeof(AlccDev), cudaMemcpyDeviceToHost,
+                           h->st));
+  CUDA_TRY(cudaStreamSynchronize(h->st));
+  return CR_OK;
+}
+
+// penalty (or update) sweep over y1 + reduce + stats block; leaves stats in host mirror
+cr_status outer_stats(cr_handle* h, const AlccFns& f, const AlccArgs& aa, bool update,
+                      double cdiv) {
+  CUDA_TRY(launch_alcc(f.records, h->alcc.blocks, kPBlock, aa, h->st));
+  SweepArgs sa = penalty_sweep_args(h, cdiv);
+  CUDA_TRY((cudaError_t)launch_sweep(update ? h->alcc.kupd : h->alcc.kpen, sa, h->st));
+  const ReduceArgs ra = reduce_args(h, false, nullptr, false);
+  CUDA_TRY(launch_reduce(ra, h->st));
+  CUDA_TRY(launch_alcc(f.stats, 1, kSBlock, aa, h->st));
+  return pull_dev(h);
+}
+
+}  // namespace
+}  // namespace crb
+
+extern "C" {
+
+cr_status cr_sigma_A(cr_handle* h, int32_t which, double tol, int32_t max_iters, double* sigma,
+                     int32_t* iters, int32_t* converged) {
+  if (!h || !sigma || !iters || !converged || max_iters < 1 || (which != 1 && which != 2))
+    return CR_EINVAL;
+  CUDA_TRY(cudaSetDevice(h->device));
+  const int64_t cols = which == 1 ? h->N : h->N * h->n;
+  // fixed seeded start (operators.cpp:309-313)
+  std::vector<double> v((size_t)cols);
+  host::normal_stream(0x5eedULL, 97, cols, v.data());
+  double ss = 0;
+  for (double x : v) ss += x * x;
+  const double nv = std::sqrt(ss);
+  for (double& x : v) x /= nv;
+  CUDA_TRY(cudaMemcpyAsync(h->pw_u, v.data(), sizeof(double) * cols, cudaMemcpyHostToDevice,
+                           h->st));
+  PowerLoopArgs pa{};
+  pa.u = h->pw_u;
+  pa.v = h->pw_v;
+  pa.X = h->X;
+  pa.gram = h->gram;
+  pa.part = h->ps_part;
+  pa.part2 = h->ps_part2;
+  pa.state = h->ps_state;
+  pa.N = h->N;
+  pa.n = (int)h->n;
+  pa.max_iters = max_iters;
+  pa.tol = tol;
+  pa.op = which;
+  CUDA_TRY(launch_power_loop(pa, h->power_grid, h->st));
+  double st[3];
+  CUDA_TRY(cudaMemcpyAsync(st, h->ps_state, sizeof(st), cudaMemcpyDeviceToHost, h->st));
+  CUDA_TRY(cudaStreamSynchronize(h->st));
+  *sigma = st[0];
+  *iters = (int32_t)st[1];
+  *converged = (int32_t)st[2];
+  return CR_OK;
+}
+
+cr_status cr_alcc_solve(cr_handle* h, const cr_alcc_config* cfg, const double* warm_y,
+                        const double* warm_xi, double* y_out, double* xi_out,
+                        cr_snapshot* history, int64_t* mapg_iters, cr_alcc_result* res) {
+  if (!h || !cfg || !warm_y || !warm_xi || !res) return CR_EINVAL;
+  if (!(cfg->c > 1)) return fail(h, CR_EINVAL, "alcc: c must be > 1");          // alcc.cpp:59
+  if (!(cfg->kappa > 0)) return fail(h, CR_EINVAL, "alcc: kappa must be > 0");  // :60
+  if (!(cfg->mu1 > 0)) return fail(h, CR_EINVAL, "alcc: mu1 must be > 0");      // :61
+  if (cfg->max_outer < 0 || cfg->mapg_cap < 1)
+    return fail(h, CR_EINVAL, "alcc: bad iteration limits");
+  if (h->comm != nullptr || h->R != h->N)
+    return fail(h, CR_EINVAL, "alcc: standalone ALCC runs on an unsharded handle");
+  CUDA_TRY(cudaSetDevice(h->device));
+  const auto t_start = std::chrono::steady_clock::now();
+  auto seconds = [&]() {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
+  };
+  {
+    const cr_status s = ensure_alcc(h);
+    if (s != CR_OK) return s;
+  }
+  h->begun = false;  // the dual buffers now hold ALCC multipliers
+  AlccBufs& b = h->alcc;
+  b.done = false;
+  const int64_t N = h->N, n = h->n, Nn = N * n;
+  const double gamma = h->gamma;
+  std::memset(res, 0, sizeof(*res));
+
+  double sA1 = cfg->sigma_A1, sA2 = cfg->sigma_A2;
+  if (!(sA1 > 0)) {
+    int32_t it = 0, cv = 0;
+    const cr_status s = cr_sigma_A(h, 1, 1e-6, 5000, &sA1, &it, &cv);
+    if (s != CR_OK) return s;
+    res->sigma_A1_iters = it;
+  }
+  if (!(sA2 > 0)) {
+    int32_t it = 0, cv = 0;
+    const cr_status s = cr_sigma_A(h, 2, 1e-6, 5000, &sA2, &it, &cv);
+    if (s != CR_OK) return s;
+    res->sigma_A2_iters = it;
+  }
+  res->sigma_A1 = sA1;
+  res->sigma_A2 = sA2;
+  res->sigma_seconds = seconds();
+
+  const AlccFns& f = kFns[n - 1];
+  const AlccArgs aa = alcc_args(h);
+  // start point and theta_1 = 0 in slot 0
+  CUDA_TRY(cudaMemcpyAsync(b.p1, warm_y, sizeof(double) * N, cudaMemcpyHostToDevice, h->st));
+  CUDA_TRY(cudaMemcpyAsync(b.p1 + N, warm_xi, sizeof(double) * Nn, cudaMemcpyHostToDevice, h->st));
+  const size_t vbytes = sizeof(double) * (size_t)h->R * (size_t)h->ld;
+  CUDA_TRY(cudaMemsetAsync(h->V[0], 0, vbytes, h->st));
+  CUDA_TRY(cudaMemsetAsync(h->V[1], 0, vbytes, h->st));
+  AlccDev& d = *b.host;
+  std::memset(&d, 0, sizeof(d));
+  d.cur = 0;
+  d.mu = cfg->mu1;
+  d.gamma = gamma;
+  d.Bbar_y = cfg->Bbar_y;
+  d.Bbar_xi = cfg->Bbar_xi;
+  d.halt = 1;
+  {
+    const cr_status s = push_dev(h);
+    if (s != CR_OK) return s;
+  }
+  CUDA_TRY(launch_alcc(f.project, 1, kSBlock, aa, h->st));
+
+  // P_1 at the start point (alcc.cpp:75-84)
+  double mu = cfg->mu1;
+  double tau, alpha_y, alpha_xi;
+  {
+    const cr_status s = outer_stats(h, f, aa, false, cfg->c);
+    if (s != CR_OK) return s;
+    const double p1 = d.stats[0] / (2.0 * mu) + gamma * d.stats[1] / (2.0 * mu) + 0.5 * d.stats[5];
+    if (!std::isfinite(p1)) return fail(h, CR_ENONFINITE, "alcc: non-finite P_1 at the start point");
+    tau = std::max(cfg->tau1_scale * p1, 1e-16);
+    alpha_y = alpha_xi = cfg->alpha1_scale * (cfg->Bbar_y + cfg->Bbar_xi);
+  }
+  const int GI = 16;
+  if (!b.gexec || b.graph_iters != GI) {
+    const cr_status s = build_mapg_graph(h, f, aa, GI);
+    if (s != CR_OK) return s;
+  }
+
+  res->reason = CR_ITER_BUDGET;
+  const double m = (double)N * (double)(N - 1);
+  for (int64_t k = 1; k <= cfg->max_outer; ++k) {
+    const double L_y = 1.0 / mu + sA1 * sA1;  // alcc.cpp:101-102
+    const double L_xi = gamma / mu + sA2 * sA2;
+    const double lmax_real =
+        4.0 * std::sqrt((L_y * cfg->Bbar_y * cfg->Bbar_y + L_xi * cfg->Bbar_xi * cfg->Bbar_xi) / tau);
+    int64_t lmax = (int64_t)std::ceil(lmax_real);
+    if (lmax < 10) lmax = 10;
+    if (lmax > cfg->mapg_cap) lmax = cfg->mapg_cap;
+    d.ell = 0;
+    d.lmax = lmax;
+    d.halt = 0;
+    d.hit_cap = 0;
+    d.nonfinite = 0;
+    d.t = 1.0;
+    d.mu = mu;
+    d.L_y = L_y;
+    d.L_xi = L_xi;
+    d.alpha_y = alpha_y;
+    d.alpha_xi = alpha_xi;
+    {
+      const cr_status s = push_dev(h);
+      if (s != CR_OK) return s;
+    }
+    CUDA_TRY(launch_alcc(f.reset, b.blocks, kPBlock, aa, h->st));
+    for (;;) {
+      CUDA_TRY(cudaGraphLaunch(b.gexec, h->st));
+      const cr_status s = pull_dev(h);
+      if (s != CR_OK) return s;
+      if (d.halt) break;
+    }
+    if (d.nonfinite) {
+      res->reason = CR_ERROR;
+      return fail(h, CR_ENONFINITE, "mapg: non-finite gradient");
+    }
+    if (mapg_iters) mapg_iters[k - 1] = d.ell;
+    res->mapg_iters_total += d.ell;
+    if (d.hit_cap) res->hit_cap_any = 1;
+
+    // outer statistics at y1 and theta_{k+1} = v / c into the other slot
+    {
+      const cr_status s = outer_stats(h, f, aa, true, cfg->c);
+      if (s != CR_OK) return s;
+    }
+    const double sq_y = d.stats[0], sq_xi = d.stats[1];
+    const double infeas_raw = std::sqrt(d.stats[7]);
+    const double gap_raw = mu * d.stats[6];
+    const double mu2 = mu * mu;
+    const double dual_value = -0.5 * (mu2 * d.stats[2]) - (mu2 * d.stats[3]) / (2.0 * gamma) -
+                              mu * d.stats[4];
+    const double primal_value = 0.5 * sq_y + 0.5 * gamma * sq_xi;
+    res->certified_gap = primal_value - dual_value;
+    res->infeas_raw = infeas_raw;
+    res->gap_raw = gap_raw;
+    res->outer_iters = k;
+    res->objective = 0.5 * sq_y;
+    b.mu = mu;
+    b.done = true;
+    const double infeas_norm = infeas_raw / std::sqrt(m);
+    const double gap_norm = gap_raw / m;
+    if (history) {
+      cr_snapshot& sn = history[k - 1];
+      sn.iter = (double)k;
+      sn.objective = 0.5 * sq_y;
+      sn.reg_objective = primal_value;
+      sn.infeas_raw = infeas_raw;
+      sn.infeas_norm = infeas_norm;
+      sn.gap_raw = gap_raw;
+      sn.gap_norm = gap_norm;
+      sn.wall_time_s = seconds();
+    }
+    if (infeas_norm <= cfg->infeas_norm_tol && std::fabs(gap_norm) <= cfg->gap_norm_tol) {
+      res->reason = CR_THRESHOLDS;
+      break;
+    }
+    if (seconds() > cfg->max_seconds) {
+      res->reason = CR_TIME_BUDGET;
+      break;
+    }
+    // alcc.cpp:176-183: theta_{k+1} is already in the other slot
+    d.cur = 1 - d.cur;
+    mu *= cfg->c;
+    const double decay = std::pow(cfg->c * std::pow((double)k, 1.0 + cfg->kappa), 2.0);
+    tau /= decay;
+    alpha_y /= decay;
+    alpha_xi /= decay;
+  }
+  // the multiplier export reads theta_k of the last outer step: undo a final flip
+  if (res->outer_iters > 0 && res->reason == CR_ITER_BUDGET) d.cur = 1 - d.cur;
+  {
+    const cr_status s = push_dev(h);
+    if (s != CR_OK) return s;
+  }
+  if (y_out) CUDA_TRY(cudaMemcpyAsync(y_out, b.p1, sizeof(double) * N, cudaMemcpyDeviceToHost, h->st));
+  if (xi_out)
+    CUDA_TRY(cudaMemcpyAsync(xi_out, b.p1 + N, sizeof(double) * Nn, cudaMemcpyDeviceToHost, h->st));
+  CUDA_TRY(cudaStreamSynchronize(h->st));
+  if (res->outer_iters == 0) {  // max_outer = 0: the projected start point
+    double sy = 0;
+    std::vector<double> y0((size_t)N);
+    CUDA_TRY(cudaMemcpy(y0.data(), b.p1, sizeof(double) * N, cudaMemcpyDeviceToHost));
+    std::vector<double> yb((size_t)N);
+    CUDA_TRY(cudaMemcpy(yb.data(), h->ybar, sizeof(double) * N, cudaMemcpyDeviceToHost));
+    for (int64_t i = 0; i < N; ++i) sy += (y0[i] - yb[i]) * (y0[i] - yb[i]);
+    res->objective = 0.5 * sy;
+  }
+  res->wall_seconds = seconds();
+  return CR_OK;
+}
+
+cr_status cr_alcc_multiplier(cr_handle* h, int64_t row_begin, int64_t row_end, double* out) {
+  if (!h || !out || row_begin < 0 || row_end > h->N || row_begin > row_end) return CR_EINVAL;
+  if (!h->alcc.done) return fail(h, CR_ESTATE, "alcc: no finished solve on this handle");
+  CUDA_TRY(cudaSetDevice(h->device));
+  const int64_t N = h->N;
+  const double* V = h->V[h->alcc.host->cur];
+  const int64_t per = std::max<int64_t>(1, h->stage_elems / (N - 1));
+  for (int64_t ra = row_begin; ra < row_end; ra += per) {
+    const int64_t rb = std::min(row_end, ra + per);
+    const long long total = (rb - ra) * (N - 1);
+    long long g = (total + 255) / 256;
+    if (g > 4096) g = 4096;
+    if (g < 1) g = 1;
+    multiplier_out_kernel<<<(unsigned)g, 256, 0, h->st>>>(h->stage, V, h->alcc.mu, h->rowrec,
+                                                          h->colrec, N, (int)h->n, h->ld, ra, rb);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaMemcpyAsync(out + (ra - row_begin) * (N - 1), h->stage,
+                             sizeof(double) * (size_t)total, cudaMemcpyDeviceToHost, h->st));
+    CUDA_TRY(cudaStreamSynchronize(h->st));
+  }
+  return CR_OK;
+}
+
+}  // extern "C"

@@ -77,6 +77,7 @@ struct SweepArgs {
   const double* coef;     // {s_cur, s_prev, beta} (DevCtrl fields or constants)
   const int* stopped;     // nullptr: always run
   double invL;            // 1 / L_g (0 turns the step into a pure copy + aggregate)
+  double cdiv;            // kModePenaltyUpdate: theta_{k+1} = v / cdiv (alcc.cpp:176)
   long long N, R, r0, ld;
   long long U;            // rows of the (tile, row) unit space per CTA
   int S;                  // column strips (32*C columns each)
@@ -85,7 +86,13 @@ struct SweepArgs {
   int maxspan;            // max segments (tiles) one CTA can touch
 };
 
-enum SweepMode { kModePapg = 0, kModePower = 1 };
+// kModePapg:   the P-APG step above (reads V, V'; writes V')
+// kModePower:  aggregates of the residual itself (sigma_max(C) by sweeps)
+// kModePenalty / kModePenaltyUpdate: the ALCC penalty oracle (alcc.cpp:33-47,
+//   :124-127): v = max(theta - row, 0) with theta = V[cur]; aggregates of v and
+//   scalars (S_vv, S_vr, -, S_nn). The update variant also writes v / cdiv
+//   into V[1-cur] (the next outer multiplier, alcc.cpp:176).
+enum SweepMode { kModePapg = 0, kModePower = 1, kModePenalty = 2, kModePenaltyUpdate = 3 };
 
 // returns the kernel attribute table entry for (n, mode); host side helpers
 struct SweepKernelInfo {

@@ -1,0 +1,190 @@
+// handle.cuh -- the C-ABI handle (include/cvxreg_b200.h: cr_handle) shared by
+// capi.cu (P-APG, metrics, sharding) and alcc.cu (standalone ALCC), plus the
+// small helpers both use (error capture, pooled allocation, sweep/reduce args).
+#pragma once
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <chrono>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/cvxreg_b200.h"
+#include "device.cuh"
+#include "kernels.cuh"
+#include "small.cuh"
+
+namespace crb {
+struct AlccDev;  // alcc.cu
+struct AlccBufs {
+  AlccDev* dev = nullptr;       // device-resident MAPG / outer state
+  AlccDev* host = nullptr;      // pinned mirror
+  double *p1 = nullptr, *p1p = nullptr, *p2 = nullptr;  // [y | xi] points (N (n+1))
+  double *part1 = nullptr, *part2 = nullptr;            // per-block partials
+  unsigned int* counter = nullptr;
+  SweepKernelInfo kpen{}, kupd{};
+  cudaGraphExec_t gexec = nullptr;
+  int graph_iters = 0;
+  int blocks = 0;
+  bool done = false;            // a finished solve is on the handle (multiplier export)
+  double mu = 0;                // mu of the last outer step
+};
+}  // namespace crb
+
+using namespace crb;  // the ABI translation units all work in crb
+
+struct cr_handle {
+  int device = 0;
+  cudaStream_t st = nullptr;
+  int64_t N = 0, n = 0, r0 = 0, r1 = 0, R = 0, ld = 0;
+  int RP = 0;
+  double gamma = 1e-3;
+  SweepKernelInfo kp{}, kw{};
+  int S = 0;            // column strips
+  int T = 0;            // sweep CTA column tiles = row-sum slices
+  int variant = 0;      // kSweepDfma / kSweepMma
+  // persistent small-N loop (small.cu)
+  bool small_mode = false;
+  SmallInfo ks{};
+  int small_grid = 0, small_S = 0, small_P = 0;
+  double *s_colpart = nullptr, *s_rowpart = nullptr, *s_scalpart = nullptr, *s_k2part = nullptr;
+  int G = 0;            // sweep CTAs (one persistent wave)
+  int maxspan = 0;      // tiles one CTA's unit range can touch
+  long long U = 0;      // (tile, row) units per CTA
+  int k2_blocks = 0;
+  unsigned int* counter = nullptr;
+  // device buffers
+  double *X = nullptr, *ybar = nullptr, *rowrec = nullptr, *colrec = nullptr;
+  double *V[2] = {nullptr, nullptr}, *vpos[2] = {nullptr, nullptr};
+  double *xbuf = nullptr, *aggsave = nullptr;
+  double *colpart = nullptr, *rowpart = nullptr, *scalpart = nullptr;
+  double *k2part = nullptr, *k2sum = nullptr, *hist = nullptr;
+  double *yout = nullptr, *xiout = nullptr;
+  double *pw_u = nullptr, *pw_v = nullptr, *pw_part = nullptr, *pw_sum = nullptr;
+  double *gram = nullptr, *ps_part = nullptr, *ps_part2 = nullptr, *ps_state = nullptr;
+  int power_grid = 0;  // closed-form power iteration (power.cu)
+  bool sigma_by_sweep = false;  // CRB_SIGMA=sweep: O(N^2 n) power steps through the sweep
+  double *consts = nullptr;  // {1, 1, 0}
+  int *izero = nullptr;      // constant 0 (slot index / never halted)
+  double *stage = nullptr;
+  int64_t stage_elems = 0;
+  int64_t hist_cap = 0;
+  DevCtrl* ctrl_d = nullptr;
+  DevCtrl* ctrl_h = nullptr;     // pinned mirror (latest copy)
+  DevCtrl* ctrl_poll = nullptr;  // pinned, 2 polling slots
+  long long* pause_h = nullptr;  // pinned {pause_at, halt}
+  // NCCL
+  ncclComm_t comm = nullptr;
+  int rank = 0, world = 1;
+  // loop state
+  cr_papg_config cfg{};
+  bool begun = false;
+  int graph_iters = 0;  // 0: direct launches
+  cudaGraphExec_t gexec = nullptr;
+  double sigma_C = 0, L = 0, sigma_seconds = 0;
+  int sigma_iters = 0, sigma_conv = 1;
+  std::chrono::steady_clock::time_point t_begin;
+  double loop_seconds = 0;
+  // timing
+  cudaEvent_t ev_start = nullptr, ev_end = nullptr, ev_poll[2] = {nullptr, nullptr};
+  std::vector<cudaEvent_t> ev_sweep;  // pairs
+  double last_seconds = 0, last_sweep_seconds = 0;
+  int64_t last_launches = 0;
+  // standalone ALCC (alcc.cu)
+  crb::AlccBufs alcc{};
+  std::string err;
+};
+
+inline cr_status fail(cr_handle* h, cr_status s, const std::string& what) {
+  if (h) h->err = what;
+  return s;
+}
+
+#define CUDA_TRY(call)                                                                   \
+  do {                                                                                   \
+    cudaError_t e_ = (call);                                                             \
+    if (e_ != cudaSuccess)                                                               \
+      return fail(h, CR_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_));      \
+  } while (0)
+
+#define NCCL_TRY(call)                                                                   \
+  do {                                                                                   \
+    ncclResult_t r_ = (call);                                                            \
+    if (r_ != ncclSuccess)                                                               \
+      return fail(h, CR_ENCCL, std::string(#call) + ": " + ncclGetErrorString(r_));      \
+  } while (0)
+
+// Device buffers come from the device's stream-ordered memory pool, which is
+// told to keep freed memory: a service that creates a handle per solve reuses
+// the mapping instead of paying cudaMalloc/cudaFree of gigabytes each time.
+extern cudaStream_t g_alloc_stream;  // stream of the handle being created (capi.cu)
+template <typename T>
+inline cudaError_t dalloc(T** p, size_t count) {
+  return cudaMallocAsync((void**)p, (count ? count : 1) * sizeof(T), g_alloc_stream);
+}
+inline void dfree(void* p, cudaStream_t s) {
+  if (p) cudaFreeAsync(p, s);
+}
+inline void keep_pool_memory(int device) {
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+}
+
+inline int64_t payload_len(const cr_handle* h) { return h->N * (h->n + 2) + kScal; }
+
+inline SweepArgs sweep_args(cr_handle* h, int mode, bool agg_only) {
+  SweepArgs a{};
+  a.V0 = h->V[0];
+  a.V1 = h->V[1];
+  a.cur = &h->ctrl_d->cur;
+  a.rowrec = h->rowrec;
+  a.colrec = h->colrec;
+  a.colpart = h->colpart;
+  a.rowpart = h->rowpart;
+  a.scalpart = h->scalpart;
+  a.coef = agg_only ? h->consts : &h->ctrl_d->s_cur;
+  a.stopped = (mode == kModePapg && !agg_only) ? &h->ctrl_d->halt : nullptr;
+  a.invL = agg_only ? 0.0 : 1.0 / h->L;
+  a.N = h->N;
+  a.R = h->R;
+  a.r0 = h->r0;
+  a.ld = h->ld;
+  a.S = h->S;
+  a.T = h->T;
+  a.G = h->G;
+  a.U = h->U;
+  a.maxspan = h->maxspan;
+  return a;
+}
+
+inline ReduceArgs reduce_args(cr_handle* h, bool with_k2, const int* stopped, bool fuse_control) {
+  ReduceArgs a{};
+  a.colpart = h->colpart;
+  a.rowpart = h->rowpart;
+  a.scalpart = h->scalpart;
+  a.k2part = h->k2part;
+  a.agg_out = h->xbuf;
+  a.k2sum = with_k2 ? h->k2sum : nullptr;
+  a.stopped = stopped;
+  a.rank = h->rank;
+  a.ctrl = fuse_control ? h->ctrl_d : nullptr;
+  a.hist = h->hist;
+  a.counter = h->counter;
+  a.N = h->N;
+  a.ld = h->ld;
+  a.R = h->R;
+  a.r0 = h->r0;
+  a.nw = (long long)h->G * h->kp.warps_per_block;
+  a.nk2 = with_k2 ? h->k2_blocks : 0;
+  a.n1 = (int)h->n + 1;
+  a.S = h->T;
+  a.TC = h->kp.tile_cols;
+  a.G = h->G;
+  a.U = h->U;
+  a.maxspan = h->maxspan;
+  return a;
+}

@@ -69,6 +69,7 @@ struct PowerLoopArgs {
   int n;
   int max_iters;
   double tol;
+  int op;               // 0: C (cols N(n+1)), 1: A1 (cols N), 2: A2 (cols N n)
 };
 
 // one-shot metric sweeps over a given point (metrics.cu)

@@ -1,4 +1,4 @@
-// power.cu -- K4': sigma_max(C) by the power method (operators.cpp:302-339 on
+// power.cu -- K4': sigma_max(C), sigma_max(A1), sigma_max(A2) by the power method (operators.cpp:302-339 on
 // op_C, :353-369) with a closed-form O(N n^2) step, the whole iteration in one
 // cooperative launch.
 //
@@ -114,6 +114,47 @@ __device__ __forceinline__ void apply_point(const double* v, const double* X, co
   acc[1] += vu;
 }
 
+// op_A1 (operators.cpp:341-345): A1^T A1 = 2 (N I - 1 1^T) over all N(N-1)
+// rows, so u_l = 2 (N v_l - A) with A = sum v.
+__device__ __forceinline__ void apply_point_a1(const double* v, const double* sums, long long N,
+                                               long long l, double* u, double (&acc)[2]) {
+  const double a = __ldcg(v + l);
+  const double ul = 2.0 * ((double)N * a - sums[0]);
+  __stcg(u + l, ul);
+  acc[0] = fma(ul, ul, acc[0]);
+  acc[1] = fma(a, ul, acc[1]);
+}
+
+// op_A2 (operators.cpp:347-351): block diagonal, one n x n block per column
+// point l: M_l = sum_l1 (x_l1 - x_l)(x_l1 - x_l)^T = S - s x^T - x s^T + N x x^T
+template <int NN>
+__device__ __forceinline__ void apply_point_a2(const double* v, const double* X, const double* gram,
+                                               long long N, long long l, double* u,
+                                               double (&acc)[2]) {
+  const double* S = gram;
+  const double* sx = gram + NN * NN;
+  double b[NN], x[NN];
+  double xb = 0.0, sb = 0.0;
+#pragma unroll
+  for (int j = 0; j < NN; ++j) {
+    b[j] = __ldcg(v + l * NN + j);
+    x[j] = X[l * NN + j];
+    xb = fma(x[j], b[j], xb);
+    sb = fma(sx[j], b[j], sb);
+  }
+  const double Nxb = (double)N * xb;
+#pragma unroll
+  for (int j = 0; j < NN; ++j) {
+    double Sb = 0.0;
+#pragma unroll
+    for (int k = 0; k < NN; ++k) Sb = fma(S[j * NN + k], b[k], Sb);
+    const double uj = (Sb - sx[j] * xb) + x[j] * (Nxb - sb);
+    __stcg(u + l * NN + j, uj);
+    acc[0] = fma(uj, uj, acc[0]);
+    acc[1] = fma(b[j], uj, acc[1]);
+  }
+}
+
 // fixed-order block sum of W per-thread values with warp butterflies (small smem)
 template <int W>
 __device__ __forceinline__ void block_sum_store(double (&v)[W], double* out) {
@@ -169,15 +210,32 @@ __global__ void __launch_bounds__(kQBlock) power_loop_kernel(const PowerLoopArgs
       double acc[W];
 #pragma unroll
       for (int w = 0; w < W; ++w) acc[w] = 0.0;
-      for (long long l = tid; l < N; l += nthreads) sums_point<NN>(a.u, a.v, norm_u, a.X, N, l, acc);
+      if (a.op == 0) {
+        for (long long l = tid; l < N; l += nthreads)
+          sums_point<NN>(a.u, a.v, norm_u, a.X, N, l, acc);
+      } else {  // A1, A2: v = u / |u| (and A = sum v for A1)
+        const long long cols = a.op == 1 ? N : N * NN;
+        for (long long k = tid; k < cols; k += nthreads) {
+          const double vk = __ldcg(a.u + k) / norm_u;
+          __stcg(a.v + k, vk);
+          acc[0] += vk;
+        }
+      }
       block_sum_store<W>(acc, a.part + (long long)blockIdx.x * W);
     }
     grid.sync();
     grid_records_sum<W>(a.part, gridDim.x, sums);
     {
       double acc[2] = {0.0, 0.0};
-      for (long long l = tid; l < N; l += nthreads)
-        apply_point<NN>(a.v, a.X, a.gram, sums, N, l, a.u, acc);
+      if (a.op == 0) {
+        for (long long l = tid; l < N; l += nthreads)
+          apply_point<NN>(a.v, a.X, a.gram, sums, N, l, a.u, acc);
+      } else if (a.op == 1) {
+        for (long long l = tid; l < N; l += nthreads) apply_point_a1(a.v, sums, N, l, a.u, acc);
+      } else {
+        for (long long l = tid; l < N; l += nthreads)
+          apply_point_a2<NN>(a.v, a.X, a.gram, N, l, a.u, acc);
+      }
       block_sum_store<2>(acc, a.part2 + (long long)blockIdx.x * 2);
     }
     grid.sync();

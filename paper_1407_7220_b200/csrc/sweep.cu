@@ -82,7 +82,7 @@ struct ColState {       // registers of one lane's C columns
   bool valid[C];
 };
 struct Coef {
-  double s_c, s_p, beta, invL;
+  double s_c, s_p, beta, invL, cdiv;
 };
 struct Scal {
   double vv, vr, tr, nn;
@@ -117,6 +117,8 @@ __device__ __forceinline__ void run_stage(const StageView& sv, int nr, int lane,
       if (MODE == kModePapg) {
         vc = *reinterpret_cast<const VT*>(sv.vc + q * TC);
         vp = *reinterpret_cast<const VT*>(sv.vp + q * TC);
+      } else if (MODE == kModePenalty || MODE == kModePenaltyUpdate) {
+        vc = *reinterpret_cast<const VT*>(sv.vc + q * TC);
       }
       double rs = 0.0;
 #pragma unroll
@@ -147,6 +149,13 @@ __device__ __forceinline__ void run_stage(const StageView& sv, int nr, int lane,
           sc.tr = fma(th2, row, sc.tr);
           const double m = keep_if_neg(row);
           sc.nn = fma(m, m, sc.nn);
+        } else if (MODE == kModePenalty || MODE == kModePenaltyUpdate) {
+          v = keep_if_nonneg(vget(vc, k) - row);
+          if (MODE == kModePenaltyUpdate) vset(out, k, v / cf.cdiv);
+          sc.vv = fma(v, v, sc.vv);
+          sc.vr = fma(v, row, sc.vr);
+          const double m = keep_if_neg(row);
+          sc.nn = fma(m, m, sc.nn);
         } else {
           v = row;
           sc.vv = fma(row, row, sc.vv);
@@ -156,7 +165,8 @@ __device__ __forceinline__ void run_stage(const StageView& sv, int nr, int lane,
         for (int j = 0; j < NN; ++j) cs.acc[k][1 + j] = fma(v, x[j], cs.acc[k][1 + j]);
         rs += v;
       }
-      if (MODE == kModePapg) st_stream(reinterpret_cast<VT*>(sv.gout + q * sv.ld), out);
+      if (MODE == kModePapg || MODE == kModePenaltyUpdate)
+        st_stream(reinterpret_cast<VT*>(sv.gout + q * sv.ld), out);
       rs += __shfl_xor_sync(0xffffffffu, rs, 16);
       if (lane < 16) sv.srs[q * kRsPitch + lane] = rs;
     }
@@ -180,7 +190,8 @@ __global__ void __launch_bounds__(threads_per_cta<NN>()) sweep_kernel(const Swee
   uint64_t* empty = full + kNS;
 
   if (a.stopped != nullptr && *a.stopped) return;
-  const int cur = (MODE == kModePapg) ? *a.cur : 0;
+  const int cur = (MODE != kModePower) ? *a.cur : 0;
+  constexpr bool kPen = MODE == kModePenalty || MODE == kModePenaltyUpdate;
   const double* Vc = cur ? a.V1 : a.V0;
   double* Vp = cur ? a.V0 : a.V1;
 
@@ -220,8 +231,8 @@ __global__ void __launch_bounds__(threads_per_cta<NN>()) sweep_kernel(const Swee
           if (i >= kNS) mbar_wait(&empty[s], (uint32_t)(((i / kNS) - 1) & 1));
           const int nr = (int)min((long long)TR, rhi - r);
           double* st = stages + s * SD;
-          const uint32_t bytes =
-              (MODE == kModePapg ? 2u * nr * vbytes : 0u) + (uint32_t)nr * RP * 8u;
+          const uint32_t bytes = (MODE == kModePapg ? 2u * nr * vbytes : 0u) +
+                                 (kPen ? (uint32_t)nr * vbytes : 0u) + (uint32_t)nr * RP * 8u;
           mbar_arrive_expect_tx(&full[s], bytes);
           if (MODE == kModePapg) {
             for (int q = 0; q < nr; ++q) {
@@ -229,6 +240,9 @@ __global__ void __launch_bounds__(threads_per_cta<NN>()) sweep_kernel(const Swee
               bulk_g2s(st + q * TC, Vc + off, vbytes, &full[s], pol_stream);
               bulk_g2s(st + (TR + q) * TC, Vp + off, vbytes, &full[s], pol_stream);
             }
+          } else if (kPen) {
+            for (int q = 0; q < nr; ++q)
+              bulk_g2s(st + q * TC, Vc + (r + q) * a.ld + c0, vbytes, &full[s], pol_stream);
           }
           bulk_g2s(st + 2 * TR * TC, a.rowrec + (a.r0 + r) * RP, (uint32_t)nr * RP * 8u,
                    &full[s], pol_keep);
@@ -241,7 +255,7 @@ __global__ void __launch_bounds__(threads_per_cta<NN>()) sweep_kernel(const Swee
   // ---------------------------------------------------------------- consumers
   double* srs = srs_all + warp * 32 * kRsPitch;
   const int lane_off = warp * W + lane * C;
-  Coef cf{1.0, 0.0, 0.0, a.invL};
+  Coef cf{1.0, 0.0, 0.0, a.invL, a.cdiv};
   if (MODE == kModePapg) {
     cf.s_c = a.coef[0];
     cf.s_p = a.coef[1];
@@ -354,8 +368,10 @@ __global__ void __launch_bounds__(threads_per_cta<NN>()) sweep_kernel(const Swee
 template <int NN>
 SweepKernelInfo info_for(int mode) {
   SweepKernelInfo inf{};
-  inf.fn = mode == kModePapg ? (const void*)sweep_kernel<NN, kModePapg>
-                             : (const void*)sweep_kernel<NN, kModePower>;
+  inf.fn = mode == kModePapg      ? (const void*)sweep_kernel<NN, kModePapg>
+           : mode == kModePower   ? (const void*)sweep_kernel<NN, kModePower>
+           : mode == kModePenalty ? (const void*)sweep_kernel<NN, kModePenalty>
+                                  : (const void*)sweep_kernel<NN, kModePenaltyUpdate>;
   inf.strip_cols = 32 * cols_per_lane<NN>();
   inf.warps_per_block = consumer_warps<NN>();
   inf.tile_cols = tile_cols<NN>();

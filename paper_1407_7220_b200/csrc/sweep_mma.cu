@@ -79,7 +79,7 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
 }
 
 struct MCoef {
-  double s_c, s_p, beta, invL;
+  double s_c, s_p, beta, invL, cdiv;
 };
 struct MScal {
   double vv, vr, tr, nn;
@@ -90,6 +90,7 @@ template <int NN, int MODE, bool MASK, bool UNIT>
 __device__ __forceinline__ void mma_stage(const double* __restrict__ sv, const double* __restrict__ svp,
                                           const double* __restrict__ srec, double* gout,
                                           long long ld, long long gcol0, long long grow0, int nr,
+                                          long long ncols,
                                           int lane, const double (&A)[mma_ct<NN>()][ksteps<NN>()],
                                           double (&D)[mma_ct<NN>()][fblocks<NN>()][2],
                                           const double (&Cc)[mma_ct<NN>()], const MCoef& cf,
@@ -133,7 +134,9 @@ __device__ __forceinline__ void mma_stage(const double* __restrict__ sv, const d
       const bool rv = !MASK || rr < nr;  // row present in this (partial) stage
       double row = j == 0 ? d0 : d1;
       if (SPLIT) row += yr[j] + Cc[ct];  // y_l1 - c_l2 (Cc holds -c_l2)
-      if (MASK && (gcol0 + cl == grow0 + rr || !rv)) row = 0.0;
+      // diagonal, rows past a partial stage, pad columns (with y - c split out
+      // of the MMA a pad column's zero fragments no longer zero its row)
+      if (MASK && (gcol0 + cl == grow0 + rr || !rv || gcol0 + cl >= ncols)) row = 0.0;
       if (MODE == kModePapg) {
         const double c1 = sv[rr * kTCP + cl];
         const double p1 = svp[rr * kTCP + cl];
@@ -152,6 +155,14 @@ __device__ __forceinline__ void mma_stage(const double* __restrict__ sv, const d
         const double m = keep_if_neg(row);
         sc.nn = fma(m, m, sc.nn);
         if (rv) st_stream(gout + rr * ld + cl, v[j]);
+      } else if (MODE == kModePenalty || MODE == kModePenaltyUpdate) {
+        const double th = (MASK && !rv) ? 0.0 : sv[rr * kTCP + cl];
+        v[j] = keep_if_nonneg(th - row);
+        sc.vv = fma(v[j], v[j], sc.vv);
+        sc.vr = fma(v[j], row, sc.vr);
+        const double m = keep_if_neg(row);
+        sc.nn = fma(m, m, sc.nn);
+        if (MODE == kModePenaltyUpdate && rv) st_stream(gout + rr * ld + cl, v[j] / cf.cdiv);
       } else {
         v[j] = row;
         sc.vv = fma(row, row, sc.vv);
@@ -180,7 +191,8 @@ __global__ void __launch_bounds__(mma_threads<NN>(), kMinCtas) sweep_mma_kernel(
   uint64_t* empty = full + kNS;
 
   if (a.stopped != nullptr && *a.stopped) return;
-  const int cur = (MODE == kModePapg) ? *a.cur : 0;
+  const int cur = (MODE != kModePower) ? *a.cur : 0;
+  constexpr bool kPen = MODE == kModePenalty || MODE == kModePenaltyUpdate;
   const double* Vc = cur ? a.V1 : a.V0;
   double* Vp = cur ? a.V0 : a.V1;
 
@@ -217,8 +229,8 @@ __global__ void __launch_bounds__(mma_threads<NN>(), kMinCtas) sweep_mma_kernel(
           if (i >= kNS) mbar_wait(&empty[s], (uint32_t)(((i / kNS) - 1) & 1));
           const int nr = (int)min((long long)kTR, rhi - r);
           double* st = stages + s * SD;
-          const uint32_t bytes =
-              (MODE == kModePapg ? 2u * nr * vbytes : 0u) + (uint32_t)nr * RQ * 8u;
+          const uint32_t bytes = (MODE == kModePapg ? 2u * nr * vbytes : 0u) +
+                                 (kPen ? (uint32_t)nr * vbytes : 0u) + (uint32_t)nr * RQ * 8u;
           mbar_arrive_expect_tx(&full[s], bytes);
           if (MODE == kModePapg) {
             for (int qq = 0; qq < nr; ++qq) {
@@ -226,6 +238,9 @@ __global__ void __launch_bounds__(mma_threads<NN>(), kMinCtas) sweep_mma_kernel(
               bulk_g2s(st + qq * kTCP, Vc + off, vbytes, &full[s], pol_stream);
               bulk_g2s(st + (kTR + qq) * kTCP, Vp + off, vbytes, &full[s], pol_stream);
             }
+          } else if (kPen) {
+            for (int qq = 0; qq < nr; ++qq)
+              bulk_g2s(st + qq * kTCP, Vc + (r + qq) * a.ld + c0, vbytes, &full[s], pol_stream);
           }
           bulk_g2s(st + 2 * kTR * kTCP, a.rowrec + (a.r0 + r) * RQ, (uint32_t)nr * RQ * 8u,
                    &full[s], pol_keep);
@@ -238,7 +253,7 @@ __global__ void __launch_bounds__(mma_threads<NN>(), kMinCtas) sweep_mma_kernel(
   // ---------------------------------------------------------------- consumers
   const int q = lane & 3;
   const int c8 = lane >> 2;
-  MCoef cf{1.0, 0.0, 0.0, a.invL};
+  MCoef cf{1.0, 0.0, 0.0, a.invL, a.cdiv};
   if (MODE == kModePapg) {
     cf.s_c = a.coef[0];
     cf.s_p = a.coef[1];
@@ -285,21 +300,23 @@ __global__ void __launch_bounds__(mma_threads<NN>(), kMinCtas) sweep_mma_kernel(
         const double* srec = st + 2 * kTR * kTCP;
         double* gout = Vp + r * a.ld + gcol0;
         const long long grow0 = a.r0 + r;
-        // warp-uniform: no diagonal in this 8-row block of the warp's columns, full stage
-        const bool clean = nr == kTR && (grow0 + kTR <= gcol0 || grow0 >= gcol0 + kW);
+        // warp-uniform: no diagonal in this 8-row block of the warp's columns, full
+        // stage, no pad column
+        const bool clean = nr == kTR && gcol0 + kW <= a.N &&
+                           (grow0 + kTR <= gcol0 || grow0 >= gcol0 + kW);
         if (clean) {
           if (unit_scale)
-            mma_stage<NN, MODE, false, true>(sv, svp, srec, gout, a.ld, gcol0, grow0, nr, lane, A,
+            mma_stage<NN, MODE, false, true>(sv, svp, srec, gout, a.ld, gcol0, grow0, nr, a.N, lane, A,
                                              D, Cc, cf, sc, rsj);
           else
-            mma_stage<NN, MODE, false, false>(sv, svp, srec, gout, a.ld, gcol0, grow0, nr, lane,
+            mma_stage<NN, MODE, false, false>(sv, svp, srec, gout, a.ld, gcol0, grow0, nr, a.N, lane,
                                               A, D, Cc, cf, sc, rsj);
         } else {
           if (unit_scale)
-            mma_stage<NN, MODE, true, true>(sv, svp, srec, gout, a.ld, gcol0, grow0, nr, lane, A,
+            mma_stage<NN, MODE, true, true>(sv, svp, srec, gout, a.ld, gcol0, grow0, nr, a.N, lane, A,
                                              D, Cc, cf, sc, rsj);
           else
-            mma_stage<NN, MODE, true, false>(sv, svp, srec, gout, a.ld, gcol0, grow0, nr, lane, A,
+            mma_stage<NN, MODE, true, false>(sv, svp, srec, gout, a.ld, gcol0, grow0, nr, a.N, lane, A,
                                              D, Cc, cf, sc, rsj);
         }
       }
@@ -375,8 +392,10 @@ template <int NN>
 SweepKernelInfo info_for(int mode) {
   CRB_GEO(NN)
   SweepKernelInfo inf{};
-  inf.fn = mode == kModePapg ? (const void*)sweep_mma_kernel<NN, kModePapg>
-                             : (const void*)sweep_mma_kernel<NN, kModePower>;
+  inf.fn = mode == kModePapg      ? (const void*)sweep_mma_kernel<NN, kModePapg>
+           : mode == kModePower   ? (const void*)sweep_mma_kernel<NN, kModePower>
+           : mode == kModePenalty ? (const void*)sweep_mma_kernel<NN, kModePenalty>
+                                  : (const void*)sweep_mma_kernel<NN, kModePenaltyUpdate>;
   inf.strip_cols = kW;
   inf.warps_per_block = kCW;
   inf.tile_cols = kTC;

@@ -8,6 +8,7 @@ Names, argument meaning and error behaviour follow the reference:
   certificate_for_iterate(...)                  papg.hpp:85-90
   prepare_problem(data, gamma)                  preprocess.hpp:42
   gen_instance(spec)                            testgen.hpp:27
+  alcc_solve(prep, cfg, warm=None)              alcc.hpp:134-136 (standalone ALCC)
 Shape / precondition errors raise ValueError (std::invalid_argument);
 numerical failures raise RuntimeError (std::runtime_error), e.g.
 "papg: non-finite dual gradient" (papg.cpp:184-185).
@@ -209,6 +210,46 @@ def certificate_for_iterate(gamma, delta, B_xi_estimate, sigma_max_C):  # papg.c
     return float(out[0]), float(out[1])
 
 
+@dataclass
+class AlccConfig:  # alcc.hpp:71-83
+    mu1: float = 1.0
+    tau1_scale: float = 1e-2
+    alpha1_scale: float = 1e-3
+    c: float = 5.0
+    kappa: float = 0.5
+    max_outer: int = 30
+    mapg_cap: int = 200000
+    infeas_norm_tol: float = 1e-1
+    gap_norm_tol: float = 1e-6
+    max_seconds: float = float("inf")
+    record_history: bool = True
+    # device knobs: inject spectral norms instead of estimating them
+    sigma_A1: float = 0.0
+    sigma_A2: float = 0.0
+
+    def to_c(self, bounds: "ProblemBounds") -> nat.AlccConfigC:
+        return nat.AlccConfigC(self.mu1, self.tau1_scale, self.alpha1_scale, self.c, self.kappa,
+                               self.max_outer, self.mapg_cap, self.infeas_norm_tol,
+                               self.gap_norm_tol, self.max_seconds, int(self.record_history), 0,
+                               self.sigma_A1, self.sigma_A2, bounds.Bbar_y, bounds.Bbar_xi)
+
+
+@dataclass
+class AlccResult:  # alcc.hpp:110-118
+    point: PrimalPoint
+    multiplier: np.ndarray | None
+    objective: float
+    certified_gap: float
+    infeas_raw: float
+    mapg_iters_total: int
+    report: SolveReport
+    gap_raw: float = 0.0
+    mapg_iters: np.ndarray | None = None
+    hit_cap: bool = False
+    sigma_A1: float = 0.0
+    sigma_A2: float = 0.0
+
+
 class DualSolver:
     """One device handle over pair rows [row_begin, row_end) of an N x N
     problem (the whole matrix on one GPU by default). Owns the device-resident
@@ -381,6 +422,59 @@ class DualSolver:
         s = C.c_double(0)
         _raise(self._L.cr_time_sweep(self.h, k, C.byref(s)), self.h)
         return s.value
+
+
+    # ---- standalone ALCC (alcc.cpp:193-208) on this handle's device buffers
+    def sigma_A(self, which, tol=1e-6, max_iters=5000):
+        """estimate_sigma_max(op_A1) (which=1) / (op_A2) (which=2), operators.cpp:302-351."""
+        s = C.c_double(0)
+        it = C.c_int32(0)
+        cv = C.c_int32(0)
+        _raise(self._L.cr_sigma_A(self.h, which, tol, max_iters, C.byref(s), C.byref(it),
+                                  C.byref(cv)), self.h)
+        return s.value, it.value, bool(cv.value)
+
+    def alcc(self, cfg: "AlccConfig", bounds: ProblemBounds, warm: PrimalPoint):
+        c = cfg.to_c(bounds)
+        N, n = self.N, self.n
+        y = np.empty(N)
+        xi = np.empty(N * n)
+        K = max(int(cfg.max_outer), 0)
+        hist = np.zeros((max(K, 1), 8))
+        mi = np.zeros(max(K, 1), np.int64)
+        res = nat.AlccResultC()
+        _raise(self._L.cr_alcc_solve(self.h, C.byref(c), nat.ptr(_f64(warm.y)),
+                                     nat.ptr(_f64(warm.xi)), nat.ptr(y), nat.ptr(xi),
+                                     nat.ptr(hist) if cfg.record_history else None,
+                                     mi.ctypes.data_as(C.POINTER(C.c_int64)), C.byref(res)),
+               self.h)
+        k = int(res.outer_iters)
+        return res, y, xi, hist[:k] if cfg.record_history else hist[:0], mi[:k]
+
+    def alcc_multiplier(self, row_begin=0, row_end=None):
+        row_end = self.N if row_end is None else row_end
+        out = np.empty((row_end - row_begin) * (self.N - 1))
+        _raise(self._L.cr_alcc_multiplier(self.h, row_begin, row_end, nat.ptr(out)), self.h)
+        return out
+
+
+def alcc_solve(prep: PreparedProblem, cfg: AlccConfig | None = None,
+               warm: PrimalPoint | None = None, device=0, want_multiplier=True) -> AlccResult:
+    """Standalone Fig-3 augmented Lagrangian (alcc.cpp:193-208 -> alcc_core
+    :54-191), centres (ybar, 0), balls from prep.bounds, warm start = the
+    exactly feasible affine point unless given (runner.cpp:278-286)."""
+    cfg = cfg or AlccConfig()
+    warm = warm or prep.feasible
+    data = prep.data
+    with DualSolver(data.xs, data.ys, prep.bounds.gamma, device) as s:
+        res, y, xi, hist, mi = s.alcc(cfg, prep.bounds, warm)
+        mult = s.alcc_multiplier() if (want_multiplier and res.outer_iters > 0) else None
+    history = [MetricsSnapshot(int(h[0]), *map(float, h[1:])) for h in hist]
+    rep = SolveReport(history=history, reason=TermReason(res.reason), iters=int(res.outer_iters),
+                      wall_seconds=res.wall_seconds, history_array=hist)
+    return AlccResult(PrimalPoint(y, xi), mult, res.objective, res.certified_gap, res.infeas_raw,
+                      int(res.mapg_iters_total), rep, res.gap_raw, mi, bool(res.hit_cap_any),
+                      res.sigma_A1, res.sigma_A2)
 
 
 def _solve(prep: PreparedProblem, cfg: PapgConfig, theta0, use_momentum, want_dual=True):
