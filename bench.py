@@ -50,6 +50,9 @@ def parse():
     ap.add_argument("--config", choices=sorted(CONFIGS), default="cfg2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true", help="skip time-to-tolerance and e2e")
+    ap.add_argument("--solver", choices=["papg", "alcc"], default="papg",
+                    help="papg: the north-star P-APG step (default); alcc: one MAPG iteration "
+                         "of the standalone ALCC (SURVEY 8f row f1)")
     return ap.parse_args()
 
 
@@ -349,8 +352,142 @@ def run_ours(args):
     return 0
 
 
+ALCC_BYTES_PER_PAIR = 8  # theta_k read once per MAPG iteration
+
+
+def cpu_alcc_rate(cfg, threads, k_lo=1, k_hi=3):
+    """Oracle ALCC (alcc.cpp:54-191 restated) per-MAPG-iteration rate: two
+    single-outer-step runs with MAPG capped at k_lo and k_hi iterations."""
+    from oracle import oracle as O
+
+    X, y = O.gen_instance(cfg["kind"], cfg["N"], cfg["n"], cfg["noise"], 1, cfg["pieces"])
+    p = O.prepare(X, y)
+    kw = dict(gamma=p.gamma, Bbar_y=p.Bbar_y, Bbar_xi=p.Bbar_xi, warm_y=p.feas_y,
+              warm_xi=p.feas_xi, sigma_A1=100.0, sigma_A2=100.0, max_outer=1,
+              alpha1_scale=1e-30, infeas_norm_tol=-1.0, threads=threads, record_history=False)
+    t0 = time.perf_counter()
+    a = O.alcc(X, p.ys, mapg_cap=k_lo, **kw)
+    b = O.alcc(X, p.ys, mapg_cap=k_hi, **kw)
+    spent = time.perf_counter() - t0
+    per_iter = max(b.wall_seconds - a.wall_seconds, 1e-9) / max(b.mapg_iters_total -
+                                                                a.mapg_iters_total, 1)
+    N = cfg["N"]
+    sample = (f"{cfg['kind']} N={N} n={cfg['n']}: oracle ALCC, one outer step with MAPG capped at "
+              f"{k_lo} and {k_hi} iterations, {threads} thread(s), {per_iter:.3f} s/MAPG iteration")
+    return N * N / per_iter, spent, sample
+
+
+def run_alcc_reference(args):
+    if int(os.environ.get("RANK", "0")) != 0:
+        return 0
+    cfg = workload(args.config, 1)
+    threads = os.cpu_count() or 1
+    need = 7 * 8 * cfg["N"] ** 2
+    if need > 0.8 * host_mem_available():
+        print(json.dumps({"impl": "reference", "unavailable": "ALCC oracle needs 7 N^2 doubles"}))
+        return 0
+    rate, spent, sample = cpu_alcc_rate(cfg, threads)
+    line = {
+        "impl": "reference", "metric": "MAPG pair evaluations/s", "value": rate,
+        "unit": "pair-evals/s", "n_gpus": args.gpus, "steps": 2, "warmup": 1,
+        "ms_per_step": cfg["N"] ** 2 / rate * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"alcc {args.config}: {cfg['kind']} N={cfg['N']} n={cfg['n']}",
+                   "N": cfg["N"], "n": cfg["n"], "solver": "alcc"},
+        "cpu_baseline": {"value": rate, "unit": "pair-evals/s", "cores": threads, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": rate, "unit": "pair-evals/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_alcc_ours(args):
+    """One MAPG iteration of the standalone ALCC is the step (penalty sweep +
+    reduce + gradient + projection/momentum kernels, device-resident)."""
+    import torch
+
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    rank = int(os.environ.get("RANK", "0"))
+    torch.cuda.set_device(local)
+    import paper_1407_7220_b200 as crb
+
+    cfg = workload(args.config, 1)
+    N, n = cfg["N"], cfg["n"]
+    data = crb.gen_instance(crb.GeneratorSpec(cfg["kind"], n, N, cfg["noise"], 1, cfg["pieces"]))
+    prep = crb.prepare_problem(data)
+    W, K = max(args.warmup, 3), max(args.steps, 10)
+    with crb.DualSolver(prep.data.xs, prep.data.ys, prep.bounds.gamma, local) as s:
+        t0 = time.perf_counter()
+        s1 = s.sigma_A(1)
+        s2 = s.sigma_A(2)
+        sig_s = time.perf_counter() - t0
+        # alpha1_scale -> 0: the displacement test never fires, MAPG runs exactly cap steps
+        base = dict(max_outer=1, alpha1_scale=1e-30, infeas_norm_tol=-1.0, sigma_A1=s1[0],
+                    sigma_A2=s2[0], record_history=False)
+        s.alcc(crb.AlccConfig(mapg_cap=W, **base), prep.bounds, prep.feasible)
+        with ClockSampler(local) as clk:
+            torch.cuda.synchronize()
+            res, *_ = s.alcc(crb.AlccConfig(mapg_cap=K, **base), prep.bounds, prep.feasible)
+            torch.cuda.synchronize()
+        sweep_s = s.time_penalty_sweep(20)
+        variant = s.sweep_variant
+    iters = int(res.mapg_iters_total)
+    assert iters == K, (iters, K)
+    dev = res.mapg_seconds
+    value = N * N * iters / dev
+    peaks, peak_kind = measured_peaks()
+    achieved = ALCC_BYTES_PER_PAIR * N * N / sweep_s / 1e9
+    roofline = {"bound": "hbm", "unit": "GB/s", "achieved": achieved, "peak": peaks["hbm_gbs"],
+                "frac": achieved / peaks["hbm_gbs"], "traffic": None, "peak_kind": peak_kind,
+                "kernel": f"penalty sweep ({variant})",
+                "algorithmic_bytes_per_launch": ALCC_BYTES_PER_PAIR * N * N,
+                "sweep_share_of_step": sweep_s * iters / dev,
+                "note": "8 B/pair leaves the sweep FP64-issue bound, not HBM bound"}
+    extras = {}
+    if not args.no_extras:
+        ecfg = crb.AlccConfig(mapg_cap=K, max_outer=1, alpha1_scale=1e-30, infeas_norm_tol=-1.0,
+                              record_history=False)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        er = crb.alcc_solve(prep, ecfg, want_multiplier=False)
+        e_s = time.perf_counter() - t0
+        extras["e2e"] = {"value": N * N * er.mapg_iters_total / e_s, "unit": "pair-evals/s",
+                         "h2d_bytes_per_step": 8 * (N * n + N) * 2 / K,
+                         "d2h_bytes_per_step": 8 * (N + N * n) / K, "seconds": e_s,
+                         "iterations": er.mapg_iters_total,
+                         "includes": "handle create + H2D, sigma(A1), sigma(A2), one outer step "
+                                     "of K MAPG iterations, D2H of (y, xi)"}
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline and 7 * 8 * N * N <= 0.8 * host_mem_available():
+        threads = os.cpu_count() or 1
+        rate, spent, sample = cpu_alcc_rate(cfg, threads)
+        cpu = {"value": rate, "unit": "pair-evals/s", "cores": threads, "kind": "port",
+               "sample": sample}
+    line = {
+        "metric": "MAPG pair evaluations/s", "value": value, "unit": "pair-evals/s", "n_gpus": 1,
+        "steps": K, "warmup": W, "ms_per_step": dev / iters * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded BASELINE generator)",
+        "config": {"workload": f"alcc {args.config}: {cfg['kind']} N={N} n={n} (one outer step, "
+                               f"K MAPG iterations)", "N": N, "n": n, "solver": "alcc",
+                   "sweep_variant": variant, "sigma_A": [s1[0], s2[0]],
+                   "sigma_power_steps": [s1[1], s2[1]], "sigma_seconds": sig_s,
+                   "l2": "theta (0.8 GB) > L2, no flush",
+                   "timing": "CUDA events around the MAPG graph launches"},
+        "roofline": roofline, "cpu_baseline": cpu, "gpu_launches": int(res.launches),
+        "clocks": clk.summary(),
+    }
+    line.update(extras)
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def main():
     args = parse()
+    if args.solver == "alcc":
+        return run_alcc_reference(args) if args.impl == "reference" else run_alcc_ours(args)
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

@@ -213,6 +213,8 @@ typedef struct {
   double sigma_A1;
   double sigma_A2;
   double sigma_seconds;
+  double mapg_seconds;     /* device time of the MAPG loops (CUDA events) */
+  int64_t launches;        /* kernels enqueued by the MAPG loops (incl. halted no-ops) */
 } cr_alcc_result;
 
 /* sigma_max(A1) (which = 1) or sigma_max(A2) (which = 2) by the reference's
@@ -229,6 +231,8 @@ cr_status cr_alcc_solve(cr_handle *h, const cr_alcc_config *cfg, const double *w
 /* lambda = mu_k (theta_k - R(y, xi))_+ of the last outer step for pair rows
    l1 in [row_begin, row_end), canonical order ((row_end-row_begin) x (N-1)). */
 cr_status cr_alcc_multiplier(cr_handle *h, int64_t row_begin, int64_t row_end, double *out);
+/* Time k penalty-sweep launches (theta_k at the handle's records, read-only). */
+cr_status cr_time_penalty_sweep(cr_handle *h, int32_t k, double *avg_seconds);
 
 /* ---- host utilities (no device) ----------------------------------------- */
 /* kinds: 0 quadratic, 1 exponential, 2 affine-noiseless, 3 custom-1d

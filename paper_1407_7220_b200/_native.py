@@ -58,7 +58,8 @@ class AlccResultC(C.Structure):
         ("hit_cap_any", C.c_int32), ("sigma_A1_iters", C.c_int32), ("sigma_A2_iters", C.c_int32),
         ("certified_gap", C.c_double), ("infeas_raw", C.c_double), ("gap_raw", C.c_double),
         ("objective", C.c_double), ("wall_seconds", C.c_double), ("sigma_A1", C.c_double),
-        ("sigma_A2", C.c_double), ("sigma_seconds", C.c_double),
+        ("sigma_A2", C.c_double), ("sigma_seconds", C.c_double), ("mapg_seconds", C.c_double),
+        ("launches", C.c_int64),
     ]
 
 
@@ -71,7 +72,7 @@ EXPORTS = [
     "cr_sweep_variant", "cr_papg_begin_resume", "cr_set_observations", "cr_infeasibility",
     "cr_duality_gap", "cr_evaluate_estimator", "cr_repair_feasibility",
     "cr_gen_instance", "cr_prepare_problem", "cr_certificate", "cr_momentum_next",
-    "cr_sigma_A", "cr_alcc_solve", "cr_alcc_multiplier",
+    "cr_sigma_A", "cr_alcc_solve", "cr_alcc_multiplier", "cr_time_penalty_sweep",
 ]
 
 _lib = None
@@ -129,6 +130,7 @@ def load():
         "cr_alcc_solve": (st, [vp, C.POINTER(AlccConfigC), _P, _P, _P, _P, _P,
                                C.POINTER(i64), C.POINTER(AlccResultC)]),
         "cr_alcc_multiplier": (st, [vp, i64, i64, _P]),
+        "cr_time_penalty_sweep": (st, [vp, i32, _P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

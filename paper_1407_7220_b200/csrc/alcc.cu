@@ -604,12 +604,15 @@ cr_status cr_alcc_solve(cr_handle* h, const cr_alcc_config* cfg, const double* w
     if (s != CR_OK) return s;
   }
   CUDA_TRY(launch_alcc(f.project, 1, kSBlock, aa, h->st));
+  double mapg_ms = 0;
+  int64_t launches = 0;
 
-  // P_1 at the start point (alcc.cpp:75-84)
+  // P_1 at the start point (alcc.cpp:75-84); the update sweep supplies S_vv and
+  // writes v / c into the unused slot (overwritten by the first outer step)
   double mu = cfg->mu1;
   double tau, alpha_y, alpha_xi;
   {
-    const cr_status s = outer_stats(h, f, aa, false, cfg->c);
+    const cr_status s = outer_stats(h, f, aa, true, cfg->c);
     if (s != CR_OK) return s;
     const double p1 = d.stats[0] / (2.0 * mu) + gamma * d.stats[1] / (2.0 * mu) + 0.5 * d.stats[5];
     if (!std::isfinite(p1)) return fail(h, CR_ENONFINITE, "alcc: non-finite P_1 at the start point");
@@ -647,12 +650,21 @@ cr_status cr_alcc_solve(cr_handle* h, const cr_alcc_config* cfg, const double* w
       const cr_status s = push_dev(h);
       if (s != CR_OK) return s;
     }
+    CUDA_TRY(cudaEventRecord(h->ev_start, h->st));
     CUDA_TRY(launch_alcc(f.reset, b.blocks, kPBlock, aa, h->st));
+    launches += 1;
     for (;;) {
       CUDA_TRY(cudaGraphLaunch(b.gexec, h->st));
+      launches += 4 * (int64_t)b.graph_iters;
+      CUDA_TRY(cudaEventRecord(h->ev_end, h->st));
       const cr_status s = pull_dev(h);
       if (s != CR_OK) return s;
       if (d.halt) break;
+    }
+    {
+      float ms = 0;
+      CUDA_TRY(cudaEventElapsedTime(&ms, h->ev_start, h->ev_end));
+      mapg_ms += ms;
     }
     if (d.nonfinite) {
       res->reason = CR_ERROR;
@@ -730,6 +742,23 @@ cr_status cr_alcc_solve(cr_handle* h, const cr_alcc_config* cfg, const double* w
     res->objective = 0.5 * sy;
   }
   res->wall_seconds = seconds();
+  res->mapg_seconds = mapg_ms * 1e-3;
+  res->launches = launches;
+  return CR_OK;
+}
+
+cr_status cr_time_penalty_sweep(cr_handle* h, int32_t k, double* avg_seconds) {
+  if (!h || k < 1 || !avg_seconds) return CR_EINVAL;
+  if (!h->alcc.done) return fail(h, CR_ESTATE, "alcc: no finished solve on this handle");
+  CUDA_TRY(cudaSetDevice(h->device));
+  const SweepArgs sa = penalty_sweep_args(h, 1.0);  // read-only on theta
+  CUDA_TRY(cudaEventRecord(h->ev_start, h->st));
+  for (int i = 0; i < k; ++i) CUDA_TRY((cudaError_t)launch_sweep(h->alcc.kpen, sa, h->st));
+  CUDA_TRY(cudaEventRecord(h->ev_end, h->st));
+  CUDA_TRY(cudaEventSynchronize(h->ev_end));
+  float ms = 0;
+  CUDA_TRY(cudaEventElapsedTime(&ms, h->ev_start, h->ev_end));
+  *avg_seconds = ms * 1e-3 / k;
   return CR_OK;
 }
 

@@ -89,9 +89,9 @@ struct SweepArgs {
 // kModePapg:   the P-APG step above (reads V, V'; writes V')
 // kModePower:  aggregates of the residual itself (sigma_max(C) by sweeps)
 // kModePenalty / kModePenaltyUpdate: the ALCC penalty oracle (alcc.cpp:33-47,
-//   :124-127): v = max(theta - row, 0) with theta = V[cur]; aggregates of v and
-//   scalars (S_vv, S_vr, -, S_nn). The update variant also writes v / cdiv
-//   into V[1-cur] (the next outer multiplier, alcc.cpp:176).
+//   :124-127): v = max(theta - row, 0) with theta = V[cur]; aggregates of v.
+//   The update variant (outer step) also accumulates the scalars (S_vv, S_vr,
+//   -, S_nn) and writes v / cdiv into V[1-cur] (the next multiplier, alcc.cpp:176).
 enum SweepMode { kModePapg = 0, kModePower = 1, kModePenalty = 2, kModePenaltyUpdate = 3 };
 
 // returns the kernel attribute table entry for (n, mode); host side helpers

@@ -151,11 +151,13 @@ __device__ __forceinline__ void run_stage(const StageView& sv, int nr, int lane,
           sc.nn = fma(m, m, sc.nn);
         } else if (MODE == kModePenalty || MODE == kModePenaltyUpdate) {
           v = keep_if_nonneg(vget(vc, k) - row);
-          if (MODE == kModePenaltyUpdate) vset(out, k, v / cf.cdiv);
-          sc.vv = fma(v, v, sc.vv);
-          sc.vr = fma(v, row, sc.vr);
-          const double m = keep_if_neg(row);
-          sc.nn = fma(m, m, sc.nn);
+          if (MODE == kModePenaltyUpdate) {  // outer step: statistics + theta_{k+1}
+            vset(out, k, v / cf.cdiv);
+            sc.vv = fma(v, v, sc.vv);
+            sc.vr = fma(v, row, sc.vr);
+            const double m = keep_if_neg(row);
+            sc.nn = fma(m, m, sc.nn);
+          }
         } else {
           v = row;
           sc.vv = fma(row, row, sc.vv);

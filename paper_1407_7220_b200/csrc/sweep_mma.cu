@@ -158,11 +158,13 @@ __device__ __forceinline__ void mma_stage(const double* __restrict__ sv, const d
       } else if (MODE == kModePenalty || MODE == kModePenaltyUpdate) {
         const double th = (MASK && !rv) ? 0.0 : sv[rr * kTCP + cl];
         v[j] = keep_if_nonneg(th - row);
-        sc.vv = fma(v[j], v[j], sc.vv);
-        sc.vr = fma(v[j], row, sc.vr);
-        const double m = keep_if_neg(row);
-        sc.nn = fma(m, m, sc.nn);
-        if (MODE == kModePenaltyUpdate && rv) st_stream(gout + rr * ld + cl, v[j] / cf.cdiv);
+        if (MODE == kModePenaltyUpdate) {  // outer step: statistics + theta_{k+1}
+          sc.vv = fma(v[j], v[j], sc.vv);
+          sc.vr = fma(v[j], row, sc.vr);
+          const double m = keep_if_neg(row);
+          sc.nn = fma(m, m, sc.nn);
+          if (rv) st_stream(gout + rr * ld + cl, v[j] / cf.cdiv);
+        }
       } else {
         v[j] = row;
         sc.vv = fma(row, row, sc.vv);

@@ -451,6 +451,12 @@ class DualSolver:
         k = int(res.outer_iters)
         return res, y, xi, hist[:k] if cfg.record_history else hist[:0], mi[:k]
 
+    def time_penalty_sweep(self, k=10):
+        """Times k penalty-sweep launches on the last ALCC state (read-only)."""
+        s = C.c_double(0)
+        _raise(self._L.cr_time_penalty_sweep(self.h, k, C.byref(s)), self.h)
+        return s.value
+
     def alcc_multiplier(self, row_begin=0, row_end=None):
         row_end = self.N if row_end is None else row_end
         out = np.empty((row_end - row_begin) * (self.N - 1))
