@@ -22,6 +22,8 @@
  *                        (alcc_core src/alcc.cpp:54-191, MAPG src/engines.cpp:57-106)
  *   cr_alcc_multiplier   AlccResult::multiplier                  include/cvxreg/alcc.hpp:110-118
  *   cr_sigma_A           estimate_sigma_max(op_A1 / op_A2)       src/operators.cpp:341-351
+ *   cr_set_partition     make_partition + DualDecomposition      src/dataset.cpp:119-130,
+ *                        (general-K P-APG(ALCC))                 src/papg.cpp:66-132
  *
  * Threading: a handle is confined to one host thread. Distinct handles may
  * be driven concurrently. Sharded runs use one handle (and one process) per
@@ -233,6 +235,22 @@ cr_status cr_alcc_solve(cr_handle *h, const cr_alcc_config *cfg, const double *w
 cr_status cr_alcc_multiplier(cr_handle *h, int64_t row_begin, int64_t row_end, double *out);
 /* Time k penalty-sweep launches (theta_k at the handle's records, read-only). */
 cr_status cr_time_penalty_sweep(cr_handle *h, int32_t k, double *avg_seconds);
+
+/* ---- general-K partition: P-APG(ALCC) ------------- */
+/* make_partition (dataset.cpp:119-130) + DualDecomposition (papg.cpp:66-86):
+   K blocks of nbar = N/K consecutive points (N % K == 0, nbar >= n+1); every
+   block QP is solved by the ALCC (alcc_solve_block, alcc.cpp:222-258) with
+   the inner config, warm-started from the previous block minimiser; the block
+   balls use the feasible affine point (feas_y: N shifted frame, feas_xi: N*n).
+   K == N (or 0) selects the singleton closed form. Call before cr_papg_begin;
+   unsharded handles only. theta / C eta then use the general cross ordering
+   (indexing.hpp:9-37), N(N-nbar) + N entries. */
+cr_status cr_set_partition(cr_handle *h, int64_t K, const double *feas_y, const double *feas_xi,
+                           const cr_alcc_config *inner);
+/* MAPG iterations and seconds spent in block solves since cr_papg_begin, the
+   within-block sigma(A1) and the per-block sigma(A2) (K entries, may be NULL). */
+cr_status cr_partition_stats(const cr_handle *h, int64_t *inner_iters, double *inner_seconds,
+                             double *sigma_A1, double *sigma_A2);
 
 /* ---- host utilities (no device) ----------------------------------------- */
 /* kinds: 0 quadratic, 1 exponential, 2 affine-noiseless, 3 custom-1d

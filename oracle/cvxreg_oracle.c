@@ -919,13 +919,13 @@ static void project_ball_c(double *v, const double *center, int64_t len, double 
   }
 }
 
-/* PenaltyOracle::eval (alcc.cpp:33-47), standalone centres (ybar, 0) */
+/* PenaltyOracle::eval (alcc.cpp:33-47) over a row set with centres (cy, cxi) */
 typedef struct {
   rows_ctx *rows;
-  const double *cy;
-  const double *theta; /* m */
+  const double *cy, *cxi; /* cxi NULL: 0 */
+  const double *theta;    /* m */
   double mu, gamma;
-  int64_t N, n;
+  int64_t N, n;           /* points of the row set */
   double *res, *vneg, *ay, *axi; /* scratch */
 } pen_ctx;
 
@@ -940,39 +940,34 @@ static void penalty_grad(pen_ctx *p, const double *y, const double *xi, double *
   rows_adjoint(p->rows, p->vneg, p->ay, p->axi);
   for (int64_t i = 0; i < p->N; ++i) gy[i] = (y[i] - p->cy[i]) / p->mu - p->ay[i];
   const double gm = p->gamma / p->mu;
-  for (int64_t i = 0; i < p->N * p->n; ++i) gxi[i] = gm * xi[i] - p->axi[i];
+  for (int64_t i = 0; i < p->N * p->n; ++i)
+    gxi[i] = gm * (xi[i] - (p->cxi ? p->cxi[i] : 0.0)) - p->axi[i];
 }
 
-int cro_alcc(const double *X, const double *ys, int64_t N, int64_t n, double gamma,
-             double Bbar_y, double Bbar_xi, double sigma_A1, double sigma_A2,
-             const double *warm_y, const double *warm_xi, const cro_alcc_config *cfg,
-             cro_alcc_result *res) {
+/* alcc_core (alcc.cpp:54-191) on the within rows of the nb points Xb (the
+   standalone FullRows set is the single block of all N points). target > 0:
+   block stop rule (alcc.cpp:153-155), else the standalone thresholds. */
+static int alcc_core_c(const double *Xb, int64_t N, int64_t n, const double *cy,
+                       const double *cxi, double gamma, double Bbar_y, double Bbar_xi,
+                       double sigma_A1, double sigma_A2, const cro_alcc_config *cfg,
+                       double target, const double *warm_y, const double *warm_xi,
+                       cro_alcc_result *res) {
   const double start = now_seconds();
-  if (N < 2 || n < 1 || !(gamma > 0)) return -1;
   if (!(cfg->c > 1) || !(cfg->kappa > 0) || !(cfg->mu1 > 0)) return -1; /* alcc.cpp:59-61 */
   const int threads = cfg->threads > 1 ? cfg->threads : 1;
   const int64_t m = N * (N - 1);
   const int64_t Nn = N * n;
-  if (!(sigma_A1 > 0)) {
-    int it, cv;
-    if (cro_sigma_A(X, N, n, 1, 1e-6, 5000, &sigma_A1, &it, &cv)) return -2;
-  }
-  if (!(sigma_A2 > 0)) {
-    int it, cv;
-    if (cro_sigma_A(X, N, n, 2, 1e-6, 5000, &sigma_A2, &it, &cv)) return -2;
-  }
-  res->sigma_A1 = sigma_A1;
-  res->sigma_A2 = sigma_A2;
-
-  rows_ctx rc = {X, N, n, threads, (double *)malloc(sizeof(double) * (size_t)(m + N)),
+  rows_ctx rc = {Xb, N, n, threads, (double *)malloc(sizeof(double) * (size_t)(m + N)),
                  (double *)malloc(sizeof(double) * (size_t)(m + N))};
-  double *theta = (double *)calloc((size_t)m, sizeof(double));
-  double *res_v = (double *)malloc(sizeof(double) * (size_t)m);
-  double *vneg = (double *)malloc(sizeof(double) * (size_t)m);
-  double *work = (double *)malloc(sizeof(double) * (size_t)m);
-  /* point buffers: y, xi, y1, y1_prev, y2, xi1, xi1_prev, xi2, gy, gxi, ay, axi */
+  double *theta = (double *)calloc((size_t)(m > 0 ? m : 1), sizeof(double));
+  double *res_v = (double *)malloc(sizeof(double) * (size_t)(m > 0 ? m : 1));
+  double *vneg = (double *)malloc(sizeof(double) * (size_t)(m > 0 ? m : 1));
+  double *work = (double *)malloc(sizeof(double) * (size_t)(m > 0 ? m : 1));
+  double *rows_center = (double *)malloc(sizeof(double) * (size_t)(m > 0 ? m : 1));
+  /* point buffers: y, y1, y1_prev, y2, gy, ay | xi, xi1, xi1_prev, xi2, gxi, axi */
   double *pb = (double *)malloc(sizeof(double) * (size_t)(6 * N + 6 * Nn));
-  if (!rc.rowbuf || !rc.zbuf || !theta || !res_v || !vneg || !work || !pb) return -3;
+  if (!rc.rowbuf || !rc.zbuf || !theta || !res_v || !vneg || !work || !rows_center || !pb)
+    return -3;
   double *y = pb, *y1 = pb + N, *y1p = pb + 2 * N, *y2 = pb + 3 * N, *gy = pb + 4 * N,
          *ay = pb + 5 * N;
   double *xi = pb + 6 * N, *xi1 = xi + Nn, *xi1p = xi + 2 * Nn, *xi2 = xi + 3 * Nn,
@@ -981,33 +976,38 @@ int cro_alcc(const double *X, const double *ys, int64_t N, int64_t n, double gam
   double mu = cfg->mu1;
   memcpy(y, warm_y, sizeof(double) * (size_t)N); /* alcc.cpp:68-69 */
   memcpy(xi, warm_xi, sizeof(double) * (size_t)Nn);
-  project_ball_c(y, ys, N, Bbar_y);
-  project_ball_c(xi, NULL, Nn, Bbar_xi);
+  project_ball_c(y, cy, N, Bbar_y);
+  project_ball_c(xi, cxi, Nn, Bbar_xi);
 
-  pen_ctx pen = {&rc, ys, theta, mu, gamma, N, n, work, vneg, ay, axi};
+  pen_ctx pen = {&rc, cy, cxi, theta, mu, gamma, N, n, work, vneg, ay, axi};
   double tau, alpha_y, alpha_xi;
+  int rcode = 0;
   { /* alcc.cpp:75-84: P_1 at the start point */
     penalty_grad(&pen, y, xi, gy, gxi);
     double sy = 0, sx = 0, sv = 0;
-    for (int64_t i = 0; i < N; ++i) sy += (y[i] - ys[i]) * (y[i] - ys[i]);
-    for (int64_t i = 0; i < Nn; ++i) sx += xi[i] * xi[i];
+    for (int64_t i = 0; i < N; ++i) sy += (y[i] - cy[i]) * (y[i] - cy[i]);
+    for (int64_t i = 0; i < Nn; ++i) {
+      const double d = xi[i] - (cxi ? cxi[i] : 0.0);
+      sx += d * d;
+    }
     for (int64_t i = 0; i < m; ++i) sv += vneg[i] * vneg[i];
     const double p1 = sy / (2.0 * mu) + gamma * sx / (2.0 * mu) + 0.5 * sv;
-    if (!isfinite(p1)) return -4;
+    if (!isfinite(p1)) { rcode = -4; goto out; }
     tau = cfg->tau1_scale * p1;
     if (tau < 1e-16) tau = 1e-16;
     alpha_y = alpha_xi = cfg->alpha1_scale * (Bbar_y + Bbar_xi);
   }
-  /* rows_center = R(ybar, 0): needed only through lambda . rows_center */
-  double *rows_center = (double *)malloc(sizeof(double) * (size_t)m);
-  memset(gxi, 0, sizeof(double) * (size_t)Nn);
-  rows_forward(&rc, ys, gxi, rows_center);
+  if (cxi) {
+    rows_forward(&rc, cy, cxi, rows_center);
+  } else {
+    memset(gxi, 0, sizeof(double) * (size_t)Nn);
+    rows_forward(&rc, cy, gxi, rows_center);
+  }
 
   res->reason = CRO_ITER_BUDGET;
   res->mapg_iters_total = 0;
   res->outer_iters = 0;
   res->hit_cap_any = 0;
-  int rcode = 0;
   for (int64_t k = 1; k <= cfg->max_outer; ++k) {
     const double L_y = 1.0 / mu + sigma_A1 * sigma_A1; /* :101-102 */
     const double L_xi = gamma / mu + sigma_A2 * sigma_A2;
@@ -1032,10 +1032,10 @@ int cro_alcc(const double *X, const double *ys, int64_t N, int64_t n, double gam
       for (int64_t i = 0; i < Nn; ++i) if (!isfinite(gxi[i])) { rcode = -5; goto out; }
       { double *tmp = y1p; y1p = y1; y1 = tmp; }
       for (int64_t i = 0; i < N; ++i) y1[i] = y2[i] - gy[i] / L_y;
-      project_ball_c(y1, ys, N, Bbar_y);
+      project_ball_c(y1, cy, N, Bbar_y);
       { double *tmp = xi1p; xi1p = xi1; xi1 = tmp; }
       for (int64_t i = 0; i < Nn; ++i) xi1[i] = xi2[i] - gxi[i] / L_xi;
-      project_ball_c(xi1, NULL, Nn, Bbar_xi);
+      project_ball_c(xi1, cxi, Nn, Bbar_xi);
       inner = ell;
       double dy = 0, dx = 0;
       for (int64_t i = 0; i < N; ++i) dy += (y1[i] - y2[i]) * (y1[i] - y2[i]);
@@ -1056,7 +1056,7 @@ int cro_alcc(const double *X, const double *ys, int64_t N, int64_t n, double gam
 
     /* :124-160 */
     rows_forward(&rc, y, xi, res_v);
-    double nn = 0, gap_raw = 0, lc = 0;
+    double nn = 0, gap_raw = 0, lc = 0, ll = 0;
     for (int64_t i = 0; i < m; ++i) {
       const double d = theta[i] - res_v[i];
       vneg[i] = d > 0.0 ? d : 0.0;
@@ -1066,20 +1066,25 @@ int cro_alcc(const double *X, const double *ys, int64_t N, int64_t n, double gam
       nn += neg * neg;
       gap_raw += lam * res_v[i];
       lc += lam * rows_center[i];
+      ll += lam * lam;
     }
     const double infeas_raw = sqrt(nn);
     rows_adjoint(&rc, work, ay, axi);
     const double dual_value = -0.5 * dot(ay, ay, N) - dot(axi, axi, Nn) / (2.0 * gamma) - lc;
     double sy = 0, sx = 0;
-    for (int64_t i = 0; i < N; ++i) sy += (y[i] - ys[i]) * (y[i] - ys[i]);
-    for (int64_t i = 0; i < Nn; ++i) sx += xi[i] * xi[i];
+    for (int64_t i = 0; i < N; ++i) sy += (y[i] - cy[i]) * (y[i] - cy[i]);
+    for (int64_t i = 0; i < Nn; ++i) {
+      const double d = xi[i] - (cxi ? cxi[i] : 0.0);
+      sx += d * d;
+    }
     const double primal_value = 0.5 * sy + 0.5 * gamma * sx;
-    res->certified_gap = primal_value - dual_value;
+    const double certified = primal_value - dual_value;
+    res->certified_gap = certified;
     res->infeas_raw = infeas_raw;
     res->gap_raw = gap_raw;
     res->outer_iters = k;
-    const double infeas_norm = infeas_raw / sqrt((double)m);
-    const double gap_norm = gap_raw / (double)m;
+    const double infeas_norm = m > 0 ? infeas_raw / sqrt((double)m) : 0.0;
+    const double gap_norm = m > 0 ? gap_raw / (double)m : 0.0;
     if (cfg->record_history && res->history) {
       double *h = res->history + (k - 1) * 8;
       h[0] = (double)k;
@@ -1092,7 +1097,10 @@ int cro_alcc(const double *X, const double *ys, int64_t N, int64_t n, double gam
       h[7] = now_seconds() - start;
     }
     if (res->multiplier) memcpy(res->multiplier, work, sizeof(double) * (size_t)m);
-    if (infeas_norm <= cfg->infeas_norm_tol && fabs(gap_norm) <= cfg->gap_norm_tol) {
+    int stop;
+    if (target > 0) stop = certified <= target && sqrt(ll) * infeas_raw <= target;
+    else stop = infeas_norm <= cfg->infeas_norm_tol && fabs(gap_norm) <= cfg->gap_norm_tol;
+    if (stop) {
       res->reason = CRO_THRESHOLDS;
       break;
     }
@@ -1112,7 +1120,7 @@ out:
     if (res->y) memcpy(res->y, y, sizeof(double) * (size_t)N);
     if (res->xi) memcpy(res->xi, xi, sizeof(double) * (size_t)Nn);
     double sy = 0;
-    for (int64_t i = 0; i < N; ++i) sy += (y[i] - ys[i]) * (y[i] - ys[i]);
+    for (int64_t i = 0; i < N; ++i) sy += (y[i] - cy[i]) * (y[i] - cy[i]);
     res->objective = 0.5 * sy;
   } else {
     res->reason = CRO_ERROR;
@@ -1121,4 +1129,380 @@ out:
   free(rc.rowbuf); free(rc.zbuf); free(theta); free(res_v); free(vneg); free(work); free(pb);
   free(rows_center);
   return rcode;
+}
+
+int cro_alcc(const double *X, const double *ys, int64_t N, int64_t n, double gamma,
+             double Bbar_y, double Bbar_xi, double sigma_A1, double sigma_A2,
+             const double *warm_y, const double *warm_xi, const cro_alcc_config *cfg,
+             cro_alcc_result *res) {
+  if (N < 2 || n < 1 || !(gamma > 0)) return -1;
+  if (!(cfg->c > 1) || !(cfg->kappa > 0) || !(cfg->mu1 > 0)) return -1;
+  if (!(sigma_A1 > 0)) {
+    int it, cv;
+    if (cro_sigma_A(X, N, n, 1, 1e-6, 5000, &sigma_A1, &it, &cv)) return -2;
+  }
+  if (!(sigma_A2 > 0)) {
+    int it, cv;
+    if (cro_sigma_A(X, N, n, 2, 1e-6, 5000, &sigma_A2, &it, &cv)) return -2;
+  }
+  res->sigma_A1 = sigma_A1;
+  res->sigma_A2 = sigma_A2;
+  /* alcc_solve (alcc.cpp:193-208): FullRows, centres (ybar, 0) */
+  return alcc_core_c(X, N, n, ys, NULL, gamma, Bbar_y, Bbar_xi, sigma_A1, sigma_A2, cfg, 0.0,
+                     warm_y, warm_xi, res);
+}
+
+/* ============================================ general-K P-APG(ALCC) (f2) */
+/* operators.cpp:128-153 with K blocks of nbar points: cross rows ordered by
+   block pair (i, j), i != j, then (l1, l2) lexicographic (indexing.hpp:9-37). */
+void cro_apply_C_k(const double *X, int64_t N, int64_t n, int64_t K, const double *y,
+                   const double *xi, double *out) {
+  const int64_t nbar = N / K;
+  int64_t r = 0;
+  for (int64_t i = 0; i < K; ++i)
+    for (int64_t j = 0; j < K; ++j) {
+      if (i == j) continue;
+      for (int64_t l1 = i * nbar; l1 < (i + 1) * nbar; ++l1) {
+        const double y1 = y[l1];
+        const double *x1 = X + l1 * n;
+        for (int64_t l2 = j * nbar; l2 < (j + 1) * nbar; ++l2) {
+          double acc = y1 - y[l2];
+          const double *xi2 = xi + l2 * n;
+          const double *x2 = X + l2 * n;
+          for (int64_t jj = 0; jj < n; ++jj) acc -= xi2[jj] * (x1[jj] - x2[jj]);
+          out[r++] = acc;
+        }
+      }
+    }
+  for (int64_t l = 0; l < N; ++l) out[r + l] = y[l];
+}
+
+/* operators.cpp:155-180 */
+void cro_apply_C_T_k(const double *X, int64_t N, int64_t n, int64_t K, const double *theta,
+                     double *out_y, double *out_xi) {
+  const int64_t nbar = N / K;
+  const int64_t rows_cross = N * (N - nbar);
+  for (int64_t l = 0; l < N; ++l) out_y[l] = theta[rows_cross + l];
+  memset(out_xi, 0, sizeof(double) * (size_t)(N * n));
+  int64_t r = 0;
+  for (int64_t i = 0; i < K; ++i)
+    for (int64_t j = 0; j < K; ++j) {
+      if (i == j) continue;
+      for (int64_t l1 = i * nbar; l1 < (i + 1) * nbar; ++l1) {
+        const double *x1 = X + l1 * n;
+        for (int64_t l2 = j * nbar; l2 < (j + 1) * nbar; ++l2) {
+          const double tr = theta[r++];
+          out_y[l1] += tr;
+          out_y[l2] -= tr;
+          double *o2 = out_xi + l2 * n;
+          const double *x2 = X + l2 * n;
+          for (int64_t jj = 0; jj < n; ++jj) o2[jj] -= tr * (x1[jj] - x2[jj]);
+        }
+      }
+    }
+}
+
+/* operators.cpp:302-339 on op_C (:353-369) with K blocks */
+int cro_sigma_C_k(const double *X, int64_t N, int64_t n, int64_t K, double tol, int max_iters,
+                  double *sigma, int *iters, int *converged) {
+  if (K == N) return cro_sigma_C(X, N, n, tol, max_iters, sigma, iters, converged);
+  const int64_t nbar = N / K;
+  const int64_t cols = N * (n + 1);
+  const int64_t rows = N * (N - nbar) + N;
+  double *v = (double *)malloc(sizeof(double) * (size_t)cols);
+  double *u = (double *)malloc(sizeof(double) * (size_t)cols);
+  double *w = (double *)malloc(sizeof(double) * (size_t)rows);
+  if (!v || !u || !w) { free(v); free(u); free(w); return -1; }
+  xo256 g = rng_stream(0x5eedULL, 97);
+  for (int64_t k = 0; k < cols; ++k) v[k] = xo_normal(&g);
+  const double nv = sqrt(dot(v, v, cols));
+  for (int64_t k = 0; k < cols; ++k) v[k] /= nv;
+  double lambda_prev = 0;
+  *converged = 1;
+  *iters = 0;
+  for (int it = 1; it <= max_iters; ++it) {
+    cro_apply_C_k(X, N, n, K, v, v + N, w);
+    const double lambda = dot(w, w, rows);
+    cro_apply_C_T_k(X, N, n, K, w, u, u + N);
+    const double norm_u = sqrt(dot(u, u, cols));
+    if (norm_u == 0 || lambda == 0) {
+      *sigma = 0;
+      *iters = it;
+      free(v); free(u); free(w);
+      return 0;
+    }
+    for (int64_t k = 0; k < cols; ++k) v[k] = u[k] / norm_u;
+    *iters = it;
+    if (it > 1 && fabs(lambda - lambda_prev) <= tol * lambda) {
+      *sigma = sqrt(lambda) * 1.01;
+      free(v); free(u); free(w);
+      return 0;
+    }
+    lambda_prev = lambda;
+  }
+  *sigma = sqrt(lambda_prev) * 1.10;
+  *converged = 0;
+  free(v); free(u); free(w);
+  return 0;
+}
+
+typedef struct {
+  const double *X, *ys, *feas_y, *feas_xi;
+  int64_t N, n, K, nbar;
+  double gamma;
+  int threads;
+  const cro_alcc_config *inner;
+  double sigma_A1, *sigma_A2;   /* estimate_block_sigmas (alcc.cpp:208-220) */
+  double *warm_y, *warm_xi;     /* per-block warm starts (papg.cpp:74-86) */
+  double *q_y, *q_xi, *ey, *exi;
+  double *blk_obj, *blk_inf2;
+  int64_t *blk_iters;
+  int err;
+} dgk_ctx;
+
+/* alcc_solve_block (alcc.cpp:222-258) */
+static void solve_block(dgk_ctx *c, int64_t i, double tol) {
+  const int64_t nb = c->nbar, n = c->n, base = i * nb;
+  const double gamma = c->gamma;
+  double *cy = (double *)malloc(sizeof(double) * (size_t)nb);
+  double *cxi = (double *)malloc(sizeof(double) * (size_t)(nb * n));
+  for (int64_t a = 0; a < nb; ++a) cy[a] = c->ys[base + a] + c->q_y[base + a];
+  for (int64_t a = 0; a < nb * n; ++a) cxi[a] = c->q_xi[base * n + a] / gamma;
+  double sy = 0, sx = 0;
+  for (int64_t a = 0; a < nb; ++a) {
+    const double d = c->feas_y[base + a] - cy[a];
+    sy += d * d;
+  }
+  for (int64_t a = 0; a < nb * n; ++a) {
+    const double d = c->feas_xi[base * n + a] - cxi[a];
+    sx += d * d;
+  }
+  const double Bsq = sy + gamma * sx;
+  double Bbar = sqrt(Bsq);
+  if (Bbar < 1e-8) Bbar = 1e-8;
+  cro_alcc_result r;
+  memset(&r, 0, sizeof(r));
+  r.y = c->ey + base;
+  r.xi = c->exi + base * n;
+  const int rc = alcc_core_c(c->X + base * n, nb, n, cy, cxi, gamma, Bbar, Bbar / sqrt(gamma),
+                             c->sigma_A1, c->sigma_A2[i], c->inner, tol, c->warm_y + base,
+                             c->warm_xi + base * n, &r);
+  if (rc != 0) c->err = rc;
+  /* block objective (alcc.cpp:254-256) */
+  double o1 = 0, o2 = 0, o3 = 0, o4 = 0;
+  for (int64_t a = 0; a < nb; ++a) {
+    const double d = r.y[a] - c->ys[base + a];
+    o1 += d * d;
+    o3 += c->q_y[base + a] * r.y[a];
+  }
+  for (int64_t a = 0; a < nb * n; ++a) {
+    o2 += r.xi[a] * r.xi[a];
+    o4 += c->q_xi[base * n + a] * r.xi[a];
+  }
+  c->blk_obj[i] = 0.5 * o1 + 0.5 * gamma * o2 - o3 - o4;
+  c->blk_inf2[i] = r.infeas_raw * r.infeas_raw;
+  c->blk_iters[i] = r.mapg_iters_total;
+  memcpy(c->warm_y + base, r.y, sizeof(double) * (size_t)nb);
+  memcpy(c->warm_xi + base * n, r.xi, sizeof(double) * (size_t)(nb * n));
+  free(cy);
+  free(cxi);
+}
+
+/* DualDecomposition::dual_gradient (papg.cpp:89-132) */
+static double dual_gradient_k(dgk_ctx *c, const double *theta, double tol, double *C_eta,
+                              double *within, int64_t *inner_iters) {
+  cro_apply_C_T_k(c->X, c->N, c->n, c->K, theta, c->q_y, c->q_xi);
+  if (c->threads > 1) {
+#pragma omp parallel for schedule(dynamic, 1) num_threads(c->threads)
+    for (int64_t i = 0; i < c->K; ++i) solve_block(c, i, tol);
+  } else {
+    for (int64_t i = 0; i < c->K; ++i) solve_block(c, i, tol);
+  }
+  double g = 0, inf2 = 0;
+  int64_t it = 0;
+  for (int64_t i = 0; i < c->K; ++i) { /* gather in block order */
+    g += c->blk_obj[i];
+    inf2 += c->blk_inf2[i];
+    it += c->blk_iters[i];
+  }
+  *within = sqrt(inf2);
+  if (inner_iters) *inner_iters = it;
+  cro_apply_C_k(c->X, c->N, c->n, c->K, c->ey, c->exi, C_eta);
+  return g;
+}
+
+int cro_papg_k(const double *X, const double *ys, int64_t N, int64_t n, int64_t K,
+               const cro_config *cfg, const cro_alcc_config *inner, const double *feas_y,
+               const double *feas_xi, const double *theta0, cro_result *res,
+               int64_t *inner_iters_out) {
+  const double start = now_seconds();
+  if (N < 2 || n < 1 || cfg->gamma <= 0 || K < 1 || N % K != 0) return -1;
+  const int64_t nbar = N / K;
+  if (nbar < n + 1) return -1; /* dataset.cpp:127-128 */
+  const int threads = cfg->threads > 1 ? cfg->threads : 1;
+  const int64_t rows_total = N * (N - 1);
+  const int64_t rows_cross = N * (N - nbar);
+  const int64_t dim = rows_cross + N;
+  const double infeas_div = sqrt((double)rows_total);
+  const double gap_div = (double)rows_total;
+
+  dgk_ctx c;
+  memset(&c, 0, sizeof(c));
+  c.X = X; c.ys = ys; c.feas_y = feas_y; c.feas_xi = feas_xi;
+  c.N = N; c.n = n; c.K = K; c.nbar = nbar; c.gamma = cfg->gamma; c.threads = threads;
+  c.inner = inner;
+  c.sigma_A2 = (double *)malloc(sizeof(double) * (size_t)K);
+  { /* estimate_block_sigmas (alcc.cpp:206-220) */
+    int it, cv;
+    if (cro_sigma_A(X, nbar, n, 1, 1e-6, 5000, &c.sigma_A1, &it, &cv)) return -2;
+    for (int64_t i = 0; i < K; ++i)
+      if (cro_sigma_A(X + i * nbar * n, nbar, n, 2, 1e-6, 5000, &c.sigma_A2[i], &it, &cv))
+        return -2;
+  }
+  double sigma_C = cfg->sigma_C;
+  res->sigma_iters = 0;
+  res->sigma_converged = 1;
+  if (!(sigma_C > 0)) {
+    int it = 0, conv = 0;
+    if (cro_sigma_C_k(X, N, n, K, 1e-6, 5000, &sigma_C, &it, &conv)) return -2;
+    res->sigma_iters = it;
+    res->sigma_converged = conv;
+  }
+  const double L_g = sigma_C * sigma_C / cfg->gamma;
+  double B_theta = cfg->B_theta > 0 ? cfg->B_theta : 10.0 * sqrt((double)N);
+  res->sigma_C = sigma_C;
+  res->L_g = L_g;
+  res->reason = CRO_ITER_BUDGET;
+
+  c.warm_y = (double *)malloc(sizeof(double) * (size_t)N);
+  c.warm_xi = (double *)malloc(sizeof(double) * (size_t)(N * n));
+  memcpy(c.warm_y, feas_y, sizeof(double) * (size_t)N);
+  memcpy(c.warm_xi, feas_xi, sizeof(double) * (size_t)(N * n));
+  c.q_y = (double *)malloc(sizeof(double) * (size_t)N);
+  c.q_xi = (double *)malloc(sizeof(double) * (size_t)(N * n));
+  c.ey = (double *)malloc(sizeof(double) * (size_t)N);
+  c.exi = (double *)malloc(sizeof(double) * (size_t)(N * n));
+  c.blk_obj = (double *)malloc(sizeof(double) * (size_t)K);
+  c.blk_inf2 = (double *)malloc(sizeof(double) * (size_t)K);
+  c.blk_iters = (int64_t *)malloc(sizeof(int64_t) * (size_t)K);
+
+  double *theta1 = (double *)calloc((size_t)dim, sizeof(double));
+  double *theta1_prev = (double *)malloc(sizeof(double) * (size_t)dim);
+  double *theta2 = (double *)malloc(sizeof(double) * (size_t)dim);
+  double *C_eta = (double *)malloc(sizeof(double) * (size_t)dim);
+  if (theta0) {
+    memcpy(theta1, theta0, sizeof(double) * (size_t)dim);
+    cro_project_nonneg_ball(theta1, dim, B_theta);
+  }
+  memcpy(theta1_prev, theta1, sizeof(double) * (size_t)dim);
+  memcpy(theta2, theta1, sizeof(double) * (size_t)dim);
+  double t = 1.0, g_star_upper = INFINITY;
+  int64_t ell = 0, inner_total = 0;
+  int restarts = 0, rc = 0;
+  while (1) {
+    ++ell;
+    const double inv3 = 1.0 / ((double)ell * (double)ell * (double)ell);
+    const double inner_tol = cfg->inner_tol_floor < inv3 ? cfg->inner_tol_floor : inv3;
+    double within = 0;
+    int64_t it = 0;
+    const double g_value = dual_gradient_k(&c, theta2, inner_tol, C_eta, &within, &it);
+    inner_total += it;
+    if (c.err) { rc = c.err; res->reason = CRO_ERROR; break; }
+    int finite = 1;
+    for (int64_t i = 0; i < dim; ++i) if (!isfinite(C_eta[i])) { finite = 0; break; }
+    if (!finite) { res->reason = CRO_ERROR; rc = -4; break; }
+    { double *tmp = theta1_prev; theta1_prev = theta1; theta1 = tmp; }
+    for (int64_t i = 0; i < dim; ++i) theta1[i] = theta2[i] - C_eta[i] / L_g;
+    cro_project_nonneg_ball(theta1, dim, B_theta);
+    double cross_sq = 0, all_sq = 0;
+    for (int64_t i = 0; i < dim; ++i) {
+      const double m = -C_eta[i] > 0.0 ? -C_eta[i] : 0.0;
+      if (i < rows_cross) cross_sq += m * m;
+      all_sq += m * m;
+    }
+    const double cross_infeas = rows_cross > 0 ? sqrt(cross_sq) : 0.0;
+    const double t2c = dot(theta2, C_eta, dim);
+    const double fw = B_theta * sqrt(all_sq) + t2c;
+    const double cushion = 2.0 * inner_tol * (double)K;
+    const double cand = g_value + fw + cushion;
+    if (cand < g_star_upper) g_star_upper = cand;
+    const double gap_raw = cfg->use_momentum ? dot(theta1, C_eta, dim) : t2c;
+    const double infeas_raw = sqrt(within * within + cross_infeas * cross_infeas);
+    const double gap_norm = gap_raw / gap_div;
+    const double infeas_norm = infeas_raw / infeas_div;
+    if (cfg->record_history && res->history) {
+      double obj = 0, xx = 0;
+      for (int64_t i = 0; i < N; ++i) { const double d = c.ey[i] - ys[i]; obj += d * d; }
+      for (int64_t i = 0; i < N * n; ++i) xx += c.exi[i] * c.exi[i];
+      double *h = res->history + (ell - 1) * 8;
+      h[0] = (double)ell;
+      h[1] = 0.5 * obj;
+      h[2] = 0.5 * obj + 0.5 * cfg->gamma * xx;
+      h[3] = infeas_raw;
+      h[4] = infeas_norm;
+      h[5] = gap_raw;
+      h[6] = gap_norm;
+      h[7] = now_seconds() - start;
+    }
+    res->iters = ell;
+    int stop = 0;
+    if (fabs(gap_norm) <= cfg->gap_norm_tol && infeas_norm <= cfg->infeas_norm_tol) {
+      res->reason = CRO_THRESHOLDS;
+      stop = 1;
+    } else if (ell >= cfg->max_iters) {
+      res->reason = CRO_ITER_BUDGET;
+      stop = 1;
+    } else if (now_seconds() - start > cfg->max_seconds) {
+      res->reason = CRO_TIME_BUDGET;
+      stop = 1;
+    }
+    if (stop) {
+      const double n1 = sqrt(dot(theta1, theta1, dim));
+      const int saturated = n1 > 0.99 * B_theta;
+      if (saturated && cfg->adaptive_B_theta && res->reason == CRO_THRESHOLDS &&
+          restarts < cfg->max_restarts) {
+        B_theta *= 2.0;
+        ++restarts;
+        memcpy(theta2, theta1, sizeof(double) * (size_t)dim);
+        memcpy(theta1_prev, theta1, sizeof(double) * (size_t)dim);
+        t = 1.0;
+        g_star_upper = INFINITY;
+        continue;
+      }
+      res->saturated = saturated;
+      break;
+    }
+    if (cfg->use_momentum) {
+      const double t_next = cro_momentum_next(t);
+      const double beta = (t - 1.0) / t_next;
+      for (int64_t i = 0; i < dim; ++i) theta2[i] = theta1[i] + beta * (theta1[i] - theta1_prev[i]);
+      t = t_next;
+    } else {
+      memcpy(theta2, theta1, sizeof(double) * (size_t)dim);
+    }
+  }
+  if (rc == 0) {
+    if (res->c_eta) memcpy(res->c_eta, C_eta, sizeof(double) * (size_t)dim);
+    double ft = 1.0 / pow((double)ell, 3.0);
+    if (cfg->inner_tol_floor < ft) ft = cfg->inner_tol_floor;
+    if (cfg->final_resolve_tol < ft) ft = cfg->final_resolve_tol;
+    double within = 0;
+    int64_t it = 0;
+    const double g_final = dual_gradient_k(&c, theta1, ft, C_eta, &within, &it);
+    inner_total += it;
+    res->g_final = g_final;
+    const double d = g_star_upper - (g_final - 2.0 * ft * (double)K);
+    res->delta_estimate = d > 0 ? d : 0.0;
+    if (res->y) memcpy(res->y, c.ey, sizeof(double) * (size_t)N);
+    if (res->xi) memcpy(res->xi, c.exi, sizeof(double) * (size_t)(N * n));
+    if (res->theta) memcpy(res->theta, theta1, sizeof(double) * (size_t)dim);
+    res->B_theta = B_theta;
+    res->restarts = restarts;
+  }
+  if (inner_iters_out) *inner_iters_out = inner_total;
+  res->wall_seconds = now_seconds() - start;
+  free(theta1); free(theta1_prev); free(theta2); free(C_eta);
+  free(c.q_y); free(c.q_xi); free(c.ey); free(c.exi); free(c.warm_y); free(c.warm_xi);
+  free(c.blk_obj); free(c.blk_inf2); free(c.blk_iters); free(c.sigma_A2);
+  return rc;
 }

@@ -152,6 +152,21 @@ int cro_alcc(const double *X, const double *ys, int64_t N, int64_t n, double gam
              const double *warm_y, const double *warm_xi, const cro_alcc_config *cfg,
              cro_alcc_result *res);
 
+/* ---- general-K P-APG(ALCC) (papg.cpp:66-283 with alcc_solve_block; 8f row f2) ---- */
+void cro_apply_C_k(const double *X, int64_t N, int64_t n, int64_t K, const double *y,
+                   const double *xi, double *out /* N(N-nbar)+N */);
+void cro_apply_C_T_k(const double *X, int64_t N, int64_t n, int64_t K, const double *theta,
+                     double *out_y, double *out_xi);
+int cro_sigma_C_k(const double *X, int64_t N, int64_t n, int64_t K, double tol, int max_iters,
+                  double *sigma, int *iters, int *converged);
+/* cfg: the dual loop (cfg->threads > 1: blocks in parallel, deterministic);
+   inner: PapgConfig::inner; feas_*: prepare_problem's feasible point (block
+   balls and first warm starts). theta/c_eta in res have N(N-nbar)+N entries. */
+int cro_papg_k(const double *X, const double *ys, int64_t N, int64_t n, int64_t K,
+               const cro_config *cfg, const cro_alcc_config *inner, const double *feas_y,
+               const double *feas_xi, const double *theta0, cro_result *res,
+               int64_t *inner_iters_out);
+
 #ifdef __cplusplus
 }
 #endif

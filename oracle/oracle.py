@@ -112,6 +112,14 @@ def lib():
         L.cro_sigma_A.argtypes = [_P, i64, i64, i32, d, i32, _P, C.POINTER(i32), C.POINTER(i32)]
         L.cro_alcc.argtypes = [_P, _P, i64, i64, d, d, d, d, d, _P, _P,
                                C.POINTER(CroAlccConfig), C.POINTER(CroAlccResult)]
+        L.cro_apply_C_k.argtypes = [_P, i64, i64, i64, _P, _P, _P]
+        L.cro_apply_C_k.restype = None
+        L.cro_apply_C_T_k.argtypes = [_P, i64, i64, i64, _P, _P, _P]
+        L.cro_apply_C_T_k.restype = None
+        L.cro_sigma_C_k.argtypes = [_P, i64, i64, i64, d, i32, _P, C.POINTER(i32), C.POINTER(i32)]
+        L.cro_papg_k.argtypes = [_P, _P, i64, i64, i64, C.POINTER(CroConfig),
+                                 C.POINTER(CroAlccConfig), _P, _P, _P, C.POINTER(CroResult),
+                                 C.POINTER(C.c_int64)]
         L.cro_cross_position.argtypes = [i64, i64, i64, i64]
         L.cro_cross_position.restype = i64
         _lib = L
@@ -370,3 +378,81 @@ def alcc(X, ys, *, gamma, Bbar_y, Bbar_xi, warm_y, warm_xi, sigma_A1=0.0, sigma_
                       REASONS[res.reason], bool(res.hit_cap_any), res.certified_gap,
                       res.infeas_raw, res.gap_raw, res.objective, res.wall_seconds,
                       res.sigma_A1, res.sigma_A2)
+
+
+def apply_C_k(X, K, y, xi):
+    X = _c(X)
+    N, n = X.shape
+    out = np.empty(N * (N - N // K) + N)
+    lib().cro_apply_C_k(_p(X), N, n, K, _p(_c(y)), _p(_c(xi).reshape(-1)), _p(out))
+    return out
+
+
+def apply_C_T_k(X, K, theta):
+    X = _c(X)
+    N, n = X.shape
+    oy = np.empty(N)
+    oxi = np.empty(N * n)
+    lib().cro_apply_C_T_k(_p(X), N, n, K, _p(_c(theta)), _p(oy), _p(oxi))
+    return oy, oxi
+
+
+def sigma_C_k(X, K, tol=1e-6, max_iters=5000):
+    X = _c(X)
+    s = np.zeros(1)
+    it = C.c_int(0)
+    cv = C.c_int(0)
+    rc = lib().cro_sigma_C_k(_p(X), X.shape[0], X.shape[1], K, tol, max_iters, _p(s),
+                             C.byref(it), C.byref(cv))
+    if rc != 0:
+        raise MemoryError("oracle sigma_C_k failed")
+    return float(s[0]), it.value, bool(cv.value)
+
+
+INNER_DEFAULTS = dict(mu1=1.0, tau1_scale=1e-2, alpha1_scale=1e-3, c=5.0, kappa=0.5,
+                      max_outer=30, mapg_cap=200000, infeas_norm_tol=1e-1, gap_norm_tol=1e-6,
+                      max_seconds=float("inf"), record_history=True)
+
+
+def papg_k(X, ys, K, feas_y, feas_xi, *, inner=None, gamma=1e-3, B_theta=0.0,
+           adaptive_B_theta=True, max_restarts=6, gap_norm_tol=1e-6, infeas_norm_tol=1e-1,
+           max_iters=100000, max_seconds=7200.0, inner_tol_floor=1e-6, final_resolve_tol=1e-10,
+           record_history=True, use_momentum=True, sigma_C=0.0, threads=1, theta0=None,
+           want_c_eta=False):
+    """General-K P-APG(ALCC) (papg.cpp:136-283, dual_gradient :89-132,
+    alcc_solve_block alcc.cpp:222-258)."""
+    X = _c(X)
+    ys = _c(ys)
+    N, n = X.shape
+    nbar = N // K
+    dim = N * (N - nbar) + N
+    cfg = CroConfig(gamma, B_theta, int(adaptive_B_theta), max_restarts, gap_norm_tol,
+                    infeas_norm_tol, max_iters, max_seconds, inner_tol_floor, final_resolve_tol,
+                    int(record_history), int(use_momentum), sigma_C, threads, 0)
+    ic = dict(INNER_DEFAULTS)
+    ic.update(inner or {})
+    icfg = CroAlccConfig(ic["mu1"], ic["tau1_scale"], ic["alpha1_scale"], ic["c"], ic["kappa"],
+                         ic["max_outer"], ic["mapg_cap"], ic["infeas_norm_tol"],
+                         ic["gap_norm_tol"], ic["max_seconds"], int(ic["record_history"]), 1)
+    y = np.empty(N)
+    xi = np.empty(N * n)
+    theta = np.empty(dim)
+    c_eta = np.empty(dim) if want_c_eta else None
+    hist = np.zeros((max_iters if record_history else 0, 8))
+    res = CroResult()
+    res.y, res.xi, res.theta, res.c_eta = _p(y), _p(xi), _p(theta), _p(c_eta)
+    res.history = _p(hist) if record_history else None
+    t0 = None if theta0 is None else _c(theta0)
+    inner_it = C.c_int64(0)
+    rc = lib().cro_papg_k(_p(X), _p(ys), N, n, K, C.byref(cfg), C.byref(icfg), _p(_c(feas_y)),
+                          _p(_c(feas_xi).reshape(-1)), _p(t0), C.byref(res), C.byref(inner_it))
+    if rc == -4:
+        raise RuntimeError("papg: non-finite dual gradient")
+    if rc != 0:
+        raise RuntimeError(f"oracle papg_k failed ({rc})")
+    out = OracleResult(y, xi.reshape(N, n), theta, c_eta, hist[: res.iters], int(res.iters),
+                       REASONS[res.reason], res.restarts, bool(res.saturated), res.g_final,
+                       res.delta_estimate, res.sigma_C, res.L_g, res.B_theta, res.wall_seconds,
+                       res.sigma_iters)
+    out.extra["inner_iters"] = inner_it.value
+    return out

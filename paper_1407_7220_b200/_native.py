@@ -73,6 +73,7 @@ EXPORTS = [
     "cr_duality_gap", "cr_evaluate_estimator", "cr_repair_feasibility",
     "cr_gen_instance", "cr_prepare_problem", "cr_certificate", "cr_momentum_next",
     "cr_sigma_A", "cr_alcc_solve", "cr_alcc_multiplier", "cr_time_penalty_sweep",
+    "cr_set_partition", "cr_partition_stats",
 ]
 
 _lib = None
@@ -131,6 +132,8 @@ def load():
                                C.POINTER(i64), C.POINTER(AlccResultC)]),
         "cr_alcc_multiplier": (st, [vp, i64, i64, _P]),
         "cr_time_penalty_sweep": (st, [vp, i32, _P]),
+        "cr_set_partition": (st, [vp, i64, _P, _P, C.POINTER(AlccConfigC)]),
+        "cr_partition_stats": (st, [vp, C.POINTER(i64), _P, _P, _P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

@@ -60,7 +60,10 @@ constexpr int kSBlock = 1024;  // single-block kernels
 struct AlccArgs {
   AlccDev* d;
   const double* X;
-  const double* cy;     // ybar (ball centre of y; xi centre is 0)
+  const double* cy;     // ball / quadratic centre of y (ybar standalone, ybar_i + q_y per block)
+  const double* cxi;    // centre of xi (nullptr: 0 standalone, q_xi / gamma per block)
+  const double* fy;     // block mode: the feasible affine slice (radius, alcc.cpp:238-243)
+  const double* fxi;
   const double* agg;    // [rowsum N | colagg N (n+1) | scalars]
   double *p1, *p1p, *p2;
   double *rowrec, *colrec;
@@ -112,6 +115,10 @@ __device__ __forceinline__ void records_sum2(const double* part, int count, doub
   out[1] = v[1];
 }
 
+__device__ __forceinline__ double cxi_at(const AlccArgs& a, long long i) {
+  return a.cxi != nullptr ? a.cxi[i] : 0.0;
+}
+
 template <int NN>
 __device__ __forceinline__ void write_records(const AlccArgs& a, long long l, double y,
                                               const double* xi /* NN */) {
@@ -137,7 +144,10 @@ __global__ void __launch_bounds__(kSBlock) project_start_kernel(const AlccArgs a
     const double d = a.p1[l] - a.cy[l];
     v[0] = fma(d, d, v[0]);
   }
-  for (long long i = threadIdx.x; i < N * NN; i += kSBlock) v[1] = fma(a.p1[N + i], a.p1[N + i], v[1]);
+  for (long long i = threadIdx.x; i < N * NN; i += kSBlock) {
+    const double d = a.p1[N + i] - cxi_at(a, i);
+    v[1] = fma(d, d, v[1]);
+  }
   block_sum_all<2, kSBlock>(v);
   const double dy = sqrt(v[0]), dx = sqrt(v[1]);
   const double By = a.d->Bbar_y, Bx = a.d->Bbar_xi;
@@ -147,7 +157,34 @@ __global__ void __launch_bounds__(kSBlock) project_start_kernel(const AlccArgs a
   }
   if (dx > Bx) {
     const double f = Bx / dx;
-    for (long long i = threadIdx.x; i < N * NN; i += kSBlock) a.p1[N + i] = 0.0 + f * (a.p1[N + i] - 0.0);
+    for (long long i = threadIdx.x; i < N * NN; i += kSBlock) {
+      const double c = cxi_at(a, i);
+      a.p1[N + i] = c + f * (a.p1[N + i] - c);
+    }
+  }
+}
+
+// block radius (alcc.cpp:238-243): Bbar = max(sqrt(|yhat - c_y|^2 + gamma |xihat - c_xi|^2),
+// 1e-8); Bbar_y = Bbar, Bbar_xi = Bbar / sqrt(gamma). One block.
+template <int NN>
+__global__ void __launch_bounds__(kSBlock) block_bounds_kernel(const AlccArgs a) {
+  const long long N = a.N;
+  double v[2] = {0.0, 0.0};
+  for (long long l = threadIdx.x; l < N; l += kSBlock) {
+    const double d = a.fy[l] - a.cy[l];
+    v[0] = fma(d, d, v[0]);
+  }
+  for (long long i = threadIdx.x; i < N * NN; i += kSBlock) {
+    const double d = a.fxi[i] - cxi_at(a, i);
+    v[1] = fma(d, d, v[1]);
+  }
+  block_sum_all<2, kSBlock>(v);
+  if (threadIdx.x == 0) {
+    const double gamma = a.d->gamma;
+    const double Bsq = v[0] + gamma * v[1];
+    const double B = fmax(sqrt(Bsq), 1e-8);
+    a.d->Bbar_y = B;
+    a.d->Bbar_xi = B / sqrt(gamma);
   }
 }
 
@@ -208,12 +245,13 @@ __global__ void __launch_bounds__(kPBlock) mapg_grad_kernel(const AlccArgs a) {
     for (int j = 0; j < NN; ++j) {
       const long long k = N + l * NN + j;
       const double adj = cs * a.X[l * NN + j] - ca[1 + j];
-      const double g = gm * a.p2[k] - adj;
+      const double g = gm * (a.p2[k] - cxi_at(a, l * NN + j)) - adj;
       bad |= !isfinite(g);
       const double x1 = a.p2[k] - g / Lx;
       a.p1p[k] = a.p1[k];
       a.p1[k] = x1;
-      acc[1] = fma(x1, x1, acc[1]);
+      const double dx = x1 - cxi_at(a, l * NN + j);
+      acc[1] = fma(dx, dx, acc[1]);
     }
   }
   if (bad) d->nonfinite = 1;
@@ -256,7 +294,8 @@ __global__ void __launch_bounds__(kPBlock) mapg_step_kernel(const AlccArgs a) {
       const long long k = N + l * NN + j;
       double x1 = a.p1[k];
       if (sx) {
-        x1 = 0.0 + fx * (x1 - 0.0);
+        const double c = cxi_at(a, l * NN + j);
+        x1 = c + fx * (x1 - c);
         a.p1[k] = x1;
       }
       const double ex = x1 - a.p2[k];
@@ -307,10 +346,12 @@ __global__ void __launch_bounds__(kSBlock) alcc_stats_kernel(const AlccArgs a) {
     v[4] = fma(a.cy[l], ay, v[4]);
 #pragma unroll
     for (int j = 0; j < NN; ++j) {
-      const double xi = a.p1[N + l * NN + j];
-      v[1] = fma(xi, xi, v[1]);
+      const double c = cxi_at(a, l * NN + j);
+      const double dx = a.p1[N + l * NN + j] - c;
+      v[1] = fma(dx, dx, v[1]);
       const double ax = ca[0] * a.X[l * NN + j] - ca[1 + j];
       v[3] = fma(ax, ax, v[3]);
+      v[4] = fma(c, ax, v[4]);  // lambda . rows_center = (A1^T l).c_y + (A2^T l).c_xi
     }
   }
   block_sum_all<5, kSBlock>(v);
@@ -354,14 +395,15 @@ struct AlccTab {
   static constexpr AlccKernel grad = mapg_grad_kernel<NN>;
   static constexpr AlccKernel step = mapg_step_kernel<NN>;
   static constexpr AlccKernel stats = alcc_stats_kernel<NN>;
+  static constexpr AlccKernel bounds = block_bounds_kernel<NN>;
 };
 struct AlccFns {
-  AlccKernel project, reset, records, grad, step, stats;
+  AlccKernel project, reset, records, grad, step, stats, bounds;
 };
 template <int NN>
 constexpr AlccFns fns_for() {
-  return {AlccTab<NN>::project, AlccTab<NN>::reset, AlccTab<NN>::records,
-          AlccTab<NN>::grad,    AlccTab<NN>::step,  AlccTab<NN>::stats};
+  return {AlccTab<NN>::project, AlccTab<NN>::reset, AlccTab<NN>::records, AlccTab<NN>::grad,
+          AlccTab<NN>::step,    AlccTab<NN>::stats, AlccTab<NN>::bounds};
 }
 constexpr AlccFns kFns[kMaxN] = {
     fns_for<1>(),  fns_for<2>(),  fns_for<3>(),  fns_for<4>(),  fns_for<5>(),  fns_for<6>(),
@@ -373,7 +415,10 @@ AlccArgs alcc_args(cr_handle* h) {
   AlccArgs a{};
   a.d = h->alcc.dev;
   a.X = h->X;
-  a.cy = h->ybar;
+  a.cy = h->alcc.cy ? h->alcc.cy : h->ybar;
+  a.cxi = h->alcc.cxi;
+  a.fy = h->alcc.fy;
+  a.fxi = h->alcc.fxi;
   a.agg = h->xbuf;
   a.p1 = h->alcc.p1;
   a.p1p = h->alcc.p1p;
@@ -497,6 +542,21 @@ cr_status outer_stats(cr_handle* h, const AlccFns& f, const AlccArgs& aa, bool u
 }
 
 }  // namespace
+
+cr_status alcc_prepare(cr_handle* h) { return ensure_alcc(h); }
+
+void alcc_release(cr_handle* h) {
+  AlccBufs& b = h->alcc;
+  if (b.gexec) cudaGraphExecDestroy(b.gexec);
+  for (double* p : {b.p1, b.p1p, b.p2, b.part1, b.part2}) dfree(p, h->st);
+  dfree(b.counter, h->st);
+  dfree(b.dev, h->st);
+  if (b.host) {
+    if (h->st) cudaStreamSynchronize(h->st);
+    cudaFreeHost(b.host);
+  }
+  b = AlccBufs{};
+}
 }  // namespace crb
 
 extern "C" {
@@ -539,55 +599,28 @@ cr_status cr_sigma_A(cr_handle* h, int32_t which, double tol, int32_t max_iters,
   return CR_OK;
 }
 
-cr_status cr_alcc_solve(cr_handle* h, const cr_alcc_config* cfg, const double* warm_y,
-                        const double* warm_xi, double* y_out, double* xi_out,
-                        cr_snapshot* history, int64_t* mapg_iters, cr_alcc_result* res) {
-  if (!h || !cfg || !warm_y || !warm_xi || !res) return CR_EINVAL;
-  if (!(cfg->c > 1)) return fail(h, CR_EINVAL, "alcc: c must be > 1");          // alcc.cpp:59
-  if (!(cfg->kappa > 0)) return fail(h, CR_EINVAL, "alcc: kappa must be > 0");  // :60
-  if (!(cfg->mu1 > 0)) return fail(h, CR_EINVAL, "alcc: mu1 must be > 0");      // :61
-  if (cfg->max_outer < 0 || cfg->mapg_cap < 1)
-    return fail(h, CR_EINVAL, "alcc: bad iteration limits");
-  if (h->comm != nullptr || h->R != h->N)
-    return fail(h, CR_EINVAL, "alcc: standalone ALCC runs on an unsharded handle");
-  CUDA_TRY(cudaSetDevice(h->device));
+}  // extern "C"
+
+namespace crb {
+// alcc_core (alcc.cpp:54-191) on this handle's row set, starting from the point
+// already in alcc.p1. target > 0: block stop rule (alcc.cpp:153-155) and the
+// block radius from the feasible slice (alcc.cpp:238-243); else the standalone
+// thresholds with cfg's radii. The point stays in alcc.p1.
+cr_status alcc_run(cr_handle* h, const cr_alcc_config* cfg, double sA1, double sA2,
+                   double target, bool block_mode, cr_snapshot* history, int64_t* mapg_iters,
+                   cr_alcc_result* res) {
   const auto t_start = std::chrono::steady_clock::now();
   auto seconds = [&]() {
     return std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
   };
-  {
-    const cr_status s = ensure_alcc(h);
-    if (s != CR_OK) return s;
-  }
   h->begun = false;  // the dual buffers now hold ALCC multipliers
   AlccBufs& b = h->alcc;
   b.done = false;
-  const int64_t N = h->N, n = h->n, Nn = N * n;
+  const int64_t N = h->N, n = h->n;
   const double gamma = h->gamma;
-  std::memset(res, 0, sizeof(*res));
-
-  double sA1 = cfg->sigma_A1, sA2 = cfg->sigma_A2;
-  if (!(sA1 > 0)) {
-    int32_t it = 0, cv = 0;
-    const cr_status s = cr_sigma_A(h, 1, 1e-6, 5000, &sA1, &it, &cv);
-    if (s != CR_OK) return s;
-    res->sigma_A1_iters = it;
-  }
-  if (!(sA2 > 0)) {
-    int32_t it = 0, cv = 0;
-    const cr_status s = cr_sigma_A(h, 2, 1e-6, 5000, &sA2, &it, &cv);
-    if (s != CR_OK) return s;
-    res->sigma_A2_iters = it;
-  }
-  res->sigma_A1 = sA1;
-  res->sigma_A2 = sA2;
-  res->sigma_seconds = seconds();
-
   const AlccFns& f = kFns[n - 1];
   const AlccArgs aa = alcc_args(h);
-  // start point and theta_1 = 0 in slot 0
-  CUDA_TRY(cudaMemcpyAsync(b.p1, warm_y, sizeof(double) * N, cudaMemcpyHostToDevice, h->st));
-  CUDA_TRY(cudaMemcpyAsync(b.p1 + N, warm_xi, sizeof(double) * Nn, cudaMemcpyHostToDevice, h->st));
+  // theta_1 = 0 in slot 0
   const size_t vbytes = sizeof(double) * (size_t)h->R * (size_t)h->ld;
   CUDA_TRY(cudaMemsetAsync(h->V[0], 0, vbytes, h->st));
   CUDA_TRY(cudaMemsetAsync(h->V[1], 0, vbytes, h->st));
@@ -603,6 +636,12 @@ cr_status cr_alcc_solve(cr_handle* h, const cr_alcc_config* cfg, const double* w
     const cr_status s = push_dev(h);
     if (s != CR_OK) return s;
   }
+  if (block_mode) {
+    CUDA_TRY(launch_alcc(f.bounds, 1, kSBlock, aa, h->st));
+    const cr_status s = pull_dev(h);
+    if (s != CR_OK) return s;
+  }
+  const double By = d.Bbar_y, Bx = d.Bbar_xi;
   CUDA_TRY(launch_alcc(f.project, 1, kSBlock, aa, h->st));
   double mapg_ms = 0;
   int64_t launches = 0;
@@ -617,7 +656,7 @@ cr_status cr_alcc_solve(cr_handle* h, const cr_alcc_config* cfg, const double* w
     const double p1 = d.stats[0] / (2.0 * mu) + gamma * d.stats[1] / (2.0 * mu) + 0.5 * d.stats[5];
     if (!std::isfinite(p1)) return fail(h, CR_ENONFINITE, "alcc: non-finite P_1 at the start point");
     tau = std::max(cfg->tau1_scale * p1, 1e-16);
-    alpha_y = alpha_xi = cfg->alpha1_scale * (cfg->Bbar_y + cfg->Bbar_xi);
+    alpha_y = alpha_xi = cfg->alpha1_scale * (By + Bx);
   }
   const int GI = 16;
   if (!b.gexec || b.graph_iters != GI) {
@@ -630,8 +669,7 @@ cr_status cr_alcc_solve(cr_handle* h, const cr_alcc_config* cfg, const double* w
   for (int64_t k = 1; k <= cfg->max_outer; ++k) {
     const double L_y = 1.0 / mu + sA1 * sA1;  // alcc.cpp:101-102
     const double L_xi = gamma / mu + sA2 * sA2;
-    const double lmax_real =
-        4.0 * std::sqrt((L_y * cfg->Bbar_y * cfg->Bbar_y + L_xi * cfg->Bbar_xi * cfg->Bbar_xi) / tau);
+    const double lmax_real = 4.0 * std::sqrt((L_y * By * By + L_xi * Bx * Bx) / tau);
     int64_t lmax = (int64_t)std::ceil(lmax_real);
     if (lmax < 10) lmax = 10;
     if (lmax > cfg->mapg_cap) lmax = cfg->mapg_cap;
@@ -686,15 +724,16 @@ cr_status cr_alcc_solve(cr_handle* h, const cr_alcc_config* cfg, const double* w
     const double dual_value = -0.5 * (mu2 * d.stats[2]) - (mu2 * d.stats[3]) / (2.0 * gamma) -
                               mu * d.stats[4];
     const double primal_value = 0.5 * sq_y + 0.5 * gamma * sq_xi;
-    res->certified_gap = primal_value - dual_value;
+    const double certified = primal_value - dual_value;
+    res->certified_gap = certified;
     res->infeas_raw = infeas_raw;
     res->gap_raw = gap_raw;
     res->outer_iters = k;
     res->objective = 0.5 * sq_y;
     b.mu = mu;
     b.done = true;
-    const double infeas_norm = infeas_raw / std::sqrt(m);
-    const double gap_norm = gap_raw / m;
+    const double infeas_norm = m > 0 ? infeas_raw / std::sqrt(m) : 0.0;
+    const double gap_norm = m > 0 ? gap_raw / m : 0.0;
     if (history) {
       cr_snapshot& sn = history[k - 1];
       sn.iter = (double)k;
@@ -706,7 +745,12 @@ cr_status cr_alcc_solve(cr_handle* h, const cr_alcc_config* cfg, const double* w
       sn.gap_norm = gap_norm;
       sn.wall_time_s = seconds();
     }
-    if (infeas_norm <= cfg->infeas_norm_tol && std::fabs(gap_norm) <= cfg->gap_norm_tol) {
+    bool stop;
+    if (target > 0)  // alcc.cpp:153-155, |lambda| = mu |v|
+      stop = certified <= target && (mu * std::sqrt(d.stats[5])) * infeas_raw <= target;
+    else
+      stop = infeas_norm <= cfg->infeas_norm_tol && std::fabs(gap_norm) <= cfg->gap_norm_tol;
+    if (stop) {
       res->reason = CR_THRESHOLDS;
       break;
     }
@@ -728,22 +772,71 @@ cr_status cr_alcc_solve(cr_handle* h, const cr_alcc_config* cfg, const double* w
     const cr_status s = push_dev(h);
     if (s != CR_OK) return s;
   }
+  if (res->outer_iters == 0) {  // max_outer = 0: the projected start point
+    const cr_status s = outer_stats(h, f, aa, false, cfg->c);
+    if (s != CR_OK) return s;
+    res->objective = 0.5 * d.stats[0];
+  }
+  res->mapg_seconds += mapg_ms * 1e-3;
+  res->launches += launches;
+  res->wall_seconds += seconds();
+  return CR_OK;
+}
+}  // namespace crb
+
+extern "C" {
+
+cr_status cr_alcc_solve(cr_handle* h, const cr_alcc_config* cfg, const double* warm_y,
+                        const double* warm_xi, double* y_out, double* xi_out,
+                        cr_snapshot* history, int64_t* mapg_iters, cr_alcc_result* res) {
+  if (!h || !cfg || !warm_y || !warm_xi || !res) return CR_EINVAL;
+  if (!(cfg->c > 1)) return fail(h, CR_EINVAL, "alcc: c must be > 1");          // alcc.cpp:59
+  if (!(cfg->kappa > 0)) return fail(h, CR_EINVAL, "alcc: kappa must be > 0");  // :60
+  if (!(cfg->mu1 > 0)) return fail(h, CR_EINVAL, "alcc: mu1 must be > 0");      // :61
+  if (cfg->max_outer < 0 || cfg->mapg_cap < 1)
+    return fail(h, CR_EINVAL, "alcc: bad iteration limits");
+  if (h->comm != nullptr || h->R != h->N)
+    return fail(h, CR_EINVAL, "alcc: standalone ALCC runs on an unsharded handle");
+  CUDA_TRY(cudaSetDevice(h->device));
+  const auto t_start = std::chrono::steady_clock::now();
+  {
+    const cr_status s = ensure_alcc(h);
+    if (s != CR_OK) return s;
+  }
+  AlccBufs& b = h->alcc;
+  b.cy = nullptr;  // standalone centres (ybar, 0)
+  b.cxi = nullptr;
+  const int64_t N = h->N, n = h->n, Nn = N * n;
+  std::memset(res, 0, sizeof(*res));
+  double sA1 = cfg->sigma_A1, sA2 = cfg->sigma_A2;
+  if (!(sA1 > 0)) {
+    int32_t it = 0, cv = 0;
+    const cr_status s = cr_sigma_A(h, 1, 1e-6, 5000, &sA1, &it, &cv);
+    if (s != CR_OK) return s;
+    res->sigma_A1_iters = it;
+  }
+  if (!(sA2 > 0)) {
+    int32_t it = 0, cv = 0;
+    const cr_status s = cr_sigma_A(h, 2, 1e-6, 5000, &sA2, &it, &cv);
+    if (s != CR_OK) return s;
+    res->sigma_A2_iters = it;
+  }
+  res->sigma_A1 = sA1;
+  res->sigma_A2 = sA2;
+  res->sigma_seconds =
+      std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
+  CUDA_TRY(cudaMemcpyAsync(b.p1, warm_y, sizeof(double) * N, cudaMemcpyHostToDevice, h->st));
+  CUDA_TRY(cudaMemcpyAsync(b.p1 + N, warm_xi, sizeof(double) * Nn, cudaMemcpyHostToDevice, h->st));
+  {
+    const cr_status s = alcc_run(h, cfg, sA1, sA2, 0.0, false, history, mapg_iters, res);
+    if (s != CR_OK) return s;
+  }
   if (y_out) CUDA_TRY(cudaMemcpyAsync(y_out, b.p1, sizeof(double) * N, cudaMemcpyDeviceToHost, h->st));
   if (xi_out)
     CUDA_TRY(cudaMemcpyAsync(xi_out, b.p1 + N, sizeof(double) * Nn, cudaMemcpyDeviceToHost, h->st));
   CUDA_TRY(cudaStreamSynchronize(h->st));
-  if (res->outer_iters == 0) {  // max_outer = 0: the projected start point
-    double sy = 0;
-    std::vector<double> y0((size_t)N);
-    CUDA_TRY(cudaMemcpy(y0.data(), b.p1, sizeof(double) * N, cudaMemcpyDeviceToHost));
-    std::vector<double> yb((size_t)N);
-    CUDA_TRY(cudaMemcpy(yb.data(), h->ybar, sizeof(double) * N, cudaMemcpyDeviceToHost));
-    for (int64_t i = 0; i < N; ++i) sy += (y0[i] - yb[i]) * (y0[i] - yb[i]);
-    res->objective = 0.5 * sy;
-  }
-  res->wall_seconds = seconds();
-  res->mapg_seconds = mapg_ms * 1e-3;
-  res->launches = launches;
+  res->wall_seconds =
+      std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
   return CR_OK;
 }
 

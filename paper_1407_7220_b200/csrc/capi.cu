@@ -29,6 +29,18 @@ using namespace crb;
 
 cudaStream_t g_alloc_stream = nullptr;
 
+namespace crb {  // general.cu: P-APG(ALCC) with K blocks
+cr_status general_begin(cr_handle* h);
+cr_status general_iterate(cr_handle* h, int64_t max_steps, int64_t* done, int32_t* stopped,
+                          double* sweep_seconds, int64_t* launches);
+cr_status general_final(cr_handle* h, double final_tol);
+cr_status general_get_theta(cr_handle* h, double* out);
+cr_status general_get_rows(cr_handle* h, double* out);
+cr_status general_theta_in(cr_handle* h, const double* theta0);
+void general_release(cr_handle* h);
+void alcc_release(cr_handle* h);
+}  // namespace crb
+
 namespace {
 
 PrimalArgs primal_args(cr_handle* h, int mode) {
@@ -318,6 +330,8 @@ void cr_destroy(cr_handle* h) {
   if (!h) return;
   cudaSetDevice(h->device);
   if (h->st) cudaStreamSynchronize(h->st);
+  if (h->part.K > 0) general_release(h);
+  alcc_release(h);
   if (h->gexec) cudaGraphExecDestroy(h->gexec);
   if (h->comm) ncclCommDestroy(h->comm);
   double* bufs[] = {h->X,       h->ybar,    h->rowrec,  h->colrec,   h->V[0],   h->V[1],
@@ -381,7 +395,9 @@ cr_status cr_sigma_C(cr_handle* h, double tol, int32_t max_iters, double* sigma,
   for (double& x : v) x /= nv;
   CUDA_TRY(cudaMemcpyAsync(h->pw_u, v.data(), sizeof(double) * cols, cudaMemcpyHostToDevice,
                            h->st));
-  if (!h->sigma_by_sweep) {  // whole power iteration in one cooperative launch
+  // closed-form steps assume singleton blocks; a K-block partition masks the
+  // same-block pairs inside the sweep instead
+  if (!h->sigma_by_sweep && h->part.K == 0) {  // whole power iteration in one cooperative launch
     PowerLoopArgs pa{};
     pa.u = h->pw_u;
     pa.v = h->pw_v;
@@ -529,7 +545,7 @@ cr_status begin_impl(cr_handle* h, const cr_papg_config* cfg, const double* thet
   c.max_seconds = cfg->max_seconds;
   c.gap_div = (double)N * (double)(N - 1);
   c.infeas_div = std::sqrt(c.gap_div);
-  c.K = (double)N;  // singleton partition
+  c.K = h->part.K > 0 ? (double)h->part.K : (double)N;  // papg.cpp:198 cushion
   if (resume) {  // theta1 = Pi_Q2(theta0), theta0 = s V[cur] >= 0: a rescale only
     const double nrm = prev.theta1_norm;
     const double sc = nrm > c.B_theta ? c.B_theta / nrm : 1.0;
@@ -549,17 +565,22 @@ cr_status begin_impl(cr_handle* h, const cr_papg_config* cfg, const double* thet
     CUDA_TRY(cudaMemsetAsync(h->aggsave, 0, sizeof(double) * payload_len(h), h->st));
   }
 
+  if (theta0 && h->part.K > 0) {
+    const cr_status s = general_theta_in(h, theta0);
+    if (s != CR_OK) return s;
+  }
   if (theta0) {  // warm start: theta1 = Pi_Q2(theta0) (papg.cpp:159-164)
     const int64_t rowlen = N - 1;
     const int64_t rows_per = std::max<int64_t>(1, h->stage_elems / rowlen);
-    for (int64_t ra = 0; ra < h->R; ra += rows_per) {
+    for (int64_t ra = 0; ra < h->R && h->part.K == 0; ra += rows_per) {
       const int64_t rb = std::min(h->R, ra + rows_per);
       CUDA_TRY(cudaMemcpyAsync(h->stage, theta0 + ra * rowlen,
                                sizeof(double) * (rb - ra) * rowlen, cudaMemcpyHostToDevice,
                                h->st));
       CUDA_TRY(launch_theta_in(h->stage, h->V[0], N, h->ld, h->r0, ra, rb, h->st));
     }
-    const double* tpos = theta0 + h->R * rowlen;
+    const double* tpos =
+        theta0 + (h->part.K > 0 ? h->N * (h->N - h->part.nbar) : h->R * rowlen);
     double pos_sq = 0;
     for (int64_t l = 0; l < N; ++l) {
       const double t = tpos[l] > 0 ? tpos[l] : 0.0;
@@ -583,9 +604,10 @@ cr_status begin_impl(cr_handle* h, const cr_papg_config* cfg, const double* thet
   {
     const char* sm = std::getenv("CRB_SMALL");
     const double vbytes2 = 2.0 * 8.0 * (double)h->R * (double)h->ld;
-    bool want = h->comm == nullptr && cfg->graph_iters == 0 && vbytes2 <= 48e6;
+    bool want = h->comm == nullptr && cfg->graph_iters == 0 && vbytes2 <= 48e6 &&
+                h->part.K == 0;
     if (sm && sm[0] == '0') want = false;
-    if (sm && sm[0] == '1' && h->comm == nullptr && h->R == h->N) want = true;
+    if (sm && sm[0] == '1' && h->comm == nullptr && h->R == h->N && h->part.K == 0) want = true;
     h->small_mode = false;
     if (want) {
       h->ks = small_loop_info((int)h->n);
@@ -618,7 +640,11 @@ cr_status begin_impl(cr_handle* h, const cr_papg_config* cfg, const double* thet
   }
 
   // batch size: graphs when an iteration is short, direct launches otherwise
-  if (cfg->graph_iters > 0) {
+  if (h->part.K > 0) {
+    h->graph_iters = 0;  // host-driven (block solves between the kernels)
+    const cr_status s = general_begin(h);
+    if (s != CR_OK) return s;
+  } else if (cfg->graph_iters > 0) {
     h->graph_iters = cfg->graph_iters;
   } else if (cfg->graph_iters < 0) {
     h->graph_iters = 0;
@@ -667,6 +693,19 @@ cr_status cr_papg_iterate(cr_handle* h, int64_t max_steps, int64_t* done, int32_
   if (pause < ell0) pause = LLONG_MAX;
   cr_status s = set_pause(h, pause);
   if (s != CR_OK) return s;
+  if (h->part.K > 0) {  // general-K partition: host-driven iterations (general.cu)
+    const auto wall0 = std::chrono::steady_clock::now();
+    double sw = 0;
+    int64_t nl = 0;
+    s = general_iterate(h, max_steps, done, stopped, &sw, &nl);
+    const double wall =
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();
+    h->last_seconds = wall;
+    h->last_sweep_seconds = sw;
+    h->last_launches = nl;
+    h->loop_seconds += wall;
+    return s;
+  }
   if (h->small_mode) {  // one persistent launch, halts on termination or pause
     if (h->ctrl_h->stopped || max_steps == 0) {
       h->last_seconds = 0;
@@ -799,6 +838,7 @@ cr_status cr_papg_iterate(cr_handle* h, int64_t max_steps, int64_t* done, int32_
 
 cr_status cr_iter_local(cr_handle* h) {
   if (!h) return CR_EINVAL;
+  if (h->part.K > 0) return fail(h, CR_EINVAL, "partition: the exchange seam is singleton-only");
   if (!h->begun) return fail(h, CR_ESTATE, "papg: iterate before begin");
   CUDA_TRY(cudaSetDevice(h->device));
   cr_status s = set_pause(h, LLONG_MAX);
@@ -846,10 +886,18 @@ cr_status cr_papg_finish(cr_handle* h, cr_papg_result* res, double* y, double* x
   cr_status s = sync_ctrl(h);
   if (s != CR_OK) return s;
   const DevCtrl& c = *h->ctrl_h;
-  // final re-solve at theta1 (papg.cpp:265-277): primal of s_cur * V[cur]
-  const PrimalArgs pa = primal_args(h, 1);
-  CUDA_TRY(launch_primal(pa, h->st));
-  CUDA_TRY(launch_reduce_records(h->k2part, h->k2_blocks, kK2Scal, h->k2sum, h->st));
+  double ft = 1.0 / std::pow((double)c.ell, 3.0);  // papg.cpp:266-269
+  ft = std::min(ft, h->cfg.inner_tol_floor);
+  ft = std::min(ft, h->cfg.final_resolve_tol);
+  if (h->part.K > 0) {  // block re-solves at theta1 (general.cu)
+    s = general_final(h, ft);
+    if (s != CR_OK) return s;
+  } else {
+    // final re-solve at theta1 (papg.cpp:265-277): primal of s_cur * V[cur]
+    const PrimalArgs pa = primal_args(h, 1);
+    CUDA_TRY(launch_primal(pa, h->st));
+    CUDA_TRY(launch_reduce_records(h->k2part, h->k2_blocks, kK2Scal, h->k2sum, h->st));
+  }
   double k2[kK2Scal];
   CUDA_TRY(cudaMemcpyAsync(k2, h->k2sum, sizeof(k2), cudaMemcpyDeviceToHost, h->st));
   if (y) CUDA_TRY(cudaMemcpyAsync(y, h->yout, sizeof(double) * h->N, cudaMemcpyDeviceToHost, h->st));
@@ -861,10 +909,6 @@ cr_status cr_papg_finish(cr_handle* h, cr_papg_result* res, double* y, double* x
     CUDA_TRY(cudaMemcpyAsync(history, h->hist, sizeof(double) * 8 * nh, cudaMemcpyDeviceToHost,
                              h->st));
   CUDA_TRY(cudaStreamSynchronize(h->st));
-  const double ell = (double)c.ell;
-  double ft = 1.0 / std::pow(ell, 3.0);
-  ft = std::min(ft, h->cfg.inner_tol_floor);
-  ft = std::min(ft, h->cfg.final_resolve_tol);
   std::memset(res, 0, sizeof(*res));
   res->iters = c.ell;
   res->reason = c.reason;
@@ -906,6 +950,7 @@ cr_status cr_get_theta(cr_handle* h, double* out) {
   CUDA_TRY(cudaSetDevice(h->device));
   cr_status s = sync_ctrl(h);
   if (s != CR_OK) return s;
+  if (h->part.K > 0) return general_get_theta(h, out);
   const int cur = h->ctrl_h->cur;
   const double sc = h->ctrl_h->s_cur;
   const int64_t rowlen = h->N - 1;
@@ -928,6 +973,7 @@ cr_status cr_get_rows(cr_handle* h, double* out) {
   if (!h || !out) return CR_EINVAL;
   if (!h->begun) return fail(h, CR_ESTATE, "no dual state");
   CUDA_TRY(cudaSetDevice(h->device));
+  if (h->part.K > 0) return general_get_rows(h, out);
   const int64_t rowlen = h->N - 1;
   const int64_t rows_per = std::max<int64_t>(1, h->stage_elems / rowlen);
   for (int64_t ra = 0; ra < h->R; ra += rows_per) {

@@ -63,6 +63,9 @@ struct DevCtrl {
   // metrics of the last completed iteration (papg.cpp:191-208)
   double gap_raw, gap_norm, infeas_raw, infeas_norm, g_value, fw, theta1_norm;
   double objective, reg_objective;
+  // general-K partition: |within-block infeasibility| of the current eta
+  // (dual_gradient's within_infeas_raw, papg.cpp:128), host-set per iteration
+  double within_raw;
 };
 
 struct SweepArgs {
@@ -84,7 +87,25 @@ struct SweepArgs {
   int T;                  // column tiles (CW strips each)
   int G;                  // CTAs (persistent, one wave)
   int maxspan;            // max segments (tiles) one CTA can touch
+  long long nbar;         // block size of the partition: pairs inside one block are
+                          // masked like the diagonal (1: singleton blocks)
 };
+
+// same block of the partition. BLK = false: singleton blocks (the diagonal);
+// the blocked test is a separate instantiation so the singleton kernels carry
+// no 64-bit division code (it cost 17% of the cfg2 sweep, measured).
+template <bool BLK>
+__host__ __device__ __forceinline__ bool same_block(long long a, long long b, long long nbar) {
+  if constexpr (BLK) return a / nbar == b / nbar;
+  else return a == b;
+}
+// the row range [r0, r0 + nr) and column range [c0, c0 + nc) share no block
+template <bool BLK>
+__host__ __device__ __forceinline__ bool blocks_disjoint(long long r0, long long nr, long long c0,
+                                                         long long nc, long long nbar) {
+  if constexpr (BLK) return (r0 + nr - 1) / nbar < c0 / nbar || r0 / nbar > (c0 + nc - 1) / nbar;
+  else return r0 + nr <= c0 || r0 >= c0 + nc;
+}
 
 // kModePapg:   the P-APG step above (reads V, V'; writes V')
 // kModePower:  aggregates of the residual itself (sigma_max(C) by sweeps)
@@ -105,8 +126,10 @@ struct SweepKernelInfo {
   int smem_bytes;
 };
 enum SweepVariant { kSweepDfma = 0, kSweepMma = 1 };
-SweepKernelInfo sweep_dfma_info(int n, int mode);  // sweep.cu (CUDA-core DFMA)
-SweepKernelInfo sweep_mma_info(int n, int mode);   // sweep_mma.cu (DMMA tensor cores)
+// blocked = true: same-block pairs of a K-block partition masked (kModePapg /
+// kModePower only)
+SweepKernelInfo sweep_dfma_info(int n, int mode, bool blocked = false);  // sweep.cu (CUDA-core DFMA)
+SweepKernelInfo sweep_mma_info(int n, int mode, bool blocked = false);   // sweep_mma.cu (DMMA)
 int launch_sweep(const SweepKernelInfo& info, const SweepArgs& a, void* stream);
 
 }  // namespace crb

@@ -21,6 +21,9 @@ struct AlccBufs {
   AlccDev* dev = nullptr;       // device-resident MAPG / outer state
   AlccDev* host = nullptr;      // pinned mirror
   double *p1 = nullptr, *p1p = nullptr, *p2 = nullptr;  // [y | xi] points (N (n+1))
+  // block mode (general-K P-APG sub-problem): centres and the feasible slice;
+  // cy == nullptr means the standalone centres (ybar, 0)
+  double *cy = nullptr, *cxi = nullptr, *fy = nullptr, *fxi = nullptr;
   double *part1 = nullptr, *part2 = nullptr;            // per-block partials
   unsigned int* counter = nullptr;
   SweepKernelInfo kpen{}, kupd{};
@@ -29,6 +32,23 @@ struct AlccBufs {
   int blocks = 0;
   bool done = false;            // a finished solve is on the handle (multiplier export)
   double mu = 0;                // mu of the last outer step
+};
+// general-K P-APG(ALCC) state (general.cu): K blocks of nbar points, one ALCC
+// sub-problem handle per block (alcc_solve_block, alcc.cpp:222-258)
+struct Partition {
+  int64_t K = 0, nbar = 1;
+  std::vector<cr_handle*> blocks;
+  cr_alcc_config inner{};
+  double sigma_A1 = 0;                 // within A1 (the same in every block)
+  std::vector<double> sigma_A2;        // within A2 per block
+  std::vector<double> block_infeas;    // last ALCC infeasibility per block
+  double *cy = nullptr, *cxi = nullptr;      // block centres ybar + q_y, q_xi / gamma
+  double *qy = nullptr, *qxi = nullptr;      // C^T theta2 (objective terms)
+  double *th2pos = nullptr;                  // theta2 of the y >= 0 rows
+  double *ey = nullptr, *exi = nullptr;      // eta (block minimisers)
+  double *fy = nullptr, *fxi = nullptr;      // feasible affine point (prepare_problem)
+  int64_t inner_iters = 0;
+  double inner_seconds = 0;
 };
 }  // namespace crb
 
@@ -93,6 +113,8 @@ struct cr_handle {
   int64_t last_launches = 0;
   // standalone ALCC (alcc.cu)
   crb::AlccBufs alcc{};
+  // general-K partition (general.cu); K == 0: singleton blocks
+  crb::Partition part{};
   std::string err;
 };
 
@@ -158,6 +180,7 @@ inline SweepArgs sweep_args(cr_handle* h, int mode, bool agg_only) {
   a.G = h->G;
   a.U = h->U;
   a.maxspan = h->maxspan;
+  a.nbar = h->part.K > 0 ? h->part.nbar : 1;
   return a;
 }
 

@@ -154,7 +154,8 @@ __device__ __forceinline__ void control_logic(DevCtrl* c, const double* scal, co
   c->g_star_upper = fmin(c->g_star_upper, g_value + fw + cushion);
   // gap / infeasibility (papg.cpp:201-208)
   const double gap_raw = c->use_momentum ? s_new * S_vr : S_tr;
-  const double infeas_raw = cross_infeas;
+  const double within = c->within_raw;  // 0 for singleton blocks
+  const double infeas_raw = sqrt(within * within + cross_infeas * cross_infeas);
   const double gap_norm = gap_raw / c->gap_div;
   const double infeas_norm = infeas_raw / c->infeas_div;
   const double wall = (double)(globaltimer() - c->t_start_ns) * 1e-9;

@@ -96,9 +96,10 @@ struct StageView {
   long long col0;     // global column of this lane's first column
   long long g0;       // global row of stage row 0
   double* srs;        // row-sum transpose slot of stage row 0
+  long long nbar;     // partition block size (same-block pairs masked)
 };
 
-template <int NN, int MODE, int TR, int TC, bool MASK, bool UNIT>
+template <int NN, int MODE, int TR, int TC, bool MASK, bool UNIT, bool BLK>
 __device__ __forceinline__ void run_stage(const StageView& sv, int nr, int lane,
                                           ColState<NN, cols_per_lane<NN>()>& cs, const Coef& cf,
                                           Scal& sc) {
@@ -131,7 +132,7 @@ __device__ __forceinline__ void run_stage(const StageView& sv, int nr, int lane,
           if (j + 1 < NN) rb = fma(x[j + 1], cs.xi[k][j + 1], rb);
         }
         double row = ra + rb;
-        if (MASK && (!cs.valid[k] || sv.col0 + k == sv.g0 + q)) row = 0.0;
+        if (MASK && (!cs.valid[k] || same_block<BLK>(sv.col0 + k, sv.g0 + q, sv.nbar))) row = 0.0;
         double v;
         if (MODE == kModePapg) {
           double th2;
@@ -175,7 +176,7 @@ __device__ __forceinline__ void run_stage(const StageView& sv, int nr, int lane,
   }
 }
 
-template <int NN, int MODE>
+template <int NN, int MODE, bool BLK>
 __global__ void __launch_bounds__(threads_per_cta<NN>()) sweep_kernel(const SweepArgs a) {
   constexpr int kCW = consumer_warps<NN>();
   constexpr int C = cols_per_lane<NN>();
@@ -301,15 +302,17 @@ __global__ void __launch_bounds__(threads_per_cta<NN>()) sweep_kernel(const Swee
       if (active) {
         const double* st = stages + s * SD;
         StageView sv{st + lane_off, st + TR * TC + lane_off, st + 2 * TR * TC,
-                     Vp + r * a.ld + col0, a.ld, col0, a.r0 + r, srs + win * kRsPitch};
-        // the diagonal or a pad column touches this stage: per-pair masks
-        const bool clean = strip_full && (sv.g0 + nr <= strip_lo || sv.g0 >= strip_lo + W);
+                     Vp + r * a.ld + col0, a.ld, col0, a.r0 + r, srs + win * kRsPitch,
+                     a.nbar};
+        // the diagonal (a same-block pair) or a pad column touches this stage:
+        // per-pair masks
+        const bool clean = strip_full && blocks_disjoint<BLK>(sv.g0, nr, strip_lo, W, a.nbar);
         if (clean) {
-          if (unit_scale) run_stage<NN, MODE, TR, TC, false, true>(sv, nr, lane, cs, cf, sc);
-          else run_stage<NN, MODE, TR, TC, false, false>(sv, nr, lane, cs, cf, sc);
+          if (unit_scale) run_stage<NN, MODE, TR, TC, false, true, BLK>(sv, nr, lane, cs, cf, sc);
+          else run_stage<NN, MODE, TR, TC, false, false, BLK>(sv, nr, lane, cs, cf, sc);
         } else {
-          if (unit_scale) run_stage<NN, MODE, TR, TC, true, true>(sv, nr, lane, cs, cf, sc);
-          else run_stage<NN, MODE, TR, TC, true, false>(sv, nr, lane, cs, cf, sc);
+          if (unit_scale) run_stage<NN, MODE, TR, TC, true, true, BLK>(sv, nr, lane, cs, cf, sc);
+          else run_stage<NN, MODE, TR, TC, true, false, BLK>(sv, nr, lane, cs, cf, sc);
         }
       }
       __syncwarp();
@@ -368,12 +371,19 @@ __global__ void __launch_bounds__(threads_per_cta<NN>()) sweep_kernel(const Swee
 }
 
 template <int NN>
-SweepKernelInfo info_for(int mode) {
+SweepKernelInfo info_for(int mode, bool blocked) {
   SweepKernelInfo inf{};
-  inf.fn = mode == kModePapg      ? (const void*)sweep_kernel<NN, kModePapg>
-           : mode == kModePower   ? (const void*)sweep_kernel<NN, kModePower>
-           : mode == kModePenalty ? (const void*)sweep_kernel<NN, kModePenalty>
-                                  : (const void*)sweep_kernel<NN, kModePenaltyUpdate>;
+  if (blocked) {
+    inf.fn = mode == kModePapg    ? (const void*)sweep_kernel<NN, kModePapg, true>
+             : mode == kModePower ? (const void*)sweep_kernel<NN, kModePower, true>
+                                  : nullptr;
+    if (!inf.fn) return inf;
+  } else {
+    inf.fn = mode == kModePapg      ? (const void*)sweep_kernel<NN, kModePapg, false>
+             : mode == kModePower   ? (const void*)sweep_kernel<NN, kModePower, false>
+             : mode == kModePenalty ? (const void*)sweep_kernel<NN, kModePenalty, false>
+                                    : (const void*)sweep_kernel<NN, kModePenaltyUpdate, false>;
+  }
   inf.strip_cols = 32 * cols_per_lane<NN>();
   inf.warps_per_block = consumer_warps<NN>();
   inf.tile_cols = tile_cols<NN>();
@@ -390,19 +400,21 @@ SweepKernelInfo info_for(int mode) {
 
 template <int... Ns> struct Table;
 template <int N0, int... Ns> struct Table<N0, Ns...> {
-  static SweepKernelInfo info(int n, int mode) {
-    return n == N0 ? info_for<N0>(mode) : Table<Ns...>::info(n, mode);
+  static SweepKernelInfo info(int n, int mode, bool blocked) {
+    return n == N0 ? info_for<N0>(mode, blocked) : Table<Ns...>::info(n, mode, blocked);
   }
 };
 template <> struct Table<> {
-  static SweepKernelInfo info(int, int) { return SweepKernelInfo{}; }
+  static SweepKernelInfo info(int, int, bool) { return SweepKernelInfo{}; }
 };
 using AllN = Table<1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16, 17, 18, 19, 20, 21, 22,
                    23, 24>;
 
 }  // namespace
 
-SweepKernelInfo sweep_dfma_info(int n, int mode) { return AllN::info(n, mode); }
+SweepKernelInfo sweep_dfma_info(int n, int mode, bool blocked) {
+  return AllN::info(n, mode, blocked);
+}
 
 int launch_sweep(const SweepKernelInfo& info, const SweepArgs& a, void* stream) {
   void* args[] = {const_cast<SweepArgs*>(&a)};

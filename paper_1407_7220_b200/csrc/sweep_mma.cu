@@ -86,11 +86,11 @@ struct MScal {
 };
 
 // One 8-row stage for one warp. MASK: diagonal / partial-stage masking.
-template <int NN, int MODE, bool MASK, bool UNIT>
+template <int NN, int MODE, bool MASK, bool UNIT, bool BLK>
 __device__ __forceinline__ void mma_stage(const double* __restrict__ sv, const double* __restrict__ svp,
                                           const double* __restrict__ srec, double* gout,
                                           long long ld, long long gcol0, long long grow0, int nr,
-                                          long long ncols,
+                                          long long ncols, long long nbar,
                                           int lane, const double (&A)[mma_ct<NN>()][ksteps<NN>()],
                                           double (&D)[mma_ct<NN>()][fblocks<NN>()][2],
                                           const double (&Cc)[mma_ct<NN>()], const MCoef& cf,
@@ -136,7 +136,8 @@ __device__ __forceinline__ void mma_stage(const double* __restrict__ sv, const d
       if (SPLIT) row += yr[j] + Cc[ct];  // y_l1 - c_l2 (Cc holds -c_l2)
       // diagonal, rows past a partial stage, pad columns (with y - c split out
       // of the MMA a pad column's zero fragments no longer zero its row)
-      if (MASK && (gcol0 + cl == grow0 + rr || !rv || gcol0 + cl >= ncols)) row = 0.0;
+      if (MASK && (same_block<BLK>(gcol0 + cl, grow0 + rr, nbar) || !rv || gcol0 + cl >= ncols))
+        row = 0.0;
       if (MODE == kModePapg) {
         const double c1 = sv[rr * kTCP + cl];
         const double p1 = svp[rr * kTCP + cl];
@@ -179,7 +180,7 @@ __device__ __forceinline__ void mma_stage(const double* __restrict__ sv, const d
   }
 }
 
-template <int NN, int MODE>
+template <int NN, int MODE, bool BLK>
 __global__ void __launch_bounds__(mma_threads<NN>(), kMinCtas) sweep_mma_kernel(const SweepArgs a) {
   CRB_GEO(NN)
   constexpr int KS = ksteps<NN>();
@@ -305,20 +306,20 @@ __global__ void __launch_bounds__(mma_threads<NN>(), kMinCtas) sweep_mma_kernel(
         // warp-uniform: no diagonal in this 8-row block of the warp's columns, full
         // stage, no pad column
         const bool clean = nr == kTR && gcol0 + kW <= a.N &&
-                           (grow0 + kTR <= gcol0 || grow0 >= gcol0 + kW);
+                           blocks_disjoint<BLK>(grow0, kTR, gcol0, kW, a.nbar);
         if (clean) {
           if (unit_scale)
-            mma_stage<NN, MODE, false, true>(sv, svp, srec, gout, a.ld, gcol0, grow0, nr, a.N, lane, A,
+            mma_stage<NN, MODE, false, true, BLK>(sv, svp, srec, gout, a.ld, gcol0, grow0, nr, a.N, a.nbar, lane, A,
                                              D, Cc, cf, sc, rsj);
           else
-            mma_stage<NN, MODE, false, false>(sv, svp, srec, gout, a.ld, gcol0, grow0, nr, a.N, lane,
+            mma_stage<NN, MODE, false, false, BLK>(sv, svp, srec, gout, a.ld, gcol0, grow0, nr, a.N, a.nbar, lane,
                                               A, D, Cc, cf, sc, rsj);
         } else {
           if (unit_scale)
-            mma_stage<NN, MODE, true, true>(sv, svp, srec, gout, a.ld, gcol0, grow0, nr, a.N, lane, A,
+            mma_stage<NN, MODE, true, true, BLK>(sv, svp, srec, gout, a.ld, gcol0, grow0, nr, a.N, a.nbar, lane, A,
                                              D, Cc, cf, sc, rsj);
           else
-            mma_stage<NN, MODE, true, false>(sv, svp, srec, gout, a.ld, gcol0, grow0, nr, a.N, lane, A,
+            mma_stage<NN, MODE, true, false, BLK>(sv, svp, srec, gout, a.ld, gcol0, grow0, nr, a.N, a.nbar, lane, A,
                                              D, Cc, cf, sc, rsj);
         }
       }
@@ -391,13 +392,20 @@ __global__ void __launch_bounds__(mma_threads<NN>(), kMinCtas) sweep_mma_kernel(
 }
 
 template <int NN>
-SweepKernelInfo info_for(int mode) {
+SweepKernelInfo info_for(int mode, bool blocked) {
   CRB_GEO(NN)
   SweepKernelInfo inf{};
-  inf.fn = mode == kModePapg      ? (const void*)sweep_mma_kernel<NN, kModePapg>
-           : mode == kModePower   ? (const void*)sweep_mma_kernel<NN, kModePower>
-           : mode == kModePenalty ? (const void*)sweep_mma_kernel<NN, kModePenalty>
-                                  : (const void*)sweep_mma_kernel<NN, kModePenaltyUpdate>;
+  if (blocked) {
+    inf.fn = mode == kModePapg    ? (const void*)sweep_mma_kernel<NN, kModePapg, true>
+             : mode == kModePower ? (const void*)sweep_mma_kernel<NN, kModePower, true>
+                                  : nullptr;
+    if (!inf.fn) return inf;
+  } else {
+    inf.fn = mode == kModePapg      ? (const void*)sweep_mma_kernel<NN, kModePapg, false>
+             : mode == kModePower   ? (const void*)sweep_mma_kernel<NN, kModePower, false>
+             : mode == kModePenalty ? (const void*)sweep_mma_kernel<NN, kModePenalty, false>
+                                    : (const void*)sweep_mma_kernel<NN, kModePenaltyUpdate, false>;
+  }
   inf.strip_cols = kW;
   inf.warps_per_block = kCW;
   inf.tile_cols = kTC;
@@ -414,18 +422,20 @@ SweepKernelInfo info_for(int mode) {
 
 template <int... Ns> struct Table;
 template <int N0, int... Ns> struct Table<N0, Ns...> {
-  static SweepKernelInfo info(int n, int mode) {
-    return n == N0 ? info_for<N0>(mode) : Table<Ns...>::info(n, mode);
+  static SweepKernelInfo info(int n, int mode, bool blocked) {
+    return n == N0 ? info_for<N0>(mode, blocked) : Table<Ns...>::info(n, mode, blocked);
   }
 };
 template <> struct Table<> {
-  static SweepKernelInfo info(int, int) { return SweepKernelInfo{}; }
+  static SweepKernelInfo info(int, int, bool) { return SweepKernelInfo{}; }
 };
 using AllN = Table<1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16, 17, 18, 19, 20, 21, 22,
                    23, 24>;
 
 }  // namespace
 
-SweepKernelInfo sweep_mma_info(int n, int mode) { return AllN::info(n, mode); }
+SweepKernelInfo sweep_mma_info(int n, int mode, bool blocked) {
+  return AllN::info(n, mode, blocked);
+}
 
 }  // namespace crb

@@ -89,7 +89,7 @@ class GeneratorSpec:  # testgen.hpp:13-19 (+ pieces for the BASELINE kinds)
 
 
 @dataclass
-class PapgConfig:  # papg.hpp:7-21 (inner ALCC settings unused in closed form)
+class PapgConfig:  # papg.hpp:7-21 (+ the partition size K of make_partition)
     gamma: float = 1e-3
     B_theta: float = 0.0
     adaptive_B_theta: bool = True
@@ -102,6 +102,8 @@ class PapgConfig:  # papg.hpp:7-21 (inner ALCC settings unused in closed form)
     inner_tol_floor: float = 1e-6
     final_resolve_tol: float = 1e-10
     record_history: bool = True
+    inner: "AlccConfig | None" = None  # block ALCC settings (papg.hpp:19), K < N only
+    K: int = 0                 # blocks (make_partition, dataset.cpp:119); 0 or N: singleton
     # device knobs (not in the reference)
     sigma_C: float = 0.0       # > 0: inject sigma_max(C)
     graph_iters: int = 0       # 0 auto, > 0 graph batch, < 0 direct launches
@@ -274,6 +276,7 @@ class DualSolver:
             raise RuntimeError(msg)
         self.h = h
         self.cfg = None
+        self.K = 0
 
     def close(self):
         if getattr(self, "h", None) is not None and self.h.value:
@@ -400,13 +403,19 @@ class DualSolver:
                                              nat.ptr(out)), self.h)
         return out
 
+    def _dual_len(self):
+        K = getattr(self, "K", 0)
+        if K:
+            return self.N * (self.N - self.N // K) + self.N
+        return (self.row_end - self.row_begin) * (self.N - 1) + self.N
+
     def theta(self):
-        out = np.empty((self.row_end - self.row_begin) * (self.N - 1) + self.N)
+        out = np.empty(self._dual_len())
         _raise(self._L.cr_get_theta(self.h, nat.ptr(out)), self.h)
         return out
 
     def rows(self):
-        out = np.empty((self.row_end - self.row_begin) * (self.N - 1) + self.N)
+        out = np.empty(self._dual_len())
         _raise(self._L.cr_get_rows(self.h, nat.ptr(out)), self.h)
         return out
 
@@ -423,6 +432,26 @@ class DualSolver:
         _raise(self._L.cr_time_sweep(self.h, k, C.byref(s)), self.h)
         return s.value
 
+
+    # ---- general-K partition (P-APG(ALCC), papg.cpp:66-132)
+    def set_partition(self, K, feasible: PrimalPoint, inner: "AlccConfig | None" = None):
+        """K blocks of N/K consecutive points; K = N (or 0) selects singleton blocks."""
+        inner = inner or AlccConfig()
+        c = inner.to_c(ProblemBounds(0.0, 0.0, 0.0, 0.0))
+        _raise(self._L.cr_set_partition(self.h, K, nat.ptr(_f64(feasible.y)),
+                                        nat.ptr(_f64(feasible.xi)), C.byref(c)), self.h)
+        self.K = K if 0 < K < self.N else 0
+
+    def partition_stats(self):
+        K = getattr(self, "K", 0)
+        it = C.c_int64(0)
+        sec = C.c_double(0)
+        s1 = C.c_double(0)
+        s2 = np.zeros(max(K, 1))
+        _raise(self._L.cr_partition_stats(self.h, C.byref(it), C.byref(sec), C.byref(s1),
+                                          nat.ptr(s2)), self.h)
+        return dict(inner_iters=it.value, inner_seconds=sec.value, sigma_A1=s1.value,
+                    sigma_A2=s2[:K].copy())
 
     # ---- standalone ALCC (alcc.cpp:193-208) on this handle's device buffers
     def sigma_A(self, which, tol=1e-6, max_iters=5000):
@@ -485,7 +514,11 @@ def alcc_solve(prep: PreparedProblem, cfg: AlccConfig | None = None,
 
 def _solve(prep: PreparedProblem, cfg: PapgConfig, theta0, use_momentum, want_dual=True):
     data = prep.data
+    N = data.N
     with DualSolver(data.xs, data.ys, cfg.gamma, cfg.device) as s:
+        K = cfg.K if 0 < cfg.K < N else 0
+        if K:
+            s.set_partition(K, prep.feasible, cfg.inner)
         s.begin(cfg, use_momentum, theta0)
         stopped = False
         while not stopped:
@@ -494,8 +527,8 @@ def _solve(prep: PreparedProblem, cfg: PapgConfig, theta0, use_momentum, want_du
         dual = None
         if want_dual:
             th = s.theta()
-            N = data.N
-            dual = DualPoint(th[: N * (N - 1)], th[N * (N - 1):])
+            cross = N * (N - (N // K if K else 1))
+            dual = DualPoint(th[:cross], th[cross:])
     history = [MetricsSnapshot(int(h[0]), *map(float, h[1:])) for h in hist]
     rep = SolveReport(history=history, reason=TermReason(res.reason), iters=int(res.iters),
                       wall_seconds=res.wall_seconds, restarts=res.restarts,
