@@ -14,6 +14,8 @@
 #pragma once
 #include <cstdint>
 #include <cstddef>
+#include <algorithm>
+#include <limits>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -66,6 +68,22 @@ struct GeneratorSpec {  // testgen.hpp:13-19 (+ pieces for the BASELINE kinds)
   Index pieces = 0;
 };
 
+struct AlccConfig {  // alcc.hpp:71-83
+  double mu1 = 1.0;
+  double tau1_scale = 1e-2;
+  double alpha1_scale = 1e-3;
+  double c = 5.0;
+  double kappa = 0.5;
+  Index max_outer = 30;
+  Index mapg_cap = 200000;
+  double infeas_norm_tol = 1e-1;
+  double gap_norm_tol = 1e-6;
+  double max_seconds = std::numeric_limits<double>::infinity();
+  bool record_history = true;
+  // device knobs: inject the spectral norms instead of estimating them
+  double sigma_A1 = 0, sigma_A2 = 0;
+};
+
 struct PapgConfig {  // papg.hpp:7-21
   double gamma = 1e-3;
   double B_theta = 0;
@@ -78,7 +96,10 @@ struct PapgConfig {  // papg.hpp:7-21
   int workers = 0;  // unused: the device replaces the block worker pool
   double inner_tol_floor = 1e-6;
   double final_resolve_tol = 1e-10;
+  AlccConfig inner;  // block QPs of a K < N partition
   bool record_history = true;
+  // the partition (make_partition, dataset.cpp:119): 0 or N = singleton blocks
+  Index K = 0;
   // device knobs
   int device = 0;
   double sigma_C = 0;   // > 0: inject sigma_max(C)
@@ -125,7 +146,38 @@ struct PapgResult {  // papg.hpp:60-69
   double B_theta = 0;
 };
 
+struct AlccResult {  // alcc.hpp:110-118
+  PrimalPoint point;
+  std::vector<double> multiplier;
+  double objective = 0;
+  double certified_gap = 0;
+  double infeas_raw = 0;
+  Index mapg_iters_total = 0;
+  SolveReport report;
+};
+
 namespace detail {
+inline cr_alcc_config to_c(const AlccConfig& a) {
+  cr_alcc_config c{};
+  c.mu1 = a.mu1;
+  c.tau1_scale = a.tau1_scale;
+  c.alpha1_scale = a.alpha1_scale;
+  c.c = a.c;
+  c.kappa = a.kappa;
+  c.max_outer = a.max_outer;
+  c.mapg_cap = a.mapg_cap;
+  c.infeas_norm_tol = a.infeas_norm_tol;
+  c.gap_norm_tol = a.gap_norm_tol;
+  c.max_seconds = a.max_seconds;
+  c.record_history = a.record_history ? 1 : 0;
+  c.sigma_A1 = a.sigma_A1;
+  c.sigma_A2 = a.sigma_A2;
+  return c;
+}
+inline MetricsSnapshot from_c(const cr_snapshot& s) {
+  return {static_cast<Index>(s.iter), s.objective, s.reg_objective, s.infeas_raw,
+          s.infeas_norm, s.gap_raw, s.gap_norm, s.wall_time_s};
+}
 inline void check(cr_status s, const cr_handle* h = nullptr) {
   if (s == CR_OK) return;
   const std::string msg = h ? cr_last_error(h) : cr_status_string(s);
@@ -143,10 +195,17 @@ inline PapgResult solve(const PreparedProblem& prep, const PapgConfig& cfg,
   const Index N = d.N(), n = d.n();
   if (static_cast<Index>(d.xs.size()) != N * n)
     throw std::invalid_argument("papg: xs/ys row count mismatch");
-  if (theta0 && static_cast<Index>(theta0->size()) != N * (N - 1) + N)
+  const Index K = (cfg.K > 0 && cfg.K < N) ? cfg.K : 0;
+  const Index cross = K ? N * (N - N / K) : N * (N - 1);
+  if (theta0 && static_cast<Index>(theta0->size()) != cross + N)
     throw std::invalid_argument("papg: warm-start theta has wrong size");  // papg.cpp:160-161
   Handle hd;
   check(cr_create(d.xs.data(), d.ys.data(), N, n, cfg.gamma, cfg.device, 0, N, &hd.h), hd.h);
+  if (K) {  // P-APG(ALCC) with K blocks (papg.cpp:66-132)
+    const cr_alcc_config inner = to_c(cfg.inner);
+    check(cr_set_partition(hd.h, K, prep.feasible.y.data(), prep.feasible.xi.data(), &inner),
+          hd.h);
+  }
   cr_papg_config c{};
   c.gamma = cfg.gamma;
   c.B_theta = cfg.B_theta;
@@ -170,21 +229,17 @@ inline PapgResult solve(const PreparedProblem& prep, const PapgConfig& cfg,
   check(cr_papg_solve(hd.h, &c, theta0 ? theta0->data() : nullptr, &r, out.point.y.data(),
                       out.point.xi.data(), hist.empty() ? nullptr : hist.data()),
         hd.h);
-  std::vector<double> th(static_cast<size_t>(N * (N - 1) + N));
+  std::vector<double> th(static_cast<size_t>(cross + N));
   check(cr_get_theta(hd.h, th.data()), hd.h);
-  out.dual.theta_cross.assign(th.begin(), th.begin() + N * (N - 1));
-  out.dual.theta_pos.assign(th.begin() + N * (N - 1), th.end());
+  out.dual.theta_cross.assign(th.begin(), th.begin() + cross);
+  out.dual.theta_pos.assign(th.begin() + cross, th.end());
   out.report.reason = static_cast<TermReason>(r.reason);
   out.report.iters = r.iters;
   out.report.wall_seconds = r.wall_seconds;
   out.report.restarts = r.restarts;
   out.report.saturated = r.saturated != 0;
-  for (Index i = 0; i < r.iters && i < static_cast<Index>(hist.size()); ++i) {
-    const cr_snapshot& s = hist[static_cast<size_t>(i)];
-    out.report.history.push_back({static_cast<Index>(s.iter), s.objective, s.reg_objective,
-                                  s.infeas_raw, s.infeas_norm, s.gap_raw, s.gap_norm,
-                                  s.wall_time_s});
-  }
+  for (Index i = 0; i < r.iters && i < static_cast<Index>(hist.size()); ++i)
+    out.report.history.push_back(from_c(hist[static_cast<size_t>(i)]));
   out.g_final = r.g_final;
   out.delta_estimate = r.delta_estimate;
   out.sigma_C = r.sigma_C;
@@ -268,6 +323,43 @@ inline PrimalPoint repair_feasibility(const PrimalPoint& eta, const Dataset& dat
                 hd.h);
   PrimalPoint out = eta;
   detail::check(cr_repair_feasibility(hd.h, eta.y.data(), eta.xi.data(), out.y.data()), hd.h);
+  return out;
+}
+
+// standalone ALCC (alcc.cpp:193-208): centres (ybar, 0), balls from prep.bounds
+inline AlccResult alcc_solve(const PreparedProblem& prep, const AlccConfig& cfg,
+                             const PrimalPoint& warm, int device = 0) {
+  const Dataset& d = prep.data;
+  const Index N = d.N(), n = d.n();
+  detail::Handle hd;
+  detail::check(cr_create(d.xs.data(), d.ys.data(), N, n, prep.bounds.gamma, device, 0, N,
+                          &hd.h),
+                hd.h);
+  cr_alcc_config c = detail::to_c(cfg);
+  c.Bbar_y = prep.bounds.Bbar_y;
+  c.Bbar_xi = prep.bounds.Bbar_xi;
+  AlccResult out;
+  out.point.y.resize(static_cast<size_t>(N));
+  out.point.xi.resize(static_cast<size_t>(N * n));
+  std::vector<cr_snapshot> hist(static_cast<size_t>(std::max<Index>(cfg.max_outer, 1)));
+  cr_alcc_result r{};
+  detail::check(cr_alcc_solve(hd.h, &c, warm.y.data(), warm.xi.data(), out.point.y.data(),
+                              out.point.xi.data(), hist.data(), nullptr, &r),
+                hd.h);
+  if (r.outer_iters > 0) {
+    out.multiplier.resize(static_cast<size_t>(N * (N - 1)));
+    detail::check(cr_alcc_multiplier(hd.h, 0, N, out.multiplier.data()), hd.h);
+  }
+  out.objective = r.objective;
+  out.certified_gap = r.certified_gap;
+  out.infeas_raw = r.infeas_raw;
+  out.mapg_iters_total = r.mapg_iters_total;
+  out.report.reason = static_cast<TermReason>(r.reason);
+  out.report.iters = r.outer_iters;
+  out.report.wall_seconds = r.wall_seconds;
+  if (cfg.record_history)
+    for (Index k = 0; k < r.outer_iters; ++k)
+      out.report.history.push_back(detail::from_c(hist[static_cast<size_t>(k)]));
   return out;
 }
 

@@ -1,7 +1,11 @@
 // dropin_demo.cpp -- exercises the C++ drop-in (include/cvxreg_b200/papg.hpp)
-// the way a reference caller would (runner.cpp:306-308 calls papg_solve).
-// in:  [N, n, iters, sigma_C, X (N*n, row-major), ys_shifted (N)] as float64
-// out: [iters, y (N), theta (N(N-1)+N)] as float64
+// the way a reference caller would (runner.cpp:278-308 calls papg_solve /
+// alcc_solve).
+// in:  [N, n, iters, sigma_C, K, mode, X (N*n, row-major), ys_shifted (N),
+//       feas_y (N), feas_xi (N*n), B_theta, Bbar_y, Bbar_xi, gamma] as float64
+//       mode 0: papg_solve with K blocks (0: singleton), iters dual iterations
+//       mode 1: alcc_solve from the feasible point, iters outer steps
+// out: [iters, y (N), theta (papg) or multiplier (alcc)] as float64
 #include <cstdio>
 #include <fstream>
 #include <iostream>
@@ -9,41 +13,70 @@
 
 #include "cvxreg_b200/papg.hpp"
 
+namespace b2 = cvxreg::b200;
+
 int main(int argc, char** argv) {
   if (argc != 3) {
     std::cerr << "usage: dropin_demo in.bin out.bin\n";
     return 2;
   }
   std::ifstream in(argv[1], std::ios::binary);
-  std::vector<double> head(4);
-  in.read(reinterpret_cast<char*>(head.data()), 4 * sizeof(double));
-  const auto N = static_cast<cvxreg::b200::Index>(head[0]);
-  const auto n = static_cast<cvxreg::b200::Index>(head[1]);
-  cvxreg::b200::PreparedProblem prep;
+  std::vector<double> head(6);
+  in.read(reinterpret_cast<char*>(head.data()), 6 * sizeof(double));
+  const auto N = static_cast<b2::Index>(head[0]);
+  const auto n = static_cast<b2::Index>(head[1]);
+  const auto iters = static_cast<b2::Index>(head[2]);
+  const auto K = static_cast<b2::Index>(head[4]);
+  const int mode = static_cast<int>(head[5]);
+  b2::PreparedProblem prep;
+  auto rd = [&](std::vector<double>& v, size_t count) {
+    v.resize(count);
+    in.read(reinterpret_cast<char*>(v.data()), count * sizeof(double));
+  };
   prep.data.n_ = n;
-  prep.data.xs.resize(static_cast<size_t>(N * n));
-  prep.data.ys.resize(static_cast<size_t>(N));
-  in.read(reinterpret_cast<char*>(prep.data.xs.data()), prep.data.xs.size() * sizeof(double));
-  in.read(reinterpret_cast<char*>(prep.data.ys.data()), prep.data.ys.size() * sizeof(double));
-  cvxreg::b200::PapgConfig cfg;
-  cfg.max_iters = static_cast<cvxreg::b200::Index>(head[2]);
-  cfg.sigma_C = head[3];
-  cfg.gap_norm_tol = -1.0;
-  cfg.infeas_norm_tol = -1.0;
+  rd(prep.data.xs, static_cast<size_t>(N * n));
+  rd(prep.data.ys, static_cast<size_t>(N));
+  rd(prep.feasible.y, static_cast<size_t>(N));
+  rd(prep.feasible.xi, static_cast<size_t>(N * n));
+  std::vector<double> b;
+  rd(b, 4);
+  prep.bounds = {b[0], b[1], b[2], b[3]};
   try {
-    const cvxreg::b200::PapgResult r = cvxreg::b200::papg_solve(prep, cfg);
     std::ofstream out(argv[2], std::ios::binary);
-    const double iters = static_cast<double>(r.report.iters);
-    out.write(reinterpret_cast<const char*>(&iters), sizeof(double));
-    out.write(reinterpret_cast<const char*>(r.point.y.data()), r.point.y.size() * sizeof(double));
-    out.write(reinterpret_cast<const char*>(r.dual.theta_cross.data()),
-              r.dual.theta_cross.size() * sizeof(double));
-    out.write(reinterpret_cast<const char*>(r.dual.theta_pos.data()),
-              r.dual.theta_pos.size() * sizeof(double));
-    std::printf("papg_solve: %lld iterations, reason %s\n", static_cast<long long>(r.report.iters),
-                cvxreg::b200::to_string(r.report.reason).c_str());
+    auto put = [&](const std::vector<double>& v) {
+      out.write(reinterpret_cast<const char*>(v.data()), v.size() * sizeof(double));
+    };
+    if (mode == 0) {
+      b2::PapgConfig cfg;
+      cfg.max_iters = iters;
+      cfg.sigma_C = head[3];
+      cfg.gap_norm_tol = -1.0;
+      cfg.infeas_norm_tol = -1.0;
+      cfg.K = K;
+      cfg.inner.max_outer = 6;
+      cfg.inner.mapg_cap = 1000;
+      const b2::PapgResult r = b2::papg_solve(prep, cfg);
+      put({static_cast<double>(r.report.iters)});
+      put(r.point.y);
+      put(r.dual.theta_cross);
+      put(r.dual.theta_pos);
+      std::printf("papg_solve (K=%lld): %lld iterations, reason %s\n", static_cast<long long>(K),
+                  static_cast<long long>(r.report.iters), b2::to_string(r.report.reason).c_str());
+    } else {
+      b2::AlccConfig cfg;
+      cfg.max_outer = iters;
+      cfg.mapg_cap = 1000;
+      const b2::AlccResult r = b2::alcc_solve(prep, cfg, prep.feasible);
+      put({static_cast<double>(r.report.iters)});
+      put(r.point.y);
+      put(r.multiplier);
+      std::printf("alcc_solve: %lld outer steps, %lld MAPG iterations, reason %s\n",
+                  static_cast<long long>(r.report.iters),
+                  static_cast<long long>(r.mapg_iters_total),
+                  b2::to_string(r.report.reason).c_str());
+    }
   } catch (const std::exception& e) {
-    std::cerr << "papg_solve failed: " << e.what() << "\n";
+    std::cerr << "solve failed: " << e.what() << "\n";
     return 1;
   }
   return 0;

@@ -294,21 +294,56 @@ def test_full_size_properties(kind, N, n, noise, pieces, iters):
     assert infeas == pytest.approx(h[-1, 3], rel=1e-9)
 
 
-def test_cpp_dropin_binary(oracle, tmp_path):
+def _demo_input(oracle, tmp_path, X, y, iters, sigma, K, mode):
+    P = oracle.prepare(X, y)
+    inp = tmp_path / f"in{K}_{mode}.bin"
+    np.concatenate([[X.shape[0], X.shape[1], iters, sigma, K, mode], X.reshape(-1), P.ys,
+                    P.feas_y, P.feas_xi, [P.B_theta, P.Bbar_y, P.Bbar_xi, P.gamma]]
+                   ).astype(np.float64).tofile(inp)
+    return P, inp
+
+
+def _run_demo(inp, tmp_path):
     exe = os.path.join(ROOT, "paper_1407_7220_b200", "cxx_dropin_demo")
     assert os.path.exists(exe), "built by __graft_entry__.build()"
-    X, ys = instance(oracle, "maxaffine-uniform", 240, 5, 0.1, 3, 8)
-    s, _, _ = oracle.sigma_C(X)
-    inp = tmp_path / "in.bin"
     out = tmp_path / "out.bin"
-    np.concatenate([[X.shape[0], X.shape[1], 50, s], X.reshape(-1), ys]).astype(np.float64).tofile(inp)
     subprocess.run([exe, str(inp), str(out)], check=True)
-    res = np.fromfile(out, dtype=np.float64)
+    return np.fromfile(out, dtype=np.float64)
+
+
+def test_cpp_dropin_binary(oracle, tmp_path):
+    X, y = oracle.gen_instance("maxaffine-uniform", 240, 5, 0.1, 3, 8)
+    s, _, _ = oracle.sigma_C(X)
+    P, inp = _demo_input(oracle, tmp_path, X, y, 50, s, 0, 0)
+    res = _run_demo(inp, tmp_path)
     N = X.shape[0]
-    iters, y, theta = int(res[0]), res[1:1 + N], res[1 + N:]
-    o = oracle_run(oracle, X, ys, max_iters=50, gap_norm_tol=-1.0, infeas_norm_tol=-1.0, sigma_C=s)
+    iters, yy, theta = int(res[0]), res[1:1 + N], res[1 + N:]
+    o = oracle_run(oracle, X, P.ys, max_iters=50, gap_norm_tol=-1.0, infeas_norm_tol=-1.0,
+                   sigma_C=s)
     assert iters == o.iters
-    assert rel(theta, o.theta) <= TOL_THETA and rel(y, o.y) <= TOL_Y
+    assert rel(theta, o.theta) <= TOL_THETA and rel(yy, o.y) <= TOL_Y
+
+
+def test_cpp_dropin_general_k_and_alcc(oracle, tmp_path):
+    """papg_solve with a K-block partition and alcc_solve through the C++ drop-in"""
+    X, y = oracle.gen_instance("sqnorm-uniform", 36, 2, 0.2, 5)
+    K = 3
+    s = oracle.sigma_C_k(X, K)[0]
+    P, inp = _demo_input(oracle, tmp_path, X, y, 3, s, K, 0)
+    res = _run_demo(inp, tmp_path)
+    N = 36
+    o = oracle.papg_k(X, P.ys, K, P.feas_y, P.feas_xi, inner=dict(max_outer=6, mapg_cap=1000),
+                      sigma_C=s, max_iters=3, gap_norm_tol=-1.0, infeas_norm_tol=-1.0)
+    assert int(res[0]) == o.iters
+    assert rel(res[1 + N:], o.theta) <= 1e-9 and rel(res[1:1 + N], o.y) <= 1e-8
+    P, inp = _demo_input(oracle, tmp_path, X, y, 4, 0.0, 0, 1)
+    res = _run_demo(inp, tmp_path)
+    oa = oracle.alcc(X, P.ys, gamma=P.gamma, Bbar_y=P.Bbar_y, Bbar_xi=P.Bbar_xi,
+                     warm_y=P.feas_y, warm_xi=P.feas_xi, max_outer=4, mapg_cap=1000,
+                     want_multiplier=True)
+    assert int(res[0]) == oa.outer_iters
+    assert rel(res[1:1 + N], oa.y) <= 1e-9
+    assert rel(res[1 + N:], oa.multiplier) <= 1e-6
 
 
 def test_nccl_attached_single_rank(oracle):
