@@ -50,9 +50,11 @@ def parse():
     ap.add_argument("--config", choices=sorted(CONFIGS), default="cfg2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true", help="skip time-to-tolerance and e2e")
-    ap.add_argument("--solver", choices=["papg", "alcc"], default="papg",
+    ap.add_argument("--solver", choices=["papg", "alcc", "papg-alcc"], default="papg",
                     help="papg: the north-star P-APG step (default); alcc: one MAPG iteration "
-                         "of the standalone ALCC (SURVEY 8f row f1)")
+                         "of the standalone ALCC (SURVEY 8f row f1); papg-alcc: one dual "
+                         "iteration of the general-K P-APG(ALCC) (row f2)")
+    ap.add_argument("--K", type=int, default=2, help="blocks for --solver papg-alcc")
     return ap.parse_args()
 
 
@@ -484,8 +486,92 @@ def run_alcc_ours(args):
     return 0
 
 
+# f2 workload: the reference's default solver (K = 2) with a bounded inner ALCC so a
+# step is a fixed amount of work on both arms (identical inner iteration counts)
+GEN_INNER = dict(max_outer=5, mapg_cap=200)
+
+
+def run_general(args, impl):
+    if int(os.environ.get("RANK", "0")) != 0:
+        return 0
+    cfg = workload(args.config, 1)
+    N, n, K = cfg["N"], cfg["n"], args.K
+    K_steps = max(1, min(args.steps, 5)) if impl == "reference" else max(1, args.steps)
+    line_cfg = {"workload": f"papg-alcc {args.config}: {cfg['kind']} N={N} n={n} K={K} "
+                            f"(inner ALCC max_outer={GEN_INNER['max_outer']}, "
+                            f"mapg_cap={GEN_INNER['mapg_cap']})",
+                "N": N, "n": n, "K": K, "solver": "papg-alcc"}
+    if impl == "reference":
+        from oracle import oracle as O
+        X, y = O.gen_instance(cfg["kind"], N, n, cfg["noise"], 1, cfg["pieces"])
+        p = O.prepare(X, y)
+        threads = os.cpu_count() or 1
+        sig = 300.0  # the step size does not change the cost of an iteration
+        kw = dict(inner=GEN_INNER, sigma_C=sig, gap_norm_tol=-1.0, infeas_norm_tol=-1.0,
+                  record_history=False, inner_threads=threads)
+        a = O.papg_k(X, p.ys, K, p.feas_y, p.feas_xi, max_iters=1, **kw)
+        b = O.papg_k(X, p.ys, K, p.feas_y, p.feas_xi, max_iters=1 + K_steps, **kw)
+        per = max(b.wall_seconds - a.wall_seconds, 1e-9) / K_steps
+        rate = 1.0 / per
+        sample = (f"oracle papg_k (papg.cpp + alcc.cpp restated), runs of 1 and {1 + K_steps} "
+                  f"dual iterations, blocks sequential, {threads} thread(s) per block solve, "
+                  f"{per:.3f} s/iteration")
+        line = {"impl": "reference", "metric": "P-APG(ALCC) dual iterations/s", "value": rate,
+                "unit": "iterations/s", "n_gpus": args.gpus, "steps": K_steps, "warmup": 1,
+                "ms_per_step": per * 1e3, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": line_cfg,
+                "cpu_baseline": {"value": rate, "unit": "iterations/s", "cores": threads,
+                                 "kind": "port", "sample": sample},
+                "e2e": {"value": rate, "unit": "iterations/s", "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return 0
+    import torch
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    import paper_1407_7220_b200 as crb
+    data = crb.gen_instance(crb.GeneratorSpec(cfg["kind"], n, N, cfg["noise"], 1, cfg["pieces"]))
+    prep = crb.prepare_problem(data)
+    inner = crb.AlccConfig(**GEN_INNER)
+    W = max(args.warmup, 3) if args.warmup else 3
+    with crb.DualSolver(prep.data.xs, prep.data.ys, prep.bounds.gamma, local) as s:
+        s.set_partition(K, prep.feasible, inner)
+        sig = s.sigma_C()
+        pc = crb.PapgConfig(K=K, inner=inner, max_iters=W + K_steps + 4, gap_norm_tol=-1.0,
+                            infeas_norm_tol=-1.0, sigma_C=sig[0], device=local)
+        s.begin(pc)
+        s.iterate(W)
+        st0 = s.partition_stats()
+        with ClockSampler(local) as clk:
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            done, stopped = s.iterate(K_steps)
+            torch.cuda.synchronize()
+            wall = time.perf_counter() - t0
+        st1 = s.partition_stats()
+        sec, launches, sweep_s = s.last_timing()
+    inner_it = st1["inner_iters"] - st0["inner_iters"]
+    nb = N // K
+    pairs = K_steps * N * (N - nb) + inner_it * nb * nb
+    line = {"metric": "P-APG(ALCC) dual iterations/s", "value": K_steps / wall,
+            "unit": "iterations/s", "n_gpus": 1, "steps": K_steps, "warmup": W,
+            "ms_per_step": wall / K_steps * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded BASELINE generator)",
+            "config": dict(line_cfg, sigma_C=sig[0], inner_mapg_iterations=inner_it,
+                           pair_evaluations=pairs, pair_evals_per_s=pairs / wall,
+                           cross_sweep_seconds=sweep_s,
+                           timing="host wall clock around device-synchronised iterations "
+                                  "(host-driven block solves)"),
+            "roofline": None, "cpu_baseline": None, "gpu_launches": None,
+            "clocks": clk.summary()}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def main():
     args = parse()
+    if args.solver == "papg-alcc":
+        return run_general(args, args.impl)
     if args.solver == "alcc":
         return run_alcc_reference(args) if args.impl == "reference" else run_alcc_ours(args)
     if args.impl == "reference":

@@ -69,7 +69,7 @@ typedef struct {
   int32_t use_momentum;     /* 1: papg_solve, 0: dual_gradient_ascent */
   double sigma_C;           /* > 0: use this sigma_max(C) instead of estimating it */
   int32_t graph_iters;      /* iterations per CUDA graph launch; <= 0: auto */
-  int32_t pad_;
+  int32_t workers;          /* K-block partition: concurrent block solves; <= 0: 16 */
 } cr_papg_config;
 
 /* one MetricsSnapshot (metrics.hpp:13-22) */

@@ -93,7 +93,7 @@ struct PapgConfig {  // papg.hpp:7-21
   double infeas_norm_tol = 1e-1;
   Index max_iters = 100000;
   double max_seconds = 7200;
-  int workers = 0;  // unused: the device replaces the block worker pool
+  int workers = 0;  // concurrent block solves of a K-block partition (<= 0: 16)
   double inner_tol_floor = 1e-6;
   double final_resolve_tol = 1e-10;
   AlccConfig inner;  // block QPs of a K < N partition
@@ -221,6 +221,7 @@ inline PapgResult solve(const PreparedProblem& prep, const PapgConfig& cfg,
   c.use_momentum = momentum ? 1 : 0;
   c.sigma_C = cfg.sigma_C;
   c.graph_iters = cfg.graph_iters;
+  c.workers = cfg.workers;
   PapgResult out;
   out.point.y.resize(static_cast<size_t>(N));
   out.point.xi.resize(static_cast<size_t>(N * n));

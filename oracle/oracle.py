@@ -418,7 +418,7 @@ def papg_k(X, ys, K, feas_y, feas_xi, *, inner=None, gamma=1e-3, B_theta=0.0,
            adaptive_B_theta=True, max_restarts=6, gap_norm_tol=1e-6, infeas_norm_tol=1e-1,
            max_iters=100000, max_seconds=7200.0, inner_tol_floor=1e-6, final_resolve_tol=1e-10,
            record_history=True, use_momentum=True, sigma_C=0.0, threads=1, theta0=None,
-           want_c_eta=False):
+           want_c_eta=False, inner_threads=1):
     """General-K P-APG(ALCC) (papg.cpp:136-283, dual_gradient :89-132,
     alcc_solve_block alcc.cpp:222-258)."""
     X = _c(X)
@@ -433,7 +433,8 @@ def papg_k(X, ys, K, feas_y, feas_xi, *, inner=None, gamma=1e-3, B_theta=0.0,
     ic.update(inner or {})
     icfg = CroAlccConfig(ic["mu1"], ic["tau1_scale"], ic["alpha1_scale"], ic["c"], ic["kappa"],
                          ic["max_outer"], ic["mapg_cap"], ic["infeas_norm_tol"],
-                         ic["gap_norm_tol"], ic["max_seconds"], int(ic["record_history"]), 1)
+                         ic["gap_norm_tol"], ic["max_seconds"], int(ic["record_history"]),
+                         inner_threads)
     y = np.empty(N)
     xi = np.empty(N * n)
     theta = np.empty(dim)

@@ -25,7 +25,7 @@ class PapgConfigC(C.Structure):
         ("max_iters", C.c_int64), ("max_seconds", C.c_double),
         ("inner_tol_floor", C.c_double), ("final_resolve_tol", C.c_double),
         ("record_history", C.c_int32), ("use_momentum", C.c_int32),
-        ("sigma_C", C.c_double), ("graph_iters", C.c_int32), ("pad_", C.c_int32),
+        ("sigma_C", C.c_double), ("graph_iters", C.c_int32), ("workers", C.c_int32),
     ]
 
 

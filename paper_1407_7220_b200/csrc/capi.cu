@@ -642,6 +642,7 @@ cr_status begin_impl(cr_handle* h, const cr_papg_config* cfg, const double* thet
   // batch size: graphs when an iteration is short, direct launches otherwise
   if (h->part.K > 0) {
     h->graph_iters = 0;  // host-driven (block solves between the kernels)
+    h->part.workers = cfg->workers;
     const cr_status s = general_begin(h);
     if (s != CR_OK) return s;
   } else if (cfg->graph_iters > 0) {

@@ -20,10 +20,12 @@
 #include <math.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <climits>
 #include <cmath>
 #include <cstring>
+#include <thread>
 #include <vector>
 
 #include "handle.cuh"
@@ -268,23 +270,49 @@ cr_status solve_blocks(cr_handle* h, double tol, double* within) {
   CUDA_TRY(cudaStreamSynchronize(h->st));  // centres ready
   const auto t0 = std::chrono::steady_clock::now();
   const int64_t nb = P.nbar, n = h->n;
-  double sq = 0;
-  for (int64_t b = 0; b < P.K; ++b) {
+  std::vector<cr_status> st((size_t)P.K, CR_OK);
+  std::vector<cr_alcc_result> rs((size_t)P.K);
+  // one block solve per worker on its own handle/stream (parallel_blocks,
+  // papg.cpp:29-58): independent tasks writing their own slots
+  auto task = [&](int64_t b) {
     cr_handle* hb = P.blocks[(size_t)b];
-    cr_alcc_result r;
+    cr_alcc_result& r = rs[(size_t)b];
     std::memset(&r, 0, sizeof(r));
-    const cr_status s = alcc_run(hb, &P.inner, P.sigma_A1, P.sigma_A2[(size_t)b], tol, true,
-                                 nullptr, nullptr, &r);
-    if (s != CR_OK) return fail(h, s, "block " + std::to_string(b) + ": " + hb->err);
-    CUDA_TRY(cudaMemcpyAsync(P.ey + b * nb, hb->alcc.p1, sizeof(double) * nb,
-                             cudaMemcpyDeviceToDevice, hb->st));
-    CUDA_TRY(cudaMemcpyAsync(P.exi + b * nb * n, hb->alcc.p1 + nb, sizeof(double) * nb * n,
-                             cudaMemcpyDeviceToDevice, hb->st));
+    cudaSetDevice(hb->device);
+    cr_status s = alcc_run(hb, &P.inner, P.sigma_A1, P.sigma_A2[(size_t)b], tol, true, nullptr,
+                           nullptr, &r);
+    if (s == CR_OK) {
+      cudaError_t e = cudaMemcpyAsync(P.ey + b * nb, hb->alcc.p1, sizeof(double) * nb,
+                                      cudaMemcpyDeviceToDevice, hb->st);
+      if (e == cudaSuccess)
+        e = cudaMemcpyAsync(P.exi + b * nb * n, hb->alcc.p1 + nb, sizeof(double) * nb * n,
+                            cudaMemcpyDeviceToDevice, hb->st);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(hb->st);
+      if (e != cudaSuccess) s = fail(hb, CR_ECUDA, cudaGetErrorString(e));
+    }
+    st[(size_t)b] = s;
+  };
+  const int64_t workers = std::min<int64_t>(P.K, P.workers > 0 ? P.workers : 16);
+  if (workers <= 1) {
+    for (int64_t b = 0; b < P.K; ++b) task(b);
+  } else {
+    std::atomic<int64_t> next{0};
+    std::vector<std::thread> pool;
+    for (int64_t w = 0; w < workers; ++w)
+      pool.emplace_back([&]() {
+        for (int64_t b; (b = next.fetch_add(1)) < P.K;) task(b);
+      });
+    for (auto& t : pool) t.join();
+  }
+  double sq = 0;
+  for (int64_t b = 0; b < P.K; ++b) {  // gathered in block order (papg.cpp:124-128)
+    if (st[(size_t)b] != CR_OK)
+      return fail(h, st[(size_t)b], "block " + std::to_string(b) + ": " + P.blocks[(size_t)b]->err);
+    const cr_alcc_result& r = rs[(size_t)b];
     P.block_infeas[(size_t)b] = r.infeas_raw;
-    sq += r.infeas_raw * r.infeas_raw;  // papg.cpp:118, :125-128
+    sq += r.infeas_raw * r.infeas_raw;
     P.inner_iters += r.mapg_iters_total;
   }
-  for (cr_handle* hb : P.blocks) CUDA_TRY(cudaStreamSynchronize(hb->st));
   P.inner_seconds += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   *within = std::sqrt(sq);
   return CR_OK;

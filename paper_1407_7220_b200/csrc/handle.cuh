@@ -49,6 +49,7 @@ struct Partition {
   double *fy = nullptr, *fxi = nullptr;      // feasible affine point (prepare_problem)
   int64_t inner_iters = 0;
   double inner_seconds = 0;
+  int workers = 0;                     // concurrent block solves (PapgConfig::workers); 0: 16
 };
 }  // namespace crb
 

@@ -114,7 +114,8 @@ class PapgConfig:  # papg.hpp:7-21 (+ the partition size K of make_partition)
                                self.max_restarts, self.gap_norm_tol, self.infeas_norm_tol,
                                int(self.max_iters), self.max_seconds, self.inner_tol_floor,
                                self.final_resolve_tol, int(self.record_history),
-                               int(use_momentum), self.sigma_C, self.graph_iters, 0)
+                               int(use_momentum), self.sigma_C, self.graph_iters,
+                               int(self.workers))
 
 
 @dataclass
