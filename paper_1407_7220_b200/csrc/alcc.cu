@@ -24,18 +24,21 @@
 // One outer step (alcc.cpp:124-183) = records(y1) + kModePenaltyUpdate sweep
 // (stats + theta_{k+1}) + reduce + one stats block; the scalar logic runs on
 // the host exactly as in the reference.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <math.h>
 
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
 #include "handle.cuh"
 #include "host.hpp"
 #include "iteration.cuh"
+#include "pipeline.cuh"
 
 namespace crb {
 
@@ -386,6 +389,225 @@ __global__ void multiplier_out_kernel(double* stage, const double* V, double mu,
   }
 }
 
+// ---- small sub-problems: the whole MAPG call in one cooperative launch --------
+// For N up to a few thousand points (general-K blocks, config 1) an MAPG
+// iteration is a few microseconds of work and the 4-launch graph is bound by
+// launch latency. Here one launch runs engines.cpp:69-106 to its stop with
+// three grid barriers per iteration:
+//   A  penalty sweep: warp per (32-column strip, row chunk), v = max(theta -
+//      row, 0), column partials [N][n+1][P] and row-sum partials [N][S]
+//   B  warp per point: fixed-order partial sums (lanes over partials), the
+//      gradient step y1 = y2 - grad / L, block partials of the ball distances
+//   C  every block sums the distance partials in the same order (identical
+//      projection decisions), projection, displacement, momentum, records
+//   D  every block sums the displacement partials -> identical stop decision
+namespace cgx = cooperative_groups;
+constexpr int kLBlock = 256;
+
+struct LoopArgs {
+  AlccArgs a;
+  const double* V0;
+  const double* V1;
+  double* colpart;  // [N][n+1][P]
+  double* rowpart;  // [N][S]
+  double* partB;    // [G][3]: |y1 - c_y|^2, |xi1 - c_xi|^2, non-finite count
+  double* partC;    // [G][2]: displacement^2 (y, xi)
+  long long ld;
+  int S, P;
+};
+
+template <int W>
+__device__ __forceinline__ void grid_sum(const double* part, int G, double (&out)[W]) {
+  double v[W];
+#pragma unroll
+  for (int w = 0; w < W; ++w) v[w] = 0.0;
+  for (int g = threadIdx.x; g < G; g += kLBlock) {
+#pragma unroll
+    for (int w = 0; w < W; ++w) v[w] += __ldcg(part + (long long)g * W + w);
+  }
+  block_sum_all<W, kLBlock>(v);
+#pragma unroll
+  for (int w = 0; w < W; ++w) out[w] = v[w];
+}
+
+template <int NN>
+__global__ void __launch_bounds__(kLBlock) mapg_loop_kernel(const LoopArgs L) {
+  constexpr int RP = rec_pitch(NN);
+  cgx::grid_group grid = cgx::this_grid();
+  const AlccArgs& a = L.a;
+  AlccDev* d = a.d;
+  const long long N = a.N;
+  const long long tid = (long long)blockIdx.x * kLBlock + threadIdx.x;
+  const long long nthreads = (long long)gridDim.x * kLBlock;
+  const int lane = threadIdx.x & 31;
+  const long long gwarp = tid >> 5, nwarps = nthreads >> 5;
+  const int G = gridDim.x;
+  const double* th = d->cur ? L.V1 : L.V0;
+  const double mu = d->mu, gm = d->gamma / d->mu, Ly = d->L_y, Lx = d->L_xi;
+  const double ay = d->alpha_y, ax = d->alpha_xi, By = d->Bbar_y, Bx = d->Bbar_xi;
+  const long long lmax = d->lmax;
+  double t = d->t;
+  long long ell = d->ell;
+  bool hit = false, bad = false;
+  double disp_y = 0.0, disp_x = 0.0;
+  while (ell < lmax) {
+    // ---- A: penalty sweep partials
+    for (long long w = gwarp; w < (long long)L.S * L.P; w += nwarps) {
+      const int strip = (int)(w % L.S);
+      const int chunk = (int)(w / L.S);
+      const long long rlo = N * chunk / L.P, rhi = N * (chunk + 1) / L.P;
+      const long long col = (long long)strip * 32 + lane;
+      const bool valid = col < N;
+      const double* cr = a.colrec + (valid ? col : 0) * RP;
+      double xi[NN], acc[NN + 1];
+      const double cc = valid ? __ldcg(cr + NN) : 0.0;
+#pragma unroll
+      for (int j = 0; j < NN; ++j) xi[j] = valid ? __ldcg(cr + j) : 0.0;
+#pragma unroll
+      for (int j = 0; j <= NN; ++j) acc[j] = 0.0;
+      for (long long r = rlo; r < rhi; ++r) {
+        const double* xr = a.rowrec + r * RP;
+        double x[NN];
+#pragma unroll
+        for (int j = 0; j < NN; ++j) x[j] = __ldcg(xr + j);
+        double row = __ldcg(xr + NN + 1) + cc;
+#pragma unroll
+        for (int j = 0; j < NN; ++j) row = fma(x[j], xi[j], row);
+        if (!valid || col == r) row = 0.0;
+        const double tv = valid ? __ldg(th + r * L.ld + col) : 0.0;
+        const double v = keep_if_nonneg(tv - row);
+        acc[0] += v;
+#pragma unroll
+        for (int j = 0; j < NN; ++j) acc[1 + j] = fma(v, x[j], acc[1 + j]);
+        double rs = v;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) rs += __shfl_xor_sync(0xffffffffu, rs, o);
+        if (lane == 0) __stcg(L.rowpart + r * L.S + strip, rs);
+      }
+      if (valid) {
+        double* dst = L.colpart + (col * (NN + 1)) * L.P + chunk;
+#pragma unroll
+        for (int j = 0; j <= NN; ++j) __stcg(dst + (long long)j * L.P, acc[j]);
+      }
+    }
+    grid.sync();
+    // ---- B: reduce per point + gradient step
+    {
+      double pb[3] = {0.0, 0.0, 0.0};
+      for (long long l = gwarp; l < N; l += nwarps) {
+        double rs = 0.0;
+        for (int sidx = lane; sidx < L.S; sidx += 32) rs += __ldcg(L.rowpart + l * L.S + sidx);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) rs += __shfl_xor_sync(0xffffffffu, rs, o);
+        double ca[NN + 1];
+#pragma unroll
+        for (int j = 0; j <= NN; ++j) {
+          double sj = 0.0;
+          const double* src = L.colpart + (l * (NN + 1) + j) * L.P;
+          for (int p = lane; p < L.P; p += 32) sj += __ldcg(src + p);
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) sj += __shfl_xor_sync(0xffffffffu, sj, o);
+          ca[j] = sj;
+        }
+        if (lane == 0) {
+          const double cs = ca[0];
+          const double y2 = __ldcg(a.p2 + l);
+          const double gy = (y2 - a.cy[l]) / mu - (rs - cs);
+          bool b = !isfinite(gy);
+          const double y1 = y2 - gy / Ly;
+          __stcg(a.p1p + l, __ldcg(a.p1 + l));
+          __stcg(a.p1 + l, y1);
+          const double dy = y1 - a.cy[l];
+          pb[0] = fma(dy, dy, pb[0]);
+#pragma unroll
+          for (int j = 0; j < NN; ++j) {
+            const long long k = N + l * NN + j;
+            const double adj = cs * a.X[l * NN + j] - ca[1 + j];
+            const double c = cxi_at(a, l * NN + j);
+            const double g = gm * (__ldcg(a.p2 + k) - c) - adj;
+            b |= !isfinite(g);
+            const double x1 = __ldcg(a.p2 + k) - g / Lx;
+            __stcg(a.p1p + k, __ldcg(a.p1 + k));
+            __stcg(a.p1 + k, x1);
+            const double dx = x1 - c;
+            pb[1] = fma(dx, dx, pb[1]);
+          }
+          if (b) pb[2] += 1.0;
+        }
+      }
+      block_sum_all<3, kLBlock>(pb);
+      if (threadIdx.x == 0) {
+        for (int w = 0; w < 3; ++w) __stcg(L.partB + (long long)blockIdx.x * 3 + w, pb[w]);
+      }
+    }
+    grid.sync();
+    // ---- C: projections, displacements, momentum, records
+    double dist[3];
+    grid_sum<3>(L.partB, G, dist);
+    bad = dist[2] != 0.0;
+    {
+      const double dy = sqrt(dist[0]), dx = sqrt(dist[1]);
+      const bool sy = dy > By, sx = dx > Bx;
+      const double fy = sy ? By / dy : 1.0, fx = sx ? Bx / dx : 1.0;
+      const double t_next = 0.5 * (1.0 + sqrt(1.0 + 4.0 * t * t));
+      const double beta = (t - 1.0) / t_next;
+      double pc[2] = {0.0, 0.0};
+      for (long long l = tid; l < N; l += nthreads) {
+        double y1 = __ldcg(a.p1 + l);
+        if (sy) {
+          y1 = a.cy[l] + fy * (y1 - a.cy[l]);
+          __stcg(a.p1 + l, y1);
+        }
+        const double e = y1 - __ldcg(a.p2 + l);
+        pc[0] = fma(e, e, pc[0]);
+        const double y2n = y1 + beta * (y1 - __ldcg(a.p1p + l));
+        __stcg(a.p2 + l, y2n);
+        double xi2[NN];
+#pragma unroll
+        for (int j = 0; j < NN; ++j) {
+          const long long k = N + l * NN + j;
+          double x1 = __ldcg(a.p1 + k);
+          if (sx) {
+            const double c = cxi_at(a, l * NN + j);
+            x1 = c + fx * (x1 - c);
+            __stcg(a.p1 + k, x1);
+          }
+          const double ex = x1 - __ldcg(a.p2 + k);
+          pc[1] = fma(ex, ex, pc[1]);
+          xi2[j] = x1 + beta * (x1 - __ldcg(a.p1p + k));
+          __stcg(a.p2 + k, xi2[j]);
+        }
+        write_records<NN>(a, l, y2n, xi2);
+      }
+      block_sum_all<2, kLBlock>(pc);
+      if (threadIdx.x == 0) {
+        __stcg(L.partC + (long long)blockIdx.x * 2, pc[0]);
+        __stcg(L.partC + (long long)blockIdx.x * 2 + 1, pc[1]);
+      }
+      t = t_next;
+    }
+    grid.sync();
+    // ---- D: identical stop decision in every block (engines.cpp:104-105)
+    double disp[2];
+    grid_sum<2>(L.partC, G, disp);
+    disp_y = sqrt(disp[0]);
+    disp_x = sqrt(disp[1]);
+    ++ell;
+    const bool stop = disp_y <= ay && disp_x <= ax;
+    if (!stop && ell == lmax) hit = true;
+    if (stop || bad) break;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    d->ell = ell;
+    d->t = t;
+    d->hit_cap = hit ? 1 : 0;
+    d->nonfinite = bad ? 1 : 0;
+    d->disp_y = disp_y;
+    d->disp_xi = disp_x;
+    d->halt = 1;
+  }
+}
+
 using AlccKernel = void (*)(const AlccArgs);
 template <int NN>
 struct AlccTab {
@@ -405,6 +627,16 @@ constexpr AlccFns fns_for() {
   return {AlccTab<NN>::project, AlccTab<NN>::reset, AlccTab<NN>::records, AlccTab<NN>::grad,
           AlccTab<NN>::step,    AlccTab<NN>::stats, AlccTab<NN>::bounds};
 }
+template <int NN>
+constexpr const void* loop_fn() {
+  return (const void*)mapg_loop_kernel<NN>;
+}
+const void* const kLoopFns[kMaxN] = {
+    loop_fn<1>(),  loop_fn<2>(),  loop_fn<3>(),  loop_fn<4>(),  loop_fn<5>(),  loop_fn<6>(),
+    loop_fn<7>(),  loop_fn<8>(),  loop_fn<9>(),  loop_fn<10>(), loop_fn<11>(), loop_fn<12>(),
+    loop_fn<13>(), loop_fn<14>(), loop_fn<15>(), loop_fn<16>(), loop_fn<17>(), loop_fn<18>(),
+    loop_fn<19>(), loop_fn<20>(), loop_fn<21>(), loop_fn<22>(), loop_fn<23>(), loop_fn<24>()};
+
 constexpr AlccFns kFns[kMaxN] = {
     fns_for<1>(),  fns_for<2>(),  fns_for<3>(),  fns_for<4>(),  fns_for<5>(),  fns_for<6>(),
     fns_for<7>(),  fns_for<8>(),  fns_for<9>(),  fns_for<10>(), fns_for<11>(), fns_for<12>(),
@@ -448,7 +680,7 @@ SweepArgs penalty_sweep_args(cr_handle* h, double cdiv) {
   return a;
 }
 
-cr_status ensure_alcc(cr_handle* h) {
+cr_status ensure_alcc(cr_handle* h, bool allow_loop) {
   AlccBufs& b = h->alcc;
   if (b.dev) return CR_OK;
   const int64_t P = h->N * (h->n + 1);
@@ -479,6 +711,38 @@ cr_status ensure_alcc(cr_handle* h) {
   }
   if (!b.kpen.fn || !b.kupd.fn || b.kpen.max_blocks_per_sm < 1 || b.kupd.max_blocks_per_sm < 1)
     return fail(h, CR_EINVAL, "alcc: no penalty sweep kernel for this n");
+  // small sub-problems: one cooperative launch per MAPG call (CRB_ALCC_LOOP=0 disables)
+  const char* env = std::getenv("CRB_ALCC_LOOP");
+  const bool want = allow_loop && h->N <= 2048 && !(env && env[0] == '0');
+  if (want) {
+    const void* fn = kLoopFns[h->n - 1];
+    int bps = 0, sms = 148;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, fn, kLBlock, 0) != cudaSuccess) bps = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device);
+    const long long S = (h->N + 31) / 32;
+    long long P = std::max<long long>(1, (h->N + 31) / 32);
+    long long G = (S * P + 7) / 8;
+    const long long Gmax = (long long)bps * sms;
+    if (Gmax >= 1) {
+      if (G > Gmax) {
+        G = Gmax;
+        P = std::max<long long>(1, G * 8 / S);
+        G = std::min<long long>(Gmax, (S * P + 7) / 8);
+      }
+      cudaError_t e2 = cudaSuccess;
+      if (e2 == cudaSuccess) e2 = dalloc(&b.lcolpart, (size_t)(h->N * (h->n + 1) * P));
+      if (e2 == cudaSuccess) e2 = dalloc(&b.lrowpart, (size_t)(h->N * S));
+      if (e2 == cudaSuccess) e2 = dalloc(&b.lpartB, (size_t)(3 * G));
+      if (e2 == cudaSuccess) e2 = dalloc(&b.lpartC, (size_t)(2 * G));
+      if (e2 != cudaSuccess) {
+        cudaGetLastError();
+        return fail(h, CR_ENOMEM, "alcc: loop buffers");
+      }
+      b.loop_G = (int)G;
+      b.loop_S = (int)S;
+      b.loop_P = (int)P;
+    }
+  }
   return CR_OK;
 }
 
@@ -543,12 +807,16 @@ cr_status outer_stats(cr_handle* h, const AlccFns& f, const AlccArgs& aa, bool u
 
 }  // namespace
 
-cr_status alcc_prepare(cr_handle* h) { return ensure_alcc(h); }
+// sub-problem handles of a partition run concurrently: the per-launch path
+// (a cooperative launch would serialise them)
+cr_status alcc_prepare(cr_handle* h) { return ensure_alcc(h, false); }
 
 void alcc_release(cr_handle* h) {
   AlccBufs& b = h->alcc;
   if (b.gexec) cudaGraphExecDestroy(b.gexec);
-  for (double* p : {b.p1, b.p1p, b.p2, b.part1, b.part2}) dfree(p, h->st);
+  for (double* p : {b.p1, b.p1p, b.p2, b.part1, b.part2, b.lcolpart, b.lrowpart, b.lpartB,
+                    b.lpartC})
+    dfree(p, h->st);
   dfree(b.counter, h->st);
   dfree(b.dev, h->st);
   if (b.host) {
@@ -659,7 +927,7 @@ cr_status alcc_run(cr_handle* h, const cr_alcc_config* cfg, double sA1, double s
     alpha_y = alpha_xi = cfg->alpha1_scale * (By + Bx);
   }
   const int GI = 16;
-  if (!b.gexec || b.graph_iters != GI) {
+  if (b.loop_G == 0 && (!b.gexec || b.graph_iters != GI)) {
     const cr_status s = build_mapg_graph(h, f, aa, GI);
     if (s != CR_OK) return s;
   }
@@ -691,13 +959,34 @@ cr_status alcc_run(cr_handle* h, const cr_alcc_config* cfg, double sA1, double s
     CUDA_TRY(cudaEventRecord(h->ev_start, h->st));
     CUDA_TRY(launch_alcc(f.reset, b.blocks, kPBlock, aa, h->st));
     launches += 1;
-    for (;;) {
-      CUDA_TRY(cudaGraphLaunch(b.gexec, h->st));
-      launches += 4 * (int64_t)b.graph_iters;
+    if (b.loop_G > 0) {  // the whole MAPG call in one cooperative launch
+      LoopArgs la{};
+      la.a = aa;
+      la.V0 = h->V[0];
+      la.V1 = h->V[1];
+      la.colpart = b.lcolpart;
+      la.rowpart = b.lrowpart;
+      la.partB = b.lpartB;
+      la.partC = b.lpartC;
+      la.ld = h->ld;
+      la.S = b.loop_S;
+      la.P = b.loop_P;
+      void* args[] = {&la};
+      CUDA_TRY(cudaLaunchCooperativeKernel(kLoopFns[n - 1], dim3((unsigned)b.loop_G),
+                                           dim3(kLBlock), args, 0, h->st));
+      launches += 1;
       CUDA_TRY(cudaEventRecord(h->ev_end, h->st));
       const cr_status s = pull_dev(h);
       if (s != CR_OK) return s;
-      if (d.halt) break;
+    } else {
+      for (;;) {
+        CUDA_TRY(cudaGraphLaunch(b.gexec, h->st));
+        launches += 4 * (int64_t)b.graph_iters;
+        CUDA_TRY(cudaEventRecord(h->ev_end, h->st));
+        const cr_status s = pull_dev(h);
+        if (s != CR_OK) return s;
+        if (d.halt) break;
+      }
     }
     {
       float ms = 0;
@@ -800,7 +1089,7 @@ cr_status cr_alcc_solve(cr_handle* h, const cr_alcc_config* cfg, const double* w
   CUDA_TRY(cudaSetDevice(h->device));
   const auto t_start = std::chrono::steady_clock::now();
   {
-    const cr_status s = ensure_alcc(h);
+    const cr_status s = ensure_alcc(h, true);
     if (s != CR_OK) return s;
   }
   AlccBufs& b = h->alcc;

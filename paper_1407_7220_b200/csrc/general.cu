@@ -24,10 +24,12 @@
 #include <chrono>
 #include <climits>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <thread>
 #include <vector>
 
+#include "balcc.cuh"
 #include "handle.cuh"
 #include "iteration.cuh"
 
@@ -265,8 +267,65 @@ unsigned grid_of(long long count) {
 
 // DualDecomposition::dual_gradient's block loop (papg.cpp:107-130): every block
 // from its warm start, eta gathered in block order, within infeasibility
+cr_status solve_blocks_batched(cr_handle* h, double tol, double* within) {
+  Partition& P = h->part;
+  const auto t0 = std::chrono::steady_clock::now();
+  BalccArgs a{};
+  a.X = h->X;
+  a.cy = P.cy;
+  a.cxi = P.cxi;
+  a.fy = P.fy;
+  a.fxi = P.fxi;
+  a.ey = P.ey;
+  a.exi = P.exi;
+  a.sigma_A2 = P.d_sigma_A2;
+  a.sigma_A1 = P.sigma_A1;
+  a.gamma = h->gamma;
+  a.target = tol;
+  a.cfg = P.inner;
+  a.theta = P.w_theta;
+  a.y1p = P.w_y1p;
+  a.y2 = P.w_y2;
+  a.x1p = P.w_x1p;
+  a.x2 = P.w_x2;
+  a.cc = P.w_cc;
+  a.rs = P.w_rs;
+  a.cs = P.w_cs;
+  a.vx = P.w_vx;
+  a.scratch = P.w_scratch;
+  a.scratch_per_block = balcc_scratch_per_block(P.nbar, (int)h->n);
+  a.infeas = P.w_infeas;
+  a.iters = P.w_iters;
+  a.status = P.w_status;
+  a.nbar = P.nbar;
+  a.K = (int)P.K;
+  CUDA_TRY(launch_balcc(a, (int)h->n, h->st));
+  std::vector<double> inf((size_t)P.K);
+  std::vector<long long> its((size_t)P.K);
+  std::vector<int> sts((size_t)P.K);
+  CUDA_TRY(cudaMemcpyAsync(inf.data(), P.w_infeas, sizeof(double) * P.K, cudaMemcpyDeviceToHost,
+                           h->st));
+  CUDA_TRY(cudaMemcpyAsync(its.data(), P.w_iters, sizeof(long long) * P.K,
+                           cudaMemcpyDeviceToHost, h->st));
+  CUDA_TRY(cudaMemcpyAsync(sts.data(), P.w_status, sizeof(int) * P.K, cudaMemcpyDeviceToHost,
+                           h->st));
+  CUDA_TRY(cudaStreamSynchronize(h->st));
+  double sq = 0;
+  for (int64_t b = 0; b < P.K; ++b) {  // gathered in block order (papg.cpp:124-128)
+    if (sts[(size_t)b] != 0)
+      return fail(h, CR_ENONFINITE, "block " + std::to_string(b) + ": mapg: non-finite gradient");
+    P.block_infeas[(size_t)b] = inf[(size_t)b];
+    sq += inf[(size_t)b] * inf[(size_t)b];
+    P.inner_iters += its[(size_t)b];
+  }
+  P.inner_seconds += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  *within = std::sqrt(sq);
+  return CR_OK;
+}
+
 cr_status solve_blocks(cr_handle* h, double tol, double* within) {
   Partition& P = h->part;
+  if (P.batched) return solve_blocks_batched(h, tol, within);
   CUDA_TRY(cudaStreamSynchronize(h->st));  // centres ready
   const auto t0 = std::chrono::steady_clock::now();
   const int64_t nb = P.nbar, n = h->n;
@@ -351,6 +410,12 @@ cr_status pull_ctrl(cr_handle* h) {
 cr_status general_begin(cr_handle* h) {
   Partition& P = h->part;
   const int64_t nb = P.nbar, n = h->n;
+  if (P.batched) {  // the block minimisers live in ey / exi (warm starts in place)
+    CUDA_TRY(cudaMemcpyAsync(P.ey, P.fy, sizeof(double) * h->N, cudaMemcpyDeviceToDevice, h->st));
+    CUDA_TRY(cudaMemcpyAsync(P.exi, P.fxi, sizeof(double) * h->N * n, cudaMemcpyDeviceToDevice,
+                             h->st));
+    CUDA_TRY(cudaStreamSynchronize(h->st));
+  }
   for (int64_t b = 0; b < P.K; ++b) {
     cr_handle* hb = P.blocks[(size_t)b];
     CUDA_TRY(cudaMemcpyAsync(hb->alcc.p1, P.fy + b * nb, sizeof(double) * nb,
@@ -476,7 +541,12 @@ void general_release(cr_handle* h) {
   if (P.K > 0) select_sweeps(h, false);
   for (cr_handle* hb : P.blocks) cr_destroy(hb);
   P.blocks.clear();
-  for (double* b : {P.cy, P.cxi, P.qy, P.qxi, P.th2pos, P.ey, P.exi, P.fy, P.fxi}) dfree(b, h->st);
+  for (double* b : {P.cy, P.cxi, P.qy, P.qxi, P.th2pos, P.ey, P.exi, P.fy, P.fxi, P.w_theta,
+                    P.w_y1p, P.w_y2, P.w_x1p, P.w_x2, P.w_cc, P.w_rs, P.w_cs, P.w_vx,
+                    P.w_infeas, P.d_sigma_A2, P.w_scratch})
+    dfree(b, h->st);
+  dfree(P.w_iters, h->st);
+  dfree(P.w_status, h->st);
   P = Partition{};
 }
 
@@ -557,6 +627,32 @@ cr_status cr_set_partition(cr_handle* h, int64_t K, const double* feas_y, const 
     }
     s = cr_sigma_A(hb, 2, 1e-6, 5000, &P.sigma_A2[(size_t)b], &it, &cv);
     if (s != CR_OK) return fail(h, s, "partition: sigma(A2)");
+  }
+  // small blocks: every block ALCC in one launch (balcc.cu); CRB_BALCC=0 disables
+  const char* env = std::getenv("CRB_BALCC");
+  if (nbar <= balcc_max_block() && !(env && env[0] == '0')) {
+    g_alloc_stream = h->st;
+    cudaError_t e2 = cudaSuccess;
+    for (double** b : {&P.w_y1p, &P.w_y2, &P.w_cc, &P.w_rs, &P.w_cs})
+      if (e2 == cudaSuccess) e2 = dalloc(b, (size_t)N);
+    for (double** b : {&P.w_x1p, &P.w_x2, &P.w_vx})
+      if (e2 == cudaSuccess) e2 = dalloc(b, (size_t)(N * n));
+    if (e2 == cudaSuccess) e2 = dalloc(&P.w_theta, (size_t)(N * nbar));
+    if (e2 == cudaSuccess)
+      e2 = dalloc(&P.w_scratch, (size_t)(K * balcc_scratch_per_block(nbar, (int)n)));
+    if (e2 == cudaSuccess) e2 = dalloc(&P.w_infeas, (size_t)K);
+    if (e2 == cudaSuccess) e2 = dalloc(&P.d_sigma_A2, (size_t)K);
+    if (e2 == cudaSuccess) e2 = dalloc(&P.w_iters, (size_t)K);
+    if (e2 == cudaSuccess) e2 = dalloc(&P.w_status, (size_t)K);
+    if (e2 != cudaSuccess) {
+      cudaGetLastError();
+      general_release(h);
+      return fail(h, CR_ENOMEM, "partition: batched block workspaces");
+    }
+    CUDA_TRY(cudaMemcpyAsync(P.d_sigma_A2, P.sigma_A2.data(), sizeof(double) * K,
+                             cudaMemcpyHostToDevice, h->st));
+    CUDA_TRY(cudaStreamSynchronize(h->st));
+    P.batched = true;
   }
   return CR_OK;
 }

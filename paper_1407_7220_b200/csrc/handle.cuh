@@ -30,6 +30,9 @@ struct AlccBufs {
   cudaGraphExec_t gexec = nullptr;
   int graph_iters = 0;
   int blocks = 0;
+  // small sub-problems: cooperative MAPG loop (grid, strips, row chunks, partials)
+  int loop_G = 0, loop_S = 0, loop_P = 0;
+  double *lcolpart = nullptr, *lrowpart = nullptr, *lpartB = nullptr, *lpartC = nullptr;
   bool done = false;            // a finished solve is on the handle (multiplier export)
   double mu = 0;                // mu of the last outer step
 };
@@ -50,6 +53,15 @@ struct Partition {
   int64_t inner_iters = 0;
   double inner_seconds = 0;
   int workers = 0;                     // concurrent block solves (PapgConfig::workers); 0: 16
+  // small blocks: all block ALCCs in one launch, one CTA per block (balcc.cu)
+  bool batched = false;
+  double *w_theta = nullptr, *w_y1p = nullptr, *w_y2 = nullptr, *w_x1p = nullptr,
+         *w_x2 = nullptr, *w_cc = nullptr, *w_rs = nullptr, *w_cs = nullptr, *w_vx = nullptr,
+         *w_infeas = nullptr;
+  long long* w_iters = nullptr;
+  int* w_status = nullptr;
+  double* d_sigma_A2 = nullptr;        // device copy of sigma_A2
+  double* w_scratch = nullptr;         // batched sweep partials
 };
 }  // namespace crb
 

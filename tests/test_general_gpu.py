@@ -62,16 +62,24 @@ def assert_parity(o, g, tol_theta=1e-9, tol_y=1e-8):
     assert g["res"].g_final == pytest.approx(o.g_final, rel=1e-8, abs=1e-12)
 
 
+@pytest.mark.parametrize("path", ["batched", "handles"])
 @pytest.mark.parametrize("N,n,K,seed", [(24, 1, 2, 1), (30, 2, 3, 2), (36, 2, 4, 3),
                                          (40, 3, 2, 4), (48, 5, 4, 5)])
-def test_general_k_parity(oracle, N, n, K, seed):
+def test_general_k_parity(oracle, monkeypatch, path, N, n, K, seed):
+    """both block-solver paths: one CTA per block in one launch (balcc.cu) and
+    one sub-problem handle per block (CRB_BALCC=0)"""
+    if path == "handles":
+        monkeypatch.setenv("CRB_BALCC", "0")
     X, P = problem(oracle, "sqnorm-uniform", N, n, 0.2, seed)
     o, g = run_both(oracle, X, P, K, max_iters=4, gap_norm_tol=-1.0)
     assert o.iters == 4
     assert_parity(o, g)
 
 
-def test_general_k_parity_mma_variant(oracle):
+@pytest.mark.parametrize("path", ["batched", "handles"])
+def test_general_k_parity_mma_variant(oracle, monkeypatch, path):
+    if path == "handles":
+        monkeypatch.setenv("CRB_BALCC", "0")
     X, P = problem(oracle, "maxaffine-uniform", 48, 7, 0.2, 6, 3)
     o, g = run_both(oracle, X, P, 3, max_iters=3, gap_norm_tol=-1.0)
     assert_parity(o, g)
