@@ -76,11 +76,12 @@ cr_status enqueue_iteration(cr_handle* h, int phase, cudaEvent_t ev_a, cudaEvent
     CUDA_TRY(launch_primal(pa, h->st));
     const SweepArgs sa = sweep_args(h, kModePapg, false);
     if (ev_a) CUDA_TRY(cudaEventRecord(ev_a, h->st));
-    CUDA_TRY((cudaError_t)launch_sweep(h->kp, sa, h->st));
+    CUDA_TRY((cudaError_t)launch_sweep(papg_sweep(h), sa, h->st));
     if (ev_b) CUDA_TRY(cudaEventRecord(ev_b, h->st));
     // single GPU, full iteration: the reduce kernel's last block runs the control step
     const bool fuse = phase == 0 && h->comm == nullptr;
-    const ReduceArgs ra = reduce_args(h, true, &h->ctrl_d->halt, fuse);
+    const ReduceArgs ra =
+        reduce_args(h, true, &h->ctrl_d->halt, fuse, papg_sweep(h).warps_per_block);
     CUDA_TRY(launch_reduce(ra, h->st));
     if (use_nccl && h->comm)
       NCCL_TRY(ncclAllReduce(h->xbuf, h->xbuf, (size_t)payload_len(h), ncclDouble, ncclSum,
@@ -221,6 +222,16 @@ cr_status cr_create(const double* Xh, const double* ybar_shifted, int64_t N, int
   h->variant = n <= 6 ? kSweepDfma : kSweepMma;
   if (var && std::strcmp(var, "dfma") == 0) h->variant = kSweepDfma;
   if (var && std::strcmp(var, "mma") == 0) h->variant = kSweepMma;
+  // masked dual store (sweep_sparse.cu), opt-in with CRB_SPARSE=1: it moves
+  // 12x fewer bytes but is latency bound and slower than the dense sweep
+  // (DESIGN.md section 11); DMMA geometry for every n
+  const char* sp = std::getenv("CRB_SPARSE");
+  h->sparse_ok = (sp && sp[0] == '1') && !(var && std::strcmp(var, "dfma") == 0);
+  if (h->sparse_ok) {
+    h->variant = kSweepMma;
+    h->ksp = sweep_sparse_info((int)n, false);
+    if (!h->ksp.fn || h->ksp.max_blocks_per_sm < 1) h->sparse_ok = false;
+  }
   if (h->variant == kSweepMma) {
     h->kp = sweep_mma_info((int)n, kModePapg);
     h->kw = sweep_mma_info((int)n, kModePower);
@@ -258,13 +269,19 @@ cr_status cr_create(const double* Xh, const double* ybar_shifted, int64_t N, int
   ALLOC(h->colrec, N * RP);
   ALLOC(h->V[0], vlen);
   ALLOC(h->V[1], vlen);
+  if (h->sparse_ok) {
+    ALLOC(h->M[0], (size_t)h->T * h->R * kMaskWords);
+    ALLOC(h->M[1], (size_t)h->T * h->R * kMaskWords);
+  }
   ALLOC(h->vpos[0], N);
   ALLOC(h->vpos[1], N);
   ALLOC(h->xbuf, payload_len(h));
   ALLOC(h->aggsave, payload_len(h));
   ALLOC(h->colpart, (size_t)h->G * h->maxspan * h->kp.tile_cols * (n + 1));
   ALLOC(h->rowpart, (size_t)h->T * h->R);
-  ALLOC(h->scalpart, (size_t)h->G * h->kp.warps_per_block * kScal);
+  ALLOC(h->scalpart, (size_t)h->G * std::max(h->kp.warps_per_block,
+                                              h->sparse_ok ? h->ksp.warps_per_block : 0) *
+                        kScal);
   ALLOC(h->k2part, (size_t)h->k2_blocks * kK2Scal);
   ALLOC(h->k2sum, kK2Scal);
   ALLOC(h->yout, N);
@@ -343,6 +360,8 @@ void cr_destroy(cr_handle* h) {
   for (double* b : {h->s_colpart, h->s_rowpart, h->s_scalpart, h->s_k2part}) dfree(b, h->st);
   dfree(h->izero, h->st);
   dfree(h->counter, h->st);
+  dfree(h->M[0], h->st);
+  dfree(h->M[1], h->st);
   dfree(h->ctrl_d, h->st);
   if (h->st) cudaStreamSynchronize(h->st);
   if (h->ctrl_h) cudaFreeHost(h->ctrl_h);
@@ -556,7 +575,26 @@ cr_status begin_impl(cr_handle* h, const cr_papg_config* cfg, const double* thet
   std::memcpy(h->ctrl_h, &c, sizeof(c));
 
   const size_t vbytes = sizeof(double) * (size_t)h->R * (size_t)h->ld;
+  // small N (V, V' L2-resident, one GPU): one persistent cooperative launch runs
+  // many iterations (small.cu). CRB_SMALL=0 disables, CRB_SMALL=1 forces.
+  const char* smenv = std::getenv("CRB_SMALL");
+  bool want_small = h->comm == nullptr && cfg->graph_iters == 0 &&
+                    2.0 * 8.0 * (double)h->R * (double)h->ld <= 48e6 && h->part.K == 0;
+  if (smenv && smenv[0] == '0') want_small = false;
+  if (smenv && smenv[0] == '1' && h->comm == nullptr && h->R == h->N && h->part.K == 0)
+    want_small = true;
+  // masked dual store for the per-kernel path; a resumed solve keeps the layout
+  // of the state it continues
+  if (resume) {
+    if (h->masked) want_small = false;
+  } else {
+    h->masked = h->sparse_ok && !want_small;
+  }
   if (!resume) {
+    if (h->masked) {
+      CUDA_TRY(cudaMemsetAsync(h->M[0], 0, sizeof(uint16_t) * h->T * h->R * kMaskWords, h->st));
+      CUDA_TRY(cudaMemsetAsync(h->M[1], 0, sizeof(uint16_t) * h->T * h->R * kMaskWords, h->st));
+    }
     CUDA_TRY(cudaMemsetAsync(h->V[0], 0, vbytes, h->st));
     CUDA_TRY(cudaMemsetAsync(h->V[1], 0, vbytes, h->st));
     CUDA_TRY(cudaMemsetAsync(h->vpos[0], 0, sizeof(double) * N, h->st));
@@ -588,10 +626,12 @@ cr_status begin_impl(cr_handle* h, const cr_papg_config* cfg, const double* thet
     }
     CUDA_TRY(cudaMemcpyAsync(h->stage, tpos, sizeof(double) * N, cudaMemcpyHostToDevice, h->st));
     CUDA_TRY(launch_pos_in(h->vpos[0], h->stage, N, h->st));
+    if (h->masked)
+      CUDA_TRY(launch_mask_build(h->V[0], h->M[0], N, h->ld, h->R, h->kp.tile_cols, h->T, h->st));
     // aggregates and |.|^2 of max(theta0, 0): a sweep with 1/L = 0 is a copy
     const SweepArgs sa = sweep_args(h, kModePapg, true);
-    CUDA_TRY((cudaError_t)launch_sweep(h->kp, sa, h->st));
-    const ReduceArgs ra = reduce_args(h, false, nullptr, false);
+    CUDA_TRY((cudaError_t)launch_sweep(papg_sweep(h), sa, h->st));
+    const ReduceArgs ra = reduce_args(h, false, nullptr, false, papg_sweep(h).warps_per_block);
     CUDA_TRY(launch_reduce(ra, h->st));
     if (h->comm)
       NCCL_TRY(ncclAllReduce(h->xbuf, h->xbuf, (size_t)payload_len(h), ncclDouble, ncclSum,
@@ -599,15 +639,8 @@ cr_status begin_impl(cr_handle* h, const cr_papg_config* cfg, const double* thet
     CUDA_TRY(launch_warm_ctrl(h->ctrl_d, h->xbuf + N * (h->n + 2), pos_sq, h->st));
   }
 
-  // small N (V, V' L2-resident, one GPU): one persistent cooperative launch runs
-  // many iterations (small.cu). CRB_SMALL=0 disables, CRB_SMALL=1 forces.
   {
-    const char* sm = std::getenv("CRB_SMALL");
-    const double vbytes2 = 2.0 * 8.0 * (double)h->R * (double)h->ld;
-    bool want = h->comm == nullptr && cfg->graph_iters == 0 && vbytes2 <= 48e6 &&
-                h->part.K == 0;
-    if (sm && sm[0] == '0') want = false;
-    if (sm && sm[0] == '1' && h->comm == nullptr && h->R == h->N && h->part.K == 0) want = true;
+    const bool want = want_small;
     h->small_mode = false;
     if (want) {
       h->ks = small_loop_info((int)h->n);
@@ -958,7 +991,8 @@ cr_status cr_get_theta(cr_handle* h, double* out) {
   const int64_t rows_per = std::max<int64_t>(1, h->stage_elems / rowlen);
   for (int64_t ra = 0; ra < h->R; ra += rows_per) {
     const int64_t rb = std::min(h->R, ra + rows_per);
-    CUDA_TRY(launch_theta_out(h->stage, h->V[cur], sc, h->N, h->ld, h->r0, ra, rb, h->st));
+    CUDA_TRY(launch_theta_out(h->stage, h->V[cur], sc, h->N, h->ld, h->r0, ra, rb, h->st,
+                              h->masked ? h->M[cur] : nullptr, h->R, h->kp.tile_cols));
     CUDA_TRY(cudaMemcpyAsync(out + ra * rowlen, h->stage, sizeof(double) * (rb - ra) * rowlen,
                              cudaMemcpyDeviceToHost, h->st));
     CUDA_TRY(cudaStreamSynchronize(h->st));
@@ -1009,7 +1043,7 @@ cr_status cr_time_sweep(cr_handle* h, int32_t k, double* avg_seconds) {
   SweepArgs sa = sweep_args(h, kModePapg, false);
   sa.stopped = nullptr;
   CUDA_TRY(cudaEventRecord(h->ev_start, h->st));
-  for (int i = 0; i < k; ++i) CUDA_TRY((cudaError_t)launch_sweep(h->kp, sa, h->st));
+  for (int i = 0; i < k; ++i) CUDA_TRY((cudaError_t)launch_sweep(papg_sweep(h), sa, h->st));
   CUDA_TRY(cudaEventRecord(h->ev_end, h->st));
   CUDA_TRY(cudaEventSynchronize(h->ev_end));
   float ms = 0;
@@ -1059,6 +1093,8 @@ cr_status pair_metrics(cr_handle* h, PointBufs& b, bool with_theta, double out[2
   a.rowrec = b.rowrec;
   a.colrec = b.colrec;
   a.V = with_theta ? h->V[h->ctrl_h->cur] : nullptr;
+  a.M = (with_theta && h->masked) ? h->M[h->ctrl_h->cur] : nullptr;
+  a.TC = h->kp.tile_cols;
   a.s = h->ctrl_h->s_cur;
   a.part = b.part;
   a.N = h->N;

@@ -89,7 +89,20 @@ struct SweepArgs {
   int maxspan;            // max segments (tiles) one CTA can touch
   long long nbar;         // block size of the partition: pairs inside one block are
                           // masked like the diagonal (1: singleton blocks)
+  uint16_t* M0;           // masked dual store (sweep_sparse.cu): live bits of V[0], V[1]
+  uint16_t* M1;
 };
+
+// Masked dual store: per buffer, 16 uint16 words per (column tile t, local row r)
+// ([T][R][16], tile-major); bit b of word w = column t*TC + 16w + b is live.
+// A clear bit means 0 whatever V holds.
+constexpr int kMaskWords = 16;
+__host__ __device__ __forceinline__ bool mask_live(const uint16_t* M, long long R, int TC,
+                                                   long long r, long long col) {
+  const long long t = col / TC;
+  const int cl = (int)(col - t * TC);
+  return (M[(t * R + r) * kMaskWords + (cl >> 4)] >> (cl & 15)) & 1;
+}
 
 // same block of the partition. BLK = false: singleton blocks (the diagonal);
 // the blocked test is a separate instantiation so the singleton kernels carry
@@ -130,6 +143,7 @@ enum SweepVariant { kSweepDfma = 0, kSweepMma = 1 };
 // kModePower only)
 SweepKernelInfo sweep_dfma_info(int n, int mode, bool blocked = false);  // sweep.cu (CUDA-core DFMA)
 SweepKernelInfo sweep_mma_info(int n, int mode, bool blocked = false);   // sweep_mma.cu (DMMA)
+SweepKernelInfo sweep_sparse_info(int n, bool blocked = false);  // sweep_sparse.cu (masked, P-APG)
 int launch_sweep(const SweepKernelInfo& info, const SweepArgs& a, void* stream);
 
 }  // namespace crb

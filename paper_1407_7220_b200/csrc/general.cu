@@ -169,12 +169,14 @@ __device__ __forceinline__ void cross_pair(long long idx, long long K, long long
 }
 
 __global__ void theta_k_out_kernel(double* stage, const double* V, double s, long long K,
-                                   long long nbar, long long ld, long long a, long long b) {
+                                   long long nbar, long long ld, long long a, long long b,
+                                   const uint16_t* M, long long R, int TC) {
   for (long long i = a + (long long)blockIdx.x * blockDim.x + threadIdx.x; i < b;
        i += (long long)gridDim.x * blockDim.x) {
     long long l1, l2;
     cross_pair(i, K, nbar, &l1, &l2);
-    stage[i - a] = s * V[l1 * ld + l2];
+    const bool live = M == nullptr || mask_live(M, R, TC, l1, l2);
+    stage[i - a] = live ? s * V[l1 * ld + l2] : 0.0;
   }
 }
 
@@ -393,6 +395,11 @@ cr_status select_sweeps(cr_handle* h, bool blocked) {
     return fail(h, CR_EINVAL, "partition: no blocked sweep kernel for this n");
   h->kp = kp;
   h->kw = kw;
+  if (h->sparse_ok) {
+    h->ksp = sweep_sparse_info(n, blocked);
+    if (!h->ksp.fn || h->ksp.max_blocks_per_sm < 1)
+      return fail(h, CR_EINVAL, "partition: no masked sweep kernel for this n");
+  }
   return CR_OK;
 }
 
@@ -449,9 +456,10 @@ cr_status general_iterate(cr_handle* h, int64_t max_steps, int64_t* done, int32_
     CUDA_TRY(launch_gen(f.finish, gen_args(h, 0), h->st));
     const SweepArgs sa = sweep_args(h, kModePapg, false);
     CUDA_TRY(cudaEventRecord(h->ev_start, h->st));
-    CUDA_TRY((cudaError_t)launch_sweep(h->kp, sa, h->st));
+    CUDA_TRY((cudaError_t)launch_sweep(papg_sweep(h), sa, h->st));
     CUDA_TRY(cudaEventRecord(h->ev_end, h->st));
-    const ReduceArgs ra = reduce_args(h, true, &h->ctrl_d->halt, true);
+    const ReduceArgs ra =
+        reduce_args(h, true, &h->ctrl_d->halt, true, papg_sweep(h).warps_per_block);
     CUDA_TRY(launch_reduce(ra, h->st));
     s = pull_ctrl(h);
     if (s != CR_OK) return s;
@@ -489,8 +497,9 @@ cr_status general_get_theta(cr_handle* h, double* out) {
   const long long cross = h->N * (h->N - P.nbar);
   for (long long a = 0; a < cross; a += h->stage_elems) {
     const long long b = std::min<long long>(cross, a + h->stage_elems);
-    theta_k_out_kernel<<<grid_of(b - a), 256, 0, h->st>>>(h->stage, h->V[cur], sc, P.K, P.nbar,
-                                                         h->ld, a, b);
+    theta_k_out_kernel<<<grid_of(b - a), 256, 0, h->st>>>(
+        h->stage, h->V[cur], sc, P.K, P.nbar, h->ld, a, b, h->masked ? h->M[cur] : nullptr, h->R,
+        h->kp.tile_cols);
     CUDA_TRY(cudaGetLastError());
     CUDA_TRY(cudaMemcpyAsync(out + a, h->stage, sizeof(double) * (b - a), cudaMemcpyDeviceToHost,
                              h->st));

@@ -124,6 +124,11 @@ struct cr_handle {
   std::vector<cudaEvent_t> ev_sweep;  // pairs
   double last_seconds = 0, last_sweep_seconds = 0;
   int64_t last_launches = 0;
+  // masked dual store (sweep_sparse.cu): live-bit words of V[0], V[1]
+  uint16_t* M[2] = {nullptr, nullptr};
+  bool sparse_ok = false;   // the masked P-APG sweep is available (MMA geometry)
+  bool masked = false;      // this solve runs it (not the small-N loop)
+  SweepKernelInfo ksp{};
   // standalone ALCC (alcc.cu)
   crb::AlccBufs alcc{};
   // general-K partition (general.cu); K == 0: singleton blocks
@@ -194,10 +199,15 @@ inline SweepArgs sweep_args(cr_handle* h, int mode, bool agg_only) {
   a.U = h->U;
   a.maxspan = h->maxspan;
   a.nbar = h->part.K > 0 ? h->part.nbar : 1;
+  a.M0 = h->M[0];
+  a.M1 = h->M[1];
   return a;
 }
+// the P-APG sweep of this solve: masked (sparse) or dense
+inline const SweepKernelInfo& papg_sweep(const cr_handle* h) { return h->masked ? h->ksp : h->kp; }
 
-inline ReduceArgs reduce_args(cr_handle* h, bool with_k2, const int* stopped, bool fuse_control) {
+inline ReduceArgs reduce_args(cr_handle* h, bool with_k2, const int* stopped, bool fuse_control,
+                              int sweep_warps = 0) {
   ReduceArgs a{};
   a.colpart = h->colpart;
   a.rowpart = h->rowpart;
@@ -214,7 +224,7 @@ inline ReduceArgs reduce_args(cr_handle* h, bool with_k2, const int* stopped, bo
   a.ld = h->ld;
   a.R = h->R;
   a.r0 = h->r0;
-  a.nw = (long long)h->G * h->kp.warps_per_block;
+  a.nw = (long long)h->G * (sweep_warps > 0 ? sweep_warps : h->kp.warps_per_block);
   a.nk2 = with_k2 ? h->k2_blocks : 0;
   a.n1 = (int)h->n + 1;
   a.S = h->T;

@@ -224,14 +224,33 @@ __global__ void theta_in_kernel(const double* stage, double* V, long long N, lon
 }
 
 __global__ void theta_out_kernel(double* stage, const double* V, double s, long long N,
-                                 long long ld, long long r0, long long ra, long long rb) {
+                                 long long ld, long long r0, long long ra, long long rb,
+                                 const uint16_t* M, long long R, int TC) {
   const long long total = (rb - ra) * (N - 1);
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
        i += (long long)gridDim.x * blockDim.x) {
     const long long lr = i / (N - 1), k = i % (N - 1);
     const long long gr = r0 + ra + lr;
     const long long c = k + (k >= gr ? 1 : 0);
-    stage[i] = s * V[(ra + lr) * ld + c];
+    const bool live = M == nullptr || mask_live(M, R, TC, ra + lr, c);
+    stage[i] = live ? s * V[(ra + lr) * ld + c] : 0.0;
+  }
+}
+
+__global__ void mask_build_kernel(const double* V, uint16_t* M, long long N, long long ld,
+                                  long long R, int TC, int T) {
+  const long long total = (long long)T * R * kMaskWords;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int w = (int)(i % kMaskWords);
+    const long long tr = i / kMaskWords;
+    const long long r = tr % R, t = tr / R;
+    uint32_t bits = 0;
+    for (int b = 0; b < 16; ++b) {
+      const long long c = t * TC + 16 * w + b;
+      if (16 * w + b < TC && c < N && c < ld && V[r * ld + c] > 0.0) bits |= 1u << b;
+    }
+    M[i] = (uint16_t)bits;
   }
 }
 
@@ -352,9 +371,16 @@ cudaError_t launch_theta_in(const double* stage, double* V, long long N, long lo
 
 cudaError_t launch_theta_out(double* stage, const double* V, double sc, long long N,
                              long long ld, long long r0, long long ra, long long rb,
-                             cudaStream_t s) {
+                             cudaStream_t s, const uint16_t* M, long long R, int TC) {
   theta_out_kernel<<<grid_for((rb - ra) * (N - 1), 256, 4096), 256, 0, s>>>(stage, V, sc, N, ld,
-                                                                            r0, ra, rb);
+                                                                            r0, ra, rb, M, R, TC);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_mask_build(const double* V, uint16_t* M, long long N, long long ld,
+                              long long R, int TC, int T, cudaStream_t s) {
+  mask_build_kernel<<<grid_for((long long)T * R * kMaskWords, 256, 4096), 256, 0, s>>>(
+      V, M, N, ld, R, TC, T);
   return cudaGetLastError();
 }
 

@@ -23,67 +23,12 @@
 #include <cstdint>
 
 #include "device.cuh"
+#include "mma_geo.cuh"
 #include "pipeline.cuh"
 
 namespace crb {
 
 namespace {
-
-// CTA geometry per n (measured, profiles/): n <= 12: 7 consumer warps x 4
-// tiles (8 warps -> 255-register cap); n > 12: 15 consumer warps x 2 tiles
-// (16 warps, 128 registers) -- more warps hide the longer DMMA chains.
-template <int NN>
-__host__ __device__ constexpr int mma_cw() { return NN <= 12 ? 7 : 15; }  // consumer warps
-template <int NN>
-__host__ __device__ constexpr int mma_ct() { return NN <= 12 ? 4 : 2; }   // 8-col tiles / warp
-template <int NN>
-__host__ __device__ constexpr int mma_threads() { return (mma_cw<NN>() + 1) * 32; }
-// kW columns per warp, kTC per CTA tile, kTCP smem row pitch (+16 B: conflict-free)
-#define CRB_GEO(NN)                              \
-  constexpr int kCW = mma_cw<NN>();              \
-  constexpr int kCT = mma_ct<NN>();              \
-  constexpr int kW = 8 * kCT;                    \
-  constexpr int kTC = kCW * kW;                  \
-  constexpr int kTCP = kTC + 2;                  \
-  constexpr int kThreads = (kCW + 1) * 32;       \
-  (void)kThreads;
-constexpr int kTR = 8;                 // rows per stage (one MMA row block)
-#ifndef CRB_MMA_CTAS_PER_SM
-#define CRB_MMA_CTAS_PER_SM 1
-#endif
-constexpr int kMinCtas = CRB_MMA_CTAS_PER_SM;  // 2: 128-register cap, 3-stage ring
-constexpr int kNS = kMinCtas == 2 ? 3 : 4;     // stages
-constexpr int kWin = 32;               // row-sum window (rows)
-
-// Residual K: the n features plus (1, y) with (-c, 1) folded in -- unless
-// dropping those two columns saves a k-step, then y - c is added with DADDs.
-template <int NN>
-__host__ __device__ constexpr bool split_yc() { return (NN + 3) / 4 < (NN + 5) / 4; }
-template <int NN>
-__host__ __device__ constexpr int ksteps() { return split_yc<NN>() ? (NN + 3) / 4 : (NN + 5) / 4; }
-template <int NN>
-__host__ __device__ constexpr int fblocks() { return ((NN + 1) + 7) / 8; }
-template <int NN>
-__host__ __device__ constexpr int stage_doubles() {
-  return 2 * kTR * (mma_cw<NN>() * 8 * mma_ct<NN>() + 2) + kTR * rec_pitch(NN);
-}
-template <int NN>
-__host__ __device__ constexpr int smem_bytes() {
-  return kNS * stage_doubles<NN>() * 8 + 2 * mma_cw<NN>() * kWin * 8 + 2 * kNS * 8;
-}
-
-__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
-               : "+d"(d0), "+d"(d1)
-               : "d"(a), "d"(b));
-}
-
-struct MCoef {
-  double s_c, s_p, beta, invL, cdiv;
-};
-struct MScal {
-  double vv, vr, tr, nn;
-};
 
 // One 8-row stage for one warp. MASK: diagonal / partial-stage masking.
 template <int NN, int MODE, bool MASK, bool UNIT, bool BLK>

@@ -427,3 +427,36 @@ def test_tiny_and_ragged_sizes(oracle, monkeypatch, path, N, n):
     s, _, _ = oracle.sigma_C(X)
     kw = dict(max_iters=25, gap_norm_tol=-1.0, infeas_norm_tol=-1.0, sigma_C=s)
     assert_parity(gpu_run(X, ys, **kw), oracle_run(oracle, X, ys, **kw))
+
+
+@pytest.mark.parametrize("kind,N,n,pieces", [("maxaffine-uniform", 2500, 10, 20),
+                                              ("sqnorm-uniform", 2100, 5, 0),
+                                              ("lse-uniform", 1700, 20, 50)])
+def test_masked_store_parity(oracle, monkeypatch, kind, N, n, pieces):
+    """CRB_SPARSE=1: the masked dual store (sweep_sparse.cu) reproduces the
+    oracle like the dense sweep (N off the tile grid, graph and direct paths)"""
+    monkeypatch.setenv("CRB_SPARSE", "1")
+    monkeypatch.setenv("CRB_SMALL", "0")
+    X, ys = instance(oracle, kind, N, n, 0.1, 7, pieces)
+    s, _, _ = oracle.sigma_C(X)
+    o = oracle_run(oracle, X, ys, max_iters=60, gap_norm_tol=-1.0, infeas_norm_tol=-1.0,
+                   sigma_C=s, threads=8)
+    for gi in (0, -1):
+        g = gpu_run(X, ys, max_iters=60, gap_norm_tol=-1.0, infeas_norm_tol=-1.0, sigma_C=s,
+                    graph_iters=gi)
+        assert_parity(g, o)
+
+
+def test_masked_store_warm_start_and_blocks(oracle, monkeypatch):
+    monkeypatch.setenv("CRB_SPARSE", "1")
+    monkeypatch.setenv("CRB_SMALL", "0")
+    X, ys = instance(oracle, "maxaffine-uniform", 1200, 7, 0.1, 9, 10)
+    s, _, _ = oracle.sigma_C(X)
+    N = X.shape[0]
+    rng = np.random.default_rng(2)
+    th0 = np.maximum(rng.standard_normal(N * (N - 1) + N), 0.0) * 0.01
+    o = oracle_run(oracle, X, ys, max_iters=25, gap_norm_tol=-1.0, infeas_norm_tol=-1.0,
+                   sigma_C=s, theta0=th0, threads=8)
+    g = gpu_run(X, ys, max_iters=25, gap_norm_tol=-1.0, infeas_norm_tol=-1.0, sigma_C=s,
+                theta0=th0)
+    assert_parity(g, o)
