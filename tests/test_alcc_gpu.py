@@ -210,3 +210,15 @@ def test_alcc_full_size_consistency(oracle):
     assert (lam >= 0).all()
     o_inf = oracle.infeasibility(X, y, xi)[0]
     assert raw == pytest.approx(o_inf, rel=1e-9)
+
+
+def test_alcc_time_budget(oracle):
+    """max_seconds below one outer step: stops after the first outer step with
+    reason time_budget (alcc.cpp:167-170)"""
+    X, P = problem(oracle, "sqnorm-uniform", 40, 2, 0.2, 17)
+    bounds = crb.ProblemBounds(P.B_theta, P.Bbar_y, P.Bbar_xi, P.gamma)
+    with crb.DualSolver(X, P.ys) as s:
+        res, y, xi, hist, mi = s.alcc(crb.AlccConfig(max_seconds=1e-9, infeas_norm_tol=0.0),
+                                      bounds, crb.PrimalPoint(P.feas_y, P.feas_xi))
+    assert res.outer_iters == 1
+    assert res.reason == 2

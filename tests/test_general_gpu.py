@@ -147,3 +147,37 @@ def test_partition_errors(oracle):
             s.set_partition(15, feas)  # nbar = 2 < n + 1 (dataset.cpp:127-128)
         s.set_partition(30, feas)      # singleton: the closed form
         assert s.K == 0
+
+
+def test_general_k_dga(oracle):
+    """dual_gradient_ascent with K blocks (papg.cpp:292-296: no momentum)"""
+    X, P = problem(oracle, "sqnorm-uniform", 30, 2, 0.2, 12)
+    K = 3
+    sig = oracle.sigma_C_k(X, K)[0]
+    o = oracle.papg_k(X, P.ys, K, P.feas_y, P.feas_xi, inner=INNER, sigma_C=sig,
+                      use_momentum=False, max_iters=3, gap_norm_tol=-1.0, want_c_eta=True)
+    cfg = crb.PapgConfig(sigma_C=sig, K=K, inner=crb.AlccConfig(**INNER), max_iters=3,
+                         gap_norm_tol=-1.0)
+    with crb.DualSolver(X, P.ys, P.gamma) as s:
+        s.set_partition(K, crb.PrimalPoint(P.feas_y, P.feas_xi), cfg.inner)
+        s.begin(cfg, False)
+        s.iterate(1 << 40)
+        res, y, xi, hist = s.finish()
+        th = s.theta()
+    assert res.iters == o.iters
+    assert rel(th, o.theta) <= 1e-9
+    assert rel(y, o.y) <= 1e-8
+
+
+def test_general_k_gamma_continuation(oracle):
+    """runner-style continuation (runner.cpp:258-259): stage 2 at gamma/10
+    warm-started from stage 1's theta in the general cross ordering"""
+    from paper_1407_7220_b200 import runner as R
+    spec = crb.GeneratorSpec("sqnorm-uniform", 2, 30, 0.1, 13)
+    rep = R.run(R.RunConfig(generate=spec, K=3, max_iters=3, continuation=True,
+                            inner=crb.AlccConfig(**INNER)))
+    data = crb.gen_instance(spec)
+    raw, norm = oracle.infeasibility(data.xs, rep.solution.y, rep.solution.xi)
+    assert rep.final.infeas_raw == pytest.approx(raw, rel=1e-9, abs=1e-14)
+    assert 1 <= len(rep.history) <= 3
+    assert rep.final.reason in ("thresholds", "iter-budget")
