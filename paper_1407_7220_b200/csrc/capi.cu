@@ -270,8 +270,9 @@ cr_status cr_create(const double* Xh, const double* ybar_shifted, int64_t N, int
   ALLOC(h->V[0], vlen);
   ALLOC(h->V[1], vlen);
   if (h->sparse_ok) {
-    ALLOC(h->M[0], (size_t)h->T * h->R * kMaskWords);
-    ALLOC(h->M[1], (size_t)h->T * h->R * kMaskWords);
+    h->mstages = (int)((h->U + 7) / 8 + h->maxspan);
+    ALLOC(h->M[0], mask_words(h));
+    ALLOC(h->M[1], mask_words(h));
   }
   ALLOC(h->vpos[0], N);
   ALLOC(h->vpos[1], N);
@@ -592,8 +593,8 @@ cr_status begin_impl(cr_handle* h, const cr_papg_config* cfg, const double* thet
   }
   if (!resume) {
     if (h->masked) {
-      CUDA_TRY(cudaMemsetAsync(h->M[0], 0, sizeof(uint16_t) * h->T * h->R * kMaskWords, h->st));
-      CUDA_TRY(cudaMemsetAsync(h->M[1], 0, sizeof(uint16_t) * h->T * h->R * kMaskWords, h->st));
+      CUDA_TRY(cudaMemsetAsync(h->M[0], 0, sizeof(uint32_t) * mask_words(h), h->st));
+      CUDA_TRY(cudaMemsetAsync(h->M[1], 0, sizeof(uint32_t) * mask_words(h), h->st));
     }
     CUDA_TRY(cudaMemsetAsync(h->V[0], 0, vbytes, h->st));
     CUDA_TRY(cudaMemsetAsync(h->V[1], 0, vbytes, h->st));
@@ -627,7 +628,7 @@ cr_status begin_impl(cr_handle* h, const cr_papg_config* cfg, const double* thet
     CUDA_TRY(cudaMemcpyAsync(h->stage, tpos, sizeof(double) * N, cudaMemcpyHostToDevice, h->st));
     CUDA_TRY(launch_pos_in(h->vpos[0], h->stage, N, h->st));
     if (h->masked)
-      CUDA_TRY(launch_mask_build(h->V[0], h->M[0], N, h->ld, h->R, h->kp.tile_cols, h->T, h->st));
+      CUDA_TRY(launch_mask_build(h->V[0], h->M[0], N, h->ld, mask_geo(h), h->G, h->st));
     // aggregates and |.|^2 of max(theta0, 0): a sweep with 1/L = 0 is a copy
     const SweepArgs sa = sweep_args(h, kModePapg, true);
     CUDA_TRY((cudaError_t)launch_sweep(papg_sweep(h), sa, h->st));
@@ -992,7 +993,7 @@ cr_status cr_get_theta(cr_handle* h, double* out) {
   for (int64_t ra = 0; ra < h->R; ra += rows_per) {
     const int64_t rb = std::min(h->R, ra + rows_per);
     CUDA_TRY(launch_theta_out(h->stage, h->V[cur], sc, h->N, h->ld, h->r0, ra, rb, h->st,
-                              h->masked ? h->M[cur] : nullptr, h->R, h->kp.tile_cols));
+                              h->masked ? h->M[cur] : nullptr, mask_geo(h)));
     CUDA_TRY(cudaMemcpyAsync(out + ra * rowlen, h->stage, sizeof(double) * (rb - ra) * rowlen,
                              cudaMemcpyDeviceToHost, h->st));
     CUDA_TRY(cudaStreamSynchronize(h->st));
@@ -1094,7 +1095,7 @@ cr_status pair_metrics(cr_handle* h, PointBufs& b, bool with_theta, double out[2
   a.colrec = b.colrec;
   a.V = with_theta ? h->V[h->ctrl_h->cur] : nullptr;
   a.M = (with_theta && h->masked) ? h->M[h->ctrl_h->cur] : nullptr;
-  a.TC = h->kp.tile_cols;
+  a.mg = mask_geo(h);
   a.s = h->ctrl_h->s_cur;
   a.part = b.part;
   a.N = h->N;

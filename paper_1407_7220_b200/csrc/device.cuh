@@ -89,19 +89,46 @@ struct SweepArgs {
   int maxspan;            // max segments (tiles) one CTA can touch
   long long nbar;         // block size of the partition: pairs inside one block are
                           // masked like the diagonal (1: singleton blocks)
-  uint16_t* M0;           // masked dual store (sweep_sparse.cu): live bits of V[0], V[1]
-  uint16_t* M1;
+  uint32_t* M0;           // masked dual store (sweep_sparse.cu): live words of V[0], V[1]
+  uint32_t* M1;
+  int mstages;            // mask stage capacity per CTA (MaskGeo::stages)
 };
 
-// Masked dual store: per buffer, 16 uint16 words per (column tile t, local row r)
-// ([T][R][16], tile-major); bit b of word w = column t*TC + 16w + b is live.
-// A clear bit means 0 whatever V holds.
-constexpr int kMaskWords = 16;
-__host__ __device__ __forceinline__ bool mask_live(const uint16_t* M, long long R, int TC,
-                                                   long long r, long long col) {
-  const long long t = col / TC;
-  const int cl = (int)(col - t * TC);
-  return (M[(t * R + r) * kMaskWords + (cl >> 4)] >> (cl & 15)) & 1;
+// Masked dual store (sweep_sparse.cu): one 32-bit live word per 8-row x 8-column
+// MMA tile in the ballot order of its fragments (bit 4 c + q = column c, row
+// 2q + j of the tile, j selecting one of the tile's two words). Words are stored
+// per sweep CTA and per stage of that CTA's (static) unit range -- the split
+// is the same every iteration, so a CTA reads back exactly the words it wrote
+// and no word is shared between CTAs: [G][stages][TC/4] per buffer. A clear
+// bit means 0 whatever V holds.
+struct MaskGeo {
+  long long R, U;  // rows of the shard, (tile, row) units per sweep CTA
+  int TC;          // columns per tile
+  int stages;      // stage capacity per CTA (ceil(U/8) + segments)
+};
+__host__ __device__ __forceinline__ long long mask_word(const MaskGeo& g, long long r,
+                                                       long long col, int* bit) {
+  const long long t = col / g.TC;
+  const int cl = (int)(col - t * g.TC);
+  const long long u = t * g.R + r;
+  const long long cta = u / g.U;
+  const long long u0 = cta * g.U, u1 = u0 + g.U;
+  long long k = 0;
+  for (long long tt = u0 / g.R; tt < t; ++tt) {  // stages of the CTA's earlier segments
+    const long long lo = (u0 > tt * g.R ? u0 : tt * g.R), hi = (u1 < (tt + 1) * g.R ? u1 : (tt + 1) * g.R);
+    k += (hi - lo + 7) / 8;
+  }
+  const long long rs = (u0 > t * g.R ? u0 : t * g.R) - t * g.R;
+  k += (r - rs) / 8;
+  const int rr = (int)((r - rs) % 8);
+  *bit = 4 * (cl & 7) + (rr >> 1);
+  return (cta * g.stages + k) * (g.TC / 4) + (cl >> 3) * 2 + (rr & 1);
+}
+__host__ __device__ __forceinline__ bool mask_live(const uint32_t* M, const MaskGeo& g, long long r,
+                                                   long long col) {
+  int bit;
+  const long long w = mask_word(g, r, col, &bit);
+  return (M[w] >> bit) & 1u;
 }
 
 // same block of the partition. BLK = false: singleton blocks (the diagonal);

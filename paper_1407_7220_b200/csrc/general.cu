@@ -170,12 +170,12 @@ __device__ __forceinline__ void cross_pair(long long idx, long long K, long long
 
 __global__ void theta_k_out_kernel(double* stage, const double* V, double s, long long K,
                                    long long nbar, long long ld, long long a, long long b,
-                                   const uint16_t* M, long long R, int TC) {
+                                   const uint32_t* M, MaskGeo mg) {
   for (long long i = a + (long long)blockIdx.x * blockDim.x + threadIdx.x; i < b;
        i += (long long)gridDim.x * blockDim.x) {
     long long l1, l2;
     cross_pair(i, K, nbar, &l1, &l2);
-    const bool live = M == nullptr || mask_live(M, R, TC, l1, l2);
+    const bool live = M == nullptr || mask_live(M, mg, l1, l2);
     stage[i - a] = live ? s * V[l1 * ld + l2] : 0.0;
   }
 }
@@ -498,8 +498,8 @@ cr_status general_get_theta(cr_handle* h, double* out) {
   for (long long a = 0; a < cross; a += h->stage_elems) {
     const long long b = std::min<long long>(cross, a + h->stage_elems);
     theta_k_out_kernel<<<grid_of(b - a), 256, 0, h->st>>>(
-        h->stage, h->V[cur], sc, P.K, P.nbar, h->ld, a, b, h->masked ? h->M[cur] : nullptr, h->R,
-        h->kp.tile_cols);
+        h->stage, h->V[cur], sc, P.K, P.nbar, h->ld, a, b, h->masked ? h->M[cur] : nullptr,
+        mask_geo(h));
     CUDA_TRY(cudaGetLastError());
     CUDA_TRY(cudaMemcpyAsync(out + a, h->stage, sizeof(double) * (b - a), cudaMemcpyDeviceToHost,
                              h->st));

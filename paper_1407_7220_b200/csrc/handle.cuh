@@ -125,7 +125,8 @@ struct cr_handle {
   double last_seconds = 0, last_sweep_seconds = 0;
   int64_t last_launches = 0;
   // masked dual store (sweep_sparse.cu): live-bit words of V[0], V[1]
-  uint16_t* M[2] = {nullptr, nullptr};
+  uint32_t* M[2] = {nullptr, nullptr};
+  int mstages = 0;          // MaskGeo::stages
   bool sparse_ok = false;   // the masked P-APG sweep is available (MMA geometry)
   bool masked = false;      // this solve runs it (not the small-N loop)
   SweepKernelInfo ksp{};
@@ -201,7 +202,14 @@ inline SweepArgs sweep_args(cr_handle* h, int mode, bool agg_only) {
   a.nbar = h->part.K > 0 ? h->part.nbar : 1;
   a.M0 = h->M[0];
   a.M1 = h->M[1];
+  a.mstages = h->mstages;
   return a;
+}
+inline MaskGeo mask_geo(const cr_handle* h) {
+  return MaskGeo{h->R, h->U, h->kp.tile_cols, h->mstages};
+}
+inline size_t mask_words(const cr_handle* h) {
+  return (size_t)h->G * h->mstages * (h->kp.tile_cols / 4);
 }
 // the P-APG sweep of this solve: masked (sparse) or dense
 inline const SweepKernelInfo& papg_sweep(const cr_handle* h) { return h->masked ? h->ksp : h->kp; }

@@ -225,32 +225,50 @@ __global__ void theta_in_kernel(const double* stage, double* V, long long N, lon
 
 __global__ void theta_out_kernel(double* stage, const double* V, double s, long long N,
                                  long long ld, long long r0, long long ra, long long rb,
-                                 const uint16_t* M, long long R, int TC) {
+                                 const uint32_t* M, MaskGeo mg) {
   const long long total = (rb - ra) * (N - 1);
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
        i += (long long)gridDim.x * blockDim.x) {
     const long long lr = i / (N - 1), k = i % (N - 1);
     const long long gr = r0 + ra + lr;
     const long long c = k + (k >= gr ? 1 : 0);
-    const bool live = M == nullptr || mask_live(M, R, TC, ra + lr, c);
+    const bool live = M == nullptr || mask_live(M, mg, ra + lr, c);
     stage[i] = live ? s * V[(ra + lr) * ld + c] : 0.0;
   }
 }
 
-__global__ void mask_build_kernel(const double* V, uint16_t* M, long long N, long long ld,
-                                  long long R, int TC, int T) {
-  const long long total = (long long)T * R * kMaskWords;
+// one thread per stage word: enumerate the CTA's stages to find the tile and rows
+__global__ void mask_build_kernel(const double* V, uint32_t* M, long long N, long long ld,
+                                  MaskGeo mg, int G) {
+  const int wpst = mg.TC / 4;  // words per stage
+  const long long total = (long long)G * mg.stages * wpst;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
        i += (long long)gridDim.x * blockDim.x) {
-    const int w = (int)(i % kMaskWords);
-    const long long tr = i / kMaskWords;
-    const long long r = tr % R, t = tr / R;
-    uint32_t bits = 0;
-    for (int b = 0; b < 16; ++b) {
-      const long long c = t * TC + 16 * w + b;
-      if (16 * w + b < TC && c < N && c < ld && V[r * ld + c] > 0.0) bits |= 1u << b;
+    const int w = (int)(i % wpst);
+    const long long ks = i / wpst;
+    const long long k = ks % mg.stages, cta = ks / mg.stages;
+    const long long u0 = cta * mg.U, u1 = u0 + mg.U;
+    long long left = k;
+    long long t = u0 / mg.R, r = -1;
+    for (; t * mg.R < u1 && r < 0; ++t) {
+      const long long lo = (u0 > t * mg.R ? u0 : t * mg.R) - t * mg.R;
+      const long long hi = (u1 < (t + 1) * mg.R ? u1 : (t + 1) * mg.R) - t * mg.R;
+      const long long ns = hi > lo ? (hi - lo + 7) / 8 : 0;
+      if (left < ns) r = lo + 8 * left;
+      else left -= ns;
     }
-    M[i] = (uint16_t)bits;
+    uint32_t bits = 0;
+    if (r >= 0) {
+      --t;
+      const long long hi = (u1 < (t + 1) * mg.R ? u1 : (t + 1) * mg.R) - t * mg.R;
+      const int tl = w >> 1, j = w & 1;
+      for (int b = 0; b < 32; ++b) {
+        const long long rr = r + 2 * (b & 3) + j;
+        const long long c = t * mg.TC + tl * 8 + (b >> 2);
+        if (rr < hi && c < N && c < ld && V[rr * ld + c] > 0.0) bits |= 1u << b;
+      }
+    }
+    M[i] = bits;
   }
 }
 
@@ -371,16 +389,16 @@ cudaError_t launch_theta_in(const double* stage, double* V, long long N, long lo
 
 cudaError_t launch_theta_out(double* stage, const double* V, double sc, long long N,
                              long long ld, long long r0, long long ra, long long rb,
-                             cudaStream_t s, const uint16_t* M, long long R, int TC) {
+                             cudaStream_t s, const uint32_t* M, MaskGeo mg) {
   theta_out_kernel<<<grid_for((rb - ra) * (N - 1), 256, 4096), 256, 0, s>>>(stage, V, sc, N, ld,
-                                                                            r0, ra, rb, M, R, TC);
+                                                                            r0, ra, rb, M, mg);
   return cudaGetLastError();
 }
 
-cudaError_t launch_mask_build(const double* V, uint16_t* M, long long N, long long ld,
-                              long long R, int TC, int T, cudaStream_t s) {
-  mask_build_kernel<<<grid_for((long long)T * R * kMaskWords, 256, 4096), 256, 0, s>>>(
-      V, M, N, ld, R, TC, T);
+cudaError_t launch_mask_build(const double* V, uint32_t* M, long long N, long long ld,
+                              MaskGeo mg, int G, cudaStream_t s) {
+  mask_build_kernel<<<grid_for((long long)G * mg.stages * (mg.TC / 4), 256, 4096), 256, 0, s>>>(
+      V, M, N, ld, mg, G);
   return cudaGetLastError();
 }
 

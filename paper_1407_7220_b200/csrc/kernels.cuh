@@ -77,8 +77,8 @@ struct MetricsArgs {
   const double* rowrec;  // N x RQ records of the point (x, 1, y)
   const double* colrec;  // N x RQ (-xi, -c, 1)
   const double* V;       // optional: theta1 = s V (local rows) for the duality gap
-  const uint16_t* M;     // optional live bits of V (masked store), TC its tile width
-  int TC;
+  const uint32_t* M;     // optional live words of V (masked store)
+  MaskGeo mg;
   double s;
   double* part;          // [grid][2]: (sum min(row,0)^2, sum theta.row)
   long long N, R, r0, ld;
@@ -109,11 +109,10 @@ cudaError_t launch_theta_in(const double* stage, double* V, long long N, long lo
                             long long r0, long long ra, long long rb, cudaStream_t s);
 cudaError_t launch_theta_out(double* stage, const double* V, double sc, long long N,
                              long long ld, long long r0, long long ra, long long rb,
-                             cudaStream_t s, const uint16_t* M = nullptr, long long R = 0,
-                             int TC = 0);
-// live-bit words of a dense V (entries > 0), [T][R][16]
-cudaError_t launch_mask_build(const double* V, uint16_t* M, long long N, long long ld,
-                              long long R, int TC, int T, cudaStream_t s);
+                             cudaStream_t s, const uint32_t* M = nullptr, MaskGeo mg = {});
+// live words of a dense V (entries > 0) in the masked-store layout (device.cuh)
+cudaError_t launch_mask_build(const double* V, uint32_t* M, long long N, long long ld,
+                              MaskGeo mg, int G, cudaStream_t s);
 cudaError_t launch_rows_out(double* stage, const double* rowrec, const double* colrec,
                             long long N, int n, long long r0, long long ra, long long rb,
                             cudaStream_t s);

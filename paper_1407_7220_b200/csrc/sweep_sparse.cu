@@ -4,10 +4,11 @@
 // After a few dozen iterations almost every pair multiplier is exactly zero
 // (cfg 2: 16 % nonzero at iteration 20, 3 % at 100, 0.2 % at 2000; the
 // projection max(., 0) keeps inactive constraints at 0). The dense sweep still
-// streams 24 B per pair. Here the dual store keeps its dense value layout but
-// every 16 columns of a row carry a 16-bit mask (bit set = the value is live;
-// clear = 0 whatever the memory holds), stored tile-major ([T][R][16] per
-// buffer) so a stage's masks are one 256 B TMA copy. Per pair the residual is
+// streams 24 B per pair. Here the dual store keeps its dense value layout plus
+// one 32-bit live word per 8x8 MMA tile in the fragments' ballot order (bit =
+// lane: a live test is one shift, the new word is one ballot), stored per CTA
+// and stage of the static work split (device.cuh MaskGeo), so a stage's words
+// are one contiguous TMA copy and no word is shared by two CTAs. Per pair the residual is
 // still evaluated on the tensor cores (every constraint is checked every
 // iteration); values move only where live:
 //   producer   TMA ring (8 deep, small): row records + the two mask blocks
@@ -35,19 +36,23 @@ namespace {
 constexpr int kLook = 2;        // value gathers are issued this many stages ahead
 constexpr int kNA = 8;          // TMA ring (row records + masks): deep, it is small
 constexpr int kNB = kLook + 1;  // value ring (per-warp columns, filled by cp.async)
-constexpr int kMW = 16;         // mask halfwords per tile row (kTC / 16, padded): 32 B
+#ifndef CRB_SP_CW
+#define CRB_SP_CW 7             // consumer warps for n <= 12 (7 x 4 tiles or 14 x 2)
+#endif
 
 // Geometry: the dense kernel's column tiles (224 columns for n <= 12, 240
 // above) split over twice as many warps, 2 MMA tiles each -- without the HBM
 // stream the sweep is latency bound and needs the warps (measured: 7 consumer
 // warps x 4 tiles leave 28 % issue utilisation).
 template <int NN>
-__host__ __device__ constexpr int sp_cw() { return NN <= 12 ? 14 : 15; }
+__host__ __device__ constexpr int sp_cw() { return NN <= 12 ? CRB_SP_CW : 15; }
+template <int NN>
+__host__ __device__ constexpr int sp_ct() { return NN <= 12 ? 28 / CRB_SP_CW : 2; }
 template <int NN>
 __host__ __device__ constexpr int sp_threads() { return (sp_cw<NN>() + 1) * 32; }
 #define SP_GEO(NN)                               \
   constexpr int kCW = sp_cw<NN>();               \
-  constexpr int kCT = 2;                         \
+  constexpr int kCT = sp_ct<NN>();               \
   constexpr int kW = 8 * kCT;                    \
   constexpr int kTC = kCW * kW;                  \
   constexpr int kTCP = kTC + 2;                  \
@@ -56,8 +61,8 @@ __host__ __device__ constexpr int sp_threads() { return (sp_cw<NN>() + 1) * 32; 
   static_assert(kTC == mma_cw<NN>() * 8 * mma_ct<NN>(), "same column tiles as the dense sweep");
 
 template <int NN>
-__host__ __device__ constexpr int ringA_doubles() {  // row records + masks of V, V'
-  return kTR * rec_pitch(NN) + 2 * kTR * kMW / 4;
+__host__ __device__ constexpr int ringA_doubles() {  // row records + live words of V, V'
+  return kTR * rec_pitch(NN) + 2 * (mma_cw<NN>() * mma_ct<NN>() * 2) / 2;
 }
 template <int NN>
 __host__ __device__ constexpr int ringB_doubles() {  // V, V' values of a stage
@@ -79,15 +84,6 @@ __device__ __forceinline__ void cp_async_commit() {
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-
-// bits 4k + q of a ballot (k = 0..7) -> 8 contiguous bits
-__device__ __forceinline__ uint32_t gather_q(uint32_t b, int q) {
-  uint32_t e = (b >> q) & 0x11111111u;
-  e = (e | (e >> 3)) & 0x03030303u;
-  e = (e | (e >> 6)) & 0x000F000Fu;
-  e = (e | (e >> 12)) & 0xFFu;
-  return e;
 }
 
 // stage enumeration shared by producer and consumers: segment (tile t, rows
@@ -122,11 +118,13 @@ __device__ __forceinline__ void sp_stage(const double* __restrict__ sv, const do
                                          const double* __restrict__ srec, double* gout, long long ld,
                                          long long gcol0, long long grow0, int nr, long long ncols,
                                          long long nbar, int lane,
-                                         const double (&A)[2][ksteps<NN>()],
-                                         double (&D)[2][fblocks<NN>()][2],
-                                         const double (&Cc)[2], const MCoef& cf,
-                                         MScal& sc, double (&rs)[2], uint32_t (&mw)[2],
-                                         const uint32_t (&lc)[2], const uint32_t (&lp)[2]) {
+                                         const double (&A)[sp_ct<NN>()][ksteps<NN>()],
+                                         double (&D)[sp_ct<NN>()][fblocks<NN>()][2],
+                                         const double (&Cc)[sp_ct<NN>()], const MCoef& cf,
+                                         MScal& sc, double (&rs)[2],
+                                         uint32_t (&mw)[2 * sp_ct<NN>()],
+                                         const uint32_t (&wc)[2 * sp_ct<NN>()],
+                                         const uint32_t (&wp)[2 * sp_ct<NN>()]) {
   SP_GEO(NN)
   constexpr int KS = ksteps<NN>();
   constexpr int FB = fblocks<NN>();
@@ -134,14 +132,43 @@ __device__ __forceinline__ void sp_stage(const double* __restrict__ sv, const do
   constexpr bool SPLIT = split_yc<NN>();
   const int q = lane & 3;
   const int c8 = lane >> 2;
+  double B[KS];
+#pragma unroll
+  for (int ks = 0; ks < KS; ++ks) B[ks] = srec[c8 * RQ + ks * 4 + q];
+  rs[0] = rs[1] = 0.0;
+  // residuals of every tile first: independent DMMA chains interleave
+  double dd[kCT][2];
+#pragma unroll
+  for (int ct = 0; ct < kCT; ++ct) dd[ct][0] = dd[ct][1] = 0.0;
+#pragma unroll
+  for (int ks = 0; ks < KS; ++ks) {
+#pragma unroll
+    for (int ct = 0; ct < kCT; ++ct) dmma(dd[ct][0], dd[ct][1], A[ct][ks], B[ks]);
+  }
   double yr[2] = {0.0, 0.0};
   if (SPLIT) {
     yr[0] = srec[(2 * q) * RQ + NN + 1];
     yr[1] = srec[(2 * q + 1) * RQ + NN + 1];
   }
-  double B[KS];
+  // whole warp-stage cold (no live multiplier, no violated constraint): every
+  // contribution is an exact zero
+  {
+    bool any = false;
 #pragma unroll
-  for (int ks = 0; ks < KS; ++ks) B[ks] = srec[c8 * RQ + ks * 4 + q];
+    for (int ct = 0; ct < kCT; ++ct) {
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        double row = dd[ct][j];
+        if (SPLIT) row += yr[j] + Cc[ct];
+        any |= row < 0.0 || (((wc[2 * ct + j] | wp[2 * ct + j]) >> lane) & 1u);
+      }
+    }
+    if (!__any_sync(0xffffffffu, any)) {
+#pragma unroll
+      for (int k = 0; k < 2 * kCT; ++k) mw[k] = 0u;
+      return;
+    }
+  }
   double Ag[2][FB];
 #pragma unroll
   for (int j = 0; j < 2; ++j) {
@@ -149,13 +176,8 @@ __device__ __forceinline__ void sp_stage(const double* __restrict__ sv, const do
 #pragma unroll
     for (int fb = 0; fb < FB; ++fb) Ag[j][fb] = rv ? srec[(2 * q + j) * RQ + fb * 8 + c8] : 0.0;
   }
-  rs[0] = rs[1] = 0.0;
-  mw[0] = mw[1] = 0u;
 #pragma unroll
   for (int ct = 0; ct < kCT; ++ct) {
-    double d0 = 0.0, d1 = 0.0;
-#pragma unroll
-    for (int ks = 0; ks < KS; ++ks) dmma(d0, d1, A[ct][ks], B[ks]);
     const int cl = ct * 8 + c8;
     double rows[2];
     bool hot = false;
@@ -163,25 +185,28 @@ __device__ __forceinline__ void sp_stage(const double* __restrict__ sv, const do
     for (int j = 0; j < 2; ++j) {
       const int rr = 2 * q + j;
       const bool rv = !MASK || rr < nr;
-      double row = j == 0 ? d0 : d1;
+      double row = dd[ct][j];
       if (SPLIT) row += yr[j] + Cc[ct];
       if (MASK && (same_block<BLK>(gcol0 + cl, grow0 + rr, nbar) || !rv || gcol0 + cl >= ncols))
         row = 0.0;
       rows[j] = row;
-      hot |= row < 0.0 || (((lc[j] | lp[j]) >> cl) & 1u);
+      hot |= row < 0.0 || (((wc[2 * ct + j] | wp[2 * ct + j]) >> lane) & 1u);
     }
     // a tile with no live multiplier and no violated constraint has v = 0 and
     // contributes exact zeros to every sum: nothing to do
-    if (!__any_sync(0xffffffffu, hot)) continue;
+    if (!__any_sync(0xffffffffu, hot)) {
+      mw[2 * ct] = mw[2 * ct + 1] = 0u;
+      continue;
+    }
     double v[2];
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
       const int rr = 2 * q + j;
       const bool rv = !MASK || rr < nr;
       const double row = rows[j];
-      // live bits of this warp's columns in rows 2q, 2q+1 (clear: exactly 0)
-      const double c1 = ((lc[j] >> cl) & 1u) ? sv[rr * kTCP + cl] : 0.0;
-      const double p1 = ((lp[j] >> cl) & 1u) ? svp[rr * kTCP + cl] : 0.0;
+      // live bits of this lane's element (clear: exactly 0)
+      const double c1 = ((wc[2 * ct + j] >> lane) & 1u) ? sv[rr * kTCP + cl] : 0.0;
+      const double p1 = ((wp[2 * ct + j] >> lane) & 1u) ? svp[rr * kTCP + cl] : 0.0;
       double th2;
       if (UNIT) {
         th2 = fma(cf.beta, c1 - p1, c1);
@@ -198,8 +223,7 @@ __device__ __forceinline__ void sp_stage(const double* __restrict__ sv, const do
       sc.nn = fma(m, m, sc.nn);
       const bool live = v[j] > 0.0;
       if (rv && live) st_stream(gout + rr * ld + cl, v[j]);
-      const uint32_t b = __ballot_sync(0xffffffffu, live);
-      mw[j] |= gather_q(b, q) << (8 * ct);
+      mw[2 * ct + j] = __ballot_sync(0xffffffffu, live);
       rs[j] += v[j];
     }
     // an all-zero 8x8 tile adds nothing to the aggregates
@@ -221,7 +245,7 @@ __global__ void __launch_bounds__(sp_threads<NN>(), 1) sweep_sparse_kernel(const
   constexpr int RQ = rec_pitch(NN);
   constexpr int SA = ringA_doubles<NN>();
   constexpr int SB = ringB_doubles<NN>();
-  static_assert(kTC / 16 <= kMW, "mask tile row");
+  static_assert((2 * kCT) % 4 == 0 && (kTC / 4) % 4 == 0, "16-byte word groups");
   extern __shared__ __align__(128) double smem[];
   double* ringA = smem;                      // [kNA][records | masks]
   double* ringB = ringA + kNA * SA;          // [kNB][V | V']
@@ -233,8 +257,8 @@ __global__ void __launch_bounds__(sp_threads<NN>(), 1) sweep_sparse_kernel(const
   const int cur = *a.cur;
   const double* Vc = cur ? a.V1 : a.V0;
   double* Vp = cur ? a.V0 : a.V1;
-  const uint16_t* Mc = cur ? a.M1 : a.M0;
-  uint16_t* Mp = cur ? a.M0 : a.M1;
+  const uint32_t* Mc = cur ? a.M1 : a.M0;
+  uint32_t* Mp = cur ? a.M0 : a.M1;
 
   const long long units = (long long)a.T * a.R;
   const long long u0 = (long long)blockIdx.x * a.U;
@@ -263,13 +287,13 @@ __global__ void __launch_bounds__(sp_threads<NN>(), 1) sweep_sparse_kernel(const
         if (i >= kNA) mbar_wait_sleep(&empty[s], (uint32_t)(((i / kNA) - 1) & 1));
         const int nr = it.nr();
         double* st = ringA + s * SA;
-        const uint32_t mbytes = (uint32_t)nr * kMW * 2u;
+        const uint32_t mbytes = (uint32_t)kTC;  // kTC / 4 words
         mbar_arrive_expect_tx(&full[s], (uint32_t)nr * RQ * 8u + 2u * mbytes);
         bulk_g2s(st, a.rowrec + (a.r0 + it.r) * RQ, (uint32_t)nr * RQ * 8u, &full[s], pol_keep);
-        const long long mo = ((long long)it.t * a.R + it.r) * kMW;
-        uint16_t* sm = reinterpret_cast<uint16_t*>(st + kTR * RQ);
+        const long long mo = ((long long)blockIdx.x * a.mstages + i) * (kTC / 4);
+        uint32_t* sm = reinterpret_cast<uint32_t*>(st + kTR * RQ);
         bulk_g2s(sm, Mc + mo, mbytes, &full[s], pol_stream);
-        bulk_g2s(sm + kTR * kMW, Mp + mo, mbytes, &full[s], pol_stream);
+        bulk_g2s(sm + kTC / 4, Mp + mo, mbytes, &full[s], pol_stream);
       }
     }
     return;
@@ -281,31 +305,27 @@ __global__ void __launch_bounds__(sp_threads<NN>(), 1) sweep_sparse_kernel(const
   MCoef cf{a.coef[0], a.coef[1], a.coef[2], a.invL, 0.0};
   const bool unit_scale = (cf.s_c == 1.0) && (cf.s_p == 1.0);
   MScal sc{0.0, 0.0, 0.0, 0.0};
-  const int w0 = warp * kW / 16;  // first mask halfword of this warp's columns
 
   // gather the live values of stage j (this warp's columns) into value slot j % kNB:
-  // two lanes per (row, buffer), 16 columns each, one cp.async per live bit
+  // one lane per live word (buffer, tile, j), one cp.async per set bit
+  const int wbase = warp * kCT * 2;  // this warp's first word of a stage
   auto issue = [&](int j, const StageIt& jt) {
     const int s = j % kNA;
     mbar_wait(&full[s], (uint32_t)((j / kNA) & 1));
-    const uint16_t* sm = reinterpret_cast<const uint16_t*>(ringA + s * SA + kTR * RQ);
+    const uint32_t* sm = reinterpret_cast<const uint32_t*>(ringA + s * SA + kTR * RQ);
     double* vb = ringB + (j % kNB) * SB;
-    const int nr = jt.nr();
     const long long gcol0 = (long long)jt.t * kTC + warp * kW;
-    constexpr int kHalves = kW / 16;               // 2 (n <= 12) or 1
-    const int slot = kHalves == 2 ? (lane >> 1) : lane;  // (buffer, row) pair
-    const int half = kHalves == 2 ? (lane & 1) : 0;
-    if (slot < 2 * kTR) {
-      const int buf = slot / kTR, rr = slot % kTR;
-      if (rr < nr) {
-        uint32_t word = sm[buf * kTR * kMW + rr * kMW + w0 + half];
-        const double* src = (buf == 0 ? Vc : Vp) + (jt.r + rr) * a.ld + gcol0 + 16 * half;
-        double* dst = vb + buf * kTR * kTCP + rr * kTCP + warp * kW + 16 * half;
-        while (word) {
-          const int b = __ffs(word) - 1;
-          word &= word - 1;
-          cp_async8(dst + b, src + b);
-        }
+    if (lane < 4 * kCT) {
+      const int buf = lane / (2 * kCT), rem = lane % (2 * kCT);
+      const int ct = rem >> 1, jj = rem & 1;
+      uint32_t word = sm[buf * (kTC / 4) + wbase + rem];
+      const double* src = (buf == 0 ? Vc : Vp) + (jt.r + jj) * a.ld + gcol0 + ct * 8;
+      double* dst = vb + buf * kTR * kTCP + jj * kTCP + warp * kW + ct * 8;
+      while (word) {
+        const int b = __ffs(word) - 1;
+        word &= word - 1;
+        const int qq = b & 3, cc = b >> 2;  // row 2 qq + jj, column cc of the tile
+        cp_async8(dst + 2 * qq * kTCP + cc, src + 2 * qq * a.ld + cc);
       }
     }
     cp_async_commit();
@@ -366,21 +386,17 @@ __global__ void __launch_bounds__(sp_threads<NN>(), 1) sweep_sparse_kernel(const
     uint32_t mw[2] = {0u, 0u};
     if (active) {
       const double* sa = ringA + s * SA;
-      const uint16_t* sm = reinterpret_cast<const uint16_t*>(sa + kTR * RQ);
+      const uint32_t* sm = reinterpret_cast<const uint32_t*>(sa + kTR * RQ);
       const double* vb = ringB + (i % kNB) * SB;
       const double* sv = vb + warp * kW;
       const double* svp = vb + kTR * kTCP + warp * kW;
-      uint32_t lc[2], lp[2];
+      uint32_t wc[2 * kCT], wp[2 * kCT], mw[2 * kCT];
 #pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        const int rr = 2 * q + j;
-        if (kW == 32) {
-          lc[j] = *reinterpret_cast<const uint32_t*>(sm + rr * kMW + w0);
-          lp[j] = *reinterpret_cast<const uint32_t*>(sm + kTR * kMW + rr * kMW + w0);
-        } else {
-          lc[j] = sm[rr * kMW + w0];
-          lp[j] = sm[kTR * kMW + rr * kMW + w0];
-        }
+      for (int k = 0; k < 2 * kCT; k += 4) {  // 16-byte words groups (broadcast)
+        const uint4 c4 = *reinterpret_cast<const uint4*>(sm + wbase + k);
+        const uint4 p4 = *reinterpret_cast<const uint4*>(sm + kTC / 4 + wbase + k);
+        wc[k] = c4.x, wc[k + 1] = c4.y, wc[k + 2] = c4.z, wc[k + 3] = c4.w;
+        wp[k] = p4.x, wp[k + 1] = p4.y, wp[k + 2] = p4.z, wp[k + 3] = p4.w;
       }
       double* gout = Vp + r * a.ld + gcol0;
       const long long grow0 = a.r0 + r;
@@ -389,29 +405,24 @@ __global__ void __launch_bounds__(sp_threads<NN>(), 1) sweep_sparse_kernel(const
       if (clean) {
         if (unit_scale)
           sp_stage<NN, false, true, BLK>(sv, svp, sa, gout, a.ld, gcol0, grow0, nr, a.N, a.nbar,
-                                         lane, A, D, Cc, cf, sc, rsj, mw, lc, lp);
+                                         lane, A, D, Cc, cf, sc, rsj, mw, wc, wp);
         else
           sp_stage<NN, false, false, BLK>(sv, svp, sa, gout, a.ld, gcol0, grow0, nr, a.N, a.nbar,
-                                          lane, A, D, Cc, cf, sc, rsj, mw, lc, lp);
+                                          lane, A, D, Cc, cf, sc, rsj, mw, wc, wp);
       } else {
         if (unit_scale)
           sp_stage<NN, true, true, BLK>(sv, svp, sa, gout, a.ld, gcol0, grow0, nr, a.N, a.nbar,
-                                        lane, A, D, Cc, cf, sc, rsj, mw, lc, lp);
+                                        lane, A, D, Cc, cf, sc, rsj, mw, wc, wp);
         else
           sp_stage<NN, true, false, BLK>(sv, svp, sa, gout, a.ld, gcol0, grow0, nr, a.N, a.nbar,
-                                         lane, A, D, Cc, cf, sc, rsj, mw, lc, lp);
+                                         lane, A, D, Cc, cf, sc, rsj, mw, wc, wp);
       }
-      // new masks of rows 2q, 2q+1 for this warp's columns (lanes with c8 = 0)
-      if (c8 == 0) {
-        uint16_t* mrow = Mp + ((long long)t * a.R + r) * kMW + w0;
+      // the stage's new live words of this warp (one ballot per tile and row parity)
+      if (lane == 0) {
+        uint32_t* dst = Mp + ((long long)blockIdx.x * a.mstages + i) * (kTC / 4) + wbase;
 #pragma unroll
-        for (int j = 0; j < 2; ++j) {
-          const int rr = 2 * q + j;
-          if (rr < nr) {
-            if (kW == 32) *reinterpret_cast<uint32_t*>(mrow + rr * kMW) = mw[j];
-            else mrow[rr * kMW] = (uint16_t)mw[j];
-          }
-        }
+        for (int k = 0; k < 2 * kCT; k += 4)
+          *reinterpret_cast<uint4*>(dst + k) = make_uint4(mw[k], mw[k + 1], mw[k + 2], mw[k + 3]);
       }
     }
     __syncwarp();
@@ -518,8 +529,5 @@ using SpAll = SpTable<1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16, 17,
 }  // namespace
 
 SweepKernelInfo sweep_sparse_info(int n, bool blocked) { return SpAll::info(n, blocked); }
-
-// mask index of (local row r, column c) in the tile-major layout of the handle
-int sparse_mask_words() { return kMW; }
 
 }  // namespace crb
