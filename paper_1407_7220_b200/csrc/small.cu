@@ -123,7 +123,8 @@ __global__ void __launch_bounds__(kSBlock) small_loop_kernel(const SmallArgs a) 
             }
             const double uu = fma(-row, invL, th2);
             const double v = uu > 0.0 ? uu : 0.0;
-            if (valid) __stcg(Vp + r * a.ld + col, v);
+            if (valid && __double_as_longlong(v) != __double_as_longlong(p1))  // unchanged: no store
+              __stcg(Vp + r * a.ld + col, v);
             vv = fma(v, v, vv);
             vr = fma(v, row, vr);
             tr = fma(th2, row, tr);

@@ -168,8 +168,15 @@ __device__ __forceinline__ void run_stage(const StageView& sv, int nr, int lane,
         for (int j = 0; j < NN; ++j) cs.acc[k][1 + j] = fma(v, x[j], cs.acc[k][1 + j]);
         rs += v;
       }
-      if (MODE == kModePapg || MODE == kModePenaltyUpdate)
-        st_stream(reinterpret_cast<VT*>(sv.gout + q * sv.ld), out);
+      if (MODE == kModePenaltyUpdate) st_stream(reinterpret_cast<VT*>(sv.gout + q * sv.ld), out);
+      if (MODE == kModePapg) {
+        // v goes into the buffer that holds vp (theta1_prev): skip unchanged values
+        bool changed = false;
+#pragma unroll
+        for (int k = 0; k < C; ++k)
+          changed |= __double_as_longlong(vget(out, k)) != __double_as_longlong(vget(vp, k));
+        if (changed) st_stream(reinterpret_cast<VT*>(sv.gout + q * sv.ld), out);
+      }
       rs += __shfl_xor_sync(0xffffffffu, rs, 16);
       if (lane < 16) sv.srs[q * kRsPitch + lane] = rs;
     }

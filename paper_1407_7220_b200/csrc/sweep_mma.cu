@@ -100,7 +100,10 @@ __device__ __forceinline__ void mma_stage(const double* __restrict__ sv, const d
         sc.tr = fma(th2, row, sc.tr);
         const double m = keep_if_neg(row);
         sc.nn = fma(m, m, sc.nn);
-        if (rv) st_stream(gout + rr * ld + cl, v[j]);
+        // v goes into the buffer that holds p1 (theta1_prev): an unchanged value
+        // (late in a solve almost every pair stays 0) needs no store
+        if (rv && __double_as_longlong(v[j]) != __double_as_longlong(p1))
+          st_stream(gout + rr * ld + cl, v[j]);
       } else if (MODE == kModePenalty || MODE == kModePenaltyUpdate) {
         const double th = (MASK && !rv) ? 0.0 : sv[rr * kTCP + cl];
         v[j] = keep_if_nonneg(th - row);
