@@ -18,6 +18,7 @@ LIB = os.path.join(PKG, "libcvxreg_b200.so")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+                     *os.environ.get("CRB_NVCC_EXTRA", "").split(),
                      "-Xcompiler", "-ffp-contract=off", "-I" + os.path.join(ROOT, "include")]
 CXX_FLAGS = ["-O2", "-std=c++17", "-fPIC", "-ffp-contract=off", "-Wall", "-Wextra",
              "-I" + os.path.join(ROOT, "include")]

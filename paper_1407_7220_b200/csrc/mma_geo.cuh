@@ -7,13 +7,17 @@
 
 namespace crb {
 
-// CTA geometry per n (measured, profiles/): n <= 12: 7 consumer warps x 4
-// tiles (8 warps -> 255-register cap); n > 12: 15 consumer warps x 2 tiles
-// (16 warps, 128 registers) -- more warps hide the longer DMMA chains.
+// CTA geometry per n (measured on B200 with the store-skipping sweep, N = 1e4,
+// late iterations): 7 consumer warps x 4 tiles (8 warps,
+// 255-register cap) or 15 consumer warps x 2 tiles (16 warps, 128 registers,
+// more warps to hide the longer DMMA chains): the wide form wins for n = 9, 10
+// (387 vs 404 us) and n > 12, the narrow one elsewhere (n = 5: 363 vs 388 us).
 template <int NN>
-__host__ __device__ constexpr int mma_cw() { return NN <= 12 ? 7 : 15; }  // consumer warps
+__host__ __device__ constexpr bool mma_wide() { return NN > 12 || NN == 9 || NN == 10; }
 template <int NN>
-__host__ __device__ constexpr int mma_ct() { return NN <= 12 ? 4 : 2; }   // 8-col tiles / warp
+__host__ __device__ constexpr int mma_cw() { return mma_wide<NN>() ? 15 : 7; }  // consumer warps
+template <int NN>
+__host__ __device__ constexpr int mma_ct() { return mma_wide<NN>() ? 2 : 4; }   // 8-col tiles / warp
 template <int NN>
 __host__ __device__ constexpr int mma_threads() { return (mma_cw<NN>() + 1) * 32; }
 // kW columns per warp, kTC per CTA tile, kTCP smem row pitch (+16 B: conflict-free)

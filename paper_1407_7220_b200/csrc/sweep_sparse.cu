@@ -45,9 +45,9 @@ constexpr int kNB = kLook + 1;  // value ring (per-warp columns, filled by cp.as
 // stream the sweep is latency bound and needs the warps (measured: 7 consumer
 // warps x 4 tiles leave 28 % issue utilisation).
 template <int NN>
-__host__ __device__ constexpr int sp_cw() { return NN <= 12 ? CRB_SP_CW : 15; }
+__host__ __device__ constexpr int sp_cw() { return mma_wide<NN>() ? 15 : CRB_SP_CW; }
 template <int NN>
-__host__ __device__ constexpr int sp_ct() { return NN <= 12 ? 28 / CRB_SP_CW : 2; }
+__host__ __device__ constexpr int sp_ct() { return mma_wide<NN>() ? 2 : 28 / CRB_SP_CW; }
 template <int NN>
 __host__ __device__ constexpr int sp_threads() { return (sp_cw<NN>() + 1) * 32; }
 #define SP_GEO(NN)                               \
