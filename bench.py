@@ -272,6 +272,12 @@ def run_ours(args):
         "peak_kind": peak_kind, "kernel": f"sweep ({variant})",
         "algorithmic_bytes_per_launch": BYTES_PER_PAIR * rows * N,
         "sweep_share_of_step": (sweep_s / dev_s) if dev_s > 0 else None,
+        # secondary: fp64 flop per pair ~ 4n + 17
+        "fp64_tflops": ((4 * n + 17) * rows * N / sweep_avg / 1e12) if sweep_avg else None,
+        "note": "algorithmic bytes = 24 B per pair (read theta1, theta1_prev, write theta1_new); "
+                "the sweep skips the store of a multiplier equal to the value already in the "
+                "target buffer, so late in a solve the measured DRAM traffic ('traffic', ncu) is "
+                "~16 B per pair and the kernel is issue-bound rather than HBM-bound",
     }
 
     extras = {}
