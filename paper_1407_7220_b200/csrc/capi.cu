@@ -219,9 +219,9 @@ cr_status cr_create(const double* Xh, const double* ybar_shifted, int64_t N, int
   // DMMA tensor cores once the two rank-n contractions dominate the issue slots.
   // CRB_SWEEP=dfma|mma overrides.
   const char* var = std::getenv("CRB_SWEEP");
-  // measured on B200: the DMMA sweep is faster for every n
-  // except n = 3 (DFMA 351 vs 364 us per sweep at N = 1e4)
-  h->variant = n == 3 ? kSweepDfma : kSweepMma;
+  // measured on B200: the DMMA sweep is faster than the
+  // DFMA one for every n; CRB_SWEEP=dfma keeps the latter selectable
+  h->variant = kSweepMma;
   if (var && std::strcmp(var, "dfma") == 0) h->variant = kSweepDfma;
   if (var && std::strcmp(var, "mma") == 0) h->variant = kSweepMma;
   // masked dual store (sweep_sparse.cu), opt-in with CRB_SPARSE=1: it moves

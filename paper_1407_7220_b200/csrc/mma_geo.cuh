@@ -31,10 +31,19 @@ __host__ __device__ constexpr int mma_threads() { return (mma_cw<NN>() + 1) * 32
   (void)kThreads;
 constexpr int kTR = 8;                 // rows per stage (one MMA row block)
 #ifndef CRB_MMA_CTAS_PER_SM
-#define CRB_MMA_CTAS_PER_SM 1
+#define CRB_MMA_CTAS_PER_SM 0  // 0: per n (mma_ctas)
 #endif
-constexpr int kMinCtas = CRB_MMA_CTAS_PER_SM;  // 2: 128-register cap, 3-stage ring
-constexpr int kNS = kMinCtas == 2 ? 3 : 4;     // stages
+// CTAs per SM: the narrow geometry runs two CTAs (128-register cap, 3-stage
+// ring), the wide one (16 warps already) one. Measured on B200 (DESIGN.md
+// section 5): n = 5 363 -> 312 us, n = 12 415 -> 392 us with two; n = 10 (wide)
+// 387 -> 456 us and n = 20 524 -> 973 us, hence one for the wide form.
+template <int NN>
+__host__ __device__ constexpr int mma_ctas() {
+  return CRB_MMA_CTAS_PER_SM > 0 ? CRB_MMA_CTAS_PER_SM : (mma_wide<NN>() ? 1 : 2);
+}
+template <int NN>
+__host__ __device__ constexpr int mma_ns() { return mma_ctas<NN>() == 2 ? 3 : 4; }  // stages
+constexpr int kNS = 4;  // ring depth of the other users of this header (sweep_sparse.cu)
 constexpr int kWin = 32;               // row-sum window (rows)
 
 // Residual K: the n features plus (1, y) with (-c, 1) folded in -- unless
@@ -51,7 +60,8 @@ __host__ __device__ constexpr int stage_doubles() {
 }
 template <int NN>
 __host__ __device__ constexpr int smem_bytes() {
-  return kNS * stage_doubles<NN>() * 8 + 2 * mma_cw<NN>() * kWin * 8 + 2 * kNS * 8;
+  return mma_ns<NN>() * stage_doubles<NN>() * 8 + 2 * mma_cw<NN>() * kWin * 8 +
+         2 * mma_ns<NN>() * 8;
 }
 
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {

@@ -129,7 +129,8 @@ __device__ __forceinline__ void mma_stage(const double* __restrict__ sv, const d
 }
 
 template <int NN, int MODE, bool BLK>
-__global__ void __launch_bounds__(mma_threads<NN>(), kMinCtas) sweep_mma_kernel(const SweepArgs a) {
+__global__ void __launch_bounds__(mma_threads<NN>(), mma_ctas<NN>()) sweep_mma_kernel(const SweepArgs a) {
+  constexpr int kNS = mma_ns<NN>();
   CRB_GEO(NN)
   constexpr int KS = ksteps<NN>();
   constexpr int FB = fblocks<NN>();
