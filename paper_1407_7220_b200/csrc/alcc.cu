@@ -632,16 +632,16 @@ constexpr const void* loop_fn() {
   return (const void*)mapg_loop_kernel<NN>;
 }
 const void* const kLoopFns[kMaxN] = {
-    loop_fn<1>(),  loop_fn<2>(),  loop_fn<3>(),  loop_fn<4>(),  loop_fn<5>(),  loop_fn<6>(),
-    loop_fn<7>(),  loop_fn<8>(),  loop_fn<9>(),  loop_fn<10>(), loop_fn<11>(), loop_fn<12>(),
-    loop_fn<13>(), loop_fn<14>(), loop_fn<15>(), loop_fn<16>(), loop_fn<17>(), loop_fn<18>(),
-    loop_fn<19>(), loop_fn<20>(), loop_fn<21>(), loop_fn<22>(), loop_fn<23>(), loop_fn<24>()};
+#define CRB_LOOP_FN(N) loop_fn<N>()
+    CRB_N_SEQ(CRB_LOOP_FN)
+#undef CRB_LOOP_FN
+};
 
 constexpr AlccFns kFns[kMaxN] = {
-    fns_for<1>(),  fns_for<2>(),  fns_for<3>(),  fns_for<4>(),  fns_for<5>(),  fns_for<6>(),
-    fns_for<7>(),  fns_for<8>(),  fns_for<9>(),  fns_for<10>(), fns_for<11>(), fns_for<12>(),
-    fns_for<13>(), fns_for<14>(), fns_for<15>(), fns_for<16>(), fns_for<17>(), fns_for<18>(),
-    fns_for<19>(), fns_for<20>(), fns_for<21>(), fns_for<22>(), fns_for<23>(), fns_for<24>()};
+#define CRB_FNS_FOR(N) fns_for<N>()
+    CRB_N_SEQ(CRB_FNS_FOR)
+#undef CRB_FNS_FOR
+};
 
 AlccArgs alcc_args(cr_handle* h) {
   AlccArgs a{};

@@ -417,10 +417,10 @@ long long balcc_scratch_per_block(long long nbar, int n) {
 
 cudaError_t launch_balcc(const BalccArgs& a, int n, cudaStream_t s) {
   static constexpr BalccFn tab[kMaxN] = {
-      launch_n<1>,  launch_n<2>,  launch_n<3>,  launch_n<4>,  launch_n<5>,  launch_n<6>,
-      launch_n<7>,  launch_n<8>,  launch_n<9>,  launch_n<10>, launch_n<11>, launch_n<12>,
-      launch_n<13>, launch_n<14>, launch_n<15>, launch_n<16>, launch_n<17>, launch_n<18>,
-      launch_n<19>, launch_n<20>, launch_n<21>, launch_n<22>, launch_n<23>, launch_n<24>};
+#define CRB_LAUNCH_N(N) launch_n<N>
+      CRB_N_SEQ(CRB_LAUNCH_N)
+#undef CRB_LAUNCH_N
+};
   if (n < 1 || n > kMaxN || a.nbar > kMaxBlock) return cudaErrorInvalidValue;
   tab[n - 1](a, s);
   return cudaGetLastError();

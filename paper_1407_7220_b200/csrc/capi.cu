@@ -294,6 +294,7 @@ cr_status cr_create(const double* Xh, const double* ybar_shifted, int64_t N, int
   ALLOC(h->pw_part, (size_t)h->k2_blocks * 2);
   ALLOC(h->pw_sum, 2);
   h->power_grid = power_loop_grid(sms);
+  if (const char* pg = std::getenv("CRB_POWER_GRID")) h->power_grid = std::max(1, std::atoi(pg));
   ALLOC(h->gram, n * n + n);
   ALLOC(h->ps_part, (size_t)h->power_grid * (2 + 2 * n));
   ALLOC(h->ps_part2, (size_t)h->power_grid * 2);

@@ -220,10 +220,10 @@ constexpr GenFns gen_for() {
   return {GenTab<NN>::centres, GenTab<NN>::finish};
 }
 constexpr GenFns kGen[kMaxN] = {
-    gen_for<1>(),  gen_for<2>(),  gen_for<3>(),  gen_for<4>(),  gen_for<5>(),  gen_for<6>(),
-    gen_for<7>(),  gen_for<8>(),  gen_for<9>(),  gen_for<10>(), gen_for<11>(), gen_for<12>(),
-    gen_for<13>(), gen_for<14>(), gen_for<15>(), gen_for<16>(), gen_for<17>(), gen_for<18>(),
-    gen_for<19>(), gen_for<20>(), gen_for<21>(), gen_for<22>(), gen_for<23>(), gen_for<24>()};
+#define CRB_GEN_FOR(N) gen_for<N>()
+    CRB_N_SEQ(CRB_GEN_FOR)
+#undef CRB_GEN_FOR
+};
 
 GenArgs gen_args(cr_handle* h, int mode) {
   Partition& P = h->part;

@@ -331,12 +331,10 @@ void launch_primal_n(const PrimalArgs& a, cudaStream_t s) {
 using PrimalLauncher = void (*)(const PrimalArgs&, cudaStream_t);
 cudaError_t launch_primal(const PrimalArgs& a, cudaStream_t s) {
   static constexpr PrimalLauncher tab[kMaxN] = {
-      launch_primal_n<1>,  launch_primal_n<2>,  launch_primal_n<3>,  launch_primal_n<4>,
-      launch_primal_n<5>,  launch_primal_n<6>,  launch_primal_n<7>,  launch_primal_n<8>,
-      launch_primal_n<9>,  launch_primal_n<10>, launch_primal_n<11>, launch_primal_n<12>,
-      launch_primal_n<13>, launch_primal_n<14>, launch_primal_n<15>, launch_primal_n<16>,
-      launch_primal_n<17>, launch_primal_n<18>, launch_primal_n<19>, launch_primal_n<20>,
-      launch_primal_n<21>, launch_primal_n<22>, launch_primal_n<23>, launch_primal_n<24>};
+#define CRB_LP(N) launch_primal_n<N>
+      CRB_N_SEQ(CRB_LP)
+#undef CRB_LP
+};
   if (a.n < 1 || a.n > kMaxN) return cudaErrorInvalidValue;
   tab[a.n - 1](a, s);
   return cudaGetLastError();

@@ -131,9 +131,8 @@ using MetricsFn = void (*)(const MetricsArgs&, int, cudaStream_t);
 using EstimatorFn = void (*)(const double*, long long, const double*, const double*,
                              const double*, long long, double*, int, cudaStream_t);
 
-#define CRB_TAB(F)                                                                          \
-  {F<1>,  F<2>,  F<3>,  F<4>,  F<5>,  F<6>,  F<7>,  F<8>,  F<9>,  F<10>, F<11>, F<12>,      \
-   F<13>, F<14>, F<15>, F<16>, F<17>, F<18>, F<19>, F<20>, F<21>, F<22>, F<23>, F<24>}
+#define CRB_MET(N) metrics_n<N>
+#define CRB_EST(N) estimator_n<N>
 
 }  // namespace
 
@@ -146,7 +145,7 @@ cudaError_t launch_records(const double* X, const double* y, const double* xi, l
 }
 
 cudaError_t launch_pair_metrics(const MetricsArgs& a, int grid, cudaStream_t s) {
-  static constexpr MetricsFn tab[kMaxN] = CRB_TAB(metrics_n);
+  static constexpr MetricsFn tab[kMaxN] = {CRB_N_SEQ(CRB_MET)};
   if (a.n < 1 || a.n > kMaxN) return cudaErrorInvalidValue;
   tab[a.n - 1](a, grid, s);
   return cudaGetLastError();
@@ -155,7 +154,7 @@ cudaError_t launch_pair_metrics(const MetricsArgs& a, int grid, cudaStream_t s) 
 cudaError_t launch_estimator(const double* Xq, long long Q, const double* X, const double* y,
                              const double* xi, long long N, int n, double* out, int grid,
                              cudaStream_t s) {
-  static constexpr EstimatorFn tab[kMaxN] = CRB_TAB(estimator_n);
+  static constexpr EstimatorFn tab[kMaxN] = {CRB_N_SEQ(CRB_EST)};
   if (n < 1 || n > kMaxN) return cudaErrorInvalidValue;
   tab[n - 1](Xq, Q, X, y, xi, N, out, grid, s);
   return cudaGetLastError();

@@ -290,11 +290,10 @@ int power_loop_grid(int sms) { return sms; }  // one 256-thread block per SM
 
 cudaError_t launch_power_loop(const PowerLoopArgs& a, int grid, cudaStream_t s) {
   static constexpr PowerLoopFn tab[kMaxN] = {
-      power_loop_n<1>,  power_loop_n<2>,  power_loop_n<3>,  power_loop_n<4>,  power_loop_n<5>,
-      power_loop_n<6>,  power_loop_n<7>,  power_loop_n<8>,  power_loop_n<9>,  power_loop_n<10>,
-      power_loop_n<11>, power_loop_n<12>, power_loop_n<13>, power_loop_n<14>, power_loop_n<15>,
-      power_loop_n<16>, power_loop_n<17>, power_loop_n<18>, power_loop_n<19>, power_loop_n<20>,
-      power_loop_n<21>, power_loop_n<22>, power_loop_n<23>, power_loop_n<24>};
+#define CRB_PL(N) power_loop_n<N>
+      CRB_N_SEQ(CRB_PL)
+#undef CRB_PL
+};
   if (a.n < 1 || a.n > kMaxN) return cudaErrorInvalidValue;
   cudaError_t e = cudaSuccess;
   tab[a.n - 1](a, grid, s, &e);

@@ -243,8 +243,7 @@ template <int N0, int... Ns> struct STable<N0, Ns...> {
 template <> struct STable<> {
   static SmallInfo info(int) { return SmallInfo{}; }
 };
-using AllS = STable<1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16, 17, 18, 19, 20, 21, 22,
-                    23, 24>;
+using AllS = STable<CRB_N_LIST>;
 
 }  // namespace
 

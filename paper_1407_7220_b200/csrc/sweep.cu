@@ -414,8 +414,7 @@ template <int N0, int... Ns> struct Table<N0, Ns...> {
 template <> struct Table<> {
   static SweepKernelInfo info(int, int, bool) { return SweepKernelInfo{}; }
 };
-using AllN = Table<1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16, 17, 18, 19, 20, 21, 22,
-                   23, 24>;
+using AllN = Table<CRB_N_LIST>;
 
 }  // namespace
 

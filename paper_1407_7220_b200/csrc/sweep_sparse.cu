@@ -523,8 +523,7 @@ template <int N0, int... Ns> struct SpTable<N0, Ns...> {
 template <> struct SpTable<> {
   static SweepKernelInfo info(int, bool) { return SweepKernelInfo{}; }
 };
-using SpAll = SpTable<1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16, 17, 18, 19, 20, 21,
-                      22, 23, 24>;
+using SpAll = SpTable<CRB_N_LIST>;
 
 }  // namespace
 

@@ -91,7 +91,7 @@ def test_golden_fixtures():
 
 
 @pytest.mark.parametrize("variant", ["dfma", "mma", "small"])
-@pytest.mark.parametrize("n", list(range(1, 25)))
+@pytest.mark.parametrize("n", list(range(1, 33)))
 def test_every_n_every_sweep_path(oracle, monkeypatch, variant, n):
     """Every n on each sweep implementation: the TMA-pipelined DFMA and DMMA
     kernels (per-kernel iteration) and the persistent small-N loop."""
@@ -417,7 +417,8 @@ def test_gamma_continuation_resume(oracle):
 
 
 @pytest.mark.parametrize("path", ["small", "dfma", "mma"])
-@pytest.mark.parametrize("N,n", [(2, 1), (3, 2), (17, 16), (21, 20), (25, 24), (33, 5), (65, 13)])
+@pytest.mark.parametrize("N,n", [(2, 1), (3, 2), (17, 16), (21, 20), (25, 24), (33, 5), (65, 13),
+                                 (33, 32), (47, 27)])
 def test_tiny_and_ragged_sizes(oracle, monkeypatch, path, N, n):
     """Edge sizes: N = n + 1, N below one strip/tile, ragged last strips."""
     monkeypatch.setenv("CRB_SMALL", "1" if path == "small" else "0")

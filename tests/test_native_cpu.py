@@ -105,8 +105,8 @@ def test_device_path_fails_loudly_without_gpu():
 
 
 def test_create_rejects_invalid_shapes():
-    X = np.zeros((10, 30))
+    X = np.zeros((40, 33))
     with pytest.raises(ValueError):
-        crb.DualSolver(X, np.zeros(10))  # n > 24 is not supported yet
+        crb.DualSolver(X, np.zeros(40))  # n > 32 (kMaxN) is not supported
     with pytest.raises(ValueError):
         crb.DualSolver(np.zeros((1, 2)), np.zeros(1))
