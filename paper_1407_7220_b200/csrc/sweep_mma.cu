@@ -120,10 +120,15 @@ __device__ __forceinline__ void mma_stage(const double* __restrict__ sv, const d
       }
       rs[j] += v[j];
     }
+    // a tile whose v are all zero adds exact zeros to the aggregates (late in a
+    // solve almost every tile): skip its aggregation MMAs (the power mode's v is
+    // the residual itself, rarely zero)
+    if (MODE == kModePower || __any_sync(0xffffffffu, v[0] != 0.0 || v[1] != 0.0)) {
 #pragma unroll
-    for (int fb = 0; fb < FB; ++fb) {
-      dmma(D[ct][fb][0], D[ct][fb][1], Ag[0][fb], v[0]);
-      dmma(D[ct][fb][0], D[ct][fb][1], Ag[1][fb], v[1]);
+      for (int fb = 0; fb < FB; ++fb) {
+        dmma(D[ct][fb][0], D[ct][fb][1], Ag[0][fb], v[0]);
+        dmma(D[ct][fb][0], D[ct][fb][1], Ag[1][fb], v[1]);
+      }
     }
   }
 }
