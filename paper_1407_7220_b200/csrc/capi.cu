@@ -215,18 +215,15 @@ cr_status cr_create(const double* Xh, const double* ybar_shifted, int64_t N, int
   CUDA_TRY(cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking));
   keep_pool_memory(device);
   g_alloc_stream = h->st;
-  // sweep variant (measured on B200, profiles/): CUDA-core DFMA for small n,
-  // DMMA tensor cores once the two rank-n contractions dominate the issue slots.
-  // CRB_SWEEP=dfma|mma overrides.
+  // sweep variant, measured on B200: the DMMA sweep is
+  // faster than the CUDA-core DFMA one for every n. CRB_SWEEP=dfma|mma overrides.
   const char* var = std::getenv("CRB_SWEEP");
-  // measured on B200: the DMMA sweep is faster than the
-  // DFMA one for every n; CRB_SWEEP=dfma keeps the latter selectable
   h->variant = kSweepMma;
   if (var && std::strcmp(var, "dfma") == 0) h->variant = kSweepDfma;
   if (var && std::strcmp(var, "mma") == 0) h->variant = kSweepMma;
   // masked dual store (sweep_sparse.cu), opt-in with CRB_SPARSE=1: it moves
-  // 12x fewer bytes but is latency bound and slower than the dense sweep
-  // (DESIGN.md section 11); DMMA geometry for every n
+  // 12x fewer bytes but is issue bound and not faster than the dense sweep
+  // (DESIGN.md section 10b); DMMA geometry for every n
   const char* sp = std::getenv("CRB_SPARSE");
   h->sparse_ok = (sp && sp[0] == '1') && !(var && std::strcmp(var, "dfma") == 0);
   if (h->sparse_ok) {
