@@ -7,13 +7,16 @@
 
 namespace crb {
 
-// CTA geometry per n (measured on B200 with the store-skipping sweep, N = 1e4,
-// late iterations): 7 consumer warps x 4 tiles (8 warps,
-// 255-register cap) or 15 consumer warps x 2 tiles (16 warps, 128 registers,
-// more warps to hide the longer DMMA chains): the wide form wins for n = 9, 10
-// (387 vs 404 us) and n > 12, the narrow one elsewhere (n = 5: 363 vs 388 us).
+// CTA geometry per n, measured on B200 (store skipping and
+// the zero-tile skips make the sweep issue bound): 7 consumer warps x 4 tiles
+// at two CTAs per SM (128-register cap, 3-stage ring) for n <= 14 -- n = 10:
+// 303 vs 372 us -- and 15 consumer warps x 2 tiles at one CTA per SM above
+// (more warps hide the longer DMMA chains; n = 20: 434 vs 526 us).
+#ifndef CRB_WIDE_ABOVE
+#define CRB_WIDE_ABOVE 14
+#endif
 template <int NN>
-__host__ __device__ constexpr bool mma_wide() { return NN > 12 || NN == 9 || NN == 10; }
+__host__ __device__ constexpr bool mma_wide() { return NN > CRB_WIDE_ABOVE; }
 template <int NN>
 __host__ __device__ constexpr int mma_cw() { return mma_wide<NN>() ? 15 : 7; }  // consumer warps
 template <int NN>
@@ -33,10 +36,8 @@ constexpr int kTR = 8;                 // rows per stage (one MMA row block)
 #ifndef CRB_MMA_CTAS_PER_SM
 #define CRB_MMA_CTAS_PER_SM 0  // 0: per n (mma_ctas)
 #endif
-// CTAs per SM: the narrow geometry runs two CTAs (128-register cap, 3-stage
-// ring), the wide one (16 warps already) one. Measured on B200 (DESIGN.md
-// section 5): n = 5 363 -> 312 us, n = 12 415 -> 392 us with two; n = 10 (wide)
-// 387 -> 456 us and n = 20 524 -> 973 us, hence one for the wide form.
+// CTAs per SM: the narrow geometry runs two CTAs, the wide one (16 warps
+// already) one (two wide CTAs do not fit the register file).
 template <int NN>
 __host__ __device__ constexpr int mma_ctas() {
   return CRB_MMA_CTAS_PER_SM > 0 ? CRB_MMA_CTAS_PER_SM : (mma_wide<NN>() ? 1 : 2);

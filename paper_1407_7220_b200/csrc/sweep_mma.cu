@@ -72,7 +72,7 @@ __device__ __forceinline__ void mma_stage(const double* __restrict__ sv, const d
 #pragma unroll
     for (int ks = 0; ks < KS; ++ks) dmma(d0, d1, A[ct][ks], B[ks]);
     const int cl = ct * 8 + c8;  // column within the warp's strip
-    double v[2];
+    double v[2], rowv[2], th2v[2];
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
       const int rr = 2 * q + j;
@@ -95,11 +95,8 @@ __device__ __forceinline__ void mma_stage(const double* __restrict__ sv, const d
         }
         if (MASK && !rv) th2 = 0.0;
         v[j] = keep_if_nonneg(fma(-row, cf.invL, th2));
-        sc.vv = fma(v[j], v[j], sc.vv);
-        sc.vr = fma(v[j], row, sc.vr);
-        sc.tr = fma(th2, row, sc.tr);
-        const double m = keep_if_neg(row);
-        sc.nn = fma(m, m, sc.nn);
+        rowv[j] = row;
+        th2v[j] = th2;
         // v goes into the buffer that holds p1 (theta1_prev): an unchanged value
         // (late in a solve almost every pair stays 0) needs no store
         if (rv && __double_as_longlong(v[j]) != __double_as_longlong(p1))
@@ -118,7 +115,24 @@ __device__ __forceinline__ void mma_stage(const double* __restrict__ sv, const d
         v[j] = row;
         sc.vv = fma(row, row, sc.vv);
       }
-      rs[j] += v[j];
+      if (MODE != kModePapg) rs[j] += v[j];
+    }
+    if (MODE == kModePapg) {
+      // v = 0, theta2 = 0 and row >= 0 everywhere in the tile (late in a solve
+      // almost every tile): every scalar, row-sum and aggregate update below adds
+      // an exact zero -- skip them as a unit
+      const bool hot = v[0] != 0.0 || v[1] != 0.0 || th2v[0] != 0.0 || th2v[1] != 0.0 ||
+                       rowv[0] < 0.0 || rowv[1] < 0.0;
+      if (!__any_sync(0xffffffffu, hot)) continue;
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        sc.vv = fma(v[j], v[j], sc.vv);
+        sc.vr = fma(v[j], rowv[j], sc.vr);
+        sc.tr = fma(th2v[j], rowv[j], sc.tr);
+        const double m = keep_if_neg(rowv[j]);
+        sc.nn = fma(m, m, sc.nn);
+        rs[j] += v[j];
+      }
     }
     // a tile whose v are all zero adds exact zeros to the aggregates (late in a
     // solve almost every tile): skip its aggregation MMAs (the power mode's v is
