@@ -161,6 +161,9 @@ cr_status cr_last_timing(const cr_handle *h, double *seconds, int64_t *launches,
 /* sweep kernel variant chosen for this handle: 0 = CUDA-core DFMA,
    1 = FP64 tensor-core DMMA (override with CRB_SWEEP=dfma|mma) */
 int32_t cr_sweep_variant(const cr_handle *h);
+/* Multipliers written by the P-APG sweeps since the last reset (DMMA sweep;
+   unchanged values are not rewritten), optionally resetting the counter. */
+cr_status cr_sweep_store_count(cr_handle *h, uint64_t *count, int32_t reset);
 /* Time k sweep-kernel launches alone on the handle's stream with CUDA events
    (the dominant kernel in isolation, for the roofline). */
 cr_status cr_time_sweep(cr_handle *h, int32_t k, double *avg_seconds);

@@ -73,7 +73,7 @@ EXPORTS = [
     "cr_duality_gap", "cr_evaluate_estimator", "cr_repair_feasibility",
     "cr_gen_instance", "cr_prepare_problem", "cr_certificate", "cr_momentum_next",
     "cr_sigma_A", "cr_alcc_solve", "cr_alcc_multiplier", "cr_time_penalty_sweep",
-    "cr_set_partition", "cr_partition_stats",
+    "cr_set_partition", "cr_partition_stats", "cr_sweep_store_count",
 ]
 
 _lib = None
@@ -134,6 +134,7 @@ def load():
         "cr_time_penalty_sweep": (st, [vp, i32, _P]),
         "cr_set_partition": (st, [vp, i64, _P, _P, C.POINTER(AlccConfigC)]),
         "cr_partition_stats": (st, [vp, C.POINTER(i64), _P, _P, _P]),
+        "cr_sweep_store_count": (st, [vp, C.POINTER(u64), i32]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

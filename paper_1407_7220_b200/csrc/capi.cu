@@ -299,6 +299,7 @@ cr_status cr_create(const double* Xh, const double* ybar_shifted, int64_t N, int
   ALLOC(h->consts, 4);
   ALLOC(h->izero, 1);
   ALLOC(h->counter, 1);
+  ALLOC(h->d_stores, 1);
   ALLOC(h->ctrl_d, 1);
 #undef ALLOC
   if (e != cudaSuccess) {
@@ -336,6 +337,7 @@ cr_status cr_create(const double* Xh, const double* ybar_shifted, int64_t N, int
   CUDA_TRY(cudaMemcpyAsync(h->consts, consts, sizeof(consts), cudaMemcpyHostToDevice, h->st));
   CUDA_TRY(cudaMemsetAsync(h->izero, 0, sizeof(int), h->st));
   CUDA_TRY(cudaMemsetAsync(h->counter, 0, sizeof(unsigned int), h->st));
+  CUDA_TRY(cudaMemsetAsync(h->d_stores, 0, sizeof(unsigned long long), h->st));
   CUDA_TRY(cudaMemsetAsync(h->ctrl_d, 0, sizeof(DevCtrl), h->st));
   CUDA_TRY(launch_gram(h->X, N, (int)n, h->gram, h->st));
   const char* sig = std::getenv("CRB_SIGMA");
@@ -363,6 +365,7 @@ void cr_destroy(cr_handle* h) {
   dfree(h->counter, h->st);
   dfree(h->M[0], h->st);
   dfree(h->M[1], h->st);
+  dfree(h->d_stores, h->st);
   dfree(h->ctrl_d, h->st);
   if (h->st) cudaStreamSynchronize(h->st);
   if (h->ctrl_h) cudaFreeHost(h->ctrl_h);
@@ -1036,6 +1039,17 @@ cr_status cr_last_timing(const cr_handle* h, double* seconds, int64_t* launches,
 }
 
 int32_t cr_sweep_variant(const cr_handle* h) { return h ? h->variant : -1; }
+
+cr_status cr_sweep_store_count(cr_handle* h, uint64_t* count, int32_t reset) {
+  if (!h || !count) return CR_EINVAL;
+  CUDA_TRY(cudaSetDevice(h->device));
+  unsigned long long c = 0;
+  CUDA_TRY(cudaMemcpyAsync(&c, h->d_stores, sizeof(c), cudaMemcpyDeviceToHost, h->st));
+  if (reset) CUDA_TRY(cudaMemsetAsync(h->d_stores, 0, sizeof(c), h->st));
+  CUDA_TRY(cudaStreamSynchronize(h->st));
+  *count = c;
+  return CR_OK;
+}
 
 cr_status cr_time_sweep(cr_handle* h, int32_t k, double* avg_seconds) {
   if (!h || k < 1 || !avg_seconds) return CR_EINVAL;

@@ -97,6 +97,7 @@ struct SweepArgs {
   int maxspan;            // max segments (tiles) one CTA can touch
   long long nbar;         // block size of the partition: pairs inside one block are
                           // masked like the diagonal (1: singleton blocks)
+  unsigned long long* stores;  // optional: multipliers written by the P-APG sweep
   uint32_t* M0;           // masked dual store (sweep_sparse.cu): live words of V[0], V[1]
   uint32_t* M1;
   int mstages;            // mask stage capacity per CTA (MaskGeo::stages)

@@ -126,6 +126,7 @@ struct cr_handle {
   int64_t last_launches = 0;
   // masked dual store (sweep_sparse.cu): live-bit words of V[0], V[1]
   uint32_t* M[2] = {nullptr, nullptr};
+  unsigned long long* d_stores = nullptr;  // multipliers written by the P-APG sweeps
   int mstages = 0;          // MaskGeo::stages
   bool sparse_ok = false;   // the masked P-APG sweep is available (MMA geometry)
   bool masked = false;      // this solve runs it (not the small-N loop)
@@ -203,6 +204,7 @@ inline SweepArgs sweep_args(cr_handle* h, int mode, bool agg_only) {
   a.M0 = h->M[0];
   a.M1 = h->M[1];
   a.mstages = h->mstages;
+  a.stores = h->d_stores;
   return a;
 }
 inline MaskGeo mask_geo(const cr_handle* h) {

@@ -39,7 +39,7 @@ __device__ __forceinline__ void mma_stage(const double* __restrict__ sv, const d
                                           int lane, const double (&A)[mma_ct<NN>()][ksteps<NN>()],
                                           double (&D)[mma_ct<NN>()][fblocks<NN>()][2],
                                           const double (&Cc)[mma_ct<NN>()], const MCoef& cf,
-                                          MScal& sc, double (&rs)[2]) {
+                                          MScal& sc, double (&rs)[2], int& nst) {
   CRB_GEO(NN)
   constexpr int KS = ksteps<NN>();
   constexpr int FB = fblocks<NN>();
@@ -99,8 +99,10 @@ __device__ __forceinline__ void mma_stage(const double* __restrict__ sv, const d
         th2v[j] = th2;
         // v goes into the buffer that holds p1 (theta1_prev): an unchanged value
         // (late in a solve almost every pair stays 0) needs no store
-        if (rv && __double_as_longlong(v[j]) != __double_as_longlong(p1))
+        if (rv && __double_as_longlong(v[j]) != __double_as_longlong(p1)) {
           st_stream(gout + rr * ld + cl, v[j]);
+          ++nst;
+        }
       } else if (MODE == kModePenalty || MODE == kModePenaltyUpdate) {
         const double th = (MASK && !rv) ? 0.0 : sv[rr * kTCP + cl];
         v[j] = keep_if_nonneg(th - row);
@@ -232,6 +234,7 @@ __global__ void __launch_bounds__(mma_threads<NN>(), mma_ctas<NN>()) sweep_mma_k
   }
   const bool unit_scale = (cf.s_c == 1.0) && (cf.s_p == 1.0);
   MScal sc{0.0, 0.0, 0.0, 0.0};
+  int nst = 0;  // stores issued by this thread (P-APG mode)
   int i = 0;
   int flushes = 0;
 
@@ -278,17 +281,17 @@ __global__ void __launch_bounds__(mma_threads<NN>(), mma_ctas<NN>()) sweep_mma_k
         if (clean) {
           if (unit_scale)
             mma_stage<NN, MODE, false, true, BLK>(sv, svp, srec, gout, a.ld, gcol0, grow0, nr, a.N, a.nbar, lane, A,
-                                             D, Cc, cf, sc, rsj);
+                                             D, Cc, cf, sc, rsj, nst);
           else
             mma_stage<NN, MODE, false, false, BLK>(sv, svp, srec, gout, a.ld, gcol0, grow0, nr, a.N, a.nbar, lane,
-                                              A, D, Cc, cf, sc, rsj);
+                                              A, D, Cc, cf, sc, rsj, nst);
         } else {
           if (unit_scale)
             mma_stage<NN, MODE, true, true, BLK>(sv, svp, srec, gout, a.ld, gcol0, grow0, nr, a.N, a.nbar, lane, A,
-                                             D, Cc, cf, sc, rsj);
+                                             D, Cc, cf, sc, rsj, nst);
           else
             mma_stage<NN, MODE, true, false, BLK>(sv, svp, srec, gout, a.ld, gcol0, grow0, nr, a.N, a.nbar, lane, A,
-                                             D, Cc, cf, sc, rsj);
+                                             D, Cc, cf, sc, rsj, nst);
         }
       }
       __syncwarp();
@@ -356,6 +359,11 @@ __global__ void __launch_bounds__(mma_threads<NN>(), mma_ctas<NN>()) sweep_mma_k
     sp[1] = vr;
     sp[2] = tr;
     sp[3] = nn;
+  }
+  if (MODE == kModePapg && a.stores != nullptr) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) nst += __shfl_xor_sync(0xffffffffu, nst, off);
+    if (lane == 0 && nst) atomicAdd(a.stores, (unsigned long long)nst);
   }
 }
 

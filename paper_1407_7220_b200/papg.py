@@ -427,6 +427,12 @@ class DualSolver:
         _raise(self._L.cr_last_timing(self.h, C.byref(s), C.byref(k), C.byref(sw)), self.h)
         return s.value, k.value, sw.value
 
+    def sweep_store_count(self, reset=False):
+        """Multipliers written by the P-APG sweeps since the last reset."""
+        c = C.c_uint64(0)
+        _raise(self._L.cr_sweep_store_count(self.h, C.byref(c), int(reset)), self.h)
+        return c.value
+
     def time_sweep(self, k=10):
         """Times k sweep launches alone; clobbers the previous dual iterate."""
         s = C.c_double(0)
