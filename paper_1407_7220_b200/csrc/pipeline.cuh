@@ -39,6 +39,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 }
 // wait with a back-off: for a warp that is otherwise idle (a producer ahead of
 // its consumers) so its spin does not take issue slots from the SM's other warps
+template <int NS = 256>
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
   uint32_t done = 0;
   for (;;) {
@@ -52,7 +53,7 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) 
         : "r"(smem_u32(bar)), "r"(parity)
         : "memory");
     if (done) return;
-    __nanosleep(256);
+    __nanosleep(NS);
   }
 }
 // TMA bulk copy global -> shared, completion counted on an mbarrier

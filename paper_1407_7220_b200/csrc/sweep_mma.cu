@@ -30,16 +30,132 @@ namespace crb {
 
 namespace {
 
-// One 8-row stage for one warp. MASK: diagonal / partial-stage masking.
-template <int NN, int MODE, bool MASK, bool UNIT, bool BLK>
-__device__ __forceinline__ void mma_stage(const double* __restrict__ sv, const double* __restrict__ svp,
+// P-APG stage for one warp: the residuals of all kCT tiles first (independent
+// DMMA chains interleaved), then per tile a cold test on the inputs. With
+// theta1 = theta1_prev = 0 and row >= 0 everywhere in a tile (late in a solve
+// almost every tile) theta2 = 0 and v = 0 = theta1_prev: no store, and every
+// scalar, row-sum and aggregate update adds an exact zero -- the warp skips the
+// tile after one vote, before computing theta2 or v. MASK stages (diagonal,
+// partial stage, pad columns) always take the full path. Returns whether any
+// tile of the stage was hot (warp-uniform): a cold stage has zero row sums.
+template <int NN, bool MASK, bool UNIT, bool BLK>
+__device__ __forceinline__ bool papg_stage(const double* __restrict__ sv, const double* __restrict__ svp,
+                                           const double* __restrict__ srec, double* gout,
+                                           long long ld, long long gcol0, long long grow0, int nr,
+                                           long long ncols, long long nbar,
+                                           int lane, const double (&A)[mma_ct<NN>()][ksteps<NN>()],
+                                           double (&D)[mma_ct<NN>()][fblocks<NN>()][2],
+                                           const double (&Cc)[mma_ct<NN>()], const MCoef& cf,
+                                           MScal& sc, double (&rs)[2], int& nst) {
+  CRB_GEO(NN)
+  constexpr int KS = ksteps<NN>();
+  constexpr int FB = fblocks<NN>();
+  constexpr int RQ = rec_pitch(NN);
+  constexpr bool SPLIT = split_yc<NN>();
+  const int q = lane & 3;
+  const int c8 = lane >> 2;
+  double yr[2] = {0.0, 0.0};  // y of rows 2q, 2q+1 (split form)
+  if (SPLIT) {
+    yr[0] = srec[(2 * q) * RQ + NN + 1];
+    yr[1] = srec[(2 * q + 1) * RQ + NN + 1];
+  }
+  double d[kCT][2];
+  {
+    double B[KS];  // residual B fragments: X'[row c8][k]
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) B[ks] = srec[c8 * RQ + ks * 4 + q];
+#pragma unroll
+    for (int ct = 0; ct < kCT; ++ct) d[ct][0] = d[ct][1] = 0.0;
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+#pragma unroll
+      for (int ct = 0; ct < kCT; ++ct) dmma(d[ct][0], d[ct][1], A[ct][ks], B[ks]);
+    }
+  }
+  // stored multipliers are v >= +0 (never -0), so "both zero" is one OR of the bits
+  double* g0 = gout + (long long)(2 * q) * ld + c8;  // rows 2q, 2q+1 of the stage
+  bool any_hot = false;
+  rs[0] = 0.0;
+  rs[1] = 0.0;
+#pragma unroll
+  for (int ct = 0; ct < kCT; ++ct) {
+    const int cl = ct * 8 + c8;  // column within the warp's strip
+    double row[2], c1[2], p1[2];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int rr = 2 * q + j;
+      row[j] = d[ct][j];
+      if (SPLIT) row[j] += yr[j] + Cc[ct];  // y_l1 - c_l2 (Cc holds -c_l2)
+      c1[j] = sv[rr * kTCP + cl];
+      p1[j] = svp[rr * kTCP + cl];
+    }
+    bool hot = true;
+    if (!MASK) {
+      const unsigned long long bits =
+          (unsigned long long)__double_as_longlong(c1[0]) | (unsigned long long)__double_as_longlong(c1[1]) |
+          (unsigned long long)__double_as_longlong(p1[0]) | (unsigned long long)__double_as_longlong(p1[1]);
+      hot = bits != 0ull || (__double2hiint(row[0]) | __double2hiint(row[1])) < 0;
+    }
+    if (!__any_sync(0xffffffffu, hot)) continue;
+    any_hot = true;
+    double v[2];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int rr = 2 * q + j;
+      const bool rv = !MASK || rr < nr;  // row present in this (partial) stage
+      // diagonal, rows past a partial stage, pad columns (with y - c split out
+      // of the MMA a pad column's zero fragments no longer zero its row)
+      if (MASK && (same_block<BLK>(gcol0 + cl, grow0 + rr, nbar) || !rv || gcol0 + cl >= ncols))
+        row[j] = 0.0;
+      double th2;
+      if (UNIT) {
+        th2 = fma(cf.beta, c1[j] - p1[j], c1[j]);
+      } else {
+        const double th1 = cf.s_c * c1[j];
+        th2 = fma(cf.beta, th1 - cf.s_p * p1[j], th1);
+      }
+      if (MASK && !rv) th2 = 0.0;
+      v[j] = keep_if_nonneg(fma(-row[j], cf.invL, th2));
+      // v goes into the buffer that holds p1 (theta1_prev): an unchanged value
+      // needs no store
+      if (rv && __double_as_longlong(v[j]) != __double_as_longlong(p1[j])) {
+        st_stream(g0 + (long long)j * ld + ct * 8, v[j]);
+        ++nst;
+      }
+      sc.vv = fma(v[j], v[j], sc.vv);
+      sc.vr = fma(v[j], row[j], sc.vr);
+      sc.tr = fma(th2, row[j], sc.tr);
+      const double m = keep_if_neg(row[j]);
+      sc.nn = fma(m, m, sc.nn);
+      rs[j] += v[j];
+    }
+    // a tile whose v are all zero adds exact zeros to the aggregates: skip its
+    // aggregation MMAs
+    if (__any_sync(0xffffffffu, v[0] != 0.0 || v[1] != 0.0)) {
+#pragma unroll
+      for (int fb = 0; fb < FB; ++fb) {
+        // aggregation A fragments: [X 1][row 2q+j][feature fb*8 + c8]
+        const double a0 = (!MASK || 2 * q < nr) ? srec[(2 * q) * RQ + fb * 8 + c8] : 0.0;
+        const double a1 = (!MASK || 2 * q + 1 < nr) ? srec[(2 * q + 1) * RQ + fb * 8 + c8] : 0.0;
+        dmma(D[ct][fb][0], D[ct][fb][1], a0, v[0]);
+        dmma(D[ct][fb][0], D[ct][fb][1], a1, v[1]);
+      }
+    }
+  }
+  return any_hot;
+}
+
+// One 8-row stage for one warp, the other modes (power, penalty). MASK:
+// diagonal / partial-stage masking.
+template <int NN, int MODE, bool MASK, bool BLK>
+__device__ __forceinline__ void mma_stage(const double* __restrict__ sv,
                                           const double* __restrict__ srec, double* gout,
                                           long long ld, long long gcol0, long long grow0, int nr,
                                           long long ncols, long long nbar,
                                           int lane, const double (&A)[mma_ct<NN>()][ksteps<NN>()],
                                           double (&D)[mma_ct<NN>()][fblocks<NN>()][2],
                                           const double (&Cc)[mma_ct<NN>()], const MCoef& cf,
-                                          MScal& sc, double (&rs)[2], int& nst) {
+                                          MScal& sc, double (&rs)[2]) {
   CRB_GEO(NN)
   constexpr int KS = ksteps<NN>();
   constexpr int FB = fblocks<NN>();
@@ -72,38 +188,16 @@ __device__ __forceinline__ void mma_stage(const double* __restrict__ sv, const d
 #pragma unroll
     for (int ks = 0; ks < KS; ++ks) dmma(d0, d1, A[ct][ks], B[ks]);
     const int cl = ct * 8 + c8;  // column within the warp's strip
-    double v[2], rowv[2], th2v[2];
+    double v[2];
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
       const int rr = 2 * q + j;
       const bool rv = !MASK || rr < nr;  // row present in this (partial) stage
       double row = j == 0 ? d0 : d1;
       if (SPLIT) row += yr[j] + Cc[ct];  // y_l1 - c_l2 (Cc holds -c_l2)
-      // diagonal, rows past a partial stage, pad columns (with y - c split out
-      // of the MMA a pad column's zero fragments no longer zero its row)
       if (MASK && (same_block<BLK>(gcol0 + cl, grow0 + rr, nbar) || !rv || gcol0 + cl >= ncols))
         row = 0.0;
-      if (MODE == kModePapg) {
-        const double c1 = sv[rr * kTCP + cl];
-        const double p1 = svp[rr * kTCP + cl];
-        double th2;
-        if (UNIT) {
-          th2 = fma(cf.beta, c1 - p1, c1);
-        } else {
-          const double th1 = cf.s_c * c1;
-          th2 = fma(cf.beta, th1 - cf.s_p * p1, th1);
-        }
-        if (MASK && !rv) th2 = 0.0;
-        v[j] = keep_if_nonneg(fma(-row, cf.invL, th2));
-        rowv[j] = row;
-        th2v[j] = th2;
-        // v goes into the buffer that holds p1 (theta1_prev): an unchanged value
-        // (late in a solve almost every pair stays 0) needs no store
-        if (rv && __double_as_longlong(v[j]) != __double_as_longlong(p1)) {
-          st_stream(gout + rr * ld + cl, v[j]);
-          ++nst;
-        }
-      } else if (MODE == kModePenalty || MODE == kModePenaltyUpdate) {
+      if (MODE == kModePenalty || MODE == kModePenaltyUpdate) {
         const double th = (MASK && !rv) ? 0.0 : sv[rr * kTCP + cl];
         v[j] = keep_if_nonneg(th - row);
         if (MODE == kModePenaltyUpdate) {  // outer step: statistics + theta_{k+1}
@@ -117,28 +211,10 @@ __device__ __forceinline__ void mma_stage(const double* __restrict__ sv, const d
         v[j] = row;
         sc.vv = fma(row, row, sc.vv);
       }
-      if (MODE != kModePapg) rs[j] += v[j];
+      rs[j] += v[j];
     }
-    if (MODE == kModePapg) {
-      // v = 0, theta2 = 0 and row >= 0 everywhere in the tile (late in a solve
-      // almost every tile): every scalar, row-sum and aggregate update below adds
-      // an exact zero -- skip them as a unit
-      const bool hot = v[0] != 0.0 || v[1] != 0.0 || th2v[0] != 0.0 || th2v[1] != 0.0 ||
-                       rowv[0] < 0.0 || rowv[1] < 0.0;
-      if (!__any_sync(0xffffffffu, hot)) continue;
-#pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        sc.vv = fma(v[j], v[j], sc.vv);
-        sc.vr = fma(v[j], rowv[j], sc.vr);
-        sc.tr = fma(th2v[j], rowv[j], sc.tr);
-        const double m = keep_if_neg(rowv[j]);
-        sc.nn = fma(m, m, sc.nn);
-        rs[j] += v[j];
-      }
-    }
-    // a tile whose v are all zero adds exact zeros to the aggregates (late in a
-    // solve almost every tile): skip its aggregation MMAs (the power mode's v is
-    // the residual itself, rarely zero)
+    // a tile whose v are all zero adds exact zeros to the aggregates (the power
+    // mode's v is the residual itself, rarely zero)
     if (MODE == kModePower || __any_sync(0xffffffffu, v[0] != 0.0 || v[1] != 0.0)) {
 #pragma unroll
       for (int fb = 0; fb < FB; ++fb) {
@@ -199,7 +275,8 @@ __global__ void __launch_bounds__(mma_threads<NN>(), mma_ctas<NN>()) sweep_mma_k
         const uint32_t vbytes = (uint32_t)min((long long)kTC, a.ld - c0) * 8u;
         for (long long r = rlo; r < rhi; r += kTR, ++i) {
           const int s = i % kNS;
-          if (i >= kNS) mbar_wait(&empty[s], (uint32_t)(((i / kNS) - 1) & 1));
+          // short back-off: the spin otherwise takes ~3 % of the SM's issue slots
+          if (i >= kNS) mbar_wait_sleep<64>(&empty[s], (uint32_t)(((i / kNS) - 1) & 1));
           const int nr = (int)min((long long)kTR, rhi - r);
           double* st = stages + s * SD;
           const uint32_t bytes = (MODE == kModePapg ? 2u * nr * vbytes : 0u) +
@@ -267,6 +344,7 @@ __global__ void __launch_bounds__(mma_threads<NN>(), mma_ctas<NN>()) sweep_mma_k
       mbar_wait(&full[s], (uint32_t)((i / kNS) & 1));
       const int nr = (int)min((long long)kTR, rhi - r);
       double rsj[2] = {0.0, 0.0};
+      bool hot_stage = true;  // P-APG: false when every tile of the stage was cold
       if (active) {
         const double* st = stages + s * SD;
         const double* sv = st + warp * kW;
@@ -278,30 +356,39 @@ __global__ void __launch_bounds__(mma_threads<NN>(), mma_ctas<NN>()) sweep_mma_k
         // stage, no pad column
         const bool clean = nr == kTR && gcol0 + kW <= a.N &&
                            blocks_disjoint<BLK>(grow0, kTR, gcol0, kW, a.nbar);
-        if (clean) {
-          if (unit_scale)
-            mma_stage<NN, MODE, false, true, BLK>(sv, svp, srec, gout, a.ld, gcol0, grow0, nr, a.N, a.nbar, lane, A,
-                                             D, Cc, cf, sc, rsj, nst);
-          else
-            mma_stage<NN, MODE, false, false, BLK>(sv, svp, srec, gout, a.ld, gcol0, grow0, nr, a.N, a.nbar, lane,
-                                              A, D, Cc, cf, sc, rsj, nst);
+        if (MODE == kModePapg) {
+          if (clean) {
+            hot_stage = unit_scale
+                ? papg_stage<NN, false, true, BLK>(sv, svp, srec, gout, a.ld, gcol0, grow0, nr, a.N, a.nbar,
+                                                   lane, A, D, Cc, cf, sc, rsj, nst)
+                : papg_stage<NN, false, false, BLK>(sv, svp, srec, gout, a.ld, gcol0, grow0, nr, a.N,
+                                                    a.nbar, lane, A, D, Cc, cf, sc, rsj, nst);
+          } else {
+            hot_stage = unit_scale
+                ? papg_stage<NN, true, true, BLK>(sv, svp, srec, gout, a.ld, gcol0, grow0, nr, a.N, a.nbar,
+                                                  lane, A, D, Cc, cf, sc, rsj, nst)
+                : papg_stage<NN, true, false, BLK>(sv, svp, srec, gout, a.ld, gcol0, grow0, nr, a.N,
+                                                   a.nbar, lane, A, D, Cc, cf, sc, rsj, nst);
+          }
+        } else if (clean) {
+          mma_stage<NN, MODE, false, BLK>(sv, srec, gout, a.ld, gcol0, grow0, nr, a.N, a.nbar, lane, A, D,
+                                          Cc, cf, sc, rsj);
         } else {
-          if (unit_scale)
-            mma_stage<NN, MODE, true, true, BLK>(sv, svp, srec, gout, a.ld, gcol0, grow0, nr, a.N, a.nbar, lane, A,
-                                             D, Cc, cf, sc, rsj, nst);
-          else
-            mma_stage<NN, MODE, true, false, BLK>(sv, svp, srec, gout, a.ld, gcol0, grow0, nr, a.N, a.nbar, lane, A,
-                                             D, Cc, cf, sc, rsj, nst);
+          mma_stage<NN, MODE, true, BLK>(sv, srec, gout, a.ld, gcol0, grow0, nr, a.N, a.nbar, lane, A, D,
+                                         Cc, cf, sc, rsj);
         }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
       // row sums over the warp's 32 columns: lanes sharing q hold the same rows
+      // (a cold stage's are exact zeros already)
+      if (hot_stage) {
 #pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        rsj[j] += __shfl_xor_sync(0xffffffffu, rsj[j], 4);
-        rsj[j] += __shfl_xor_sync(0xffffffffu, rsj[j], 8);
-        rsj[j] += __shfl_xor_sync(0xffffffffu, rsj[j], 16);
+        for (int j = 0; j < 2; ++j) {
+          rsj[j] += __shfl_xor_sync(0xffffffffu, rsj[j], 4);
+          rsj[j] += __shfl_xor_sync(0xffffffffu, rsj[j], 8);
+          rsj[j] += __shfl_xor_sync(0xffffffffu, rsj[j], 16);
+        }
       }
       double* ra = rowacc + (flushes & 1) * kCW * kWin + warp * kWin;
       if (c8 == 0) {
