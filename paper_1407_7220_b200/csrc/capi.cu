@@ -6,7 +6,9 @@
 // The host loop of the reference (papg.cpp:136-283) is split: the per-
 // iteration scalar logic runs on the device (control_kernel), so the host
 // only enqueues work and polls a halt flag once per batch of iterations.
+#include <cuda.h>
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 #include <nccl.h>
 
 #include <chrono>
@@ -29,7 +31,54 @@ using namespace crb;
 
 cudaStream_t g_alloc_stream = nullptr;
 
-namespace crb {  // general.cu: P-APG(ALCC) with K blocks
+namespace crb {
+
+// 2-D tensor maps of the dual buffers for the DMMA P-APG producer: dims
+// {ld, R}, box {tile + 2, 8} (one stage, the 2 extra columns fill the
+// shared-memory pitch padding). Encoded once per handle through the driver
+// entry point (cudart is linked statically; no -lcuda). CRB_TMAP=0 keeps the
+// per-row bulk copies.
+static void encode_sweep_tmaps(cr_handle* h) {
+  h->tmap_ok = false;
+  const char* env = std::getenv("CRB_TMAP");
+  if ((env && env[0] == '0') || h->variant != kSweepMma || h->R <= 0) return;
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn) {
+      cudaGetLastError();
+      return;
+    }
+    encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
+  }
+  // 3-D view {TC, T, R} of the R x ld buffer (element (x, t, r) at r ld + t TC + x):
+  // x in [TC, TC + 2) is out of bounds, so the pitch-padding columns of a stage are
+  // zero-filled by the TMA unit instead of read from HBM. Columns >= ld of the
+  // last tile alias the next row (never consumed: those warps are inactive); the
+  // buffers carry TC doubles of slack for the last row's.
+  const cuuint64_t TC = (cuuint64_t)h->kp.tile_cols;
+  if (TC + 2 > 256 || h->T > INT_MAX || h->R > INT_MAX) return;
+  static_assert(sizeof(TmapBytes) == sizeof(CUtensorMap), "tensor map size");
+  for (int b = 0; b < 2; ++b) {
+    const cuuint64_t dims[3] = {TC, (cuuint64_t)h->T, (cuuint64_t)h->R};
+    const cuuint64_t strides[2] = {TC * sizeof(double), (cuuint64_t)h->ld * sizeof(double)};
+    const cuuint32_t box[3] = {(cuuint32_t)TC + 2, 1, 8};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    CUtensorMap m;
+    const CUresult r = encode(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, h->V[b], dims, strides, box, estr,
+                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+      if (std::getenv("CRB_DEBUG")) std::fprintf(stderr, "cvxreg_b200: tensor map encode failed (%d)\n", (int)r);
+      return;
+    }
+    std::memcpy(&h->tmV[b], &m, sizeof(m));
+  }
+  h->tmap_ok = true;
+}
+  // general.cu: P-APG(ALCC) with K blocks
 cr_status general_begin(cr_handle* h);
 cr_status general_iterate(cr_handle* h, int64_t max_steps, int64_t* done, int32_t* stopped,
                           double* sweep_seconds, int64_t* launches);
@@ -266,8 +315,9 @@ cr_status cr_create(const double* Xh, const double* ybar_shifted, int64_t N, int
   ALLOC(h->ybar, N);
   ALLOC(h->rowrec, N * RP);
   ALLOC(h->colrec, N * RP);
-  ALLOC(h->V[0], vlen);
-  ALLOC(h->V[1], vlen);
+  // + one column tile of slack: the tensor-map view of the last tile's row ends
+  ALLOC(h->V[0], vlen + h->kp.tile_cols);
+  ALLOC(h->V[1], vlen + h->kp.tile_cols);
   if (h->sparse_ok) {
     h->mstages = (int)((h->U + 7) / 8 + h->maxspan);
     ALLOC(h->M[0], mask_words(h));
@@ -306,6 +356,7 @@ cr_status cr_create(const double* Xh, const double* ybar_shifted, int64_t N, int
     cudaGetLastError();
     return fail(h, CR_ENOMEM, std::string("device allocation failed: ") + cudaGetErrorString(e));
   }
+  encode_sweep_tmaps(h);
   h->stage_elems = std::min<int64_t>((int64_t)1 << 25, h->R * (N - 1) + N);  // <= 256 MB
   if (dalloc(&h->stage, (size_t)h->stage_elems) != cudaSuccess) {
     cudaGetLastError();

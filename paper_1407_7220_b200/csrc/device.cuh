@@ -76,7 +76,19 @@ struct DevCtrl {
   double within_raw;
 };
 
+// opaque CUtensorMap (cuda.h): 128 bytes, 64-byte aligned; encoded on the host
+// (tmap.cu), read by the TMA unit from the kernel's parameter space
+struct alignas(64) TmapBytes {
+  unsigned long long w[16];
+};
+
 struct SweepArgs {
+  // tensor maps of V[0], V[1] (3-D view {TC, T, R}; box = one 8-row stage x
+  // (TC + 2) columns, the 2 out-of-bounds columns zero-filled into the
+  // shared-memory row pitch of the DMMA sweep); used by its P-APG producer when
+  // tmap != 0 -- one TMA per buffer and stage instead of one bulk copy per row
+  TmapBytes tmV[2];
+  int tmap;
   double* V0;             // V[0]; V[cur] is read, V[1-cur] is read (theta1_prev)
   double* V1;             // and then overwritten by v_{k+1}
   const int* cur;         // device slot index (DevCtrl::cur)

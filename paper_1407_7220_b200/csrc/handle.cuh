@@ -128,6 +128,8 @@ struct cr_handle {
   uint32_t* M[2] = {nullptr, nullptr};
   unsigned long long* d_stores = nullptr;  // multipliers written by the P-APG sweeps
   int mstages = 0;          // MaskGeo::stages
+  TmapBytes tmV[2] = {};    // tensor maps of V[0], V[1] for the DMMA P-APG producer
+  bool tmap_ok = false;
   bool sparse_ok = false;   // the masked P-APG sweep is available (MMA geometry)
   bool masked = false;      // this solve runs it (not the small-N loop)
   SweepKernelInfo ksp{};
@@ -205,6 +207,11 @@ inline SweepArgs sweep_args(cr_handle* h, int mode, bool agg_only) {
   a.M1 = h->M[1];
   a.mstages = h->mstages;
   a.stores = h->d_stores;
+  if (mode == kModePapg && h->tmap_ok) {
+    a.tmV[0] = h->tmV[0];
+    a.tmV[1] = h->tmV[1];
+    a.tmap = 1;
+  }
   return a;
 }
 inline MaskGeo mask_geo(const cr_handle* h) {

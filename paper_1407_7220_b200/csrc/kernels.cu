@@ -64,24 +64,37 @@ __global__ void __launch_bounds__(kBlock) reduce_kernel(const ReduceArgs a) {
     }
     return;
   }
-  const long long nb_col = (ncol + kBlock - 1) / kBlock;
+  // column aggregates: one block per (column tile, chunk of its TC x n1 values);
+  // the tile's values of one (CTA, segment) slot are contiguous, so a block sums
+  // a few contiguous slot arrays in CTA order (no per-element index division)
+  const long long per_tile = (long long)a.TC * n1;
+  const long long chunks = (per_tile + kBlock - 1) / kBlock;
+  const long long T = (N + a.TC - 1) / a.TC;
+  const long long nb_col = T * chunks;
   const long long nb_row = (N + kBlock - 1) / kBlock;
   const long long b = blockIdx.x;
   if (b < nb_col) {
-    const long long i = b * kBlock + threadIdx.x;
-    if (i < ncol) {
-      // column c of tile t was swept by CTAs g_lo..g_hi (contiguous unit ranges)
-      const long long c = i / n1, j = i % n1;
-      const long long t = c / a.TC, off = c % a.TC;
-      const long long g_lo = (t * a.R) / a.U;
-      long long g_hi = ((t + 1) * a.R - 1) / a.U;
-      if (g_hi > a.G - 1) g_hi = a.G - 1;
+    // column tile t was swept by CTAs g_lo..g_hi (contiguous unit ranges)
+    const long long t = b / chunks;
+    const long long e = (b - t * chunks) * kBlock + threadIdx.x;
+    const long long g_lo = (t * a.R) / a.U;
+    long long g_hi = ((t + 1) * a.R - 1) / a.U;
+    if (g_hi > a.G - 1) g_hi = a.G - 1;
+    __shared__ long long slot_off[64];
+    const long long nslot = g_hi - g_lo + 1;
+    for (long long k = threadIdx.x; k < nslot && k < 64; k += kBlock) {
+      const long long g = g_lo + k;
+      slot_off[k] = (g * a.maxspan + (t - (g * a.U) / a.R)) * per_tile;
+    }
+    __syncthreads();
+    if (e < per_tile && e < (N - t * a.TC) * n1) {
       double s = 0.0;
-      for (long long g = g_lo; g <= g_hi; ++g) {
-        const long long slot = g * a.maxspan + (t - (g * a.U) / a.R);
-        s += a.colpart[(slot * a.TC + off) * n1 + j];
+      for (long long k = 0; k < nslot; ++k) {
+        const long long off = k < 64 ? slot_off[k]
+                                     : ((g_lo + k) * a.maxspan + (t - ((g_lo + k) * a.U) / a.R)) * per_tile;
+        s += a.colpart[off + e];
       }
-      a.agg_out[N + i] = s;
+      a.agg_out[N + t * per_tile + e] = s;
     }
   } else if (b < nb_col + nb_row) {
     const long long r = (b - nb_col) * kBlock + threadIdx.x;
@@ -341,7 +354,8 @@ cudaError_t launch_primal(const PrimalArgs& a, cudaStream_t s) {
 }
 
 cudaError_t launch_reduce(const ReduceArgs& a, cudaStream_t s) {
-  const long long nb = (a.N * a.n1 + kBlock - 1) / kBlock + (a.N + kBlock - 1) / kBlock + 1;
+  const long long chunks = ((long long)a.TC * a.n1 + kBlock - 1) / kBlock;
+  const long long nb = (a.N + a.TC - 1) / a.TC * chunks + (a.N + kBlock - 1) / kBlock + 1;
   reduce_kernel<<<(unsigned)nb, kBlock, 0, s>>>(a);
   return cudaGetLastError();
 }

@@ -7,13 +7,13 @@
 
 namespace crb {
 
-// CTA geometry per n, measured on B200 (store skipping and
-// the zero-tile skips make the sweep issue bound): 7 consumer warps x 4 tiles
-// at two CTAs per SM (128-register cap, 3-stage ring) for n <= 14 -- n = 10:
-// 303 vs 372 us -- and 15 consumer warps x 2 tiles at one CTA per SM above
-// (more warps hide the longer DMMA chains; n = 20: 434 vs 526 us).
+// CTA geometry per n, measured on B200: 15 consumer
+// warps x 2 tiles at one CTA per SM for every n since the P-APG producer loads a
+// stage with one tensor TMA per buffer (n = 10: 268 us late vs 293 us for 7 warps
+// x 4 tiles at two CTAs per SM; n = 20: 316 us). CRB_WIDE_ABOVE = 14 restores the
+// narrow geometry for n <= 14 (the better one with per-row bulk copies).
 #ifndef CRB_WIDE_ABOVE
-#define CRB_WIDE_ABOVE 14
+#define CRB_WIDE_ABOVE 0
 #endif
 template <int NN>
 __host__ __device__ constexpr bool mma_wide() { return NN > CRB_WIDE_ABOVE; }

@@ -226,7 +226,7 @@ __device__ __forceinline__ void mma_stage(const double* __restrict__ sv,
 }
 
 template <int NN, int MODE, bool BLK>
-__global__ void __launch_bounds__(mma_threads<NN>(), mma_ctas<NN>()) sweep_mma_kernel(const SweepArgs a) {
+__global__ void __launch_bounds__(mma_threads<NN>(), mma_ctas<NN>()) sweep_mma_kernel(const __grid_constant__ SweepArgs a) {
   constexpr int kNS = mma_ns<NN>();
   CRB_GEO(NN)
   constexpr int KS = ksteps<NN>();
@@ -281,6 +281,16 @@ __global__ void __launch_bounds__(mma_threads<NN>(), mma_ctas<NN>()) sweep_mma_k
           double* st = stages + s * SD;
           const uint32_t bytes = (MODE == kModePapg ? 2u * nr * vbytes : 0u) +
                                  (kPen ? (uint32_t)nr * vbytes : 0u) + (uint32_t)nr * RQ * 8u;
+          if (MODE == kModePapg && a.tmap) {
+            // one tensor TMA per buffer: 8 rows x kTCP columns (the 2 pitch-padding
+            // columns and rows past the shard are zero-filled, not read)
+            mbar_arrive_expect_tx(&full[s], 2u * kTR * kTCP * 8u + (uint32_t)nr * RQ * 8u);
+            tma_g2s_3d(st, &a.tmV[cur], 0, t, (int)r, &full[s], pol_stream);
+            tma_g2s_3d(st + kTR * kTCP, &a.tmV[1 - cur], 0, t, (int)r, &full[s], pol_stream);
+            bulk_g2s(st + 2 * kTR * kTCP, a.rowrec + (a.r0 + r) * RQ, (uint32_t)nr * RQ * 8u,
+                     &full[s], pol_keep);
+            continue;
+          }
           mbar_arrive_expect_tx(&full[s], bytes);
           if (MODE == kModePapg) {
             for (int qq = 0; qq < nr; ++qq) {
