@@ -46,10 +46,58 @@ __global__ void control_kernel(DevCtrl* c, const double* scal /* kScal, allreduc
   control_step(c, scal, k2, hist);
 }
 
+// fixed-order sum of the sweep scalar records and the K2 records (one block):
+// per thread in record order (2 records per batch), warp butterflies, then the
+// 8 warps in order -- small shared memory and registers, so the reduce kernel's
+// column / row blocks run in a single wave
+__device__ __forceinline__ void scalar_records(const ReduceArgs& a, long long scal_at) {
+  constexpr int W = kScal + kK2Scal;
+  double v[W];
+#pragma unroll
+  for (int w = 0; w < W; ++w) v[w] = 0.0;
+  for (long long i0 = threadIdx.x; i0 < a.nw; i0 += 2 * kBlock) {
+    double r2[2][kScal];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const long long i = i0 + (long long)u * kBlock;
+#pragma unroll
+      for (int w = 0; w < kScal; ++w) r2[u][w] = i < a.nw ? a.scalpart[i * kScal + w] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+#pragma unroll
+      for (int w = 0; w < kScal; ++w) v[w] += r2[u][w];
+    }
+  }
+  for (long long i = threadIdx.x; i < a.nk2; i += kBlock) {
+#pragma unroll
+    for (int w = 0; w < kK2Scal; ++w) v[kScal + w] += a.k2part[i * kK2Scal + w];
+  }
+  __shared__ double sh[kBlock / 32][W];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int w = 0; w < W; ++w) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v[w] += __shfl_xor_sync(0xffffffffu, v[w], o);
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int w = 0; w < W; ++w) sh[warp][w] = v[w];
+  }
+  __syncthreads();
+  if (threadIdx.x < W) {
+    double t = 0.0;
+#pragma unroll
+    for (int k = 0; k < kBlock / 32; ++k) t += sh[k][threadIdx.x];
+    if (threadIdx.x < kScal) a.agg_out[scal_at + threadIdx.x] = t;
+    else if (a.k2sum != nullptr) a.k2sum[threadIdx.x - kScal] = t;
+  }
+}
+
 // K3: fixed-order reduction of the sweep partials. On a single GPU the last
 // block to finish also runs the control step (no separate launch); sharded
 // runs call control_kernel after the allreduce instead.
-__global__ void __launch_bounds__(kBlock) reduce_kernel(const ReduceArgs a) {
+__global__ void __launch_bounds__(kBlock, 6) reduce_kernel(const ReduceArgs a) {
   const long long N = a.N;
   const int n1 = a.n1;
   const long long ncol = N * n1;
@@ -71,9 +119,12 @@ __global__ void __launch_bounds__(kBlock) reduce_kernel(const ReduceArgs a) {
   const long long chunks = (per_tile + kBlock - 1) / kBlock;
   const long long T = (N + a.TC - 1) / a.TC;
   const long long nb_col = T * chunks;
-  const long long nb_row = (N + kBlock - 1) / kBlock;
-  const long long b = blockIdx.x;
-  if (b < nb_col) {
+  const long long nb_row = (N + 31) / 32;
+  // block 0: the scalar records (the longest chain, so it is dispatched first)
+  const long long b = (long long)blockIdx.x - 1;
+  if (b < 0) {
+    scalar_records(a, N + ncol);
+  } else if (b < nb_col) {
     // column tile t was swept by CTAs g_lo..g_hi (contiguous unit ranges)
     const long long t = b / chunks;
     const long long e = (b - t * chunks) * kBlock + threadIdx.x;
@@ -88,41 +139,53 @@ __global__ void __launch_bounds__(kBlock) reduce_kernel(const ReduceArgs a) {
     }
     __syncthreads();
     if (e < per_tile && e < (N - t * a.TC) * n1) {
+      // slot values loaded in batches of 4 (independent loads), summed in CTA order
       double s = 0.0;
-      for (long long k = 0; k < nslot; ++k) {
-        const long long off = k < 64 ? slot_off[k]
-                                     : ((g_lo + k) * a.maxspan + (t - ((g_lo + k) * a.U) / a.R)) * per_tile;
-        s += a.colpart[off + e];
+      for (long long k0 = 0; k0 < nslot; k0 += 4) {
+        double v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const long long k = k0 + u;
+          const long long off =
+              k < 64 ? slot_off[k < 64 ? k : 0]
+                     : ((g_lo + k) * a.maxspan + (t - ((g_lo + k) * a.U) / a.R)) * per_tile;
+          v[u] = k < nslot ? a.colpart[off + e] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (k0 + u < nslot) s += v[u];
       }
       a.agg_out[N + t * per_tile + e] = s;
     }
   } else if (b < nb_col + nb_row) {
-    const long long r = (b - nb_col) * kBlock + threadIdx.x;
-    if (r < N) {
-      double s = 0.0;
-      const long long lr = r - a.r0;
-      if (lr >= 0 && lr < a.R)
-        for (int st = 0; st < a.S; ++st) s += a.rowpart[st * a.R + lr];
-      a.agg_out[r] = s;
-    }
-  } else {
-    double v[kScal + kK2Scal];
+    // row sums: 32 rows x 8 slice groups per block (lane = row, warp = group of
+    // column-tile slices st = w, w + 8, ...), then a fixed-order combine
+    __shared__ double part[8][32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const long long r = (b - nb_col) * 32 + lane;
+    const long long lr = r - a.r0;
+    const bool own = r < N && lr >= 0 && lr < a.R;
+    double s = 0.0;
+    if (own) {
+      for (int st0 = w; st0 < a.S; st0 += 8 * 4) {
+        double v[4];
 #pragma unroll
-    for (int w = 0; w < kScal + kK2Scal; ++w) v[w] = 0.0;
-    for (long long i = threadIdx.x; i < a.nw; i += kBlock) {
+        for (int u = 0; u < 4; ++u) {
+          const int st = st0 + 8 * u;
+          v[u] = st < a.S ? a.rowpart[(long long)st * a.R + lr] : 0.0;
+        }
 #pragma unroll
-      for (int w = 0; w < kScal; ++w) v[w] += a.scalpart[i * kScal + w];
+        for (int u = 0; u < 4; ++u) s += v[u];
+      }
     }
-    for (long long i = threadIdx.x; i < a.nk2; i += kBlock) {
-#pragma unroll
-      for (int w = 0; w < kK2Scal; ++w) v[kScal + w] += a.k2part[i * kK2Scal + w];
-    }
-    __shared__ double out[kScal + kK2Scal];
-    block_reduce_store<kScal + kK2Scal>(v, out);
+    part[w][lane] = s;
     __syncthreads();
-    if (threadIdx.x < kScal) a.agg_out[N + ncol + threadIdx.x] = out[threadIdx.x];
-    else if (threadIdx.x < kScal + kK2Scal && a.k2sum != nullptr)
-      a.k2sum[threadIdx.x - kScal] = out[threadIdx.x];
+    if (w == 0 && r < N) {
+      double u = 0.0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) u += part[k][lane];
+      a.agg_out[r] = u;
+    }
   }
   if (a.ctrl == nullptr) return;
   // last block done -> control step (all blocks read the halt flag above
@@ -355,7 +418,7 @@ cudaError_t launch_primal(const PrimalArgs& a, cudaStream_t s) {
 
 cudaError_t launch_reduce(const ReduceArgs& a, cudaStream_t s) {
   const long long chunks = ((long long)a.TC * a.n1 + kBlock - 1) / kBlock;
-  const long long nb = (a.N + a.TC - 1) / a.TC * chunks + (a.N + kBlock - 1) / kBlock + 1;
+  const long long nb = (a.N + a.TC - 1) / a.TC * chunks + (a.N + 31) / 32 + 1;
   reduce_kernel<<<(unsigned)nb, kBlock, 0, s>>>(a);
   return cudaGetLastError();
 }
