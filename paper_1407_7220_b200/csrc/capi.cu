@@ -343,7 +343,8 @@ cr_status cr_create(const double* Xh, const double* ybar_shifted, int64_t N, int
   h->power_grid = power_loop_grid(sms);
   if (const char* pg = std::getenv("CRB_POWER_GRID")) h->power_grid = std::max(1, std::atoi(pg));
   ALLOC(h->gram, n * n + n);
-  ALLOC(h->ps_part, (size_t)h->power_grid * (2 + 2 * n));
+  // op-C power loop: two step-parity buffers of (4 + 2n)-value records
+  ALLOC(h->ps_part, (size_t)h->power_grid * 2 * (4 + 2 * n));
   ALLOC(h->ps_part2, (size_t)h->power_grid * 2);
   ALLOC(h->ps_state, 4);
   ALLOC(h->consts, 4);

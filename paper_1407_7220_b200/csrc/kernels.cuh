@@ -62,7 +62,7 @@ struct PowerLoopArgs {
   double* v;            // N (n+1) scratch
   const double* X;
   const double* gram;   // [S (n x n) | s (n)]
-  double* part;         // [grid][2 + 2n]
+  double* part;         // op 0: [2][grid][4 + 2n]; ops 1, 2: [grid][2 + 2n]
   double* part2;        // [grid][2]
   double* state;        // out: sigma, iterations, converged
   long long N;

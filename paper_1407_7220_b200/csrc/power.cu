@@ -114,6 +114,77 @@ __device__ __forceinline__ void apply_point(const double* v, const double* X, co
   acc[1] += vu;
 }
 
+// Linear sums of the raw vector u (A, Cs, B[n], AX[n] with a = u_y, b = u_xi):
+// the sums of v = u / |u| are these divided by |u|, so the power step needs
+// one grid barrier instead of two (SURVEY K4').
+template <int NN>
+__device__ __forceinline__ void sums_raw(double a, const double (&b)[NN], const double (&x)[NN],
+                                         double* acc /* 2 + 2 NN */) {
+  double bx = 0.0;
+#pragma unroll
+  for (int j = 0; j < NN; ++j) {
+    bx = fma(b[j], x[j], bx);
+    acc[2 + j] += b[j];
+    acc[2 + NN + j] = fma(a, x[j], acc[2 + NN + j]);
+  }
+  acc[0] += a;
+  acc[1] += a - bx;
+}
+
+// one fused point of a single-barrier power step: v_l = u_l / norm_u (kept),
+// u_l <- (C^T C v)_l with the global sums of v, accumulates (|u|^2, v.u) and the
+// raw sums of the new u for the next step
+template <int NN>
+__device__ __forceinline__ void power_point_fused(double* u, double* vout, const double* X,
+                                                  const double* gram, const double* sums,
+                                                  double norm_u, long long N, long long l,
+                                                  double (&acc)[4 + 2 * NN]) {
+  const double A = sums[0], Cs = sums[1];
+  const double* B = sums + 2;
+  const double* AX = sums + 2 + NN;
+  const double* S = gram;
+  const double* sx = gram + NN * NN;
+  const double Nm1 = (double)(N - 1);
+  const double a = __ldcg(u + l) / norm_u;
+  __stcg(vout + l, a);
+  double b[NN], x[NN];
+  double bx = 0.0;
+#pragma unroll
+  for (int j = 0; j < NN; ++j) {
+    b[j] = __ldcg(u + N + l * NN + j) / norm_u;
+    __stcg(vout + N + l * NN + j, b[j]);
+    x[j] = X[l * NN + j];
+    bx = fma(b[j], x[j], bx);
+  }
+  const double c = a - bx;
+  double Bx = 0.0, bs = 0.0;
+#pragma unroll
+  for (int j = 0; j < NN; ++j) {
+    Bx = fma(B[j] - b[j], x[j], Bx);
+    bs = fma(b[j], sx[j] - x[j], bs);
+  }
+  const double R = Nm1 * a - (Cs - c) - Bx;
+  const double Col = (A - a) - Nm1 * c - bs;
+  const double uy = a + R - Col;  // pos rows + row sums - column sums
+  __stcg(u + l, uy);
+  double uu = uy * uy, vu = a * uy;
+  double ux[NN];
+#pragma unroll
+  for (int j = 0; j < NN; ++j) {
+    double Sb = 0.0;
+#pragma unroll
+    for (int k = 0; k < NN; ++k) Sb = fma(S[j * NN + k], b[k], Sb);
+    const double T = (AX[j] - a * x[j]) - c * (sx[j] - x[j]) - (Sb - x[j] * bx);
+    ux[j] = Col * x[j] - T;
+    __stcg(u + N + l * NN + j, ux[j]);
+    uu = fma(ux[j], ux[j], uu);
+    vu = fma(b[j], ux[j], vu);
+  }
+  acc[0] += uu;
+  acc[1] += vu;
+  sums_raw<NN>(uy, ux, x, acc + 2);
+}
+
 // op_A1 (operators.cpp:341-345): A1^T A1 = 2 (N I - 1 1^T) over all N(N-1)
 // rows, so u_l = 2 (N v_l - A) with A = sum v.
 __device__ __forceinline__ void apply_point_a1(const double* v, const double* sums, long long N,
@@ -180,16 +251,41 @@ __device__ __forceinline__ void block_sum_store(double (&v)[W], double* out) {
 }
 
 // every block: out[w] = sum over the grid's records part[g][w], fixed order
-// (warp-per-column, lanes over records, butterfly)
+// (warp-per-column, lanes over records, butterfly). All of a warp's loads are
+// issued before the first add: one L2 round trip per step instead of one per
+// record batch.
 template <int W>
 __device__ __forceinline__ void grid_records_sum(const double* part, int nrec, double* out) {
+  constexpr int kWarps = kQBlock / 32;
+  constexpr int kCols = (W + kWarps - 1) / kWarps;  // columns per warp
+  constexpr int kRec = 24 / kCols > 2 ? 24 / kCols : 2;  // records per lane held at once
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int w = warp; w < W; w += kQBlock / 32) {
-    double s = 0.0;
-    for (int g = lane; g < nrec; g += 32) s += __ldcg(part + (long long)g * W + w);
+  double s[kCols];
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane == 0) out[w] = s;
+  for (int c = 0; c < kCols; ++c) s[c] = 0.0;
+  for (int g0 = 0; g0 < nrec; g0 += 32 * kRec) {
+    double v[kCols][kRec];
+#pragma unroll
+    for (int c = 0; c < kCols; ++c) {
+      const int w = warp + c * kWarps;
+#pragma unroll
+      for (int k = 0; k < kRec; ++k) {
+        const int g = g0 + k * 32 + lane;
+        v[c][k] = (w < W && g < nrec) ? __ldcg(part + (long long)g * W + w) : 0.0;
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < kCols; ++c) {
+#pragma unroll
+      for (int k = 0; k < kRec; ++k) s[c] += v[c][k];
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < kCols; ++c) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s[c] += __shfl_xor_sync(0xffffffffu, s[c], o);
+    const int w = warp + c * kWarps;
+    if (lane == 0 && w < W) out[w] = s[c];
   }
   __syncthreads();
 }
@@ -271,11 +367,90 @@ __global__ void __launch_bounds__(kQBlock) power_loop_kernel(const PowerLoopArgs
   }
 }
 
+// op 0 with one grid barrier per step: the records of step k carry (|u|^2,
+// v.u) and the raw sums of the new u; every block reduces them in the same
+// fixed order, so all blocks take identical decisions. Records are double
+// buffered by step parity (a block can be at most one barrier ahead).
+template <int NN>
+__global__ void __launch_bounds__(kQBlock) power_loop_c_kernel(const PowerLoopArgs a) {
+  constexpr int W = 2 + 2 * NN;  // raw sums
+  constexpr int W2 = 2 + W;      // (|u|^2, v.u) + raw sums
+  cg::grid_group grid = cg::this_grid();
+  const long long tid = (long long)blockIdx.x * kQBlock + threadIdx.x;
+  const long long nthreads = (long long)gridDim.x * kQBlock;
+  const long long N = a.N;
+  __shared__ double red[W2];
+  __shared__ double sums[W];
+  // prologue: raw sums of the (host-normalised) start vector
+  {
+    double acc[W2];
+#pragma unroll
+    for (int w = 0; w < W2; ++w) acc[w] = 0.0;
+    for (long long l = tid; l < N; l += nthreads) {
+      double b[NN], x[NN];
+#pragma unroll
+      for (int j = 0; j < NN; ++j) {
+        b[j] = __ldcg(a.u + N + l * NN + j);
+        x[j] = a.X[l * NN + j];
+      }
+      sums_raw<NN>(__ldcg(a.u + l), b, x, acc + 2);
+    }
+    block_sum_store<W2>(acc, a.part + (long long)blockIdx.x * W2);
+  }
+  grid.sync();
+  grid_records_sum<W2>(a.part, gridDim.x, red);
+  double norm_u = 1.0;
+  double lambda_prev = 0.0;
+  for (int it = 1; it <= a.max_iters; ++it) {
+    if (threadIdx.x < W) sums[threadIdx.x] = red[2 + threadIdx.x] / norm_u;
+    __syncthreads();
+    double* part = a.part + (long long)(it & 1) * gridDim.x * W2;
+    {
+      double acc[W2];
+#pragma unroll
+      for (int w = 0; w < W2; ++w) acc[w] = 0.0;
+      for (long long l = tid; l < N; l += nthreads)
+        power_point_fused<NN>(a.u, a.v, a.X, a.gram, sums, norm_u, N, l, acc);
+      block_sum_store<W2>(acc, part + (long long)blockIdx.x * W2);
+    }
+    grid.sync();
+    grid_records_sum<W2>(part, gridDim.x, red);
+    // identical in every block: operators.cpp:318-334
+    const double lambda = red[1];  // |C v|^2 = v . C^T C v
+    const double nu = sqrt(red[0]);
+    bool done = false;
+    double sigma = 0.0;
+    int conv = 1;
+    if (nu == 0.0 || lambda == 0.0) {
+      done = true;
+    } else {
+      norm_u = nu;
+      if (it > 1 && fabs(lambda - lambda_prev) <= a.tol * lambda) {
+        sigma = sqrt(lambda) * 1.01;
+        done = true;
+      } else if (it == a.max_iters) {
+        sigma = sqrt(lambda) * 1.10;  // the reference inflates lambda_prev = lambda here
+        conv = 0;
+        done = true;
+      }
+      lambda_prev = lambda;
+    }
+    if (done) {
+      if (blockIdx.x == 0 && threadIdx.x == 0) {
+        a.state[0] = sigma;
+        a.state[1] = (double)it;
+        a.state[2] = (double)conv;
+      }
+      return;
+    }
+  }
+}
+
 template <int NN>
 void power_loop_n(const PowerLoopArgs& a, int grid, cudaStream_t s, cudaError_t* err) {
   void* args[] = {const_cast<PowerLoopArgs*>(&a)};
-  *err = cudaLaunchCooperativeKernel((const void*)power_loop_kernel<NN>, dim3((unsigned)grid),
-                                     dim3(kQBlock), args, 0, s);
+  const void* fn = a.op == 0 ? (const void*)power_loop_c_kernel<NN> : (const void*)power_loop_kernel<NN>;
+  *err = cudaLaunchCooperativeKernel(fn, dim3((unsigned)grid), dim3(kQBlock), args, 0, s);
 }
 using PowerLoopFn = void (*)(const PowerLoopArgs&, int, cudaStream_t, cudaError_t*);
 
