@@ -356,7 +356,10 @@ def run_ours(args):
                                    + (" (weak scaling N=1e4*sqrt(p))" if world > 1 else ""),
                        "N": N, "n": n, "pairs_per_step": pairs_step,
                        "rows_per_gpu": rows, "sweep_variant": variant,
-                       "l2": "inputs > L2 (V, V' = 1.6 GB per GPU), no flush",
+                       "l2": (f"inputs > L2 (V, V' = {16 * rows * N / 1e9:.3g} GB per GPU), no flush"
+                              if 16 * rows * N > 126e6 else
+                              f"inputs < L2 (V, V' = {16 * rows * N / 1e6:.3g} MB): L2-resident "
+                              "by design, no flush"),
                        "sigma_C": sigma, "sigma_power_steps": sig_iters,
                        "timing": "CUDA events on the solver stream, max over ranks",
                        "wall_s": t_wall},
@@ -493,7 +496,8 @@ def run_alcc_ours(args):
                                f"K MAPG iterations)", "N": N, "n": n, "solver": "alcc",
                    "sweep_variant": variant, "sigma_A": [s1[0], s2[0]],
                    "sigma_power_steps": [s1[1], s2[1]], "sigma_seconds": sig_s,
-                   "l2": "theta (0.8 GB) > L2, no flush",
+                   "l2": f"theta ({8 * N * N / 1e9:.3g} GB) " + ("> L2, no flush" if 8 * N * N > 126e6
+                                                                        else "< L2, no flush"),
                    "timing": "CUDA events around the MAPG graph launches"},
         "roofline": roofline, "cpu_baseline": cpu, "gpu_launches": int(res.launches),
         "clocks": clk.summary(),
