@@ -94,14 +94,17 @@ __device__ __forceinline__ void scalar_records(const ReduceArgs& a, long long sc
   }
 }
 
-// K3: fixed-order reduction of the sweep partials. On a single GPU the last
-// block to finish also runs the control step (no separate launch); sharded
-// runs call control_kernel after the allreduce instead.
+// K3: fixed-order reduction of the sweep partials. On a single GPU block 0
+// also runs the control step (no separate launch); sharded runs call
+// control_kernel after the allreduce instead.
 __global__ void __launch_bounds__(kBlock, 6) reduce_kernel(const ReduceArgs a) {
   const long long N = a.N;
   const int n1 = a.n1;
   const long long ncol = N * n1;
-  if (a.stopped != nullptr && *a.stopped) {
+  // With the control step fused (single GPU) only block 0 looks at the halt flag:
+  // it is the block that may set it, and a halted solve's sweep did not run, so
+  // re-reducing its unchanged partials rewrites identical aggregates.
+  if (a.ctrl == nullptr && a.stopped != nullptr && *a.stopped) {
     // halted: keep the (already reduced) payload on rank 0, zero it elsewhere,
     // so a trailing in-place allreduce leaves it unchanged on every rank
     if (a.rank != 0) {
@@ -123,7 +126,14 @@ __global__ void __launch_bounds__(kBlock, 6) reduce_kernel(const ReduceArgs a) {
   // block 0: the scalar records (the longest chain, so it is dispatched first)
   const long long b = (long long)blockIdx.x - 1;
   if (b < 0) {
+    // scalars first, then (single GPU) the control step right away: it needs
+    // only the scalars, so it runs while the other blocks reduce the aggregates
+    if (a.ctrl != nullptr && a.ctrl->halt) return;
     scalar_records(a, N + ncol);
+    if (a.ctrl != nullptr) {
+      __syncthreads();
+      if (threadIdx.x == 0) control_step(a.ctrl, a.agg_out + N + ncol, a.k2sum, a.hist);
+    }
   } else if (b < nb_col) {
     // column tile t was swept by CTAs g_lo..g_hi (contiguous unit ranges)
     const long long t = b / chunks;
@@ -185,24 +195,6 @@ __global__ void __launch_bounds__(kBlock, 6) reduce_kernel(const ReduceArgs a) {
 #pragma unroll
       for (int k = 0; k < 8; ++k) u += part[k][lane];
       a.agg_out[r] = u;
-    }
-  }
-  if (a.ctrl == nullptr) return;
-  // last block done -> control step (all blocks read the halt flag above
-  // before any block can get here, so the update cannot race with them)
-  __shared__ bool last;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    last = atomicAdd(a.counter, 1u) == gridDim.x - 1;
-  }
-  __syncthreads();
-  if (last && threadIdx.x == 0) {
-    __threadfence();
-    *a.counter = 0u;
-    DevCtrl* c = a.ctrl;
-    if (!c->halt) {
-      control_step(c, a.agg_out + N + ncol, a.k2sum, a.hist);
     }
   }
 }

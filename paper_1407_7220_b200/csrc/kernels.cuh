@@ -37,7 +37,7 @@ struct ReduceArgs {
   const int* stopped;     // halted: rank 0 keeps agg_out, other ranks zero it
   DevCtrl* ctrl;          // non-null: the last block runs the control step
   double* hist;
-  unsigned int* counter;  // last-block detection (self-resetting)
+  unsigned int* counter;  // (unused by the reduce kernel; kept for the ABI of ReduceArgs users)
   int rank;
   long long N, ld, R, r0, nw, nk2, U;
   int n1, S, TC, G, maxspan;
