@@ -38,6 +38,11 @@ __global__ void __launch_bounds__(kSBlock) small_loop_kernel(const SmallArgs a) 
   const long long nwarps = nthreads >> 5;
   const long long N = a.N;
   DevCtrl* c = a.ctrl;
+  // block 0 runs the control step on a shared-memory copy of the state (loaded
+  // once per launch, written back when the launch ends); every iteration it
+  // publishes the fields the other blocks read (halt, cur, s_cur, s_prev, beta)
+  __shared__ DevCtrl sctrl;
+  if (blockIdx.x == 0 && threadIdx.x == 0) sctrl = *c;
   const bool tr0 = a.trace != nullptr && blockIdx.x == 0 && threadIdx.x == 0;
   auto stamp = [&](long long it, int k) {
     if (tr0 && it < 64) {
@@ -90,7 +95,7 @@ __global__ void __launch_bounds__(kSBlock) small_loop_kernel(const SmallArgs a) 
         for (int j = 0; j <= NN; ++j) acc[j] = 0.0;
         double vv = 0.0, vr = 0.0, tr = 0.0, nn = 0.0;
         // U rows in flight: all loads of a batch are issued before its math
-        constexpr int U = (NN + 3) <= 8 ? 4 : ((NN + 3) <= 16 ? 2 : 1);
+        constexpr int U = NN <= 5 ? 8 : ((NN + 3) <= 8 ? 4 : ((NN + 3) <= 16 ? 2 : 1));
         for (long long r0 = rlo; r0 < rhi; r0 += U) {
           double xb[U][NN], yb[U], cb[U], pb[U];
 #pragma unroll
@@ -114,6 +119,16 @@ __global__ void __launch_bounds__(kSBlock) small_loop_kernel(const SmallArgs a) 
             for (int j = 0; j < NN; ++j) row = fma(xb[u][j], xi[j], row);
             if (!valid || col == r) row = 0.0;
             const double c1 = cb[u], p1 = pb[u];
+            // cold: theta1 = theta1_prev = 0 (stored multipliers are never -0) and
+            // row >= 0 -> theta2 = 0, v = 0 = p1: no store, every update below adds
+            // an exact zero (late in a solve almost every row of a strip)
+            const bool hot = ((unsigned long long)__double_as_longlong(c1) |
+                              (unsigned long long)__double_as_longlong(p1)) != 0ull ||
+                             __double2hiint(row) < 0;
+            if (!__any_sync(0xffffffffu, hot)) {
+              if (lane == 0) __stcg(a.rowpart + r * a.S + strip, 0.0);
+              continue;
+            }
             double th2;
             if (unit) {
               th2 = fma(beta, c1 - p1, c1);
@@ -175,45 +190,75 @@ __global__ void __launch_bounds__(kSBlock) small_loop_kernel(const SmallArgs a) 
 
     // ---- C: fixed-order reduction (+ scalars and control in block 0)
     {
-      // one warp per output element: lanes split the partials, fixed butterfly
+      // 8 lanes per output element: its partials are contiguous (colpart
+      // [N(n+1)][P], rowpart [N][S]); lane g of the group sums the g-th
+      // contiguous slice, then a fixed 3-step butterfly inside the group
       const long long ncol = N * (NN + 1);
-      for (long long e = gwarp; e < ncol + N; e += nwarps) {
+      const int g = lane & 7;
+      // warp-uniform loop (4 elements per warp) so the group shuffles see every lane
+      for (long long eb = (tid >> 5) * 4; eb < ncol + N; eb += (nthreads >> 5) * 4) {
+        const long long e = eb + (lane >> 3);
+        const bool colp = e < ncol;
+        const double* src = colp ? a.colpart + e * a.P : a.rowpart + (e - ncol) * a.S;
+        const int cnt = e < ncol + N ? (colp ? a.P : a.S) : 0;
+        const int per = (cnt + 7) >> 3;
+        const int lo = g * per, hi = min(cnt, lo + per);
         double s = 0.0;
-        if (e < ncol) {
-          const double* src = a.colpart + e * a.P;  // contiguous over the chunks
-          for (int p = lane; p < a.P; p += 32) s += __ldcg(src + p);
-        } else {
-          const double* src = a.rowpart + (e - ncol) * a.S;  // contiguous over the strips
-          for (int st = lane; st < a.S; st += 32) s += __ldcg(src + st);
-        }
+        for (int p0 = lo; p0 < hi; p0 += 8) {
+          double v[8];
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-        if (lane == 0) __stcg(a.xbuf + (e < ncol ? N + e : e - ncol), s);
+          for (int u = 0; u < 8; ++u) v[u] = p0 + u < hi ? __ldcg(src + p0 + u) : 0.0;
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            if (p0 + u < hi) s += v[u];
+        }
+        s += __shfl_xor_sync(0xffffffffu, s, 1);
+        s += __shfl_xor_sync(0xffffffffu, s, 2);
+        s += __shfl_xor_sync(0xffffffffu, s, 4);
+        if (g == 0 && e < ncol + N) __stcg(a.xbuf + (colp ? N + e : e - ncol), s);
       }
       stamp(it, 5);
       if (blockIdx.x == 0) {
-        double v[kScal + kK2Scal];
+        // scalar records: thread order, warp butterflies, warps in order
+        constexpr int W = kScal + kK2Scal;
+        double v[W];
 #pragma unroll
-        for (int w = 0; w < kScal + kK2Scal; ++w) v[w] = 0.0;
-        const long long nw = gridDim.x;  // one scalar record per block
-        for (long long i = threadIdx.x; i < nw; i += kSBlock) {
+        for (int w = 0; w < W; ++w) v[w] = 0.0;
+        for (long long i = threadIdx.x; i < gridDim.x; i += kSBlock) {
 #pragma unroll
           for (int w = 0; w < kScal; ++w) v[w] += __ldcg(a.scalpart + i * kScal + w);
-        }
-        for (long long i = threadIdx.x; i < gridDim.x; i += kSBlock) {
 #pragma unroll
           for (int w = 0; w < kK2Scal; ++w) v[kScal + w] += __ldcg(a.k2part + i * kK2Scal + w);
         }
-        __shared__ double out[kScal + kK2Scal];
-        block_reduce_store<kScal + kK2Scal, kSBlock>(v, out);
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) v[w] += __shfl_xor_sync(0xffffffffu, v[w], o);
+        }
+        __shared__ double wsc[kSBlock / 32][W];
+        __shared__ double out[W];
+        if (lane == 0) {
+#pragma unroll
+          for (int w = 0; w < W; ++w) wsc[threadIdx.x >> 5][w] = v[w];
+        }
+        __syncthreads();
+        if (threadIdx.x < W) {
+          double t = 0.0;
+#pragma unroll
+          for (int k = 0; k < kSBlock / 32; ++k) t += wsc[k][threadIdx.x];
+          out[threadIdx.x] = t;
+        }
         __syncthreads();
         if (threadIdx.x == 0) {
           double* scal = a.xbuf + N + ncol;
           for (int w = 0; w < kScal; ++w) scal[w] = out[w];
           for (int w = 0; w < kK2Scal; ++w) a.k2sum[w] = out[kScal + w];
-          if (!c->halt) {
-            control_step(c, scal, a.k2sum, a.hist);
-          }
+          if (!sctrl.halt) control_step(&sctrl, out, out + kScal, a.hist);
+          __stcg(&c->halt, sctrl.halt);
+          __stcg(&c->cur, sctrl.cur);
+          __stcg(&c->s_cur, sctrl.s_cur);
+          __stcg(&c->s_prev, sctrl.s_prev);
+          __stcg(&c->beta, sctrl.beta);
           __threadfence();
         }
       }
@@ -222,6 +267,7 @@ __global__ void __launch_bounds__(kSBlock) small_loop_kernel(const SmallArgs a) 
     grid.sync();
     stamp(it, 7);
   }
+  if (blockIdx.x == 0 && threadIdx.x == 0) *c = sctrl;  // full state for the host
 }
 
 template <int NN>
