@@ -27,6 +27,39 @@ namespace {
 
 constexpr int kSBlock = 256;
 
+// Row sums of U rows over a warp's 32 columns (lane = column) with a
+// transpose-reduce: log2(U) halving exchanges (xor 16, 8, ...) leave each lane
+// one row's partial, then a butterfly over the remaining lane bits. U - 1 + (5 -
+// log2 U) shuffles instead of 5 U; fixed order, so deterministic. Returns the
+// row index (within the U) whose sum lanes with (lane & (32/U - 1)) == 0 hold.
+template <int U>
+__device__ __forceinline__ int rows_transpose_sum(double (&t)[U], int lane, double& out) {
+  int row = 0;
+  int width = U;
+  int bit = 16;
+#pragma unroll
+  for (int lvl = 0; (1 << lvl) < U; ++lvl) {
+    const bool upper = (lane & bit) != 0;
+    const int half = width >> 1;
+#pragma unroll
+    for (int i = 0; i < U / 2; ++i) {
+      if (i < half) {
+        const double send = upper ? t[i] : t[i + half];
+        const double keep = upper ? t[i + half] : t[i];
+        t[i] = keep + __shfl_xor_sync(0xffffffffu, send, bit);
+      }
+    }
+    if (upper) row += half;
+    width = half;
+    bit >>= 1;
+  }
+  double v = t[0];
+#pragma unroll
+  for (int o = bit; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  out = v;
+  return row;
+}
+
 template <int NN>
 __global__ void __launch_bounds__(kSBlock) small_loop_kernel(const SmallArgs a) {
   constexpr int RP = rec_pitch(NN);
@@ -110,10 +143,13 @@ __global__ void __launch_bounds__(kSBlock) small_loop_kernel(const SmallArgs a) 
             cb[u] = valid ? __ldcg(Vc + r * a.ld + col) : 0.0;
             pb[u] = valid ? __ldcg(Vp + r * a.ld + col) : 0.0;
           }
+          double vrow[U];  // this lane's v of the batch's rows (0 when cold / absent)
+          bool any_hot = false;
 #pragma unroll
           for (int u = 0; u < U; ++u) {
+            vrow[u] = 0.0;
             const long long r = r0 + u;
-            if (r >= rhi) break;
+            if (r >= rhi) continue;
             double row = yb[u] + cc;
 #pragma unroll
             for (int j = 0; j < NN; ++j) row = fma(xb[u][j], xi[j], row);
@@ -125,10 +161,8 @@ __global__ void __launch_bounds__(kSBlock) small_loop_kernel(const SmallArgs a) 
             const bool hot = ((unsigned long long)__double_as_longlong(c1) |
                               (unsigned long long)__double_as_longlong(p1)) != 0ull ||
                              __double2hiint(row) < 0;
-            if (!__any_sync(0xffffffffu, hot)) {
-              if (lane == 0) __stcg(a.rowpart + r * a.S + strip, 0.0);
-              continue;
-            }
+            if (!__any_sync(0xffffffffu, hot)) continue;
+            any_hot = true;
             double th2;
             if (unit) {
               th2 = fma(beta, c1 - p1, c1);
@@ -148,11 +182,14 @@ __global__ void __launch_bounds__(kSBlock) small_loop_kernel(const SmallArgs a) 
             acc[0] += v;
 #pragma unroll
             for (int j = 0; j < NN; ++j) acc[1 + j] = fma(v, xb[u][j], acc[1 + j]);
-            double rs = v;  // fixed butterfly over the strip's 32 columns
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) rs += __shfl_xor_sync(0xffffffffu, rs, o);
-            if (lane == 0) __stcg(a.rowpart + r * a.S + strip, rs);  // [N][S]
+            vrow[u] = v;
           }
+          // row sums of the batch over the strip's 32 columns -> rowpart [N][S]
+          double rs = 0.0;
+          int ru = lane / (32 / U);  // all-cold batch: zero sums, no shuffles
+          if (any_hot) ru = rows_transpose_sum<U>(vrow, lane, rs);
+          if ((lane & (32 / U - 1)) == 0 && r0 + ru < rhi)
+            __stcg(a.rowpart + (r0 + ru) * a.S + strip, rs);
         }
         // [N][n+1][P]: the P partials of one column entry are contiguous
         if (valid) {
