@@ -15,23 +15,29 @@ namespace {
 constexpr int kBlock = 256;
 constexpr int kPBlock = 64;  // O(N) kernels: small blocks so N = 1e4 still spans every SM
 
-// deterministic block reduction of W values per thread (fixed tree)
+// deterministic block reduction of W values per thread: warp butterflies, then
+// the warps' sums in warp order (threads < W write out[w]; callers that read
+// out from other threads synchronise first)
 template <int W, int BS = kBlock>
 __device__ void block_reduce_store(double (&v)[W], double* out /* W values */) {
-  __shared__ double sh[W][BS];
+  constexpr int NW = BS / 32;
+  __shared__ double sh[NW][W];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
-  for (int w = 0; w < W; ++w) sh[w][threadIdx.x] = v[w];
-  __syncthreads();
-  for (int s = BS / 2; s > 0; s >>= 1) {
-    if ((int)threadIdx.x < s) {
+  for (int w = 0; w < W; ++w) {
 #pragma unroll
-      for (int w = 0; w < W; ++w) sh[w][threadIdx.x] += sh[w][threadIdx.x + s];
-    }
-    __syncthreads();
+    for (int o = 16; o > 0; o >>= 1) v[w] += __shfl_xor_sync(0xffffffffu, v[w], o);
   }
-  if (threadIdx.x == 0) {
+  if (lane == 0) {
 #pragma unroll
-    for (int w = 0; w < W; ++w) out[w] = sh[w][0];
+    for (int w = 0; w < W; ++w) sh[warp][w] = v[w];
+  }
+  __syncthreads();
+  if ((int)threadIdx.x < W) {
+    double t = 0.0;
+#pragma unroll
+    for (int k = 0; k < NW; ++k) t += sh[k][threadIdx.x];
+    out[threadIdx.x] = t;
   }
 }
 
