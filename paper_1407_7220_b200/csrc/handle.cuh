@@ -207,7 +207,7 @@ inline SweepArgs sweep_args(cr_handle* h, int mode, bool agg_only) {
   a.M1 = h->M[1];
   a.mstages = h->mstages;
   a.stores = h->d_stores;
-  if (mode == kModePapg && h->tmap_ok) {
+  if ((mode == kModePapg || mode == kModePenalty || mode == kModePenaltyUpdate) && h->tmap_ok) {
     a.tmV[0] = h->tmV[0];
     a.tmV[1] = h->tmV[1];
     a.tmap = 1;

@@ -281,12 +281,15 @@ __global__ void __launch_bounds__(mma_threads<NN>(), mma_ctas<NN>()) sweep_mma_k
           double* st = stages + s * SD;
           const uint32_t bytes = (MODE == kModePapg ? 2u * nr * vbytes : 0u) +
                                  (kPen ? (uint32_t)nr * vbytes : 0u) + (uint32_t)nr * RQ * 8u;
-          if (MODE == kModePapg && a.tmap) {
+          if ((MODE == kModePapg || kPen) && a.tmap) {
             // one tensor TMA per buffer: 8 rows x kTCP columns (the 2 pitch-padding
-            // columns and rows past the shard are zero-filled, not read)
-            mbar_arrive_expect_tx(&full[s], 2u * kTR * kTCP * 8u + (uint32_t)nr * RQ * 8u);
+            // columns and rows past the shard are zero-filled, not read); the
+            // penalty modes read theta = V[cur] only
+            constexpr uint32_t nbuf = MODE == kModePapg ? 2u : 1u;
+            mbar_arrive_expect_tx(&full[s], nbuf * kTR * kTCP * 8u + (uint32_t)nr * RQ * 8u);
             tma_g2s_3d(st, &a.tmV[cur], 0, t, (int)r, &full[s], pol_stream);
-            tma_g2s_3d(st + kTR * kTCP, &a.tmV[1 - cur], 0, t, (int)r, &full[s], pol_stream);
+            if (MODE == kModePapg)
+              tma_g2s_3d(st + kTR * kTCP, &a.tmV[1 - cur], 0, t, (int)r, &full[s], pol_stream);
             bulk_g2s(st + 2 * kTR * kTCP, a.rowrec + (a.r0 + r) * RQ, (uint32_t)nr * RQ * 8u,
                      &full[s], pol_keep);
             continue;
