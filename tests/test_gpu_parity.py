@@ -461,3 +461,56 @@ def test_masked_store_warm_start_and_blocks(oracle, monkeypatch):
     g = gpu_run(X, ys, max_iters=25, gap_norm_tol=-1.0, infeas_norm_tol=-1.0, sigma_C=s,
                 theta0=th0)
     assert_parity(g, o)
+
+
+@pytest.mark.parametrize("kind,N,n,pieces", [("maxaffine-uniform", 1000, 10, 8),
+                                             ("lse-uniform", 777, 20, 12),
+                                             ("sqnorm-uniform", 503, 3, 0)])
+def test_tensor_map_producer_bitwise_equals_row_copies(oracle, monkeypatch, kind, N, n, pieces):
+    """The DMMA P-APG producer loads a stage with one 3-D tensor TMA per buffer
+    (pitch padding zero-filled out of bounds); CRB_TMAP=0 keeps the per-row bulk
+    copies. Same shared-memory contents -> bitwise identical solves, both at
+    oracle parity (ragged N: the last tile's view runs past ld)."""
+    monkeypatch.setenv("CRB_SMALL", "0")
+    monkeypatch.setenv("CRB_SWEEP", "mma")
+    X, ys = instance(oracle, kind, N, n, 0.1, 21, pieces)
+    s, _, _ = oracle.sigma_C(X)
+    kw = dict(max_iters=120, gap_norm_tol=-1.0, infeas_norm_tol=-1.0, sigma_C=s)
+    a = gpu_run(X, ys, **kw)
+    monkeypatch.setenv("CRB_TMAP", "0")
+    b = gpu_run(X, ys, **kw)
+    assert np.array_equal(a["theta"], b["theta"]) and np.array_equal(a["y"], b["y"])
+    assert_parity(a, oracle_run(oracle, X, ys, **kw))
+
+
+def test_alcc_penalty_sweep_tensor_map_bitwise(oracle, monkeypatch):
+    """The ALCC penalty sweeps (per-kernel path, CRB_ALCC_LOOP=0) read theta
+    through the same tensor map: bitwise identical to the per-row copies."""
+    monkeypatch.setenv("CRB_SWEEP", "mma")
+    monkeypatch.setenv("CRB_ALCC_LOOP", "0")
+    X, y = oracle.gen_instance("maxaffine-uniform", 900, 6, 0.1, 5, 6)
+    P = oracle.prepare(X, y, 1e-3)
+    cfg = crb.AlccConfig(sigma_A1=oracle.sigma_A(X, 1)[0], sigma_A2=oracle.sigma_A(X, 2)[0],
+                         max_outer=2)
+    bounds = crb.ProblemBounds(P.B_theta, P.Bbar_y, P.Bbar_xi, P.gamma)
+    out = []
+    for tm in ("1", "0"):
+        monkeypatch.setenv("CRB_TMAP", tm)
+        with crb.DualSolver(X, P.ys, P.gamma) as s:
+            res, yy, xi, hist, mi = s.alcc(cfg, bounds, crb.PrimalPoint(P.feas_y, P.feas_xi))
+            out.append((res.outer_iters, list(mi), yy, xi, s.alcc_multiplier()))
+    assert out[0][0] == out[1][0] and out[0][1] == out[1][1]
+    for k in (2, 3, 4):
+        assert np.array_equal(out[0][k], out[1][k])
+
+
+@pytest.mark.parametrize("grid", ["148", "64", "7"])
+def test_sigma_power_grid_sizes(oracle, monkeypatch, grid):
+    """One-barrier power loop: same step count and sigma (1e-10) for any grid."""
+    X, _ = instance(oracle, "maxaffine-uniform", 3000, 8, 0.1, 9, 10)
+    so, it_o, _ = oracle.sigma_C(X)
+    monkeypatch.setenv("CRB_POWER_GRID", grid)
+    with crb.DualSolver(X, np.zeros(len(X))) as d:
+        sg, it_g, conv = d.sigma_C()
+    assert it_g == it_o and conv
+    assert abs(sg - so) <= 1e-10 * so
