@@ -118,8 +118,35 @@ PrimalArgs primal_args(cr_handle* h, int mode) {
 
 // Enqueue one dual iteration (papg.cpp:176-263). phase: 0 = all,
 // 1 = local part only (K2, K1, K3), 2 = finish only (control).
+// The fused path (one GPU, singleton blocks, dense store): K3 + Kc + the next
+// iteration's K2 in one launch; the standalone primal is enqueued only at the
+// start of an iterate call / graph and is a no-op when the last fused launch
+// already computed it (DevCtrl::primal_done). Opt-in: CRB_FUSE=1.
+bool fused_path(const cr_handle* h) {
+  return h->fuse_ok && h->comm == nullptr && h->part.K == 0 && !h->masked;
+}
+
 cr_status enqueue_iteration(cr_handle* h, int phase, cudaEvent_t ev_a, cudaEvent_t ev_b,
                             bool use_nccl) {
+  if (phase == 0 && fused_path(h)) {
+    if (h->primal_pending) {
+      PrimalArgs pa = primal_args(h, 0);
+      pa.fuse_ctrl = h->ctrl_d;
+      CUDA_TRY(launch_primal(pa, h->st));
+      h->primal_pending = false;
+    }
+    const SweepArgs sa = sweep_args(h, kModePapg, false);
+    if (ev_a) CUDA_TRY(cudaEventRecord(ev_a, h->st));
+    CUDA_TRY((cudaError_t)launch_sweep(papg_sweep(h), sa, h->st));
+    if (ev_b) CUDA_TRY(cudaEventRecord(ev_b, h->st));
+    FusedArgs fa{};
+    fa.r = reduce_args(h, true, &h->ctrl_d->halt, true, papg_sweep(h).warps_per_block);
+    fa.p = primal_args(h, 0);
+    fa.ticket = h->fuse_sync;
+    fa.flag = h->fuse_sync + 1;
+    CUDA_TRY(launch_reduce_primal(fa, h->st));
+    return CR_OK;
+  }
   if (phase != 2) {
     const PrimalArgs pa = primal_args(h, 0);
     CUDA_TRY(launch_primal(pa, h->st));
@@ -143,7 +170,7 @@ cr_status enqueue_iteration(cr_handle* h, int phase, cudaEvent_t ev_a, cudaEvent
 }
 
 // our kernels per iteration (the NCCL allreduce kernel is not counted)
-int launches_per_iteration(const cr_handle* h) { return h->comm ? 4 : 3; }
+int launches_per_iteration(const cr_handle* h) { return h->comm ? 4 : (fused_path(h) ? 2 : 3); }
 
 cr_status build_graph(cr_handle* h) {
   if (h->gexec) {
@@ -153,6 +180,7 @@ cr_status build_graph(cr_handle* h) {
   cudaGraph_t g = nullptr;
   CUDA_TRY(cudaStreamBeginCapture(h->st, cudaStreamCaptureModeThreadLocal));
   cr_status s = CR_OK;
+  h->primal_pending = true;  // each graph launch starts with the (no-op unless needed) primal
   for (int i = 0; i < h->graph_iters && s == CR_OK; ++i)
     s = enqueue_iteration(h, 0, nullptr, nullptr, true);
   cudaError_t e = cudaStreamEndCapture(h->st, &g);
@@ -266,6 +294,11 @@ cr_status cr_create(const double* Xh, const double* ybar_shifted, int64_t N, int
   g_alloc_stream = h->st;
   // sweep variant, measured on B200: the DMMA sweep is
   // faster than the CUDA-core DFMA one for every n. CRB_SWEEP=dfma|mma overrides.
+  // fused reduce + primal: opt-in (CRB_FUSE=1). Measured slower than the two
+  // kernels at cfg 2 (24.8 vs 21.9 us of non-sweep time per step): the control
+  // step sits on its critical path behind 2220 per-warp scalar records
+  const char* fz = std::getenv("CRB_FUSE");
+  h->fuse_ok = fz && fz[0] == '1';
   const char* var = std::getenv("CRB_SWEEP");
   h->variant = kSweepMma;
   if (var && std::strcmp(var, "dfma") == 0) h->variant = kSweepDfma;
@@ -332,7 +365,8 @@ cr_status cr_create(const double* Xh, const double* ybar_shifted, int64_t N, int
   ALLOC(h->scalpart, (size_t)h->G * std::max(h->kp.warps_per_block,
                                               h->sparse_ok ? h->ksp.warps_per_block : 0) *
                         kScal);
-  ALLOC(h->k2part, (size_t)h->k2_blocks * kK2Scal);
+  // K2 records of the standalone primal (k2_blocks) or the fused kernel's point blocks
+  ALLOC(h->k2part, (size_t)std::max(h->k2_blocks, fused_blocks(N)) * kK2Scal);
   ALLOC(h->k2sum, kK2Scal);
   ALLOC(h->yout, N);
   ALLOC(h->xiout, N * n);
@@ -350,6 +384,7 @@ cr_status cr_create(const double* Xh, const double* ybar_shifted, int64_t N, int
   ALLOC(h->consts, 4);
   ALLOC(h->izero, 1);
   ALLOC(h->counter, 1);
+  ALLOC(h->fuse_sync, 2);
   ALLOC(h->d_stores, 1);
   ALLOC(h->ctrl_d, 1);
 #undef ALLOC
@@ -389,6 +424,7 @@ cr_status cr_create(const double* Xh, const double* ybar_shifted, int64_t N, int
   CUDA_TRY(cudaMemcpyAsync(h->consts, consts, sizeof(consts), cudaMemcpyHostToDevice, h->st));
   CUDA_TRY(cudaMemsetAsync(h->izero, 0, sizeof(int), h->st));
   CUDA_TRY(cudaMemsetAsync(h->counter, 0, sizeof(unsigned int), h->st));
+  CUDA_TRY(cudaMemsetAsync(h->fuse_sync, 0, 2 * sizeof(unsigned long long), h->st));
   CUDA_TRY(cudaMemsetAsync(h->d_stores, 0, sizeof(unsigned long long), h->st));
   CUDA_TRY(cudaMemsetAsync(h->ctrl_d, 0, sizeof(DevCtrl), h->st));
   CUDA_TRY(launch_gram(h->X, N, (int)n, h->gram, h->st));
@@ -415,6 +451,7 @@ void cr_destroy(cr_handle* h) {
   for (double* b : {h->s_colpart, h->s_rowpart, h->s_scalpart, h->s_k2part}) dfree(b, h->st);
   dfree(h->izero, h->st);
   dfree(h->counter, h->st);
+  dfree(h->fuse_sync, h->st);
   dfree(h->M[0], h->st);
   dfree(h->M[1], h->st);
   dfree(h->d_stores, h->st);
@@ -859,6 +896,8 @@ cr_status cr_papg_iterate(cr_handle* h, int64_t max_steps, int64_t* done, int32_
   }
   const bool timed_sweeps = h->graph_iters == 0;
   const int per_unit = h->graph_iters > 0 ? h->graph_iters : 4;
+  h->primal_pending = true;  // direct launches: the call starts with the (maybe no-op) primal
+  int64_t extra_launches = (h->graph_iters == 0 && fused_path(h)) ? 1 : 0;
   int64_t enq_iters = 0;
   int64_t units = 0;
   bool halted = h->ctrl_h->stopped || max_steps == 0;
@@ -916,7 +955,8 @@ cr_status cr_papg_iterate(cr_handle* h, int64_t max_steps, int64_t* done, int32_
   h->last_sweep_seconds = sw;
   h->last_launches = (h->graph_iters > 0 ? units * h->graph_iters
                                          : std::min<int64_t>(enq_iters, max_steps)) *
-                     launches_per_iteration(h);
+                         launches_per_iteration(h) +
+                     (h->graph_iters > 0 && fused_path(h) ? units : extra_launches);
   h->loop_seconds +=
       std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();
   if (done) *done = h->ctrl_h->ell;

@@ -74,6 +74,11 @@ struct DevCtrl {
   // general-K partition: |within-block infeasibility| of the current eta
   // (dual_gradient's within_infeas_raw, papg.cpp:128), host-set per iteration
   double within_raw;
+  // fused reduce + primal (kernels.cu): 1 when the primal of the next iteration
+  // has been computed (the standalone primal kernel is then a no-op); k2_count =
+  // number of K2 records the last primal wrote
+  int primal_done;
+  int k2_count;
 };
 
 // opaque CUtensorMap (cuda.h): 128 bytes, 64-byte aligned; encoded on the host

@@ -87,6 +87,10 @@ struct cr_handle {
   long long U = 0;      // (tile, row) units per CTA
   int k2_blocks = 0;
   unsigned int* counter = nullptr;
+  // fused reduce + primal (single GPU): block start tickets and the control flag
+  unsigned long long* fuse_sync = nullptr;  // [ticket, flag]
+  bool fuse_ok = false;       // this handle may run the fused path (CRB_FUSE != 0, one GPU)
+  bool primal_pending = true; // enqueue the (possibly no-op) standalone primal next
   // device buffers
   double *X = nullptr, *ybar = nullptr, *rowrec = nullptr, *colrec = nullptr;
   double *V[2] = {nullptr, nullptr}, *vpos[2] = {nullptr, nullptr};

@@ -23,6 +23,10 @@ namespace {
 template <int NN>
 __global__ void __launch_bounds__(kPBlock) primal_kernel(const PrimalArgs a) {
   if (a.stopped != nullptr && *a.stopped) return;
+  if (a.fuse_ctrl != nullptr) {  // fused path: the last fused launch already ran it
+    if (__ldcg(&a.fuse_ctrl->primal_done)) return;
+    if (blockIdx.x == 0 && threadIdx.x == 0) a.fuse_ctrl->k2_count = (int)gridDim.x;
+  }
   const long long N = a.N;
   const double s_c = a.coef[0];
   const double s_p = a.mode == 0 ? a.coef[1] : 0.0;
@@ -50,7 +54,8 @@ __global__ void control_kernel(DevCtrl* c, const double* scal /* kScal, allreduc
 // per thread in record order (2 records per batch), warp butterflies, then the
 // 8 warps in order -- small shared memory and registers, so the reduce kernel's
 // column / row blocks run in a single wave
-__device__ __forceinline__ void scalar_records(const ReduceArgs& a, long long scal_at) {
+__device__ __forceinline__ void scalar_records(const ReduceArgs& a, long long scal_at,
+                                               long long nk2) {
   constexpr int W = kScal + kK2Scal;
   double v[W];
 #pragma unroll
@@ -69,9 +74,9 @@ __device__ __forceinline__ void scalar_records(const ReduceArgs& a, long long sc
       for (int w = 0; w < kScal; ++w) v[w] += r2[u][w];
     }
   }
-  for (long long i = threadIdx.x; i < a.nk2; i += kBlock) {
+  for (long long i = threadIdx.x; i < nk2; i += kBlock) {
 #pragma unroll
-    for (int w = 0; w < kK2Scal; ++w) v[kScal + w] += a.k2part[i * kK2Scal + w];
+    for (int w = 0; w < kK2Scal; ++w) v[kScal + w] += __ldcg(a.k2part + i * kK2Scal + w);
   }
   __shared__ double sh[kBlock / 32][W];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -129,7 +134,7 @@ __global__ void __launch_bounds__(kBlock, 6) reduce_kernel(const ReduceArgs a) {
     // scalars first, then (single GPU) the control step right away: it needs
     // only the scalars, so it runs while the other blocks reduce the aggregates
     if (a.ctrl != nullptr && a.ctrl->halt) return;
-    scalar_records(a, N + ncol);
+    scalar_records(a, N + ncol, a.nk2);
     if (a.ctrl != nullptr) {
       __syncthreads();
       if (threadIdx.x == 0) control_step(a.ctrl, a.agg_out + N + ncol, a.k2sum, a.hist);
@@ -195,6 +200,139 @@ __global__ void __launch_bounds__(kBlock, 6) reduce_kernel(const ReduceArgs a) {
 #pragma unroll
       for (int k = 0; k < 8; ++k) u += part[k][lane];
       a.agg_out[r] = u;
+    }
+  }
+}
+
+// Fused K3 + Kc + K2 (one GPU, singleton blocks). Blocks take their role by
+// start order (a ticket), so the control block is always resident before any
+// block waits for it. Control block: scalar records + control step, then the
+// flag. Point blocks (32 points each): the points' row sums (T slices) and
+// column aggregates (their tile's slot arrays) -> xbuf, wait for the flag, then
+// the primal closed form of the next iteration (papg.cpp:176-182 at theta2)
+// unless the control step halted. Same fixed-order sums as reduce_kernel.
+constexpr int kFPts = 32;
+int fused_blocks_impl(long long N) { return (int)((N + kFPts - 1) / kFPts) + 1; }
+
+template <int NN>
+__global__ void __launch_bounds__(kBlock) reduce_primal_kernel(const FusedArgs f) {
+  constexpr int n1 = NN + 1;
+  const ReduceArgs& a = f.r;
+  const long long N = a.N;
+  const long long ncol = N * n1;
+  DevCtrl* c = a.ctrl;
+  __shared__ unsigned long long s_ticket;
+  if (threadIdx.x == 0) s_ticket = atomicAdd(f.ticket, 1ull);
+  __syncthreads();
+  const unsigned long long gen = s_ticket / gridDim.x;
+  const long long bid = (long long)(s_ticket % gridDim.x);
+  if (bid == 0) {  // ---- scalars + control
+    const int halted = __ldcg(&c->halt);
+    if (!halted) {
+      scalar_records(a, N + ncol, __ldcg(&c->k2_count));
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+      if (!halted) control_step(c, a.agg_out + N + ncol, a.k2sum, a.hist);
+      c->primal_done = c->halt ? 0 : 1;
+      c->k2_count = (int)gridDim.x - 1;
+      __threadfence();
+      asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(f.flag), "l"(gen + 1) : "memory");
+    }
+    return;
+  }
+  // ---- point block: points [l0, l0 + 32)
+  const long long l0 = (bid - 1) * kFPts;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  // row sums: lane = point, warp = slice group (slices st = w, w + 8, ...)
+  {
+    __shared__ double part[kBlock / 32][kFPts];
+    const long long r = l0 + lane;
+    const long long lr = r - a.r0;
+    double s = 0.0;
+    if (r < N && lr >= 0 && lr < a.R) {
+      for (int st0 = w; st0 < a.S; st0 += 8 * 4) {
+        double v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int st = st0 + 8 * u;
+          v[u] = st < a.S ? __ldcg(a.rowpart + (long long)st * a.R + lr) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) s += v[u];
+      }
+    }
+    part[w][lane] = s;
+    // column aggregates: item e = (point, value) of the block's 32 x n1 entries
+    const long long per_tile = (long long)a.TC * n1;
+    for (int e = threadIdx.x; e < kFPts * n1; e += kBlock) {
+      const long long l = l0 + e / n1;
+      if (l >= N) continue;
+      const int j = e % n1;
+      const long long t = l / a.TC;
+      const long long off = (l - t * a.TC) * n1 + j;  // within the tile's slot array
+      const long long g_lo = (t * a.R) / a.U;
+      long long g_hi = ((t + 1) * a.R - 1) / a.U;
+      if (g_hi > a.G - 1) g_hi = a.G - 1;
+      double sum = 0.0;
+      for (long long g0 = g_lo; g0 <= g_hi; g0 += 4) {
+        double v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const long long g = g0 + u;
+          v[u] = g <= g_hi
+                     ? __ldcg(a.colpart + (g * a.maxspan + (t - (g * a.U) / a.R)) * per_tile + off)
+                     : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (g0 + u <= g_hi) sum += v[u];
+      }
+      a.agg_out[N + l * n1 + j] = sum;
+    }
+    __syncthreads();
+    if (w == 0 && l0 + lane < N) {
+      double u = 0.0;
+#pragma unroll
+      for (int k = 0; k < kBlock / 32; ++k) u += part[k][lane];
+      a.agg_out[l0 + lane] = u;
+    }
+  }
+  // ---- wait for the control step of this launch
+  if (threadIdx.x == 0) {
+    unsigned long long v;
+    for (;;) {
+      asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(f.flag) : "memory");
+      if (v >= gen + 1) break;
+      __nanosleep(32);
+    }
+  }
+  __syncthreads();
+  if (__ldcg(&c->halt)) return;  // halted (or paused): no primal for a next iteration
+  // ---- K2 at theta2 of the next iteration for the block's points
+  const PrimalArgs& p = f.p;
+  const int cur = __ldcg(&c->cur);
+  const double s_c = __ldcg(&c->s_cur), s_p = __ldcg(&c->s_prev), beta = __ldcg(&c->beta);
+  const double* vposc = cur ? p.vpos1 : p.vpos0;
+  double* vposp = cur ? p.vpos0 : p.vpos1;
+  double acc[kK2Scal];
+#pragma unroll
+  for (int k = 0; k < kK2Scal; ++k) acc[k] = 0.0;
+  if (threadIdx.x < kFPts && l0 + threadIdx.x < N)
+    primal_point<NN>(p, l0 + threadIdx.x, s_c, s_p, beta, vposc, vposp, acc);
+  // the 32 primal threads are warp 0: one butterfly, fixed order
+  if (w == 0) {
+#pragma unroll
+    for (int k = 0; k < kK2Scal; ++k) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], o);
+    }
+    if (lane < kK2Scal) {
+      double val = acc[0];
+#pragma unroll
+      for (int k = 1; k < kK2Scal; ++k)
+        if (lane == k) val = acc[k];
+      p.k2part[(bid - 1) * kK2Scal + lane] = val;
     }
   }
 }
@@ -412,6 +550,24 @@ cudaError_t launch_reduce(const ReduceArgs& a, cudaStream_t s) {
   const long long chunks = ((long long)a.TC * a.n1 + kBlock - 1) / kBlock;
   const long long nb = (a.N + a.TC - 1) / a.TC * chunks + (a.N + 31) / 32 + 1;
   reduce_kernel<<<(unsigned)nb, kBlock, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+int fused_blocks(long long N) { return fused_blocks_impl(N); }
+
+template <int NN>
+void launch_reduce_primal_n(const FusedArgs& a, cudaStream_t s) {
+  reduce_primal_kernel<NN><<<(unsigned)fused_blocks_impl(a.r.N), kBlock, 0, s>>>(a);
+}
+using FusedLauncher = void (*)(const FusedArgs&, cudaStream_t);
+cudaError_t launch_reduce_primal(const FusedArgs& a, cudaStream_t s) {
+  static constexpr FusedLauncher tab[kMaxN] = {
+#define CRB_LF(N) launch_reduce_primal_n<N>
+      CRB_N_SEQ(CRB_LF)
+#undef CRB_LF
+};
+  if (a.p.n < 1 || a.p.n > kMaxN) return cudaErrorInvalidValue;
+  tab[a.p.n - 1](a, s);
   return cudaGetLastError();
 }
 

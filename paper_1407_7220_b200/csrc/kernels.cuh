@@ -19,6 +19,7 @@ struct PrimalArgs {
   double* k2part;        // [blocks][kK2Scal]
   const double* coef;    // {s_cur, s_prev, beta}
   const int* stopped;
+  DevCtrl* fuse_ctrl;    // mode 0, fused path: no-op if primal_done, else k2_count = blocks
   double* yout;          // mode 1
   double* xiout;         // mode 1
   double invL, gamma;
@@ -97,6 +98,17 @@ int power_loop_grid(int sms);
 cudaError_t launch_power_loop(const PowerLoopArgs& a, int grid, cudaStream_t s);
 cudaError_t launch_primal(const PrimalArgs& a, cudaStream_t s);
 cudaError_t launch_reduce(const ReduceArgs& a, cudaStream_t s);
+// fused K3 + Kc + K2 of the next iteration (one GPU): block 0 (by start order)
+// reduces the scalars and runs the control step; 32-point blocks reduce their
+// points' aggregates, wait for the control flag and run the primal closed form
+struct FusedArgs {
+  ReduceArgs r;
+  PrimalArgs p;
+  unsigned long long* ticket;  // block start-order counter (monotone across launches)
+  unsigned long long* flag;    // control done: generation + 1
+};
+int fused_blocks(long long N);
+cudaError_t launch_reduce_primal(const FusedArgs& a, cudaStream_t s);
 cudaError_t launch_control(DevCtrl* c, const double* scal, const double* k2, double* hist,
                            cudaStream_t s);
 cudaError_t launch_begin(DevCtrl* c, cudaStream_t s);

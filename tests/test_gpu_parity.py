@@ -514,3 +514,29 @@ def test_sigma_power_grid_sizes(oracle, monkeypatch, grid):
         sg, it_g, conv = d.sigma_C()
     assert it_g == it_o and conv
     assert abs(sg - so) <= 1e-10 * so
+
+
+@pytest.mark.parametrize("graph_iters", [-1, 16])
+def test_fused_reduce_primal_parity(oracle, monkeypatch, graph_iters):
+    """Opt-in fused K3 + Kc + K2 (CRB_FUSE=1): oracle parity, pieces and
+    thresholds termination, identical to the two-kernel path."""
+    monkeypatch.setenv("CRB_SMALL", "0")
+    X, ys = instance(oracle, "maxaffine-uniform", 1500, 7, 0.1, 31, 9)
+    s, _, _ = oracle.sigma_C(X)
+    kw = dict(max_iters=130, gap_norm_tol=-1.0, infeas_norm_tol=-1.0, sigma_C=s,
+              graph_iters=graph_iters)
+    monkeypatch.setenv("CRB_FUSE", "1")
+    a = gpu_run(X, ys, **kw)
+    assert_parity(a, oracle_run(oracle, X, ys, **kw))
+    cfg = crb.PapgConfig(**kw)
+    with crb.DualSolver(X, ys) as d:  # iterate in pieces: pauses skip the fused primal
+        d.begin(cfg)
+        for k in (1, 3, 50, 1000):
+            done, stopped = d.iterate(k)
+        assert done == 130 and stopped
+        assert np.array_equal(d.theta(), a["theta"])
+    t = gpu_run(X, ys, max_iters=5000, sigma_C=s, graph_iters=graph_iters)
+    monkeypatch.setenv("CRB_FUSE", "0")
+    u = gpu_run(X, ys, max_iters=5000, sigma_C=s, graph_iters=graph_iters)
+    assert t["res"].iters == u["res"].iters and t["res"].reason == u["res"].reason
+    assert rel(t["y"], u["y"]) <= 1e-12
