@@ -140,7 +140,7 @@ cr_status enqueue_iteration(cr_handle* h, int phase, cudaEvent_t ev_a, cudaEvent
     CUDA_TRY((cudaError_t)launch_sweep(papg_sweep(h), sa, h->st));
     if (ev_b) CUDA_TRY(cudaEventRecord(ev_b, h->st));
     FusedArgs fa{};
-    fa.r = reduce_args(h, true, &h->ctrl_d->halt, true, papg_sweep(h).warps_per_block);
+    fa.r = reduce_args(h, true, &h->ctrl_d->halt, true, papg_sweep(h).scal_recs);
     fa.p = primal_args(h, 0);
     fa.ticket = h->fuse_sync;
     fa.flag = h->fuse_sync + 1;
@@ -157,7 +157,7 @@ cr_status enqueue_iteration(cr_handle* h, int phase, cudaEvent_t ev_a, cudaEvent
     // single GPU, full iteration: the reduce kernel's last block runs the control step
     const bool fuse = phase == 0 && h->comm == nullptr;
     const ReduceArgs ra =
-        reduce_args(h, true, &h->ctrl_d->halt, fuse, papg_sweep(h).warps_per_block);
+        reduce_args(h, true, &h->ctrl_d->halt, fuse, papg_sweep(h).scal_recs);
     CUDA_TRY(launch_reduce(ra, h->st));
     if (use_nccl && h->comm)
       NCCL_TRY(ncclAllReduce(h->xbuf, h->xbuf, (size_t)payload_len(h), ncclDouble, ncclSum,
@@ -724,7 +724,7 @@ cr_status begin_impl(cr_handle* h, const cr_papg_config* cfg, const double* thet
     // aggregates and |.|^2 of max(theta0, 0): a sweep with 1/L = 0 is a copy
     const SweepArgs sa = sweep_args(h, kModePapg, true);
     CUDA_TRY((cudaError_t)launch_sweep(papg_sweep(h), sa, h->st));
-    const ReduceArgs ra = reduce_args(h, false, nullptr, false, papg_sweep(h).warps_per_block);
+    const ReduceArgs ra = reduce_args(h, false, nullptr, false, papg_sweep(h).scal_recs);
     CUDA_TRY(launch_reduce(ra, h->st));
     if (h->comm)
       NCCL_TRY(ncclAllReduce(h->xbuf, h->xbuf, (size_t)payload_len(h), ncclDouble, ncclSum,

@@ -188,6 +188,7 @@ struct SweepKernelInfo {
   int warps_per_block;    // consumer warps
   int max_blocks_per_sm;
   int tile_cols;          // TC = warps_per_block * strip_cols
+  int scal_recs;          // sweep scalar records per CTA (scalpart [G * scal_recs][kScal])
   int threads;
   int smem_bytes;
 };

@@ -459,7 +459,7 @@ cr_status general_iterate(cr_handle* h, int64_t max_steps, int64_t* done, int32_
     CUDA_TRY((cudaError_t)launch_sweep(papg_sweep(h), sa, h->st));
     CUDA_TRY(cudaEventRecord(h->ev_end, h->st));
     const ReduceArgs ra =
-        reduce_args(h, true, &h->ctrl_d->halt, true, papg_sweep(h).warps_per_block);
+        reduce_args(h, true, &h->ctrl_d->halt, true, papg_sweep(h).scal_recs);
     CUDA_TRY(launch_reduce(ra, h->st));
     s = pull_ctrl(h);
     if (s != CR_OK) return s;

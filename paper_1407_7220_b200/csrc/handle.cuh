@@ -228,7 +228,7 @@ inline size_t mask_words(const cr_handle* h) {
 inline const SweepKernelInfo& papg_sweep(const cr_handle* h) { return h->masked ? h->ksp : h->kp; }
 
 inline ReduceArgs reduce_args(cr_handle* h, bool with_k2, const int* stopped, bool fuse_control,
-                              int sweep_warps = 0) {
+                              int sweep_warps = 0 /* scalar records per sweep CTA */) {
   ReduceArgs a{};
   a.colpart = h->colpart;
   a.rowpart = h->rowpart;
@@ -245,7 +245,7 @@ inline ReduceArgs reduce_args(cr_handle* h, bool with_k2, const int* stopped, bo
   a.ld = h->ld;
   a.R = h->R;
   a.r0 = h->r0;
-  a.nw = (long long)h->G * (sweep_warps > 0 ? sweep_warps : h->kp.warps_per_block);
+  a.nw = (long long)h->G * (sweep_warps > 0 ? sweep_warps : h->kp.scal_recs);
   a.nk2 = with_k2 ? h->k2_blocks : 0;
   a.n1 = (int)h->n + 1;
   a.S = h->T;

@@ -393,6 +393,7 @@ SweepKernelInfo info_for(int mode, bool blocked) {
   }
   inf.strip_cols = 32 * cols_per_lane<NN>();
   inf.warps_per_block = consumer_warps<NN>();
+  inf.scal_recs = consumer_warps<NN>();
   inf.tile_cols = tile_cols<NN>();
   inf.threads = threads_per_cta<NN>();
   inf.smem_bytes = smem_bytes<NN>();

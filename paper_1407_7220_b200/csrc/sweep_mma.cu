@@ -453,12 +453,21 @@ __global__ void __launch_bounds__(mma_threads<NN>(), mma_ctas<NN>()) sweep_mma_k
     tr += __shfl_xor_sync(0xffffffffu, tr, off);
     nn += __shfl_xor_sync(0xffffffffu, nn, off);
   }
+  // one scalar record per CTA: the consumer warps' sums combined in warp order
+  // (in the row-sum window buffer the last flush did not use)
+  double* wsc = rowacc + (flushes & 1) * kCW * kWin;
   if (lane == 0) {
-    double* sp = a.scalpart + ((long long)blockIdx.x * kCW + warp) * kScal;
-    sp[0] = vv;
-    sp[1] = vr;
-    sp[2] = tr;
-    sp[3] = nn;
+    wsc[warp * kScal + 0] = vv;
+    wsc[warp * kScal + 1] = vr;
+    wsc[warp * kScal + 2] = tr;
+    wsc[warp * kScal + 3] = nn;
+  }
+  asm volatile("bar.sync 1, %0;" ::"r"(kCW * 32) : "memory");
+  if (warp == 0 && lane < kScal) {
+    double t = 0.0;
+#pragma unroll
+    for (int w = 0; w < kCW; ++w) t += wsc[w * kScal + lane];
+    a.scalpart[(long long)blockIdx.x * kScal + lane] = t;
   }
   if (MODE == kModePapg && a.stores != nullptr) {
 #pragma unroll
@@ -484,6 +493,7 @@ SweepKernelInfo info_for(int mode, bool blocked) {
   }
   inf.strip_cols = kW;
   inf.warps_per_block = kCW;
+  inf.scal_recs = 1;
   inf.tile_cols = kTC;
   inf.threads = kThreads;
   inf.smem_bytes = smem_bytes<NN>();

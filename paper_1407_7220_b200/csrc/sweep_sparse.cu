@@ -502,6 +502,7 @@ SweepKernelInfo sp_info_for(bool blocked) {
                    : (const void*)sweep_sparse_kernel<NN, false>;
   inf.strip_cols = kW;
   inf.warps_per_block = kCW;
+  inf.scal_recs = kCW;
   inf.tile_cols = kTC;
   inf.threads = kThreads;
   inf.smem_bytes = sp_smem_bytes<NN>();
