@@ -122,6 +122,15 @@ PrimalArgs primal_args(cr_handle* h, int mode) {
 // iteration's K2 in one launch; the standalone primal is enqueued only at the
 // start of an iterate call / graph and is a no-op when the last fused launch
 // already computed it (DevCtrl::primal_done). Opt-in: CRB_FUSE=1.
+// rng_stream(0x5eed, 97) normals, normalised (operators.cpp:309-313)
+void sigma_start_vector(int64_t cols, double* v) {
+  host::normal_stream(0x5eedULL, 97, cols, v);
+  double ss = 0;
+  for (int64_t i = 0; i < cols; ++i) ss += v[i] * v[i];
+  const double nv = std::sqrt(ss);
+  for (int64_t i = 0; i < cols; ++i) v[i] /= nv;
+}
+
 bool fused_path(const cr_handle* h) {
   return h->fuse_ok && h->comm == nullptr && h->part.K == 0 && !h->masked;
 }
@@ -288,6 +297,11 @@ cr_status cr_create(const double* Xh, const double* ybar_shifted, int64_t N, int
   h->RP = rec_pitch((int)n);
   h->gamma = gamma;
   h->cfg.gamma = gamma;
+  h->sigma_prep = std::thread([h] {  // overlaps the allocations and uploads below
+    const int64_t cols = h->N * (h->n + 1);
+    h->sigma_start.resize((size_t)cols);
+    sigma_start_vector(cols, h->sigma_start.data());
+  });
   CUDA_TRY(cudaSetDevice(device));
   CUDA_TRY(cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking));
   keep_pool_memory(device);
@@ -436,6 +450,7 @@ cr_status cr_create(const double* Xh, const double* ybar_shifted, int64_t N, int
 
 void cr_destroy(cr_handle* h) {
   if (!h) return;
+  if (h->sigma_prep.joinable()) h->sigma_prep.join();
   cudaSetDevice(h->device);
   if (h->st) cudaStreamSynchronize(h->st);
   if (h->part.K > 0) general_release(h);
@@ -498,15 +513,14 @@ cr_status cr_sigma_C(cr_handle* h, double tol, int32_t max_iters, double* sigma,
   CUDA_TRY(cudaSetDevice(h->device));
   const auto t0 = std::chrono::steady_clock::now();
   const int64_t cols = h->N * (h->n + 1);
-  // fixed seeded start (operators.cpp:309-313)
-  std::vector<double> v((size_t)cols);
-  host::normal_stream(0x5eedULL, 97, cols, v.data());
-  double ss = 0;
-  for (double x : v) ss += x * x;
-  const double nv = std::sqrt(ss);
-  for (double& x : v) x /= nv;
-  CUDA_TRY(cudaMemcpyAsync(h->pw_u, v.data(), sizeof(double) * cols, cudaMemcpyHostToDevice,
-                           h->st));
+  // fixed seeded start (operators.cpp:309-313), drawn at handle creation
+  if (h->sigma_prep.joinable()) h->sigma_prep.join();
+  if ((int64_t)h->sigma_start.size() != cols) {
+    h->sigma_start.resize((size_t)cols);
+    sigma_start_vector(cols, h->sigma_start.data());
+  }
+  CUDA_TRY(cudaMemcpyAsync(h->pw_u, h->sigma_start.data(), sizeof(double) * cols,
+                           cudaMemcpyHostToDevice, h->st));
   // closed-form steps assume singleton blocks; a K-block partition masks the
   // same-block pairs inside the sweep instead
   if (!h->sigma_by_sweep && h->part.K == 0) {  // whole power iteration in one cooperative launch

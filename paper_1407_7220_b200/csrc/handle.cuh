@@ -8,6 +8,7 @@
 #include <chrono>
 #include <cstdint>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/cvxreg_b200.h"
@@ -126,6 +127,10 @@ struct cr_handle {
   // timing
   cudaEvent_t ev_start = nullptr, ev_end = nullptr, ev_poll[2] = {nullptr, nullptr};
   std::vector<cudaEvent_t> ev_sweep;  // pairs
+  // sigma_max(C) start vector (rng_stream(0x5eed, 97), normalised), drawn on a
+  // host thread while the handle's device state is set up
+  std::thread sigma_prep;
+  std::vector<double> sigma_start;
   double last_seconds = 0, last_sweep_seconds = 0;
   int64_t last_launches = 0;
   // masked dual store (sweep_sparse.cu): live-bit words of V[0], V[1]
