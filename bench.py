@@ -321,12 +321,18 @@ def run_ours(args):
                                      " final re-solve, D2H of (y, xi)"}
         if world == 1 and args.config == "cfg2":
             # time to tolerance: BASELINE cfg 2 runs to |gap_norm| <= 1e-4 (and infeas <= 1e-1)
+            # (median of 5 fresh solves: each is ~20 ms, so host-side jitter matters)
             tcfg = crb.PapgConfig(gap_norm_tol=1e-4, device=local)
-            t0 = time.perf_counter()
-            tr = crb.papg_solve(prep, tcfg, want_dual=False)
-            tt = time.perf_counter() - t0
+            runs = []
+            for _ in range(5):
+                t0 = time.perf_counter()
+                tr = crb.papg_solve(prep, tcfg, want_dual=False)
+                runs.append((time.perf_counter() - t0, tr))
+            runs.sort(key=lambda x: x[0])
+            tt, tr = runs[len(runs) // 2]
             extras["time_to_tolerance"] = {
-                "seconds": tt, "iterations": tr.report.iters, "reason": tr.report.reason.name,
+                "seconds": tt, "seconds_min": runs[0][0], "samples": len(runs),
+                "iterations": tr.report.iters, "reason": tr.report.reason.name,
                 "sigma_seconds": tr.sigma_seconds, "sigma_power_steps": tr.sigma_iters,
                 "loop_seconds": tr.loop_seconds, "gap_norm_tol": 1e-4, "infeas_norm_tol": 0.1}
 

@@ -123,8 +123,8 @@ PrimalArgs primal_args(cr_handle* h, int mode) {
 // start of an iterate call / graph and is a no-op when the last fused launch
 // already computed it (DevCtrl::primal_done). Opt-in: CRB_FUSE=1.
 // rng_stream(0x5eed, 97) normals, normalised (operators.cpp:309-313)
-void sigma_start_vector(int64_t cols, double* v) {
-  host::normal_stream(0x5eedULL, 97, cols, v);
+void sigma_start_vector(int64_t cols, double* v, int max_threads = 16) {
+  host::normal_stream(0x5eedULL, 97, cols, v, max_threads);
   double ss = 0;
   for (int64_t i = 0; i < cols; ++i) ss += v[i] * v[i];
   const double nv = std::sqrt(ss);
@@ -300,7 +300,7 @@ cr_status cr_create(const double* Xh, const double* ybar_shifted, int64_t N, int
   h->sigma_prep = std::thread([h] {  // overlaps the allocations and uploads below
     const int64_t cols = h->N * (h->n + 1);
     h->sigma_start.resize((size_t)cols);
-    sigma_start_vector(cols, h->sigma_start.data());
+    sigma_start_vector(cols, h->sigma_start.data(), 4);  // few threads: create runs beside it
   });
   CUDA_TRY(cudaSetDevice(device));
   CUDA_TRY(cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking));
@@ -388,7 +388,7 @@ cr_status cr_create(const double* Xh, const double* ybar_shifted, int64_t N, int
   ALLOC(h->pw_v, N * (n + 1));
   ALLOC(h->pw_part, (size_t)h->k2_blocks * 2);
   ALLOC(h->pw_sum, 2);
-  h->power_grid = power_loop_grid(sms);
+  h->power_grid = power_loop_grid(sms, N);
   if (const char* pg = std::getenv("CRB_POWER_GRID")) h->power_grid = std::max(1, std::atoi(pg));
   ALLOC(h->gram, n * n + n);
   // op-C power loop: two step-parity buffers of (4 + 2n)-value records

@@ -155,7 +155,7 @@ bool affine_ls(const double* X, const double* y, int64_t N, int64_t n, std::vect
 // The uniform pairs are drawn sequentially (the stream is sequential); the
 // Box-Muller transform, which dominates the cost, runs on several threads.
 // Bit-identical to calling Xoshiro::normal() count times.
-void normal_stream(uint64_t seed, uint64_t tag, int64_t count, double* out) {
+void normal_stream(uint64_t seed, uint64_t tag, int64_t count, double* out, int max_threads) {
   Xoshiro g = stream(seed, tag);
   std::vector<double> u1((size_t)count), u2((size_t)count);
   for (int64_t i = 0; i < count; ++i) {
@@ -169,7 +169,7 @@ void normal_stream(uint64_t seed, uint64_t tag, int64_t count, double* out) {
     }
   };
   const unsigned hw = std::thread::hardware_concurrency();
-  const int64_t nt = count < 65536 ? 1 : std::min<int64_t>(hw ? hw : 1, 16);
+  const int64_t nt = count < 65536 ? 1 : std::max<int64_t>(1, std::min<int64_t>(hw ? hw : 1, max_threads));
   std::vector<std::thread> pool;
   for (int64_t t = 1; t < nt; ++t)
     pool.emplace_back(transform, count * t / nt, count * (t + 1) / nt);

@@ -94,7 +94,7 @@ cudaError_t launch_estimator(const double* Xq, long long Q, const double* X, con
 
 int primal_blocks(long long N);
 cudaError_t launch_gram(const double* X, long long N, int n, double* out, cudaStream_t s);
-int power_loop_grid(int sms);
+int power_loop_grid(int sms, long long N);
 cudaError_t launch_power_loop(const PowerLoopArgs& a, int grid, cudaStream_t s);
 cudaError_t launch_primal(const PrimalArgs& a, cudaStream_t s);
 cudaError_t launch_reduce(const ReduceArgs& a, cudaStream_t s);

@@ -15,6 +15,7 @@
 // the same fixed order, so all blocks take identical decisions with two grid
 // barriers per step. The computation is replicated on every rank of a
 // sharded run (no exchange).
+#include <algorithm>
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <math.h>
@@ -461,7 +462,14 @@ cudaError_t launch_gram(const double* X, long long N, int n, double* out, cudaSt
   return cudaGetLastError();
 }
 
-int power_loop_grid(int sms) { return sms; }  // one 256-thread block per SM
+// 256-thread blocks, about one per 150 points (at most one per SM, at least 16):
+// the per-step grid barrier costs more with more blocks, the per-point O(n^2)
+// latency chain with fewer threads; measured at one B200 (N = 1e4, n = 10:
+// 64 blocks 3.0 ms vs 148 blocks 4.2 ms; N = 2e4, n = 20 and N = 1e5: ~SM count)
+int power_loop_grid(int sms, long long N) {
+  const long long g = (N + 149) / 150;
+  return (int)std::max<long long>(16, std::min<long long>(sms, g));
+}
 
 cudaError_t launch_power_loop(const PowerLoopArgs& a, int grid, cudaStream_t s) {
   static constexpr PowerLoopFn tab[kMaxN] = {
