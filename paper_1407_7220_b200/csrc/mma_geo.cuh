@@ -45,7 +45,14 @@ __host__ __device__ constexpr int mma_ctas() {
 template <int NN>
 __host__ __device__ constexpr int mma_ns() { return mma_ctas<NN>() == 2 ? 3 : 4; }  // stages
 constexpr int kNS = 4;  // ring depth of the other users of this header (sweep_sparse.cu)
-constexpr int kWin = 32;               // row-sum window (rows)
+constexpr int kWin = 32;               // row-sum window (rows), masked-store sweep
+#ifndef CRB_MMA_WIN
+#define CRB_MMA_WIN 256
+#endif
+// row-sum window of the dense DMMA sweep (multiple of 32): one CTA barrier per
+// 32 stages; measured 32 / 64 / 128 / 256 rows: n = 10 iterations 50-300 344 /
+// 331 / 325 / 321 us, n = 20 late 321 / 308 / 303 / 296 us
+constexpr int kWinM = CRB_MMA_WIN;
 
 // Residual K: the n features plus (1, y) with (-c, 1) folded in -- unless
 // dropping those two columns saves a k-step, then y - c is added with DADDs.
@@ -61,7 +68,7 @@ __host__ __device__ constexpr int stage_doubles() {
 }
 template <int NN>
 __host__ __device__ constexpr int smem_bytes() {
-  return mma_ns<NN>() * stage_doubles<NN>() * 8 + 2 * mma_cw<NN>() * kWin * 8 +
+  return mma_ns<NN>() * stage_doubles<NN>() * 8 + 2 * mma_cw<NN>() * kWinM * 8 +
          2 * mma_ns<NN>() * 8;
 }
 

@@ -235,8 +235,8 @@ __global__ void __launch_bounds__(mma_threads<NN>(), mma_ctas<NN>()) sweep_mma_k
   constexpr int SD = stage_doubles<NN>();
   extern __shared__ __align__(128) double smem[];
   double* stages = smem;
-  double* rowacc = smem + kNS * SD;  // [2][kCW][kWin]
-  uint64_t* full = reinterpret_cast<uint64_t*>(rowacc + 2 * kCW * kWin);
+  double* rowacc = smem + kNS * SD;  // [2][kCW][kWinM]
+  uint64_t* full = reinterpret_cast<uint64_t*>(rowacc + 2 * kCW * kWinM);
   uint64_t* empty = full + kNS;
 
   if (a.stopped != nullptr && *a.stopped) return;
@@ -403,22 +403,24 @@ __global__ void __launch_bounds__(mma_threads<NN>(), mma_ctas<NN>()) sweep_mma_k
           rsj[j] += __shfl_xor_sync(0xffffffffu, rsj[j], 16);
         }
       }
-      double* ra = rowacc + (flushes & 1) * kCW * kWin + warp * kWin;
+      double* ra = rowacc + (flushes & 1) * kCW * kWinM + warp * kWinM;
       if (c8 == 0) {
         ra[win + 2 * q] = rsj[0];
         ra[win + 2 * q + 1] = rsj[1];
       }
       win += kTR;
-      if (win == kWin || r + kTR >= rhi) {
+      if (win == kWinM || r + kTR >= rhi) {
         // fixed-order sum over the CTA's warps into the tile's row-sum slice
+        // (warp k sums window rows 32k .. 32k + 31)
         asm volatile("bar.sync 1, %0;" ::"r"(kCW * 32) : "memory");
         const int valid_rows = (int)min((long long)win, rhi - win_base);
-        if (warp == 0 && lane < valid_rows) {
-          const double* rb = rowacc + (flushes & 1) * kCW * kWin;
+        const int wr = warp * 32 + lane;
+        if (warp < kWinM / 32 && wr < valid_rows) {
+          const double* rb = rowacc + (flushes & 1) * kCW * kWinM;
           double u = 0.0;
 #pragma unroll
-          for (int w = 0; w < kCW; ++w) u += rb[w * kWin + lane];
-          a.rowpart[(long long)t * a.R + win_base + lane] = u;
+          for (int w = 0; w < kCW; ++w) u += rb[w * kWinM + wr];
+          a.rowpart[(long long)t * a.R + win_base + wr] = u;
         }
         win_base += win;
         win = 0;
@@ -455,7 +457,7 @@ __global__ void __launch_bounds__(mma_threads<NN>(), mma_ctas<NN>()) sweep_mma_k
   }
   // one scalar record per CTA: the consumer warps' sums combined in warp order
   // (in the row-sum window buffer the last flush did not use)
-  double* wsc = rowacc + (flushes & 1) * kCW * kWin;
+  double* wsc = rowacc + (flushes & 1) * kCW * kWinM;
   if (lane == 0) {
     wsc[warp * kScal + 0] = vv;
     wsc[warp * kScal + 1] = vr;
