@@ -263,30 +263,53 @@ __global__ void __launch_bounds__(kBlock) reduce_primal_kernel(const FusedArgs f
       }
     }
     part[w][lane] = s;
-    // column aggregates: item e = (point, value) of the block's 32 x n1 entries
+    // column aggregates: item e = (point, value) of the block's 32 x n1 entries.
+    // The block's points lie in at most two column tiles: their (CTA, segment)
+    // slot offsets are computed once into shared memory (no per-item division)
     const long long per_tile = (long long)a.TC * n1;
+    constexpr int kMaxSlots = 32;
+    __shared__ long long slot_off[2][kMaxSlots];
+    __shared__ int nslot[2];
+    const long long tA = l0 / a.TC;
+    if (threadIdx.x < 2 * kMaxSlots) {
+      const int which = threadIdx.x / kMaxSlots, k = threadIdx.x % kMaxSlots;
+      const long long t = tA + which;
+      const long long g_lo = (t * a.R) / a.U;
+      long long g_hi = ((t + 1) * a.R - 1) / a.U;
+      if (g_hi > a.G - 1) g_hi = a.G - 1;
+      const long long g = g_lo + k;
+      if (k == 0) nslot[which] = (int)(g_hi - g_lo + 1);
+      if (g <= g_hi) slot_off[which][k] = (g * a.maxspan + (t - (g * a.U) / a.R)) * per_tile;
+    }
+    __syncthreads();
     for (int e = threadIdx.x; e < kFPts * n1; e += kBlock) {
       const long long l = l0 + e / n1;
       if (l >= N) continue;
       const int j = e % n1;
       const long long t = l / a.TC;
+      const int which = (int)(t - tA);
       const long long off = (l - t * a.TC) * n1 + j;  // within the tile's slot array
-      const long long g_lo = (t * a.R) / a.U;
-      long long g_hi = ((t + 1) * a.R - 1) / a.U;
-      if (g_hi > a.G - 1) g_hi = a.G - 1;
+      const int ns = nslot[which];
       double sum = 0.0;
-      for (long long g0 = g_lo; g0 <= g_hi; g0 += 4) {
+      for (int k0 = 0; k0 < ns; k0 += 4) {
         double v[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          const long long g = g0 + u;
-          v[u] = g <= g_hi
-                     ? __ldcg(a.colpart + (g * a.maxspan + (t - (g * a.U) / a.R)) * per_tile + off)
-                     : 0.0;
+          const int k = k0 + u;
+          long long so = 0;
+          if (k < ns) {
+            if (k < kMaxSlots) {
+              so = slot_off[which][k];
+            } else {  // more CTAs on this tile than cached slots (small N, many CTAs)
+              const long long g = (t * a.R) / a.U + k;
+              so = (g * a.maxspan + (t - (g * a.U) / a.R)) * per_tile;
+            }
+          }
+          v[u] = k < ns ? __ldcg(a.colpart + so + off) : 0.0;
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u)
-          if (g0 + u <= g_hi) sum += v[u];
+          if (k0 + u < ns) sum += v[u];
       }
       a.agg_out[N + l * n1 + j] = sum;
     }
