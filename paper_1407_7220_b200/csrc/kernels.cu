@@ -22,16 +22,29 @@ namespace {
 //     point is issued up front.
 template <int NN>
 __global__ void __launch_bounds__(kPBlock) primal_kernel(const PrimalArgs a) {
-  if (a.stopped != nullptr && *a.stopped) return;
-  if (a.fuse_ctrl != nullptr) {  // fused path: the last fused launch already ran it
-    if (__ldcg(&a.fuse_ctrl->primal_done)) return;
-    if (blockIdx.x == 0 && threadIdx.x == 0) a.fuse_ctrl->k2_count = (int)gridDim.x;
-  }
   const long long N = a.N;
+  // the halt flag, coefficients and slot index are independent loads: issue them
+  // together (one L2 round trip before the point loads, not two), and start
+  // pulling the block's first points' aggregate rows into L1 meanwhile
+  {
+    const long long l = (long long)blockIdx.x * kPBlock + threadIdx.x;
+    if (l < N) {
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(a.aggc + N + l * (NN + 1)));
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(a.aggp + N + l * (NN + 1)));
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(a.X + l * NN));
+    }
+  }
+  const int stop = a.stopped != nullptr ? *a.stopped : 0;
+  const int done = a.fuse_ctrl != nullptr ? __ldcg(&a.fuse_ctrl->primal_done) : 0;
   const double s_c = a.coef[0];
   const double s_p = a.mode == 0 ? a.coef[1] : 0.0;
   const double beta = a.mode == 0 ? a.coef[2] : 0.0;
   const int cur = *a.cur;
+  if (stop) return;
+  if (a.fuse_ctrl != nullptr) {  // fused path: the last fused launch already ran it
+    if (done) return;
+    if (blockIdx.x == 0 && threadIdx.x == 0) a.fuse_ctrl->k2_count = (int)gridDim.x;
+  }
   const double* vposc = cur ? a.vpos1 : a.vpos0;
   double* vposp = cur ? a.vpos0 : a.vpos1;
   double acc[kK2Scal];
