@@ -60,8 +60,11 @@ __device__ __forceinline__ int rows_transpose_sum(double (&t)[U], int lane, doub
   return row;
 }
 
+#ifndef CRB_SMALL_MINB
+#define CRB_SMALL_MINB 1
+#endif
 template <int NN>
-__global__ void __launch_bounds__(kSBlock) small_loop_kernel(const SmallArgs a) {
+__global__ void __launch_bounds__(kSBlock, CRB_SMALL_MINB) small_loop_kernel(const SmallArgs a) {
   constexpr int RP = rec_pitch(NN);
   cg::grid_group grid = cg::this_grid();
   const long long tid = (long long)blockIdx.x * kSBlock + threadIdx.x;
@@ -128,7 +131,10 @@ __global__ void __launch_bounds__(kSBlock) small_loop_kernel(const SmallArgs a) 
         for (int j = 0; j <= NN; ++j) acc[j] = 0.0;
         double vv = 0.0, vr = 0.0, tr = 0.0, nn = 0.0;
         // U rows in flight: all loads of a batch are issued before its math
-        constexpr int U = NN <= 5 ? 8 : ((NN + 3) <= 8 ? 4 : ((NN + 3) <= 16 ? 2 : 1));
+#ifndef CRB_SMALL_U5
+#define CRB_SMALL_U5 8
+#endif
+        constexpr int U = NN <= 5 ? CRB_SMALL_U5 : ((NN + 3) <= 8 ? 4 : ((NN + 3) <= 16 ? 2 : 1));
         for (long long r0 = rlo; r0 < rhi; r0 += U) {
           double xb[U][NN], yb[U], cb[U], pb[U];
 #pragma unroll
