@@ -282,6 +282,9 @@ def run_ours(args):
         "model_24B_per_pair_frac": (BYTES_PER_PAIR * rows * N / sweep_avg / 1e9 /
                                     peaks["hbm_gbs"]) if sweep_avg else None,
         "sweep_share_of_step": (sweep_s / dev_s) if dev_s > 0 else None,
+        "sweep_timing": "CUDA events on the solver stream around every 8th sweep launch of "
+                        "the timed region (uniform sample; the library's default, "
+                        "CRB_SWEEP_EVENTS=1 brackets every launch at ~2 % step cost)",
         # secondary: fp64 flop per pair ~ 4n + 17
         "fp64_tflops": ((4 * n + 17) * rows * N / sweep_avg / 1e12) if sweep_avg else None,
         "note": "SURVEY 8(d) models 24 B per pair (read theta1, theta1_prev, write "

@@ -909,6 +909,12 @@ cr_status cr_papg_iterate(cr_handle* h, int64_t max_steps, int64_t* done, int32_
     return CR_OK;
   }
   const bool timed_sweeps = h->graph_iters == 0;
+  // Sweep timing: an event pair around every 8th sweep (CRB_SWEEP_EVENTS=k: every
+  // k-th, 0: none); the reported sweep seconds are the sampled mean times the
+  // iterations run. Event records between the kernels cost ~6 us per iteration
+  // (2 % at cfg 2, measured), so not every sweep is bracketed.
+  int every = 8;
+  if (const char* ev = std::getenv("CRB_SWEEP_EVENTS")) every = std::max(0, std::atoi(ev));
   const int per_unit = h->graph_iters > 0 ? h->graph_iters : 4;
   h->primal_pending = true;  // direct launches: the call starts with the (maybe no-op) primal
   int64_t extra_launches = (h->graph_iters == 0 && fused_path(h)) ? 1 : 0;
@@ -924,7 +930,8 @@ cr_status cr_papg_iterate(cr_handle* h, int64_t max_steps, int64_t* done, int32_
     } else {
       for (int i = 0; i < per_unit && enq_iters + i < max_steps; ++i) {
         cudaEvent_t a = nullptr, b = nullptr;
-        if (timed_sweeps && timed_pairs < (1 << 16)) {  // event pairs created on demand
+        const bool sample = every > 0 && ((enq_iters + i) % every) == 0;
+        if (timed_sweeps && sample && timed_pairs < (1 << 16)) {  // event pairs created on demand
           while (h->ev_sweep.size() < (size_t)(2 * timed_pairs + 2)) {
             cudaEvent_t e;
             CUDA_TRY(cudaEventCreate(&e));
@@ -966,7 +973,11 @@ cr_status cr_papg_iterate(cr_handle* h, int64_t max_steps, int64_t* done, int32_
     CUDA_TRY(cudaEventElapsedTime(&m, h->ev_sweep[2 * i], h->ev_sweep[2 * i + 1]));
     sw += m * 1e-3;
   }
-  h->last_sweep_seconds = sw;
+  {
+    const int64_t ran = std::min<int64_t>(enq_iters, max_steps);
+    h->last_sweep_seconds =
+        (timed_pairs > 0 && every > 1) ? sw * (double)ran / (double)timed_pairs : sw;
+  }
   h->last_launches = (h->graph_iters > 0 ? units * h->graph_iters
                                          : std::min<int64_t>(enq_iters, max_steps)) *
                          launches_per_iteration(h) +
