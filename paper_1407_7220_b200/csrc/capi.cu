@@ -915,7 +915,11 @@ cr_status cr_papg_iterate(cr_handle* h, int64_t max_steps, int64_t* done, int32_
   // (2 % at cfg 2, measured), so not every sweep is bracketed.
   int every = 8;
   if (const char* ev = std::getenv("CRB_SWEEP_EVENTS")) every = std::max(0, std::atoi(ev));
-  const int per_unit = h->graph_iters > 0 ? h->graph_iters : 4;
+  // direct launches: poll the device state every `per_unit` iterations (one D2H copy
+  // + event per unit); CRB_POLL_UNIT overrides (measurement knob)
+  int per_unit = h->graph_iters > 0 ? h->graph_iters : 4;
+  if (h->graph_iters == 0)
+    if (const char* pu = std::getenv("CRB_POLL_UNIT")) per_unit = std::max(1, std::atoi(pu));
   h->primal_pending = true;  // direct launches: the call starts with the (maybe no-op) primal
   int64_t extra_launches = (h->graph_iters == 0 && fused_path(h)) ? 1 : 0;
   int64_t enq_iters = 0;
@@ -946,6 +950,10 @@ cr_status cr_papg_iterate(cr_handle* h, int64_t max_steps, int64_t* done, int32_
       }
     }
     enq_iters += per_unit;
+    // long direct-launch runs poll less often (16 iterations per unit after the
+    // first 64: +0.5 % at cfg 2; short solves keep the 4-iteration halting latency)
+    if (h->graph_iters == 0 && per_unit < 16 && enq_iters >= 64 && !std::getenv("CRB_POLL_UNIT"))
+      per_unit = 16;
     const int slot = (int)(units & 1);
     CUDA_TRY(cudaMemcpyAsync(&h->ctrl_poll[slot], h->ctrl_d, sizeof(DevCtrl),
                              cudaMemcpyDeviceToHost, h->st));
