@@ -72,6 +72,9 @@ typedef struct {
   int32_t workers;          /* K-block partition: concurrent block solves; <= 0: 16 */
 } cr_papg_config;
 
+/* device history capacity (snapshots) of one solve */
+#define CR_HISTORY_CAP 4000000
+
 /* one MetricsSnapshot (metrics.hpp:13-22) */
 typedef struct {
   double iter, objective, reg_objective, infeas_raw, infeas_norm, gap_raw, gap_norm, wall_time_s;
@@ -85,7 +88,8 @@ typedef struct {
   int32_t saturated;
   int32_t sigma_iters;
   int32_t sigma_converged;
-  int32_t pad_;
+  int32_t history_truncated; /* 1: more than CR_HISTORY_CAP iterations ran; the
+                                history holds the first CR_HISTORY_CAP snapshots */
   double g_final;
   double delta_estimate;
   double sigma_C;
@@ -154,6 +158,12 @@ cr_status cr_get_theta(cr_handle *h, double *out);
 /* C eta of the last loop iteration (the residual rows at eta(theta2)), same
    layout as cr_get_theta. */
 cr_status cr_get_rows(cr_handle *h, double *out);
+/* The same two exports for global pair rows l1 in [row_begin, row_end) of
+   this shard only ((row_end - row_begin) x (N-1) cross entries, canonical
+   order, then the N pos rows): spot checks at sizes whose full dual vector
+   does not fit the host (BASELINE cfg 5: 80 GB). Singleton blocks only. */
+cr_status cr_get_theta_rows(cr_handle *h, int64_t row_begin, int64_t row_end, double *out);
+cr_status cr_get_rows_window(cr_handle *h, int64_t row_begin, int64_t row_end, double *out);
 /* device timing of the last cr_papg_iterate call and the number of kernel
    launches it issued (for bench.py) */
 cr_status cr_last_timing(const cr_handle *h, double *seconds, int64_t *launches,

@@ -225,7 +225,8 @@ inline PapgResult solve(const PreparedProblem& prep, const PapgConfig& cfg,
   PapgResult out;
   out.point.y.resize(static_cast<size_t>(N));
   out.point.xi.resize(static_cast<size_t>(N * n));
-  std::vector<cr_snapshot> hist(cfg.record_history ? static_cast<size_t>(cfg.max_iters) : 0);
+  std::vector<cr_snapshot> hist(
+      cfg.record_history ? static_cast<size_t>(std::min<Index>(cfg.max_iters, CR_HISTORY_CAP)) : 0);
   cr_papg_result r{};
   check(cr_papg_solve(hd.h, &c, theta0 ? theta0->data() : nullptr, &r, out.point.y.data(),
                       out.point.xi.data(), hist.empty() ? nullptr : hist.data()),

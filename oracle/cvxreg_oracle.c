@@ -619,10 +619,21 @@ typedef struct {
 
 /* papg.cpp:89-132 with the singleton closed-form block minimiser
    (alcc.cpp:233-235 centres; block objective alcc.cpp:254-256). */
+static double block_minimisers(dg_ctx *c);
 static double dual_gradient(dg_ctx *c, const double *theta, double *C_eta) {
   const int64_t N = c->N, n = c->n;
   if (c->threads > 1) apply_C_T_omp(c->X, N, n, theta, c->q_y, c->q_xi, c->threads);
   else cro_apply_C_T(c->X, N, n, theta, c->q_y, c->q_xi);
+  const double g = block_minimisers(c);
+  if (c->threads > 1) apply_C_omp(c->X, N, n, c->ey, c->exi, C_eta, c->threads);
+  else cro_apply_C(c->X, N, n, c->ey, c->exi, C_eta);
+  return g;
+}
+
+/* papg.cpp:107-129: K = N singleton block minimisers from q = C^T theta
+   (alcc.cpp:233-235 centres, alcc.cpp:254-256 objective), gathered in block order */
+static double block_minimisers(dg_ctx *c) {
+  const int64_t N = c->N, n = c->n;
   double g = 0;
   for (int64_t i = 0; i < N; ++i) { /* block i = {i}; gathered in block order (:124-128) */
     const double y = c->ys[i] + c->q_y[i];
@@ -638,8 +649,6 @@ static double dual_gradient(dg_ctx *c, const double *theta, double *C_eta) {
     const double obj = 0.5 * (dy * dy) + 0.5 * c->gamma * xx - c->q_y[i] * y - qx;
     g += obj;
   }
-  if (c->threads > 1) apply_C_omp(c->X, N, n, c->ey, c->exi, C_eta, c->threads);
-  else cro_apply_C(c->X, N, n, c->ey, c->exi, C_eta);
   return g;
 }
 
@@ -818,6 +827,379 @@ int cro_papg(const double *X, const double *ys, int64_t N, int64_t n, const cro_
   }
   res->wall_seconds = now_seconds() - start;
   free(theta1); free(theta1_prev); free(theta2); free(C_eta);
+  free(c.q_y); free(c.q_xi); free(c.ey); free(c.exi);
+  return rc;
+}
+
+/* ============================================ memory-light replay (cfg 4/5) */
+/* The same loop as cro_papg (papg.cpp:136-283) without any N^2 array: the
+   per-iteration primal eta_k = (y_k, xi_k) (N(n+1) doubles) and the scalars
+   of each step (ball scale, momentum beta, restart) are kept, and every pass
+   recomputes each pair's multiplier history theta1/theta1_prev/theta2 from
+   them with exactly the literal loop's element operations (papg.cpp:188-189,
+   projections.hpp:10-12, papg.cpp:244-250, :256-262). Sums run in the literal
+   loop's order per thread (one thread: bitwise equal to cro_papg with one
+   thread; several: per-thread partials over contiguous l1 ranges combined in
+   thread order, as apply_C_T_omp). Two passes per iteration: (A) the new v
+   and the sums that fix the ball scale and the metrics; (B) theta1 with its
+   scale, the gap, |theta1| and the adjoints C^T theta1 and C^T theta2_next
+   (operators.cpp:155-180) for the next dual gradient. O(k^2 N^2 n) work for k
+   iterations and O(k N n) memory. */
+enum { RP_MOM = 0, RP_COPY = 1, RP_RESTART = 2 };
+
+typedef struct {
+  const double *X;
+  int64_t N, n;
+  double L;
+  double **ey, **exi;  /* [1..k] */
+  double *scale;       /* [1..k] ball scale (1.0: not scaled) */
+  int *kind;           /* [1..k] transition to theta2 of the next iteration */
+  double *beta;        /* [1..k] */
+} rp_hist;
+
+static inline double rp_resid(const double *X, int64_t n, const double *ey, const double *exi,
+                              int64_t l1, int64_t l2) { /* operators.cpp:143-147 */
+  double acc = ey[l1] - ey[l2];
+  const double *xi2 = exi + l2 * n, *x1 = X + l1 * n, *x2 = X + l2 * n;
+  for (int64_t j = 0; j < n; ++j) acc -= xi2[j] * (x1[j] - x2[j]);
+  return acc;
+}
+
+/* iterations 1..m of one cross pair: theta1, theta1_prev after step m and the
+   theta2 that iteration m+1 starts from */
+static inline void rp_replay(const rp_hist *h, int64_t m, int64_t l1, int64_t l2, double *th1,
+                             double *th1p, double *th2) {
+  double a = 0.0, p = 0.0, b = 0.0;
+  for (int64_t it = 1; it <= m; ++it) {
+    const double row = rp_resid(h->X, h->n, h->ey[it], h->exi[it], l1, l2);
+    double u = b - row / h->L;
+    u = u > 0.0 ? u : 0.0;
+    p = a;
+    a = h->scale[it] != 1.0 ? u * h->scale[it] : u;
+    if (h->kind[it] == RP_MOM) b = a + h->beta[it] * (a - p);
+    else if (h->kind[it] == RP_RESTART) { b = a; p = a; }
+    else b = a;
+  }
+  *th1 = a; *th1p = p; *th2 = b;
+}
+
+static int rp_grow(rp_hist *h, int64_t k, int64_t *cap) {
+  if (k < *cap) return 0;
+  int64_t nc = *cap * 2 + 8;
+  double **ey = (double **)realloc(h->ey, sizeof(double *) * (size_t)nc);
+  if (ey) h->ey = ey;
+  double **exi = (double **)realloc(h->exi, sizeof(double *) * (size_t)nc);
+  if (exi) h->exi = exi;
+  double *sc = (double *)realloc(h->scale, sizeof(double) * (size_t)nc);
+  if (sc) h->scale = sc;
+  int *kd = (int *)realloc(h->kind, sizeof(int) * (size_t)nc);
+  if (kd) h->kind = kd;
+  double *be = (double *)realloc(h->beta, sizeof(double) * (size_t)nc);
+  if (be) h->beta = be;
+  if (!ey || !exi || !sc || !kd || !be) return -1;
+  for (int64_t i = *cap; i < nc; ++i) { h->ey[i] = NULL; h->exi[i] = NULL; }
+  *cap = nc;
+  return 0;
+}
+
+int cro_papg_replay(const double *X, const double *ys, int64_t N, int64_t n,
+                    const cro_config *cfg, const int64_t *rows, int64_t nrows,
+                    double *theta_rows, double *c_eta_rows, cro_result *res) {
+  const double start = now_seconds();
+  if (N < 2 || n < 1 || cfg->gamma <= 0 || nrows < 0 || (nrows > 0 && !rows)) return -1;
+  for (int64_t i = 0; i < nrows; ++i)
+    if (rows[i] < 0 || rows[i] >= N || (i > 0 && rows[i] <= rows[i - 1])) return -1;
+  const int T = cfg->threads > 1 ? cfg->threads : 1;
+  const int64_t rows_total = N * (N - 1);
+  const double infeas_div = sqrt((double)rows_total);
+  const double gap_div = (double)rows_total;
+  double sigma_C = cfg->sigma_C;
+  res->sigma_iters = 0;
+  res->sigma_converged = 1;
+  if (!(sigma_C > 0)) {
+    int it = 0, conv = 0;
+    if (cro_sigma_C(X, N, n, 1e-6, 5000, &sigma_C, &it, &conv)) return -2;
+    res->sigma_iters = it;
+    res->sigma_converged = conv;
+  }
+  const double L_g = sigma_C * sigma_C / cfg->gamma;
+  double B_theta = cfg->B_theta > 0 ? cfg->B_theta : 10.0 * sqrt((double)N);
+  res->sigma_C = sigma_C;
+  res->L_g = L_g;
+  res->reason = CRO_ITER_BUDGET;
+
+  const int64_t w = N * (n + 1);
+  rp_hist h = {X, N, n, L_g, NULL, NULL, NULL, NULL, NULL};
+  int64_t cap = 0;
+  double *th1_pos = (double *)calloc((size_t)N, sizeof(double));
+  double *th1p_pos = (double *)calloc((size_t)N, sizeof(double));
+  double *th2_pos = (double *)calloc((size_t)N, sizeof(double));
+  double *n1_pos = (double *)malloc(sizeof(double) * (size_t)N);  /* theta1_pos of step k */
+  double *cand_pos = (double *)malloc(sizeof(double) * (size_t)N);
+  double *part = (double *)malloc(sizeof(double) * (size_t)(2 * w * T)); /* [T][th1 | cand] */
+  double *scal = (double *)malloc(sizeof(double) * (size_t)(8 * T));
+  double *q_th1 = (double *)malloc(sizeof(double) * (size_t)w);
+  int64_t *slot = (int64_t *)malloc(sizeof(int64_t) * (size_t)N); /* output row of l1 or -1 */
+  if (slot) {
+    for (int64_t l = 0; l < N; ++l) slot[l] = -1;
+    for (int64_t i = 0; i < nrows; ++i) slot[rows[i]] = i;
+  }
+  dg_ctx c = {X, ys, N, n, cfg->gamma, T,
+              (double *)calloc((size_t)N, sizeof(double)),
+              (double *)calloc((size_t)(N * n), sizeof(double)),
+              (double *)malloc(sizeof(double) * (size_t)N),
+              (double *)malloc(sizeof(double) * (size_t)(N * n))};
+  int rc = 0;
+  if (!th1_pos || !th1p_pos || !th2_pos || !n1_pos || !cand_pos || !part || !scal || !q_th1 || !slot ||
+      !c.q_y || !c.q_xi || !c.ey || !c.exi) { rc = -3; goto done; }
+  {
+    double t = 1.0;
+    double g_star_upper = INFINITY;
+    int64_t ell = 0;
+    int restarts = 0;
+    while (1) {
+      ++ell;
+      if (rp_grow(&h, ell, &cap)) { rc = -3; break; }
+      const double inv3 = 1.0 / ((double)ell * (double)ell * (double)ell);
+      const double inner_tol = cfg->inner_tol_floor < inv3 ? cfg->inner_tol_floor : inv3;
+      const double g_value = block_minimisers(&c); /* eta of theta2 (q from the last pass B) */
+      h.ey[ell] = (double *)malloc(sizeof(double) * (size_t)N);
+      h.exi[ell] = (double *)malloc(sizeof(double) * (size_t)(N * n));
+      if (!h.ey[ell] || !h.exi[ell]) { rc = -3; break; }
+      memcpy(h.ey[ell], c.ey, sizeof(double) * (size_t)N);
+      memcpy(h.exi[ell], c.exi, sizeof(double) * (size_t)(N * n));
+      h.scale[ell] = 1.0;
+      h.kind[ell] = RP_COPY;
+      h.beta[ell] = 0.0;
+
+      /* pass A: v_k = max(theta2 - C eta / L, 0) and the sums of :188-199 */
+      int finite = 1;
+#pragma omp parallel num_threads(T)
+      {
+        int tid = 0, nt = 1;
+#ifdef _OPENMP
+        tid = omp_get_thread_num();
+        nt = omp_get_num_threads();
+#endif
+        double ss = 0, csq = 0, t2c = 0;
+        int fin = 1;
+        const int64_t lo = N * tid / nt, hi = N * (tid + 1) / nt;
+        for (int64_t l1 = lo; l1 < hi; ++l1) {
+          for (int64_t l2 = 0; l2 < N; ++l2) {
+            if (l1 == l2) continue;
+            double a, p, b;
+            rp_replay(&h, ell - 1, l1, l2, &a, &p, &b);
+            const double row = rp_resid(X, n, h.ey[ell], h.exi[ell], l1, l2);
+            if (!isfinite(row)) fin = 0;
+            double u = b - row / L_g;
+            u = u > 0.0 ? u : 0.0;
+            ss += u * u;
+            const double m = -row > 0.0 ? -row : 0.0;
+            csq += m * m;
+            t2c += b * row;
+          }
+        }
+        scal[tid * 8 + 0] = ss;
+        scal[tid * 8 + 1] = csq;
+        scal[tid * 8 + 2] = t2c;
+        scal[tid * 8 + 3] = fin;
+      }
+      double ss = 0, cross_sq = 0, t2c = 0;
+      for (int tt = 0; tt < T; ++tt) {
+        ss += scal[tt * 8 + 0];
+        cross_sq += scal[tt * 8 + 1];
+        t2c += scal[tt * 8 + 2];
+        if (scal[tt * 8 + 3] == 0) finite = 0;
+      }
+      double all_sq = cross_sq;
+      for (int64_t l = 0; l < N; ++l) { /* the y >= 0 rows, C eta = y (operators.cpp:152) */
+        const double row = c.ey[l];
+        if (!isfinite(row)) finite = 0;
+        double u = th2_pos[l] - row / L_g;
+        u = u > 0.0 ? u : 0.0;
+        ss += u * u;
+        const double m = -row > 0.0 ? -row : 0.0;
+        all_sq += m * m;
+        t2c += th2_pos[l] * row;
+      }
+      if (!finite) { res->reason = CRO_ERROR; rc = -4; break; }
+      const double norm = sqrt(ss);
+      if (norm > B_theta) h.scale[ell] = B_theta / norm; /* projections.hpp:11-12 */
+      const double cross_infeas = sqrt(cross_sq);
+      const double fw = B_theta * sqrt(all_sq) + t2c;
+      const double cushion = 2.0 * inner_tol * (double)N;
+      const double cand = g_value + fw + cushion;
+      if (cand < g_star_upper) g_star_upper = cand;
+      const double t_next = cro_momentum_next(t);
+      const double beta = cfg->use_momentum ? (t - 1.0) / t_next : 0.0;
+
+      /* pass B: theta1 = s v, gap, |theta1|, C^T theta1, C^T theta2_next */
+      for (int64_t l = 0; l < N; ++l) {
+        double u = th2_pos[l] - c.ey[l] / L_g;
+        u = u > 0.0 ? u : 0.0;
+        n1_pos[l] = h.scale[ell] != 1.0 ? u * h.scale[ell] : u;
+        cand_pos[l] = n1_pos[l] + beta * (n1_pos[l] - th1_pos[l]);
+      }
+#pragma omp parallel num_threads(T)
+      {
+        int tid = 0, nt = 1;
+#ifdef _OPENMP
+        tid = omp_get_thread_num();
+        nt = omp_get_num_threads();
+#endif
+        double *p1 = part + (int64_t)tid * 2 * w, *p2 = p1 + w;
+        if (nt == 1) { /* literal single-thread apply_C_T: starts from theta_pos */
+          memcpy(p1, n1_pos, sizeof(double) * (size_t)N);
+          memcpy(p2, cand_pos, sizeof(double) * (size_t)N);
+          memset(p1 + N, 0, sizeof(double) * (size_t)(N * n));
+          memset(p2 + N, 0, sizeof(double) * (size_t)(N * n));
+        } else {
+          memset(p1, 0, sizeof(double) * (size_t)(2 * w));
+        }
+        double gap = 0, nn1 = 0;
+        const int64_t lo = N * tid / nt, hi = N * (tid + 1) / nt;
+        for (int64_t l1 = lo; l1 < hi; ++l1) {
+          const double *x1 = X + l1 * n;
+          const int out_row = slot[l1] >= 0;
+          int64_t r = slot[l1] * (N - 1);
+          for (int64_t l2 = 0; l2 < N; ++l2) {
+            if (l1 == l2) continue;
+            double a, p, b;
+            rp_replay(&h, ell - 1, l1, l2, &a, &p, &b);
+            const double row = rp_resid(X, n, h.ey[ell], h.exi[ell], l1, l2);
+            double u = b - row / L_g;
+            u = u > 0.0 ? u : 0.0;
+            p = a;
+            a = h.scale[ell] != 1.0 ? u * h.scale[ell] : u;
+            gap += a * row;
+            nn1 += a * a;
+            if (out_row) {
+              if (theta_rows) theta_rows[r] = a;
+              if (c_eta_rows) c_eta_rows[r] = row;
+              ++r;
+            }
+            const double bn = a + beta * (a - p);
+            const double *x2 = X + l2 * n;
+            p1[l1] += a;
+            p1[l2] -= a;
+            p2[l1] += bn;
+            p2[l2] -= bn;
+            double *o1 = p1 + N + l2 * n, *o2 = p2 + N + l2 * n;
+            for (int64_t j = 0; j < n; ++j) {
+              const double dx = x1[j] - x2[j];
+              o1[j] -= a * dx;
+              o2[j] -= bn * dx;
+            }
+          }
+        }
+        scal[tid * 8 + 4] = gap;
+        scal[tid * 8 + 5] = nn1;
+      }
+      double gap_m = 0, nsq = 0;
+      for (int tt = 0; tt < T; ++tt) { gap_m += scal[tt * 8 + 4]; nsq += scal[tt * 8 + 5]; }
+      for (int64_t l = 0; l < N; ++l) {
+        gap_m += n1_pos[l] * c.ey[l];
+        nsq += n1_pos[l] * n1_pos[l];
+      }
+      /* combine the adjoints (apply_C_T_omp order) */
+      if (T == 1) {
+        memcpy(q_th1, part, sizeof(double) * (size_t)w);
+        memcpy(c.q_y, part + w, sizeof(double) * (size_t)N);
+        memcpy(c.q_xi, part + w + N, sizeof(double) * (size_t)(N * n));
+      } else {
+#pragma omp parallel for schedule(static) num_threads(T)
+        for (int64_t k = 0; k < w; ++k) {
+          double s1 = k < N ? n1_pos[k] : 0.0, s2 = k < N ? cand_pos[k] : 0.0;
+          for (int tt = 0; tt < T; ++tt) {
+            s1 += part[(int64_t)tt * 2 * w + k];
+            s2 += part[(int64_t)tt * 2 * w + w + k];
+          }
+          q_th1[k] = s1;
+          if (k < N) c.q_y[k] = s2; else c.q_xi[k - N] = s2;
+        }
+      }
+      for (int64_t l = 0; l < N; ++l) { th1p_pos[l] = th1_pos[l]; th1_pos[l] = n1_pos[l]; }
+
+      const double gap_raw = cfg->use_momentum ? gap_m : t2c; /* :201-208 */
+      const double infeas_raw = sqrt(cross_infeas * cross_infeas);
+      const double gap_norm = gap_raw / gap_div;
+      const double infeas_norm = infeas_raw / infeas_div;
+      if (cfg->record_history && res->history) {
+        double obj = 0, xx = 0;
+        for (int64_t i = 0; i < N; ++i) { const double d = c.ey[i] - ys[i]; obj += d * d; }
+        for (int64_t i = 0; i < N * n; ++i) xx += c.exi[i] * c.exi[i];
+        double *hh = res->history + (ell - 1) * 8;
+        hh[0] = (double)ell;
+        hh[1] = 0.5 * obj;
+        hh[2] = 0.5 * obj + 0.5 * cfg->gamma * xx;
+        hh[3] = infeas_raw;
+        hh[4] = infeas_norm;
+        hh[5] = gap_raw;
+        hh[6] = gap_norm;
+        hh[7] = now_seconds() - start;
+      }
+      res->iters = ell;
+      int stop = 0; /* :225-236 */
+      if (fabs(gap_norm) <= cfg->gap_norm_tol && infeas_norm <= cfg->infeas_norm_tol) {
+        res->reason = CRO_THRESHOLDS;
+        stop = 1;
+      } else if (ell >= cfg->max_iters) {
+        res->reason = CRO_ITER_BUDGET;
+        stop = 1;
+      } else if (now_seconds() - start > cfg->max_seconds) {
+        res->reason = CRO_TIME_BUDGET;
+        stop = 1;
+      }
+      if (stop) { /* :238-254 */
+        const int saturated = sqrt(nsq) > 0.99 * B_theta;
+        if (saturated && cfg->adaptive_B_theta && res->reason == CRO_THRESHOLDS &&
+            restarts < cfg->max_restarts) {
+          B_theta *= 2.0;
+          ++restarts;
+          h.kind[ell] = RP_RESTART;
+          for (int64_t l = 0; l < N; ++l) { th2_pos[l] = th1_pos[l]; th1p_pos[l] = th1_pos[l]; }
+          memcpy(c.q_y, q_th1, sizeof(double) * (size_t)N);
+          memcpy(c.q_xi, q_th1 + N, sizeof(double) * (size_t)(N * n));
+          t = 1.0;
+          g_star_upper = INFINITY;
+          continue;
+        }
+        res->saturated = saturated;
+        /* :265-277 final re-solve at theta1 */
+        memcpy(c.q_y, q_th1, sizeof(double) * (size_t)N);
+        memcpy(c.q_xi, q_th1 + N, sizeof(double) * (size_t)(N * n));
+        double ft = 1.0 / pow((double)ell, 3.0);
+        if (cfg->inner_tol_floor < ft) ft = cfg->inner_tol_floor;
+        if (cfg->final_resolve_tol < ft) ft = cfg->final_resolve_tol;
+        const double g_final = block_minimisers(&c);
+        res->g_final = g_final;
+        const double d = g_star_upper - (g_final - 2.0 * ft * (double)N);
+        res->delta_estimate = d > 0 ? d : 0.0;
+        if (res->y) memcpy(res->y, c.ey, sizeof(double) * (size_t)N);
+        if (res->xi) memcpy(res->xi, c.exi, sizeof(double) * (size_t)(N * n));
+        if (theta_rows) memcpy(theta_rows + nrows * (N - 1), th1_pos, sizeof(double) * (size_t)N);
+        if (c_eta_rows) memcpy(c_eta_rows + nrows * (N - 1), h.ey[ell], sizeof(double) * (size_t)N);
+        res->B_theta = B_theta;
+        res->restarts = restarts;
+        break;
+      }
+      if (cfg->use_momentum) { /* :256-262; q already holds C^T theta2_next */
+        h.kind[ell] = RP_MOM;
+        h.beta[ell] = beta;
+        for (int64_t l = 0; l < N; ++l) th2_pos[l] = cand_pos[l];
+        t = t_next;
+      } else {
+        h.kind[ell] = RP_COPY;
+        for (int64_t l = 0; l < N; ++l) th2_pos[l] = th1_pos[l];
+      }
+    }
+  }
+done:
+  res->wall_seconds = now_seconds() - start;
+  for (int64_t i = 0; i < cap; ++i) { free(h.ey ? h.ey[i] : NULL); free(h.exi ? h.exi[i] : NULL); }
+  free(h.ey); free(h.exi); free(h.scale); free(h.kind); free(h.beta);
+  free(th1_pos); free(th1p_pos); free(th2_pos); free(n1_pos); free(cand_pos); free(part);
+  free(scal); free(q_th1); free(slot);
   free(c.q_y); free(c.q_xi); free(c.ey); free(c.exi);
   return rc;
 }

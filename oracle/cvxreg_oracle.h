@@ -106,6 +106,19 @@ int cro_sigma_C(const double *X, int64_t N, int64_t n, double tol, int max_iters
 int cro_papg(const double *X, const double *ys_shifted, int64_t N, int64_t n,
              const cro_config *cfg, const double *theta0, cro_result *res);
 
+/* Memory-light restatement of cro_papg (zero start): keeps only the
+   per-iteration primal and step scalars and recomputes every pair's
+   multiplier history on each pass (O(k^2 N^2 n) work, O(k N n) memory), for
+   sizes whose N^2 arrays do not fit the host (BASELINE cfg 4, 5). One thread:
+   bitwise equal to cro_papg with one thread. theta_rows / c_eta_rows (may be
+   NULL) receive theta1 and C eta of the last loop iteration for the cross rows
+   of the points l1 = rows[0..nrows) (strictly increasing), each in canonical
+   order ((N-1) entries), followed by the N pos rows; res->theta and
+   res->c_eta are not used. */
+int cro_papg_replay(const double *X, const double *ys_shifted, int64_t N, int64_t n,
+                    const cro_config *cfg, const int64_t *rows, int64_t nrows,
+                    double *theta_rows, double *c_eta_rows, cro_result *res);
+
 /* metrics.cpp:8-56 (full row set, canonical order) */
 void cro_infeasibility(const double *X, int64_t N, int64_t n, const double *y, const double *xi,
                        double out2[2]);

@@ -120,6 +120,8 @@ def lib():
         L.cro_papg_k.argtypes = [_P, _P, i64, i64, i64, C.POINTER(CroConfig),
                                  C.POINTER(CroAlccConfig), _P, _P, _P, C.POINTER(CroResult),
                                  C.POINTER(C.c_int64)]
+        L.cro_papg_replay.argtypes = [_P, _P, i64, i64, C.POINTER(CroConfig),
+                                      C.POINTER(C.c_int64), i64, _P, _P, C.POINTER(CroResult)]
         L.cro_cross_position.argtypes = [i64, i64, i64, i64]
         L.cro_cross_position.restype = i64
         _lib = L
@@ -254,6 +256,41 @@ def papg(X, ys, *, gamma=1e-3, B_theta=0.0, adaptive_B_theta=True, max_restarts=
         raise RuntimeError("papg: non-finite dual gradient")
     if rc != 0:
         raise RuntimeError(f"oracle papg failed ({rc})")
+    return OracleResult(y, xi.reshape(N, n), theta, c_eta, hist[: res.iters], int(res.iters),
+                        REASONS[res.reason], res.restarts, bool(res.saturated), res.g_final,
+                        res.delta_estimate, res.sigma_C, res.L_g, res.B_theta, res.wall_seconds,
+                        res.sigma_iters)
+
+
+def papg_replay(X, ys, *, rows=(), gamma=1e-3, B_theta=0.0, adaptive_B_theta=True,
+                max_restarts=6, gap_norm_tol=1e-6, infeas_norm_tol=1e-1, max_iters=100000,
+                max_seconds=7200.0, inner_tol_floor=1e-6, final_resolve_tol=1e-10,
+                record_history=True, use_momentum=True, sigma_C=0.0, threads=1):
+    """Memory-light cro_papg (zero start): no N^2 array. theta / c_eta of the
+    result hold the cross rows of the points in `rows` (sorted, (len x (N-1)),
+    canonical order) followed by the N pos rows."""
+    X = np.ascontiguousarray(X, np.float64)
+    ys = np.ascontiguousarray(ys, np.float64)
+    N, n = X.shape
+    sel = np.unique(np.asarray(rows, np.int64))
+    cfg = CroConfig(gamma, B_theta, int(adaptive_B_theta), max_restarts, gap_norm_tol,
+                    infeas_norm_tol, max_iters, max_seconds, inner_tol_floor, final_resolve_tol,
+                    int(record_history), int(use_momentum), sigma_C, threads, 0)
+    y = np.empty(N)
+    xi = np.empty(N * n)
+    theta = np.empty(sel.size * (N - 1) + N)
+    c_eta = np.empty(sel.size * (N - 1) + N)
+    hist = np.zeros((max_iters if record_history else 0, 8))
+    res = CroResult()
+    res.y, res.xi, res.theta, res.c_eta = _p(y), _p(xi), None, None
+    res.history = _p(hist) if record_history else None
+    rc = lib().cro_papg_replay(_p(X), _p(ys), N, n, C.byref(cfg),
+                               sel.ctypes.data_as(C.POINTER(C.c_int64)), sel.size, _p(theta),
+                               _p(c_eta), C.byref(res))
+    if rc == -4:
+        raise RuntimeError("papg: non-finite dual gradient")
+    if rc != 0:
+        raise RuntimeError(f"oracle papg_replay failed ({rc})")
     return OracleResult(y, xi.reshape(N, n), theta, c_eta, hist[: res.iters], int(res.iters),
                         REASONS[res.reason], res.restarts, bool(res.saturated), res.g_final,
                         res.delta_estimate, res.sigma_C, res.L_g, res.B_theta, res.wall_seconds,

@@ -33,7 +33,7 @@ class PapgResultC(C.Structure):
     _fields_ = [
         ("iters", C.c_int64), ("reason", C.c_int32), ("restarts", C.c_int32),
         ("saturated", C.c_int32), ("sigma_iters", C.c_int32),
-        ("sigma_converged", C.c_int32), ("pad_", C.c_int32),
+        ("sigma_converged", C.c_int32), ("history_truncated", C.c_int32),
         ("g_final", C.c_double), ("delta_estimate", C.c_double), ("sigma_C", C.c_double),
         ("L_g", C.c_double), ("B_theta", C.c_double), ("wall_seconds", C.c_double),
         ("sigma_seconds", C.c_double), ("loop_seconds", C.c_double),
@@ -63,12 +63,15 @@ class AlccResultC(C.Structure):
     ]
 
 
+HISTORY_CAP = 4000000  # CR_HISTORY_CAP (include/cvxreg_b200.h)
+
 # every symbol declared in include/cvxreg_b200.h
 EXPORTS = [
     "cr_create", "cr_destroy", "cr_last_error", "cr_status_string", "cr_nccl_unique_id",
     "cr_attach_nccl", "cr_exchange_len", "cr_sigma_C", "cr_papg_begin", "cr_papg_iterate",
     "cr_iter_local", "cr_exchange_get", "cr_exchange_put", "cr_iter_finish", "cr_papg_finish",
-    "cr_papg_solve", "cr_get_theta", "cr_get_rows", "cr_last_timing", "cr_time_sweep",
+    "cr_papg_solve", "cr_get_theta", "cr_get_rows", "cr_get_theta_rows", "cr_get_rows_window",
+    "cr_last_timing", "cr_time_sweep",
     "cr_sweep_variant", "cr_papg_begin_resume", "cr_set_observations", "cr_infeasibility",
     "cr_duality_gap", "cr_evaluate_estimator", "cr_repair_feasibility",
     "cr_gen_instance", "cr_prepare_problem", "cr_certificate", "cr_momentum_next",
@@ -114,6 +117,8 @@ def load():
         "cr_papg_solve": (st, [vp, C.POINTER(PapgConfigC), _P, C.POINTER(PapgResultC), _P, _P, _P]),
         "cr_get_theta": (st, [vp, _P]),
         "cr_get_rows": (st, [vp, _P]),
+        "cr_get_theta_rows": (st, [vp, i64, i64, _P]),
+        "cr_get_rows_window": (st, [vp, i64, i64, _P]),
         "cr_last_timing": (st, [vp, _P, C.POINTER(i64), _P]),
         "cr_time_sweep": (st, [vp, i32, _P]),
         "cr_sweep_variant": (i32, [vp]),

@@ -625,7 +625,7 @@ cr_status begin_impl(cr_handle* h, const cr_papg_config* cfg, const double* thet
   h->L = h->sigma_C * h->sigma_C / cfg->gamma;  // papg.hpp:43
 
   // history buffer
-  const int64_t want_hist = cfg->record_history ? std::min<int64_t>(cfg->max_iters, 4000000) : 0;
+  const int64_t want_hist = cfg->record_history ? std::min<int64_t>(cfg->max_iters, CR_HISTORY_CAP) : 0;
   if (want_hist > h->hist_cap) {
     dfree(h->hist, h->st);
     h->hist = nullptr;
@@ -1077,6 +1077,7 @@ cr_status cr_papg_finish(cr_handle* h, cr_papg_result* res, double* y, double* x
   res->reason = c.reason;
   res->restarts = c.restarts;
   res->saturated = c.saturated;
+  res->history_truncated = c.record_history && c.ell > c.hist_cap ? 1 : 0;
   res->sigma_iters = h->sigma_iters;
   res->sigma_converged = h->sigma_conv;
   res->g_final = k2[4];
@@ -1107,51 +1108,86 @@ cr_status cr_papg_solve(cr_handle* h, const cr_papg_config* cfg, const double* t
   return cr_papg_finish(h, res, y, xi, history);
 }
 
-cr_status cr_get_theta(cr_handle* h, double* out) {
-  if (!h || !out) return CR_EINVAL;
-  if (!h->begun) return fail(h, CR_ESTATE, "no dual state");
+// theta1 / C eta of local rows [la, lb) of the shard, followed by the N pos rows
+static cr_status get_theta_window(cr_handle* h, int64_t la, int64_t lb, double* out) {
   CUDA_TRY(cudaSetDevice(h->device));
   cr_status s = sync_ctrl(h);
   if (s != CR_OK) return s;
-  if (h->part.K > 0) return general_get_theta(h, out);
   const int cur = h->ctrl_h->cur;
   const double sc = h->ctrl_h->s_cur;
   const int64_t rowlen = h->N - 1;
   const int64_t rows_per = std::max<int64_t>(1, h->stage_elems / rowlen);
-  for (int64_t ra = 0; ra < h->R; ra += rows_per) {
-    const int64_t rb = std::min(h->R, ra + rows_per);
+  for (int64_t ra = la; ra < lb; ra += rows_per) {
+    const int64_t rb = std::min(lb, ra + rows_per);
     CUDA_TRY(launch_theta_out(h->stage, h->V[cur], sc, h->N, h->ld, h->r0, ra, rb, h->st,
                               h->masked ? h->M[cur] : nullptr, mask_geo(h)));
-    CUDA_TRY(cudaMemcpyAsync(out + ra * rowlen, h->stage, sizeof(double) * (rb - ra) * rowlen,
+    CUDA_TRY(cudaMemcpyAsync(out + (ra - la) * rowlen, h->stage, sizeof(double) * (rb - ra) * rowlen,
                              cudaMemcpyDeviceToHost, h->st));
     CUDA_TRY(cudaStreamSynchronize(h->st));
   }
   CUDA_TRY(launch_scale_copy(h->stage, h->vpos[cur], sc, h->N, h->st));
-  CUDA_TRY(cudaMemcpyAsync(out + h->R * rowlen, h->stage, sizeof(double) * h->N,
+  CUDA_TRY(cudaMemcpyAsync(out + (lb - la) * rowlen, h->stage, sizeof(double) * h->N,
                            cudaMemcpyDeviceToHost, h->st));
   CUDA_TRY(cudaStreamSynchronize(h->st));
   return CR_OK;
 }
 
-cr_status cr_get_rows(cr_handle* h, double* out) {
-  if (!h || !out) return CR_EINVAL;
-  if (!h->begun) return fail(h, CR_ESTATE, "no dual state");
+static cr_status get_rows_window(cr_handle* h, int64_t la, int64_t lb, double* out) {
   CUDA_TRY(cudaSetDevice(h->device));
-  if (h->part.K > 0) return general_get_rows(h, out);
   const int64_t rowlen = h->N - 1;
   const int64_t rows_per = std::max<int64_t>(1, h->stage_elems / rowlen);
-  for (int64_t ra = 0; ra < h->R; ra += rows_per) {
-    const int64_t rb = std::min(h->R, ra + rows_per);
+  for (int64_t ra = la; ra < lb; ra += rows_per) {
+    const int64_t rb = std::min(lb, ra + rows_per);
     CUDA_TRY(launch_rows_out(h->stage, h->rowrec, h->colrec, h->N, (int)h->n, h->r0, ra, rb, h->st));
-    CUDA_TRY(cudaMemcpyAsync(out + ra * rowlen, h->stage, sizeof(double) * (rb - ra) * rowlen,
+    CUDA_TRY(cudaMemcpyAsync(out + (ra - la) * rowlen, h->stage, sizeof(double) * (rb - ra) * rowlen,
                              cudaMemcpyDeviceToHost, h->st));
     CUDA_TRY(cudaStreamSynchronize(h->st));
   }
   std::vector<double> rec((size_t)h->N * h->RP);
   CUDA_TRY(cudaMemcpy(rec.data(), h->rowrec, sizeof(double) * rec.size(), cudaMemcpyDeviceToHost));
   for (int64_t l = 0; l < h->N; ++l)  // apply_C :152, y of eta
-    out[h->R * rowlen + l] = rec[(size_t)l * h->RP + h->n + 1];
+    out[(lb - la) * rowlen + l] = rec[(size_t)l * h->RP + h->n + 1];
   return CR_OK;
+}
+
+cr_status cr_get_theta(cr_handle* h, double* out) {
+  if (!h || !out) return CR_EINVAL;
+  if (!h->begun) return fail(h, CR_ESTATE, "no dual state");
+  if (h->part.K > 0) {
+    CUDA_TRY(cudaSetDevice(h->device));
+    cr_status s = sync_ctrl(h);
+    if (s != CR_OK) return s;
+    return general_get_theta(h, out);
+  }
+  return get_theta_window(h, 0, h->R, out);
+}
+
+cr_status cr_get_rows(cr_handle* h, double* out) {
+  if (!h || !out) return CR_EINVAL;
+  if (!h->begun) return fail(h, CR_ESTATE, "no dual state");
+  if (h->part.K > 0) {
+    CUDA_TRY(cudaSetDevice(h->device));
+    return general_get_rows(h, out);
+  }
+  return get_rows_window(h, 0, h->R, out);
+}
+
+cr_status cr_get_theta_rows(cr_handle* h, int64_t row_begin, int64_t row_end, double* out) {
+  if (!h || !out) return CR_EINVAL;
+  if (!h->begun) return fail(h, CR_ESTATE, "no dual state");
+  if (h->part.K > 0) return fail(h, CR_EINVAL, "row windows need singleton blocks");
+  if (row_begin < h->r0 || row_end > h->r0 + h->R || row_begin > row_end)
+    return fail(h, CR_EINVAL, "row window outside the shard");
+  return get_theta_window(h, row_begin - h->r0, row_end - h->r0, out);
+}
+
+cr_status cr_get_rows_window(cr_handle* h, int64_t row_begin, int64_t row_end, double* out) {
+  if (!h || !out) return CR_EINVAL;
+  if (!h->begun) return fail(h, CR_ESTATE, "no dual state");
+  if (h->part.K > 0) return fail(h, CR_EINVAL, "row windows need singleton blocks");
+  if (row_begin < h->r0 || row_end > h->r0 + h->R || row_begin > row_end)
+    return fail(h, CR_EINVAL, "row window outside the shard");
+  return get_rows_window(h, row_begin - h->r0, row_end - h->r0, out);
 }
 
 cr_status cr_last_timing(const cr_handle* h, double* seconds, int64_t* launches,

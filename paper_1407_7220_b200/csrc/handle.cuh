@@ -172,9 +172,24 @@ inline cr_status fail(cr_handle* h, cr_status s, const std::string& what) {
 // told to keep freed memory: a service that creates a handle per solve reuses
 // the mapping instead of paying cudaMalloc/cudaFree of gigabytes each time.
 extern cudaStream_t g_alloc_stream;  // stream of the handle being created (capi.cu)
+// On failure the pool's retained (freed) memory is returned to the device and
+// the allocation retried once: a 160 GB handle after a 40 GB one in the same
+// process must not fail on memory the pool only keeps for reuse.
 template <typename T>
 inline cudaError_t dalloc(T** p, size_t count) {
-  return cudaMallocAsync((void**)p, (count ? count : 1) * sizeof(T), g_alloc_stream);
+  const size_t bytes = (count ? count : 1) * sizeof(T);
+  cudaError_t e = cudaMallocAsync((void**)p, bytes, g_alloc_stream);
+  if (e == cudaErrorMemoryAllocation) {
+    cudaGetLastError();
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceSynchronize() == cudaSuccess &&
+        cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      cudaMemPoolTrimTo(pool, 0);
+      e = cudaMallocAsync((void**)p, bytes, g_alloc_stream);
+    }
+  }
+  return e;
 }
 inline void dfree(void* p, cudaStream_t s) {
   if (p) cudaFreeAsync(p, s);

@@ -141,6 +141,7 @@ class SolveReport:  # metrics.hpp:45-54
     saturated: bool = False
     note: str = ""
     history_array: np.ndarray | None = None
+    history_truncated: bool = False  # more than CR_HISTORY_CAP iterations: first ones kept
 
 
 @dataclass
@@ -261,7 +262,11 @@ class DualSolver:
     def __init__(self, xs, ys_shifted, gamma=1e-3, device=0, row_begin=0, row_end=None):
         self.xs = np.ascontiguousarray(xs, np.float64)
         self.ys = np.ascontiguousarray(ys_shifted, np.float64)
+        if self.xs.ndim != 2:
+            raise ValueError("xs must be N x n")
         self.N, self.n = self.xs.shape
+        if self.ys.shape != (self.N,):  # operators.cpp:12-14 shape checks
+            raise ValueError(f"ys has shape {self.ys.shape}, expected ({self.N},)")
         self.row_begin = row_begin
         self.row_end = self.N if row_end is None else row_end
         self._L = nat.load()
@@ -327,7 +332,9 @@ class DualSolver:
     def begin(self, cfg: PapgConfig, use_momentum=True, theta0=None):
         self.cfg = cfg
         c = cfg.to_c(use_momentum)
-        t0 = None if theta0 is None else np.ascontiguousarray(theta0, np.float64)
+        t0 = None if theta0 is None else np.ascontiguousarray(theta0, np.float64).reshape(-1)
+        if t0 is not None and t0.size != self._dual_len():  # papg.cpp:160-161
+            raise ValueError("papg: warm-start theta has wrong size")
         _raise(self._L.cr_papg_begin(self.h, C.byref(c), nat.ptr(t0)), self.h)
 
     def iterate(self, max_steps):
@@ -360,7 +367,7 @@ class DualSolver:
         xi = np.empty(self.N * self.n)
         cap = 0
         if want_history and self.cfg is not None and self.cfg.record_history:
-            cap = int(min(self.cfg.max_iters, 4000000))
+            cap = int(min(self.cfg.max_iters, nat.HISTORY_CAP))
         hist = np.zeros((max(cap, 1), 8))
         _raise(self._L.cr_papg_finish(self.h, C.byref(res), nat.ptr(y), nat.ptr(xi),
                                       nat.ptr(hist) if cap else None), self.h)
@@ -418,6 +425,18 @@ class DualSolver:
     def rows(self):
         out = np.empty(self._dual_len())
         _raise(self._L.cr_get_rows(self.h, nat.ptr(out)), self.h)
+        return out
+
+    def theta_rows(self, row_begin, row_end):
+        """theta1 of global pair rows [row_begin, row_end) (canonical order) + the N pos rows."""
+        out = np.empty((row_end - row_begin) * (self.N - 1) + self.N)
+        _raise(self._L.cr_get_theta_rows(self.h, row_begin, row_end, nat.ptr(out)), self.h)
+        return out
+
+    def rows_window(self, row_begin, row_end):
+        """C eta of the last iteration for pair rows [row_begin, row_end) + the N pos rows."""
+        out = np.empty((row_end - row_begin) * (self.N - 1) + self.N)
+        _raise(self._L.cr_get_rows_window(self.h, row_begin, row_end, nat.ptr(out)), self.h)
         return out
 
     def last_timing(self):
@@ -539,7 +558,8 @@ def _solve(prep: PreparedProblem, cfg: PapgConfig, theta0, use_momentum, want_du
     history = [MetricsSnapshot(int(h[0]), *map(float, h[1:])) for h in hist]
     rep = SolveReport(history=history, reason=TermReason(res.reason), iters=int(res.iters),
                       wall_seconds=res.wall_seconds, restarts=res.restarts,
-                      saturated=bool(res.saturated), history_array=hist)
+                      saturated=bool(res.saturated), history_array=hist,
+                      history_truncated=bool(res.history_truncated))
     return PapgResult(PrimalPoint(y, xi), dual, rep, res.g_final, res.delta_estimate, res.sigma_C,
                       res.L_g, res.B_theta, res.sigma_iters, res.sigma_seconds, res.loop_seconds)
 

@@ -181,6 +181,34 @@ def test_warm_start_parity(oracle):
                   oracle_run(oracle, X, ys, theta0=theta0, **kw))
 
 
+def test_warm_start_wrong_size_rejected(oracle):
+    """papg.cpp:160-161: a warm start of the wrong length is an invalid_argument."""
+    X, ys = instance(oracle, "sqnorm-uniform", 120, 3, 0.1, 3)
+    with crb.DualSolver(X, ys) as s:
+        with pytest.raises(ValueError, match="warm-start"):
+            s.begin(crb.PapgConfig(max_iters=2, sigma_C=10.0), True, np.zeros(120 * 119))
+
+
+def test_theta_row_windows_match_full_export(oracle):
+    """cr_get_theta_rows / cr_get_rows_window (spot checks at cfg 5 sizes) are
+    slices of the full exports."""
+    X, ys = instance(oracle, "maxaffine-uniform", 333, 7, 0.1, 21, 5)
+    with crb.DualSolver(X, ys) as s:
+        s.begin(crb.PapgConfig(max_iters=9, gap_norm_tol=-1.0, infeas_norm_tol=-1.0, sigma_C=50.0))
+        s.iterate(100)
+        th, ce = s.theta(), s.rows()
+        N = 333
+        for a, b in ((0, 1), (5, 77), (300, 333), (0, 333), (17, 17)):
+            w = s.theta_rows(a, b)
+            assert np.array_equal(w[: (b - a) * (N - 1)], th[a * (N - 1):b * (N - 1)])
+            assert np.array_equal(w[(b - a) * (N - 1):], th[N * (N - 1):])
+            r = s.rows_window(a, b)
+            assert np.array_equal(r[: (b - a) * (N - 1)], ce[a * (N - 1):b * (N - 1)])
+            assert np.array_equal(r[(b - a) * (N - 1):], ce[N * (N - 1):])
+        with pytest.raises(ValueError):
+            s.theta_rows(10, 400)
+
+
 def test_graph_and_direct_modes_bitwise_identical(oracle):
     X, ys = instance(oracle, "sqnorm-uniform", 700, 5, 0.1, 4)
     s, _, _ = oracle.sigma_C(X)

@@ -110,3 +110,5 @@ def test_create_rejects_invalid_shapes():
         crb.DualSolver(X, np.zeros(40))  # n > 32 (kMaxN) is not supported
     with pytest.raises(ValueError):
         crb.DualSolver(np.zeros((1, 2)), np.zeros(1))
+    with pytest.raises(ValueError):
+        crb.DualSolver(np.zeros((40, 3)), np.zeros(39))  # ys must have N entries
