@@ -23,9 +23,11 @@ namespace crb {
 
 constexpr int kMaxN = 32;    // templated register path covers n = 1..kMaxN
 // every per-n kernel table is generated from these two lists (keep them = 1..kMaxN)
+#ifndef CRB_N_LIST  // (-DCRB_N_LIST=10: one-n builds for SASS inspection only)
 #define CRB_N_LIST                                                                           \
   1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16, 17, 18, 19, 20, 21, 22, 23, 24, 25, \
       26, 27, 28, 29, 30, 31, 32
+#endif
 #define CRB_N_SEQ(F)                                                                         \
   F(1), F(2), F(3), F(4), F(5), F(6), F(7), F(8), F(9), F(10), F(11), F(12), F(13), F(14),   \
       F(15), F(16), F(17), F(18), F(19), F(20), F(21), F(22), F(23), F(24), F(25), F(26),    \

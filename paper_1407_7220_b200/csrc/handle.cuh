@@ -202,7 +202,10 @@ inline void keep_pool_memory(int device) {
   }
 }
 
-inline int64_t payload_len(const cr_handle* h) { return h->N * (h->n + 2) + kScal; }
+// [row sums N | colagg N(n+1) | kScal sweep scalars | clock]: the clock slot
+// carries the elapsed seconds of the shard that owns row 0 (0 elsewhere), so
+// the summed payload gives every rank the same time-budget decision
+inline int64_t payload_len(const cr_handle* h) { return h->N * (h->n + 2) + kScal + 1; }
 
 inline SweepArgs sweep_args(cr_handle* h, int mode, bool agg_only) {
   SweepArgs a{};
@@ -259,6 +262,7 @@ inline ReduceArgs reduce_args(cr_handle* h, bool with_k2, const int* stopped, bo
   a.stopped = stopped;
   a.rank = h->rank;
   a.ctrl = fuse_control ? h->ctrl_d : nullptr;
+  a.clk = with_k2 ? h->ctrl_d : nullptr;
   a.hist = h->hist;
   a.counter = h->counter;
   a.N = h->N;

@@ -137,8 +137,10 @@ __device__ __forceinline__ double momentum_next(double t) {  // engines.hpp:11-1
 }
 
 // Kc: papg.cpp:187-262 on the reduced scalars. One thread.
+// wall_in >= 0: the elapsed seconds to test the time budget against (sharded
+// runs: one clock for all ranks); < 0: this GPU's own clock
 __device__ __forceinline__ void control_logic(DevCtrl* c, const double* scal, const double* k2,
-                                              double* hist) {
+                                              double* hist, double wall_in) {
   const long long ell = c->ell + 1;
   const double S_vv = scal[0] + k2[0];
   const double S_vr = scal[1] + k2[1];
@@ -164,7 +166,7 @@ __device__ __forceinline__ void control_logic(DevCtrl* c, const double* scal, co
   const double infeas_raw = sqrt(within * within + cross_infeas * cross_infeas);
   const double gap_norm = gap_raw / c->gap_div;
   const double infeas_norm = infeas_raw / c->infeas_div;
-  const double wall = (double)(globaltimer() - c->t_start_ns) * 1e-9;
+  const double wall = wall_in >= 0.0 ? wall_in : (double)(globaltimer() - c->t_start_ns) * 1e-9;
   c->gap_raw = gap_raw;
   c->gap_norm = gap_norm;
   c->infeas_raw = infeas_raw;
@@ -234,14 +236,14 @@ __device__ __forceinline__ void control_logic(DevCtrl* c, const double* scal, co
 // The state block is copied to registers, updated and written back: one round
 // trip to memory instead of a chain of dependent field accesses.
 __device__ __noinline__ void control_step(DevCtrl* cg, const double* scal_g, const double* k2_g,
-                                          double* hist) {
+                                          double* hist, double wall_in = -1.0) {
   DevCtrl c = *cg;
   double scal[kScal], k2[kK2Scal];
 #pragma unroll
   for (int w = 0; w < kScal; ++w) scal[w] = scal_g[w];
 #pragma unroll
   for (int w = 0; w < kK2Scal; ++w) k2[w] = k2_g[w];
-  control_logic(&c, scal, k2, hist);
+  control_logic(&c, scal, k2, hist, wall_in);
   c.halt = (c.stopped || c.ell >= c.pause_at) ? 1 : 0;
   *cg = c;
 }

@@ -56,11 +56,14 @@ __global__ void __launch_bounds__(kPBlock) primal_kernel(const PrimalArgs a) {
   block_reduce_store<kK2Scal, kPBlock>(acc, a.k2part + (long long)blockIdx.x * kK2Scal);
 }
 
-__global__ void control_kernel(DevCtrl* c, const double* scal /* kScal, allreduced */,
+// sharded / phased iterations: scal[kScal] is the payload's clock slot (the
+// elapsed time of the shard owning row 0), so every rank takes the same
+// time-budget decision (papg.cpp:233-236)
+__global__ void control_kernel(DevCtrl* c, const double* scal /* kScal + clock, allreduced */,
                                const double* k2 /* kK2Scal, replicated */, double* hist) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   if (c->halt) return;
-  control_step(c, scal, k2, hist);
+  control_step(c, scal, k2, hist, scal[kScal]);
 }
 
 // fixed-order sum of the sweep scalar records and the K2 records (one block):
@@ -110,6 +113,8 @@ __device__ __forceinline__ void scalar_records(const ReduceArgs& a, long long sc
     if (threadIdx.x < kScal) a.agg_out[scal_at + threadIdx.x] = t;
     else if (a.k2sum != nullptr) a.k2sum[threadIdx.x - kScal] = t;
   }
+  if (threadIdx.x == 0 && a.clk != nullptr)
+    a.agg_out[scal_at + kScal] = a.r0 == 0 ? (double)(globaltimer() - a.clk->t_start_ns) * 1e-9 : 0.0;
 }
 
 // K3: fixed-order reduction of the sweep partials. On a single GPU block 0
@@ -126,7 +131,7 @@ __global__ void __launch_bounds__(kBlock, 6) reduce_kernel(const ReduceArgs a) {
     // halted: keep the (already reduced) payload on rank 0, zero it elsewhere,
     // so a trailing in-place allreduce leaves it unchanged on every rank
     if (a.rank != 0) {
-      const long long total = N + ncol + kScal;
+      const long long total = N + ncol + kScal + 1;
       for (long long i = (long long)blockIdx.x * kBlock + threadIdx.x; i < total;
            i += (long long)gridDim.x * kBlock)
         a.agg_out[i] = 0.0;

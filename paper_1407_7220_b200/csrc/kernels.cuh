@@ -37,6 +37,8 @@ struct ReduceArgs {
   double* k2sum;          // kK2Scal (may be null)
   const int* stopped;     // halted: rank 0 keeps agg_out, other ranks zero it
   DevCtrl* ctrl;          // non-null: the last block runs the control step
+  const DevCtrl* clk;     // non-null: write the payload's clock slot (elapsed seconds
+                          // since clk->t_start_ns on the shard with r0 == 0, else 0)
   double* hist;
   unsigned int* counter;  // (unused by the reduce kernel; kept for the ABI of ReduceArgs users)
   int rank;

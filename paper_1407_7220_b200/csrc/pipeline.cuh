@@ -107,4 +107,25 @@ __device__ __forceinline__ double keep_if_neg(double r) {
   return __hiloint2double(hi & m, lo & m);
 }
 
+// acc += min(r, 0)^2 in three instructions: r >= 0 keeps only its low word, a
+// subnormal of at most 2^-1042 whose square rounds to +0 (acc + 0 = acc)
+__device__ __forceinline__ void acc_neg_sq(double& acc, double r) {
+  const int hi = __double2hiint(r);
+  const double m = __hiloint2double(hi & (hi >> 31), __double2loint(r));
+  acc = fma(m, m, acc);
+}
+// *p = v (streaming) and ++count when v != old (v, old >= +0: numeric != is the
+// bit test), as one predicated store instead of a branch
+__device__ __forceinline__ void store_if_changed(double* p, double v, double old, int& count) {
+  asm volatile(
+      "{\n"
+      ".reg .pred q;\n"
+      "setp.neu.f64 q, %2, %3;\n"
+      "@q st.global.cs.f64 [%1], %2;\n"
+      "@q add.s32 %0, %0, 1;\n"
+      "}\n"
+      : "+r"(count)
+      : "l"(p), "d"(v), "d"(old));
+}
+
 }  // namespace crb

@@ -30,23 +30,25 @@ namespace crb {
 
 namespace {
 
-// P-APG stage for one warp: the residuals of all kCT tiles first (independent
-// DMMA chains interleaved), then per tile a cold test on the inputs. With
-// theta1 = theta1_prev = 0 and row >= 0 everywhere in a tile (late in a solve
-// almost every tile) theta2 = 0 and v = 0 = theta1_prev: no store, and every
-// scalar, row-sum and aggregate update adds an exact zero -- the warp skips the
-// tile after one vote, before computing theta2 or v. MASK stages (diagonal,
-// partial stage, pad columns) always take the full path. Returns whether any
-// tile of the stage was hot (warp-uniform): a cold stage has zero row sums.
-template <int NN, bool MASK, bool UNIT, bool BLK>
-__device__ __forceinline__ bool papg_stage(const double* __restrict__ sv, const double* __restrict__ svp,
-                                           const double* __restrict__ srec, double* gout,
-                                           long long ld, long long gcol0, long long grow0, int nr,
-                                           long long ncols, long long nbar,
-                                           int lane, const double (&A)[mma_ct<NN>()][ksteps<NN>()],
-                                           double (&D)[mma_ct<NN>()][fblocks<NN>()][2],
-                                           const double (&Cc)[mma_ct<NN>()], const MCoef& cf,
-                                           MScal& sc, double (&rs)[2], int& nst) {
+// Lean P-APG stage for a clean stage (no diagonal in the warp's columns, all 8
+// rows present, no pad column), one warp: the residuals of all kCT tiles first
+// (independent DMMA chains interleaved), then per tile theta2, v, the store of a
+// changed multiplier, the scalar sums and the aggregation MMAs.
+// TEST: per-tile cold test on the inputs -- with theta1 = theta1_prev = 0 and
+// row >= 0 everywhere in a tile (late in a solve almost every tile) theta2 = 0
+// and v = 0 = theta1_prev: no store, and every scalar, row-sum and aggregate
+// update adds an exact zero, so the warp skips the tile after one vote; a tile
+// whose v are all zero skips its aggregation MMAs. !TEST: no tests at all (the
+// dense early iterations, where no tile is cold). Both variants evaluate the
+// same expressions for a hot tile, so results are bitwise identical. Returns
+// the number of cold tiles (TEST).
+template <int NN, bool UNIT, bool TEST>
+__device__ __forceinline__ int papg_clean(const double* __restrict__ sv, const double* __restrict__ svp,
+                                          const double* __restrict__ srec, double* g0, double* g1,
+                                          int lane, const double (&A)[mma_ct<NN>()][ksteps<NN>()],
+                                          double (&D)[mma_ct<NN>()][fblocks<NN>()][2],
+                                          const double (&Cc)[mma_ct<NN>()], const MCoef& cf, MScal& sc,
+                                          double (&rs)[2], int& nst) {
   CRB_GEO(NN)
   constexpr int KS = ksteps<NN>();
   constexpr int FB = fblocks<NN>();
@@ -54,10 +56,19 @@ __device__ __forceinline__ bool papg_stage(const double* __restrict__ sv, const 
   constexpr bool SPLIT = split_yc<NN>();
   const int q = lane & 3;
   const int c8 = lane >> 2;
+  const double* r0 = srec + (2 * q) * RQ;  // records of rows 2q, 2q+1
+  const double* r1 = r0 + RQ;
   double yr[2] = {0.0, 0.0};  // y of rows 2q, 2q+1 (split form)
   if (SPLIT) {
-    yr[0] = srec[(2 * q) * RQ + NN + 1];
-    yr[1] = srec[(2 * q + 1) * RQ + NN + 1];
+    yr[0] = r0[NN + 1];
+    yr[1] = r1[NN + 1];
+  }
+  // aggregation A fragments, shared by the stage's tiles: [X 1][row 2q+j][feature fb*8 + c8]
+  double Ag[2][FB];
+#pragma unroll
+  for (int fb = 0; fb < FB; ++fb) {
+    Ag[0][fb] = r0[fb * 8 + c8];
+    Ag[1][fb] = r1[fb * 8 + c8];
   }
   double d[kCT][2];
   {
@@ -72,9 +83,7 @@ __device__ __forceinline__ bool papg_stage(const double* __restrict__ sv, const 
       for (int ct = 0; ct < kCT; ++ct) dmma(d[ct][0], d[ct][1], A[ct][ks], B[ks]);
     }
   }
-  // stored multipliers are v >= +0 (never -0), so "both zero" is one OR of the bits
-  double* g0 = gout + (long long)(2 * q) * ld + c8;  // rows 2q, 2q+1 of the stage
-  bool any_hot = false;
+  int cold = 0;
   rs[0] = 0.0;
   rs[1] = 0.0;
 #pragma unroll
@@ -89,24 +98,20 @@ __device__ __forceinline__ bool papg_stage(const double* __restrict__ sv, const 
       c1[j] = sv[rr * kTCP + cl];
       p1[j] = svp[rr * kTCP + cl];
     }
-    bool hot = true;
-    if (!MASK) {
+    if (TEST) {
+      // stored multipliers are v >= +0 (never -0), so "both zero" is one OR of the bits
       const unsigned long long bits =
           (unsigned long long)__double_as_longlong(c1[0]) | (unsigned long long)__double_as_longlong(c1[1]) |
           (unsigned long long)__double_as_longlong(p1[0]) | (unsigned long long)__double_as_longlong(p1[1]);
-      hot = bits != 0ull || (__double2hiint(row[0]) | __double2hiint(row[1])) < 0;
+      const bool hot = bits != 0ull || (__double2hiint(row[0]) | __double2hiint(row[1])) < 0;
+      if (!__any_sync(0xffffffffu, hot)) {
+        ++cold;
+        continue;
+      }
     }
-    if (!__any_sync(0xffffffffu, hot)) continue;
-    any_hot = true;
     double v[2];
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
-      const int rr = 2 * q + j;
-      const bool rv = !MASK || rr < nr;  // row present in this (partial) stage
-      // diagonal, rows past a partial stage, pad columns (with y - c split out
-      // of the MMA a pad column's zero fragments no longer zero its row)
-      if (MASK && (same_block<BLK>(gcol0 + cl, grow0 + rr, nbar) || !rv || gcol0 + cl >= ncols))
-        row[j] = 0.0;
       double th2;
       if (UNIT) {
         th2 = fma(cf.beta, c1[j] - p1[j], c1[j]);
@@ -114,35 +119,111 @@ __device__ __forceinline__ bool papg_stage(const double* __restrict__ sv, const 
         const double th1 = cf.s_c * c1[j];
         th2 = fma(cf.beta, th1 - cf.s_p * p1[j], th1);
       }
-      if (MASK && !rv) th2 = 0.0;
       v[j] = keep_if_nonneg(fma(-row[j], cf.invL, th2));
       // v goes into the buffer that holds p1 (theta1_prev): an unchanged value
       // needs no store
-      if (rv && __double_as_longlong(v[j]) != __double_as_longlong(p1[j])) {
-        st_stream(g0 + (long long)j * ld + ct * 8, v[j]);
-        ++nst;
-      }
+      store_if_changed((j ? g1 : g0) + ct * 8, v[j], p1[j], nst);
       sc.vv = fma(v[j], v[j], sc.vv);
       sc.vr = fma(v[j], row[j], sc.vr);
       sc.tr = fma(th2, row[j], sc.tr);
-      const double m = keep_if_neg(row[j]);
-      sc.nn = fma(m, m, sc.nn);
+      acc_neg_sq(sc.nn, row[j]);  // min(row, 0)^2
       rs[j] += v[j];
     }
-    // a tile whose v are all zero adds exact zeros to the aggregates: skip its
-    // aggregation MMAs
-    if (__any_sync(0xffffffffu, v[0] != 0.0 || v[1] != 0.0)) {
+    // a tile whose v are all zero adds exact zeros to the aggregates
+    if (!TEST || __any_sync(0xffffffffu, v[0] != 0.0 || v[1] != 0.0)) {
 #pragma unroll
       for (int fb = 0; fb < FB; ++fb) {
-        // aggregation A fragments: [X 1][row 2q+j][feature fb*8 + c8]
-        const double a0 = (!MASK || 2 * q < nr) ? srec[(2 * q) * RQ + fb * 8 + c8] : 0.0;
-        const double a1 = (!MASK || 2 * q + 1 < nr) ? srec[(2 * q + 1) * RQ + fb * 8 + c8] : 0.0;
-        dmma(D[ct][fb][0], D[ct][fb][1], a0, v[0]);
-        dmma(D[ct][fb][0], D[ct][fb][1], a1, v[1]);
+        dmma(D[ct][fb][0], D[ct][fb][1], Ag[0][fb], v[0]);
+        dmma(D[ct][fb][0], D[ct][fb][1], Ag[1][fb], v[1]);
       }
     }
   }
-  return any_hot;
+  return cold;
+}
+
+// P-APG stage with masking (diagonal, partial stage, pad columns), one warp.
+template <int NN, bool UNIT, bool BLK>
+__device__ __forceinline__ void papg_masked(const double* __restrict__ sv, const double* __restrict__ svp,
+                                            const double* __restrict__ srec, double* gout,
+                                            long long ld, long long gcol0, long long grow0, int nr,
+                                            long long ncols, long long nbar,
+                                            int lane, const double (&A)[mma_ct<NN>()][ksteps<NN>()],
+                                            double (&D)[mma_ct<NN>()][fblocks<NN>()][2],
+                                            const double (&Cc)[mma_ct<NN>()], const MCoef& cf,
+                                            MScal& sc, double (&rs)[2], int& nst) {
+  CRB_GEO(NN)
+  constexpr int KS = ksteps<NN>();
+  constexpr int FB = fblocks<NN>();
+  constexpr int RQ = rec_pitch(NN);
+  constexpr bool SPLIT = split_yc<NN>();
+  const int q = lane & 3;
+  const int c8 = lane >> 2;
+  double yr[2] = {0.0, 0.0};
+  if (SPLIT) {
+    yr[0] = srec[(2 * q) * RQ + NN + 1];
+    yr[1] = srec[(2 * q + 1) * RQ + NN + 1];
+  }
+  double Ag[2][FB];
+#pragma unroll
+  for (int fb = 0; fb < FB; ++fb) {
+    Ag[0][fb] = (2 * q < nr) ? srec[(2 * q) * RQ + fb * 8 + c8] : 0.0;
+    Ag[1][fb] = (2 * q + 1 < nr) ? srec[(2 * q + 1) * RQ + fb * 8 + c8] : 0.0;
+  }
+  double d[kCT][2];
+  {
+    double B[KS];
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) B[ks] = srec[c8 * RQ + ks * 4 + q];
+#pragma unroll
+    for (int ct = 0; ct < kCT; ++ct) d[ct][0] = d[ct][1] = 0.0;
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+#pragma unroll
+      for (int ct = 0; ct < kCT; ++ct) dmma(d[ct][0], d[ct][1], A[ct][ks], B[ks]);
+    }
+  }
+  double* g0 = gout + (long long)(2 * q) * ld + c8;
+  rs[0] = 0.0;
+  rs[1] = 0.0;
+#pragma unroll
+  for (int ct = 0; ct < kCT; ++ct) {
+    const int cl = ct * 8 + c8;
+    double v[2];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int rr = 2 * q + j;
+      const bool rv = rr < nr;  // row present in this (partial) stage
+      double row = d[ct][j];
+      if (SPLIT) row += yr[j] + Cc[ct];
+      // diagonal, rows past a partial stage, pad columns (with y - c split out
+      // of the MMA a pad column's zero fragments no longer zero its row)
+      if (same_block<BLK>(gcol0 + cl, grow0 + rr, nbar) || !rv || gcol0 + cl >= ncols) row = 0.0;
+      const double c1 = sv[rr * kTCP + cl];
+      const double p1 = svp[rr * kTCP + cl];
+      double th2;
+      if (UNIT) {
+        th2 = fma(cf.beta, c1 - p1, c1);
+      } else {
+        const double th1 = cf.s_c * c1;
+        th2 = fma(cf.beta, th1 - cf.s_p * p1, th1);
+      }
+      if (!rv) th2 = 0.0;
+      v[j] = keep_if_nonneg(fma(-row, cf.invL, th2));
+      if (rv) store_if_changed(g0 + (long long)j * ld + ct * 8, v[j], p1, nst);
+      sc.vv = fma(v[j], v[j], sc.vv);
+      sc.vr = fma(v[j], row, sc.vr);
+      sc.tr = fma(th2, row, sc.tr);
+      acc_neg_sq(sc.nn, row);
+      rs[j] += v[j];
+    }
+    if (__any_sync(0xffffffffu, v[0] != 0.0 || v[1] != 0.0)) {
+#pragma unroll
+      for (int fb = 0; fb < FB; ++fb) {
+        dmma(D[ct][fb][0], D[ct][fb][1], Ag[0][fb], v[0]);
+        dmma(D[ct][fb][0], D[ct][fb][1], Ag[1][fb], v[1]);
+      }
+    }
+  }
 }
 
 // One 8-row stage for one warp, the other modes (power, penalty). MASK:
@@ -325,6 +406,7 @@ __global__ void __launch_bounds__(mma_threads<NN>(), mma_ctas<NN>()) sweep_mma_k
   const bool unit_scale = (cf.s_c == 1.0) && (cf.s_p == 1.0);
   MScal sc{0.0, 0.0, 0.0, 0.0};
   int nst = 0;  // stores issued by this thread (P-APG mode)
+  int probe = 0, pstage = 0;  // adaptive cold test (P-APG mode)
   int i = 0;
   int flushes = 0;
 
@@ -350,9 +432,99 @@ __global__ void __launch_bounds__(mma_threads<NN>(), mma_ctas<NN>()) sweep_mma_k
 #pragma unroll
       for (int fb = 0; fb < FB; ++fb) D[ct][fb][0] = D[ct][fb][1] = 0.0;
     }
-    int win = 0;
-    long long win_base = rlo;
-    for (long long r = rlo; r < rhi; r += kTR, ++i) {
+    if constexpr (MODE == kModePapg && !BLK) {
+      // lean stage loop of the singleton P-APG sweep: 32-bit stage counters, the
+      // stages that meet the diagonal precomputed per segment, the output
+      // pointer advanced per stage
+      const int nrows = (int)(rhi - rlo);
+      const int nstage = (nrows + kTR - 1) / kTR;
+      const long long base = a.r0 + rlo;  // global row of the segment's first stage
+      // stage s (rows base + 8s .. +8) meets the warp's columns [gcol0, gcol0 + kW)
+      // iff s in [s_dlo, s_dhi)
+      const long long dlo = gcol0 - kTR - base, dhi = gcol0 + kW - 1 - base;
+      const int s_dlo = (int)max(0ll, (dlo >= 0 ? dlo / kTR : -((-dlo + kTR - 1) / kTR)) + 1);
+      const int s_dhi = (int)max(0ll, min((long long)nstage, (dhi >= 0 ? dhi / kTR : -((-dhi + kTR - 1) / kTR)) + 1));
+      const int s_part = (nrows % kTR) ? nstage - 1 : nstage;  // partial last stage
+      const bool full_warp = gcol0 + kW <= a.N;
+      double* gout = Vp + rlo * a.ld + gcol0;
+      const long long gstep = (long long)kTR * a.ld;
+      // this lane's output rows 2q, 2q+1 (column c8) of the current stage
+      double* o0 = gout + (long long)(2 * q) * a.ld + c8;
+      double* o1 = o0 + a.ld;
+      int win = 0, win_base = 0;
+      for (int st8 = 0; st8 < nstage; ++st8, ++i, gout += gstep, o0 += gstep, o1 += gstep) {
+        const int s = i % kNS;
+        mbar_wait(&full[s], (uint32_t)((i / kNS) & 1));
+        double rsj[2] = {0.0, 0.0};
+        bool hot_stage = true;
+        if (active) {
+          const double* stg = stages + s * SD;
+          const double* sv = stg + warp * kW;
+          const double* svp = stg + kTR * kTCP + warp * kW;
+          const double* srec = stg + 2 * kTR * kTCP;
+          const bool clean = full_warp && (st8 < s_dlo || st8 >= s_dhi) && st8 < s_part;
+          if (clean) {
+            // per-warp adaptive cold test: a tested stage that finds a cold tile
+            // keeps the test on for the next 8 stages; otherwise every 8th stage
+            // probes and the others run without any test
+            const bool test = probe > 0 || (pstage & 7) == 0;
+            ++pstage;
+            if (test) {
+              const int cold = unit_scale
+                  ? papg_clean<NN, true, true>(sv, svp, srec, o0, o1, lane, A, D, Cc, cf, sc, rsj, nst)
+                  : papg_clean<NN, false, true>(sv, svp, srec, o0, o1, lane, A, D, Cc, cf, sc, rsj, nst);
+              probe = cold ? 8 : (probe > 0 ? probe - 1 : 0);
+              hot_stage = cold < kCT;
+            } else if (unit_scale) {
+              papg_clean<NN, true, false>(sv, svp, srec, o0, o1, lane, A, D, Cc, cf, sc, rsj, nst);
+            } else {
+              papg_clean<NN, false, false>(sv, svp, srec, o0, o1, lane, A, D, Cc, cf, sc, rsj, nst);
+            }
+          } else {
+            const int nr = min(kTR, nrows - st8 * kTR);
+            const long long grow0 = base + (long long)st8 * kTR;
+            if (unit_scale)
+              papg_masked<NN, true, false>(sv, svp, srec, gout, a.ld, gcol0, grow0, nr, a.N, a.nbar,
+                                           lane, A, D, Cc, cf, sc, rsj, nst);
+            else
+              papg_masked<NN, false, false>(sv, svp, srec, gout, a.ld, gcol0, grow0, nr, a.N, a.nbar,
+                                            lane, A, D, Cc, cf, sc, rsj, nst);
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+        double rsum = 0.0;  // row sums, as in the generic loop below
+        if (hot_stage) {
+          const bool b2 = (lane & 4) != 0;
+          const double send = b2 ? rsj[0] : rsj[1];
+          rsum = b2 ? rsj[1] : rsj[0];
+          rsum += __shfl_xor_sync(0xffffffffu, send, 4);
+          rsum += __shfl_xor_sync(0xffffffffu, rsum, 8);
+          rsum += __shfl_xor_sync(0xffffffffu, rsum, 16);
+        }
+        double* ra = rowacc + (flushes & 1) * kCW * kWinM + warp * kWinM;
+        if (lane < 8) ra[win + 2 * (lane & 3) + ((lane >> 2) & 1)] = rsum;
+        win += kTR;
+        if (win == kWinM || st8 == nstage - 1) {
+          asm volatile("bar.sync 1, %0;" ::"r"(kCW * 32) : "memory");
+          const int valid_rows = min(win, nrows - win_base);
+          const int wr = warp * 32 + lane;
+          if (warp < kWinM / 32 && wr < valid_rows) {
+            const double* rb = rowacc + (flushes & 1) * kCW * kWinM;
+            double u = 0.0;
+#pragma unroll
+            for (int w = 0; w < kCW; ++w) u += rb[w * kWinM + wr];
+            a.rowpart[(long long)t * a.R + rlo + win_base + wr] = u;
+          }
+          win_base += win;
+          win = 0;
+          ++flushes;
+        }
+      }
+    } else {
+  int win = 0;
+      long long win_base = rlo;
+      for (long long r = rlo; r < rhi; r += kTR, ++i) {
       const int s = i % kNS;
       mbar_wait(&full[s], (uint32_t)((i / kNS) & 1));
       const int nr = (int)min((long long)kTR, rhi - r);
@@ -364,6 +536,8 @@ __global__ void __launch_bounds__(mma_threads<NN>(), mma_ctas<NN>()) sweep_mma_k
         const double* svp = st + kTR * kTCP + warp * kW;
         const double* srec = st + 2 * kTR * kTCP;
         double* gout = Vp + r * a.ld + gcol0;
+        double* o0 = gout + (long long)(2 * q) * a.ld + c8;
+        double* o1 = o0 + a.ld;
         const long long grow0 = a.r0 + r;
         // warp-uniform: no diagonal in this 8-row block of the warp's columns, full
         // stage, no pad column
@@ -371,17 +545,29 @@ __global__ void __launch_bounds__(mma_threads<NN>(), mma_ctas<NN>()) sweep_mma_k
                            blocks_disjoint<BLK>(grow0, kTR, gcol0, kW, a.nbar);
         if (MODE == kModePapg) {
           if (clean) {
-            hot_stage = unit_scale
-                ? papg_stage<NN, false, true, BLK>(sv, svp, srec, gout, a.ld, gcol0, grow0, nr, a.N, a.nbar,
-                                                   lane, A, D, Cc, cf, sc, rsj, nst)
-                : papg_stage<NN, false, false, BLK>(sv, svp, srec, gout, a.ld, gcol0, grow0, nr, a.N,
-                                                    a.nbar, lane, A, D, Cc, cf, sc, rsj, nst);
+            // per-warp adaptive cold test: a tested stage that finds a cold tile
+            // keeps the test on for the next 8 stages; otherwise every 8th stage
+            // probes and the others run without any test
+            const bool test = probe > 0 || (pstage & 7) == 0;
+            ++pstage;
+            if (test) {
+              const int cold = unit_scale
+                  ? papg_clean<NN, true, true>(sv, svp, srec, o0, o1, lane, A, D, Cc, cf, sc, rsj, nst)
+                  : papg_clean<NN, false, true>(sv, svp, srec, o0, o1, lane, A, D, Cc, cf, sc, rsj, nst);
+              probe = cold ? 8 : (probe > 0 ? probe - 1 : 0);
+              hot_stage = cold < kCT;
+            } else if (unit_scale) {
+              papg_clean<NN, true, false>(sv, svp, srec, o0, o1, lane, A, D, Cc, cf, sc, rsj, nst);
+            } else {
+              papg_clean<NN, false, false>(sv, svp, srec, o0, o1, lane, A, D, Cc, cf, sc, rsj, nst);
+            }
           } else {
-            hot_stage = unit_scale
-                ? papg_stage<NN, true, true, BLK>(sv, svp, srec, gout, a.ld, gcol0, grow0, nr, a.N, a.nbar,
-                                                  lane, A, D, Cc, cf, sc, rsj, nst)
-                : papg_stage<NN, true, false, BLK>(sv, svp, srec, gout, a.ld, gcol0, grow0, nr, a.N,
-                                                   a.nbar, lane, A, D, Cc, cf, sc, rsj, nst);
+            if (unit_scale)
+              papg_masked<NN, true, BLK>(sv, svp, srec, gout, a.ld, gcol0, grow0, nr, a.N, a.nbar,
+                                         lane, A, D, Cc, cf, sc, rsj, nst);
+            else
+              papg_masked<NN, false, BLK>(sv, svp, srec, gout, a.ld, gcol0, grow0, nr, a.N, a.nbar,
+                                          lane, A, D, Cc, cf, sc, rsj, nst);
           }
         } else if (clean) {
           mma_stage<NN, MODE, false, BLK>(sv, srec, gout, a.ld, gcol0, grow0, nr, a.N, a.nbar, lane, A, D,
@@ -393,21 +579,21 @@ __global__ void __launch_bounds__(mma_threads<NN>(), mma_ctas<NN>()) sweep_mma_k
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
-      // row sums over the warp's 32 columns: lanes sharing q hold the same rows
-      // (a cold stage's are exact zeros already)
+      // row sums over the warp's columns: lanes sharing q hold the same rows
+      // 2q, 2q+1; the first exchange leaves each lane one of the two (row 2q +
+      // bit 2 of the lane), then two butterflies; lane b*4 + q ends with row
+      // 2q + b (a cold stage's sums are exact zeros already)
+      double rsum = 0.0;
       if (hot_stage) {
-#pragma unroll
-        for (int j = 0; j < 2; ++j) {
-          rsj[j] += __shfl_xor_sync(0xffffffffu, rsj[j], 4);
-          rsj[j] += __shfl_xor_sync(0xffffffffu, rsj[j], 8);
-          rsj[j] += __shfl_xor_sync(0xffffffffu, rsj[j], 16);
-        }
+        const bool b2 = (lane & 4) != 0;
+        const double send = b2 ? rsj[0] : rsj[1];
+        rsum = b2 ? rsj[1] : rsj[0];
+        rsum += __shfl_xor_sync(0xffffffffu, send, 4);
+        rsum += __shfl_xor_sync(0xffffffffu, rsum, 8);
+        rsum += __shfl_xor_sync(0xffffffffu, rsum, 16);
       }
       double* ra = rowacc + (flushes & 1) * kCW * kWinM + warp * kWinM;
-      if (c8 == 0) {
-        ra[win + 2 * q] = rsj[0];
-        ra[win + 2 * q + 1] = rsj[1];
-      }
+      if (lane < 8) ra[win + 2 * (lane & 3) + ((lane >> 2) & 1)] = rsum;
       win += kTR;
       if (win == kWinM || r + kTR >= rhi) {
         // fixed-order sum over the CTA's warps into the tile's row-sum slice
@@ -426,6 +612,7 @@ __global__ void __launch_bounds__(mma_threads<NN>(), mma_ctas<NN>()) sweep_mma_k
         win = 0;
         ++flushes;
       }
+    }
     }
     if (active) {  // column partials: thread holds (feature fb*8+c8, cols 2q+{0,1})
       const long long slot = (long long)blockIdx.x * a.maxspan + (t - t_first);

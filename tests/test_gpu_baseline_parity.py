@@ -59,11 +59,15 @@ def need(host_gb=0.0, dev_gb=0.0):
     if host_gb and host_bytes_free() < host_gb * 1e9:
         pytest.skip(f"needs {host_gb:.0f} GB of host memory (MemAvailable rule, BASELINE.md section 3)")
     if dev_gb:
-        import torch
+        import subprocess  # (no torch here: it must not load a second NCCL into this process)
 
-        free, _ = torch.cuda.mem_get_info(0)
-        if free < dev_gb * 1e9:
-            pytest.skip(f"needs {dev_gb:.0f} GB of free device memory")
+        # total, not free: this process's memory pool may still hold an earlier
+        # test's buffers, which the library returns to the device on demand
+        out = subprocess.run(["nvidia-smi", "--query-gpu=memory.total", "--format=csv,noheader,nounits",
+                              "-i", "0"], capture_output=True, text=True).stdout
+        total = float(out.split()[0]) * 2**20 if out.strip() else 0.0
+        if total < dev_gb * 1e9:
+            pytest.skip(f"needs a device with {dev_gb:.0f} GB")
 
 
 def instance(oracle, cfg):

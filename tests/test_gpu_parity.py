@@ -268,6 +268,43 @@ def test_row_sharded_emulation_on_one_gpu(oracle):
     assert rel(res[0][1], o.y) <= TOL_Y and np.array_equal(res[0][1], res[1][1])
 
 
+def test_sharded_time_budget_is_rank_consistent(oracle):
+    """Shards whose clocks disagree (the second begins 0.15 s after the first)
+    still stop on the same iteration for the time budget: every rank tests the
+    budget against the clock slot of the summed payload, which carries the
+    elapsed time of the shard owning row 0 (papg.cpp:233-236). A rank that
+    stopped on its own clock would leave the others blocked in the next
+    allreduce."""
+    import time
+
+    X, ys = instance(oracle, "maxaffine-uniform", 300, 5, 0.1, 3, 10)
+    N, cut = X.shape[0], 140
+    cfg = crb.PapgConfig(max_iters=10**6, gap_norm_tol=-1.0, infeas_norm_tol=-1.0, sigma_C=50.0,
+                         max_seconds=0.4)
+    shards = [crb.DualSolver(X, ys, row_begin=0, row_end=cut),
+              crb.DualSolver(X, ys, row_begin=cut, row_end=N)]
+    try:
+        shards[0].begin(cfg)
+        time.sleep(0.15)
+        shards[1].begin(cfg)
+        for it in range(100000):
+            for d in shards:
+                d.iter_local()
+            total = shards[0].exchange_get() + shards[1].exchange_get()
+            for d in shards:
+                d.exchange_put(total)
+            stops = [d.iter_finish() for d in shards]
+            assert stops[0] == stops[1], it
+            if stops[0]:
+                break
+        res = [d.finish()[0] for d in shards]
+    finally:
+        for d in shards:
+            d.close()
+    assert res[0].iters == res[1].iters
+    assert res[0].reason == res[1].reason == 2  # time budget
+
+
 def test_nonfinite_gradient_raises():
     rng = np.random.default_rng(1)
     X = rng.uniform(-1, 1, size=(50, 3))
