@@ -40,6 +40,13 @@ CONFIGS = {  # BASELINE.json configs
     "cfg4": dict(kind="sqnorm-uniform", N=50000, n=10, noise=0.2, pieces=0),
     "cfg5": dict(kind="maxaffine-uniform", N=100000, n=5, noise=0.1, pieces=10),
 }
+# sigma_max(C) of each seeded instance (seed 1), for the CPU legs: the device power loop's
+# value (profiles/r1n_bench_cfg*.json), which is parity-pinned to the oracle's literal power
+# iteration (same step count, sigma within 1e-10: tests/test_gpu_parity.py). The oracle's own
+# power iteration is two O(N^2 n) passes per step, too long to run inside a bench.
+SIGMA_C = {"cfg1": 75.04526292327877, "cfg2": 289.16619141812674, "cfg3": 532.8884553986682,
+           "cfg4": 664.0047049267016, "cfg5": 781.778824412929}
+CPU_SAMPLE_S = 30.0  # bound on one CPU sample's work (seconds)
 
 
 def parse():
@@ -150,26 +157,45 @@ def cpu_feasible(cfg):
     return need <= 0.8 * avail, need, avail
 
 
-def cpu_oracle_rate(cfg, threads, k_lo=1, k_hi=4):
-    """Oracle (CPU restatement of papg.cpp) per-iteration rate on the config:
-    difference of two runs (k_lo, k_hi iterations) removes setup and the final
-    re-solve. Returns (pair-updates/s, seconds of CPU work, sample text)."""
+def cpu_instance(cfg):
     from oracle import oracle as O
 
     X, y = O.gen_instance(cfg["kind"], cfg["N"], cfg["n"], cfg["noise"], 1, cfg["pieces"])
-    p = O.prepare(X, y)
-    sigma = 300.0  # step size does not change the cost of an iteration
-    kw = dict(sigma_C=sigma, gap_norm_tol=-1.0, infeas_norm_tol=-1.0, threads=threads,
-              record_history=False, want_theta=False)
+    return O, X, O.prepare(X, y)
+
+
+def cpu_oracle_rate(name, cfg, threads, warm, steps, inst=None):
+    """Oracle (CPU restatement of papg.cpp) per-iteration rate on the config: one run of
+    warm + steps iterations with sigma_C injected; the timed span is the history's wall
+    clock (papg.cpp:220 wall_time_s) from the end of iteration `warm` to the end of
+    iteration warm + steps, so setup, warm-up and the final re-solve are outside it.
+    Returns (pair-updates/s, seconds of CPU work, sample text, seconds per iteration)."""
+    O, X, p = inst or cpu_instance(cfg)
     t0 = time.perf_counter()
-    a = O.papg(X, p.ys, max_iters=k_lo, **kw).wall_seconds
-    b = O.papg(X, p.ys, max_iters=k_hi, **kw).wall_seconds
+    r = O.papg(X, p.ys, max_iters=warm + steps, sigma_C=SIGMA_C[name], gap_norm_tol=-1.0,
+               infeas_norm_tol=-1.0, threads=threads, record_history=True, want_theta=False)
     spent = time.perf_counter() - t0
-    per_iter = max(b - a, 1e-9) / (k_hi - k_lo)
+    h = r.history
+    t_hi = h[warm + steps - 1, 7]
+    t_lo = h[warm - 1, 7] if warm > 0 else 0.0
+    per_iter = max(t_hi - t_lo, 1e-9) / steps
     N = cfg["N"]
-    sample = (f"{cfg['kind']} N={N} n={cfg['n']}: {k_hi - k_lo} dual iterations "
-              f"(runs of {k_lo} and {k_hi}), {threads} thread(s), {per_iter:.3f} s/iteration")
-    return N * N / per_iter, spent, sample
+    sample = (f"{cfg['kind']} N={N} n={cfg['n']}: dual iterations {warm + 1}..{warm + steps} "
+              f"of one oracle run (history wall clock), {threads} thread(s), "
+              f"{per_iter:.3f} s/iteration")
+    return N * N / per_iter, spent, sample, per_iter
+
+
+def cpu_time_to_tolerance(name, cfg, threads, inst=None):
+    """Oracle solve of the config to its tolerance (cfg 2: |gap_norm| <= 1e-4, infeas_norm
+    <= 0.1), sigma_C injected: measured, not extrapolated."""
+    O, X, p = inst or cpu_instance(cfg)
+    r = O.papg(X, p.ys, sigma_C=SIGMA_C[name], gap_norm_tol=1e-4, infeas_norm_tol=0.1,
+               threads=threads, record_history=False, want_theta=False)
+    return {"seconds": r.wall_seconds, "iterations": r.iters, "reason": r.reason,
+            "threads": threads, "sigma_C": SIGMA_C[name],
+            "includes": "oracle papg loop from zero start to the tolerance and the final re-solve "
+                        "(sigma_C injected, not estimated)"}
 
 
 def run_reference(args):
@@ -184,17 +210,30 @@ def run_reference(args):
                           f"CPU restatement needs {need / 1e9:.0f} GB (4 N^2 doubles) > 0.8 x "
                           f"MemAvailable {avail / 1e9:.0f} GB (BASELINE.md feasibility rule)"}))
         return 0
-    k_hi = 1 + max(1, min(args.steps, 4))
-    rate, spent, sample = cpu_oracle_rate(cfg, threads, 1, k_hi)
+    W, K = max(args.warmup, 1), max(args.steps, 1)
+    inst = cpu_instance(cfg)
+    # bound the run to a few minutes: estimate the per-iteration time from one iteration
+    # at the configs whose iteration is long (cfg 3, 4); cfg 1 and 2 run W + K as asked
+    note = ""
+    if cfg["N"] > 10000:
+        _, _, _, est = cpu_oracle_rate(args.config, cfg, threads, 0, 1, inst)
+        budget = 180.0
+        if (W + K) * est > budget:
+            K0, W0 = K, W
+            W = 1
+            K = max(1, int(budget / est) - W)
+            note = f"; steps {K0}/warmup {W0} reduced to {K}/{W} to bound the run to ~{budget:.0f} s"
+    rate, spent, sample, per = cpu_oracle_rate(args.config, cfg, threads, W, K, inst)
     line = {
         "impl": "reference", "metric": "pair-constraint updates/s", "value": rate,
-        "unit": "pair-updates/s", "n_gpus": args.gpus, "steps": k_hi - 1, "warmup": 1,
-        "ms_per_step": cfg["N"] ** 2 / rate * 1e3, "higher_is_better": True,
+        "unit": "pair-updates/s", "n_gpus": args.gpus, "steps": K, "warmup": W,
+        "ms_per_step": per * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"{args.config}: {cfg['kind']} N={cfg['N']} n={cfg['n']}",
-                   "N": cfg["N"], "n": cfg["n"], "pairs_per_step": cfg["N"] ** 2},
+                   "N": cfg["N"], "n": cfg["n"], "pairs_per_step": cfg["N"] ** 2,
+                   "sigma_C": SIGMA_C[args.config]},
         "cpu_baseline": {"value": rate, "unit": "pair-updates/s", "cores": threads,
-                         "kind": "port", "sample": sample},
+                         "kind": "port", "sample": sample + note},
         "e2e": {"value": rate, "unit": "pair-updates/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
         "note": "oracle/cvxreg_oracle.c (CPU restatement of papg.cpp:136-283, OpenMP rows); "
@@ -202,6 +241,36 @@ def run_reference(args):
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+def device_rate(crb, name, device, W, K):
+    """Iterations W+1 .. W+K of one config on one GPU: pair-updates/s (CUDA events on the
+    solver stream) and the sweep's HBM fraction on the bytes it moved."""
+    import torch
+
+    c = CONFIGS[name]
+    N, n = c["N"], c["n"]
+    data = crb.gen_instance(crb.GeneratorSpec(c["kind"], n, N, c["noise"], 1, c["pieces"]))
+    prep = crb.prepare_problem(data)
+    with crb.DualSolver(prep.data.xs, prep.data.ys, device=device) as s:
+        sigma, sig_iters, _ = s.sigma_C()
+        s.begin(crb.PapgConfig(max_iters=W + K + 4, gap_norm_tol=-1.0, infeas_norm_tol=-1.0,
+                               sigma_C=sigma, device=device))
+        s.iterate(W)
+        torch.cuda.synchronize()
+        s.sweep_store_count(reset=True)
+        done, stopped = s.iterate(K)
+        torch.cuda.synchronize()
+        dev_s, launches, sweep_s = s.last_timing()
+        stores = s.sweep_store_count()
+    peaks, _ = measured_peaks()
+    moved = READ_BYTES_PER_PAIR * N * N + 8.0 * stores / K
+    return {"workload": f"{name}: {c['kind']} N={N} n={n}", "iterations": f"{W + 1}..{W + K}",
+            "value": N * N * K / dev_s, "unit": "pair-updates/s", "ms_per_step": dev_s / K * 1e3,
+            "sweep_ms": sweep_s / K * 1e3,
+            "roofline_frac": moved / (sweep_s / K) / 1e9 / peaks["hbm_gbs"],
+            "model_24B_per_pair_frac": 24.0 * N * N / (sweep_s / K) / 1e9 / peaks["hbm_gbs"],
+            "sigma_C": sigma, "sigma_power_steps": sig_iters, "gpu_launches": launches}
 
 
 def run_ours(args):
@@ -338,6 +407,11 @@ def run_ours(args):
                 "iterations": tr.report.iters, "reason": tr.report.reason.name,
                 "sigma_seconds": tr.sigma_seconds, "sigma_power_steps": tr.sigma_iters,
                 "loop_seconds": tr.loop_seconds, "gap_norm_tol": 1e-4, "infeas_norm_tol": 0.1}
+        if world == 1 and args.config == "cfg2":
+            # per-iteration rates of the other single-GPU configs at a
+            # fixed k, measured by the driver in the same run (early, dense iterations)
+            extras["other_configs"] = {c: device_rate(crb, c, local, 5, 10)
+                                       for c in ("cfg3", "cfg4")}
 
     cpu = None
     ok, need, avail = cpu_feasible(cfg)
@@ -347,12 +421,22 @@ def run_ours(args):
                          f"{avail / 1e9:.0f} GB"}
     if rank == 0 and world == 1 and not args.no_cpu_baseline and ok:
         threads = os.cpu_count() or 1
-        rate, spent, sample = cpu_oracle_rate(cfg, threads)
+        inst = cpu_instance(cfg)
+        rate, spent, sample, per = cpu_oracle_rate(args.config, cfg, threads, 1, 3, inst)
         cpu = {"value": rate, "unit": "pair-updates/s", "cores": threads, "kind": "port",
                "sample": sample}
+        # the 1-thread rate beside the all-core one (the reference's
+        # operators.cpp:128-180 are single-threaded); one iteration when it fits the bound
+        est1 = per * threads
+        if 2 * est1 <= CPU_SAMPLE_S or args.config in ("cfg1", "cfg2"):
+            r1, _, s1, _ = cpu_oracle_rate(args.config, cfg, 1, 1, 1, inst)
+            extras["cpu_baseline_1thread"] = {"value": r1, "unit": "pair-updates/s", "cores": 1,
+                                              "kind": "port", "sample": s1}
         if "time_to_tolerance" in extras:
-            extras["time_to_tolerance"]["cpu_port_iterations_only_s"] = (
-                extras["time_to_tolerance"]["iterations"] * N * N / rate)
+            # measured oracle solve to the same tolerance on all host threads
+            extras["time_to_tolerance"]["cpu"] = cpu_time_to_tolerance(args.config, cfg, threads,
+                                                                       inst)
+        del inst
 
     if rank == 0:
         line = {
@@ -536,7 +620,7 @@ def run_general(args, impl):
         X, y = O.gen_instance(cfg["kind"], N, n, cfg["noise"], 1, cfg["pieces"])
         p = O.prepare(X, y)
         threads = os.cpu_count() or 1
-        sig = 300.0  # the step size does not change the cost of an iteration
+        sig = SIGMA_C.get(args.config, 300.0) if K == N else 300.0  # cost does not depend on it
         kw = dict(inner=GEN_INNER, sigma_C=sig, gap_norm_tol=-1.0, infeas_norm_tol=-1.0,
                   record_history=False, inner_threads=threads)
         a = O.papg_k(X, p.ys, K, p.feas_y, p.feas_xi, max_iters=1, **kw)

@@ -168,11 +168,17 @@ cr_status cr_get_rows_window(cr_handle *h, int64_t row_begin, int64_t row_end, d
    launches it issued (for bench.py) */
 cr_status cr_last_timing(const cr_handle *h, double *seconds, int64_t *launches,
                          double *sweep_seconds);
+/* Durations (s) of the sweep launches the last cr_papg_iterate call bracketed
+   with CUDA events (every launch of a call of at most 64 iterations, else every
+   8th; CRB_SWEEP_EVENTS=k overrides), in launch order: up to cap into out,
+   *count = how many there were. */
+cr_status cr_last_sweep_times(const cr_handle *h, double *out, int64_t cap, int64_t *count);
 /* sweep kernel variant chosen for this handle: 0 = CUDA-core DFMA,
    1 = FP64 tensor-core DMMA (override with CRB_SWEEP=dfma|mma) */
 int32_t cr_sweep_variant(const cr_handle *h);
-/* Multipliers written by the P-APG sweeps since the last reset (DMMA sweep;
-   unchanged values are not rewritten), optionally resetting the counter. */
+/* Multipliers written by the P-APG sweeps since the last reset (DMMA sweep:
+   a 32-byte sector holding no changed multiplier is not rewritten, a sector
+   with a change is written whole), optionally resetting the counter. */
 cr_status cr_sweep_store_count(cr_handle *h, uint64_t *count, int32_t reset);
 /* Time k sweep-kernel launches alone on the handle's stream with CUDA events
    (the dominant kernel in isolation, for the roofline). */

@@ -913,7 +913,9 @@ cr_status cr_papg_iterate(cr_handle* h, int64_t max_steps, int64_t* done, int32_
   // k-th, 0: none); the reported sweep seconds are the sampled mean times the
   // iterations run. Event records between the kernels cost ~6 us per iteration
   // (2 % at cfg 2, measured), so not every sweep is bracketed.
-  int every = 8;
+  // A call of at most 64 iterations brackets every sweep (a short call's early
+  // iterations differ too much for a sample).
+  int every = max_steps <= 64 ? 1 : 8;
   if (const char* ev = std::getenv("CRB_SWEEP_EVENTS")) every = std::max(0, std::atoi(ev));
   // direct launches: poll the device state every `per_unit` iterations (one D2H copy
   // + event per unit); CRB_POLL_UNIT overrides (measurement knob)
@@ -976,10 +978,12 @@ cr_status cr_papg_iterate(cr_handle* h, int64_t max_steps, int64_t* done, int32_
   CUDA_TRY(cudaEventElapsedTime(&ms, h->ev_start, h->ev_end));
   h->last_seconds = units > 0 ? ms * 1e-3 : 0.0;
   double sw = 0;
+  h->last_sweep_times.clear();
   for (int64_t i = 0; i < timed_pairs; ++i) {
     float m = 0;
     CUDA_TRY(cudaEventElapsedTime(&m, h->ev_sweep[2 * i], h->ev_sweep[2 * i + 1]));
     sw += m * 1e-3;
+    h->last_sweep_times.push_back(m * 1e-3);
   }
   {
     const int64_t ran = std::min<int64_t>(enq_iters, max_steps);
@@ -1196,6 +1200,15 @@ cr_status cr_last_timing(const cr_handle* h, double* seconds, int64_t* launches,
   if (seconds) *seconds = h->last_seconds;
   if (launches) *launches = h->last_launches;
   if (sweep_seconds) *sweep_seconds = h->last_sweep_seconds;
+  return CR_OK;
+}
+
+cr_status cr_last_sweep_times(const cr_handle* h, double* out, int64_t cap, int64_t* count) {
+  if (!h || cap < 0) return CR_EINVAL;
+  const int64_t k = (int64_t)h->last_sweep_times.size();
+  if (count) *count = k;
+  if (out)
+    for (int64_t i = 0; i < std::min(k, cap); ++i) out[i] = h->last_sweep_times[i];
   return CR_OK;
 }
 

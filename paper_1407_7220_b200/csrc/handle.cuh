@@ -132,6 +132,7 @@ struct cr_handle {
   std::thread sigma_prep;
   std::vector<double> sigma_start;
   double last_seconds = 0, last_sweep_seconds = 0;
+  std::vector<double> last_sweep_times;  // per bracketed sweep launch of the last call (s)
   int64_t last_launches = 0;
   // masked dual store (sweep_sparse.cu): live-bit words of V[0], V[1]
   uint32_t* M[2] = {nullptr, nullptr};

@@ -17,10 +17,16 @@ namespace crb {
 #endif
 template <int NN>
 __host__ __device__ constexpr bool mma_wide() { return NN > CRB_WIDE_ABOVE; }
+#ifndef CRB_CW  // geometry overrides of the wide layout (measurement builds)
+#define CRB_CW 15
+#endif
+#ifndef CRB_CT
+#define CRB_CT 2
+#endif
 template <int NN>
-__host__ __device__ constexpr int mma_cw() { return mma_wide<NN>() ? 15 : 7; }  // consumer warps
+__host__ __device__ constexpr int mma_cw() { return mma_wide<NN>() ? CRB_CW : 7; }  // consumer warps
 template <int NN>
-__host__ __device__ constexpr int mma_ct() { return mma_wide<NN>() ? 2 : 4; }   // 8-col tiles / warp
+__host__ __device__ constexpr int mma_ct() { return mma_wide<NN>() ? CRB_CT : 4; }   // 8-col tiles / warp
 template <int NN>
 __host__ __device__ constexpr int mma_threads() { return (mma_cw<NN>() + 1) * 32; }
 // kW columns per warp, kTC per CTA tile, kTCP smem row pitch (+16 B: conflict-free)
@@ -42,8 +48,13 @@ template <int NN>
 __host__ __device__ constexpr int mma_ctas() {
   return CRB_MMA_CTAS_PER_SM > 0 ? CRB_MMA_CTAS_PER_SM : (mma_wide<NN>() ? 1 : 2);
 }
+#ifndef CRB_MMA_NS
+#define CRB_MMA_NS 0  // 0: per geometry (mma_ns)
+#endif
 template <int NN>
-__host__ __device__ constexpr int mma_ns() { return mma_ctas<NN>() == 2 ? 3 : 4; }  // stages
+__host__ __device__ constexpr int mma_ns() {  // ring stages
+  return CRB_MMA_NS > 0 ? CRB_MMA_NS : (mma_ctas<NN>() == 2 ? 3 : 4);
+}
 constexpr int kNS = 4;  // ring depth of the other users of this header (sweep_sparse.cu)
 constexpr int kWin = 32;               // row-sum window (rows), masked-store sweep
 #ifndef CRB_MMA_WIN
@@ -62,6 +73,30 @@ template <int NN>
 __host__ __device__ constexpr int ksteps() { return split_yc<NN>() ? (NN + 3) / 4 : (NN + 5) / 4; }
 template <int NN>
 __host__ __device__ constexpr int fblocks() { return ((NN + 1) + 7) / 8; }
+// P-APG aggregation split: the DMMA aggregation runs whole 8-feature blocks of
+// [X 1]; a short remainder of R = (n+1) mod 8 features (the last x columns and
+// the column sum) runs on DFMA/DADD in the lanes that hold v instead of a
+// padded DMMA block (2R fp64 warp instructions per tile, 4R pipe cycles, vs 32
+// for the block's two DMMAs). n = 10: 1 block + x8, x9 and the column sum.
+// Remainders above 3 features (n = 5, 20) keep the padded block: the extra
+// per-lane accumulators spill at 128 registers.
+#ifndef CRB_AGG_REM_MAX
+#define CRB_AGG_REM_MAX 0
+#endif
+template <int NN>
+__host__ __device__ constexpr bool agg_split() {
+  return (NN + 1) % 8 > 0 && (NN + 1) % 8 <= CRB_AGG_REM_MAX;
+}
+// DMMA feature blocks of the P-APG aggregation
+template <int NN>
+__host__ __device__ constexpr int agg_fbd() { return agg_split<NN>() ? (NN + 1) / 8 : fblocks<NN>(); }
+// x features on DFMA, and those plus the column sum
+template <int NN>
+__host__ __device__ constexpr int agg_rx() { return agg_split<NN>() ? NN - 8 * ((NN + 1) / 8) : 0; }
+template <int NN>
+__host__ __device__ constexpr int agg_re() { return agg_split<NN>() ? agg_rx<NN>() + 1 : 0; }
+__host__ __device__ constexpr int max1(int x) { return x > 0 ? x : 1; }
+
 template <int NN>
 __host__ __device__ constexpr int stage_doubles() {
   return 2 * kTR * (mma_cw<NN>() * 8 * mma_ct<NN>() + 2) + kTR * rec_pitch(NN);

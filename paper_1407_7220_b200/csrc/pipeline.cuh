@@ -37,6 +37,34 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+// the same on 32-bit shared addresses (precomputed once per kernel)
+__device__ __forceinline__ void mbar_wait_u32(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+#ifndef CRB_ARRIVE_RELAXED
+#define CRB_ARRIVE_RELAXED 1
+#endif
+// Consumer release of a ring slot. The default .release semantics make the
+// arrive wait until the thread's earlier global stores are performed, which
+// puts a store round trip on every stage of a sweep that writes multipliers;
+// the slot only needs the warp's shared-memory reads of the stage complete
+// (WAR against the next TMA fill), and those are: every loaded value has been
+// consumed before the __syncwarp that precedes the arrive. So .relaxed.
+__device__ __forceinline__ void mbar_arrive_u32(uint32_t bar) {
+#if CRB_ARRIVE_RELAXED
+  asm volatile("mbarrier.arrive.relaxed.cta.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+#else
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+#endif
+}
 // wait with a back-off: for a warp that is otherwise idle (a producer ahead of
 // its consumers) so its spin does not take issue slots from the SM's other warps
 template <int NS = 256>
@@ -95,6 +123,38 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
 }
 
 
+// Sector-granular store for the 8 x 8 MMA fragment layout (lane = 4 c8 + q holds
+// column c8 of the tile's rows 2q, 2q+1): the lanes of one 32-byte sector (4
+// consecutive columns of a row: c8 = 4g .. 4g + 3, lanes q + 16 g + 4 k) store
+// together when any of them changed, so L2 evicts whole sectors -- a partially
+// written sector costs a read-modify-write at the memory controller (measured:
+// cfg 2 iterations 6-25 433 -> 388 us per sweep, iterations 1-5 549 -> 419 us).
+// Unchanged lanes rewrite the value the sector already holds, so the buffer
+// contents are identical. All 32 lanes must call it (ballot); `valid` = false
+// (rows past a partial stage: the whole sector row) never stores. `count` counts
+// the multipliers written (8 bytes each).
+#ifndef CRB_STORE_GRAN
+#define CRB_STORE_GRAN 32  // bytes: 8 = per multiplier, 32 = sector, 64 = tile row
+#endif
+__device__ __forceinline__ void store_changed_sector(double* p, double v, double old, bool valid,
+                                                     int lane, int& count) {
+  const bool ch = valid && __double_as_longlong(v) != __double_as_longlong(old);
+  if (CRB_STORE_GRAN == 8) {
+    if (ch) {
+      st_stream(p, v);
+      ++count;
+    }
+    return;
+  }
+  const unsigned m = __ballot_sync(0xffffffffu, ch);
+  const unsigned grp = CRB_STORE_GRAN == 64 ? (m >> (lane & 3)) & 0x11111111u
+                                            : (m >> ((lane & 3) | (lane & 16))) & 0x1111u;
+  if (grp) {
+    st_stream(p, v);
+    ++count;
+  }
+}
+
 // max(u, 0) and min(r, 0) on the sign bit: three integer ops, no FSEL chains
 __device__ __forceinline__ double keep_if_nonneg(double u) {
   const int hi = __double2hiint(u), lo = __double2loint(u);
@@ -114,18 +174,43 @@ __device__ __forceinline__ void acc_neg_sq(double& acc, double r) {
   const double m = __hiloint2double(hi & (hi >> 31), __double2loint(r));
   acc = fma(m, m, acc);
 }
-// *p = v (streaming) and ++count when v != old (v, old >= +0: numeric != is the
-// bit test), as one predicated store instead of a branch
+// *p = v (streaming) and ++count when v != old, as one predicated store instead
+// of a branch. v, old >= +0 (never -0), so numeric != is the 64-bit pattern test:
+// an integer compare keeps it off the fp64 pipe the DMMAs share
+#ifndef CRB_PROBE_STORE
+#define CRB_PROBE_STORE 0  // measurement probe only: 1 = no stores, 2 = store every v
+#endif
 __device__ __forceinline__ void store_if_changed(double* p, double v, double old, int& count) {
+  if (CRB_PROBE_STORE == 1) return;
+  if (CRB_PROBE_STORE == 2) {
+    st_stream(p, v);
+    return;
+  }
+  if (CRB_PROBE_STORE == 3) {  // same instructions, L2-resident targets (64 KB per 4 MB)
+    const unsigned long long a = (unsigned long long)p;
+    p = (double*)((a & ~((1ull << 22) - 1)) | (a & 0xFFF8ull));
+  }
+  if (CRB_PROBE_STORE == 4) {  // same instructions, default (not streaming) cache policy
+    asm volatile(
+        "{\n"
+        ".reg .pred q;\n"
+        "setp.ne.b64 q, %3, %4;\n"
+        "@q st.global.f64 [%1], %2;\n"
+        "@q add.s32 %0, %0, 1;\n"
+        "}\n"
+        : "+r"(count)
+        : "l"(p), "d"(v), "l"(__double_as_longlong(v)), "l"(__double_as_longlong(old)));
+    return;
+  }
   asm volatile(
       "{\n"
       ".reg .pred q;\n"
-      "setp.neu.f64 q, %2, %3;\n"
+      "setp.ne.b64 q, %3, %4;\n"
       "@q st.global.cs.f64 [%1], %2;\n"
       "@q add.s32 %0, %0, 1;\n"
       "}\n"
       : "+r"(count)
-      : "l"(p), "d"(v), "d"(old));
+      : "l"(p), "d"(v), "l"(__double_as_longlong(v)), "l"(__double_as_longlong(old)));
 }
 
 }  // namespace crb

@@ -21,37 +21,101 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdio>
 
 #include "device.cuh"
 #include "mma_geo.cuh"
 #include "pipeline.cuh"
 
+// producer back-off while a slot drains (ns)
+#ifndef CRB_PROD_SLEEP
+#define CRB_PROD_SLEEP 64
+#endif
+// measurement probe only (wrong results): consumers skip the P-APG stage work,
+// leaving the TMA ring, barriers and row-sum flushes (the memory-side floor)
+#ifndef CRB_PROBE_MEMONLY
+#define CRB_PROBE_MEMONLY 0
+#endif
+#ifndef CRB_PROBE_SKIP  // measurement probe (wrong results): 1 residual, 2 aggregation, 4 sums, 8 row-sum shuffles
+#define CRB_PROBE_SKIP 0
+#endif
+#ifndef CRB_PROBE_TIMING  // measurement probe: clock64 wait accounting, printf from 2 CTAs
+#define CRB_PROBE_TIMING 0
+#endif
+
 namespace crb {
 
 namespace {
 
+// P-APG aggregation of one tile's v (fragment rows 2q, 2q+1 of column c8):
+// the DMMA feature blocks, then the DFMA remainder (agg_split: the last x
+// features and the column sum, accumulated per lane and reduced over q at the
+// end of the segment).
+template <int NN>
+__device__ __forceinline__ void papg_agg(const double (&Ag)[2][max1(agg_fbd<NN>())],
+                                         const double (&xr)[2][max1(agg_rx<NN>())], const double (&v)[2],
+                                         double (&D)[max1(agg_fbd<NN>())][2], double (&E)[max1(agg_re<NN>())]) {
+  constexpr int FBD = agg_fbd<NN>();
+  constexpr int RX = agg_rx<NN>();
+#pragma unroll
+  for (int fb = 0; fb < FBD; ++fb) {
+    dmma(D[fb][0], D[fb][1], Ag[0][fb], v[0]);
+    dmma(D[fb][0], D[fb][1], Ag[1][fb], v[1]);
+  }
+  if constexpr (agg_re<NN>() > 0) {
+#pragma unroll
+    for (int r = 0; r < RX; ++r) E[r] = fma(xr[1][r], v[1], fma(xr[0][r], v[0], E[r]));
+    E[RX] = (E[RX] + v[0]) + v[1];
+  }
+}
+
+// Residual tiles of one stage for one warp: row^T (8 cols x 8 rows) per tile as
+// KS chained k-steps, the kCT tiles' chains interleaved.
+template <int NN>
+__device__ __forceinline__ void stage_residual(const double* __restrict__ srec, int lane,
+                                               const double (&A)[mma_ct<NN>()][ksteps<NN>()],
+                                               double (&d)[mma_ct<NN>()][2]) {
+  constexpr int kCT = mma_ct<NN>();
+  constexpr int KS = ksteps<NN>();
+  constexpr int RQ = rec_pitch(NN);
+  const int q = lane & 3;
+  const int c8 = lane >> 2;
+  double B[KS];  // residual B fragments: X'[row c8][k]
+#pragma unroll
+  for (int ks = 0; ks < KS; ++ks) B[ks] = srec[c8 * RQ + ks * 4 + q];
+#pragma unroll
+  for (int ct = 0; ct < kCT; ++ct) d[ct][0] = d[ct][1] = 0.0;
+#pragma unroll
+  for (int ks = 0; ks < KS; ++ks) {
+#pragma unroll
+    for (int ct = 0; ct < kCT; ++ct) dmma(d[ct][0], d[ct][1], A[ct][ks], B[ks]);
+  }
+}
+
 // Lean P-APG stage for a clean stage (no diagonal in the warp's columns, all 8
 // rows present, no pad column), one warp: the residuals of all kCT tiles first
 // (independent DMMA chains interleaved), then per tile theta2, v, the store of a
-// changed multiplier, the scalar sums and the aggregation MMAs.
+// changed multiplier, the scalar sums and the aggregation.
 // TEST: per-tile cold test on the inputs -- with theta1 = theta1_prev = 0 and
 // row >= 0 everywhere in a tile (late in a solve almost every tile) theta2 = 0
 // and v = 0 = theta1_prev: no store, and every scalar, row-sum and aggregate
 // update adds an exact zero, so the warp skips the tile after one vote; a tile
-// whose v are all zero skips its aggregation MMAs. !TEST: no tests at all (the
+// whose v are all zero skips its aggregation. !TEST: no tests at all (the
 // dense early iterations, where no tile is cold). Both variants evaluate the
 // same expressions for a hot tile, so results are bitwise identical. Returns
 // the number of cold tiles (TEST).
 template <int NN, bool UNIT, bool TEST>
 __device__ __forceinline__ int papg_clean(const double* __restrict__ sv, const double* __restrict__ svp,
                                           const double* __restrict__ srec, double* g0, double* g1,
-                                          int lane, const double (&A)[mma_ct<NN>()][ksteps<NN>()],
-                                          double (&D)[mma_ct<NN>()][fblocks<NN>()][2],
+                                          int lane, const double (&d)[mma_ct<NN>()][2],
+                                          double (&D)[mma_ct<NN>()][max1(agg_fbd<NN>())][2],
+                                          double (&E)[mma_ct<NN>()][max1(agg_re<NN>())],
                                           const double (&Cc)[mma_ct<NN>()], const MCoef& cf, MScal& sc,
                                           double (&rs)[2], int& nst) {
   CRB_GEO(NN)
   constexpr int KS = ksteps<NN>();
-  constexpr int FB = fblocks<NN>();
+  constexpr int FBD = agg_fbd<NN>();
+  constexpr int RX = agg_rx<NN>();
   constexpr int RQ = rec_pitch(NN);
   constexpr bool SPLIT = split_yc<NN>();
   const int q = lane & 3;
@@ -63,25 +127,19 @@ __device__ __forceinline__ int papg_clean(const double* __restrict__ sv, const d
     yr[0] = r0[NN + 1];
     yr[1] = r1[NN + 1];
   }
-  // aggregation A fragments, shared by the stage's tiles: [X 1][row 2q+j][feature fb*8 + c8]
-  double Ag[2][FB];
+  // aggregation A fragments ([X 1][row 2q+j][feature fb*8 + c8]) and the DFMA
+  // remainder's x of rows 2q, 2q+1, shared by the stage's tiles
+  double Ag[2][max1(FBD)];
+  double xr[2][max1(RX)];
 #pragma unroll
-  for (int fb = 0; fb < FB; ++fb) {
+  for (int fb = 0; fb < FBD; ++fb) {
     Ag[0][fb] = r0[fb * 8 + c8];
     Ag[1][fb] = r1[fb * 8 + c8];
   }
-  double d[kCT][2];
-  {
-    double B[KS];  // residual B fragments: X'[row c8][k]
 #pragma unroll
-    for (int ks = 0; ks < KS; ++ks) B[ks] = srec[c8 * RQ + ks * 4 + q];
-#pragma unroll
-    for (int ct = 0; ct < kCT; ++ct) d[ct][0] = d[ct][1] = 0.0;
-#pragma unroll
-    for (int ks = 0; ks < KS; ++ks) {
-#pragma unroll
-      for (int ct = 0; ct < kCT; ++ct) dmma(d[ct][0], d[ct][1], A[ct][ks], B[ks]);
-    }
+  for (int r = 0; r < RX; ++r) {
+    xr[0][r] = r0[8 * FBD + r];
+    xr[1][r] = r1[8 * FBD + r];
   }
   int cold = 0;
   rs[0] = 0.0;
@@ -122,21 +180,137 @@ __device__ __forceinline__ int papg_clean(const double* __restrict__ sv, const d
       v[j] = keep_if_nonneg(fma(-row[j], cf.invL, th2));
       // v goes into the buffer that holds p1 (theta1_prev): an unchanged value
       // needs no store
-      store_if_changed((j ? g1 : g0) + ct * 8, v[j], p1[j], nst);
+      store_changed_sector((j ? g1 : g0) + ct * 8, v[j], p1[j], true, lane, nst);
       sc.vv = fma(v[j], v[j], sc.vv);
       sc.vr = fma(v[j], row[j], sc.vr);
       sc.tr = fma(th2, row[j], sc.tr);
       acc_neg_sq(sc.nn, row[j]);  // min(row, 0)^2
-      rs[j] += v[j];
+      if (!TEST && ct == 0)
+        rs[j] = v[j];  // = 0 + v exactly
+      else
+        rs[j] += v[j];
     }
     // a tile whose v are all zero adds exact zeros to the aggregates
-    if (!TEST || __any_sync(0xffffffffu, v[0] != 0.0 || v[1] != 0.0)) {
+    if (!TEST || __any_sync(0xffffffffu, v[0] != 0.0 || v[1] != 0.0))
+      papg_agg<NN>(Ag, xr, v, D[ct], E[ct]);
+  }
+  return cold;
+}
+
+// Residual of one stage from the lane's B-fragment pointer (lb: X'[row c8][q]).
+template <int NN>
+__device__ __forceinline__ void lean_residual(const double* __restrict__ lb,
+                                              const double (&A)[mma_ct<NN>()][ksteps<NN>()],
+                                              double (&d)[mma_ct<NN>()][2]) {
+  constexpr int kCT = mma_ct<NN>();
+  constexpr int KS = ksteps<NN>();
+  double B[KS];
 #pragma unroll
-      for (int fb = 0; fb < FB; ++fb) {
-        dmma(D[ct][fb][0], D[ct][fb][1], Ag[0][fb], v[0]);
-        dmma(D[ct][fb][0], D[ct][fb][1], Ag[1][fb], v[1]);
+  for (int ks = 0; ks < KS; ++ks) B[ks] = lb[ks * 4];
+#pragma unroll
+  for (int ct = 0; ct < kCT; ++ct) d[ct][0] = d[ct][1] = 0.0;
+  if (CRB_PROBE_SKIP & 1) {  // probe: one DFMA instead of the residual DMMAs
+#pragma unroll
+    for (int ct = 0; ct < kCT; ++ct) {
+      d[ct][0] = A[ct][0] * B[0];
+      d[ct][1] = A[ct][1] * B[0];
+    }
+  } else {
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+#pragma unroll
+      for (int ct = 0; ct < kCT; ++ct) dmma(d[ct][0], d[ct][1], A[ct][ks], B[ks]);
+    }
+  }
+}
+
+// Lean-loop form of papg_clean: the stage's lane-dependent smem addresses come
+// in precomputed (lv: theta1 of row 2q, tile 0, column c8 of the warp; lb: the
+// residual B fragment X'[row c8][q]; lr: the record of row 2q; la: lr + c8), the output rows
+// 2q, 2q+1 are o0, o0 + ld, and the residual is computed here. Same expressions
+// as papg_clean (bitwise-equal results).
+template <int NN, bool UNIT, bool TEST>
+__device__ __forceinline__ int papg_lean(const double* __restrict__ lv, const double* __restrict__ lb,
+                                         const double* __restrict__ lr, const double* __restrict__ la,
+                                         double* o0, long long ld, int lane,
+                                         const double (&A)[mma_ct<NN>()][ksteps<NN>()],
+                                         double (&D)[mma_ct<NN>()][max1(agg_fbd<NN>())][2],
+                                         double (&E)[mma_ct<NN>()][max1(agg_re<NN>())],
+                                         const double (&Cc)[mma_ct<NN>()], const MCoef& cf, MScal& sc,
+                                         double (&rs)[2], int& nst) {
+  CRB_GEO(NN)
+  constexpr int KS = ksteps<NN>();
+  constexpr int FBD = agg_fbd<NN>();
+  constexpr int RX = agg_rx<NN>();
+  constexpr int RQ = rec_pitch(NN);
+  constexpr bool SPLIT = split_yc<NN>();
+  double d[kCT][2];
+  lean_residual<NN>(lb, A, d);
+  double Ag[2][max1(FBD)];
+  double xr[2][max1(RX)];
+#pragma unroll
+  for (int fb = 0; fb < FBD; ++fb) {
+    Ag[0][fb] = la[fb * 8];
+    Ag[1][fb] = la[RQ + fb * 8];
+  }
+#pragma unroll
+  for (int r = 0; r < RX; ++r) {  // x of rows 2q, 2q+1 for the DFMA remainder
+    xr[0][r] = lr[8 * FBD + r];
+    xr[1][r] = lr[RQ + 8 * FBD + r];
+  }
+  double yr[2] = {0.0, 0.0};  // y of rows 2q, 2q+1 (split form)
+  if (SPLIT) {
+    yr[0] = lr[NN + 1];
+    yr[1] = lr[RQ + NN + 1];
+  }
+  int cold = 0;
+  rs[0] = 0.0;
+  rs[1] = 0.0;
+#pragma unroll
+  for (int ct = 0; ct < kCT; ++ct) {
+    double row[2], c1[2], p1[2];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      row[j] = d[ct][j];
+      if (SPLIT) row[j] += yr[j] + Cc[ct];
+      c1[j] = lv[j * kTCP + ct * 8];
+      p1[j] = lv[(kTR + j) * kTCP + ct * 8];
+    }
+    if (TEST) {
+      const unsigned long long bits =
+          (unsigned long long)__double_as_longlong(c1[0]) | (unsigned long long)__double_as_longlong(c1[1]) |
+          (unsigned long long)__double_as_longlong(p1[0]) | (unsigned long long)__double_as_longlong(p1[1]);
+      const bool hot = bits != 0ull || (__double2hiint(row[0]) | __double2hiint(row[1])) < 0;
+      if (!__any_sync(0xffffffffu, hot)) {
+        ++cold;
+        continue;
       }
     }
+    double v[2];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      double th2;
+      if (UNIT) {
+        th2 = fma(cf.beta, c1[j] - p1[j], c1[j]);
+      } else {
+        const double th1 = cf.s_c * c1[j];
+        th2 = fma(cf.beta, th1 - cf.s_p * p1[j], th1);
+      }
+      v[j] = keep_if_nonneg(fma(-row[j], cf.invL, th2));
+      store_changed_sector(o0 + (j ? ld : 0) + ct * 8, v[j], p1[j], true, lane, nst);
+      if (!(CRB_PROBE_SKIP & 4)) {
+        sc.vv = fma(v[j], v[j], sc.vv);
+        sc.vr = fma(v[j], row[j], sc.vr);
+        sc.tr = fma(th2, row[j], sc.tr);
+        acc_neg_sq(sc.nn, row[j]);
+      }
+      if (!TEST && ct == 0)
+        rs[j] = v[j];
+      else
+        rs[j] += v[j];
+    }
+    if (!(CRB_PROBE_SKIP & 2) && (!TEST || __any_sync(0xffffffffu, v[0] != 0.0 || v[1] != 0.0)))
+      papg_agg<NN>(Ag, xr, v, D[ct], E[ct]);
   }
   return cold;
 }
@@ -147,13 +321,15 @@ __device__ __forceinline__ void papg_masked(const double* __restrict__ sv, const
                                             const double* __restrict__ srec, double* gout,
                                             long long ld, long long gcol0, long long grow0, int nr,
                                             long long ncols, long long nbar,
-                                            int lane, const double (&A)[mma_ct<NN>()][ksteps<NN>()],
-                                            double (&D)[mma_ct<NN>()][fblocks<NN>()][2],
+                                            int lane, const double (&d)[mma_ct<NN>()][2],
+                                            double (&D)[mma_ct<NN>()][max1(agg_fbd<NN>())][2],
+                                            double (&E)[mma_ct<NN>()][max1(agg_re<NN>())],
                                             const double (&Cc)[mma_ct<NN>()], const MCoef& cf,
                                             MScal& sc, double (&rs)[2], int& nst) {
   CRB_GEO(NN)
   constexpr int KS = ksteps<NN>();
-  constexpr int FB = fblocks<NN>();
+  constexpr int FBD = agg_fbd<NN>();
+  constexpr int RX = agg_rx<NN>();
   constexpr int RQ = rec_pitch(NN);
   constexpr bool SPLIT = split_yc<NN>();
   const int q = lane & 3;
@@ -163,24 +339,15 @@ __device__ __forceinline__ void papg_masked(const double* __restrict__ sv, const
     yr[0] = srec[(2 * q) * RQ + NN + 1];
     yr[1] = srec[(2 * q + 1) * RQ + NN + 1];
   }
-  double Ag[2][FB];
+  double Ag[2][max1(FBD)];
+  double xr[2][max1(RX)];
 #pragma unroll
-  for (int fb = 0; fb < FB; ++fb) {
-    Ag[0][fb] = (2 * q < nr) ? srec[(2 * q) * RQ + fb * 8 + c8] : 0.0;
-    Ag[1][fb] = (2 * q + 1 < nr) ? srec[(2 * q + 1) * RQ + fb * 8 + c8] : 0.0;
-  }
-  double d[kCT][2];
-  {
-    double B[KS];
+  for (int j = 0; j < 2; ++j) {
+    const bool rv = 2 * q + j < nr;
 #pragma unroll
-    for (int ks = 0; ks < KS; ++ks) B[ks] = srec[c8 * RQ + ks * 4 + q];
+    for (int fb = 0; fb < FBD; ++fb) Ag[j][fb] = rv ? srec[(2 * q + j) * RQ + fb * 8 + c8] : 0.0;
 #pragma unroll
-    for (int ct = 0; ct < kCT; ++ct) d[ct][0] = d[ct][1] = 0.0;
-#pragma unroll
-    for (int ks = 0; ks < KS; ++ks) {
-#pragma unroll
-      for (int ct = 0; ct < kCT; ++ct) dmma(d[ct][0], d[ct][1], A[ct][ks], B[ks]);
-    }
+    for (int r = 0; r < RX; ++r) xr[j][r] = rv ? srec[(2 * q + j) * RQ + 8 * FBD + r] : 0.0;
   }
   double* g0 = gout + (long long)(2 * q) * ld + c8;
   rs[0] = 0.0;
@@ -209,20 +376,14 @@ __device__ __forceinline__ void papg_masked(const double* __restrict__ sv, const
       }
       if (!rv) th2 = 0.0;
       v[j] = keep_if_nonneg(fma(-row, cf.invL, th2));
-      if (rv) store_if_changed(g0 + (long long)j * ld + ct * 8, v[j], p1, nst);
+      store_changed_sector(g0 + (long long)j * ld + ct * 8, v[j], p1, rv, lane, nst);
       sc.vv = fma(v[j], v[j], sc.vv);
       sc.vr = fma(v[j], row, sc.vr);
       sc.tr = fma(th2, row, sc.tr);
       acc_neg_sq(sc.nn, row);
       rs[j] += v[j];
     }
-    if (__any_sync(0xffffffffu, v[0] != 0.0 || v[1] != 0.0)) {
-#pragma unroll
-      for (int fb = 0; fb < FB; ++fb) {
-        dmma(D[ct][fb][0], D[ct][fb][1], Ag[0][fb], v[0]);
-        dmma(D[ct][fb][0], D[ct][fb][1], Ag[1][fb], v[1]);
-      }
-    }
+    if (__any_sync(0xffffffffu, v[0] != 0.0 || v[1] != 0.0)) papg_agg<NN>(Ag, xr, v, D[ct], E[ct]);
   }
 }
 
@@ -349,6 +510,10 @@ __global__ void __launch_bounds__(mma_threads<NN>(), mma_ctas<NN>()) sweep_mma_k
       const uint64_t pol_stream = policy_evict_first();
       const uint64_t pol_keep = policy_evict_last();
       int i = 0;
+#if CRB_PROBE_TIMING
+      const long long pt0 = clock64();
+      long long pw = 0;
+#endif
       for (int t = t_first; t <= t_last; ++t) {
         const long long rlo = max(u0, (long long)t * a.R) - (long long)t * a.R;
         const long long rhi = min(u1, (long long)(t + 1) * a.R) - (long long)t * a.R;
@@ -357,7 +522,13 @@ __global__ void __launch_bounds__(mma_threads<NN>(), mma_ctas<NN>()) sweep_mma_k
         for (long long r = rlo; r < rhi; r += kTR, ++i) {
           const int s = i % kNS;
           // short back-off: the spin otherwise takes ~3 % of the SM's issue slots
-          if (i >= kNS) mbar_wait_sleep<64>(&empty[s], (uint32_t)(((i / kNS) - 1) & 1));
+#if CRB_PROBE_TIMING
+          const long long tp0 = clock64();
+#endif
+          if (i >= kNS) mbar_wait_sleep<CRB_PROD_SLEEP>(&empty[s], (uint32_t)(((i / kNS) - 1) & 1));
+#if CRB_PROBE_TIMING
+          pw += clock64() - tp0;
+#endif
           const int nr = (int)min((long long)kTR, rhi - r);
           double* st = stages + s * SD;
           const uint32_t bytes = (MODE == kModePapg ? 2u * nr * vbytes : 0u) +
@@ -390,11 +561,20 @@ __global__ void __launch_bounds__(mma_threads<NN>(), mma_ctas<NN>()) sweep_mma_k
                    &full[s], pol_keep);
         }
       }
+#if CRB_PROBE_TIMING
+      if ((blockIdx.x == 0 || blockIdx.x == 77) && MODE == kModePapg)
+        printf("probe cta %d producer total %lld wait_empty %lld stages %d\n", (int)blockIdx.x,
+               clock64() - pt0, pw, i);
+#endif
     }
     return;
   }
 
   // ---------------------------------------------------------------- consumers
+#if CRB_PROBE_TIMING
+  const long long p_t0 = clock64();
+  long long p_wait = 0, p_bar = 0;
+#endif
   const int q = lane & 3;
   const int c8 = lane >> 2;
   MCoef cf{1.0, 0.0, 0.0, a.invL, a.cdiv};
@@ -417,7 +597,12 @@ __global__ void __launch_bounds__(mma_threads<NN>(), mma_ctas<NN>()) sweep_mma_k
     const bool active = gcol0 < a.N;
     // residual A fragments: Xi'[col][k] (zero for pad columns -> row = 0 there)
     double A[kCT][KS];
-    double D[kCT][FB][2];
+    // column aggregates: DMMA fragments (P-APG: agg_fbd blocks) and the P-APG
+    // DFMA remainder
+    constexpr int FBK = MODE == kModePapg ? max1(agg_fbd<NN>()) : FB;
+    constexpr int RE = agg_re<NN>();
+    double D[kCT][FBK][2];
+    double E[kCT][max1(RE)];
     double Cc[kCT];
 #pragma unroll
     for (int ct = 0; ct < kCT; ++ct) {
@@ -430,12 +615,14 @@ __global__ void __launch_bounds__(mma_threads<NN>(), mma_ctas<NN>()) sweep_mma_k
       }
       Cc[ct] = cv ? __ldg(a.colrec + col * RQ + NN) : 0.0;
 #pragma unroll
-      for (int fb = 0; fb < FB; ++fb) D[ct][fb][0] = D[ct][fb][1] = 0.0;
+      for (int fb = 0; fb < FBK; ++fb) D[ct][fb][0] = D[ct][fb][1] = 0.0;
+#pragma unroll
+      for (int r = 0; r < max1(RE); ++r) E[ct][r] = 0.0;
     }
     if constexpr (MODE == kModePapg && !BLK) {
       // lean stage loop of the singleton P-APG sweep: 32-bit stage counters, the
-      // stages that meet the diagonal precomputed per segment, the output
-      // pointer advanced per stage
+      // ring slot and phase advanced incrementally, lane addresses precomputed,
+      // the stages that meet the diagonal precomputed per segment
       const int nrows = (int)(rhi - rlo);
       const int nstage = (nrows + kTR - 1) / kTR;
       const long long base = a.r0 + rlo;  // global row of the segment's first stage
@@ -444,57 +631,73 @@ __global__ void __launch_bounds__(mma_threads<NN>(), mma_ctas<NN>()) sweep_mma_k
       const long long dlo = gcol0 - kTR - base, dhi = gcol0 + kW - 1 - base;
       const int s_dlo = (int)max(0ll, (dlo >= 0 ? dlo / kTR : -((-dlo + kTR - 1) / kTR)) + 1);
       const int s_dhi = (int)max(0ll, min((long long)nstage, (dhi >= 0 ? dhi / kTR : -((-dhi + kTR - 1) / kTR)) + 1));
-      const int s_part = (nrows % kTR) ? nstage - 1 : nstage;  // partial last stage
-      const bool full_warp = gcol0 + kW <= a.N;
-      double* gout = Vp + rlo * a.ld + gcol0;
+      // stages below s_clean_end can be clean (not the partial last stage, none
+      // when the warp holds a pad column)
+      const int s_clean_end = (gcol0 + kW <= a.N) ? ((nrows % kTR) ? nstage - 1 : nstage) : 0;
+      double* gout = Vp + rlo * a.ld + gcol0;  // the warp's output block of stage 0
       const long long gstep = (long long)kTR * a.ld;
-      // this lane's output rows 2q, 2q+1 (column c8) of the current stage
-      double* o0 = gout + (long long)(2 * q) * a.ld + c8;
-      double* o1 = o0 + a.ld;
+      const long long lane_out = (long long)(2 * q) * a.ld + c8;
+      // lane offsets inside a stage (doubles)
+      const int off_v = (2 * q) * kTCP + warp * kW + c8;
+      const int off_b = 2 * kTR * kTCP + c8 * RQ + q;
+      const int off_r = 2 * kTR * kTCP + (2 * q) * RQ;
+      const uint32_t full_u = smem_u32(full), empty_u = smem_u32(empty);
+      uint32_t slot = (uint32_t)i % kNS, phase = ((uint32_t)i / kNS) & 1u;
+      double* const rowacc_lane = rowacc + warp * kWinM + 2 * (lane & 3) + ((lane >> 2) & 1);
       int win = 0, win_base = 0;
-      for (int st8 = 0; st8 < nstage; ++st8, ++i, gout += gstep, o0 += gstep, o1 += gstep) {
-        const int s = i % kNS;
-        mbar_wait(&full[s], (uint32_t)((i / kNS) & 1));
+      for (int st8 = 0; st8 < nstage; ++st8, gout += gstep) {
+        mbar_wait_u32(full_u + 8u * slot, phase);
         double rsj[2] = {0.0, 0.0};
         bool hot_stage = true;
-        if (active) {
-          const double* stg = stages + s * SD;
-          const double* sv = stg + warp * kW;
-          const double* svp = stg + kTR * kTCP + warp * kW;
-          const double* srec = stg + 2 * kTR * kTCP;
-          const bool clean = full_warp && (st8 < s_dlo || st8 >= s_dhi) && st8 < s_part;
-          if (clean) {
+        if (active && !CRB_PROBE_MEMONLY) {
+          const double* stg = stages + slot * SD;
+          const double* lv = stg + off_v;
+          const double* lb = stg + off_b;
+          const double* lr = stg + off_r;
+          const double* la = lr + c8;
+          if ((st8 < s_dlo || st8 >= s_dhi) && st8 < s_clean_end) {
+            double* o0 = gout + lane_out;
             // per-warp adaptive cold test: a tested stage that finds a cold tile
             // keeps the test on for the next 8 stages; otherwise every 8th stage
             // probes and the others run without any test
-            const bool test = probe > 0 || (pstage & 7) == 0;
-            ++pstage;
-            if (test) {
+            if (probe > 0 || (pstage & 7) == 0) {
               const int cold = unit_scale
-                  ? papg_clean<NN, true, true>(sv, svp, srec, o0, o1, lane, A, D, Cc, cf, sc, rsj, nst)
-                  : papg_clean<NN, false, true>(sv, svp, srec, o0, o1, lane, A, D, Cc, cf, sc, rsj, nst);
+                  ? papg_lean<NN, true, true>(lv, lb, lr, la, o0, a.ld, lane, A, D, E, Cc, cf, sc, rsj, nst)
+                  : papg_lean<NN, false, true>(lv, lb, lr, la, o0, a.ld, lane, A, D, E, Cc, cf, sc, rsj, nst);
               probe = cold ? 8 : (probe > 0 ? probe - 1 : 0);
               hot_stage = cold < kCT;
             } else if (unit_scale) {
-              papg_clean<NN, true, false>(sv, svp, srec, o0, o1, lane, A, D, Cc, cf, sc, rsj, nst);
+              papg_lean<NN, true, false>(lv, lb, lr, la, o0, a.ld, lane, A, D, E, Cc, cf, sc, rsj, nst);
             } else {
-              papg_clean<NN, false, false>(sv, svp, srec, o0, o1, lane, A, D, Cc, cf, sc, rsj, nst);
+              papg_lean<NN, false, false>(lv, lb, lr, la, o0, a.ld, lane, A, D, E, Cc, cf, sc, rsj, nst);
             }
+            ++pstage;
           } else {
             const int nr = min(kTR, nrows - st8 * kTR);
             const long long grow0 = base + (long long)st8 * kTR;
+            const double* sv = stg + warp * kW;
+            const double* svp = sv + kTR * kTCP;
+            const double* srec = stg + 2 * kTR * kTCP;
+            double dres[kCT][2];
+            stage_residual<NN>(srec, lane, A, dres);
             if (unit_scale)
               papg_masked<NN, true, false>(sv, svp, srec, gout, a.ld, gcol0, grow0, nr, a.N, a.nbar,
-                                           lane, A, D, Cc, cf, sc, rsj, nst);
+                                           lane, dres, D, E, Cc, cf, sc, rsj, nst);
             else
               papg_masked<NN, false, false>(sv, svp, srec, gout, a.ld, gcol0, grow0, nr, a.N, a.nbar,
-                                            lane, A, D, Cc, cf, sc, rsj, nst);
+                                            lane, dres, D, E, Cc, cf, sc, rsj, nst);
           }
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[s]);
+        if (lane == 0) mbar_arrive_u32(empty_u + 8u * slot);
+        if (++slot == (uint32_t)kNS) {
+          slot = 0;
+          phase ^= 1u;
+        }
         double rsum = 0.0;  // row sums, as in the generic loop below
-        if (hot_stage) {
+        if (CRB_PROBE_SKIP & 8) {
+          rsum = rsj[0] + rsj[1];
+        } else if (hot_stage) {
           const bool b2 = (lane & 4) != 0;
           const double send = b2 ? rsj[0] : rsj[1];
           rsum = b2 ? rsj[1] : rsj[0];
@@ -502,11 +705,16 @@ __global__ void __launch_bounds__(mma_threads<NN>(), mma_ctas<NN>()) sweep_mma_k
           rsum += __shfl_xor_sync(0xffffffffu, rsum, 8);
           rsum += __shfl_xor_sync(0xffffffffu, rsum, 16);
         }
-        double* ra = rowacc + (flushes & 1) * kCW * kWinM + warp * kWinM;
-        if (lane < 8) ra[win + 2 * (lane & 3) + ((lane >> 2) & 1)] = rsum;
+        if (lane < 8) rowacc_lane[(flushes & 1) * kCW * kWinM + win] = rsum;
         win += kTR;
         if (win == kWinM || st8 == nstage - 1) {
+#if CRB_PROBE_TIMING
+          const long long tb0 = clock64();
+#endif
           asm volatile("bar.sync 1, %0;" ::"r"(kCW * 32) : "memory");
+#if CRB_PROBE_TIMING
+          p_bar += clock64() - tb0;
+#endif
           const int valid_rows = min(win, nrows - win_base);
           const int wr = warp * 32 + lane;
           if (warp < kWinM / 32 && wr < valid_rows) {
@@ -521,6 +729,7 @@ __global__ void __launch_bounds__(mma_threads<NN>(), mma_ctas<NN>()) sweep_mma_k
           ++flushes;
         }
       }
+      i += nstage;
     } else {
   int win = 0;
       long long win_base = rlo;
@@ -543,7 +752,9 @@ __global__ void __launch_bounds__(mma_threads<NN>(), mma_ctas<NN>()) sweep_mma_k
         // stage, no pad column
         const bool clean = nr == kTR && gcol0 + kW <= a.N &&
                            blocks_disjoint<BLK>(grow0, kTR, gcol0, kW, a.nbar);
-        if (MODE == kModePapg) {
+        if constexpr (MODE == kModePapg) {
+          double dc[kCT][2];
+          stage_residual<NN>(srec, lane, A, dc);
           if (clean) {
             // per-warp adaptive cold test: a tested stage that finds a cold tile
             // keeps the test on for the next 8 stages; otherwise every 8th stage
@@ -552,22 +763,22 @@ __global__ void __launch_bounds__(mma_threads<NN>(), mma_ctas<NN>()) sweep_mma_k
             ++pstage;
             if (test) {
               const int cold = unit_scale
-                  ? papg_clean<NN, true, true>(sv, svp, srec, o0, o1, lane, A, D, Cc, cf, sc, rsj, nst)
-                  : papg_clean<NN, false, true>(sv, svp, srec, o0, o1, lane, A, D, Cc, cf, sc, rsj, nst);
+                  ? papg_clean<NN, true, true>(sv, svp, srec, o0, o1, lane, dc, D, E, Cc, cf, sc, rsj, nst)
+                  : papg_clean<NN, false, true>(sv, svp, srec, o0, o1, lane, dc, D, E, Cc, cf, sc, rsj, nst);
               probe = cold ? 8 : (probe > 0 ? probe - 1 : 0);
               hot_stage = cold < kCT;
             } else if (unit_scale) {
-              papg_clean<NN, true, false>(sv, svp, srec, o0, o1, lane, A, D, Cc, cf, sc, rsj, nst);
+              papg_clean<NN, true, false>(sv, svp, srec, o0, o1, lane, dc, D, E, Cc, cf, sc, rsj, nst);
             } else {
-              papg_clean<NN, false, false>(sv, svp, srec, o0, o1, lane, A, D, Cc, cf, sc, rsj, nst);
+              papg_clean<NN, false, false>(sv, svp, srec, o0, o1, lane, dc, D, E, Cc, cf, sc, rsj, nst);
             }
           } else {
             if (unit_scale)
               papg_masked<NN, true, BLK>(sv, svp, srec, gout, a.ld, gcol0, grow0, nr, a.N, a.nbar,
-                                         lane, A, D, Cc, cf, sc, rsj, nst);
+                                         lane, dc, D, E, Cc, cf, sc, rsj, nst);
             else
               papg_masked<NN, false, BLK>(sv, svp, srec, gout, a.ld, gcol0, grow0, nr, a.N, a.nbar,
-                                          lane, A, D, Cc, cf, sc, rsj, nst);
+                                          lane, dc, D, E, Cc, cf, sc, rsj, nst);
           }
         } else if (clean) {
           mma_stage<NN, MODE, false, BLK>(sv, srec, gout, a.ld, gcol0, grow0, nr, a.N, a.nbar, lane, A, D,
@@ -616,10 +827,11 @@ __global__ void __launch_bounds__(mma_threads<NN>(), mma_ctas<NN>()) sweep_mma_k
     }
     if (active) {  // column partials: thread holds (feature fb*8+c8, cols 2q+{0,1})
       const long long slot = (long long)blockIdx.x * a.maxspan + (t - t_first);
+      constexpr int FBW = MODE == kModePapg ? agg_fbd<NN>() : FB;  // DMMA blocks in use
 #pragma unroll
       for (int ct = 0; ct < kCT; ++ct) {
 #pragma unroll
-        for (int fb = 0; fb < FB; ++fb) {
+        for (int fb = 0; fb < FBW; ++fb) {
           const int f = fb * 8 + c8;
           if (f <= NN) {
             const int slotf = (f == NN) ? 0 : 1 + f;  // colagg = (colsum, V^T X)
@@ -630,10 +842,28 @@ __global__ void __launch_bounds__(mma_threads<NN>(), mma_ctas<NN>()) sweep_mma_k
             }
           }
         }
+        if constexpr (MODE == kModePapg && RE > 0) {
+          // DFMA remainder: lanes 4 c8 + q hold rows 2q, 2q+1 of column c8; sum over q
+          const long long coff = (long long)warp * kW + ct * 8 + c8;
+#pragma unroll
+          for (int r = 0; r < RE; ++r) {
+            double e = E[ct][r];
+            e += __shfl_xor_sync(0xffffffffu, e, 1);
+            e += __shfl_xor_sync(0xffffffffu, e, 2);
+            const int f = 8 * agg_fbd<NN>() + r;  // feature; r == RE - 1: the column sum
+            const int slotf = (r == RE - 1) ? 0 : 1 + f;
+            if (q == 0) a.colpart[(slot * kTC + coff) * (NN + 1) + slotf] = e;
+          }
+        }
       }
     }
   }
 
+#if CRB_PROBE_TIMING
+  if (lane == 0 && (blockIdx.x == 0 || blockIdx.x == 77) && MODE == kModePapg)
+    printf("probe cta %d warp %d total %lld wait_full %lld bar %lld\n", (int)blockIdx.x, warp,
+           clock64() - p_t0, p_wait, p_bar);
+#endif
   double vv = sc.vv, vr = sc.vr, tr = sc.tr, nn = sc.nn;
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) {

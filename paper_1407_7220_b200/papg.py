@@ -446,8 +446,18 @@ class DualSolver:
         _raise(self._L.cr_last_timing(self.h, C.byref(s), C.byref(k), C.byref(sw)), self.h)
         return s.value, k.value, sw.value
 
+    def last_sweep_times(self):
+        """Durations (s) of the sweep launches the last iterate call bracketed with
+        CUDA events, in launch order (every launch of a call of <= 64 iterations)."""
+        k = C.c_int64(0)
+        _raise(self._L.cr_last_sweep_times(self.h, None, 0, C.byref(k)), self.h)
+        out = np.zeros(k.value)
+        _raise(self._L.cr_last_sweep_times(self.h, nat.ptr(out), k.value, C.byref(k)), self.h)
+        return out
+
     def sweep_store_count(self, reset=False):
-        """Multipliers written by the P-APG sweeps since the last reset."""
+        """Multipliers written by the P-APG sweeps since the last reset (whole
+        32-byte sectors: those with a changed multiplier)."""
         c = C.c_uint64(0)
         _raise(self._L.cr_sweep_store_count(self.h, C.byref(c), int(reset)), self.h)
         return c.value
