@@ -81,7 +81,7 @@ __host__ __device__ constexpr int fblocks() { return ((NN + 1) + 7) / 8; }
 // Remainders above 3 features (n = 5, 20) keep the padded block: the extra
 // per-lane accumulators spill at 128 registers.
 #ifndef CRB_AGG_REM_MAX
-#define CRB_AGG_REM_MAX 0
+#define CRB_AGG_REM_MAX 3
 #endif
 template <int NN>
 __host__ __device__ constexpr bool agg_split() {
@@ -101,10 +101,19 @@ template <int NN>
 __host__ __device__ constexpr int stage_doubles() {
   return 2 * kTR * (mma_cw<NN>() * 8 * mma_ct<NN>() + 2) + kTR * rec_pitch(NN);
 }
+// P-APG lean loop: the residual A fragments of each warp's columns live in
+// shared memory (reloaded per stage) instead of 2 x ksteps registers per lane
+#ifndef CRB_A_SMEM
+#define CRB_A_SMEM 0
+#endif
+template <int NN>
+__host__ __device__ constexpr int afrag_doubles() {
+  return CRB_A_SMEM ? mma_cw<NN>() * mma_ct<NN>() * ksteps<NN>() * 32 : 0;
+}
 template <int NN>
 __host__ __device__ constexpr int smem_bytes() {
   return mma_ns<NN>() * stage_doubles<NN>() * 8 + 2 * mma_cw<NN>() * kWinM * 8 +
-         2 * mma_ns<NN>() * 8;
+         2 * mma_ns<NN>() * 8 + afrag_doubles<NN>() * 8;
 }
 
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {

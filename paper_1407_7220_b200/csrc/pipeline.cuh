@@ -3,6 +3,10 @@
 #pragma once
 #include <cstdint>
 
+#ifndef CRB_PROBE_STORE
+#define CRB_PROBE_STORE 0  // measurement probe only: 1 = no stores, 2 = store every v
+#endif
+
 namespace crb {
 
 __device__ __forceinline__ void st_stream(double* p, double v) {
@@ -139,6 +143,7 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
 __device__ __forceinline__ void store_changed_sector(double* p, double v, double old, bool valid,
                                                      int lane, int& count) {
   const bool ch = valid && __double_as_longlong(v) != __double_as_longlong(old);
+  if (CRB_PROBE_STORE == 1) return;
   if (CRB_STORE_GRAN == 8) {
     if (ch) {
       st_stream(p, v);
@@ -177,9 +182,6 @@ __device__ __forceinline__ void acc_neg_sq(double& acc, double r) {
 // *p = v (streaming) and ++count when v != old, as one predicated store instead
 // of a branch. v, old >= +0 (never -0), so numeric != is the 64-bit pattern test:
 // an integer compare keeps it off the fp64 pipe the DMMAs share
-#ifndef CRB_PROBE_STORE
-#define CRB_PROBE_STORE 0  // measurement probe only: 1 = no stores, 2 = store every v
-#endif
 __device__ __forceinline__ void store_if_changed(double* p, double v, double old, int& count) {
   if (CRB_PROBE_STORE == 1) return;
   if (CRB_PROBE_STORE == 2) {

@@ -480,6 +480,7 @@ __global__ void __launch_bounds__(mma_threads<NN>(), mma_ctas<NN>()) sweep_mma_k
   double* rowacc = smem + kNS * SD;  // [2][kCW][kWinM]
   uint64_t* full = reinterpret_cast<uint64_t*>(rowacc + 2 * kCW * kWinM);
   uint64_t* empty = full + kNS;
+  double* afrag = reinterpret_cast<double*>(empty + kNS);  // [kCW][kCT][KS][32] (CRB_A_SMEM)
 
   if (a.stopped != nullptr && *a.stopped) return;
   const int cur = (MODE != kModePower) ? *a.cur : 0;
@@ -643,6 +644,15 @@ __global__ void __launch_bounds__(mma_threads<NN>(), mma_ctas<NN>()) sweep_mma_k
       const int off_r = 2 * kTR * kTCP + (2 * q) * RQ;
       const uint32_t full_u = smem_u32(full), empty_u = smem_u32(empty);
       uint32_t slot = (uint32_t)i % kNS, phase = ((uint32_t)i / kNS) & 1u;
+      const double* const aw = afrag + warp * kCT * KS * 32 + lane;
+      if (CRB_A_SMEM) {
+        double* w = afrag + warp * kCT * KS * 32 + lane;
+#pragma unroll
+        for (int ct = 0; ct < kCT; ++ct)
+#pragma unroll
+          for (int ks = 0; ks < KS; ++ks) w[(ct * KS + ks) * 32] = A[ct][ks];
+        __syncwarp();
+      }
       double* const rowacc_lane = rowacc + warp * kWinM + 2 * (lane & 3) + ((lane >> 2) & 1);
       int win = 0, win_base = 0;
       for (int st8 = 0; st8 < nstage; ++st8, gout += gstep) {
@@ -650,6 +660,11 @@ __global__ void __launch_bounds__(mma_threads<NN>(), mma_ctas<NN>()) sweep_mma_k
         double rsj[2] = {0.0, 0.0};
         bool hot_stage = true;
         if (active && !CRB_PROBE_MEMONLY) {
+          double Al[kCT][KS];
+#pragma unroll
+          for (int ct = 0; ct < kCT; ++ct)
+#pragma unroll
+            for (int ks = 0; ks < KS; ++ks) Al[ct][ks] = CRB_A_SMEM ? aw[(ct * KS + ks) * 32] : A[ct][ks];
           const double* stg = stages + slot * SD;
           const double* lv = stg + off_v;
           const double* lb = stg + off_b;
@@ -662,14 +677,14 @@ __global__ void __launch_bounds__(mma_threads<NN>(), mma_ctas<NN>()) sweep_mma_k
             // probes and the others run without any test
             if (probe > 0 || (pstage & 7) == 0) {
               const int cold = unit_scale
-                  ? papg_lean<NN, true, true>(lv, lb, lr, la, o0, a.ld, lane, A, D, E, Cc, cf, sc, rsj, nst)
-                  : papg_lean<NN, false, true>(lv, lb, lr, la, o0, a.ld, lane, A, D, E, Cc, cf, sc, rsj, nst);
+                  ? papg_lean<NN, true, true>(lv, lb, lr, la, o0, a.ld, lane, Al, D, E, Cc, cf, sc, rsj, nst)
+                  : papg_lean<NN, false, true>(lv, lb, lr, la, o0, a.ld, lane, Al, D, E, Cc, cf, sc, rsj, nst);
               probe = cold ? 8 : (probe > 0 ? probe - 1 : 0);
               hot_stage = cold < kCT;
             } else if (unit_scale) {
-              papg_lean<NN, true, false>(lv, lb, lr, la, o0, a.ld, lane, A, D, E, Cc, cf, sc, rsj, nst);
+              papg_lean<NN, true, false>(lv, lb, lr, la, o0, a.ld, lane, Al, D, E, Cc, cf, sc, rsj, nst);
             } else {
-              papg_lean<NN, false, false>(lv, lb, lr, la, o0, a.ld, lane, A, D, E, Cc, cf, sc, rsj, nst);
+              papg_lean<NN, false, false>(lv, lb, lr, la, o0, a.ld, lane, Al, D, E, Cc, cf, sc, rsj, nst);
             }
             ++pstage;
           } else {
@@ -679,7 +694,7 @@ __global__ void __launch_bounds__(mma_threads<NN>(), mma_ctas<NN>()) sweep_mma_k
             const double* svp = sv + kTR * kTCP;
             const double* srec = stg + 2 * kTR * kTCP;
             double dres[kCT][2];
-            stage_residual<NN>(srec, lane, A, dres);
+            stage_residual<NN>(srec, lane, Al, dres);
             if (unit_scale)
               papg_masked<NN, true, false>(sv, svp, srec, gout, a.ld, gcol0, grow0, nr, a.N, a.nbar,
                                            lane, dres, D, E, Cc, cf, sc, rsj, nst);
