@@ -12,6 +12,7 @@
 #include <nccl.h>
 
 #include <chrono>
+#include <mutex>
 #include <climits>
 #include <cmath>
 #include <cstdio>
@@ -30,6 +31,31 @@
 using namespace crb;
 
 cudaStream_t g_alloc_stream = nullptr;
+
+// Process-wide pool of the handles' small pinned host blocks (control-state
+// mirrors): cudaMallocHost costs ~0.4 ms per call, three per handle, which a
+// service creating one handle per solve would pay every time.
+namespace {
+std::mutex g_pin_mu;
+std::vector<std::pair<size_t, void*>> g_pin_free;
+}  // namespace
+static cudaError_t pinned_get(void** p, size_t bytes) {
+  {
+    std::lock_guard<std::mutex> lk(g_pin_mu);
+    for (size_t i = 0; i < g_pin_free.size(); ++i)
+      if (g_pin_free[i].first == bytes) {
+        *p = g_pin_free[i].second;
+        g_pin_free.erase(g_pin_free.begin() + (long)i);
+        return cudaSuccess;
+      }
+  }
+  return cudaMallocHost(p, bytes);
+}
+static void pinned_put(void* p, size_t bytes) {
+  if (!p) return;
+  std::lock_guard<std::mutex> lk(g_pin_mu);
+  g_pin_free.emplace_back(bytes, p);
+}
 
 namespace crb {
 
@@ -122,14 +148,6 @@ PrimalArgs primal_args(cr_handle* h, int mode) {
 // iteration's K2 in one launch; the standalone primal is enqueued only at the
 // start of an iterate call / graph and is a no-op when the last fused launch
 // already computed it (DevCtrl::primal_done). Opt-in: CRB_FUSE=1.
-// rng_stream(0x5eed, 97) normals, normalised (operators.cpp:309-313)
-void sigma_start_vector(int64_t cols, double* v, int max_threads = 16) {
-  host::normal_stream(0x5eedULL, 97, cols, v, max_threads);
-  double ss = 0;
-  for (int64_t i = 0; i < cols; ++i) ss += v[i] * v[i];
-  const double nv = std::sqrt(ss);
-  for (int64_t i = 0; i < cols; ++i) v[i] /= nv;
-}
 
 bool fused_path(const cr_handle* h) {
   return h->fuse_ok && h->comm == nullptr && h->part.K == 0 && !h->masked;
@@ -297,13 +315,21 @@ cr_status cr_create(const double* Xh, const double* ybar_shifted, int64_t N, int
   h->RP = rec_pitch((int)n);
   h->gamma = gamma;
   h->cfg.gamma = gamma;
+  const bool tdbg = std::getenv("CRB_DEBUG_CREATE") != nullptr;
+  const auto tc0 = std::chrono::steady_clock::now();
+  auto tmark = [&](const char* what) {
+    if (tdbg)
+      std::fprintf(stderr, "create %-12s %.3f ms\n", what,
+                   std::chrono::duration<double>(std::chrono::steady_clock::now() - tc0).count() * 1e3);
+  };
   h->sigma_prep = std::thread([h] {  // overlaps the allocations and uploads below
     const int64_t cols = h->N * (h->n + 1);
-    h->sigma_start.resize((size_t)cols);
-    sigma_start_vector(cols, h->sigma_start.data(), 4);  // few threads: create runs beside it
+    h->sigma_start.resize((size_t)(2 * cols));
+    host::uniform_pairs(0x5eedULL, 97, cols, h->sigma_start.data());  // beside the creation
   });
   CUDA_TRY(cudaSetDevice(device));
   CUDA_TRY(cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking));
+  tmark("stream");
   keep_pool_memory(device);
   g_alloc_stream = h->st;
   // sweep variant, measured on B200: the DMMA sweep is
@@ -336,6 +362,7 @@ cr_status cr_create(const double* Xh, const double* ybar_shifted, int64_t N, int
   }
   if (!h->kp.fn || !h->kw.fn || h->kp.max_blocks_per_sm < 1)
     return fail(h, CR_EINVAL, "no sweep kernel for this n");
+  tmark("kernel info");
   const int W = h->kp.strip_cols;
   h->S = (int)((N + W - 1) / W);
   h->ld = (int64_t)h->S * W;
@@ -406,33 +433,29 @@ cr_status cr_create(const double* Xh, const double* ybar_shifted, int64_t N, int
     cudaGetLastError();
     return fail(h, CR_ENOMEM, std::string("device allocation failed: ") + cudaGetErrorString(e));
   }
+  tmark("allocs");
   encode_sweep_tmaps(h);
+  tmark("tmaps");
   h->stage_elems = std::min<int64_t>((int64_t)1 << 25, h->R * (N - 1) + N);  // <= 256 MB
   if (dalloc(&h->stage, (size_t)h->stage_elems) != cudaSuccess) {
     cudaGetLastError();
     return fail(h, CR_ENOMEM, "stage allocation failed");
   }
-  CUDA_TRY(cudaMallocHost(&h->ctrl_h, sizeof(DevCtrl)));
-  CUDA_TRY(cudaMallocHost(&h->ctrl_poll, 2 * sizeof(DevCtrl)));
-  CUDA_TRY(cudaMallocHost(&h->pause_h, 2 * sizeof(long long)));
+  CUDA_TRY(pinned_get((void**)&h->ctrl_h, sizeof(DevCtrl)));
+  CUDA_TRY(pinned_get((void**)&h->ctrl_poll, 2 * sizeof(DevCtrl)));
+  CUDA_TRY(pinned_get((void**)&h->pause_h, 2 * sizeof(long long)));
   std::memset(h->ctrl_h, 0, sizeof(DevCtrl));
   CUDA_TRY(cudaEventCreate(&h->ev_start));
   CUDA_TRY(cudaEventCreate(&h->ev_end));
   CUDA_TRY(cudaEventCreateWithFlags(&h->ev_poll[0], cudaEventDisableTiming));
   CUDA_TRY(cudaEventCreateWithFlags(&h->ev_poll[1], cudaEventDisableTiming));
+  tmark("pinned+events");
 
   // static inputs: X, ybar, row records (y placeholder, x, pad)
   CUDA_TRY(cudaMemcpyAsync(h->X, Xh, sizeof(double) * N * n, cudaMemcpyHostToDevice, h->st));
   CUDA_TRY(cudaMemcpyAsync(h->ybar, ybar_shifted, sizeof(double) * N, cudaMemcpyHostToDevice,
                            h->st));
-  std::vector<double> rec((size_t)N * RP, 0.0);
-  for (int64_t l = 0; l < N; ++l) {
-    for (int64_t j = 0; j < n; ++j) rec[l * RP + j] = Xh[l * n + j];  // (x, 1, y)
-    rec[l * RP + n] = 1.0;
-    rec[l * RP + n + 1] = ybar_shifted[l];
-  }
-  CUDA_TRY(cudaMemcpyAsync(h->rowrec, rec.data(), sizeof(double) * rec.size(),
-                           cudaMemcpyHostToDevice, h->st));
+  CUDA_TRY(launch_rowrec_init(h->X, h->ybar, h->rowrec, N, (int)n, (int)RP, h->st));  // (x, 1, y)
   CUDA_TRY(cudaMemsetAsync(h->colrec, 0, sizeof(double) * N * RP, h->st));
   const double consts[4] = {1.0, 1.0, 0.0, 0.0};
   CUDA_TRY(cudaMemcpyAsync(h->consts, consts, sizeof(consts), cudaMemcpyHostToDevice, h->st));
@@ -444,7 +467,9 @@ cr_status cr_create(const double* Xh, const double* ybar_shifted, int64_t N, int
   CUDA_TRY(launch_gram(h->X, N, (int)n, h->gram, h->st));
   const char* sig = std::getenv("CRB_SIGMA");
   h->sigma_by_sweep = sig && std::strcmp(sig, "sweep") == 0;
+  tmark("uploads");
   CUDA_TRY(cudaStreamSynchronize(h->st));
+  tmark("sync");
   return CR_OK;
 }
 
@@ -461,7 +486,7 @@ void cr_destroy(cr_handle* h) {
                     h->vpos[0], h->vpos[1], h->xbuf,    h->aggsave,  h->colpart, h->rowpart,
                     h->scalpart, h->k2part, h->k2sum,   h->hist,     h->yout,   h->xiout,
                     h->pw_u,    h->pw_v,    h->pw_part, h->pw_sum,   h->consts, h->stage,
-                    h->gram,    h->ps_part, h->ps_part2, h->ps_state};
+                    h->gram,    h->ps_part, h->ps_part2, h->ps_state, h->sv_u12};
   for (double* b : bufs) dfree(b, h->st);
   for (double* b : {h->s_colpart, h->s_rowpart, h->s_scalpart, h->s_k2part}) dfree(b, h->st);
   dfree(h->izero, h->st);
@@ -472,9 +497,9 @@ void cr_destroy(cr_handle* h) {
   dfree(h->d_stores, h->st);
   dfree(h->ctrl_d, h->st);
   if (h->st) cudaStreamSynchronize(h->st);
-  if (h->ctrl_h) cudaFreeHost(h->ctrl_h);
-  if (h->ctrl_poll) cudaFreeHost(h->ctrl_poll);
-  if (h->pause_h) cudaFreeHost(h->pause_h);
+  pinned_put(h->ctrl_h, sizeof(DevCtrl));
+  pinned_put(h->ctrl_poll, 2 * sizeof(DevCtrl));
+  pinned_put(h->pause_h, 2 * sizeof(long long));
   for (cudaEvent_t ev : h->ev_sweep) cudaEventDestroy(ev);
   if (h->ev_start) cudaEventDestroy(h->ev_start);
   if (h->ev_end) cudaEventDestroy(h->ev_end);
@@ -515,12 +540,14 @@ cr_status cr_sigma_C(cr_handle* h, double tol, int32_t max_iters, double* sigma,
   const int64_t cols = h->N * (h->n + 1);
   // fixed seeded start (operators.cpp:309-313), drawn at handle creation
   if (h->sigma_prep.joinable()) h->sigma_prep.join();
-  if ((int64_t)h->sigma_start.size() != cols) {
-    h->sigma_start.resize((size_t)cols);
-    sigma_start_vector(cols, h->sigma_start.data());
+  if ((int64_t)h->sigma_start.size() != 2 * cols) {
+    h->sigma_start.resize((size_t)(2 * cols));
+    host::uniform_pairs(0x5eedULL, 97, cols, h->sigma_start.data());
   }
-  CUDA_TRY(cudaMemcpyAsync(h->pw_u, h->sigma_start.data(), sizeof(double) * cols,
+  if (!h->sv_u12) CUDA_TRY(dalloc(&h->sv_u12, (size_t)(2 * cols + 256)));
+  CUDA_TRY(cudaMemcpyAsync(h->sv_u12, h->sigma_start.data(), sizeof(double) * 2 * cols,
                            cudaMemcpyHostToDevice, h->st));
+  CUDA_TRY(launch_start_vector(h->sv_u12, h->pw_u, cols, h->sv_u12 + 2 * cols, h->st));
   // closed-form steps assume singleton blocks; a K-block partition masks the
   // same-block pairs inside the sweep instead
   if (!h->sigma_by_sweep && h->part.K == 0) {  // whole power iteration in one cooperative launch

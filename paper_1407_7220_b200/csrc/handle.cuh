@@ -130,7 +130,8 @@ struct cr_handle {
   // sigma_max(C) start vector (rng_stream(0x5eed, 97), normalised), drawn on a
   // host thread while the handle's device state is set up
   std::thread sigma_prep;
-  std::vector<double> sigma_start;
+  std::vector<double> sigma_start;  // uniform pairs of the sigma start vector (host drawn)
+  double* sv_u12 = nullptr;          // their device copy + 256 doubles of block partials
   double last_seconds = 0, last_sweep_seconds = 0;
   std::vector<double> last_sweep_times;  // per bracketed sweep launch of the last call (s)
   int64_t last_launches = 0;

@@ -152,6 +152,17 @@ bool affine_ls(const double* X, const double* y, int64_t N, int64_t n, std::vect
 
 }  // namespace
 
+// The uniform pairs (u1, u2) of `count` Box-Muller draws, interleaved, in
+// stream order: the sequential part of normal_stream (the device applies the
+// transform for the sigma start vector).
+void uniform_pairs(uint64_t seed, uint64_t tag, int64_t count, double* out2) {
+  Xoshiro g = stream(seed, tag);
+  for (int64_t i = 0; i < count; ++i) {
+    out2[2 * i] = g.uniform();
+    out2[2 * i + 1] = g.uniform();
+  }
+}
+
 // The uniform pairs are drawn sequentially (the stream is sequential); the
 // Box-Muller transform, which dominates the cost, runs on several threads.
 // Bit-identical to calling Xoshiro::normal() count times.

@@ -8,6 +8,7 @@ namespace host {
 
 // xoshiro256++ named sub-stream normals (rng.hpp:41-59), row-major fill
 void normal_stream(uint64_t seed, uint64_t tag, int64_t count, double* out, int max_threads = 16);
+void uniform_pairs(uint64_t seed, uint64_t tag, int64_t count, double* out2);
 
 }  // namespace host
 }  // namespace crb

@@ -378,6 +378,15 @@ __global__ void __launch_bounds__(kBlock) reduce_primal_kernel(const FusedArgs f
   }
 }
 
+__global__ void rowrec_init_kernel(const double* X, const double* ybar, double* rowrec, long long N,
+                                   int n, int RP) {
+  const long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= N * RP) return;
+  const long long l = k / RP;
+  const int j = (int)(k - l * RP);
+  rowrec[k] = j < n ? X[l * n + j] : (j == n ? 1.0 : (j == n + 1 ? ybar[l] : 0.0));
+}
+
 __global__ void begin_kernel(DevCtrl* c) {
   if (threadIdx.x == 0 && blockIdx.x == 0) c->t_start_ns = globaltimer();
 }
@@ -625,6 +634,13 @@ cudaError_t launch_begin(DevCtrl* c, cudaStream_t s) {
 
 cudaError_t launch_stamp(unsigned long long* out, cudaStream_t s) {
   stamp_kernel<<<1, 32, 0, s>>>(out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_rowrec_init(const double* X, const double* ybar, double* rowrec, long long N, int n,
+                               int RP, cudaStream_t s) {
+  const long long tot = N * RP;
+  rowrec_init_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(X, ybar, rowrec, N, n, RP);
   return cudaGetLastError();
 }
 

@@ -95,6 +95,12 @@ cudaError_t launch_estimator(const double* Xq, long long Q, const double* X, con
                              cudaStream_t s);
 
 int primal_blocks(long long N);
+// row records (x, 1, ybar, 0 ...) of every point, pitch RP (handle creation)
+cudaError_t launch_rowrec_init(const double* X, const double* ybar, double* rowrec, long long N, int n,
+                               int RP, cudaStream_t s);
+// sigma start vector from host-drawn uniform pairs (power.cu); part: 148 doubles
+cudaError_t launch_start_vector(const double* u12, double* v, long long cols, double* part,
+                                cudaStream_t s);
 cudaError_t launch_gram(const double* X, long long N, int n, double* out, cudaStream_t s);
 int power_loop_grid(int sms, long long N);
 cudaError_t launch_power_loop(const PowerLoopArgs& a, int grid, cudaStream_t s);

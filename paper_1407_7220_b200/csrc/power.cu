@@ -16,6 +16,7 @@
 // barriers per step. The computation is replicated on every rank of a
 // sharded run (no exchange).
 #include <algorithm>
+#include <cstdlib>
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <math.h>
@@ -447,6 +448,223 @@ __global__ void __launch_bounds__(kQBlock) power_loop_c_kernel(const PowerLoopAr
   }
 }
 
+// op 0 on one thread-block cluster (kPcCta CTAs of kPcThreads threads): the
+// points are split into kPcCta contiguous ranges, each CTA keeps its points'
+// x and the power vector u in shared memory for the whole iteration (no
+// global traffic per step), and the per-step records -- (|u|^2, v.u) and the
+// raw sums of the new u, as in power_loop_c_kernel -- are exchanged through
+// distributed shared memory: every CTA writes its record into every CTA's
+// slot of a step-parity double buffer, one cluster barrier, then every CTA
+// sums the kPcCta records in rank order (identical decisions everywhere).
+// v = u / |u| is formed as u * (1 / |u|): within an ulp of the division.
+constexpr int kPcCta = 16;      // non-portable cluster size (B200 supports 16)
+#ifndef CRB_PC_THREADS
+#define CRB_PC_THREADS 512
+#endif
+constexpr int kPcThreads = CRB_PC_THREADS;  // measured 512 / 640 / 768: 1.47 / 1.75 / 2.21 ms (cfg 2)
+
+template <int NN>
+__host__ __device__ constexpr int pc_w2() { return 4 + 2 * NN; }
+
+// dynamic shared memory (doubles) for ppc points per CTA
+template <int NN>
+__host__ __device__ constexpr long long pc_smem_doubles(long long ppc) {
+  return ppc * (2 * NN + 1) + NN * NN + NN + 2LL * kPcCta * pc_w2<NN>() +
+         (kPcThreads / 32) * pc_w2<NN>() + pc_w2<NN>();
+}
+
+template <int NN>
+__global__ void __launch_bounds__(kPcThreads, 1) power_cluster_kernel(const PowerLoopArgs a, long long ppc) {
+  constexpr int W = 2 + 2 * NN;  // raw sums
+  constexpr int W2 = 2 + W;      // (|u|^2, v.u) + raw sums
+  cg::cluster_group cluster = cg::this_cluster();
+  const int rank = (int)cluster.block_rank();
+  extern __shared__ __align__(16) double sm[];
+  double* sx = sm;                            // [ppc][NN]
+  double* su = sx + ppc * NN;                 // [ppc][NN + 1]: a, b
+  double* S = su + ppc * (NN + 1);            // NN x NN
+  double* sxs = S + NN * NN;                  // s (NN)
+  double* rec = sxs + NN;                     // [2][kPcCta][W2]
+  double* wpart = rec + 2 * kPcCta * W2;      // [warps][W2]
+  double* red = wpart + (kPcThreads / 32) * W2;  // W2
+  const long long N = a.N;
+  const long long l0 = (long long)rank * ppc;
+  const long long l1 = min(N, l0 + ppc);
+  const int np = (int)max(0LL, l1 - l0);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int e = tid; e < NN * NN + NN; e += kPcThreads) S[e] = a.gram[e];
+  for (long long k = tid; k < (long long)np * NN; k += kPcThreads) sx[k] = a.X[l0 * NN + k];
+  for (int p = tid; p < np; p += kPcThreads) {
+    su[p * (NN + 1)] = a.u[l0 + p];
+#pragma unroll
+    for (int j = 0; j < NN; ++j) su[p * (NN + 1) + 1 + j] = a.u[N + (l0 + p) * NN + j];
+  }
+  __syncthreads();
+
+  // CTA record -> every CTA's slot `buf`, cluster barrier, rank-order sum into red
+  auto exchange = [&](double (&acc)[W2], int buf) {
+    // transpose reduction over the warp: 31 shuffles for up to 32 values (lane w
+    // ends with the warp total of value w) instead of 5 per value
+    {
+      double t[32];
+#pragma unroll
+      for (int w = 0; w < 32; ++w) t[w] = w < W2 ? acc[w] : 0.0;
+#pragma unroll
+      for (int h = 16; h >= 1; h >>= 1) {
+        const bool up = (lane & h) != 0;
+#pragma unroll
+        for (int k = 0; k < h; ++k) {
+          const double send = up ? t[k] : t[k + h];
+          const double keep = up ? t[k + h] : t[k];
+          t[k] = keep + __shfl_xor_sync(0xffffffffu, send, h);
+        }
+      }
+      // lane l holds value index bitrev-free: the kept half at each level is
+      // selected by the lane's own bit, so the value index is the lane id
+      if (lane < W2) wpart[warp * W2 + lane] = t[0];
+    }
+    __syncthreads();
+    if (tid < W2) {
+      double t = 0.0;
+#pragma unroll 4
+      for (int k = 0; k < kPcThreads / 32; ++k) t += wpart[k * W2 + tid];
+      double* slot = rec + ((long long)buf * kPcCta + rank) * W2 + tid;
+      for (int r = 0; r < kPcCta; ++r) *cluster.map_shared_rank(slot, r) = t;
+    }
+    cluster.sync();
+    if (tid < W2) {
+      double t = 0.0;
+      const double* rb = rec + (long long)buf * kPcCta * W2 + tid;
+#pragma unroll 4
+      for (int r = 0; r < kPcCta; ++r) t += rb[r * W2];
+      red[tid] = t;
+    }
+    __syncthreads();
+  };
+
+  {  // prologue: raw sums of the (host-normalised) start vector
+    double acc[W2];
+#pragma unroll
+    for (int w = 0; w < W2; ++w) acc[w] = 0.0;
+    for (int p = tid; p < np; p += kPcThreads) {
+      double b[NN], x[NN];
+#pragma unroll
+      for (int j = 0; j < NN; ++j) {
+        b[j] = su[p * (NN + 1) + 1 + j];
+        x[j] = sx[p * NN + j];
+      }
+      sums_raw<NN>(su[p * (NN + 1)], b, x, acc + 2);
+    }
+    exchange(acc, 1);
+  }
+  const double Nm1 = (double)(N - 1);
+  double norm_u = 1.0;
+  double lambda_prev = 0.0;
+  for (int it = 1; it <= a.max_iters; ++it) {
+    const double inv = 1.0 / norm_u;
+    double* sums = wpart;  // the global sums of v (the warp partials are free here)
+    if (tid < W) sums[tid] = red[2 + tid] / norm_u;
+    __syncthreads();
+    const double A = sums[0], Cs = sums[1];
+    double acc[W2];
+#pragma unroll
+    for (int w = 0; w < W2; ++w) acc[w] = 0.0;
+    for (int p = tid; p < np; p += kPcThreads) {
+      double* up = su + p * (NN + 1);
+      const double av = up[0] * inv;
+      double b[NN], x[NN];
+      double bx = 0.0;
+#pragma unroll
+      for (int j = 0; j < NN; ++j) {
+        b[j] = up[1 + j] * inv;
+        x[j] = sx[p * NN + j];
+        bx = fma(b[j], x[j], bx);
+      }
+      const double c = av - bx;
+      double Bx = 0.0, bs = 0.0;
+#pragma unroll
+      for (int j = 0; j < NN; ++j) {
+        Bx = fma(sums[2 + j] - b[j], x[j], Bx);
+        bs = fma(b[j], sxs[j] - x[j], bs);
+      }
+      const double R = Nm1 * av - (Cs - c) - Bx;
+      const double Col = (A - av) - Nm1 * c - bs;
+      const double uy = av + R - Col;
+      up[0] = uy;
+      double uu = uy * uy, vu = av * uy;
+      double ux[NN];
+#pragma unroll
+      for (int j = 0; j < NN; ++j) {
+        double Sb = 0.0;
+#pragma unroll
+        for (int k = 0; k < NN; ++k) Sb = fma(S[j * NN + k], b[k], Sb);
+        const double T = (sums[2 + NN + j] - av * x[j]) - c * (sxs[j] - x[j]) - (Sb - x[j] * bx);
+        ux[j] = Col * x[j] - T;
+        up[1 + j] = ux[j];
+        uu = fma(ux[j], ux[j], uu);
+        vu = fma(b[j], ux[j], vu);
+      }
+      acc[0] += uu;
+      acc[1] += vu;
+      sums_raw<NN>(uy, ux, x, acc + 2);
+    }
+    exchange(acc, it & 1);
+    // identical in every CTA: operators.cpp:318-334
+    const double lambda = red[1];
+    const double nu = sqrt(red[0]);
+    bool done = false;
+    double sigma = 0.0;
+    int conv = 1;
+    if (nu == 0.0 || lambda == 0.0) {
+      done = true;
+    } else {
+      norm_u = nu;
+      if (it > 1 && fabs(lambda - lambda_prev) <= a.tol * lambda) {
+        sigma = sqrt(lambda) * 1.01;
+        done = true;
+      } else if (it == a.max_iters) {
+        sigma = sqrt(lambda) * 1.10;  // the reference inflates lambda_prev = lambda here
+        conv = 0;
+        done = true;
+      }
+      lambda_prev = lambda;
+    }
+    if (done) {
+      if (rank == 0 && tid == 0) {
+        a.state[0] = sigma;
+        a.state[1] = (double)it;
+        a.state[2] = (double)conv;
+      }
+      cluster.sync();  // no CTA leaves while another may still write into its records
+      return;
+    }
+  }
+}
+
+template <int NN>
+cudaError_t power_cluster_n(const PowerLoopArgs& a, cudaStream_t s) {
+  const long long ppc = (a.N + kPcCta - 1) / kPcCta;
+  const size_t bytes = (size_t)pc_smem_doubles<NN>(ppc) * sizeof(double);
+  const void* fn = (const void*)power_cluster_kernel<NN>;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(kPcCta);
+  cfg.blockDim = dim3(kPcThreads);
+  cfg.dynamicSmemBytes = bytes;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = kPcCta;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, power_cluster_kernel<NN>, a, ppc);
+}
+using PowerClusterFn = cudaError_t (*)(const PowerLoopArgs&, cudaStream_t);
+
 template <int NN>
 void power_loop_n(const PowerLoopArgs& a, int grid, cudaStream_t s, cudaError_t* err) {
   void* args[] = {const_cast<PowerLoopArgs*>(&a)};
@@ -456,6 +674,44 @@ void power_loop_n(const PowerLoopArgs& a, int grid, cudaStream_t s, cudaError_t*
 using PowerLoopFn = void (*)(const PowerLoopArgs&, int, cudaStream_t, cudaError_t*);
 
 }  // namespace
+
+// sigma start vector (operators.cpp:309-313): Box-Muller cosine branch of the
+// host-drawn uniform pairs of rng_stream(0x5eed, 97) (u12 interleaved), then
+// v / |v|. The device log/cos agree with the host's to within an ulp or two.
+constexpr int kSvBlocks = 148;
+__global__ void __launch_bounds__(256) start_normals_kernel(const double* u12, double* v, long long cols,
+                                                            double* part) {
+  double ss[1] = {0.0};
+  for (long long i = (long long)blockIdx.x * 256 + threadIdx.x; i < cols; i += (long long)kSvBlocks * 256) {
+    double a = u12[2 * i];
+    if (a <= 0.0) a = 0x1.0p-53;
+    const double x = sqrt(-2.0 * log(a)) * cos(6.28318530717958647692528676655900577 * u12[2 * i + 1]);
+    v[i] = x;
+    ss[0] = fma(x, x, ss[0]);
+  }
+  __shared__ double o[1];
+  block_reduce_store<1>(ss, o);
+  __syncthreads();
+  if (threadIdx.x == 0) part[blockIdx.x] = o[0];
+}
+__global__ void __launch_bounds__(256) start_scale_kernel(double* v, long long cols, const double* part) {
+  __shared__ double nv;
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int b = 0; b < kSvBlocks; ++b) t += part[b];  // fixed order, every block alike
+    nv = sqrt(t);
+  }
+  __syncthreads();
+  for (long long i = (long long)blockIdx.x * 256 + threadIdx.x; i < cols; i += (long long)kSvBlocks * 256)
+    v[i] = v[i] / nv;
+}
+
+cudaError_t launch_start_vector(const double* u12, double* v, long long cols, double* part,
+                                cudaStream_t s) {
+  start_normals_kernel<<<kSvBlocks, 256, 0, s>>>(u12, v, cols, part);
+  start_scale_kernel<<<kSvBlocks, 256, 0, s>>>(v, cols, part);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_gram(const double* X, long long N, int n, double* out, cudaStream_t s) {
   gram_kernel<<<n * n + n, kBlock, 0, s>>>(X, N, n, out);
@@ -471,7 +727,32 @@ int power_loop_grid(int sms, long long N) {
   return (int)std::max<long long>(16, std::min<long long>(sms, g));
 }
 
+// The cluster form when one CTA's share of the points fits its shared memory
+// (N = 1e4, n = 10: 105 KB per CTA) and n <= 10; otherwise the cooperative
+// grid loop.
+// CRB_SIGMA_CLUSTER=0 forces the grid loop.
+bool power_cluster_fits(long long N, int n) {
+  if (const char* e = std::getenv("CRB_SIGMA_CLUSTER"))
+    if (e[0] == '0') return false;
+  if (n > 10) return false;  // n > 10: the per-thread record spills at 512 threads
+  const long long ppc = (N + kPcCta - 1) / kPcCta;
+  const long long d = ppc * (2LL * n + 1) + (long long)n * n + n + 2LL * kPcCta * (4 + 2 * n) +
+                      (kPcThreads / 32 + 1) * (4LL + 2 * n);
+  return d * 8 <= 200 * 1024;
+}
+
 cudaError_t launch_power_loop(const PowerLoopArgs& a, int grid, cudaStream_t s) {
+  if (a.op == 0 && power_cluster_fits(a.N, a.n)) {
+    static constexpr PowerClusterFn ctab[kMaxN] = {
+#define CRB_PC(N) power_cluster_n<N>
+        CRB_N_SEQ(CRB_PC)
+#undef CRB_PC
+    };
+    if (a.n < 1 || a.n > kMaxN) return cudaErrorInvalidValue;
+    const cudaError_t e = ctab[a.n - 1](a, s);
+    if (e == cudaSuccess) return e;
+    cudaGetLastError();  // no cluster launch here: the grid loop below
+  }
   static constexpr PowerLoopFn tab[kMaxN] = {
 #define CRB_PL(N) power_loop_n<N>
       CRB_N_SEQ(CRB_PL)

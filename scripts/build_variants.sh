@@ -1,13 +1,15 @@
 #!/usr/bin/env bash
-# build n=10-only sweep variants in parallel: ab/<name>.so for each "name:flags" argument
+# build n=10-only variants of one source (SRC, default sweep_mma.cu) in parallel:
+# ab/<name>.so for each "name:flags" argument
 set -e
 B=build/cvxreg_b200
-objs=$(ls $B/*.o | grep -v sweep_mma.cu.o)
+SRC=${SRC:-sweep_mma.cu}
+objs=$(ls $B/*.o | grep -v $SRC.o)
 for spec in "$@"; do
   name=${spec%%:*}; flags=${spec#*:}
   ( /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 \
       -Xcompiler -fPIC -Xcompiler -ffp-contract=off -Iinclude -DCRB_N_LIST=10 $flags \
-      -c paper_1407_7220_b200/csrc/sweep_mma.cu -o /tmp/v_$name.o && \
+      -c paper_1407_7220_b200/csrc/$SRC -o /tmp/v_$name.o && \
     /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -shared -o ab/$name.so \
       /tmp/v_$name.o $objs -lnccl -lcudart_static -lrt -lpthread -ldl && echo built $name ) &
 done

@@ -581,6 +581,23 @@ def test_sigma_power_grid_sizes(oracle, monkeypatch, grid):
     assert abs(sg - so) <= 1e-10 * so
 
 
+@pytest.mark.parametrize("path", ["cluster", "grid"])
+@pytest.mark.parametrize("kind,N,n,pieces", [("maxaffine-uniform", 4000, 10, 20),
+                                             ("sqnorm-uniform", 1777, 5, 0),
+                                             ("quadratic", 901, 1, 0)])
+def test_sigma_cluster_and_grid_paths(oracle, monkeypatch, path, kind, N, n, pieces):
+    """sigma_max(C) from the single-cluster power loop (DSMEM records, n <= 10)
+    and from the cooperative grid loop: the oracle's step count and sigma."""
+    if path == "grid":
+        monkeypatch.setenv("CRB_SIGMA_CLUSTER", "0")
+    X, _ = instance(oracle, kind, N, n, 0.1, 5, pieces)
+    so, it_o, co = oracle.sigma_C(X)
+    with crb.DualSolver(X, np.zeros(len(X))) as d:
+        sg, it_g, cg = d.sigma_C()
+    assert it_g == it_o and cg == co
+    assert abs(sg - so) <= 1e-10 * so
+
+
 @pytest.mark.parametrize("graph_iters", [-1, 16])
 def test_fused_reduce_primal_parity(oracle, monkeypatch, graph_iters):
     """Opt-in fused K3 + Kc + K2 (CRB_FUSE=1): oracle parity, pieces and
