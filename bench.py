@@ -81,12 +81,14 @@ def measured_peaks():
         return {"hbm_gbs": 6650.0}, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic(cfgname, variant):
-    """dram bytes (read + write) per sweep launch from the committed ncu capture."""
+def ncu_traffic(cfgname, variant, warmup, steps):
+    """DRAM bytes (read + write) per sweep launch, averaged over the launches of this
+    command's timed region, from the committed ncu capture of the same command
+    (profiles/sweep_traffic.json); None when no capture matches the window."""
     try:
         with open(os.path.join(ROOT, "profiles", "sweep_traffic.json")) as f:
             d = json.load(f)
-        e = d.get(f"{cfgname}:{variant}")
+        e = d.get(f"{cfgname}:{variant}:w{warmup}k{steps}")
         return None if e is None else float(e["dram_bytes_per_launch"])
     except (OSError, ValueError, KeyError):
         return None
@@ -344,23 +346,27 @@ def run_ours(args):
     roofline = {
         "bound": "hbm", "unit": "GB/s", "achieved": achieved, "peak": peaks["hbm_gbs"],
         "frac": (achieved / peaks["hbm_gbs"]) if achieved else None,
-        "traffic": ncu_traffic(args.config if world == 1 else "", variant),
+        "traffic": ncu_traffic(args.config if world == 1 else "", variant, W, K),
+        "traffic_source": "ncu dram__bytes_read.sum + dram__bytes_write.sum, mean over the sweep "
+                          "launches of the same command's timed region (profiles/sweep_traffic.json)",
         "peak_kind": peak_kind, "kernel": f"sweep ({variant})",
         "algorithmic_bytes_per_launch": alg_bytes,
         "stores_per_launch": stores / K,
         "model_24B_per_pair_frac": (BYTES_PER_PAIR * rows * N / sweep_avg / 1e9 /
                                     peaks["hbm_gbs"]) if sweep_avg else None,
         "sweep_share_of_step": (sweep_s / dev_s) if dev_s > 0 else None,
-        "sweep_timing": "CUDA events on the solver stream around every 8th sweep launch of "
-                        "the timed region (uniform sample; the library's default, "
-                        "CRB_SWEEP_EVENTS=1 brackets every launch at ~2 % step cost)",
+        "sweep_timing": ("CUDA events on the solver stream around every sweep launch of the "
+                         "timed region" if K <= 64 else
+                         "CUDA events on the solver stream around every 8th sweep launch of the "
+                         "timed region (uniform sample; CRB_SWEEP_EVENTS=1 brackets every launch)"),
+        "sweep_launches_timed": K if K <= 64 else (K + 7) // 8,
         # secondary: fp64 flop per pair ~ 4n + 17
         "fp64_tflops": ((4 * n + 17) * rows * N / sweep_avg / 1e12) if sweep_avg else None,
         "note": "SURVEY 8(d) models 24 B per pair (read theta1, theta1_prev, write "
-                "theta1_new); the sweep does not rewrite a multiplier equal to the value "
-                "already in the target buffer, so the algorithmic bytes are the 16 B/pair "
-                "reads plus 8 B per store actually issued (counted on the device); "
-                "'model_24B_per_pair_frac' keeps the 24 B view",
+                "theta1_new); the sweep does not rewrite a 32-byte sector whose multipliers "
+                "are all unchanged (a sector with a change is written whole), so the "
+                "algorithmic bytes are the 16 B/pair reads plus 8 B per multiplier written "
+                "(counted on the device); 'model_24B_per_pair_frac' keeps the 24 B view",
     }
 
     extras = {}
