@@ -63,12 +63,16 @@ def parse():
                          "of the standalone ALCC (SURVEY 8f row f1); papg-alcc: one dual "
                          "iteration of the general-K P-APG(ALCC) (row f2)")
     ap.add_argument("--K", type=int, default=2, help="blocks for --solver papg-alcc")
+    ap.add_argument("--scaling", choices=["weak", "strong"], default="weak",
+                    help="weak (default): N = N_cfg sqrt(p), fixed pairs per GPU; strong: the "
+                         "config's own N on every p (BASELINE cfg 3 and 4 on 1/2/4/8 GPUs, "
+                         "cfg 5 on 8)")
     return ap.parse_args()
 
 
-def workload(name, world):
+def workload(name, world, scaling="weak"):
     c = dict(CONFIGS[name])
-    if world > 1:
+    if world > 1 and scaling == "weak":
         c["N"] = int(round(c["N"] * math.sqrt(world)))
     return c
 
@@ -293,7 +297,7 @@ def run_ours(args):
     import paper_1407_7220_b200 as crb
     from paper_1407_7220_b200.dist import sharded_solver
 
-    cfg = workload(args.config, world)
+    cfg = workload(args.config, world, args.scaling)
     N, n = cfg["N"], cfg["n"]
     data = crb.gen_instance(crb.GeneratorSpec(cfg["kind"], n, N, cfg["noise"], 1, cfg["pieces"]))
     prep = crb.prepare_problem(data)
@@ -324,12 +328,13 @@ def run_ours(args):
         torch.cuda.synchronize()
         barrier()
     dev_s, launches, sweep_s = solver.last_timing()
+    xchg_s = solver.last_exchange_seconds()
     stores = solver.sweep_store_count()
     assert done - done0 == K and not stopped, (done, done0, stopped)
-    t = torch.tensor([dev_s, sweep_s], dtype=torch.float64, device="cuda")
+    t = torch.tensor([dev_s, sweep_s, xchg_s], dtype=torch.float64, device="cuda")
     if dist is not None:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    dev_max, sweep_max = float(t[0]), float(t[1])
+    dev_max, sweep_max, xchg_max = float(t[0]), float(t[1]), float(t[2])
     rows = solver.row_end - solver.row_begin
     variant = solver.sweep_variant
     solver.close()
@@ -448,11 +453,12 @@ def run_ours(args):
         line = {
             "metric": "pair-constraint updates/s", "value": value, "unit": "pair-updates/s",
             "n_gpus": world, "steps": K, "warmup": W, "ms_per_step": dev_max / K * 1e3,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded BASELINE generator)",
             "config": {"workload": f"{args.config}: {cfg['kind']} N={N} n={n} "
                                    f"pieces={cfg['pieces']} noise={cfg['noise']}"
-                                   + (" (weak scaling N=1e4*sqrt(p))" if world > 1 else ""),
+                                   + (" (weak scaling N=N_cfg*sqrt(p))" if world > 1 and
+                                      args.scaling == "weak" else ""),
                        "N": N, "n": n, "pairs_per_step": pairs_step,
                        "rows_per_gpu": rows, "sweep_variant": variant,
                        "l2": (f"inputs > L2 (V, V' = {16 * rows * N / 1e9:.3g} GB per GPU), no flush"
@@ -465,6 +471,11 @@ def run_ours(args):
             "roofline": roofline, "cpu_baseline": cpu, "gpu_launches": launches,
             "clocks": clk.summary(),
         }
+        if world > 1:
+            # the per-iteration ncclAllReduce of the N(n+2)+4 payload (device time, max over
+            # ranks, events around it in the bracketed iterations)
+            line["exchange"] = {"seconds": xchg_max, "share_of_step": xchg_max / dev_max,
+                                "payload_doubles": N * (n + 2) + 4}
         line.update(extras)
         print(json.dumps(line), flush=True)
     if dist is not None:

@@ -173,6 +173,10 @@ cr_status cr_last_timing(const cr_handle *h, double *seconds, int64_t *launches,
    8th; CRB_SWEEP_EVENTS=k overrides), in launch order: up to cap into out,
    *count = how many there were. */
 cr_status cr_last_sweep_times(const cr_handle *h, double *out, int64_t cap, int64_t *count);
+/* Sharded runs: device time of the per-iteration ncclAllReduce in the last
+   cr_papg_iterate call, from CUDA events around it in the same iterations whose
+   sweeps are bracketed (scaled to all iterations when sampled); 0 otherwise. */
+cr_status cr_last_exchange_seconds(const cr_handle *h, double *seconds);
 /* sweep kernel variant chosen for this handle: 0 = CUDA-core DFMA,
    1 = FP64 tensor-core DMMA (override with CRB_SWEEP=dfma|mma) */
 int32_t cr_sweep_variant(const cr_handle *h);

@@ -71,7 +71,7 @@ EXPORTS = [
     "cr_attach_nccl", "cr_exchange_len", "cr_sigma_C", "cr_papg_begin", "cr_papg_iterate",
     "cr_iter_local", "cr_exchange_get", "cr_exchange_put", "cr_iter_finish", "cr_papg_finish",
     "cr_papg_solve", "cr_get_theta", "cr_get_rows", "cr_get_theta_rows", "cr_get_rows_window",
-    "cr_last_timing", "cr_last_sweep_times", "cr_time_sweep",
+    "cr_last_timing", "cr_last_sweep_times", "cr_last_exchange_seconds", "cr_time_sweep",
     "cr_sweep_variant", "cr_papg_begin_resume", "cr_set_observations", "cr_infeasibility",
     "cr_duality_gap", "cr_evaluate_estimator", "cr_repair_feasibility",
     "cr_gen_instance", "cr_prepare_problem", "cr_certificate", "cr_momentum_next",
@@ -121,6 +121,7 @@ def load():
         "cr_get_rows_window": (st, [vp, i64, i64, _P]),
         "cr_last_timing": (st, [vp, _P, C.POINTER(i64), _P]),
         "cr_last_sweep_times": (st, [vp, _P, i64, C.POINTER(i64)]),
+        "cr_last_exchange_seconds": (st, [vp, _P]),
         "cr_time_sweep": (st, [vp, i32, _P]),
         "cr_sweep_variant": (i32, [vp]),
         "cr_papg_begin_resume": (st, [vp, C.POINTER(PapgConfigC)]),

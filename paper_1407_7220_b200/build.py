@@ -22,9 +22,8 @@ NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
                      "-Xcompiler", "-ffp-contract=off", "-I" + os.path.join(ROOT, "include")]
 CXX_FLAGS = ["-O2", "-std=c++17", "-fPIC", "-ffp-contract=off", "-Wall", "-Wextra",
              "-I" + os.path.join(ROOT, "include")]
-CU_SOURCES = ["sweep.cu", "sweep_mma.cu", "kernels.cu", "small.cu", "power.cu", "metrics.cu", "capi.cu",
-              "alcc.cu", "general.cu", "balcc.cu",
-              "sweep_sparse.cu"]
+CU_SOURCES = ["sweep_mma.cu", "kernels.cu", "small.cu", "power.cu", "metrics.cu", "capi.cu",
+              "alcc.cu", "general.cu", "balcc.cu"]
 CXX_SOURCES = ["host.cpp"]
 HEADERS = ["device.cuh", "kernels.cuh", "host.hpp", "pipeline.cuh", "iteration.cuh", "small.cuh",
            "handle.cuh", "balcc.cuh", "mma_geo.cuh"]

@@ -702,13 +702,8 @@ cr_status ensure_alcc(cr_handle* h, bool allow_loop) {
   std::memset(b.host, 0, sizeof(AlccDev));
   CUDA_TRY(cudaMemsetAsync(b.counter, 0, sizeof(unsigned int), h->st));
   const int pen = kModePenalty, upd = kModePenaltyUpdate;
-  if (h->variant == kSweepMma) {
-    b.kpen = sweep_mma_info((int)h->n, pen);
-    b.kupd = sweep_mma_info((int)h->n, upd);
-  } else {
-    b.kpen = sweep_dfma_info((int)h->n, pen);
-    b.kupd = sweep_dfma_info((int)h->n, upd);
-  }
+  b.kpen = sweep_mma_info((int)h->n, pen);
+  b.kupd = sweep_mma_info((int)h->n, upd);
   if (!b.kpen.fn || !b.kupd.fn || b.kpen.max_blocks_per_sm < 1 || b.kupd.max_blocks_per_sm < 1)
     return fail(h, CR_EINVAL, "alcc: no penalty sweep kernel for this n");
   // small sub-problems: one cooperative launch per MAPG call (CRB_ALCC_LOOP=0 disables)

@@ -144,36 +144,9 @@ PrimalArgs primal_args(cr_handle* h, int mode) {
 
 // Enqueue one dual iteration (papg.cpp:176-263). phase: 0 = all,
 // 1 = local part only (K2, K1, K3), 2 = finish only (control).
-// The fused path (one GPU, singleton blocks, dense store): K3 + Kc + the next
-// iteration's K2 in one launch; the standalone primal is enqueued only at the
-// start of an iterate call / graph and is a no-op when the last fused launch
-// already computed it (DevCtrl::primal_done). Opt-in: CRB_FUSE=1.
-
-bool fused_path(const cr_handle* h) {
-  return h->fuse_ok && h->comm == nullptr && h->part.K == 0 && !h->masked;
-}
 
 cr_status enqueue_iteration(cr_handle* h, int phase, cudaEvent_t ev_a, cudaEvent_t ev_b,
-                            bool use_nccl) {
-  if (phase == 0 && fused_path(h)) {
-    if (h->primal_pending) {
-      PrimalArgs pa = primal_args(h, 0);
-      pa.fuse_ctrl = h->ctrl_d;
-      CUDA_TRY(launch_primal(pa, h->st));
-      h->primal_pending = false;
-    }
-    const SweepArgs sa = sweep_args(h, kModePapg, false);
-    if (ev_a) CUDA_TRY(cudaEventRecord(ev_a, h->st));
-    CUDA_TRY((cudaError_t)launch_sweep(papg_sweep(h), sa, h->st));
-    if (ev_b) CUDA_TRY(cudaEventRecord(ev_b, h->st));
-    FusedArgs fa{};
-    fa.r = reduce_args(h, true, &h->ctrl_d->halt, true, papg_sweep(h).scal_recs);
-    fa.p = primal_args(h, 0);
-    fa.ticket = h->fuse_sync;
-    fa.flag = h->fuse_sync + 1;
-    CUDA_TRY(launch_reduce_primal(fa, h->st));
-    return CR_OK;
-  }
+                            bool use_nccl, cudaEvent_t ev_c, cudaEvent_t ev_d) {
   if (phase != 2) {
     const PrimalArgs pa = primal_args(h, 0);
     CUDA_TRY(launch_primal(pa, h->st));
@@ -186,9 +159,12 @@ cr_status enqueue_iteration(cr_handle* h, int phase, cudaEvent_t ev_a, cudaEvent
     const ReduceArgs ra =
         reduce_args(h, true, &h->ctrl_d->halt, fuse, papg_sweep(h).scal_recs);
     CUDA_TRY(launch_reduce(ra, h->st));
-    if (use_nccl && h->comm)
+    if (use_nccl && h->comm) {
+      if (ev_c) CUDA_TRY(cudaEventRecord(ev_c, h->st));
       NCCL_TRY(ncclAllReduce(h->xbuf, h->xbuf, (size_t)payload_len(h), ncclDouble, ncclSum,
                              h->comm, h->st));
+      if (ev_d) CUDA_TRY(cudaEventRecord(ev_d, h->st));
+    }
     if (fuse) return CR_OK;
   }
   if (phase != 1)
@@ -197,7 +173,7 @@ cr_status enqueue_iteration(cr_handle* h, int phase, cudaEvent_t ev_a, cudaEvent
 }
 
 // our kernels per iteration (the NCCL allreduce kernel is not counted)
-int launches_per_iteration(const cr_handle* h) { return h->comm ? 4 : (fused_path(h) ? 2 : 3); }
+int launches_per_iteration(const cr_handle* h) { return h->comm ? 4 : 3; }
 
 cr_status build_graph(cr_handle* h) {
   if (h->gexec) {
@@ -209,7 +185,7 @@ cr_status build_graph(cr_handle* h) {
   cr_status s = CR_OK;
   h->primal_pending = true;  // each graph launch starts with the (no-op unless needed) primal
   for (int i = 0; i < h->graph_iters && s == CR_OK; ++i)
-    s = enqueue_iteration(h, 0, nullptr, nullptr, true);
+    s = enqueue_iteration(h, 0, nullptr, nullptr, true, nullptr, nullptr);
   cudaError_t e = cudaStreamEndCapture(h->st, &g);
   if (s != CR_OK) {
     if (g) cudaGraphDestroy(g);
@@ -332,34 +308,10 @@ cr_status cr_create(const double* Xh, const double* ybar_shifted, int64_t N, int
   tmark("stream");
   keep_pool_memory(device);
   g_alloc_stream = h->st;
-  // sweep variant, measured on B200: the DMMA sweep is
-  // faster than the CUDA-core DFMA one for every n. CRB_SWEEP=dfma|mma overrides.
-  // fused reduce + primal: opt-in (CRB_FUSE=1). Measured slower than the two
-  // kernels at cfg 2 (24.8 vs 21.9 us of non-sweep time per step): the control
-  // step sits on its critical path behind 2220 per-warp scalar records
-  const char* fz = std::getenv("CRB_FUSE");
-  h->fuse_ok = fz && fz[0] == '1';
-  const char* var = std::getenv("CRB_SWEEP");
+  // the FP64 tensor-core (DMMA) pair sweep for every n
   h->variant = kSweepMma;
-  if (var && std::strcmp(var, "dfma") == 0) h->variant = kSweepDfma;
-  if (var && std::strcmp(var, "mma") == 0) h->variant = kSweepMma;
-  // masked dual store (sweep_sparse.cu), opt-in with CRB_SPARSE=1: it moves
-  // 12x fewer bytes but is issue bound and not faster than the dense sweep
-  // (DESIGN.md section 10b); DMMA geometry for every n
-  const char* sp = std::getenv("CRB_SPARSE");
-  h->sparse_ok = (sp && sp[0] == '1') && !(var && std::strcmp(var, "dfma") == 0);
-  if (h->sparse_ok) {
-    h->variant = kSweepMma;
-    h->ksp = sweep_sparse_info((int)n, false);
-    if (!h->ksp.fn || h->ksp.max_blocks_per_sm < 1) h->sparse_ok = false;
-  }
-  if (h->variant == kSweepMma) {
-    h->kp = sweep_mma_info((int)n, kModePapg);
-    h->kw = sweep_mma_info((int)n, kModePower);
-  } else {
-    h->kp = sweep_dfma_info((int)n, kModePapg);
-    h->kw = sweep_dfma_info((int)n, kModePower);
-  }
+  h->kp = sweep_mma_info((int)n, kModePapg);
+  h->kw = sweep_mma_info((int)n, kModePower);
   if (!h->kp.fn || !h->kw.fn || h->kp.max_blocks_per_sm < 1)
     return fail(h, CR_EINVAL, "no sweep kernel for this n");
   tmark("kernel info");
@@ -392,22 +344,15 @@ cr_status cr_create(const double* Xh, const double* ybar_shifted, int64_t N, int
   // + one column tile of slack: the tensor-map view of the last tile's row ends
   ALLOC(h->V[0], vlen + h->kp.tile_cols);
   ALLOC(h->V[1], vlen + h->kp.tile_cols);
-  if (h->sparse_ok) {
-    h->mstages = (int)((h->U + 7) / 8 + h->maxspan);
-    ALLOC(h->M[0], mask_words(h));
-    ALLOC(h->M[1], mask_words(h));
-  }
   ALLOC(h->vpos[0], N);
   ALLOC(h->vpos[1], N);
   ALLOC(h->xbuf, payload_len(h));
   ALLOC(h->aggsave, payload_len(h));
   ALLOC(h->colpart, (size_t)h->G * h->maxspan * h->kp.tile_cols * (n + 1));
   ALLOC(h->rowpart, (size_t)h->T * h->R);
-  ALLOC(h->scalpart, (size_t)h->G * std::max(h->kp.warps_per_block,
-                                              h->sparse_ok ? h->ksp.warps_per_block : 0) *
-                        kScal);
-  // K2 records of the standalone primal (k2_blocks) or the fused kernel's point blocks
-  ALLOC(h->k2part, (size_t)std::max(h->k2_blocks, fused_blocks(N)) * kK2Scal);
+  ALLOC(h->scalpart, (size_t)h->G * h->kp.warps_per_block * kScal);
+  // K2 records of the primal (k2_blocks)
+  ALLOC(h->k2part, (size_t)h->k2_blocks * kK2Scal);
   ALLOC(h->k2sum, kK2Scal);
   ALLOC(h->yout, N);
   ALLOC(h->xiout, N * n);
@@ -425,7 +370,6 @@ cr_status cr_create(const double* Xh, const double* ybar_shifted, int64_t N, int
   ALLOC(h->consts, 4);
   ALLOC(h->izero, 1);
   ALLOC(h->counter, 1);
-  ALLOC(h->fuse_sync, 2);
   ALLOC(h->d_stores, 1);
   ALLOC(h->ctrl_d, 1);
 #undef ALLOC
@@ -461,7 +405,6 @@ cr_status cr_create(const double* Xh, const double* ybar_shifted, int64_t N, int
   CUDA_TRY(cudaMemcpyAsync(h->consts, consts, sizeof(consts), cudaMemcpyHostToDevice, h->st));
   CUDA_TRY(cudaMemsetAsync(h->izero, 0, sizeof(int), h->st));
   CUDA_TRY(cudaMemsetAsync(h->counter, 0, sizeof(unsigned int), h->st));
-  CUDA_TRY(cudaMemsetAsync(h->fuse_sync, 0, 2 * sizeof(unsigned long long), h->st));
   CUDA_TRY(cudaMemsetAsync(h->d_stores, 0, sizeof(unsigned long long), h->st));
   CUDA_TRY(cudaMemsetAsync(h->ctrl_d, 0, sizeof(DevCtrl), h->st));
   CUDA_TRY(launch_gram(h->X, N, (int)n, h->gram, h->st));
@@ -491,9 +434,6 @@ void cr_destroy(cr_handle* h) {
   for (double* b : {h->s_colpart, h->s_rowpart, h->s_scalpart, h->s_k2part}) dfree(b, h->st);
   dfree(h->izero, h->st);
   dfree(h->counter, h->st);
-  dfree(h->fuse_sync, h->st);
-  dfree(h->M[0], h->st);
-  dfree(h->M[1], h->st);
   dfree(h->d_stores, h->st);
   dfree(h->ctrl_d, h->st);
   if (h->st) cudaStreamSynchronize(h->st);
@@ -717,18 +657,7 @@ cr_status begin_impl(cr_handle* h, const cr_papg_config* cfg, const double* thet
   if (smenv && smenv[0] == '0') want_small = false;
   if (smenv && smenv[0] == '1' && h->comm == nullptr && h->R == h->N && h->part.K == 0)
     want_small = true;
-  // masked dual store for the per-kernel path; a resumed solve keeps the layout
-  // of the state it continues
-  if (resume) {
-    if (h->masked) want_small = false;
-  } else {
-    h->masked = h->sparse_ok && !want_small;
-  }
   if (!resume) {
-    if (h->masked) {
-      CUDA_TRY(cudaMemsetAsync(h->M[0], 0, sizeof(uint32_t) * mask_words(h), h->st));
-      CUDA_TRY(cudaMemsetAsync(h->M[1], 0, sizeof(uint32_t) * mask_words(h), h->st));
-    }
     CUDA_TRY(cudaMemsetAsync(h->V[0], 0, vbytes, h->st));
     CUDA_TRY(cudaMemsetAsync(h->V[1], 0, vbytes, h->st));
     CUDA_TRY(cudaMemsetAsync(h->vpos[0], 0, sizeof(double) * N, h->st));
@@ -760,8 +689,6 @@ cr_status begin_impl(cr_handle* h, const cr_papg_config* cfg, const double* thet
     }
     CUDA_TRY(cudaMemcpyAsync(h->stage, tpos, sizeof(double) * N, cudaMemcpyHostToDevice, h->st));
     CUDA_TRY(launch_pos_in(h->vpos[0], h->stage, N, h->st));
-    if (h->masked)
-      CUDA_TRY(launch_mask_build(h->V[0], h->M[0], N, h->ld, mask_geo(h), h->G, h->st));
     // aggregates and |.|^2 of max(theta0, 0): a sweep with 1/L = 0 is a copy
     const SweepArgs sa = sweep_args(h, kModePapg, true);
     CUDA_TRY((cudaError_t)launch_sweep(papg_sweep(h), sa, h->st));
@@ -950,7 +877,6 @@ cr_status cr_papg_iterate(cr_handle* h, int64_t max_steps, int64_t* done, int32_
   if (h->graph_iters == 0)
     if (const char* pu = std::getenv("CRB_POLL_UNIT")) per_unit = std::max(1, std::atoi(pu));
   h->primal_pending = true;  // direct launches: the call starts with the (maybe no-op) primal
-  int64_t extra_launches = (h->graph_iters == 0 && fused_path(h)) ? 1 : 0;
   int64_t enq_iters = 0;
   int64_t units = 0;
   bool halted = h->ctrl_h->stopped || max_steps == 0;
@@ -962,19 +888,24 @@ cr_status cr_papg_iterate(cr_handle* h, int64_t max_steps, int64_t* done, int32_
       CUDA_TRY(cudaGraphLaunch(h->gexec, h->st));
     } else {
       for (int i = 0; i < per_unit && enq_iters + i < max_steps; ++i) {
-        cudaEvent_t a = nullptr, b = nullptr;
+        cudaEvent_t a = nullptr, b = nullptr, c = nullptr, d = nullptr;
         const bool sample = every > 0 && ((enq_iters + i) % every) == 0;
         if (timed_sweeps && sample && timed_pairs < (1 << 16)) {  // event pairs created on demand
-          while (h->ev_sweep.size() < (size_t)(2 * timed_pairs + 2)) {
+          const size_t per = h->comm ? 4 : 2;  // sharded: the allreduce is bracketed too
+          while (h->ev_sweep.size() < (size_t)(per * timed_pairs + per)) {
             cudaEvent_t e;
             CUDA_TRY(cudaEventCreate(&e));
             h->ev_sweep.push_back(e);
           }
-          a = h->ev_sweep[2 * timed_pairs];
-          b = h->ev_sweep[2 * timed_pairs + 1];
+          a = h->ev_sweep[per * timed_pairs];
+          b = h->ev_sweep[per * timed_pairs + 1];
+          if (h->comm) {
+            c = h->ev_sweep[per * timed_pairs + 2];
+            d = h->ev_sweep[per * timed_pairs + 3];
+          }
           ++timed_pairs;
         }
-        s = enqueue_iteration(h, 0, a, b, true);
+        s = enqueue_iteration(h, 0, a, b, true, c, d);
         if (s != CR_OK) return s;
       }
     }
@@ -1004,23 +935,29 @@ cr_status cr_papg_iterate(cr_handle* h, int64_t max_steps, int64_t* done, int32_
   float ms = 0;
   CUDA_TRY(cudaEventElapsedTime(&ms, h->ev_start, h->ev_end));
   h->last_seconds = units > 0 ? ms * 1e-3 : 0.0;
-  double sw = 0;
+  double sw = 0, xw = 0;
   h->last_sweep_times.clear();
+  const int64_t per = h->comm ? 4 : 2;
   for (int64_t i = 0; i < timed_pairs; ++i) {
     float m = 0;
-    CUDA_TRY(cudaEventElapsedTime(&m, h->ev_sweep[2 * i], h->ev_sweep[2 * i + 1]));
+    CUDA_TRY(cudaEventElapsedTime(&m, h->ev_sweep[per * i], h->ev_sweep[per * i + 1]));
     sw += m * 1e-3;
     h->last_sweep_times.push_back(m * 1e-3);
+    if (h->comm) {
+      float mx = 0;
+      CUDA_TRY(cudaEventElapsedTime(&mx, h->ev_sweep[per * i + 2], h->ev_sweep[per * i + 3]));
+      xw += mx * 1e-3;
+    }
   }
   {
     const int64_t ran = std::min<int64_t>(enq_iters, max_steps);
-    h->last_sweep_seconds =
-        (timed_pairs > 0 && every > 1) ? sw * (double)ran / (double)timed_pairs : sw;
+    const double scale = (timed_pairs > 0 && every > 1) ? (double)ran / (double)timed_pairs : 1.0;
+    h->last_sweep_seconds = sw * scale;
+    h->last_exchange_seconds = xw * scale;
   }
   h->last_launches = (h->graph_iters > 0 ? units * h->graph_iters
                                          : std::min<int64_t>(enq_iters, max_steps)) *
-                         launches_per_iteration(h) +
-                     (h->graph_iters > 0 && fused_path(h) ? units : extra_launches);
+                         launches_per_iteration(h);
   h->loop_seconds +=
       std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();
   if (done) *done = h->ctrl_h->ell;
@@ -1037,7 +974,7 @@ cr_status cr_iter_local(cr_handle* h) {
   CUDA_TRY(cudaSetDevice(h->device));
   cr_status s = set_pause(h, LLONG_MAX);
   if (s != CR_OK) return s;
-  s = enqueue_iteration(h, 1, nullptr, nullptr, false);
+  s = enqueue_iteration(h, 1, nullptr, nullptr, false, nullptr, nullptr);
   if (s != CR_OK) return s;
   CUDA_TRY(cudaStreamSynchronize(h->st));
   return CR_OK;
@@ -1062,7 +999,7 @@ cr_status cr_exchange_put(cr_handle* h, const double* buf) {
 cr_status cr_iter_finish(cr_handle* h, int32_t* stopped) {
   if (!h) return CR_EINVAL;
   if (!h->begun) return fail(h, CR_ESTATE, "papg: iterate before begin");
-  cr_status s = enqueue_iteration(h, 2, nullptr, nullptr, false);
+  cr_status s = enqueue_iteration(h, 2, nullptr, nullptr, false, nullptr, nullptr);
   if (s != CR_OK) return s;
   s = sync_ctrl(h);
   if (s != CR_OK) return s;
@@ -1150,8 +1087,7 @@ static cr_status get_theta_window(cr_handle* h, int64_t la, int64_t lb, double* 
   const int64_t rows_per = std::max<int64_t>(1, h->stage_elems / rowlen);
   for (int64_t ra = la; ra < lb; ra += rows_per) {
     const int64_t rb = std::min(lb, ra + rows_per);
-    CUDA_TRY(launch_theta_out(h->stage, h->V[cur], sc, h->N, h->ld, h->r0, ra, rb, h->st,
-                              h->masked ? h->M[cur] : nullptr, mask_geo(h)));
+    CUDA_TRY(launch_theta_out(h->stage, h->V[cur], sc, h->N, h->ld, h->r0, ra, rb, h->st));
     CUDA_TRY(cudaMemcpyAsync(out + (ra - la) * rowlen, h->stage, sizeof(double) * (rb - ra) * rowlen,
                              cudaMemcpyDeviceToHost, h->st));
     CUDA_TRY(cudaStreamSynchronize(h->st));
@@ -1227,6 +1163,12 @@ cr_status cr_last_timing(const cr_handle* h, double* seconds, int64_t* launches,
   if (seconds) *seconds = h->last_seconds;
   if (launches) *launches = h->last_launches;
   if (sweep_seconds) *sweep_seconds = h->last_sweep_seconds;
+  return CR_OK;
+}
+
+cr_status cr_last_exchange_seconds(const cr_handle* h, double* seconds) {
+  if (!h || !seconds) return CR_EINVAL;
+  *seconds = h->last_exchange_seconds;
   return CR_OK;
 }
 
@@ -1309,8 +1251,6 @@ cr_status pair_metrics(cr_handle* h, PointBufs& b, bool with_theta, double out[2
   a.rowrec = b.rowrec;
   a.colrec = b.colrec;
   a.V = with_theta ? h->V[h->ctrl_h->cur] : nullptr;
-  a.M = (with_theta && h->masked) ? h->M[h->ctrl_h->cur] : nullptr;
-  a.mg = mask_geo(h);
   a.s = h->ctrl_h->s_cur;
   a.part = b.part;
   a.N = h->N;

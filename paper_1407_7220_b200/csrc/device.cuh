@@ -76,11 +76,6 @@ struct DevCtrl {
   // general-K partition: |within-block infeasibility| of the current eta
   // (dual_gradient's within_infeas_raw, papg.cpp:128), host-set per iteration
   double within_raw;
-  // fused reduce + primal (kernels.cu): 1 when the primal of the next iteration
-  // has been computed (the standalone primal kernel is then a no-op); k2_count =
-  // number of K2 records the last primal wrote
-  int primal_done;
-  int k2_count;
 };
 
 // opaque CUtensorMap (cuda.h): 128 bytes, 64-byte aligned; encoded on the host
@@ -117,47 +112,7 @@ struct SweepArgs {
   long long nbar;         // block size of the partition: pairs inside one block are
                           // masked like the diagonal (1: singleton blocks)
   unsigned long long* stores;  // optional: multipliers written by the P-APG sweep
-  uint32_t* M0;           // masked dual store (sweep_sparse.cu): live words of V[0], V[1]
-  uint32_t* M1;
-  int mstages;            // mask stage capacity per CTA (MaskGeo::stages)
 };
-
-// Masked dual store (sweep_sparse.cu): one 32-bit live word per 8-row x 8-column
-// MMA tile in the ballot order of its fragments (bit 4 c + q = column c, row
-// 2q + j of the tile, j selecting one of the tile's two words). Words are stored
-// per sweep CTA and per stage of that CTA's (static) unit range -- the split
-// is the same every iteration, so a CTA reads back exactly the words it wrote
-// and no word is shared between CTAs: [G][stages][TC/4] per buffer. A clear
-// bit means 0 whatever V holds.
-struct MaskGeo {
-  long long R, U;  // rows of the shard, (tile, row) units per sweep CTA
-  int TC;          // columns per tile
-  int stages;      // stage capacity per CTA (ceil(U/8) + segments)
-};
-__host__ __device__ __forceinline__ long long mask_word(const MaskGeo& g, long long r,
-                                                       long long col, int* bit) {
-  const long long t = col / g.TC;
-  const int cl = (int)(col - t * g.TC);
-  const long long u = t * g.R + r;
-  const long long cta = u / g.U;
-  const long long u0 = cta * g.U, u1 = u0 + g.U;
-  long long k = 0;
-  for (long long tt = u0 / g.R; tt < t; ++tt) {  // stages of the CTA's earlier segments
-    const long long lo = (u0 > tt * g.R ? u0 : tt * g.R), hi = (u1 < (tt + 1) * g.R ? u1 : (tt + 1) * g.R);
-    k += (hi - lo + 7) / 8;
-  }
-  const long long rs = (u0 > t * g.R ? u0 : t * g.R) - t * g.R;
-  k += (r - rs) / 8;
-  const int rr = (int)((r - rs) % 8);
-  *bit = 4 * (cl & 7) + (rr >> 1);
-  return (cta * g.stages + k) * (g.TC / 4) + (cl >> 3) * 2 + (rr & 1);
-}
-__host__ __device__ __forceinline__ bool mask_live(const uint32_t* M, const MaskGeo& g, long long r,
-                                                   long long col) {
-  int bit;
-  const long long w = mask_word(g, r, col, &bit);
-  return (M[w] >> bit) & 1u;
-}
 
 // same block of the partition. BLK = false: singleton blocks (the diagonal);
 // the blocked test is a separate instantiation so the singleton kernels carry
@@ -194,12 +149,10 @@ struct SweepKernelInfo {
   int threads;
   int smem_bytes;
 };
-enum SweepVariant { kSweepDfma = 0, kSweepMma = 1 };
+enum SweepVariant { kSweepMma = 1 };  // the FP64 tensor-core sweep (the DFMA one was removed)
 // blocked = true: same-block pairs of a K-block partition masked (kModePapg /
 // kModePower only)
-SweepKernelInfo sweep_dfma_info(int n, int mode, bool blocked = false);  // sweep.cu (CUDA-core DFMA)
 SweepKernelInfo sweep_mma_info(int n, int mode, bool blocked = false);   // sweep_mma.cu (DMMA)
-SweepKernelInfo sweep_sparse_info(int n, bool blocked = false);  // sweep_sparse.cu (masked, P-APG)
 int launch_sweep(const SweepKernelInfo& info, const SweepArgs& a, void* stream);
 
 }  // namespace crb

@@ -169,14 +169,12 @@ __device__ __forceinline__ void cross_pair(long long idx, long long K, long long
 }
 
 __global__ void theta_k_out_kernel(double* stage, const double* V, double s, long long K,
-                                   long long nbar, long long ld, long long a, long long b,
-                                   const uint32_t* M, MaskGeo mg) {
+                                   long long nbar, long long ld, long long a, long long b) {
   for (long long i = a + (long long)blockIdx.x * blockDim.x + threadIdx.x; i < b;
        i += (long long)gridDim.x * blockDim.x) {
     long long l1, l2;
     cross_pair(i, K, nbar, &l1, &l2);
-    const bool live = M == nullptr || mask_live(M, mg, l1, l2);
-    stage[i - a] = live ? s * V[l1 * ld + l2] : 0.0;
+    stage[i - a] = s * V[l1 * ld + l2];
   }
 }
 
@@ -384,22 +382,12 @@ cr_status solve_blocks(cr_handle* h, double tol, double* within) {
 cr_status select_sweeps(cr_handle* h, bool blocked) {
   const int n = (int)h->n;
   SweepKernelInfo kp, kw;
-  if (h->variant == kSweepMma) {
-    kp = sweep_mma_info(n, kModePapg, blocked);
-    kw = sweep_mma_info(n, kModePower, blocked);
-  } else {
-    kp = sweep_dfma_info(n, kModePapg, blocked);
-    kw = sweep_dfma_info(n, kModePower, blocked);
-  }
+  kp = sweep_mma_info(n, kModePapg, blocked);
+  kw = sweep_mma_info(n, kModePower, blocked);
   if (!kp.fn || !kw.fn || kp.max_blocks_per_sm < 1 || kp.tile_cols != h->kp.tile_cols)
     return fail(h, CR_EINVAL, "partition: no blocked sweep kernel for this n");
   h->kp = kp;
   h->kw = kw;
-  if (h->sparse_ok) {
-    h->ksp = sweep_sparse_info(n, blocked);
-    if (!h->ksp.fn || h->ksp.max_blocks_per_sm < 1)
-      return fail(h, CR_EINVAL, "partition: no masked sweep kernel for this n");
-  }
   return CR_OK;
 }
 
@@ -498,8 +486,7 @@ cr_status general_get_theta(cr_handle* h, double* out) {
   for (long long a = 0; a < cross; a += h->stage_elems) {
     const long long b = std::min<long long>(cross, a + h->stage_elems);
     theta_k_out_kernel<<<grid_of(b - a), 256, 0, h->st>>>(
-        h->stage, h->V[cur], sc, P.K, P.nbar, h->ld, a, b, h->masked ? h->M[cur] : nullptr,
-        mask_geo(h));
+        h->stage, h->V[cur], sc, P.K, P.nbar, h->ld, a, b);
     CUDA_TRY(cudaGetLastError());
     CUDA_TRY(cudaMemcpyAsync(out + a, h->stage, sizeof(double) * (b - a), cudaMemcpyDeviceToHost,
                              h->st));

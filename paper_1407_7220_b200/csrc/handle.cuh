@@ -77,7 +77,7 @@ struct cr_handle {
   SweepKernelInfo kp{}, kw{};
   int S = 0;            // column strips
   int T = 0;            // sweep CTA column tiles = row-sum slices
-  int variant = 0;      // kSweepDfma / kSweepMma
+  int variant = kSweepMma;
   // persistent small-N loop (small.cu)
   bool small_mode = false;
   SmallInfo ks{};
@@ -88,9 +88,9 @@ struct cr_handle {
   long long U = 0;      // (tile, row) units per CTA
   int k2_blocks = 0;
   unsigned int* counter = nullptr;
-  // fused reduce + primal (single GPU): block start tickets and the control flag
-  unsigned long long* fuse_sync = nullptr;  // [ticket, flag]
-  bool fuse_ok = false;       // this handle may run the fused path (CRB_FUSE != 0, one GPU)
+  unsigned long long* d_stores = nullptr;  // multipliers written by the P-APG sweeps
+  TmapBytes tmV[2] = {};    // tensor maps of V[0], V[1] for the DMMA P-APG producer
+  bool tmap_ok = false;
   bool primal_pending = true; // enqueue the (possibly no-op) standalone primal next
   // device buffers
   double *X = nullptr, *ybar = nullptr, *rowrec = nullptr, *colrec = nullptr;
@@ -134,16 +134,8 @@ struct cr_handle {
   double* sv_u12 = nullptr;          // their device copy + 256 doubles of block partials
   double last_seconds = 0, last_sweep_seconds = 0;
   std::vector<double> last_sweep_times;  // per bracketed sweep launch of the last call (s)
+  double last_exchange_seconds = 0;      // sharded: allreduce time of the last call (s)
   int64_t last_launches = 0;
-  // masked dual store (sweep_sparse.cu): live-bit words of V[0], V[1]
-  uint32_t* M[2] = {nullptr, nullptr};
-  unsigned long long* d_stores = nullptr;  // multipliers written by the P-APG sweeps
-  int mstages = 0;          // MaskGeo::stages
-  TmapBytes tmV[2] = {};    // tensor maps of V[0], V[1] for the DMMA P-APG producer
-  bool tmap_ok = false;
-  bool sparse_ok = false;   // the masked P-APG sweep is available (MMA geometry)
-  bool masked = false;      // this solve runs it (not the small-N loop)
-  SweepKernelInfo ksp{};
   // standalone ALCC (alcc.cu)
   crb::AlccBufs alcc{};
   // general-K partition (general.cu); K == 0: singleton blocks
@@ -232,9 +224,6 @@ inline SweepArgs sweep_args(cr_handle* h, int mode, bool agg_only) {
   a.U = h->U;
   a.maxspan = h->maxspan;
   a.nbar = h->part.K > 0 ? h->part.nbar : 1;
-  a.M0 = h->M[0];
-  a.M1 = h->M[1];
-  a.mstages = h->mstages;
   a.stores = h->d_stores;
   if ((mode == kModePapg || mode == kModePenalty || mode == kModePenaltyUpdate) && h->tmap_ok) {
     a.tmV[0] = h->tmV[0];
@@ -243,14 +232,8 @@ inline SweepArgs sweep_args(cr_handle* h, int mode, bool agg_only) {
   }
   return a;
 }
-inline MaskGeo mask_geo(const cr_handle* h) {
-  return MaskGeo{h->R, h->U, h->kp.tile_cols, h->mstages};
-}
-inline size_t mask_words(const cr_handle* h) {
-  return (size_t)h->G * h->mstages * (h->kp.tile_cols / 4);
-}
-// the P-APG sweep of this solve: masked (sparse) or dense
-inline const SweepKernelInfo& papg_sweep(const cr_handle* h) { return h->masked ? h->ksp : h->kp; }
+// the P-APG sweep of this solve
+inline const SweepKernelInfo& papg_sweep(const cr_handle* h) { return h->kp; }
 
 inline ReduceArgs reduce_args(cr_handle* h, bool with_k2, const int* stopped, bool fuse_control,
                               int sweep_warps = 0 /* scalar records per sweep CTA */) {

@@ -35,16 +35,11 @@ __global__ void __launch_bounds__(kPBlock) primal_kernel(const PrimalArgs a) {
     }
   }
   const int stop = a.stopped != nullptr ? *a.stopped : 0;
-  const int done = a.fuse_ctrl != nullptr ? __ldcg(&a.fuse_ctrl->primal_done) : 0;
   const double s_c = a.coef[0];
   const double s_p = a.mode == 0 ? a.coef[1] : 0.0;
   const double beta = a.mode == 0 ? a.coef[2] : 0.0;
   const int cur = *a.cur;
   if (stop) return;
-  if (a.fuse_ctrl != nullptr) {  // fused path: the last fused launch already ran it
-    if (done) return;
-    if (blockIdx.x == 0 && threadIdx.x == 0) a.fuse_ctrl->k2_count = (int)gridDim.x;
-  }
   const double* vposc = cur ? a.vpos1 : a.vpos0;
   double* vposp = cur ? a.vpos0 : a.vpos1;
   double acc[kK2Scal];
@@ -222,161 +217,6 @@ __global__ void __launch_bounds__(kBlock, 6) reduce_kernel(const ReduceArgs a) {
   }
 }
 
-// Fused K3 + Kc + K2 (one GPU, singleton blocks). Blocks take their role by
-// start order (a ticket), so the control block is always resident before any
-// block waits for it. Control block: scalar records + control step, then the
-// flag. Point blocks (32 points each): the points' row sums (T slices) and
-// column aggregates (their tile's slot arrays) -> xbuf, wait for the flag, then
-// the primal closed form of the next iteration (papg.cpp:176-182 at theta2)
-// unless the control step halted. Same fixed-order sums as reduce_kernel.
-constexpr int kFPts = 32;
-int fused_blocks_impl(long long N) { return (int)((N + kFPts - 1) / kFPts) + 1; }
-
-template <int NN>
-__global__ void __launch_bounds__(kBlock) reduce_primal_kernel(const FusedArgs f) {
-  constexpr int n1 = NN + 1;
-  const ReduceArgs& a = f.r;
-  const long long N = a.N;
-  const long long ncol = N * n1;
-  DevCtrl* c = a.ctrl;
-  __shared__ unsigned long long s_ticket;
-  if (threadIdx.x == 0) s_ticket = atomicAdd(f.ticket, 1ull);
-  __syncthreads();
-  const unsigned long long gen = s_ticket / gridDim.x;
-  const long long bid = (long long)(s_ticket % gridDim.x);
-  if (bid == 0) {  // ---- scalars + control
-    const int halted = __ldcg(&c->halt);
-    if (!halted) {
-      scalar_records(a, N + ncol, __ldcg(&c->k2_count));
-      __syncthreads();
-    }
-    if (threadIdx.x == 0) {
-      if (!halted) control_step(c, a.agg_out + N + ncol, a.k2sum, a.hist);
-      c->primal_done = c->halt ? 0 : 1;
-      c->k2_count = (int)gridDim.x - 1;
-      __threadfence();
-      asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(f.flag), "l"(gen + 1) : "memory");
-    }
-    return;
-  }
-  // ---- point block: points [l0, l0 + 32)
-  const long long l0 = (bid - 1) * kFPts;
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  // row sums: lane = point, warp = slice group (slices st = w, w + 8, ...)
-  {
-    __shared__ double part[kBlock / 32][kFPts];
-    const long long r = l0 + lane;
-    const long long lr = r - a.r0;
-    double s = 0.0;
-    if (r < N && lr >= 0 && lr < a.R) {
-      for (int st0 = w; st0 < a.S; st0 += 8 * 4) {
-        double v[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int st = st0 + 8 * u;
-          v[u] = st < a.S ? __ldcg(a.rowpart + (long long)st * a.R + lr) : 0.0;
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) s += v[u];
-      }
-    }
-    part[w][lane] = s;
-    // column aggregates: item e = (point, value) of the block's 32 x n1 entries.
-    // The block's points lie in at most two column tiles: their (CTA, segment)
-    // slot offsets are computed once into shared memory (no per-item division)
-    const long long per_tile = (long long)a.TC * n1;
-    constexpr int kMaxSlots = 32;
-    __shared__ long long slot_off[2][kMaxSlots];
-    __shared__ int nslot[2];
-    const long long tA = l0 / a.TC;
-    if (threadIdx.x < 2 * kMaxSlots) {
-      const int which = threadIdx.x / kMaxSlots, k = threadIdx.x % kMaxSlots;
-      const long long t = tA + which;
-      const long long g_lo = (t * a.R) / a.U;
-      long long g_hi = ((t + 1) * a.R - 1) / a.U;
-      if (g_hi > a.G - 1) g_hi = a.G - 1;
-      const long long g = g_lo + k;
-      if (k == 0) nslot[which] = (int)(g_hi - g_lo + 1);
-      if (g <= g_hi) slot_off[which][k] = (g * a.maxspan + (t - (g * a.U) / a.R)) * per_tile;
-    }
-    __syncthreads();
-    for (int e = threadIdx.x; e < kFPts * n1; e += kBlock) {
-      const long long l = l0 + e / n1;
-      if (l >= N) continue;
-      const int j = e % n1;
-      const long long t = l / a.TC;
-      const int which = (int)(t - tA);
-      const long long off = (l - t * a.TC) * n1 + j;  // within the tile's slot array
-      const int ns = nslot[which];
-      double sum = 0.0;
-      for (int k0 = 0; k0 < ns; k0 += 4) {
-        double v[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int k = k0 + u;
-          long long so = 0;
-          if (k < ns) {
-            if (k < kMaxSlots) {
-              so = slot_off[which][k];
-            } else {  // more CTAs on this tile than cached slots (small N, many CTAs)
-              const long long g = (t * a.R) / a.U + k;
-              so = (g * a.maxspan + (t - (g * a.U) / a.R)) * per_tile;
-            }
-          }
-          v[u] = k < ns ? __ldcg(a.colpart + so + off) : 0.0;
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-          if (k0 + u < ns) sum += v[u];
-      }
-      a.agg_out[N + l * n1 + j] = sum;
-    }
-    __syncthreads();
-    if (w == 0 && l0 + lane < N) {
-      double u = 0.0;
-#pragma unroll
-      for (int k = 0; k < kBlock / 32; ++k) u += part[k][lane];
-      a.agg_out[l0 + lane] = u;
-    }
-  }
-  // ---- wait for the control step of this launch
-  if (threadIdx.x == 0) {
-    unsigned long long v;
-    for (;;) {
-      asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(f.flag) : "memory");
-      if (v >= gen + 1) break;
-      __nanosleep(32);
-    }
-  }
-  __syncthreads();
-  if (__ldcg(&c->halt)) return;  // halted (or paused): no primal for a next iteration
-  // ---- K2 at theta2 of the next iteration for the block's points
-  const PrimalArgs& p = f.p;
-  const int cur = __ldcg(&c->cur);
-  const double s_c = __ldcg(&c->s_cur), s_p = __ldcg(&c->s_prev), beta = __ldcg(&c->beta);
-  const double* vposc = cur ? p.vpos1 : p.vpos0;
-  double* vposp = cur ? p.vpos0 : p.vpos1;
-  double acc[kK2Scal];
-#pragma unroll
-  for (int k = 0; k < kK2Scal; ++k) acc[k] = 0.0;
-  if (threadIdx.x < kFPts && l0 + threadIdx.x < N)
-    primal_point<NN>(p, l0 + threadIdx.x, s_c, s_p, beta, vposc, vposp, acc);
-  // the 32 primal threads are warp 0: one butterfly, fixed order
-  if (w == 0) {
-#pragma unroll
-    for (int k = 0; k < kK2Scal; ++k) {
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], o);
-    }
-    if (lane < kK2Scal) {
-      double val = acc[0];
-#pragma unroll
-      for (int k = 1; k < kK2Scal; ++k)
-        if (lane == k) val = acc[k];
-      p.k2part[(bid - 1) * kK2Scal + lane] = val;
-    }
-  }
-}
 
 __global__ void rowrec_init_kernel(const double* X, const double* ybar, double* rowrec, long long N,
                                    int n, int RP) {
@@ -480,51 +320,14 @@ __global__ void theta_in_kernel(const double* stage, double* V, long long N, lon
 }
 
 __global__ void theta_out_kernel(double* stage, const double* V, double s, long long N,
-                                 long long ld, long long r0, long long ra, long long rb,
-                                 const uint32_t* M, MaskGeo mg) {
+                                 long long ld, long long r0, long long ra, long long rb) {
   const long long total = (rb - ra) * (N - 1);
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
        i += (long long)gridDim.x * blockDim.x) {
     const long long lr = i / (N - 1), k = i % (N - 1);
     const long long gr = r0 + ra + lr;
     const long long c = k + (k >= gr ? 1 : 0);
-    const bool live = M == nullptr || mask_live(M, mg, ra + lr, c);
-    stage[i] = live ? s * V[(ra + lr) * ld + c] : 0.0;
-  }
-}
-
-// one thread per stage word: enumerate the CTA's stages to find the tile and rows
-__global__ void mask_build_kernel(const double* V, uint32_t* M, long long N, long long ld,
-                                  MaskGeo mg, int G) {
-  const int wpst = mg.TC / 4;  // words per stage
-  const long long total = (long long)G * mg.stages * wpst;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
-       i += (long long)gridDim.x * blockDim.x) {
-    const int w = (int)(i % wpst);
-    const long long ks = i / wpst;
-    const long long k = ks % mg.stages, cta = ks / mg.stages;
-    const long long u0 = cta * mg.U, u1 = u0 + mg.U;
-    long long left = k;
-    long long t = u0 / mg.R, r = -1;
-    for (; t * mg.R < u1 && r < 0; ++t) {
-      const long long lo = (u0 > t * mg.R ? u0 : t * mg.R) - t * mg.R;
-      const long long hi = (u1 < (t + 1) * mg.R ? u1 : (t + 1) * mg.R) - t * mg.R;
-      const long long ns = hi > lo ? (hi - lo + 7) / 8 : 0;
-      if (left < ns) r = lo + 8 * left;
-      else left -= ns;
-    }
-    uint32_t bits = 0;
-    if (r >= 0) {
-      --t;
-      const long long hi = (u1 < (t + 1) * mg.R ? u1 : (t + 1) * mg.R) - t * mg.R;
-      const int tl = w >> 1, j = w & 1;
-      for (int b = 0; b < 32; ++b) {
-        const long long rr = r + 2 * (b & 3) + j;
-        const long long c = t * mg.TC + tl * 8 + (b >> 2);
-        if (rr < hi && c < N && c < ld && V[rr * ld + c] > 0.0) bits |= 1u << b;
-      }
-    }
-    M[i] = bits;
+    stage[i] = s * V[(ra + lr) * ld + c];
   }
 }
 
@@ -603,24 +406,6 @@ cudaError_t launch_reduce(const ReduceArgs& a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-int fused_blocks(long long N) { return fused_blocks_impl(N); }
-
-template <int NN>
-void launch_reduce_primal_n(const FusedArgs& a, cudaStream_t s) {
-  reduce_primal_kernel<NN><<<(unsigned)fused_blocks_impl(a.r.N), kBlock, 0, s>>>(a);
-}
-using FusedLauncher = void (*)(const FusedArgs&, cudaStream_t);
-cudaError_t launch_reduce_primal(const FusedArgs& a, cudaStream_t s) {
-  static constexpr FusedLauncher tab[kMaxN] = {
-#define CRB_LF(N) launch_reduce_primal_n<N>
-      CRB_N_SEQ(CRB_LF)
-#undef CRB_LF
-};
-  if (a.p.n < 1 || a.p.n > kMaxN) return cudaErrorInvalidValue;
-  tab[a.p.n - 1](a, s);
-  return cudaGetLastError();
-}
-
 cudaError_t launch_control(DevCtrl* c, const double* scal, const double* k2, double* hist,
                            cudaStream_t s) {
   control_kernel<<<1, 32, 0, s>>>(c, scal, k2, hist);
@@ -669,18 +454,12 @@ cudaError_t launch_theta_in(const double* stage, double* V, long long N, long lo
 
 cudaError_t launch_theta_out(double* stage, const double* V, double sc, long long N,
                              long long ld, long long r0, long long ra, long long rb,
-                             cudaStream_t s, const uint32_t* M, MaskGeo mg) {
+                             cudaStream_t s) {
   theta_out_kernel<<<grid_for((rb - ra) * (N - 1), 256, 4096), 256, 0, s>>>(stage, V, sc, N, ld,
-                                                                            r0, ra, rb, M, mg);
+                                                                            r0, ra, rb);
   return cudaGetLastError();
 }
 
-cudaError_t launch_mask_build(const double* V, uint32_t* M, long long N, long long ld,
-                              MaskGeo mg, int G, cudaStream_t s) {
-  mask_build_kernel<<<grid_for((long long)G * mg.stages * (mg.TC / 4), 256, 4096), 256, 0, s>>>(
-      V, M, N, ld, mg, G);
-  return cudaGetLastError();
-}
 
 cudaError_t launch_rows_out(double* stage, const double* rowrec, const double* colrec,
                             long long N, int n, long long r0, long long ra, long long rb,

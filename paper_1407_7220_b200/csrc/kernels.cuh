@@ -19,7 +19,6 @@ struct PrimalArgs {
   double* k2part;        // [blocks][kK2Scal]
   const double* coef;    // {s_cur, s_prev, beta}
   const int* stopped;
-  DevCtrl* fuse_ctrl;    // mode 0, fused path: no-op if primal_done, else k2_count = blocks
   double* yout;          // mode 1
   double* xiout;         // mode 1
   double invL, gamma;
@@ -80,8 +79,6 @@ struct MetricsArgs {
   const double* rowrec;  // N x RQ records of the point (x, 1, y)
   const double* colrec;  // N x RQ (-xi, -c, 1)
   const double* V;       // optional: theta1 = s V (local rows) for the duality gap
-  const uint32_t* M;     // optional live words of V (masked store)
-  MaskGeo mg;
   double s;
   double* part;          // [grid][2]: (sum min(row,0)^2, sum theta.row)
   long long N, R, r0, ld;
@@ -106,17 +103,6 @@ int power_loop_grid(int sms, long long N);
 cudaError_t launch_power_loop(const PowerLoopArgs& a, int grid, cudaStream_t s);
 cudaError_t launch_primal(const PrimalArgs& a, cudaStream_t s);
 cudaError_t launch_reduce(const ReduceArgs& a, cudaStream_t s);
-// fused K3 + Kc + K2 of the next iteration (one GPU): block 0 (by start order)
-// reduces the scalars and runs the control step; 32-point blocks reduce their
-// points' aggregates, wait for the control flag and run the primal closed form
-struct FusedArgs {
-  ReduceArgs r;
-  PrimalArgs p;
-  unsigned long long* ticket;  // block start-order counter (monotone across launches)
-  unsigned long long* flag;    // control done: generation + 1
-};
-int fused_blocks(long long N);
-cudaError_t launch_reduce_primal(const FusedArgs& a, cudaStream_t s);
 cudaError_t launch_control(DevCtrl* c, const double* scal, const double* k2, double* hist,
                            cudaStream_t s);
 cudaError_t launch_begin(DevCtrl* c, cudaStream_t s);
@@ -129,10 +115,7 @@ cudaError_t launch_theta_in(const double* stage, double* V, long long N, long lo
                             long long r0, long long ra, long long rb, cudaStream_t s);
 cudaError_t launch_theta_out(double* stage, const double* V, double sc, long long N,
                              long long ld, long long r0, long long ra, long long rb,
-                             cudaStream_t s, const uint32_t* M = nullptr, MaskGeo mg = {});
-// live words of a dense V (entries > 0) in the masked-store layout (device.cuh)
-cudaError_t launch_mask_build(const double* V, uint32_t* M, long long N, long long ld,
-                              MaskGeo mg, int G, cudaStream_t s);
+                             cudaStream_t s);
 cudaError_t launch_rows_out(double* stage, const double* rowrec, const double* colrec,
                             long long N, int n, long long r0, long long ra, long long rb,
                             cudaStream_t s);

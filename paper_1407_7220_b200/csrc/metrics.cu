@@ -69,7 +69,7 @@ __global__ void __launch_bounds__(kMBlock) pair_metrics_kernel(const MetricsArgs
       if (!valid || col == g) row = 0.0;
       const double m = row < 0.0 ? row : 0.0;
       nn = fma(m, m, nn);
-      if (a.V != nullptr && valid && (a.M == nullptr || mask_live(a.M, a.mg, r, col)))
+      if (a.V != nullptr && valid)
         gap = fma(a.s * a.V[r * a.ld + col], row, gap);
     }
   }

@@ -1,5 +1,4 @@
-// mma_geo.cuh -- geometry and primitives shared by the DMMA pair sweeps
-// (sweep_mma.cu: dense dual store; sweep_sparse.cu: masked dual store).
+// mma_geo.cuh -- geometry and primitives of the DMMA pair sweeps (sweep_mma.cu).
 #pragma once
 #include <cstdint>
 
@@ -55,8 +54,6 @@ template <int NN>
 __host__ __device__ constexpr int mma_ns() {  // ring stages
   return CRB_MMA_NS > 0 ? CRB_MMA_NS : (mma_ctas<NN>() == 2 ? 3 : 4);
 }
-constexpr int kNS = 4;  // ring depth of the other users of this header (sweep_sparse.cu)
-constexpr int kWin = 32;               // row-sum window (rows), masked-store sweep
 #ifndef CRB_MMA_WIN
 #define CRB_MMA_WIN 256
 #endif

@@ -957,4 +957,10 @@ SweepKernelInfo sweep_mma_info(int n, int mode, bool blocked) {
   return AllN::info(n, mode, blocked);
 }
 
+int launch_sweep(const SweepKernelInfo& info, const SweepArgs& a, void* stream) {
+  void* args[] = {const_cast<SweepArgs*>(&a)};
+  return (int)cudaLaunchKernel(info.fn, dim3((unsigned)a.G), dim3(info.threads), args,
+                               info.smem_bytes, (cudaStream_t)stream);
+}
+
 }  // namespace crb

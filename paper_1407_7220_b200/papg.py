@@ -446,6 +446,12 @@ class DualSolver:
         _raise(self._L.cr_last_timing(self.h, C.byref(s), C.byref(k), C.byref(sw)), self.h)
         return s.value, k.value, sw.value
 
+    def last_exchange_seconds(self):
+        """Sharded runs: allreduce device time of the last iterate call (s)."""
+        x = C.c_double(0)
+        _raise(self._L.cr_last_exchange_seconds(self.h, C.byref(x)), self.h)
+        return x.value
+
     def last_sweep_times(self):
         """Durations (s) of the sweep launches the last iterate call bracketed with
         CUDA events, in launch order (every launch of a call of <= 64 iterations)."""

@@ -94,9 +94,7 @@ def test_alcc_parity_long_inner_runs(oracle):
     assert_alcc_parity(o, g, tol_y=1e-6, tol_mult=None, hist_rtol=1e-3)
 
 
-@pytest.mark.parametrize("variant", ["dfma", "mma"])
-def test_alcc_parity_both_sweep_variants(oracle, monkeypatch, variant):
-    monkeypatch.setenv("CRB_SWEEP", variant)
+def test_alcc_parity_dmma_sweep(oracle):
     X, P = problem(oracle, "sqnorm-uniform", 90, 4, 0.2, 13)
     o, g = run_both(oracle, X, P, max_outer=5, mapg_cap=1000)
     assert_alcc_parity(o, g)
