@@ -112,7 +112,10 @@ def test_config1_full_2000_iterations(oracle, monkeypatch, small):
     s, _, _ = oracle.sigma_C(X)
     kw = dict(max_iters=2000, gap_norm_tol=-1.0, infeas_norm_tol=-1.0, sigma_C=s)
     o = oracle_run(oracle, X, ys, threads=8, **kw)
-    assert_parity(gpu_run(X, ys, **kw), o, hist_rtol=1e-8)
+    g = gpu_run(X, ys, **kw)
+    assert_parity(g, o, hist_rtol=1e-8)
+    print(f"config1 small={small}: iters={o.iters} theta {rel(g['theta'], o.theta):.2e} "
+          f"rows {rel(g['rows'], o.c_eta):.2e} y {rel(g['y'], o.y):.2e}")
 
 
 @pytest.mark.parametrize("method", ["closed-form", "sweep"])
