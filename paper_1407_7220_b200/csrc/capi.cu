@@ -139,6 +139,7 @@ PrimalArgs primal_args(cr_handle* h, int mode) {
   a.N = h->N;
   a.n = (int)h->n;
   a.mode = mode;
+  a.tr_adjoint = h->part.K == 0 ? 1 : 0;  // singleton per-kernel sweep: theta2 . C eta from K2
   return a;
 }
 
@@ -809,6 +810,7 @@ cr_status cr_papg_iterate(cr_handle* h, int64_t max_steps, int64_t* done, int32_
     } else {
       SmallArgs sa{};
       sa.pa = primal_args(h, 0);
+      sa.pa.tr_adjoint = 0;  // the small-N loop's sweep accumulates theta2 . row itself
       sa.V0 = h->V[0];
       sa.V1 = h->V[1];
       sa.colpart = h->s_colpart;
@@ -865,8 +867,9 @@ cr_status cr_papg_iterate(cr_handle* h, int64_t max_steps, int64_t* done, int32_
   const bool timed_sweeps = h->graph_iters == 0;
   // Sweep timing: an event pair around every 8th sweep (CRB_SWEEP_EVENTS=k: every
   // k-th, 0: none); the reported sweep seconds are the sampled mean times the
-  // iterations run. Event records between the kernels cost ~6 us per iteration
-  // (2 % at cfg 2, measured), so not every sweep is bracketed.
+  // iterations run. Event records between the kernels cost ~5 us per cfg 2
+  // iteration (measured 384.8 vs 379.9 us; external event nodes in a captured
+  // graph cost more: 388.9 us at 4 iterations per graph), so long calls sample.
   // A call of at most 64 iterations brackets every sweep (a short call's early
   // iterations differ too much for a sample).
   int every = max_steps <= 64 ? 1 : 8;

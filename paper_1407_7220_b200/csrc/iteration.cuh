@@ -117,7 +117,9 @@ __device__ __forceinline__ void primal_point(const PrimalArgs& a, long long l, d
     vposp[l] = vnew;
     acc[0] = fma(vnew, vnew, acc[0]);
     acc[1] = fma(vnew, y, acc[1]);
-    acc[2] = fma(th2pos, y, acc[2]);
+    // theta2 . C eta (papg.cpp:191-199): C^T theta2 = (q_y, q_xi) by linearity, so
+    // summed over the points the cross pairs' theta2 . row is y (rs - cs) + xi . q_xi
+    acc[2] = a.tr_adjoint ? acc[2] + fma(y, qy, qx) : fma(th2pos, y, acc[2]);
   } else {
     a.yout[l] = y;
 #pragma unroll

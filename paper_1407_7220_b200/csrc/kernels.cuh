@@ -25,6 +25,10 @@ struct PrimalArgs {
   long long N;
   int n;
   int mode;              // 0 iteration, 1 final
+  // 1: the k2 record's theta2.C eta slot carries all of it through the adjoint,
+  // sum_l y_l q_y_l + xi_l . q_xi_l (the singleton per-kernel sweep does not
+  // accumulate theta2 . row); 0: only the y >= 0 rows' theta2_pos y
+  int tr_adjoint;
 };
 
 struct ReduceArgs {

@@ -36,6 +36,20 @@
 #ifndef CRB_PROBE_MEMONLY
 #define CRB_PROBE_MEMONLY 0
 #endif
+#ifndef CRB_LEAN_ORDER  // 1: a tile's aggregation MMAs issued before its stores and sums
+#define CRB_LEAN_ORDER 1
+#endif
+// 1: the singleton sweep leaves theta2 . row to K2 (PrimalArgs::tr_adjoint);
+// must agree with primal_args() in capi.cu
+#ifndef CRB_TR_ADJOINT
+#define CRB_TR_ADJOINT 1
+#endif
+#ifndef CRB_PROBE_NOWAIT  // probe: producer fills the ring once, consumers never wait (compute only)
+#define CRB_PROBE_NOWAIT 0
+#endif
+#ifndef CRB_RS_SMEM  // lean P-APG loop: row sums through a 32-row shared window, no shuffles
+#define CRB_RS_SMEM 1
+#endif
 #ifndef CRB_PROBE_SKIP  // measurement probe (wrong results): 1 residual, 2 aggregation, 4 sums, 8 row-sum shuffles
 #define CRB_PROBE_SKIP 0
 #endif
@@ -286,22 +300,29 @@ __device__ __forceinline__ int papg_lean(const double* __restrict__ lv, const do
         continue;
       }
     }
-    double v[2];
+    double v[2], th2[2];
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
-      double th2;
       if (UNIT) {
-        th2 = fma(cf.beta, c1[j] - p1[j], c1[j]);
+        th2[j] = fma(cf.beta, c1[j] - p1[j], c1[j]);
       } else {
         const double th1 = cf.s_c * c1[j];
-        th2 = fma(cf.beta, th1 - cf.s_p * p1[j], th1);
+        th2[j] = fma(cf.beta, th1 - cf.s_p * p1[j], th1);
       }
-      v[j] = keep_if_nonneg(fma(-row[j], cf.invL, th2));
+      v[j] = keep_if_nonneg(fma(-row[j], cf.invL, th2[j]));
+    }
+    // the aggregation MMAs go first (long latency, 16 pipe cycles each); the
+    // stores and the scalar sums fill behind them (CRB_LEAN_ORDER = 0: old order)
+    const bool agg = !(CRB_PROBE_SKIP & 2) &&
+                     (!TEST || __any_sync(0xffffffffu, v[0] != 0.0 || v[1] != 0.0));
+    if (CRB_LEAN_ORDER == 1 && agg) papg_agg<NN>(Ag, xr, v, D[ct], E[ct]);
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
       store_changed_sector(o0 + (j ? ld : 0) + ct * 8, v[j], p1[j], true, lane, nst);
       if (!(CRB_PROBE_SKIP & 4)) {
         sc.vv = fma(v[j], v[j], sc.vv);
         sc.vr = fma(v[j], row[j], sc.vr);
-        sc.tr = fma(th2, row[j], sc.tr);
+        if (!CRB_TR_ADJOINT) sc.tr = fma(th2[j], row[j], sc.tr);
         acc_neg_sq(sc.nn, row[j]);
       }
       if (!TEST && ct == 0)
@@ -309,14 +330,13 @@ __device__ __forceinline__ int papg_lean(const double* __restrict__ lv, const do
       else
         rs[j] += v[j];
     }
-    if (!(CRB_PROBE_SKIP & 2) && (!TEST || __any_sync(0xffffffffu, v[0] != 0.0 || v[1] != 0.0)))
-      papg_agg<NN>(Ag, xr, v, D[ct], E[ct]);
+    if (CRB_LEAN_ORDER == 0 && agg) papg_agg<NN>(Ag, xr, v, D[ct], E[ct]);
   }
   return cold;
 }
 
 // P-APG stage with masking (diagonal, partial stage, pad columns), one warp.
-template <int NN, bool UNIT, bool BLK>
+template <int NN, bool UNIT, bool BLK, bool TR = true>
 __device__ __forceinline__ void papg_masked(const double* __restrict__ sv, const double* __restrict__ svp,
                                             const double* __restrict__ srec, double* gout,
                                             long long ld, long long gcol0, long long grow0, int nr,
@@ -379,7 +399,7 @@ __device__ __forceinline__ void papg_masked(const double* __restrict__ sv, const
       store_changed_sector(g0 + (long long)j * ld + ct * 8, v[j], p1, rv, lane, nst);
       sc.vv = fma(v[j], v[j], sc.vv);
       sc.vr = fma(v[j], row, sc.vr);
-      sc.tr = fma(th2, row, sc.tr);
+      if (TR) sc.tr = fma(th2, row, sc.tr);
       acc_neg_sq(sc.nn, row);
       rs[j] += v[j];
     }
@@ -526,6 +546,7 @@ __global__ void __launch_bounds__(mma_threads<NN>(), mma_ctas<NN>()) sweep_mma_k
 #if CRB_PROBE_TIMING
           const long long tp0 = clock64();
 #endif
+          if (CRB_PROBE_NOWAIT && i >= kNS) break;
           if (i >= kNS) mbar_wait_sleep<CRB_PROD_SLEEP>(&empty[s], (uint32_t)(((i / kNS) - 1) & 1));
 #if CRB_PROBE_TIMING
           pw += clock64() - tp0;
@@ -654,9 +675,16 @@ __global__ void __launch_bounds__(mma_threads<NN>(), mma_ctas<NN>()) sweep_mma_k
         __syncwarp();
       }
       double* const rowacc_lane = rowacc + warp * kWinM + 2 * (lane & 3) + ((lane >> 2) & 1);
+#if CRB_RS_SMEM
+      // row-sum window of kRsW rows: per buffer [kRsW/2 row pairs][kCW warps][8 column lanes][2]
+      constexpr int kRsW = 32;
+      constexpr int kRsBuf = kRsW / 2 * kCW * 16;
+      static_assert(kRsBuf <= kCW * kWinM, "row-sum window must fit the rowacc buffers");
+      double* const rs_lane = rowacc + (q * kCW + warp) * 16 + c8 * 2;
+#endif
       int win = 0, win_base = 0;
       for (int st8 = 0; st8 < nstage; ++st8, gout += gstep) {
-        mbar_wait_u32(full_u + 8u * slot, phase);
+        if (!CRB_PROBE_NOWAIT || i + st8 < kNS) mbar_wait_u32(full_u + 8u * slot, phase);
         double rsj[2] = {0.0, 0.0};
         bool hot_stage = true;
         if (active && !CRB_PROBE_MEMONLY) {
@@ -696,10 +724,10 @@ __global__ void __launch_bounds__(mma_threads<NN>(), mma_ctas<NN>()) sweep_mma_k
             double dres[kCT][2];
             stage_residual<NN>(srec, lane, Al, dres);
             if (unit_scale)
-              papg_masked<NN, true, false>(sv, svp, srec, gout, a.ld, gcol0, grow0, nr, a.N, a.nbar,
+              papg_masked<NN, true, false, false>(sv, svp, srec, gout, a.ld, gcol0, grow0, nr, a.N, a.nbar,
                                            lane, dres, D, E, Cc, cf, sc, rsj, nst);
             else
-              papg_masked<NN, false, false>(sv, svp, srec, gout, a.ld, gcol0, grow0, nr, a.N, a.nbar,
+              papg_masked<NN, false, false, false>(sv, svp, srec, gout, a.ld, gcol0, grow0, nr, a.N, a.nbar,
                                             lane, dres, D, E, Cc, cf, sc, rsj, nst);
           }
         }
@@ -709,6 +737,35 @@ __global__ void __launch_bounds__(mma_threads<NN>(), mma_ctas<NN>()) sweep_mma_k
           slot = 0;
           phase ^= 1u;
         }
+#if CRB_RS_SMEM
+        // row sums without shuffles: every lane parks its two rows' partials over
+        // its 2 tiles in the window; the flush sums the 8 column lanes x kCW warps
+        // of a row in a fixed order (every kRsW rows, one CTA barrier)
+        (void)hot_stage;
+        *reinterpret_cast<double2*>(rs_lane + (flushes & 1) * kRsBuf + (win >> 1) * kCW * 16) =
+            make_double2(rsj[0], rsj[1]);
+        win += kTR;
+        if (win == kRsW || st8 == nstage - 1) {
+          asm volatile("bar.sync 1, %0;" ::"r"(kCW * 32) : "memory");
+          const int valid_rows = min(win, nrows - win_base);
+          const int tid = warp * 32 + lane;
+          if (tid < kRsW * 8) {  // 8 threads per row: column lane g, then a 3-step butterfly
+            const int r = tid >> 3, g = tid & 7;
+            const double* rb = rowacc + (flushes & 1) * kRsBuf + ((r >> 1) * kCW * 8 + g) * 2 + (r & 1);
+            double u = 0.0;
+#pragma unroll
+            for (int w = 0; w < kCW; ++w) u += rb[w * 16];
+            u += __shfl_xor_sync(0xffffffffu, u, 1);
+            u += __shfl_xor_sync(0xffffffffu, u, 2);
+            u += __shfl_xor_sync(0xffffffffu, u, 4);
+            if (g == 0 && r < valid_rows) a.rowpart[(long long)t * a.R + rlo + win_base + r] = u;
+          }
+          win_base += win;
+          win = 0;
+          ++flushes;
+        }
+        continue;
+#endif
         double rsum = 0.0;  // row sums, as in the generic loop below
         if (CRB_PROBE_SKIP & 8) {
           rsum = rsj[0] + rsj[1];

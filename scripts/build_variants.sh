@@ -4,7 +4,8 @@
 set -e
 B=build/cvxreg_b200
 SRC=${SRC:-sweep_mma.cu}
-objs=$(ls $B/*.o | grep -v $SRC.o)
+EXCL=${EXCL:-$SRC}
+objs=$(ls $B/*.o | grep -v $EXCL.o)
 for spec in "$@"; do
   name=${spec%%:*}; flags=${spec#*:}
   ( /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 \
