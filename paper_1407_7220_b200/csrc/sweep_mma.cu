@@ -335,6 +335,73 @@ __device__ __forceinline__ int papg_lean(const double* __restrict__ lv, const do
   return cold;
 }
 
+// Lean-loop stage of the ALCC penalty sweep (kModePenalty, alcc.cpp:33-47):
+// v = max(theta_k - row, 0) over a clean stage, its row sums and column
+// aggregates; theta_k = V[cur] is the stage's first buffer. TEST: the same
+// per-tile cold test as the P-APG stage (theta = 0 and row >= 0: v = 0 exactly).
+template <int NN, bool TEST>
+__device__ __forceinline__ int pen_lean(const double* __restrict__ lv, const double* __restrict__ lb,
+                                        const double* __restrict__ lr, const double* __restrict__ la,
+                                        const double (&A)[mma_ct<NN>()][ksteps<NN>()],
+                                        double (&D)[mma_ct<NN>()][max1(agg_fbd<NN>())][2],
+                                        double (&E)[mma_ct<NN>()][max1(agg_re<NN>())],
+                                        const double (&Cc)[mma_ct<NN>()], double (&rs)[2]) {
+  CRB_GEO(NN)
+  constexpr int FBD = agg_fbd<NN>();
+  constexpr int RX = agg_rx<NN>();
+  constexpr int RQ = rec_pitch(NN);
+  constexpr bool SPLIT = split_yc<NN>();
+  double d[kCT][2];
+  lean_residual<NN>(lb, A, d);
+  double Ag[2][max1(FBD)];
+  double xr[2][max1(RX)];
+#pragma unroll
+  for (int fb = 0; fb < FBD; ++fb) {
+    Ag[0][fb] = la[fb * 8];
+    Ag[1][fb] = la[RQ + fb * 8];
+  }
+#pragma unroll
+  for (int r = 0; r < RX; ++r) {
+    xr[0][r] = lr[8 * FBD + r];
+    xr[1][r] = lr[RQ + 8 * FBD + r];
+  }
+  double yr[2] = {0.0, 0.0};
+  if (SPLIT) {
+    yr[0] = lr[NN + 1];
+    yr[1] = lr[RQ + NN + 1];
+  }
+  int cold = 0;
+  rs[0] = 0.0;
+  rs[1] = 0.0;
+#pragma unroll
+  for (int ct = 0; ct < kCT; ++ct) {
+    double row[2], th[2];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      row[j] = d[ct][j];
+      if (SPLIT) row[j] += yr[j] + Cc[ct];
+      th[j] = lv[j * kTCP + ct * 8];
+    }
+    if (TEST) {
+      const unsigned long long bits =
+          (unsigned long long)__double_as_longlong(th[0]) | (unsigned long long)__double_as_longlong(th[1]);
+      const bool hot = bits != 0ull || (__double2hiint(row[0]) | __double2hiint(row[1])) < 0;
+      if (!__any_sync(0xffffffffu, hot)) {
+        ++cold;
+        continue;
+      }
+    }
+    double v[2];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      v[j] = keep_if_nonneg(th[j] - row[j]);
+      rs[j] += v[j];
+    }
+    if (!TEST || __any_sync(0xffffffffu, v[0] != 0.0 || v[1] != 0.0)) papg_agg<NN>(Ag, xr, v, D[ct], E[ct]);
+  }
+  return cold;
+}
+
 // P-APG stage with masking (diagonal, partial stage, pad columns), one warp.
 template <int NN, bool UNIT, bool BLK, bool TR = true>
 __device__ __forceinline__ void papg_masked(const double* __restrict__ sv, const double* __restrict__ svp,
@@ -407,6 +474,13 @@ __device__ __forceinline__ void papg_masked(const double* __restrict__ sv, const
   }
 }
 
+// DMMA feature blocks of the column aggregates per mode: the P-APG and ALCC
+// penalty sweeps use the split aggregation (agg_split), the power step all blocks
+template <int NN, int MODE>
+__host__ __device__ constexpr int mode_fbk() {
+  return MODE == kModePower ? fblocks<NN>() : max1(agg_fbd<NN>());
+}
+
 // One 8-row stage for one warp, the other modes (power, penalty). MASK:
 // diagonal / partial-stage masking.
 template <int NN, int MODE, bool MASK, bool BLK>
@@ -415,12 +489,15 @@ __device__ __forceinline__ void mma_stage(const double* __restrict__ sv,
                                           long long ld, long long gcol0, long long grow0, int nr,
                                           long long ncols, long long nbar,
                                           int lane, const double (&A)[mma_ct<NN>()][ksteps<NN>()],
-                                          double (&D)[mma_ct<NN>()][fblocks<NN>()][2],
+                                          double (&D)[mma_ct<NN>()][mode_fbk<NN, MODE>()][2],
+                                          double (&E)[mma_ct<NN>()][max1(agg_re<NN>())],
                                           const double (&Cc)[mma_ct<NN>()], const MCoef& cf,
                                           MScal& sc, double (&rs)[2]) {
   CRB_GEO(NN)
   constexpr int KS = ksteps<NN>();
-  constexpr int FB = fblocks<NN>();
+  constexpr bool kPen = MODE != kModePower;  // split aggregation (papg_agg)
+  constexpr int FB = kPen ? agg_fbd<NN>() : fblocks<NN>();
+  constexpr int RX = agg_rx<NN>();
   constexpr int RQ = rec_pitch(NN);
   constexpr bool SPLIT = split_yc<NN>();
   const int q = lane & 3;
@@ -434,13 +511,16 @@ __device__ __forceinline__ void mma_stage(const double* __restrict__ sv,
   double B[KS];
 #pragma unroll
   for (int ks = 0; ks < KS; ++ks) B[ks] = srec[c8 * RQ + ks * 4 + q];
-  // aggregation A fragments: [X 1][row 2q+j][feature fb*8 + c8]
-  double Ag[2][FB];
+  // aggregation A fragments: [X 1][row 2q+j][feature fb*8 + c8] (+ the split's x)
+  double Ag[2][max1(FB)];
+  double xr[2][max1(RX)];
 #pragma unroll
   for (int j = 0; j < 2; ++j) {
     const bool rv = !MASK || (2 * q + j < nr);
 #pragma unroll
     for (int fb = 0; fb < FB; ++fb) Ag[j][fb] = rv ? srec[(2 * q + j) * RQ + fb * 8 + c8] : 0.0;
+#pragma unroll
+    for (int r = 0; r < RX; ++r) xr[j][r] = (kPen && rv) ? srec[(2 * q + j) * RQ + 8 * FB + r] : 0.0;
   }
   rs[0] = 0.0;
   rs[1] = 0.0;
@@ -478,10 +558,14 @@ __device__ __forceinline__ void mma_stage(const double* __restrict__ sv,
     // a tile whose v are all zero adds exact zeros to the aggregates (the power
     // mode's v is the residual itself, rarely zero)
     if (MODE == kModePower || __any_sync(0xffffffffu, v[0] != 0.0 || v[1] != 0.0)) {
+      if constexpr (kPen) {
+        papg_agg<NN>(Ag, xr, v, D[ct], E[ct]);
+      } else {
 #pragma unroll
-      for (int fb = 0; fb < FB; ++fb) {
-        dmma(D[ct][fb][0], D[ct][fb][1], Ag[0][fb], v[0]);
-        dmma(D[ct][fb][0], D[ct][fb][1], Ag[1][fb], v[1]);
+        for (int fb = 0; fb < FB; ++fb) {
+          dmma(D[ct][fb][0], D[ct][fb][1], Ag[0][fb], v[0]);
+          dmma(D[ct][fb][0], D[ct][fb][1], Ag[1][fb], v[1]);
+        }
       }
     }
   }
@@ -621,7 +705,7 @@ __global__ void __launch_bounds__(mma_threads<NN>(), mma_ctas<NN>()) sweep_mma_k
     double A[kCT][KS];
     // column aggregates: DMMA fragments (P-APG: agg_fbd blocks) and the P-APG
     // DFMA remainder
-    constexpr int FBK = MODE == kModePapg ? max1(agg_fbd<NN>()) : FB;
+    constexpr int FBK = mode_fbk<NN, MODE>();
     constexpr int RE = agg_re<NN>();
     double D[kCT][FBK][2];
     double E[kCT][max1(RE)];
@@ -641,8 +725,8 @@ __global__ void __launch_bounds__(mma_threads<NN>(), mma_ctas<NN>()) sweep_mma_k
 #pragma unroll
       for (int r = 0; r < max1(RE); ++r) E[ct][r] = 0.0;
     }
-    if constexpr (MODE == kModePapg && !BLK) {
-      // lean stage loop of the singleton P-APG sweep: 32-bit stage counters, the
+    if constexpr ((MODE == kModePapg || MODE == kModePenalty) && !BLK) {
+      // lean stage loop of the singleton P-APG and ALCC penalty sweeps: 32-bit stage counters, the
       // ring slot and phase advanced incrementally, lane addresses precomputed,
       // the stages that meet the diagonal precomputed per segment
       const int nrows = (int)(rhi - rlo);
@@ -703,7 +787,16 @@ __global__ void __launch_bounds__(mma_threads<NN>(), mma_ctas<NN>()) sweep_mma_k
             // per-warp adaptive cold test: a tested stage that finds a cold tile
             // keeps the test on for the next 8 stages; otherwise every 8th stage
             // probes and the others run without any test
-            if (probe > 0 || (pstage & 7) == 0) {
+            if constexpr (MODE == kModePenalty) {
+              (void)o0;
+              if (probe > 0 || (pstage & 7) == 0) {
+                const int cold = pen_lean<NN, true>(lv, lb, lr, la, Al, D, E, Cc, rsj);
+                probe = cold ? 8 : (probe > 0 ? probe - 1 : 0);
+                hot_stage = cold < kCT;
+              } else {
+                pen_lean<NN, false>(lv, lb, lr, la, Al, D, E, Cc, rsj);
+              }
+            } else if (probe > 0 || (pstage & 7) == 0) {
               const int cold = unit_scale
                   ? papg_lean<NN, true, true>(lv, lb, lr, la, o0, a.ld, lane, Al, D, E, Cc, cf, sc, rsj, nst)
                   : papg_lean<NN, false, true>(lv, lb, lr, la, o0, a.ld, lane, Al, D, E, Cc, cf, sc, rsj, nst);
@@ -721,14 +814,20 @@ __global__ void __launch_bounds__(mma_threads<NN>(), mma_ctas<NN>()) sweep_mma_k
             const double* sv = stg + warp * kW;
             const double* svp = sv + kTR * kTCP;
             const double* srec = stg + 2 * kTR * kTCP;
-            double dres[kCT][2];
-            stage_residual<NN>(srec, lane, Al, dres);
-            if (unit_scale)
-              papg_masked<NN, true, false, false>(sv, svp, srec, gout, a.ld, gcol0, grow0, nr, a.N, a.nbar,
-                                           lane, dres, D, E, Cc, cf, sc, rsj, nst);
-            else
-              papg_masked<NN, false, false, false>(sv, svp, srec, gout, a.ld, gcol0, grow0, nr, a.N, a.nbar,
-                                            lane, dres, D, E, Cc, cf, sc, rsj, nst);
+            if constexpr (MODE == kModePenalty) {
+              (void)svp;
+              mma_stage<NN, MODE, true, false>(sv, srec, gout, a.ld, gcol0, grow0, nr, a.N, a.nbar, lane,
+                                               Al, D, E, Cc, cf, sc, rsj);
+            } else {
+              double dres[kCT][2];
+              stage_residual<NN>(srec, lane, Al, dres);
+              if (unit_scale)
+                papg_masked<NN, true, false, false>(sv, svp, srec, gout, a.ld, gcol0, grow0, nr, a.N, a.nbar,
+                                                    lane, dres, D, E, Cc, cf, sc, rsj, nst);
+              else
+                papg_masked<NN, false, false, false>(sv, svp, srec, gout, a.ld, gcol0, grow0, nr, a.N, a.nbar,
+                                                     lane, dres, D, E, Cc, cf, sc, rsj, nst);
+            }
           }
         }
         __syncwarp();
@@ -854,10 +953,10 @@ __global__ void __launch_bounds__(mma_threads<NN>(), mma_ctas<NN>()) sweep_mma_k
           }
         } else if (clean) {
           mma_stage<NN, MODE, false, BLK>(sv, srec, gout, a.ld, gcol0, grow0, nr, a.N, a.nbar, lane, A, D,
-                                          Cc, cf, sc, rsj);
+                                          E, Cc, cf, sc, rsj);
         } else {
           mma_stage<NN, MODE, true, BLK>(sv, srec, gout, a.ld, gcol0, grow0, nr, a.N, a.nbar, lane, A, D,
-                                         Cc, cf, sc, rsj);
+                                         E, Cc, cf, sc, rsj);
         }
       }
       __syncwarp();
@@ -899,7 +998,7 @@ __global__ void __launch_bounds__(mma_threads<NN>(), mma_ctas<NN>()) sweep_mma_k
     }
     if (active) {  // column partials: thread holds (feature fb*8+c8, cols 2q+{0,1})
       const long long slot = (long long)blockIdx.x * a.maxspan + (t - t_first);
-      constexpr int FBW = MODE == kModePapg ? agg_fbd<NN>() : FB;  // DMMA blocks in use
+      constexpr int FBW = MODE == kModePower ? FB : agg_fbd<NN>();  // DMMA blocks in use
 #pragma unroll
       for (int ct = 0; ct < kCT; ++ct) {
 #pragma unroll
@@ -914,7 +1013,7 @@ __global__ void __launch_bounds__(mma_threads<NN>(), mma_ctas<NN>()) sweep_mma_k
             }
           }
         }
-        if constexpr (MODE == kModePapg && RE > 0) {
+        if constexpr (MODE != kModePower && RE > 0) {
           // DFMA remainder: lanes 4 c8 + q hold rows 2q, 2q+1 of column c8; sum over q
           const long long coff = (long long)warp * kW + ct * 8 + c8;
 #pragma unroll
