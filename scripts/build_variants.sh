@@ -9,7 +9,7 @@ objs=$(ls $B/*.o | grep -v $EXCL.o)
 for spec in "$@"; do
   name=${spec%%:*}; flags=${spec#*:}
   ( /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 \
-      -Xcompiler -fPIC -Xcompiler -ffp-contract=off -Iinclude -DCRB_N_LIST=10 $flags \
+      -Xcompiler -fPIC -Xcompiler -ffp-contract=off -Iinclude -DCRB_N_LIST=${NLIST:-10} $flags \
       -c paper_1407_7220_b200/csrc/$SRC -o /tmp/v_$name.o && \
     /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -shared -o ab/$name.so \
       /tmp/v_$name.o $objs -lnccl -lcudart_static -lrt -lpthread -ldl && echo built $name ) &
