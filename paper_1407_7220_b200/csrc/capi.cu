@@ -653,8 +653,11 @@ cr_status begin_impl(cr_handle* h, const cr_papg_config* cfg, const double* thet
   // small N (V, V' L2-resident, one GPU): one persistent cooperative launch runs
   // many iterations (small.cu). CRB_SMALL=0 disables, CRB_SMALL=1 forces.
   const char* smenv = std::getenv("CRB_SMALL");
+  // measured crossover against the per-kernel path with CUDA graphs (us/iteration,
+  // n = 5: N = 600 16.4 vs 20.8, N = 1000 20.0 vs 21.2, N = 1500 28.4 vs 23.0;
+  // N = 1000, n = 10: 29.5 vs 24.7): N^2 (n + 2) <= 7e6
   bool want_small = h->comm == nullptr && cfg->graph_iters == 0 &&
-                    2.0 * 8.0 * (double)h->R * (double)h->ld <= 48e6 && h->part.K == 0;
+                    (double)h->R * (double)h->N * (double)(h->n + 2) <= 7.0e6 && h->part.K == 0;
   if (smenv && smenv[0] == '0') want_small = false;
   if (smenv && smenv[0] == '1' && h->comm == nullptr && h->R == h->N && h->part.K == 0)
     want_small = true;
