@@ -6,24 +6,29 @@
 
 namespace crb {
 
-// CTA geometry per n, measured on B200: 15 consumer
-// warps x 2 tiles at one CTA per SM for every n since the P-APG producer loads a
-// stage with one tensor TMA per buffer (n = 10: 268 us late vs 293 us for 7 warps
-// x 4 tiles at two CTAs per SM; n = 20: 316 us). CRB_WIDE_ABOVE = 14 restores the
-// narrow geometry for n <= 14 (the better one with per-row bulk copies).
+// CTA geometry per n, measured on B200: 11 or 15 consumer
+// warps x 2 tiles at one CTA per SM (mma_cw) since the P-APG producer loads a
+// stage with one tensor TMA per buffer. CRB_WIDE_ABOVE = 14 restores the narrow
+// geometry (7 warps x 4 tiles, two CTAs per SM) for n <= 14.
 #ifndef CRB_WIDE_ABOVE
 #define CRB_WIDE_ABOVE 0
 #endif
 template <int NN>
 __host__ __device__ constexpr bool mma_wide() { return NN > CRB_WIDE_ABOVE; }
-#ifndef CRB_CW  // geometry overrides of the wide layout (measurement builds)
-#define CRB_CW 15
+#ifndef CRB_CW  // geometry overrides of the wide layout (measurement builds; 0: per n)
+#define CRB_CW 0
 #endif
 #ifndef CRB_CT
 #define CRB_CT 2
 #endif
+// consumer warps per CTA (x 2 tiles): 15 for 9 <= n <= 14, else 11 -- measured at
+// N = 1e4, iterations 6-25, us per sweep with 15 / 11 warps: n = 1 394 / 390, 3
+// 388 / 378, 5 383 / 373, 8 372 / 367, 10 365 / 381, 12 370 / 386, 16 431 / 411,
+// 20 (N = 2e4) 2074 / 1909, 24 601 / 523, 32 837 / 632 (profiles/r2_experiments.md)
 template <int NN>
-__host__ __device__ constexpr int mma_cw() { return mma_wide<NN>() ? CRB_CW : 7; }  // consumer warps
+__host__ __device__ constexpr int mma_cw() {
+  return !mma_wide<NN>() ? 7 : (CRB_CW > 0 ? CRB_CW : ((NN >= 9 && NN <= 14) ? 15 : 11));
+}
 template <int NN>
 __host__ __device__ constexpr int mma_ct() { return mma_wide<NN>() ? CRB_CT : 4; }   // 8-col tiles / warp
 template <int NN>
