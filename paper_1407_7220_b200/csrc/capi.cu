@@ -727,7 +727,8 @@ cr_status begin_impl(cr_handle* h, const cr_papg_config* cfg, const double* thet
         if (e == cudaSuccess) e = dalloc(&h->s_rowpart, (size_t)h->small_S * h->N);
         if (e == cudaSuccess)
           e = dalloc(&h->s_scalpart, (size_t)h->small_grid * kScal);
-        if (e == cudaSuccess) e = dalloc(&h->s_k2part, (size_t)h->small_grid * kK2Scal);
+        // K2 records double buffered by iteration parity + the launch's clock slot
+        if (e == cudaSuccess) e = dalloc(&h->s_k2part, (size_t)2 * h->small_grid * kK2Scal + 1);
         if (e != cudaSuccess) {
           cudaGetLastError();
           return fail(h, CR_ENOMEM, "small-N buffers");
@@ -820,6 +821,7 @@ cr_status cr_papg_iterate(cr_handle* h, int64_t max_steps, int64_t* done, int32_
       sa.rowpart = h->s_rowpart;
       sa.scalpart = h->s_scalpart;
       sa.k2part = h->s_k2part;
+      sa.clock = reinterpret_cast<unsigned long long*>(h->s_k2part + (size_t)2 * h->small_grid * kK2Scal);
       sa.xbuf = h->xbuf;
       sa.k2sum = h->k2sum;
       sa.hist = h->hist;
@@ -853,7 +855,7 @@ cr_status cr_papg_iterate(cr_handle* h, int64_t max_steps, int64_t* done, int32_
         int cnt = 0;
         for (int it = 1; it < 64 && tb[it * 8 + 7] != 0; ++it, ++cnt)
           for (int k = 0; k < 7; ++k) acc[k] += (double)(tb[it * 8 + k + 1] - tb[it * 8 + k]);
-        std::fprintf(stderr, "small-loop phases (ns, mean of %d): A %.0f syncA %.0f B %.0f syncB %.0f C %.0f ctl %.0f syncC %.0f\n",
+        std::fprintf(stderr, "small-loop phases (ns, mean of %d): - %.0f - %.0f B %.0f syncB %.0f C+ctl %.0f A %.0f sync %.0f\n",
                      cnt, acc[0] / cnt, acc[1] / cnt, acc[2] / cnt, acc[3] / cnt, acc[4] / cnt,
                      acc[5] / cnt, acc[6] / cnt);
         cudaFree(trace);

@@ -74,11 +74,14 @@ __global__ void __launch_bounds__(kSBlock, CRB_SMALL_MINB) small_loop_kernel(con
   const long long nwarps = nthreads >> 5;
   const long long N = a.N;
   DevCtrl* c = a.ctrl;
-  // block 0 runs the control step on a shared-memory copy of the state (loaded
-  // once per launch, written back when the launch ends); every iteration it
-  // publishes the fields the other blocks read (halt, cur, s_cur, s_prev, beta)
+  // every block keeps the control state in shared memory (loaded once per
+  // launch) and runs the control step itself on the same fixed-order sums, so
+  // all blocks take identical decisions without a broadcast; block 0 writes the
+  // history and the final state
   __shared__ DevCtrl sctrl;
-  if (blockIdx.x == 0 && threadIdx.x == 0) sctrl = *c;
+  if (threadIdx.x < (int)(sizeof(DevCtrl) / 8))
+    reinterpret_cast<unsigned long long*>(&sctrl)[threadIdx.x] =
+        __ldcg(reinterpret_cast<const unsigned long long*>(c) + threadIdx.x);
   const bool tr0 = a.trace != nullptr && blockIdx.x == 0 && threadIdx.x == 0;
   auto stamp = [&](long long it, int k) {
     if (tr0 && it < 64) {
@@ -87,26 +90,39 @@ __global__ void __launch_bounds__(kSBlock, CRB_SMALL_MINB) small_loop_kernel(con
       a.trace[it * 8 + k] = t;
     }
   };
+  // the block's points (contiguous) for the reduction and the primal closed form
+  const long long ppb = (N + gridDim.x - 1) / gridDim.x;
+  const long long pl0 = (long long)blockIdx.x * ppb;
+  const long long pl1 = min(N, pl0 + ppb);
+  const long long nk2 = gridDim.x;
+  // K2 of the next iteration for the block's points -> k2part[parity][block]
+  auto primal_phase = [&]() {
+    const int cur = sctrl.cur;
+    const double* vposc = cur ? a.pa.vpos1 : a.pa.vpos0;
+    double* vposp = cur ? a.pa.vpos0 : a.pa.vpos1;
+    double acc[kK2Scal];
+#pragma unroll
+    for (int w = 0; w < kK2Scal; ++w) acc[w] = 0.0;
+    for (long long l = pl0 + threadIdx.x; l < pl1; l += kSBlock)
+      primal_point<NN>(a.pa, l, sctrl.s_cur, sctrl.s_prev, sctrl.beta, vposc, vposp, acc);
+    block_reduce_store<kK2Scal, kSBlock>(
+        acc, a.k2part + (((sctrl.ell + 1) & 1) * nk2 + blockIdx.x) * kK2Scal);
+  };
+  __syncthreads();
+  if (!sctrl.halt) primal_phase();  // the first iteration's primal
+  grid.sync();
 
   for (long long it = 0; it < a.max_iters; ++it) {
     stamp(it, 0);
-    if (__ldcg(&c->halt)) break;  // written before the last grid barrier
-    const int cur = __ldcg(&c->cur);
-    const double s_c = __ldcg(&c->s_cur), s_p = __ldcg(&c->s_prev), beta = __ldcg(&c->beta);
-    const double* vposc = cur ? a.pa.vpos1 : a.pa.vpos0;
-    double* vposp = cur ? a.pa.vpos0 : a.pa.vpos1;
-
-    // ---- A: primal closed form (K2)
-    {
-      double acc[kK2Scal];
-#pragma unroll
-      for (int w = 0; w < kK2Scal; ++w) acc[w] = 0.0;
-      for (long long l = tid; l < N; l += nthreads)
-        primal_point<NN>(a.pa, l, s_c, s_p, beta, vposc, vposp, acc);
-      block_reduce_store<kK2Scal, kSBlock>(acc, a.k2part + (long long)blockIdx.x * kK2Scal);
+    if (sctrl.halt) break;  // identical in every block
+    const int cur = sctrl.cur;
+    const double s_c = sctrl.s_cur, s_p = sctrl.s_prev, beta = sctrl.beta;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {  // one clock for the time budget of every block
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      __stcg(&a.clock[0], t);
     }
     stamp(it, 1);
-    grid.sync();
     stamp(it, 2);
 
     // ---- B: pair sweep
@@ -231,80 +247,84 @@ __global__ void __launch_bounds__(kSBlock, CRB_SMALL_MINB) small_loop_kernel(con
     grid.sync();
     stamp(it, 4);
 
-    // ---- C: fixed-order reduction (+ scalars and control in block 0)
+    // ---- C + control + the next iteration's primal, in every block:
+    // warps 0-3 reduce the scalar records (sweep + K2, fixed order) and thread 0
+    // runs the control step; warps 4-7 reduce the block's points' aggregates
+    // (8 lanes per element over its contiguous partials); then the primal
     {
-      // 8 lanes per output element: its partials are contiguous (colpart
-      // [N(n+1)][P], rowpart [N][S]); lane g of the group sums the g-th
-      // contiguous slice, then a fixed 3-step butterfly inside the group
       const long long ncol = N * (NN + 1);
-      const int g = lane & 7;
-      // warp-uniform loop (4 elements per warp) so the group shuffles see every lane
-      for (long long eb = (tid >> 5) * 4; eb < ncol + N; eb += (nthreads >> 5) * 4) {
-        const long long e = eb + (lane >> 3);
-        const bool colp = e < ncol;
-        const double* src = colp ? a.colpart + e * a.P : a.rowpart + (e - ncol) * a.S;
-        const int cnt = e < ncol + N ? (colp ? a.P : a.S) : 0;
-        const int per = (cnt + 7) >> 3;
-        const int lo = g * per, hi = min(cnt, lo + per);
-        double s = 0.0;
-        for (int p0 = lo; p0 < hi; p0 += 8) {
-          double v[8];
-#pragma unroll
-          for (int u = 0; u < 8; ++u) v[u] = p0 + u < hi ? __ldcg(src + p0 + u) : 0.0;
-#pragma unroll
-          for (int u = 0; u < 8; ++u)
-            if (p0 + u < hi) s += v[u];
-        }
-        s += __shfl_xor_sync(0xffffffffu, s, 1);
-        s += __shfl_xor_sync(0xffffffffu, s, 2);
-        s += __shfl_xor_sync(0xffffffffu, s, 4);
-        if (g == 0 && e < ncol + N) __stcg(a.xbuf + (colp ? N + e : e - ncol), s);
-      }
-      stamp(it, 5);
-      if (blockIdx.x == 0) {
-        // scalar records: thread order, warp butterflies, warps in order
+      const int w = threadIdx.x >> 5;
+      if (w < 4) {
         constexpr int W = kScal + kK2Scal;
+        const long long par = ((sctrl.ell + 1) & 1) * nk2;
         double v[W];
 #pragma unroll
-        for (int w = 0; w < W; ++w) v[w] = 0.0;
-        for (long long i = threadIdx.x; i < gridDim.x; i += kSBlock) {
+        for (int k = 0; k < W; ++k) v[k] = 0.0;
+        for (long long i = threadIdx.x; i < gridDim.x; i += 128) {
 #pragma unroll
-          for (int w = 0; w < kScal; ++w) v[w] += __ldcg(a.scalpart + i * kScal + w);
+          for (int k = 0; k < kScal; ++k) v[k] += __ldcg(a.scalpart + i * kScal + k);
 #pragma unroll
-          for (int w = 0; w < kK2Scal; ++w) v[kScal + w] += __ldcg(a.k2part + i * kK2Scal + w);
+          for (int k = 0; k < kK2Scal; ++k) v[kScal + k] += __ldcg(a.k2part + (par + i) * kK2Scal + k);
         }
 #pragma unroll
-        for (int w = 0; w < W; ++w) {
+        for (int k = 0; k < W; ++k) {
 #pragma unroll
-          for (int o = 16; o > 0; o >>= 1) v[w] += __shfl_xor_sync(0xffffffffu, v[w], o);
+          for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
         }
-        __shared__ double wsc[kSBlock / 32][W];
+        __shared__ double sh[4][W];
         __shared__ double out[W];
         if (lane == 0) {
 #pragma unroll
-          for (int w = 0; w < W; ++w) wsc[threadIdx.x >> 5][w] = v[w];
+          for (int k = 0; k < W; ++k) sh[w][k] = v[k];
         }
-        __syncthreads();
-        if (threadIdx.x < W) {
-          double t = 0.0;
-#pragma unroll
-          for (int k = 0; k < kSBlock / 32; ++k) t += wsc[k][threadIdx.x];
-          out[threadIdx.x] = t;
-        }
-        __syncthreads();
+        asm volatile("bar.sync 2, 128;" ::: "memory");
+        if (threadIdx.x < W) out[threadIdx.x] = ((sh[0][threadIdx.x] + sh[1][threadIdx.x]) + sh[2][threadIdx.x]) +
+                                                sh[3][threadIdx.x];
+        asm volatile("bar.sync 2, 128;" ::: "memory");
         if (threadIdx.x == 0) {
-          double* scal = a.xbuf + N + ncol;
-          for (int w = 0; w < kScal; ++w) scal[w] = out[w];
-          for (int w = 0; w < kK2Scal; ++w) a.k2sum[w] = out[kScal + w];
-          if (!sctrl.halt) control_step(&sctrl, out, out + kScal, a.hist);
-          __stcg(&c->halt, sctrl.halt);
-          __stcg(&c->cur, sctrl.cur);
-          __stcg(&c->s_cur, sctrl.s_cur);
-          __stcg(&c->s_prev, sctrl.s_prev);
-          __stcg(&c->beta, sctrl.beta);
-          __threadfence();
+          if (blockIdx.x == 0) {
+            double* scal = a.xbuf + N + ncol;
+            for (int k = 0; k < kScal; ++k) scal[k] = out[k];
+            for (int k = 0; k < kK2Scal; ++k) a.k2sum[k] = out[kScal + k];
+          }
+          if (!sctrl.halt) {
+            const double wall = (double)(__ldcg(&a.clock[0]) - sctrl.t_start_ns) * 1e-9;
+            control_step(&sctrl, out, out + kScal, blockIdx.x == 0 ? a.hist : nullptr, wall);
+          }
+        }
+      } else {
+        const int t4 = threadIdx.x - 128;
+        const int g = lane & 7;
+        const long long nel = (pl1 - pl0) * (NN + 2);  // (n+1) column values + the row sum per point
+        // warp-uniform loop (4 elements per warp) so the group shuffles see every lane
+        for (long long eb = (t4 >> 5) * 4; eb < nel; eb += 16) {
+          const long long e = eb + (lane >> 3);
+          const bool ok = e < nel;
+          const long long l = pl0 + (ok ? e / (NN + 2) : 0);
+          const int j = ok ? (int)(e % (NN + 2)) : 0;
+          const bool colp = j <= NN;
+          const double* src = colp ? a.colpart + (l * (NN + 1) + j) * a.P : a.rowpart + l * a.S;
+          const int cnt = ok ? (colp ? a.P : a.S) : 0;
+          const int per = (cnt + 7) >> 3;
+          const int lo = g * per, hi = min(cnt, lo + per);
+          double sum = 0.0;
+          for (int p0 = lo; p0 < hi; p0 += 8) {
+            double vv[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) vv[u] = p0 + u < hi ? __ldcg(src + p0 + u) : 0.0;
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+              if (p0 + u < hi) sum += vv[u];
+          }
+          sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+          sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+          sum += __shfl_xor_sync(0xffffffffu, sum, 4);
+          if (g == 0 && ok) __stcg(a.xbuf + (colp ? N + l * (NN + 1) + j : l), sum);
         }
       }
+      __syncthreads();
+      stamp(it, 5);
+      if (!sctrl.halt) primal_phase();  // identical decision in every block
     }
     stamp(it, 6);
     grid.sync();

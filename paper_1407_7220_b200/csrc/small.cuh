@@ -23,6 +23,7 @@ struct SmallArgs {
   long long max_iters; // iterations this launch may run (halts earlier on termination)
   int S, P;            // 32-column strips, row chunks
   unsigned long long* trace;  // optional: block 0 phase timestamps (CRB_TRACE), 8 per iteration
+  unsigned long long* clock;  // one timestamp per iteration (block 0): every block's time budget
 };
 
 struct SmallInfo {
