@@ -21,6 +21,7 @@ GEN_KINDS = {
     "sqnorm-uniform": 10, "maxaffine-uniform": 11, "lse-uniform": 12,
 }
 REASONS = {0: "thresholds", 1: "iter_budget", 2: "time_budget", 3: "error"}
+REASONS_INV = {v: k for k, v in REASONS.items()}
 
 
 class CroConfig(C.Structure):
