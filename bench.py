@@ -11,9 +11,13 @@ GPU sweeps the same 1e8 pairs per iteration over its row block.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
---impl reference times the reference's algorithm on the host CPU (the
-oracle port, oracle/cvxreg_oracle.c, all host threads; the reference itself
-cannot be built here) on the same config and metric.
+--impl reference times the reference's own CPU implementation on the host
+cores: oracle/_ref (the reference's proj/core sources compiled unmodified, see
+oracle/Makefile target `ref`) when it is present, run on a bounded sample of
+the same workload (same generator and n, N <= 2000: its sigma_C estimation is
+two single-threaded O(N^2 n) passes per power step and cannot be injected);
+the oracle port (oracle/cvxreg_oracle.c, all host threads, full N) otherwise.
+The line carries both numbers.
 """
 from __future__ import annotations
 
@@ -47,6 +51,7 @@ CONFIGS = {  # BASELINE.json configs
 SIGMA_C = {"cfg1": 75.04526292327877, "cfg2": 289.16619141812674, "cfg3": 532.8884553986682,
            "cfg4": 664.0047049267016, "cfg5": 781.778824412929}
 CPU_SAMPLE_S = 30.0  # bound on one CPU sample's work (seconds)
+REF_SAMPLE_N = 2000  # N of the compiled reference's bounded sample (sigma_C: ~320 power steps)
 
 
 def parse():
@@ -192,6 +197,42 @@ def cpu_oracle_rate(name, cfg, threads, warm, steps, inst=None):
     return N * N / per_iter, spent, sample, per_iter
 
 
+def cpu_reference_available():
+    from oracle import ref as R
+
+    return R.available()
+
+
+def cpu_reference_rate(cfg, threads, warm, steps):
+    """The REFERENCE's own papg_solve (oracle/_ref: proj/core compiled unmodified, singleton
+    blocks through Partition{N, 1}) on a bounded sample of the workload: same generator, n,
+    noise and seed at N = min(N_cfg, REF_SAMPLE_N). The timed span is the history's wall clock
+    (papg.cpp:220) from the end of iteration `warm` to the end of iteration warm + steps: the
+    reference's own sigma_C estimation (papg.cpp:66; it cannot be injected) and the final
+    re-solve are outside it. `threads` are the block-pool workers (papg.cpp:69-72); the
+    operators are single-threaded (operators.cpp:128-180).
+    Returns (pair-updates/s, seconds per iteration, sample text, total seconds)."""
+    from oracle import oracle as O
+    from oracle import ref as R
+
+    N = min(cfg["N"], REF_SAMPLE_N)
+    X, y = O.gen_instance(cfg["kind"], N, cfg["n"], cfg["noise"], 1, cfg["pieces"])
+    P = R.prepare(X, y)
+    t0 = time.perf_counter()
+    r = R.papg(X, P.ys, feas_y=P.feas_y, feas_xi=P.feas_xi, max_iters=warm + steps,
+               gap_norm_tol=-1.0, infeas_norm_tol=-1.0, threads=threads, want_theta=False)
+    spent = time.perf_counter() - t0
+    h = r.history
+    t_lo = h[warm - 1, 7] if warm > 0 else 0.0
+    per_iter = max(h[warm + steps - 1, 7] - t_lo, 1e-9) / steps
+    sample = (f"{cfg['kind']} N={N} n={cfg['n']} (bounded sample of N={cfg['N']}): dual iterations "
+              f"{warm + 1}..{warm + steps} of the reference's papg_solve compiled from proj/core "
+              f"(history wall clock, its sigma_C estimation excluded), {threads} block-pool "
+              f"worker(s), single-threaded operators, {per_iter:.3f} s/iteration, "
+              f"{spent:.0f} s in all")
+    return N * N / per_iter, per_iter, sample, spent
+
+
 def cpu_time_to_tolerance(name, cfg, threads, inst=None):
     """Oracle solve of the config to its tolerance (cfg 2: |gap_norm| <= 1e-4, infeas_norm
     <= 0.1), sigma_C injected: measured, not extrapolated."""
@@ -210,6 +251,8 @@ def run_reference(args):
         return 0
     cfg = workload(args.config, 1)
     threads = os.cpu_count() or 1
+    if cpu_reference_available():
+        return run_reference_compiled(args, cfg, threads)
     ok, need, avail = cpu_feasible(cfg)
     if not ok:
         print(json.dumps({"impl": "reference", "unavailable":
@@ -245,6 +288,37 @@ def run_reference(args):
         "note": "oracle/cvxreg_oracle.c (CPU restatement of papg.cpp:136-283, OpenMP rows); "
                 "the reference does not build here (Eigen3/vendor absent, alcc.cpp:200-203)",
     }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_reference_compiled(args, cfg, threads):
+    """--impl reference with oracle/_ref present: the reference's own code (bounded sample),
+    and the oracle port on all host threads at the full N beside it when that is feasible."""
+    W, K = max(args.warmup, 1), max(args.steps, 1)
+    rate, per, sample, _ = cpu_reference_rate(cfg, threads, W, K)
+    Ns = min(cfg["N"], REF_SAMPLE_N)
+    line = {
+        "impl": "reference", "metric": "pair-constraint updates/s", "value": rate,
+        "unit": "pair-updates/s", "n_gpus": args.gpus, "steps": K, "warmup": W,
+        "ms_per_step": per * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{args.config}: {cfg['kind']} N={cfg['N']} n={cfg['n']}",
+                   "N": cfg["N"], "n": cfg["n"], "pairs_per_step": cfg["N"] ** 2,
+                   "sample_N": Ns, "sample_pairs_per_step": Ns * Ns},
+        "cpu_baseline": {"value": rate, "unit": "pair-updates/s", "cores": threads,
+                         "kind": "reference", "sample": sample},
+        "e2e": {"value": rate, "unit": "pair-updates/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "note": "oracle/_ref: the reference's proj/core sources compiled unmodified (Eigen calls "
+                "served by oracle/eigen_shim, see DESIGN.md section 6); the per-pair rate does not "
+                "depend on N (0.0235 G/s at N = 2000, 0.0232 at N = 4000 in the build container)",
+    }
+    ok, _, _ = cpu_feasible(cfg)
+    if ok and cfg["N"] <= 10000:
+        pr, _, ps, _ = cpu_oracle_rate(args.config, cfg, threads, 1, 3)
+        line["cpu_port_allcores"] = {"value": pr, "unit": "pair-updates/s", "cores": threads,
+                                     "kind": "port", "sample": ps}
     print(json.dumps(line), flush=True)
     return 0
 
@@ -436,6 +510,13 @@ def run_ours(args):
         rate, spent, sample, per = cpu_oracle_rate(args.config, cfg, threads, 1, 3, inst)
         cpu = {"value": rate, "unit": "pair-updates/s", "cores": threads, "kind": "port",
                "sample": sample}
+        if cpu_reference_available():
+            # the reference's own compiled code on a bounded sample is the baseline; the
+            # all-core OpenMP port at the full N stays beside it
+            extras["cpu_port_allcores"] = cpu
+            rr, _, rs, _ = cpu_reference_rate(cfg, threads, 1, 3)
+            cpu = {"value": rr, "unit": "pair-updates/s", "cores": threads, "kind": "reference",
+                   "sample": rs}
         # the 1-thread rate beside the all-core one (the reference's
         # operators.cpp:128-180 are single-threaded); one iteration when it fits the bound
         est1 = per * threads

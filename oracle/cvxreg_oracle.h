@@ -7,12 +7,19 @@
  * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
  * --impl reference legs may load it. The product library never links it.
  *
- * Parity status: the reference cannot be compiled here (Eigen3 and vendor/
- * headers absent, alcc.cpp:200-203 arity error) and cannot run singleton
- * blocks (dataset.cpp:125-126). It ships no tests or golden vectors. This
- * restatement is therefore pinned against the SPEC.md worked examples and
- * analytic known-answer tests only ("parity unpinned" w.r.t. a reference
- * binary; see DESIGN.md section "Oracle").
+ * Parity status: PINNED to the reference's own code. The reference's proj/core
+ * sources compile unmodified into oracle/_ref/libcvxreg_ref.so (oracle/Makefile
+ * target `ref`: Eigen calls served by oracle/eigen_shim, alcc.cpp through
+ * ref_build/alcc_tu.cpp because of its arity error at alcc.cpp:200-203; the
+ * singleton mode that make_partition rejects, dataset.cpp:125-126, is reached
+ * with Partition{N, 1} built directly). tests/test_oracle_vs_reference.py
+ * compares this restatement with it live and against the committed outputs
+ * tests/golden/ref_*.npz (scripts/make_ref_golden.py): operators, generators,
+ * PRNG streams and the singleton P-APG trajectory agree bitwise or to 1e-13,
+ * sigma_max with identical step counts, general K and ALCC with identical
+ * iteration counts. The SPEC.md worked examples and analytic known-answer
+ * tests (tests/test_oracle_spec.py) stay as a second pin. See DESIGN.md
+ * section "Oracle".
  */
 #ifndef CVXREG_ORACLE_H
 #define CVXREG_ORACLE_H
