@@ -116,9 +116,23 @@ const char *cr_status_string(cr_status s);
 /* ---- multi-GPU: one handle per rank, NCCL allreduce over NVLink ----------- */
 cr_status cr_nccl_unique_id(uint8_t id_out[128]);
 cr_status cr_attach_nccl(cr_handle *h, const uint8_t id[128], int rank, int world);
-/* Host-exchange seam (tests / emulation): bytes of the per-iteration
-   aggregate payload, see cr_papg_iterate_phased. */
+/* Host-exchange seam (tests / emulation): doubles of the per-iteration
+   aggregate payload (canonical-block mode: of all D block payloads). */
 int64_t cr_exchange_len(const cr_handle *h);
+/* GPU-count-invariant sums (results must not depend on the
+   worker count; the reference gathers block results in block order,
+   papg.cpp:122-129). Rows are cut into D canonical blocks
+   [floor(j N / D), floor((j + 1) N / D)); the handle's rows must be a union of
+   blocks (world | D with the balanced shards of cr_create's callers). Every
+   block is swept by its own launches with its own CTA shares, its payload
+   reduced on its own, the payloads of all ranks are allgathered (instead of
+   the allreduce) and summed in block order 0..D-1 on every rank. theta, y and
+   xi after k iterations are then bitwise the same on 1, 2, 4 ... GPUs for a
+   fixed D. D = 0 (default) turns it off. Call before cr_papg_begin;
+   singleton blocks only. cr_canonical_blocks reports D, the handle's first
+   block and its block count. */
+cr_status cr_set_canonical_blocks(cr_handle *h, int32_t D);
+cr_status cr_canonical_blocks(const cr_handle *h, int32_t *D, int32_t *first, int32_t *count);
 
 /* ---- sigma_max(C) by power iteration (operators.cpp:302-339) ------------- */
 cr_status cr_sigma_C(cr_handle *h, double tol, int32_t max_iters, double *sigma,

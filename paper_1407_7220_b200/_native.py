@@ -77,6 +77,7 @@ EXPORTS = [
     "cr_gen_instance", "cr_prepare_problem", "cr_certificate", "cr_momentum_next",
     "cr_sigma_A", "cr_alcc_solve", "cr_alcc_multiplier", "cr_time_penalty_sweep",
     "cr_set_partition", "cr_partition_stats", "cr_sweep_store_count",
+    "cr_set_canonical_blocks", "cr_canonical_blocks",
 ]
 
 _lib = None
@@ -106,6 +107,8 @@ def load():
         "cr_nccl_unique_id": (st, [C.c_char_p]),
         "cr_attach_nccl": (st, [vp, C.c_char_p, C.c_int, C.c_int]),
         "cr_exchange_len": (i64, [vp]),
+        "cr_set_canonical_blocks": (st, [vp, i32]),
+        "cr_canonical_blocks": (st, [vp, C.POINTER(i32), C.POINTER(i32), C.POINTER(i32)]),
         "cr_sigma_C": (st, [vp, d, i32, _P, C.POINTER(i32), C.POINTER(i32)]),
         "cr_papg_begin": (st, [vp, C.POINTER(PapgConfigC), _P]),
         "cr_papg_iterate": (st, [vp, i64, C.POINTER(i64), C.POINTER(i32)]),

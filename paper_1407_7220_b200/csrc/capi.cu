@@ -64,10 +64,10 @@ namespace crb {
 // shared-memory pitch padding). Encoded once per handle through the driver
 // entry point (cudart is linked statically; no -lcuda). CRB_TMAP=0 keeps the
 // per-row bulk copies.
-static void encode_sweep_tmaps(cr_handle* h) {
-  h->tmap_ok = false;
+// Tensor maps of rows [row_off, row_off + rows) of both dual buffers.
+static bool encode_tmap_pair(cr_handle* h, int64_t row_off, int64_t rows, TmapBytes out[2]) {
   const char* env = std::getenv("CRB_TMAP");
-  if ((env && env[0] == '0') || h->variant != kSweepMma || h->R <= 0) return;
+  if ((env && env[0] == '0') || h->variant != kSweepMma || rows <= 0) return false;
   static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
   if (!encode) {
     void* fn = nullptr;
@@ -75,7 +75,7 @@ static void encode_sweep_tmaps(cr_handle* h) {
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
         q != cudaDriverEntryPointSuccess || !fn) {
       cudaGetLastError();
-      return;
+      return false;
     }
     encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
   }
@@ -85,25 +85,27 @@ static void encode_sweep_tmaps(cr_handle* h) {
   // last tile alias the next row (never consumed: those warps are inactive); the
   // buffers carry TC doubles of slack for the last row's.
   const cuuint64_t TC = (cuuint64_t)h->kp.tile_cols;
-  if (TC + 2 > 256 || h->T > INT_MAX || h->R > INT_MAX) return;
+  if (TC + 2 > 256 || h->T > INT_MAX || rows > INT_MAX) return false;
   static_assert(sizeof(TmapBytes) == sizeof(CUtensorMap), "tensor map size");
   for (int b = 0; b < 2; ++b) {
-    const cuuint64_t dims[3] = {TC, (cuuint64_t)h->T, (cuuint64_t)h->R};
+    const cuuint64_t dims[3] = {TC, (cuuint64_t)h->T, (cuuint64_t)rows};
     const cuuint64_t strides[2] = {TC * sizeof(double), (cuuint64_t)h->ld * sizeof(double)};
     const cuuint32_t box[3] = {(cuuint32_t)TC + 2, 1, 8};
     const cuuint32_t estr[3] = {1, 1, 1};
     CUtensorMap m;
-    const CUresult r = encode(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, h->V[b], dims, strides, box, estr,
-                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                              CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    const CUresult r = encode(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, h->V[b] + row_off * h->ld,
+                              dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                              CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) {
       if (std::getenv("CRB_DEBUG")) std::fprintf(stderr, "cvxreg_b200: tensor map encode failed (%d)\n", (int)r);
-      return;
+      return false;
     }
-    std::memcpy(&h->tmV[b], &m, sizeof(m));
+    std::memcpy(&out[b], &m, sizeof(m));
   }
-  h->tmap_ok = true;
+  return true;
 }
+static void encode_sweep_tmaps(cr_handle* h) { h->tmap_ok = encode_tmap_pair(h, 0, h->R, h->tmV); }
   // general.cu: P-APG(ALCC) with K blocks
 cr_status general_begin(cr_handle* h);
 cr_status general_iterate(cr_handle* h, int64_t max_steps, int64_t* done, int32_t* stopped,
@@ -143,11 +145,108 @@ PrimalArgs primal_args(cr_handle* h, int mode) {
   return a;
 }
 
+void release_canon(cr_handle* h) {
+  for (CanonBlock& b : h->canon) {
+    dfree(b.colpart, h->st);
+    dfree(b.rowpart, h->st);
+    dfree(b.scalpart, h->st);
+  }
+  h->canon.clear();
+  dfree(h->canon_pay, h->st);
+  h->canon_pay = nullptr;
+  h->canon_D = 0;
+  h->canon_first = 0;
+}
+
+// canonical-block views of the sweep / reduce arguments
+SweepArgs sweep_args_block(cr_handle* h, const CanonBlock& b, int mode, bool agg_only) {
+  SweepArgs a = sweep_args(h, mode, agg_only);
+  a.V0 = h->V[0] + b.a * h->ld;
+  a.V1 = h->V[1] + b.a * h->ld;
+  a.colpart = b.colpart;
+  a.rowpart = b.rowpart;
+  a.scalpart = b.scalpart;
+  a.R = b.R;
+  a.r0 = h->r0 + b.a;
+  a.G = b.G;
+  a.U = b.U;
+  a.maxspan = b.maxspan;
+  a.tmap = 0;
+  if (b.tmap_ok) {
+    a.tmV[0] = b.tmV[0];
+    a.tmV[1] = b.tmV[1];
+    a.tmap = 1;
+  }
+  return a;
+}
+
+ReduceArgs reduce_args_block(cr_handle* h, const CanonBlock& b, int index, bool with_k2,
+                             const int* stopped) {
+  ReduceArgs a = reduce_args(h, with_k2, stopped, false, papg_sweep(h).scal_recs);
+  a.colpart = b.colpart;
+  a.rowpart = b.rowpart;
+  a.scalpart = b.scalpart;
+  a.agg_out = h->canon_pay + (size_t)(h->canon_first + index) * (size_t)payload_len(h);
+  a.rank = 0;  // a halted solve keeps every block payload (the combine is idempotent)
+  a.R = b.R;
+  a.r0 = h->r0 + b.a;
+  a.nw = (long long)b.G * papg_sweep(h).scal_recs;
+  a.G = b.G;
+  a.U = b.U;
+  a.maxspan = b.maxspan;
+  return a;
+}
+
+// sweeps + reduces of the local canonical blocks, then (use_nccl) the allgather of
+// the block payloads; the combine is left to the caller's finish phase
+cr_status enqueue_canon_local(cr_handle* h, bool agg_only, const int* stopped, bool with_k2,
+                              cudaEvent_t ev_a, cudaEvent_t ev_b, bool use_nccl,
+                              cudaEvent_t ev_c, cudaEvent_t ev_d) {
+  if (ev_a) CUDA_TRY(cudaEventRecord(ev_a, h->st));
+  for (const CanonBlock& b : h->canon) {
+    const SweepArgs sa = sweep_args_block(h, b, kModePapg, agg_only);
+    CUDA_TRY((cudaError_t)launch_sweep(papg_sweep(h), sa, h->st));
+  }
+  if (ev_b) CUDA_TRY(cudaEventRecord(ev_b, h->st));
+  for (size_t i = 0; i < h->canon.size(); ++i) {
+    const ReduceArgs ra = reduce_args_block(h, h->canon[i], (int)i, with_k2 && i == 0, stopped);
+    CUDA_TRY(launch_reduce(ra, h->st));
+  }
+  if (use_nccl && h->comm) {
+    const size_t count = h->canon.size() * (size_t)payload_len(h);
+    if (ev_c) CUDA_TRY(cudaEventRecord(ev_c, h->st));
+    NCCL_TRY(ncclAllGather(h->canon_pay + (size_t)h->canon_first * (size_t)payload_len(h),
+                           h->canon_pay, count, ncclDouble, h->comm, h->st));
+    if (ev_d) CUDA_TRY(cudaEventRecord(ev_d, h->st));
+  }
+  return CR_OK;
+}
+
+cr_status enqueue_canon_combine(cr_handle* h) {
+  CUDA_TRY(launch_canon_combine(h->canon_pay, h->canon_D, payload_len(h), h->xbuf, h->st));
+  return CR_OK;
+}
+
 // Enqueue one dual iteration (papg.cpp:176-263). phase: 0 = all,
 // 1 = local part only (K2, K1, K3), 2 = finish only (control).
 
 cr_status enqueue_iteration(cr_handle* h, int phase, cudaEvent_t ev_a, cudaEvent_t ev_b,
                             bool use_nccl, cudaEvent_t ev_c, cudaEvent_t ev_d) {
+  if (!h->canon.empty()) {  // canonical row blocks: per-block launches, ordered combine
+    if (phase != 2) {
+      const PrimalArgs pa = primal_args(h, 0);
+      CUDA_TRY(launch_primal(pa, h->st));
+      const cr_status s = enqueue_canon_local(h, false, &h->ctrl_d->halt, true, ev_a, ev_b,
+                                              use_nccl, ev_c, ev_d);
+      if (s != CR_OK) return s;
+    }
+    if (phase != 1) {
+      const cr_status s = enqueue_canon_combine(h);
+      if (s != CR_OK) return s;
+      CUDA_TRY(launch_control(h->ctrl_d, h->xbuf + h->N * (h->n + 2), h->k2sum, h->hist, h->st));
+    }
+    return CR_OK;
+  }
   if (phase != 2) {
     const PrimalArgs pa = primal_args(h, 0);
     CUDA_TRY(launch_primal(pa, h->st));
@@ -174,7 +273,10 @@ cr_status enqueue_iteration(cr_handle* h, int phase, cudaEvent_t ev_a, cudaEvent
 }
 
 // our kernels per iteration (the NCCL allreduce kernel is not counted)
-int launches_per_iteration(const cr_handle* h) { return h->comm ? 4 : 3; }
+int launches_per_iteration(const cr_handle* h) {
+  if (!h->canon.empty()) return 3 + 2 * (int)h->canon.size();  // primal, sweeps, reduces, combine, control
+  return h->comm ? 4 : 3;
+}
 
 cr_status build_graph(cr_handle* h) {
   if (h->gexec) {
@@ -270,7 +372,10 @@ const char* cr_status_string(cr_status s) {
 
 const char* cr_last_error(const cr_handle* h) { return h ? h->err.c_str() : "null handle"; }
 
-int64_t cr_exchange_len(const cr_handle* h) { return h ? payload_len(h) : 0; }
+int64_t cr_exchange_len(const cr_handle* h) {
+  if (!h) return 0;
+  return h->canon.empty() ? payload_len(h) : (int64_t)h->canon_D * payload_len(h);
+}
 
 cr_status cr_create(const double* Xh, const double* ybar_shifted, int64_t N, int64_t n,
                     double gamma, int device, int64_t row_begin, int64_t row_end,
@@ -433,6 +538,7 @@ void cr_destroy(cr_handle* h) {
                     h->gram,    h->ps_part, h->ps_part2, h->ps_state, h->sv_u12};
   for (double* b : bufs) dfree(b, h->st);
   for (double* b : {h->s_colpart, h->s_rowpart, h->s_scalpart, h->s_k2part}) dfree(b, h->st);
+  release_canon(h);
   dfree(h->izero, h->st);
   dfree(h->counter, h->st);
   dfree(h->d_stores, h->st);
@@ -448,6 +554,72 @@ void cr_destroy(cr_handle* h) {
   if (h->ev_poll[1]) cudaEventDestroy(h->ev_poll[1]);
   if (h->st) cudaStreamDestroy(h->st);
   delete h;
+}
+
+cr_status cr_set_canonical_blocks(cr_handle* h, int32_t D) {
+  if (!h || D < 0) return CR_EINVAL;
+  if (h->begun && h->gexec) {
+    cudaGraphExecDestroy(h->gexec);
+    h->gexec = nullptr;
+  }
+  CUDA_TRY(cudaSetDevice(h->device));
+  CUDA_TRY(cudaStreamSynchronize(h->st));
+  release_canon(h);
+  if (D == 0) return CR_OK;
+  if (h->part.K > 0) return fail(h, CR_EINVAL, "canonical blocks: singleton blocks only");
+  const int64_t N = h->N;
+  if (D > N) return fail(h, CR_EINVAL, "canonical blocks: more blocks than rows");
+  // block j = rows [floor(j N / D), floor((j + 1) N / D)): the shard must be a union of blocks
+  auto bound = [&](int64_t j) { return (int64_t)(((__int128)j * N) / D); };
+  int first = -1, last = -1;
+  for (int j = 0; j <= D; ++j) {
+    if (bound(j) == h->r0 && first < 0) first = j;
+    if (bound(j) == h->r1) last = j;
+  }
+  if (first < 0 || last <= first)
+    return fail(h, CR_EINVAL, "canonical blocks: the shard's rows are not a union of blocks");
+  int sms = 148;
+  CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
+  g_alloc_stream = h->st;
+  cudaError_t e = cudaSuccess;
+  for (int j = first; j < last && e == cudaSuccess; ++j) {
+    CanonBlock b;
+    b.a = bound(j) - h->r0;
+    b.R = bound(j + 1) - bound(j);
+    const long long units = (long long)h->T * b.R;
+    long long G = (long long)sms * h->kp.max_blocks_per_sm;
+    G = std::min<long long>(G, (units + 63) / 64);
+    if (G < 1) G = 1;
+    b.U = (units + G - 1) / G;
+    b.G = (int)((units + b.U - 1) / b.U);
+    b.maxspan = (int)((b.U - 1) / b.R + 2);
+    e = dalloc(&b.colpart, (size_t)b.G * b.maxspan * h->kp.tile_cols * (h->n + 1));
+    if (e == cudaSuccess) e = dalloc(&b.rowpart, (size_t)h->T * b.R);
+    if (e == cudaSuccess) e = dalloc(&b.scalpart, (size_t)b.G * h->kp.warps_per_block * kScal);
+    b.tmap_ok = e == cudaSuccess && encode_tmap_pair(h, b.a, b.R, b.tmV);
+    h->canon.push_back(b);
+  }
+  if (e == cudaSuccess) e = dalloc(&h->canon_pay, (size_t)D * (size_t)payload_len(h));
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    release_canon(h);
+    return fail(h, CR_ENOMEM, "canonical blocks: device allocation failed");
+  }
+  h->canon_D = D;
+  h->canon_first = first;
+  CUDA_TRY(cudaMemsetAsync(h->canon_pay, 0, sizeof(double) * (size_t)D * (size_t)payload_len(h),
+                           h->st));
+  CUDA_TRY(cudaStreamSynchronize(h->st));
+  h->begun = false;  // geometry changed: begin again
+  return CR_OK;
+}
+
+cr_status cr_canonical_blocks(const cr_handle* h, int32_t* D, int32_t* first, int32_t* count) {
+  if (!h) return CR_EINVAL;
+  if (D) *D = h->canon_D;
+  if (first) *first = h->canon_first;
+  if (count) *count = (int32_t)h->canon.size();
+  return CR_OK;
 }
 
 cr_status cr_nccl_unique_id(uint8_t id_out[128]) {
@@ -661,6 +833,13 @@ cr_status begin_impl(cr_handle* h, const cr_papg_config* cfg, const double* thet
   if (smenv && smenv[0] == '0') want_small = false;
   if (smenv && smenv[0] == '1' && h->comm == nullptr && h->R == h->N && h->part.K == 0)
     want_small = true;
+  if (!h->canon.empty()) {
+    if (h->part.K > 0) return fail(h, CR_EINVAL, "canonical blocks: singleton blocks only");
+    if (h->comm && ((int)h->canon.size() * h->world != h->canon_D ||
+                    h->canon_first != h->rank * (int)h->canon.size()))
+      return fail(h, CR_EINVAL, "canonical blocks: every rank must own D / world consecutive blocks");
+    want_small = false;  // the persistent loop's shares are not canonical
+  }
   if (!resume) {
     CUDA_TRY(cudaMemsetAsync(h->V[0], 0, vbytes, h->st));
     CUDA_TRY(cudaMemsetAsync(h->V[1], 0, vbytes, h->st));
@@ -669,6 +848,9 @@ cr_status begin_impl(cr_handle* h, const cr_papg_config* cfg, const double* thet
     CUDA_TRY(cudaMemsetAsync(h->xbuf, 0, sizeof(double) * payload_len(h), h->st));
     CUDA_TRY(cudaMemsetAsync(h->aggsave, 0, sizeof(double) * payload_len(h), h->st));
   }
+  if (h->canon_pay)
+    CUDA_TRY(cudaMemsetAsync(h->canon_pay, 0,
+                             sizeof(double) * (size_t)h->canon_D * (size_t)payload_len(h), h->st));
 
   if (theta0 && h->part.K > 0) {
     const cr_status s = general_theta_in(h, theta0);
@@ -694,13 +876,20 @@ cr_status begin_impl(cr_handle* h, const cr_papg_config* cfg, const double* thet
     CUDA_TRY(cudaMemcpyAsync(h->stage, tpos, sizeof(double) * N, cudaMemcpyHostToDevice, h->st));
     CUDA_TRY(launch_pos_in(h->vpos[0], h->stage, N, h->st));
     // aggregates and |.|^2 of max(theta0, 0): a sweep with 1/L = 0 is a copy
-    const SweepArgs sa = sweep_args(h, kModePapg, true);
-    CUDA_TRY((cudaError_t)launch_sweep(papg_sweep(h), sa, h->st));
-    const ReduceArgs ra = reduce_args(h, false, nullptr, false, papg_sweep(h).scal_recs);
-    CUDA_TRY(launch_reduce(ra, h->st));
-    if (h->comm)
-      NCCL_TRY(ncclAllReduce(h->xbuf, h->xbuf, (size_t)payload_len(h), ncclDouble, ncclSum,
-                             h->comm, h->st));
+    if (!h->canon.empty()) {
+      cr_status cs = enqueue_canon_local(h, true, nullptr, false, nullptr, nullptr, true, nullptr,
+                                         nullptr);
+      if (cs == CR_OK) cs = enqueue_canon_combine(h);
+      if (cs != CR_OK) return cs;
+    } else {
+      const SweepArgs sa = sweep_args(h, kModePapg, true);
+      CUDA_TRY((cudaError_t)launch_sweep(papg_sweep(h), sa, h->st));
+      const ReduceArgs ra = reduce_args(h, false, nullptr, false, papg_sweep(h).scal_recs);
+      CUDA_TRY(launch_reduce(ra, h->st));
+      if (h->comm)
+        NCCL_TRY(ncclAllReduce(h->xbuf, h->xbuf, (size_t)payload_len(h), ncclDouble, ncclSum,
+                               h->comm, h->st));
+    }
     CUDA_TRY(launch_warm_ctrl(h->ctrl_d, h->xbuf + N * (h->n + 2), pos_sq, h->st));
   }
 
@@ -990,6 +1179,12 @@ cr_status cr_iter_local(cr_handle* h) {
 
 cr_status cr_exchange_get(cr_handle* h, double* buf) {
   if (!h || !buf) return CR_EINVAL;
+  if (!h->canon.empty()) {  // all D block payloads; only this shard's own blocks are current
+    CUDA_TRY(cudaMemcpyAsync(buf, h->canon_pay, sizeof(double) * (size_t)cr_exchange_len(h),
+                             cudaMemcpyDeviceToHost, h->st));
+    CUDA_TRY(cudaStreamSynchronize(h->st));
+    return CR_OK;
+  }
   CUDA_TRY(cudaMemcpyAsync(buf, h->xbuf, sizeof(double) * payload_len(h), cudaMemcpyDeviceToHost,
                            h->st));
   CUDA_TRY(cudaStreamSynchronize(h->st));
@@ -998,6 +1193,12 @@ cr_status cr_exchange_get(cr_handle* h, double* buf) {
 
 cr_status cr_exchange_put(cr_handle* h, const double* buf) {
   if (!h || !buf) return CR_EINVAL;
+  if (!h->canon.empty()) {  // the gathered block payloads (what ncclAllGather would leave)
+    CUDA_TRY(cudaMemcpyAsync(h->canon_pay, buf, sizeof(double) * (size_t)cr_exchange_len(h),
+                             cudaMemcpyHostToDevice, h->st));
+    CUDA_TRY(cudaStreamSynchronize(h->st));
+    return CR_OK;
+  }
   CUDA_TRY(cudaMemcpyAsync(h->xbuf, buf, sizeof(double) * payload_len(h), cudaMemcpyHostToDevice,
                            h->st));
   CUDA_TRY(cudaStreamSynchronize(h->st));

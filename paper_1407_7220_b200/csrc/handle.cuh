@@ -68,6 +68,19 @@ struct Partition {
 
 using namespace crb;  // the ABI translation units all work in crb
 
+// One canonical row block of the shard (cr_set_canonical_blocks): rows
+// [a, a + R) of the local buffers swept by their own launch, with their own
+// CTA shares and partial slots, so its payload does not depend on which GPU
+// holds the block or on how many blocks share that GPU.
+struct CanonBlock {
+  int64_t a = 0, R = 0;
+  long long U = 0;
+  int G = 0, maxspan = 0;
+  double *colpart = nullptr, *rowpart = nullptr, *scalpart = nullptr;
+  TmapBytes tmV[2] = {};
+  bool tmap_ok = false;
+};
+
 struct cr_handle {
   int device = 0;
   cudaStream_t st = nullptr;
@@ -112,6 +125,10 @@ struct cr_handle {
   DevCtrl* ctrl_h = nullptr;     // pinned mirror (latest copy)
   DevCtrl* ctrl_poll = nullptr;  // pinned, 2 polling slots
   long long* pause_h = nullptr;  // pinned {pause_at, halt}
+  // canonical row blocks (GPU-count-invariant sums); empty: off
+  std::vector<CanonBlock> canon;
+  int canon_D = 0, canon_first = 0;
+  double* canon_pay = nullptr;  // [canon_D][payload_len]: every block's payload
   // NCCL
   ncclComm_t comm = nullptr;
   int rank = 0, world = 1;

@@ -406,6 +406,23 @@ cudaError_t launch_reduce(const ReduceArgs& a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+// canonical-block mode: the payload is the sum of the D block payloads in block
+// order (left to right), whatever GPU produced each of them
+__global__ void canon_combine_kernel(const double* __restrict__ pay, int D, long long len,
+                                     double* __restrict__ out) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= len) return;
+  double s = pay[i];
+  for (int j = 1; j < D; ++j) s += pay[(long long)j * len + i];
+  out[i] = s;
+}
+
+cudaError_t launch_canon_combine(const double* pay, int D, long long len, double* out,
+                                 cudaStream_t s) {
+  canon_combine_kernel<<<(unsigned)((len + 255) / 256), 256, 0, s>>>(pay, D, len, out);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_control(DevCtrl* c, const double* scal, const double* k2, double* hist,
                            cudaStream_t s) {
   control_kernel<<<1, 32, 0, s>>>(c, scal, k2, hist);

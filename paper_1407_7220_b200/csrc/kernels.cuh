@@ -109,6 +109,8 @@ cudaError_t launch_primal(const PrimalArgs& a, cudaStream_t s);
 cudaError_t launch_reduce(const ReduceArgs& a, cudaStream_t s);
 cudaError_t launch_control(DevCtrl* c, const double* scal, const double* k2, double* hist,
                            cudaStream_t s);
+cudaError_t launch_canon_combine(const double* pay, int D, long long len, double* out,
+                                 cudaStream_t s);
 cudaError_t launch_begin(DevCtrl* c, cudaStream_t s);
 cudaError_t launch_stamp(unsigned long long* out, cudaStream_t s);
 cudaError_t launch_power_prep(const PowerArgs& a, cudaStream_t s);

@@ -7,7 +7,10 @@ momentum buffers). Every iteration each rank sweeps its rows and the ranks
 allreduce one payload of N(n+2)+4 doubles: row sums (owned rows, zeros
 elsewhere), column sums + V^T X (partial over rows) and the four sweep
 scalars. The O(N n) primal update is replicated, so y, xi and every control
-decision are identical on all ranks. The reference has no
+decision are identical on all ranks. With
+PapgConfig.canonical_blocks = D the ranks allgather D per-block payloads
+instead and sum them in block order, which makes the iterates bitwise
+independent of the GPU count (world | D). The reference has no
 distributed mode; this is the B200 scale-out of its
 single-process dual state (types.hpp:50-53).
 """
@@ -60,6 +63,8 @@ def papg_solve_sharded(prep: PreparedProblem, cfg: PapgConfig | None = None, mom
     `dual` holds this rank's rows of theta_cross and the (replicated) theta_pos."""
     cfg = cfg or PapgConfig()
     with sharded_solver(prep.data.xs, prep.data.ys, cfg.gamma, group=group) as s:
+        if cfg.canonical_blocks > 0:  # bitwise the same iterates on every world | D
+            s.set_canonical_blocks(cfg.canonical_blocks)
         s.begin(cfg, momentum)
         stopped = False
         while not stopped:

@@ -108,6 +108,7 @@ class PapgConfig:  # papg.hpp:7-21 (+ the partition size K of make_partition)
     sigma_C: float = 0.0       # > 0: inject sigma_max(C)
     graph_iters: int = 0       # 0 auto, > 0 graph batch, < 0 direct launches
     device: int = 0
+    canonical_blocks: int = 0  # D > 0: GPU-count-invariant sums over D row blocks
 
     def to_c(self, use_momentum: bool) -> nat.PapgConfigC:
         return nat.PapgConfigC(self.gamma, self.B_theta, int(self.adaptive_B_theta),
@@ -344,6 +345,18 @@ class DualSolver:
                self.h)
         return done.value, bool(stopped.value)
 
+    def set_canonical_blocks(self, D: int):
+        """GPU-count-invariant sums (cr_set_canonical_blocks): D canonical row blocks, every
+        block swept and reduced on its own, block payloads summed in block order."""
+        _raise(self._L.cr_set_canonical_blocks(self.h, int(D)), self.h)
+
+    def canonical_blocks(self):
+        """(D, first block of this handle, blocks of this handle)."""
+        D, first, count = C.c_int32(0), C.c_int32(0), C.c_int32(0)
+        _raise(self._L.cr_canonical_blocks(self.h, C.byref(D), C.byref(first), C.byref(count)),
+               self.h)
+        return D.value, first.value, count.value
+
     def iter_local(self):
         _raise(self._L.cr_iter_local(self.h), self.h)
 
@@ -561,6 +574,8 @@ def _solve(prep: PreparedProblem, cfg: PapgConfig, theta0, use_momentum, want_du
         K = cfg.K if 0 < cfg.K < N else 0
         if K:
             s.set_partition(K, prep.feasible, cfg.inner)
+        if cfg.canonical_blocks > 0:
+            s.set_canonical_blocks(cfg.canonical_blocks)
         s.begin(cfg, use_momentum, theta0)
         stopped = False
         while not stopped:
