@@ -68,6 +68,9 @@ def parse():
                          "of the standalone ALCC (SURVEY 8f row f1); papg-alcc: one dual "
                          "iteration of the general-K P-APG(ALCC) (row f2)")
     ap.add_argument("--K", type=int, default=2, help="blocks for --solver papg-alcc")
+    ap.add_argument("--canonical-blocks", type=int, default=0,
+                    help="D > 0: GPU-count-invariant sums over D canonical row blocks "
+                         "(cr_set_canonical_blocks; D must be a multiple of --gpus)")
     ap.add_argument("--scaling", choices=["weak", "strong"], default="weak",
                     help="weak (default): N = N_cfg sqrt(p), fixed pairs per GPU; strong: the "
                          "config's own N on every p (BASELINE cfg 3 and 4 on 1/2/4/8 GPUs, "
@@ -384,6 +387,8 @@ def run_ours(args):
     W, K = max(args.warmup, 3), args.steps
     pc = crb.PapgConfig(max_iters=W + K + 16, gap_norm_tol=-1.0, infeas_norm_tol=-1.0,
                         sigma_C=sigma, device=local)
+    if args.canonical_blocks > 0:
+        solver.set_canonical_blocks(args.canonical_blocks)
     solver.begin(pc)
     solver.iterate(W)
 
@@ -542,6 +547,7 @@ def run_ours(args):
                                       args.scaling == "weak" else ""),
                        "N": N, "n": n, "pairs_per_step": pairs_step,
                        "rows_per_gpu": rows, "sweep_variant": variant,
+                       "canonical_blocks": args.canonical_blocks,
                        "l2": (f"inputs > L2 (V, V' = {16 * rows * N / 1e9:.3g} GB per GPU), no flush"
                               if 16 * rows * N > 126e6 else
                               f"inputs < L2 (V, V' = {16 * rows * N / 1e6:.3g} MB): L2-resident "

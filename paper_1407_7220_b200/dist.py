@@ -29,6 +29,15 @@ def shard_rows(N: int, world: int, rank: int) -> tuple[int, int]:
     return N * rank // world, N * (rank + 1) // world
 
 
+def canonical_bounds(N: int, D: int) -> list[int]:
+    """Row boundaries of the D canonical blocks of cr_set_canonical_blocks: block j covers
+    rows [floor(j N / D), floor((j + 1) N / D)). shard_rows(N, world, r) falls on these
+    boundaries whenever world divides D."""
+    if D < 1 or D > N:
+        raise ValueError("canonical_bounds: need 1 <= D <= N")
+    return [j * N // D for j in range(D + 1)]
+
+
 def broadcast_nccl_id(group=None) -> bytes:
     """Rank 0 creates the NCCL unique id; every rank receives it (any backend)."""
     import torch.distributed as dist

@@ -9,7 +9,7 @@ import socket
 import numpy as np
 import pytest
 
-from paper_1407_7220_b200.dist import local_payload, shard_rows
+from paper_1407_7220_b200.dist import canonical_bounds, local_payload, shard_rows
 
 
 def test_shard_rows_cover_and_balance():
@@ -77,3 +77,72 @@ def test_gloo_sharded_exchange_matches_unsharded(tmp_path, world):
         assert np.allclose(r["y"], r["ref_y"], rtol=1e-12, atol=1e-12)
         assert np.allclose(r["xi"], r["ref_xi"], rtol=1e-9, atol=1e-9)
     assert np.array_equal(res[0]["y"], res[1]["y"])  # replicated primal is bitwise equal
+
+
+def test_canonical_bounds_contain_every_balanced_shard():
+    for N in (8, 37, 1000, 10001):
+        b = canonical_bounds(N, 8)
+        assert b[0] == 0 and b[-1] == N and all(x < y for x, y in zip(b, b[1:]))
+        for world in (1, 2, 4, 8):
+            for r in range(world):
+                r0, r1 = shard_rows(N, world, r)
+                assert r0 in b and r1 in b
+    with pytest.raises(ValueError):
+        canonical_bounds(4, 5)
+
+
+def _block_payloads(theta, X, D, lo, hi):
+    """Payloads of canonical blocks lo..hi-1 (host restatement of what each block's sweep +
+    reduce produces)."""
+    N = X.shape[0]
+    b = canonical_bounds(N, D)
+    return np.stack([local_payload(theta[b[j] * (N - 1): b[j + 1] * (N - 1)], theta[N * (N - 1):],
+                                   X, b[j], b[j + 1]) for j in range(lo, hi)])
+
+
+def _canon_worker(rank, world, port, N, n, D, out_dir):
+    import torch
+    import torch.distributed as dist
+
+    from oracle import oracle as O
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    X, y = O.gen_instance("maxaffine-uniform", N, n, 0.1, 5, 6)
+    p = O.prepare(X, y)
+    theta = O.papg(X, p.ys, max_iters=7, gap_norm_tol=-1, infeas_norm_tol=-1).theta
+    per = D // world
+    mine = torch.from_numpy(_block_payloads(theta, X, D, rank * per, (rank + 1) * per))
+    every = [torch.empty_like(mine) for _ in range(world)]
+    dist.all_gather(every, mine)  # the canonical-block exchange: gather, do not reduce
+    blocks = torch.cat(every).numpy()
+    total = blocks[0].copy()
+    for j in range(1, D):  # block order, on every rank
+        total += blocks[j]
+    np.save(os.path.join(out_dir, f"c{rank}.npy"), total)
+    dist.destroy_process_group()
+
+
+def test_gloo_canonical_block_exchange_is_world_size_invariant(tmp_path):
+    """The allgather + block-order sum gives bitwise the payload of a single process
+    (SPEC.md:382, 619), unlike a sum over per-rank partial sums."""
+    import torch.multiprocessing as mp
+
+    from oracle import oracle as O
+
+    N, n, D, world = 41, 3, 4, 2
+    port = _free_port()
+    mp.start_processes(_canon_worker, args=(world, port, N, n, D, str(tmp_path)), nprocs=world,
+                       join=True, start_method="spawn")
+    got = [np.load(tmp_path / f"c{r}.npy") for r in range(world)]
+    X, y = O.gen_instance("maxaffine-uniform", N, n, 0.1, 5, 6)
+    p = O.prepare(X, y)
+    theta = O.papg(X, p.ys, max_iters=7, gap_norm_tol=-1, infeas_norm_tol=-1).theta
+    blocks = _block_payloads(theta, X, D, 0, D)
+    single = blocks[0].copy()
+    for j in range(1, D):
+        single += blocks[j]
+    assert np.array_equal(got[0], single) and np.array_equal(got[1], single)
+    whole = local_payload(theta[: N * (N - 1)], theta[N * (N - 1):], X, 0, N)
+    assert np.allclose(single, whole, rtol=1e-12, atol=1e-13)
