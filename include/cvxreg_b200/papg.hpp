@@ -104,6 +104,9 @@ struct PapgConfig {  // papg.hpp:7-21
   int device = 0;
   double sigma_C = 0;   // > 0: inject sigma_max(C)
   int graph_iters = 0;  // 0 auto, > 0 CUDA-graph batch, < 0 direct launches
+  // D > 0: sums over D canonical row blocks, bitwise independent of the GPU count
+  // (cr_set_canonical_blocks); singleton blocks only
+  int canonical_blocks = 0;
 };
 
 struct MetricsSnapshot {  // metrics.hpp:13-22
@@ -206,6 +209,7 @@ inline PapgResult solve(const PreparedProblem& prep, const PapgConfig& cfg,
     check(cr_set_partition(hd.h, K, prep.feasible.y.data(), prep.feasible.xi.data(), &inner),
           hd.h);
   }
+  if (cfg.canonical_blocks > 0) check(cr_set_canonical_blocks(hd.h, cfg.canonical_blocks), hd.h);
   cr_papg_config c{};
   c.gamma = cfg.gamma;
   c.B_theta = cfg.B_theta;

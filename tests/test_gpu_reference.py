@@ -208,3 +208,55 @@ def test_live_reference_to_tolerance(monkeypatch):
     assert r.reason == "thresholds"
     assert (g["res"].iters, g["res"].reason, g["res"].restarts) == (r.iters, 0, r.restarts)
     assert rel(g["theta"], r.theta) <= 1e-12 and rel(g["y"], r.y) <= 1e-8
+
+
+# ------------------------------------------- BASELINE configurations, reference fixtures
+@pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg3"])
+def test_baseline_config_matches_the_compiled_reference(monkeypatch, name):
+    """BASELINE configs 1-3 against tests/golden/ref_baseline_<cfg>.npz: the reference's own
+    papg_solve run in the build container (scripts/make_ref_baseline_golden.py; config 1 for
+    its 2000 iterations, config 2 to its tolerance, config 3 for 10 iterations). The fixture
+    keeps y, xi, the history, the decisions, sigma_C and 12 sampled rows of theta."""
+    import bench
+    from oracle import oracle as O
+
+    path = os.path.join(GOLDEN, f"ref_baseline_{name}.npz")
+    if not os.path.exists(path):
+        pytest.skip(f"{path} not generated")
+    g = np.load(path)
+    cfg = bench.CONFIGS[name]
+    N, n = cfg["N"], cfg["n"]
+    X, _ = O.gen_instance(cfg["kind"], N, n, cfg["noise"], 1, cfg["pieces"])
+    iters, gt, ft = g["meta"]
+    g_final, delta, B_theta, L_g, sigma = g["scal"]
+    with crb.DualSolver(X, g["ys"]) as s:
+        sg, _, _ = s.sigma_C()
+        assert sg == pytest.approx(sigma, rel=1e-10)  # device power loop vs the reference's
+        pc = crb.PapgConfig(max_iters=int(iters), gap_norm_tol=float(gt),
+                            infeas_norm_tol=float(ft), sigma_C=float(sigma))
+        s.begin(pc)
+        stopped = False
+        while not stopped:
+            _, stopped = s.iterate(1 << 40)
+        res, y, xi, hist = s.finish()
+        k, restarts, reason, saturated = (int(v) for v in g["iters"])
+        assert (res.iters, res.restarts, res.reason, int(bool(res.saturated))) == \
+            (k, restarts, reason, saturated)
+        e_y, e_xi = rel(y, g["y"]), rel(xi, g["xi"])
+        num = den = 0.0
+        for r, want in zip(g["rows"], g["theta_rows"]):
+            got = s.theta_rows(int(r), int(r) + 1)
+            num += np.sum((got[: N - 1] - want) ** 2)
+            den += np.sum(want ** 2)
+            pos = got[N - 1:]
+        e_theta = np.sqrt(num / max(den, 1e-300))
+        e_pos = rel(pos, g["theta_pos"]) if np.linalg.norm(g["theta_pos"]) > 0 else \
+            np.linalg.norm(pos)
+    print(f"{name} vs compiled reference: iterations {res.iters}, |dtheta|/|theta| (sampled rows) "
+          f"{e_theta:.2e}, pos rows {e_pos:.2e}, |dy|/|y| {e_y:.2e}, |dxi|/|xi| {e_xi:.2e}")
+    assert den > 0 and e_theta <= 1e-12 and e_pos <= 1e-12
+    assert e_y <= 1e-8 and e_xi <= 1e-8
+    hist_close(hist, g["hist"], 1e-9)
+    assert res.g_final == pytest.approx(g_final, rel=1e-9)
+    assert res.delta_estimate == pytest.approx(delta, rel=1e-7, abs=1e-9)
+    assert res.B_theta == B_theta

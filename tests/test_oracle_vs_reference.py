@@ -258,3 +258,27 @@ def test_fixtures_are_current():
                gap_norm_tol=float(gt), infeas_norm_tol=float(ft), B_theta=float(B),
                use_momentum=bool(mom))
     assert np.array_equal(r.theta, g[f"theta{i}"]) and np.array_equal(r.y, g[f"y{i}"])
+
+
+@pytest.mark.slow
+@pytest.mark.skipif(not os.environ.get("CRB_SLOW_TESTS"), reason="1-2 minutes of oracle time; "
+                    "set CRB_SLOW_TESTS=1 (the GPU suite checks the same fixture on the device)")
+def test_oracle_reproduces_reference_at_baseline_config_1(oracle):
+    """BASELINE config 1 (N = 1000, n = 5, 2000 iterations): the oracle against the reference's
+    own run (tests/golden/ref_baseline_cfg1.npz, scripts/make_ref_baseline_golden.py)."""
+    path = os.path.join(GOLDEN, "ref_baseline_cfg1.npz")
+    if not os.path.exists(path):
+        pytest.skip("fixture not generated")
+    g = np.load(path)
+    X, _ = oracle.gen_instance("sqnorm-uniform", 1000, 5, 0.1, 1, 0)
+    iters, gt, ft = g["meta"]
+    r = oracle.papg(X, g["ys"], max_iters=int(iters), gap_norm_tol=float(gt),
+                    infeas_norm_tol=float(ft), sigma_C=float(g["scal"][4]),
+                    threads=os.cpu_count() or 1)
+    assert r.iters == int(g["iters"][0]) == 2000
+    N = 1000
+    cross = r.theta[: N * (N - 1)].reshape(N, N - 1)
+    assert rel(cross[g["rows"]], g["theta_rows"]) <= 1e-12
+    assert rel(r.theta, np.zeros(1)) == pytest.approx(float(g["theta_norm"]), rel=1e-12)
+    assert rel(r.y, g["y"]) <= 1e-12 and rel(r.xi, g["xi"]) <= 1e-11
+    hist_close(r.history, g["hist"], 1e-9)
