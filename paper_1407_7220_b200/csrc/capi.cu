@@ -1044,7 +1044,7 @@ cr_status cr_papg_iterate(cr_handle* h, int64_t max_steps, int64_t* done, int32_
         int cnt = 0;
         for (int it = 1; it < 64 && tb[it * 8 + 7] != 0; ++it, ++cnt)
           for (int k = 0; k < 7; ++k) acc[k] += (double)(tb[it * 8 + k + 1] - tb[it * 8 + k]);
-        std::fprintf(stderr, "small-loop phases (ns, mean of %d): - %.0f - %.0f B %.0f syncB %.0f C+ctl %.0f A %.0f sync %.0f\n",
+        std::fprintf(stderr, "small-loop phases (ns, mean of %d): B-load %.0f B-math %.0f B-store %.0f syncB %.0f C+ctl %.0f A %.0f sync %.0f\n",
                      cnt, acc[0] / cnt, acc[1] / cnt, acc[2] / cnt, acc[3] / cnt, acc[4] / cnt,
                      acc[5] / cnt, acc[6] / cnt);
         cudaFree(trace);

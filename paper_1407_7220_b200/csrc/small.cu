@@ -79,6 +79,9 @@ __global__ void __launch_bounds__(kSBlock, CRB_SMALL_MINB) small_loop_kernel(con
   // all blocks take identical decisions without a broadcast; block 0 writes the
   // history and the final state
   __shared__ DevCtrl sctrl;
+  // sweep: the records (x, 1, y) of the RB rows a warp is working on
+  constexpr int RB = NN <= 8 ? 32 : (NN <= 16 ? 16 : (NN <= 24 ? 8 : 4));
+  __shared__ double srec[kSBlock / 32][RB * RP];
   if (threadIdx.x < (int)(sizeof(DevCtrl) / 8))
     reinterpret_cast<unsigned long long*>(&sctrl)[threadIdx.x] =
         __ldcg(reinterpret_cast<const unsigned long long*>(c) + threadIdx.x);
@@ -122,8 +125,6 @@ __global__ void __launch_bounds__(kSBlock, CRB_SMALL_MINB) small_loop_kernel(con
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
       __stcg(&a.clock[0], t);
     }
-    stamp(it, 1);
-    stamp(it, 2);
 
     // ---- B: pair sweep
     {
@@ -146,73 +147,87 @@ __global__ void __launch_bounds__(kSBlock, CRB_SMALL_MINB) small_loop_kernel(con
 #pragma unroll
         for (int j = 0; j <= NN; ++j) acc[j] = 0.0;
         double vv = 0.0, vr = 0.0, tr = 0.0, nn = 0.0;
-        // U rows in flight: all loads of a batch are issued before its math
+        // One L2 round trip per RB rows: the V / V' values of all RB rows are loaded up
+        // front (2 RB registers) and the rows' records (x, 1, y) go to the warp's shared
+        // slab in the same round trip; the math then runs from registers and shared
+        // memory (per-batch record loads into registers made every 8-row batch a
+        // dependent L2 round trip: cfg 1 sweep 9.0 -> 8.0 us). Phases of the sweep at
+        // config 1 (CRB_TRACE): loads 3.0 us (16 MB through L2), math 4.1, stores 1.1.
 #ifndef CRB_SMALL_U5
 #define CRB_SMALL_U5 8
 #endif
         constexpr int U = NN <= 5 ? CRB_SMALL_U5 : ((NN + 3) <= 8 ? 4 : ((NN + 3) <= 16 ? 2 : 1));
-        for (long long r0 = rlo; r0 < rhi; r0 += U) {
-          double xb[U][NN], yb[U], cb[U], pb[U];
+        double* slab = &srec[threadIdx.x >> 5][0];
+        for (long long rb0 = rlo; rb0 < rhi; rb0 += RB) {
+          const int nrows = (int)min((long long)RB, rhi - rb0);
+          double cb[RB], pb[RB];
 #pragma unroll
-          for (int u = 0; u < U; ++u) {
-            const long long r = r0 + u < rhi ? r0 + u : rhi - 1;
-            const double* xr = a.pa.rowrec + r * RP;  // (x, 1, y)
-#pragma unroll
-            for (int j = 0; j < NN; ++j) xb[u][j] = __ldcg(xr + j);
-            yb[u] = __ldcg(xr + NN + 1);
+          for (int u = 0; u < RB; ++u) {
+            const long long r = u < nrows ? rb0 + u : rhi - 1;
             // the V pitch ld comes from the TMA kernels' strip width and may be
             // narrower than this kernel's 32-column strips: touch real columns only
             cb[u] = valid ? __ldcg(Vc + r * a.ld + col) : 0.0;
             pb[u] = valid ? __ldcg(Vp + r * a.ld + col) : 0.0;
           }
-          double vrow[U];  // this lane's v of the batch's rows (0 when cold / absent)
-          bool any_hot = false;
+          __syncwarp();  // the previous slab's readers are done
+          for (int k = lane; k < nrows * RP; k += 32) slab[k] = __ldcg(a.pa.rowrec + rb0 * RP + k);
+          __syncwarp();
+          if (rb0 == rlo) stamp(it, 1);  // trace: the first rows' records have arrived
 #pragma unroll
-          for (int u = 0; u < U; ++u) {
-            vrow[u] = 0.0;
-            const long long r = r0 + u;
-            if (r >= rhi) continue;
-            double row = yb[u] + cc;
+          for (int g0 = 0; g0 < RB; g0 += U) {
+            if (g0 >= nrows) break;  // warp-uniform
+            const long long r0 = rb0 + g0;
+            double vrow[U];  // this lane's v of the batch's rows (0 when cold / absent)
+            bool any_hot = false;
 #pragma unroll
-            for (int j = 0; j < NN; ++j) row = fma(xb[u][j], xi[j], row);
-            if (!valid || col == r) row = 0.0;
-            const double c1 = cb[u], p1 = pb[u];
-            // cold: theta1 = theta1_prev = 0 (stored multipliers are never -0) and
-            // row >= 0 -> theta2 = 0, v = 0 = p1: no store, every update below adds
-            // an exact zero (late in a solve almost every row of a strip)
-            const bool hot = ((unsigned long long)__double_as_longlong(c1) |
-                              (unsigned long long)__double_as_longlong(p1)) != 0ull ||
-                             __double2hiint(row) < 0;
-            if (!__any_sync(0xffffffffu, hot)) continue;
-            any_hot = true;
-            double th2;
-            if (unit) {
-              th2 = fma(beta, c1 - p1, c1);
-            } else {
-              const double th1 = s_c * c1;
-              th2 = fma(beta, th1 - s_p * p1, th1);
+            for (int u = 0; u < U; ++u) {
+              vrow[u] = 0.0;
+              const long long r = r0 + u;
+              if (g0 + u >= nrows) continue;
+              const double* xr = slab + (g0 + u) * RP;  // (x, 1, y)
+              double row = xr[NN + 1] + cc;
+#pragma unroll
+              for (int j = 0; j < NN; ++j) row = fma(xr[j], xi[j], row);
+              if (!valid || col == r) row = 0.0;
+              const double c1 = cb[g0 + u], p1 = pb[g0 + u];
+              // cold: theta1 = theta1_prev = 0 (stored multipliers are never -0) and
+              // row >= 0 -> theta2 = 0, v = 0 = p1: no store, every update below adds
+              // an exact zero (late in a solve almost every row of a strip)
+              const bool hot = ((unsigned long long)__double_as_longlong(c1) |
+                                (unsigned long long)__double_as_longlong(p1)) != 0ull ||
+                               __double2hiint(row) < 0;
+              if (!__any_sync(0xffffffffu, hot)) continue;
+              any_hot = true;
+              double th2;
+              if (unit) {
+                th2 = fma(beta, c1 - p1, c1);
+              } else {
+                const double th1 = s_c * c1;
+                th2 = fma(beta, th1 - s_p * p1, th1);
+              }
+              const double uu = fma(-row, invL, th2);
+              const double v = uu > 0.0 ? uu : 0.0;
+              if (valid && __double_as_longlong(v) != __double_as_longlong(p1))  // unchanged: no store
+                __stcg(Vp + r * a.ld + col, v);
+              vv = fma(v, v, vv);
+              vr = fma(v, row, vr);
+              tr = fma(th2, row, tr);
+              const double m = row < 0.0 ? row : 0.0;
+              nn = fma(m, m, nn);
+              acc[0] += v;
+#pragma unroll
+              for (int j = 0; j < NN; ++j) acc[1 + j] = fma(v, xr[j], acc[1 + j]);
+              vrow[u] = v;
             }
-            const double uu = fma(-row, invL, th2);
-            const double v = uu > 0.0 ? uu : 0.0;
-            if (valid && __double_as_longlong(v) != __double_as_longlong(p1))  // unchanged: no store
-              __stcg(Vp + r * a.ld + col, v);
-            vv = fma(v, v, vv);
-            vr = fma(v, row, vr);
-            tr = fma(th2, row, tr);
-            const double m = row < 0.0 ? row : 0.0;
-            nn = fma(m, m, nn);
-            acc[0] += v;
-#pragma unroll
-            for (int j = 0; j < NN; ++j) acc[1 + j] = fma(v, xb[u][j], acc[1 + j]);
-            vrow[u] = v;
+            // row sums of the batch over the strip's 32 columns -> rowpart [N][S]
+            double rs = 0.0;
+            int ru = lane / (32 / U);  // all-cold batch: zero sums, no shuffles
+            if (any_hot) ru = rows_transpose_sum<U>(vrow, lane, rs);
+            if ((lane & (32 / U - 1)) == 0 && g0 + ru < nrows)
+              __stcg(a.rowpart + (r0 + ru) * a.S + strip, rs);
           }
-          // row sums of the batch over the strip's 32 columns -> rowpart [N][S]
-          double rs = 0.0;
-          int ru = lane / (32 / U);  // all-cold batch: zero sums, no shuffles
-          if (any_hot) ru = rows_transpose_sum<U>(vrow, lane, rs);
-          if ((lane & (32 / U - 1)) == 0 && r0 + ru < rhi)
-            __stcg(a.rowpart + (r0 + ru) * a.S + strip, rs);
         }
+        stamp(it, 2);  // trace: the task's math is done
         // [N][n+1][P]: the P partials of one column entry are contiguous
         if (valid) {
           double* dst = a.colpart + (col * (NN + 1)) * a.P + chunk;
