@@ -906,6 +906,27 @@ cr_status begin_impl(cr_handle* h, const cr_papg_config* cfg, const double* thet
         h->small_S = (int)((h->N + 31) / 32);
         const long long warps = (long long)h->small_grid * (h->ks.threads / 32);
         h->small_P = (int)std::max<long long>(1, std::min<long long>(h->N, warps / h->small_S));
+        // resident variant (one block per SM): one (strip, chunk) task per warp and the
+        // tiles of a block's 8 warps within 200 KB of shared memory (config 1: 27 rows,
+        // 110 KB). CRB_SMALL_RESIDENT=0 keeps the L2 variant.
+        h->small_RT = 0;
+        h->small_smem = 0;
+        {
+          const SmallInfo kr = small_loop_info((int)h->n, true);
+          const long long warps1 = (long long)sms * (kr.threads / 32);
+          const long long P1 = std::max<long long>(1, std::min<long long>(h->N, warps1 / h->small_S));
+          const long long RT = (h->N + P1 - 1) / P1;
+          const char* rv = std::getenv("CRB_SMALL_RESIDENT");
+          if (!(rv && rv[0] == '0') && kr.fn && kr.max_blocks_per_sm >= 1 &&
+              (long long)h->small_S * P1 <= warps1 &&
+              small_resident_smem((int)RT, kr.threads) <= 200 * 1024) {
+            h->ks = kr;
+            h->small_grid = sms;
+            h->small_P = (int)P1;
+            h->small_RT = (int)RT;
+            h->small_smem = small_resident_smem((int)RT, kr.threads);
+          }
+        }
         for (double* b : {h->s_colpart, h->s_rowpart, h->s_scalpart, h->s_k2part})
           dfree(b, h->st);
         h->s_colpart = h->s_rowpart = h->s_scalpart = h->s_k2part = nullptr;
@@ -1020,6 +1041,7 @@ cr_status cr_papg_iterate(cr_handle* h, int64_t max_steps, int64_t* done, int32_
       sa.max_iters = max_steps;
       sa.S = h->small_S;
       sa.P = h->small_P;
+      sa.RT = h->small_RT;
       unsigned long long* trace = nullptr;
       if (std::getenv("CRB_TRACE")) {
         CUDA_TRY(cudaMalloc(&trace, 64 * 8 * sizeof(unsigned long long)));
@@ -1028,7 +1050,7 @@ cr_status cr_papg_iterate(cr_handle* h, int64_t max_steps, int64_t* done, int32_
       sa.trace = trace;
       const auto wall0 = std::chrono::steady_clock::now();
       CUDA_TRY(cudaEventRecord(h->ev_start, h->st));
-      CUDA_TRY(launch_small_loop(h->ks, sa, h->small_grid, h->st));
+      CUDA_TRY(launch_small_loop(h->ks, sa, h->small_grid, h->st, h->small_smem));
       CUDA_TRY(cudaEventRecord(h->ev_end, h->st));
       s = sync_ctrl(h);
       if (s != CR_OK) return s;

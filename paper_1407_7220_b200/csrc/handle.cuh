@@ -95,6 +95,8 @@ struct cr_handle {
   bool small_mode = false;
   SmallInfo ks{};
   int small_grid = 0, small_S = 0, small_P = 0;
+  int small_RT = 0;          // > 0: resident variant (V, V' tiles in shared memory), tile rows
+  size_t small_smem = 0;     // its dynamic shared memory per block
   double *s_colpart = nullptr, *s_rowpart = nullptr, *s_scalpart = nullptr, *s_k2part = nullptr;
   int G = 0;            // sweep CTAs (one persistent wave)
   int maxspan = 0;      // tiles one CTA's unit range can touch

@@ -26,6 +26,14 @@ namespace crb {
 namespace {
 
 constexpr int kSBlock = 256;
+// Threads per block of a variant. 512-thread blocks for the resident variant (16 warps per
+// SM on half the rows each) were measured at config 1: the sweep's math halves (3.9 -> 2.4 us)
+// but twice the column partials make its stores and the reduce slower (0.8 -> 2.3 us,
+// 3.5 -> 4.4 us): 16.9 vs 15.4 us per iteration, so every variant runs 256 threads.
+template <int NN, bool SV>
+__host__ __device__ constexpr int small_threads() {
+  return kSBlock;
+}
 
 // Row sums of U rows over a warp's 32 columns (lane = column) with a
 // transpose-reduce: log2(U) halving exchanges (xor 16, 8, ...) leave each lane
@@ -63,12 +71,18 @@ __device__ __forceinline__ int rows_transpose_sum(double (&t)[U], int lane, doub
 #ifndef CRB_SMALL_MINB
 #define CRB_SMALL_MINB 1
 #endif
-template <int NN>
-__global__ void __launch_bounds__(kSBlock, CRB_SMALL_MINB) small_loop_kernel(const SmallArgs a) {
+// SV: every warp owns one (strip, chunk) task for the whole launch and keeps its V / V' tile
+// (rows x 32 columns x 2 buffers) in shared memory: loaded once at the start of the launch,
+// written back at its end, so an iteration moves no multiplier through L2 (at config 1 the
+// 16 MB of V, V' streamed through L2 every iteration were ~3 us of the sweep).
+template <int NN, bool SV>
+__global__ void __launch_bounds__(small_threads<NN, SV>(), CRB_SMALL_MINB)
+    small_loop_kernel(const SmallArgs a) {
+  constexpr int kSB = small_threads<NN, SV>();
   constexpr int RP = rec_pitch(NN);
   cg::grid_group grid = cg::this_grid();
-  const long long tid = (long long)blockIdx.x * kSBlock + threadIdx.x;
-  const long long nthreads = (long long)gridDim.x * kSBlock;
+  const long long tid = (long long)blockIdx.x * kSB + threadIdx.x;
+  const long long nthreads = (long long)gridDim.x * kSB;
   const int lane = threadIdx.x & 31;
   const long long gwarp = tid >> 5;
   const long long nwarps = nthreads >> 5;
@@ -80,8 +94,22 @@ __global__ void __launch_bounds__(kSBlock, CRB_SMALL_MINB) small_loop_kernel(con
   // history and the final state
   __shared__ DevCtrl sctrl;
   // sweep: the records (x, 1, y) of the RB rows a warp is working on
-  constexpr int RB = NN <= 8 ? 32 : (NN <= 16 ? 16 : (NN <= 24 ? 8 : 4));
-  __shared__ double srec[kSBlock / 32][RB * RP];
+  constexpr int RB = kSB == 512 ? 16 : (NN <= 8 ? 32 : (NN <= 16 ? 16 : (NN <= 24 ? 8 : 4)));
+  __shared__ double srec[kSB / 32][RB * RP];
+  extern __shared__ double vtile[];  // SV: [warp][buffer][RT][32]
+  double* tile0 = vtile + (size_t)(threadIdx.x >> 5) * 2 * a.RT * 32;
+  double* tile1 = tile0 + (size_t)a.RT * 32;
+  // SV: the warp's task (fixed for the launch) and its tile, loaded from the dual buffers
+  const long long tw_rlo = SV && gwarp < (long long)a.S * a.P ? N * (gwarp / a.S) / a.P : 0;
+  const long long tw_rhi = SV && gwarp < (long long)a.S * a.P ? N * (gwarp / a.S + 1) / a.P : 0;
+  const long long tw_col = SV ? (gwarp % a.S) * 32 + lane : 0;
+  if constexpr (SV) {
+    for (long long i = 0; i < tw_rhi - tw_rlo; ++i) {
+      const bool ok = tw_col < N;
+      tile0[i * 32 + lane] = ok ? __ldcg(a.V0 + (tw_rlo + i) * a.ld + tw_col) : 0.0;
+      tile1[i * 32 + lane] = ok ? __ldcg(a.V1 + (tw_rlo + i) * a.ld + tw_col) : 0.0;
+    }
+  }
   if (threadIdx.x < (int)(sizeof(DevCtrl) / 8))
     reinterpret_cast<unsigned long long*>(&sctrl)[threadIdx.x] =
         __ldcg(reinterpret_cast<const unsigned long long*>(c) + threadIdx.x);
@@ -106,9 +134,9 @@ __global__ void __launch_bounds__(kSBlock, CRB_SMALL_MINB) small_loop_kernel(con
     double acc[kK2Scal];
 #pragma unroll
     for (int w = 0; w < kK2Scal; ++w) acc[w] = 0.0;
-    for (long long l = pl0 + threadIdx.x; l < pl1; l += kSBlock)
+    for (long long l = pl0 + threadIdx.x; l < pl1; l += kSB)
       primal_point<NN>(a.pa, l, sctrl.s_cur, sctrl.s_prev, sctrl.beta, vposc, vposp, acc);
-    block_reduce_store<kK2Scal, kSBlock>(
+    block_reduce_store<kK2Scal, kSB>(
         acc, a.k2part + (((sctrl.ell + 1) & 1) * nk2 + blockIdx.x) * kK2Scal);
   };
   __syncthreads();
@@ -130,6 +158,8 @@ __global__ void __launch_bounds__(kSBlock, CRB_SMALL_MINB) small_loop_kernel(con
     {
       const double* Vc = cur ? a.V1 : a.V0;
       double* Vp = cur ? a.V0 : a.V1;
+      const double* tc = cur ? tile1 : tile0;  // SV: the same two buffers, resident
+      double* tp = cur ? tile0 : tile1;
       const double invL = a.pa.invL;
       const bool unit = (s_c == 1.0) && (s_p == 1.0);
       double wsc[kScal] = {0.0, 0.0, 0.0, 0.0};
@@ -160,22 +190,22 @@ __global__ void __launch_bounds__(kSBlock, CRB_SMALL_MINB) small_loop_kernel(con
         double* slab = &srec[threadIdx.x >> 5][0];
         for (long long rb0 = rlo; rb0 < rhi; rb0 += RB) {
           const int nrows = (int)min((long long)RB, rhi - rb0);
-          double cb[RB], pb[RB];
+          double cb[SV ? 1 : RB], pb[SV ? 1 : RB];
+          if constexpr (!SV) {
 #pragma unroll
-          for (int u = 0; u < RB; ++u) {
-            const long long r = u < nrows ? rb0 + u : rhi - 1;
-            // the V pitch ld comes from the TMA kernels' strip width and may be
-            // narrower than this kernel's 32-column strips: touch real columns only
-            cb[u] = valid ? __ldcg(Vc + r * a.ld + col) : 0.0;
-            pb[u] = valid ? __ldcg(Vp + r * a.ld + col) : 0.0;
+            for (int u = 0; u < RB; ++u) {
+              const long long r = u < nrows ? rb0 + u : rhi - 1;
+              // the V pitch ld comes from the TMA kernels' strip width and may be
+              // narrower than this kernel's 32-column strips: touch real columns only
+              cb[u] = valid ? __ldcg(Vc + r * a.ld + col) : 0.0;
+              pb[u] = valid ? __ldcg(Vp + r * a.ld + col) : 0.0;
+            }
           }
           __syncwarp();  // the previous slab's readers are done
           for (int k = lane; k < nrows * RP; k += 32) slab[k] = __ldcg(a.pa.rowrec + rb0 * RP + k);
           __syncwarp();
           if (rb0 == rlo) stamp(it, 1);  // trace: the first rows' records have arrived
-#pragma unroll
-          for (int g0 = 0; g0 < RB; g0 += U) {
-            if (g0 >= nrows) break;  // warp-uniform
+          auto group = [&](const int g0) {
             const long long r0 = rb0 + g0;
             double vrow[U];  // this lane's v of the batch's rows (0 when cold / absent)
             bool any_hot = false;
@@ -189,7 +219,14 @@ __global__ void __launch_bounds__(kSBlock, CRB_SMALL_MINB) small_loop_kernel(con
 #pragma unroll
               for (int j = 0; j < NN; ++j) row = fma(xr[j], xi[j], row);
               if (!valid || col == r) row = 0.0;
-              const double c1 = cb[g0 + u], p1 = pb[g0 + u];
+              double c1, p1;
+              if constexpr (SV) {  // the lane's column of the warp's resident tile
+                c1 = tc[(r - rlo) * 32 + lane];
+                p1 = tp[(r - rlo) * 32 + lane];
+              } else {
+                c1 = cb[g0 + u];
+                p1 = pb[g0 + u];
+              }
               // cold: theta1 = theta1_prev = 0 (stored multipliers are never -0) and
               // row >= 0 -> theta2 = 0, v = 0 = p1: no store, every update below adds
               // an exact zero (late in a solve almost every row of a strip)
@@ -207,8 +244,10 @@ __global__ void __launch_bounds__(kSBlock, CRB_SMALL_MINB) small_loop_kernel(con
               }
               const double uu = fma(-row, invL, th2);
               const double v = uu > 0.0 ? uu : 0.0;
-              if (valid && __double_as_longlong(v) != __double_as_longlong(p1))  // unchanged: no store
-                __stcg(Vp + r * a.ld + col, v);
+              if (valid && __double_as_longlong(v) != __double_as_longlong(p1)) {  // unchanged: no store
+                if constexpr (SV) tp[(r - rlo) * 32 + lane] = v;
+                else __stcg(Vp + r * a.ld + col, v);
+              }
               vv = fma(v, v, vv);
               vr = fma(v, row, vr);
               tr = fma(th2, row, tr);
@@ -225,6 +264,18 @@ __global__ void __launch_bounds__(kSBlock, CRB_SMALL_MINB) small_loop_kernel(con
             if (any_hot) ru = rows_transpose_sum<U>(vrow, lane, rs);
             if ((lane & (32 / U - 1)) == 0 && g0 + ru < nrows)
               __stcg(a.rowpart + (r0 + ru) * a.S + strip, rs);
+          };
+          if constexpr (SV) {
+            // nothing indexed by g0 lives in registers: a real loop keeps the sweep's code
+            // within the instruction cache (32 unrolled rows were ~60 KB of SASS)
+#pragma unroll 1
+            for (int g0 = 0; g0 < nrows; g0 += U) group(g0);
+          } else {
+#pragma unroll
+            for (int g0 = 0; g0 < RB; g0 += U) {
+              if (g0 >= nrows) break;  // warp-uniform
+              group(g0);
+            }
           }
         }
         stamp(it, 2);  // trace: the task's math is done
@@ -245,7 +296,7 @@ __global__ void __launch_bounds__(kSBlock, CRB_SMALL_MINB) small_loop_kernel(con
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) wsc[k] += __shfl_xor_sync(0xffffffffu, wsc[k], o);
       }
-      __shared__ double bsc[kSBlock / 32][kScal];
+      __shared__ double bsc[kSB / 32][kScal];
       if (lane == 0) {
 #pragma unroll
         for (int k = 0; k < kScal; ++k) bsc[threadIdx.x >> 5][k] = wsc[k];
@@ -254,7 +305,7 @@ __global__ void __launch_bounds__(kSBlock, CRB_SMALL_MINB) small_loop_kernel(con
       if (threadIdx.x < kScal) {
         double t = 0.0;
 #pragma unroll
-        for (int w8 = 0; w8 < kSBlock / 32; ++w8) t += bsc[w8][threadIdx.x];
+        for (int w8 = 0; w8 < kSB / 32; ++w8) t += bsc[w8][threadIdx.x];
         __stcg(a.scalpart + (long long)blockIdx.x * kScal + threadIdx.x, t);
       }
     }
@@ -312,7 +363,7 @@ __global__ void __launch_bounds__(kSBlock, CRB_SMALL_MINB) small_loop_kernel(con
         const int g = lane & 7;
         const long long nel = (pl1 - pl0) * (NN + 2);  // (n+1) column values + the row sum per point
         // warp-uniform loop (4 elements per warp) so the group shuffles see every lane
-        for (long long eb = (t4 >> 5) * 4; eb < nel; eb += 16) {
+        for (long long eb = (t4 >> 5) * 4; eb < nel; eb += (kSB / 32 - 4) * 4) {
           const long long e = eb + (lane >> 3);
           const bool ok = e < nel;
           const long long l = pl0 + (ok ? e / (NN + 2) : 0);
@@ -345,16 +396,33 @@ __global__ void __launch_bounds__(kSBlock, CRB_SMALL_MINB) small_loop_kernel(con
     grid.sync();
     stamp(it, 7);
   }
+  if constexpr (SV) {  // the resident tiles go back to the dual buffers (a lane owns its column)
+    if (tw_col < N) {
+      for (long long i = 0; i < tw_rhi - tw_rlo; ++i) {
+        __stcg(a.V0 + (tw_rlo + i) * a.ld + tw_col, tile0[i * 32 + lane]);
+        __stcg(a.V1 + (tw_rlo + i) * a.ld + tw_col, tile1[i * 32 + lane]);
+      }
+    }
+  }
   if (blockIdx.x == 0 && threadIdx.x == 0) *c = sctrl;  // full state for the host
 }
 
-template <int NN>
+constexpr size_t kResidentSmemMax = 200 * 1024;
+
+template <int NN, bool SV>
 SmallInfo small_info_for() {
   SmallInfo inf{};
-  inf.fn = (const void*)small_loop_kernel<NN>;
-  inf.threads = kSBlock;
+  inf.fn = (const void*)small_loop_kernel<NN, SV>;
+  inf.threads = small_threads<NN, SV>();
+  if (SV && cudaFuncSetAttribute(inf.fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)kResidentSmemMax) != cudaSuccess) {
+    cudaGetLastError();
+    inf.fn = nullptr;
+    return inf;
+  }
   int bps = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, inf.fn, kSBlock, 0) != cudaSuccess)
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, inf.fn, inf.threads,
+                                                    SV ? kResidentSmemMax : 0) != cudaSuccess)
     bps = 0;
   inf.max_blocks_per_sm = bps;
   return inf;
@@ -362,22 +430,29 @@ SmallInfo small_info_for() {
 
 template <int... Ns> struct STable;
 template <int N0, int... Ns> struct STable<N0, Ns...> {
-  static SmallInfo info(int n) { return n == N0 ? small_info_for<N0>() : STable<Ns...>::info(n); }
+  static SmallInfo info(int n, bool sv) {
+    if (n != N0) return STable<Ns...>::info(n, sv);
+    return sv ? small_info_for<N0, true>() : small_info_for<N0, false>();
+  }
 };
 template <> struct STable<> {
-  static SmallInfo info(int) { return SmallInfo{}; }
+  static SmallInfo info(int, bool) { return SmallInfo{}; }
 };
 using AllS = STable<CRB_N_LIST>;
 
 }  // namespace
 
-SmallInfo small_loop_info(int n) { return AllS::info(n); }
+SmallInfo small_loop_info(int n, bool resident) { return AllS::info(n, resident); }
+
+size_t small_resident_smem(int RT, int threads) {
+  return (size_t)(threads / 32) * 2 * (size_t)RT * 32 * sizeof(double);
+}
 
 cudaError_t launch_small_loop(const SmallInfo& info, const SmallArgs& a, int grid,
-                              cudaStream_t s) {
+                              cudaStream_t s, size_t dyn_smem) {
   void* args[] = {const_cast<SmallArgs*>(&a)};
-  return cudaLaunchCooperativeKernel(info.fn, dim3((unsigned)grid), dim3(info.threads), args, 0,
-                                     s);
+  return cudaLaunchCooperativeKernel(info.fn, dim3((unsigned)grid), dim3(info.threads), args,
+                                     dyn_smem, s);
 }
 
 }  // namespace crb

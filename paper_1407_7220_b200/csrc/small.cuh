@@ -22,6 +22,7 @@ struct SmallArgs {
   long long N, ld;
   long long max_iters; // iterations this launch may run (halts earlier on termination)
   int S, P;            // 32-column strips, row chunks
+  int RT;              // resident variant: rows of a warp's V / V' tile (>= ceil(N / P))
   unsigned long long* trace;  // optional: block 0 phase timestamps (CRB_TRACE), 8 per iteration
   unsigned long long* clock;  // one timestamp per iteration (block 0): every block's time budget
 };
@@ -32,8 +33,12 @@ struct SmallInfo {
   int max_blocks_per_sm;
 };
 
-SmallInfo small_loop_info(int n);
+// resident = true: the variant that keeps every warp's V / V' tile in shared memory for the
+// whole launch (one (strip, chunk) task per warp; needs small_resident_smem(RT) bytes of
+// dynamic shared memory per block)
+SmallInfo small_loop_info(int n, bool resident = false);
+size_t small_resident_smem(int RT, int threads);
 cudaError_t launch_small_loop(const SmallInfo& info, const SmallArgs& a, int grid,
-                              cudaStream_t s);
+                              cudaStream_t s, size_t dyn_smem = 0);
 
 }  // namespace crb
