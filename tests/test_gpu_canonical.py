@@ -143,3 +143,22 @@ def test_canonical_blocks_errors(oracle):
         d.set_canonical_blocks(8)
         assert d.canonical_blocks() == (8, 0, 8)
         assert d.exchange_len == 8 * (120 * 5 + 5)
+
+
+def test_canonical_blocks_nccl_allgather_single_rank(oracle):
+    """The NCCL path of the mode (in-place ncclAllGather of the block payloads, captured in the
+    iteration graph or launched directly) on a one-rank communicator: the bits of the
+    communicator-free run."""
+    X, ys = instance(oracle, "maxaffine-uniform", 320, 7, 0.1, 31, 9)
+    s, _, _ = oracle.sigma_C(X)
+    kw = dict(max_iters=30, gap_norm_tol=-1.0, infeas_norm_tol=-1.0, sigma_C=s)
+    base = run_shards(X, ys, crb.PapgConfig(**kw), 1, 8, 30)
+    for graph_iters in (6, -1):
+        with crb.DualSolver(X, ys) as d:
+            d.attach_nccl(crb.DualSolver.nccl_unique_id(), 0, 1)
+            d.set_canonical_blocks(8)
+            d.begin(crb.PapgConfig(graph_iters=graph_iters, **kw))
+            done, stopped = d.iterate(1 << 30)
+            assert done == 30 and stopped
+            res, y, xi, hist = d.finish()
+            assert np.array_equal(d.theta(), base["theta"]) and np.array_equal(y, base["y"])
