@@ -112,3 +112,32 @@ def test_create_rejects_invalid_shapes():
         crb.DualSolver(np.zeros((1, 2)), np.zeros(1))
     with pytest.raises(ValueError):
         crb.DualSolver(np.zeros((40, 3)), np.zeros(39))  # ys must have N entries
+
+
+def test_host_side_generators_and_prepare_match_the_compiled_reference():
+    """The drop-in's own host code (csrc/host.cpp: gen_instance, prepare_problem) against the
+    reference's testgen.cpp / preprocess.cpp compiled in oracle/_ref, when that is present."""
+    from oracle import ref as R
+
+    if not R.available():
+        pytest.skip("oracle/_ref not built")
+    for kind, n in (("quadratic", 3), ("exponential", 4), ("affine-noiseless", 2),
+                    ("custom-1d", 1)):
+        d = crb.gen_instance(crb.GeneratorSpec(kind, n, 40, 0.3, 9))
+        Xr, yr = R.gen_instance(kind, 40, n, 0.3, 9)
+        assert np.array_equal(d.xs, Xr)
+        assert np.allclose(d.ys, yr, rtol=1e-13, atol=1e-14)
+    d = crb.gen_instance(crb.GeneratorSpec("quadratic", 4, 90, 0.5, 2))
+    p = crb.prepare_problem(d, 1e-3)
+    r = R.prepare(d.xs, d.ys, 1e-3)
+    assert np.allclose(p.data.ys, r.ys, rtol=1e-13)
+    assert p.shift == pytest.approx(r.shift, rel=1e-13)
+    assert np.allclose(p.feasible.y, r.feas_y, rtol=1e-11, atol=1e-12)
+    assert np.allclose(p.feasible.xi, r.feas_xi, rtol=1e-10, atol=1e-12)
+    b = p.bounds
+    assert (b.B_theta, b.gamma) == (r.B_theta, r.gamma)
+    assert b.Bbar_y == pytest.approx(r.Bbar_y, rel=1e-12)
+    assert b.Bbar_xi == pytest.approx(r.Bbar_xi, rel=1e-12)
+    assert crb.momentum_next(1.0) == R.momentum_next(1.0)
+    assert np.allclose(crb.certificate_for_iterate(1e-3, 0.02, 3.0, 40.0),
+                       R.certificate(1e-3, 0.02, 3.0, 40.0), rtol=1e-15)

@@ -282,3 +282,33 @@ def test_oracle_reproduces_reference_at_baseline_config_1(oracle):
     assert rel(r.theta, np.zeros(1)) == pytest.approx(float(g["theta_norm"]), rel=1e-12)
     assert rel(r.y, g["y"]) <= 1e-12 and rel(r.xi, g["xi"]) <= 1e-11
     hist_close(r.history, g["hist"], 1e-9)
+
+
+@live
+def test_live_prepare_and_size_edge_cases(oracle):
+    """Edge cases of preprocess.cpp / testgen.cpp: rank-deficient design (constant-fit
+    fallback, preprocess.cpp:27-31), exactly affine data, the minimal N = n + 1, N < n + 1."""
+    rng = np.random.default_rng(0)
+    x1 = rng.standard_normal(30)
+    X = np.stack([x1, 2 * x1, rng.standard_normal(30)], 1)  # columns 1 and 2 collinear
+    y = rng.standard_normal(30)
+    po, pr = oracle.prepare(X, y), R.prepare(X, y)
+    assert np.array_equal(pr.slope, np.zeros(3)) and np.array_equal(po.slope, pr.slope)
+    assert po.intercept == pytest.approx(pr.intercept, rel=1e-14)
+    assert np.abs(po.ys - pr.ys).max() <= 1e-13 and po.shift == pytest.approx(pr.shift, rel=1e-14)
+    X = rng.standard_normal((20, 2))
+    y = 0.5 + X @ np.array([1.0, -2.0])  # affine: the fit is exact
+    po, pr = oracle.prepare(X, y), R.prepare(X, y)
+    assert po.Bbar_y == pytest.approx(pr.Bbar_y, rel=1e-9)
+    assert po.shift == pytest.approx(pr.shift, rel=1e-12)
+    X, y = rng.standard_normal((4, 3)), rng.standard_normal(4)  # N = n + 1
+    pr = R.prepare(X, y)
+    r = R.papg(X, pr.ys, feas_y=pr.feas_y, feas_xi=pr.feas_xi, max_iters=20, gap_norm_tol=-1.0,
+               infeas_norm_tol=-1.0)
+    o = oracle.papg(X, pr.ys, max_iters=20, gap_norm_tol=-1.0, infeas_norm_tol=-1.0,
+                    sigma_C=r.sigma_C)
+    assert np.linalg.norm(r.theta) > 0 and rel(o.theta, r.theta) <= 1e-13 and rel(o.y, r.y) <= 1e-13
+    with pytest.raises(ValueError, match="N >= n"):
+        R.gen_instance("quadratic", 3, 3, 0.1, 1)
+    with pytest.raises(ValueError):
+        oracle.gen_instance("quadratic", 3, 3, 0.1, 1)
