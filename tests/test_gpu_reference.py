@@ -260,3 +260,40 @@ def test_baseline_config_matches_the_compiled_reference(monkeypatch, name):
     assert res.g_final == pytest.approx(g_final, rel=1e-9)
     assert res.delta_estimate == pytest.approx(delta, rel=1e-7, abs=1e-9)
     assert res.B_theta == B_theta
+
+
+@live
+def test_live_reference_general_k_and_alcc():
+    """f2 / f1 against the reference run on this box: papg_solve with K = 4 blocks of 60
+    points (block QPs by the reference's ALCC) and the standalone alcc_solve at N = 150."""
+    from oracle import oracle as O
+
+    X, y = O.gen_instance("maxaffine-uniform", 240, 4, 0.2, 61, 8)
+    P = R.prepare(X, y)
+    inner = dict(max_outer=8, mapg_cap=1500)
+    r = R.papg(X, P.ys, K=4, feas_y=P.feas_y, feas_xi=P.feas_xi, inner=inner, max_iters=10,
+               gap_norm_tol=-1.0, infeas_norm_tol=-1.0, threads=os.cpu_count() or 1)
+    g = gpu_papg(X, P.ys, partition=(4, P.feas_y, P.feas_xi), max_iters=10, sigma_C=r.sigma_C,
+                 K=4, gap_norm_tol=-1.0, infeas_norm_tol=-1.0, inner=crb.AlccConfig(**inner))
+    assert g["res"].iters == r.iters == 10
+    e = rel(g["theta"], r.theta), rel(g["y"], r.y)
+    print(f"live reference general K=4 N=240: |dtheta|/|theta|={e[0]:.2e} |dy|/|y|={e[1]:.2e}")
+    assert e[0] <= 1e-9 and e[1] <= 1e-8
+    hist_close(g["hist"], r.history, 1e-7)
+
+    X, y = O.gen_instance("sqnorm-uniform", 150, 3, 0.2, 62, 0)
+    P = R.prepare(X, y)
+    s1, s2 = R.sigma(X, "A1"), R.sigma(X, "A2")
+    a = R.alcc(X, P.ys, gamma=1e-3, Bbar_y=P.Bbar_y, Bbar_xi=P.Bbar_xi, warm_y=P.feas_y,
+               warm_xi=P.feas_xi, max_outer=5, mapg_cap=1500, want_multiplier=True)
+    cfg = crb.AlccConfig(sigma_A1=s1[0], sigma_A2=s2[0], max_outer=5, mapg_cap=1500)
+    bounds = crb.ProblemBounds(P.B_theta, P.Bbar_y, P.Bbar_xi, 1e-3)
+    with crb.DualSolver(X, P.ys, 1e-3) as s:
+        res, yg, xig, hist, mi = s.alcc(cfg, bounds, crb.PrimalPoint(P.feas_y, P.feas_xi))
+        mult = s.alcc_multiplier()
+    assert (res.outer_iters, res.mapg_iters_total, res.reason) == \
+        (a.outer_iters, a.mapg_iters_total, REASON[a.reason])
+    e = rel(yg, a.y), rel(mult, a.multiplier)
+    print(f"live reference ALCC N=150: outer {a.outer_iters}, MAPG {a.mapg_iters_total}, "
+          f"|dy|/|y|={e[0]:.2e} |dlambda|/|lambda|={e[1]:.2e}")
+    assert e[0] <= 1e-10 and rel(xig, a.xi) <= 1e-10 and e[1] <= 1e-7
