@@ -22,9 +22,12 @@ from .oracle import (AlccResult, CroAlccConfig, CroAlccResult, CroConfig, CroRes
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "_ref", "libcvxreg_ref.so")
+# the same sources over the Eigen stand-in's left-to-right reductions (see eigen_shim/Eigen/Dense)
+LIB_PATH_SEQ = os.path.join(HERE, "_ref", "libcvxreg_ref_seq.so")
 REF_KINDS = {"quadratic": 0, "exponential": 1, "affine-noiseless": 2, "custom-1d": 3}
 
 _lib = None
+_lib_seq = None
 
 
 def build():
@@ -34,6 +37,26 @@ def build():
 
 def available() -> bool:
     return os.path.exists(LIB_PATH)
+
+
+def available_sequential() -> bool:
+    return os.path.exists(LIB_PATH_SEQ)
+
+
+def lib_sequential():
+    """The build with left-to-right reductions; only papg and sigma are bound on it."""
+    global _lib_seq
+    if _lib_seq is None:
+        if not available_sequential():
+            raise FileNotFoundError("oracle/_ref/libcvxreg_ref_seq.so absent")
+        L = C.CDLL(LIB_PATH_SEQ)
+        d, i64, i32 = C.c_double, C.c_int64, C.c_int
+        L.ref_last_error.restype = C.c_char_p
+        L.ref_sigma.argtypes = [_P, i64, i64, i64, i32, d, i32, _P, C.POINTER(i32), C.POINTER(i32)]
+        L.ref_papg.argtypes = [_P, _P, i64, i64, i64, C.POINTER(CroConfig),
+                               C.POINTER(CroAlccConfig), i32, _P, _P, _P, C.POINTER(CroResult)]
+        _lib_seq = L
+    return _lib_seq
 
 
 def lib():
@@ -200,7 +223,7 @@ def papg(X, ys, *, K=None, shifted=True, feas_y=None, feas_xi=None, inner=None, 
          B_theta=0.0, adaptive_B_theta=True, max_restarts=6, gap_norm_tol=1e-6,
          infeas_norm_tol=1e-1, max_iters=100000, max_seconds=7200.0, inner_tol_floor=1e-6,
          final_resolve_tol=1e-10, record_history=True, use_momentum=True, threads=1,
-         theta0=None, want_theta=True, want_c_eta=False):
+         theta0=None, want_theta=True, want_c_eta=False, sequential=False):
     """The reference's papg_solve / dual_gradient_ascent (papg.cpp:287-296) with K blocks
     (default K = N: singleton blocks). `shifted=True`: ys are the shifted observations and
     (feas_y, feas_xi) the feasible point of prepare_problem (defaults: prepare() of (X, ys)
@@ -226,8 +249,11 @@ def papg(X, ys, *, K=None, shifted=True, feas_y=None, feas_xi=None, inner=None, 
     fy = _c(feas_y) if feas_y is not None else np.zeros(N)
     fxi = _c(feas_xi).reshape(-1) if feas_xi is not None else np.zeros(N * n)
     t0 = None if theta0 is None else _c(theta0)
-    rc = lib().ref_papg(_p(X), _p(ys), N, n, K, C.byref(cfg), C.byref(icfg), int(shifted),
-                        _p(fy), _p(fxi), _p(t0), C.byref(res))
+    L = lib_sequential() if sequential else lib()
+    rc = L.ref_papg(_p(X), _p(ys), N, n, K, C.byref(cfg), C.byref(icfg), int(shifted),
+                    _p(fy), _p(fxi), _p(t0), C.byref(res))
+    if rc != 0 and sequential:
+        raise RuntimeError(f"papg (sequential build): {L.ref_last_error().decode()}")
     _check(rc, "papg")
     return OracleResult(y, xi.reshape(N, n), theta, c_eta, hist[: res.iters], int(res.iters),
                         REASONS[res.reason], res.restarts, bool(res.saturated), res.g_final,

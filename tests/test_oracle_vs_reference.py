@@ -312,3 +312,27 @@ def test_live_prepare_and_size_edge_cases(oracle):
         R.gen_instance("quadratic", 3, 3, 0.1, 1)
     with pytest.raises(ValueError):
         oracle.gen_instance("quadratic", 3, 3, 0.1, 1)
+
+
+@pytest.mark.skipif(not (R.available() and R.available_sequential()),
+                    reason="oracle/_ref builds absent")
+def test_reference_results_do_not_depend_on_the_stand_ins_summation_order(oracle):
+    """Eigen is replaced by oracle/eigen_shim in the compiled reference. Its reductions
+    (norm, dot: 8 partial sums) are the one place where a real Eigen build could differ in
+    the last bits; the second build sums left to right instead. The reference's trajectory
+    moves by rounding only between the two (and the oracle agrees with both), so the choice
+    of summation order in the stand-in does not affect what is pinned."""
+    X, y = oracle.gen_instance("maxaffine-uniform", 160, 10, 0.1, 77, 20)
+    P = R.prepare(X, y)
+    kw = dict(feas_y=P.feas_y, feas_xi=P.feas_xi, max_iters=5000, gap_norm_tol=1e-4,
+              infeas_norm_tol=1e-1)
+    a = R.papg(X, P.ys, **kw)
+    b = R.papg(X, P.ys, sequential=True, **kw)
+    assert (a.iters, a.reason, a.restarts) == (b.iters, b.reason, b.restarts)
+    assert a.reason == "thresholds" and np.linalg.norm(a.theta) > 0
+    assert rel(b.theta, a.theta) <= 1e-13 and rel(b.y, a.y) <= 1e-13
+    assert b.sigma_C == pytest.approx(a.sigma_C, rel=1e-13)
+    hist_close(b.history, a.history, 1e-11)
+    o = oracle.papg(X, P.ys, max_iters=5000, gap_norm_tol=1e-4, infeas_norm_tol=1e-1,
+                    sigma_C=b.sigma_C)
+    assert o.iters == b.iters and rel(o.theta, b.theta) <= 1e-13
