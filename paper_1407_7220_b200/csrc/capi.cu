@@ -57,6 +57,34 @@ static void pinned_put(void* p, size_t bytes) {
   g_pin_free.emplace_back(bytes, p);
 }
 
+// The uniform pairs of the sigma_max(C) start vector (rng_stream(0x5eed, 97)), drawn into
+// a pinned block of the process pool (a pageable upload of the 2 N (n+1) doubles cost
+// ~0.3 ms at config 2), or into the handle's vector when no pinned memory is to be had.
+static void draw_sigma_start(cr_handle* h) {
+  const int64_t cols = h->N * (h->n + 1);
+  const size_t bytes = sizeof(double) * (size_t)(2 * cols);
+  if (h->sigma_start_pin == nullptr || h->sigma_start_bytes != bytes) {
+    pinned_put(h->sigma_start_pin, h->sigma_start_bytes);
+    h->sigma_start_pin = nullptr;
+    h->sigma_start_bytes = 0;
+    void* p = nullptr;
+    if (cudaSetDevice(h->device) == cudaSuccess && pinned_get(&p, bytes) == cudaSuccess) {
+      h->sigma_start_pin = (double*)p;
+      h->sigma_start_bytes = bytes;
+    } else {
+      cudaGetLastError();
+    }
+  }
+  if (h->sigma_start_pin) {
+    h->sigma_start_ptr = h->sigma_start_pin;
+  } else {
+    h->sigma_start.resize((size_t)(2 * cols));
+    h->sigma_start_ptr = h->sigma_start.data();
+  }
+  host::uniform_pairs(0x5eedULL, 97, cols, h->sigma_start_ptr);
+  h->sigma_start_cols = cols;
+}
+
 namespace crb {
 
 // 2-D tensor maps of the dual buffers for the DMMA P-APG producer: dims
@@ -405,9 +433,7 @@ cr_status cr_create(const double* Xh, const double* ybar_shifted, int64_t N, int
                    std::chrono::duration<double>(std::chrono::steady_clock::now() - tc0).count() * 1e3);
   };
   h->sigma_prep = std::thread([h] {  // overlaps the allocations and uploads below
-    const int64_t cols = h->N * (h->n + 1);
-    h->sigma_start.resize((size_t)(2 * cols));
-    host::uniform_pairs(0x5eedULL, 97, cols, h->sigma_start.data());  // beside the creation
+    draw_sigma_start(h);  // beside the creation
   });
   CUDA_TRY(cudaSetDevice(device));
   CUDA_TRY(cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking));
@@ -544,6 +570,8 @@ void cr_destroy(cr_handle* h) {
   dfree(h->d_stores, h->st);
   dfree(h->ctrl_d, h->st);
   if (h->st) cudaStreamSynchronize(h->st);
+  pinned_put(h->sigma_start_pin, h->sigma_start_bytes);
+  pinned_put(h->out_pin, h->out_pin_bytes);
   pinned_put(h->ctrl_h, sizeof(DevCtrl));
   pinned_put(h->ctrl_poll, 2 * sizeof(DevCtrl));
   pinned_put(h->pause_h, 2 * sizeof(long long));
@@ -653,12 +681,9 @@ cr_status cr_sigma_C(cr_handle* h, double tol, int32_t max_iters, double* sigma,
   const int64_t cols = h->N * (h->n + 1);
   // fixed seeded start (operators.cpp:309-313), drawn at handle creation
   if (h->sigma_prep.joinable()) h->sigma_prep.join();
-  if ((int64_t)h->sigma_start.size() != 2 * cols) {
-    h->sigma_start.resize((size_t)(2 * cols));
-    host::uniform_pairs(0x5eedULL, 97, cols, h->sigma_start.data());
-  }
+  if (h->sigma_start_ptr == nullptr || h->sigma_start_cols != cols) draw_sigma_start(h);
   if (!h->sv_u12) CUDA_TRY(dalloc(&h->sv_u12, (size_t)(2 * cols + 256)));
-  CUDA_TRY(cudaMemcpyAsync(h->sv_u12, h->sigma_start.data(), sizeof(double) * 2 * cols,
+  CUDA_TRY(cudaMemcpyAsync(h->sv_u12, h->sigma_start_ptr, sizeof(double) * 2 * cols,
                            cudaMemcpyHostToDevice, h->st));
   CUDA_TRY(launch_start_vector(h->sv_u12, h->pw_u, cols, h->sv_u12 + 2 * cols, h->st));
   // closed-form steps assume singleton blocks; a K-block partition masks the
@@ -1245,8 +1270,16 @@ cr_status cr_papg_finish(cr_handle* h, cr_papg_result* res, double* y, double* x
   if (!h || !res) return CR_EINVAL;
   if (!h->begun) return fail(h, CR_ESTATE, "papg: finish before begin");
   CUDA_TRY(cudaSetDevice(h->device));
+  const bool fdbg = std::getenv("CRB_DEBUG_FINISH") != nullptr;
+  const auto tf0 = std::chrono::steady_clock::now();
+  auto fmark = [&](const char* what) {
+    if (fdbg)
+      std::fprintf(stderr, "finish %-10s %.3f ms\n", what,
+                   std::chrono::duration<double>(std::chrono::steady_clock::now() - tf0).count() * 1e3);
+  };
   cr_status s = sync_ctrl(h);
   if (s != CR_OK) return s;
+  fmark("sync_ctrl");
   const DevCtrl& c = *h->ctrl_h;
   double ft = 1.0 / std::pow((double)c.ell, 3.0);  // papg.cpp:266-269
   ft = std::min(ft, h->cfg.inner_tol_floor);
@@ -1260,17 +1293,41 @@ cr_status cr_papg_finish(cr_handle* h, cr_papg_result* res, double* y, double* x
     CUDA_TRY(launch_primal(pa, h->st));
     CUDA_TRY(launch_reduce_records(h->k2part, h->k2_blocks, kK2Scal, h->k2sum, h->st));
   }
+  fmark("enqueued");
   double k2[kK2Scal];
   CUDA_TRY(cudaMemcpyAsync(k2, h->k2sum, sizeof(k2), cudaMemcpyDeviceToHost, h->st));
-  if (y) CUDA_TRY(cudaMemcpyAsync(y, h->yout, sizeof(double) * h->N, cudaMemcpyDeviceToHost, h->st));
-  if (xi)
-    CUDA_TRY(cudaMemcpyAsync(xi, h->xiout, sizeof(double) * h->N * h->n, cudaMemcpyDeviceToHost,
+  fmark("k2 copy");
+  // (y, xi) through a pinned staging block of the process pool: pageable destinations made
+  // these two copies 0.4 ms of a 12.6 ms config-2 solve
+  const size_t out_bytes = sizeof(double) * (size_t)(h->N * (h->n + 1));
+  if ((y || xi) && h->out_pin == nullptr) {
+    void* p = nullptr;
+    if (pinned_get(&p, out_bytes) == cudaSuccess) {
+      h->out_pin = (double*)p;
+      h->out_pin_bytes = out_bytes;
+    } else {
+      cudaGetLastError();
+    }
+  }
+  double* ystage = h->out_pin ? h->out_pin : y;
+  double* xistage = h->out_pin ? h->out_pin + h->N : xi;
+  if (y)
+    CUDA_TRY(cudaMemcpyAsync(ystage, h->yout, sizeof(double) * h->N, cudaMemcpyDeviceToHost,
                              h->st));
+  if (xi)
+    CUDA_TRY(cudaMemcpyAsync(xistage, h->xiout, sizeof(double) * h->N * h->n,
+                             cudaMemcpyDeviceToHost, h->st));
   const int64_t nh = std::min<int64_t>(c.ell, c.hist_cap);
   if (history && nh > 0)
     CUDA_TRY(cudaMemcpyAsync(history, h->hist, sizeof(double) * 8 * nh, cudaMemcpyDeviceToHost,
                              h->st));
+  fmark("copies");
   CUDA_TRY(cudaStreamSynchronize(h->st));
+  if (h->out_pin) {
+    if (y) std::memcpy(y, ystage, sizeof(double) * h->N);
+    if (xi) std::memcpy(xi, xistage, sizeof(double) * h->N * h->n);
+  }
+  fmark("synced");
   std::memset(res, 0, sizeof(*res));
   res->iters = c.ell;
   res->reason = c.reason;

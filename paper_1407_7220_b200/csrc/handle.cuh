@@ -149,7 +149,13 @@ struct cr_handle {
   // sigma_max(C) start vector (rng_stream(0x5eed, 97), normalised), drawn on a
   // host thread while the handle's device state is set up
   std::thread sigma_prep;
-  std::vector<double> sigma_start;  // uniform pairs of the sigma start vector (host drawn)
+  std::vector<double> sigma_start;  // uniform pairs of the sigma start vector (host drawn):
+  double* sigma_start_pin = nullptr;  // pinned block from the process pool when available,
+  size_t sigma_start_bytes = 0;       // else the vector; sigma_start_ptr points at the one in use
+  double* sigma_start_ptr = nullptr;
+  int64_t sigma_start_cols = 0;
+  double* out_pin = nullptr;          // pinned staging of (y, xi) for cr_papg_finish
+  size_t out_pin_bytes = 0;
   double* sv_u12 = nullptr;          // their device copy + 256 doubles of block partials
   double last_seconds = 0, last_sweep_seconds = 0;
   std::vector<double> last_sweep_times;  // per bracketed sweep launch of the last call (s)
