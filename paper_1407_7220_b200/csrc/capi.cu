@@ -679,13 +679,21 @@ cr_status cr_sigma_C(cr_handle* h, double tol, int32_t max_iters, double* sigma,
   CUDA_TRY(cudaSetDevice(h->device));
   const auto t0 = std::chrono::steady_clock::now();
   const int64_t cols = h->N * (h->n + 1);
+  const bool sdbg = std::getenv("CRB_DEBUG_SIGMA") != nullptr;
+  auto smark = [&](const char* what) {
+    if (sdbg)
+      std::fprintf(stderr, "sigma %-10s %.3f ms\n", what,
+                   std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() * 1e3);
+  };
   // fixed seeded start (operators.cpp:309-313), drawn at handle creation
   if (h->sigma_prep.joinable()) h->sigma_prep.join();
+  smark("joined");
   if (h->sigma_start_ptr == nullptr || h->sigma_start_cols != cols) draw_sigma_start(h);
   if (!h->sv_u12) CUDA_TRY(dalloc(&h->sv_u12, (size_t)(2 * cols + 256)));
   CUDA_TRY(cudaMemcpyAsync(h->sv_u12, h->sigma_start_ptr, sizeof(double) * 2 * cols,
                            cudaMemcpyHostToDevice, h->st));
   CUDA_TRY(launch_start_vector(h->sv_u12, h->pw_u, cols, h->sv_u12 + 2 * cols, h->st));
+  smark("start enq");
   // closed-form steps assume singleton blocks; a K-block partition masks the
   // same-block pairs inside the sweep instead
   if (!h->sigma_by_sweep && h->part.K == 0) {  // whole power iteration in one cooperative launch
@@ -702,9 +710,11 @@ cr_status cr_sigma_C(cr_handle* h, double tol, int32_t max_iters, double* sigma,
     pa.max_iters = max_iters;
     pa.tol = tol;
     CUDA_TRY(launch_power_loop(pa, h->power_grid, h->st));
+    smark("loop enq");
     double st[3];
     CUDA_TRY(cudaMemcpyAsync(st, h->ps_state, sizeof(st), cudaMemcpyDeviceToHost, h->st));
     CUDA_TRY(cudaStreamSynchronize(h->st));
+    smark("done");
     *sigma = st[0];
     *iters = (int32_t)st[1];
     *converged = (int32_t)st[2];
