@@ -143,6 +143,16 @@ def test_canonical_blocks_errors(oracle):
         d.set_canonical_blocks(8)
         assert d.canonical_blocks() == (8, 0, 8)
         assert d.exchange_len == 8 * (120 * 5 + 5)
+        # the mode is for singleton blocks: a K-block partition on top of it is refused at begin
+        P = oracle.prepare(*oracle.gen_instance("sqnorm-uniform", 120, 3, 0.1, 3))
+        d.set_partition(4, crb.PrimalPoint(P.feas_y, P.feas_xi))
+        with pytest.raises(Exception, match="singleton"):
+            d.begin(crb.PapgConfig(max_iters=2, sigma_C=10.0, K=4))
+    with crb.DualSolver(X, ys) as d:
+        P = oracle.prepare(*oracle.gen_instance("sqnorm-uniform", 120, 3, 0.1, 3))
+        d.set_partition(4, crb.PrimalPoint(P.feas_y, P.feas_xi))
+        with pytest.raises(Exception, match="singleton"):
+            d.set_canonical_blocks(8)
 
 
 def test_canonical_blocks_nccl_allgather_single_rank(oracle):
