@@ -299,7 +299,14 @@ def run_reference_compiled(args, cfg, threads):
     """--impl reference with oracle/_ref present: the reference's own code (bounded sample),
     and the oracle port on all host threads at the full N beside it when that is feasible."""
     W, K = max(args.warmup, 1), max(args.steps, 1)
+    note = ""
+    if W + K > 300:  # ~0.11 s per iteration at the sample size: keep the arm within a minute
+        K0, W0 = K, W
+        W = min(W, 10)
+        K = 300 - W
+        note = f"; steps {K0}/warmup {W0} reduced to {K}/{W} to bound the run"
     rate, per, sample, _ = cpu_reference_rate(cfg, threads, W, K)
+    sample += note
     Ns = min(cfg["N"], REF_SAMPLE_N)
     line = {
         "impl": "reference", "metric": "pair-constraint updates/s", "value": rate,
